@@ -1,0 +1,258 @@
+/* dashsvd_b200.h — C ABI of the B200-native dashSVD hot path.
+ *
+ * This is the drop-in boundary: plain pointers and sizes, no torch or CUDA
+ * types. Each entry point names the reference interface it replaces
+ * (paths relative to /root/reference/proj/core/include/dashsvd/ and
+ * .../core/src/). include/dashsvd_b200.hpp wraps it in the reference's own
+ * C++ API (dashsvd::solve & co.), and paper_2404_09276_b200/ binds it from
+ * Python with ctypes.
+ *
+ * Conventions
+ *  - Host dense matrices are column-major (dense_matrix.hpp:10-13).
+ *  - Sparse input is canonical CSR with int64 offsets and int64 column
+ *    indices and fp64 values (sparse_matrix.hpp:10-26); it is borrowed for the
+ *    duration of the call only.
+ *  - Every call returns a status (DSVD_OK or an error below). On error,
+ *    dsvd_last_error() returns the message and dsvd_last_error_index() the
+ *    RankDeficient index (errors.hpp:37-43), both thread-local.
+ *  - A context owns one CUDA stream and its workspaces; it is NOT safe for
+ *    concurrent solves from several threads (create one context per thread).
+ *  - Results are deterministic run to run on a fixed GPU count: no float
+ *    atomics, fixed reduction trees.
+ */
+#ifndef DASHSVD_B200_H
+#define DASHSVD_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define DSVD_API __attribute__((visibility("default")))
+#else
+#define DSVD_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes (mapped onto errors.hpp:10-59 by the wrappers) -------- */
+enum {
+    DSVD_OK = 0,
+    DSVD_SHAPE = 1,         /* ShapeError                                   */
+    DSVD_CONFIG = 2,        /* ConfigError                                  */
+    DSVD_RANK_DEFICIENT = 3,/* RankDeficient{index}                         */
+    DSVD_NUMERICAL = 4,     /* NumericalError (eig non-convergence, NaN)    */
+    DSVD_CUDA = 5,          /* CUDA runtime failure (reference: Error)      */
+    DSVD_OOM = 6,           /* device allocation failed (reference: Error)  */
+    DSVD_NCCL = 7,          /* collective failure (reference: Error)        */
+    DSVD_UNSUPPORTED = 8,   /* configuration outside the B200 path          */
+    DSVD_OTHER = 9
+};
+
+/* Algorithm and StopReason keep the reference enum order (solver.hpp:13-18, :45). */
+enum { DSVD_ALG_BASIC = 0, DSVD_ALG_SHIFTED = 1, DSVD_ALG_FIXED_SHIFT = 2, DSVD_ALG_DASH = 3 };
+enum { DSVD_STOP_FIXED_P = 0, DSVD_STOP_TOL_MET = 1, DSVD_STOP_P_MAX_REACHED = 2 };
+
+typedef struct dsvd_ctx dsvd_ctx;       /* device, stream, workspaces, optional NCCL comm */
+typedef struct dsvd_matrix dsvd_matrix; /* device-resident CSR(A) + CSR(A^T)              */
+
+/* SolverConfig (solver.hpp:22-38). s < 0 means the default max(1, k/2).
+ * flags: DSVD_FLAG_DIRECT runs the algorithm on `a` as given, like
+ * shifted_rsvd / dash_svd (solver.cpp:190-212); without it the entry point
+ * behaves like solve(), which factors the transpose of wide inputs and swaps
+ * U and V (solver.cpp:217-220). */
+enum { DSVD_FLAG_DIRECT = 1 };
+typedef struct {
+    int64_t k;
+    int64_t s;
+    int64_t p;
+    double tol;
+    int64_t p_max;
+    int32_t alg;
+    int32_t flags;
+    uint64_t seed;
+} dsvd_config;
+
+/* SolveResult (solver.hpp:51-61), caller-allocated.
+ *   u[m*k], s[k], v[n*k] column-major; alphas[trace_cap], s_hat[trace_cap*l]
+ *   (either trace pointer may be NULL). With outputs_on_device != 0 the
+ *   u/s/v pointers are device pointers on the context's GPU (no D2H copy).
+ *   iterations / stop_reason are written by the call. */
+typedef struct {
+    double* u;
+    double* s;
+    double* v;
+    double* alphas;
+    double* s_hat;
+    int64_t trace_cap;
+    int64_t iterations;
+    int32_t stop_reason;
+    int32_t outputs_on_device;
+} dsvd_outputs;
+
+/* IterationObserver (solver.hpp:63-74): called synchronously after each
+ * power iteration's re-orthonormalisation, before the stop check. q_before /
+ * q_after are HOST column-major n x l copies valid only during the callback. */
+typedef void (*dsvd_observer_fn)(int64_t iteration, double alpha, const double* s_hat,
+                                 int64_t l, const double* q_before, const double* q_after,
+                                 int64_t n, void* user);
+
+/* Per-context counters, filled when profiling is on (dsvd_ctx_set_profiling).
+ * Times are device milliseconds measured with CUDA events on the context's
+ * stream, summed over the last solve. */
+typedef struct {
+    double total_ms;        /* whole solve call                                  */
+    double h2d_ms;          /* CSR upload (host-input entry points only)         */
+    double csc_ms;          /* CSR -> CSR(A^T) construction                      */
+    double omega_ms;        /* Gaussian sketch generation                        */
+    double sketch_ms;       /* A^T Omega + first eigSVD                          */
+    double loop_ms;         /* power iterations                                  */
+    double finalize_ms;     /* B = A Q, eigSVD(B), U/V assembly                  */
+    double d2h_ms;          /* result download (host-output entry points only)   */
+    double spmm_ms;         /* all SpMM passes (A X and A^T Y - alpha Q)         */
+    double gram_ms;         /* Gram partials + reduction                         */
+    double eig_ms;          /* Jacobi eigensolver + rotation replay + finish     */
+    double rescale_ms;      /* Q = T V diag(1/s) (and finalize U, V products)    */
+    double allreduce_ms;    /* n x l partial-sum exchange (multi-GPU)            */
+    int64_t spmm_launches;
+    int64_t kernel_launches;/* every kernel this library launched in the solve    */
+    int64_t eig_sweeps;     /* Jacobi sweeps summed over all eigensolves          */
+    int64_t spmm_bytes;     /* algorithmic SpMM bytes (SURVEY 8d B1/B2 formulas)  */
+    double spmm_pass_ms[2]; /* pass 1 (A Q) and pass 2 (A^T Y - alpha Q), summed  */
+    int64_t spmm_pass_bytes[2];
+    int64_t spmm_pass_launches[2];
+} dsvd_stats;
+
+/* ---- errors --------------------------------------------------------------- */
+DSVD_API const char* dsvd_last_error(void);
+DSVD_API long long dsvd_last_error_index(void);
+DSVD_API const char* dsvd_version(void);
+
+/* ---- context -------------------------------------------------------------- */
+DSVD_API int dsvd_ctx_create(int device, dsvd_ctx** out);
+DSVD_API int dsvd_ctx_destroy(dsvd_ctx* ctx);
+DSVD_API int dsvd_ctx_set_profiling(dsvd_ctx* ctx, int on);
+DSVD_API int dsvd_ctx_get_stats(const dsvd_ctx* ctx, dsvd_stats* out);
+DSVD_API int dsvd_ctx_synchronize(dsvd_ctx* ctx);
+/* Tuning knobs (testing/benchmarking); unknown names -> DSVD_CONFIG. */
+DSVD_API int dsvd_ctx_set_option(dsvd_ctx* ctx, const char* name, int64_t value);
+
+/* Multi-GPU: one process per GPU. Rank 0 calls dsvd_comm_unique_id and
+ * broadcasts the 128 bytes out of band (torch.distributed in the Python
+ * layer); every rank then calls dsvd_ctx_attach_comm. A solve on an attached
+ * context treats the matrix it gets as that rank's row shard. */
+DSVD_API int dsvd_comm_unique_id(uint8_t out[128]);
+DSVD_API int dsvd_ctx_attach_comm(dsvd_ctx* ctx, int nranks, int rank, const uint8_t id[128]);
+/* Row-shard placement used by dsvd_solve_csr / dsvd_solve_csr_device on an
+ * attached context: the CSR passed is rows [row_offset, row_offset + rows) of
+ * a global_rows x cols matrix. */
+DSVD_API int dsvd_ctx_set_shard(dsvd_ctx* ctx, int64_t row_offset, int64_t global_rows);
+
+/* ---- pinned host memory (for zero-copy-speed H2D/D2H of caller buffers) --- */
+DSVD_API int dsvd_host_register(void* ptr, size_t bytes);
+DSVD_API int dsvd_host_unregister(void* ptr);
+
+/* ---- matrix handle: upload once, solve many -------------------------------
+ * Replaces holding (a, transpose(a)) for the overloads taking a precomputed
+ * transpose (solver.hpp:106-116). Builds CSR(A^T) on the device, bitwise
+ * equal to transpose(a) (sparse_matrix.cpp:35-55). */
+DSVD_API int dsvd_matrix_upload(dsvd_ctx* ctx, int64_t rows, int64_t cols, int64_t nnz,
+                       const int64_t* offsets, const int64_t* col_indices,
+                       const double* values, dsvd_matrix** out);
+/* Same, from DEVICE pointers on the context's GPU (inputs resident in HBM). */
+DSVD_API int dsvd_matrix_from_device(dsvd_ctx* ctx, int64_t rows, int64_t cols, int64_t nnz,
+                            const int64_t* d_offsets, const int64_t* d_col_indices,
+                            const double* d_values, dsvd_matrix** out);
+DSVD_API int dsvd_matrix_destroy(dsvd_matrix* m);
+/* Declare the handle a row shard: rows [row_offset, row_offset + rows) of a
+ * global_rows x cols matrix (multi-GPU solves; see dsvd_ctx_attach_comm). */
+DSVD_API int dsvd_matrix_set_shard(dsvd_matrix* m, int64_t row_offset, int64_t global_rows);
+DSVD_API int dsvd_matrix_shape(const dsvd_matrix* m, int64_t* rows, int64_t* cols, int64_t* nnz);
+/* Download the device-built transpose (int64 offsets/indices, host buffers). */
+DSVD_API int dsvd_matrix_download_transpose(const dsvd_matrix* m, int64_t* t_offsets,
+                                   int64_t* t_col_indices, double* t_values);
+
+/* ---- solvers --------------------------------------------------------------
+ * dsvd_solve             <- solve(a, at, cfg, observer)   solver.hpp:115-116 / solver.cpp:214-223
+ * dsvd_solve_csr         <- solve(a, cfg)                 solver.hpp:104 / solver.cpp:225-227
+ *                           (host CSR in, host U/S/V out; transpose built on device)
+ * alg == DSVD_ALG_SHIFTED / FIXED_SHIFT / DASH run the shifted family
+ * (shifted_rsvd :95 / dash_svd :99). alg == BASIC returns DSVD_UNSUPPORTED. */
+DSVD_API int dsvd_solve(dsvd_ctx* ctx, const dsvd_matrix* a, const dsvd_config* cfg, dsvd_outputs* out,
+               dsvd_observer_fn observer, void* user);
+DSVD_API int dsvd_solve_csr(dsvd_ctx* ctx, int64_t rows, int64_t cols, int64_t nnz,
+                   const int64_t* offsets, const int64_t* col_indices, const double* values,
+                   const dsvd_config* cfg, dsvd_outputs* out);
+/* Same as dsvd_solve_csr with the CSR already in device memory (inputs
+ * resident in HBM); the transpose is built inside the call, as solve(a, cfg)
+ * does. Workspaces are cached in the context, so repeated calls allocate nothing. */
+DSVD_API int dsvd_solve_csr_device(dsvd_ctx* ctx, int64_t rows, int64_t cols, int64_t nnz,
+                          const int64_t* d_offsets, const int64_t* d_col_indices,
+                          const double* d_values, const dsvd_config* cfg, dsvd_outputs* out);
+
+/* Device-side interval timer on the context's stream (CUDA events). */
+DSVD_API int dsvd_ctx_timer_start(dsvd_ctx* ctx);
+DSVD_API int dsvd_ctx_timer_stop(dsvd_ctx* ctx, double* elapsed_ms);
+
+/* finalize_row_basis (solver.hpp:123, solver.cpp:159-164): host q (cols x l,
+ * column-major) -> host u[rows*k], s[k], v[cols*k]. */
+DSVD_API int dsvd_finalize_row_basis(dsvd_ctx* ctx, const dsvd_matrix* a, const double* q, int64_t l,
+                            int64_t k, double* u, double* s, double* v);
+
+/* validate_config (solver.cpp:15-32), update_shift (:34-36), pve_stop_check
+ * (:38-50): pure host functions with the reference's semantics; the device
+ * loop evaluates the same expressions in the same order. */
+DSVD_API int dsvd_validate_config(const dsvd_config* cfg, int64_t rows, int64_t cols);
+DSVD_API double dsvd_update_shift(double alpha, double s_ll);
+DSVD_API int dsvd_pve_stop_check(const double* s_hat_prev, int64_t n_prev, double alpha_prev,
+                        const double* s_hat, int64_t n, double alpha, int64_t k, double tol,
+                        int* stop);
+
+/* ---- kernel-level entry points (host buffers in/out; for parity tests) ---
+ * Each runs exactly the device kernel the solver uses. */
+/* spmm (sparse_matrix.hpp:36 / .cpp:61-86): y = A x, x cols x l, y rows x l. */
+DSVD_API int dsvd_spmm(dsvd_ctx* ctx, int64_t rows, int64_t cols, int64_t nnz, const int64_t* offsets,
+              const int64_t* col_indices, const double* values, const double* x, int64_t l,
+              double* y);
+/* spmm + add_scaled fused (solver.cpp:93-94, dense_kernels.cpp:128-136):
+ * t = A y, then t += (-alpha) q unless alpha == 0. */
+DSVD_API int dsvd_spmm_shift(dsvd_ctx* ctx, int64_t rows, int64_t cols, int64_t nnz,
+                    const int64_t* offsets, const int64_t* col_indices, const double* values,
+                    const double* y, int64_t l, double alpha, const double* q, double* t);
+/* transpose (sparse_matrix.hpp:30 / .cpp:35-55) */
+DSVD_API int dsvd_transpose(dsvd_ctx* ctx, int64_t rows, int64_t cols, int64_t nnz,
+                   const int64_t* offsets, const int64_t* col_indices, const double* values,
+                   int64_t* t_offsets, int64_t* t_col_indices, double* t_values);
+/* gram (dense_kernels.hpp:24 / .cpp:91-108): g = c^T c, exactly symmetric. */
+DSVD_API int dsvd_gram(dsvd_ctx* ctx, int64_t rows, int64_t cols, const double* c, double* g);
+/* sym_eig (sym_eig.hpp:20): ascending values, column-major vectors. */
+DSVD_API int dsvd_sym_eig(dsvd_ctx* ctx, int64_t n, const double* g, double* values, double* vectors);
+/* eig_svd (decompositions.hpp:28 / .cpp:45-75). */
+DSVD_API int dsvd_eig_svd(dsvd_ctx* ctx, int64_t rows, int64_t cols, const double* c, double* u,
+                 double* s, double* v);
+/* matmul (dense_kernels.hpp:21 / .cpp:34-53): c = a b (m x kk times kk x n). */
+DSVD_API int dsvd_matmul(dsvd_ctx* ctx, int64_t m, int64_t kk, int64_t n, const double* a,
+                const double* b, double* c);
+/* gaussian_matrix (random.hpp:20 / .cpp:29-36). */
+DSVD_API int dsvd_gaussian_matrix(dsvd_ctx* ctx, int64_t rows, int64_t cols, uint64_t seed, double* out);
+DSVD_API uint64_t dsvd_splitmix64_at(uint64_t seed, uint64_t i);
+
+/* ---- synthetic inputs (host, deterministic, thread-count invariant) ------
+ * Bench/test input preparation, not part of the solve path.
+ * sparse_random (synthetic.hpp:37-38 / .cpp:72-120; config 1).
+ * powerlaw: config 2 of BASELINE.json — row degrees round(lognormal(mu,
+ * sigma)) clamped to [1, cols], columns Zipf(zipf_s) ranks mapped through a
+ * seeded permutation, sampled without replacement per row, values N(0,1).
+ * ratings: config 3 — like powerlaw with integer values 1..5.
+ * Two-phase: the call returns nnz and keeps the arrays; *_fetch copies them out. */
+DSVD_API int dsvd_synth_sparse_random(int64_t rows, int64_t cols, int64_t nnz_per_row, uint64_t seed,
+                             int row_decay, int64_t* nnz);
+DSVD_API int dsvd_synth_powerlaw(int64_t rows, int64_t cols, double mu, double sigma, double zipf_s,
+                        int ratings, uint64_t seed, int64_t* nnz);
+DSVD_API int dsvd_synth_fetch(int64_t* offsets, int64_t* col_indices, double* values);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DASHSVD_B200_H */

@@ -1,0 +1,18 @@
+"""B200-native dashSVD hot path (arXiv 2404.09276): randomized truncated SVD of
+sparse CSR matrices with dynamically shifted power iteration and PVE accuracy
+control, computed by sm_100a kernels behind the C ABI in include/dashsvd_b200.h.
+
+The public surface mirrors the reference library's dashsvd:: namespace; see
+``api`` for the mapping.
+"""
+from . import errors
+from .api import (Algorithm, Device, DeviceMatrix, EigenPair, IterationState, Orthonormalizer,
+                  ShiftTrace, SolveResult, SolverConfig, SparseMatrix, StopReason, TruncatedSvd,
+                  basic_rsvd, comm_unique_id, dash_svd, default_device, eig_svd,
+                  finalize_row_basis, gaussian_matrix, gram, matmul, pin, powerlaw, pve_stop_check,
+                  shifted_rsvd, solve, sparse_random, splitmix64_at, spmm, spmm_shift, sym_eig,
+                  transpose, unpin, update_shift, validate_config)
+from .errors import (ConfigError, DeviceError, Error, NumericalError, RankDeficient, ShapeError,
+                     UnsupportedOnDevice)
+
+__all__ = [n for n in dir() if not n.startswith("_")]

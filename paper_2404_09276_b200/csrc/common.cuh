@@ -1,0 +1,61 @@
+// Shared helpers for the sm_100a dashSVD kernels and the engine.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+
+#include "../../include/dashsvd_b200.h"
+
+namespace dsvd {
+
+// Error carried from the engine to the C ABI boundary, where it becomes a
+// status code (dsvd_* functions never throw).
+struct Failure : std::runtime_error {
+    int code;
+    long long index;
+    Failure(int c, const std::string& msg, long long idx = -1)
+        : std::runtime_error(msg), code(c), index(idx) {}
+};
+
+[[noreturn]] inline void fail(int code, const std::string& msg, long long idx = -1) {
+    throw Failure(code, msg, idx);
+}
+
+inline void cuda_check(cudaError_t e, const char* what, const char* file, int line) {
+    if (e != cudaSuccess) {
+        const int code = (e == cudaErrorMemoryAllocation) ? DSVD_OOM : DSVD_CUDA;
+        fail(code, std::string(what) + ": " + cudaGetErrorString(e) + " (" + file + ":" +
+                       std::to_string(line) + ")");
+    }
+}
+
+#define DSVD_CUDA_CHECK(x) ::dsvd::cuda_check((x), #x, __FILE__, __LINE__)
+#define DSVD_LAUNCH_CHECK() ::dsvd::cuda_check(cudaGetLastError(), "kernel launch", __FILE__, __LINE__)
+
+constexpr int kNumSMs = 148;
+
+// Row stride of every tall-skinny device block (Omega, Q, Y, T): l rounded up
+// to 4 doubles so each row starts on a 32-byte sector boundary and lanes can
+// use 128-bit loads.
+inline int64_t padded_ld(int64_t l) { return (l + 3) & ~int64_t(3); }
+
+inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// Device-side control block of one solve (lives in device memory).
+struct Control {
+    double alpha;          // shift used by the next product (solver.cpp:88)
+    double alpha_stored;   // alpha' of the stop rule (post-update alpha, :111-112)
+    int64_t iteration;     // completed power iterations
+    int64_t status_index;  // RankDeficient index
+    int64_t total_sweeps;  // Jacobi sweeps summed over the solve
+    int32_t stopped;       // loop kernels are skipped once set
+    int32_t stop_pending;  // set by the stop rule; becomes `stopped` at the next iteration
+    int32_t status;        // DSVD_OK or an error raised on the device
+    int32_t eig_sweeps;    // sweeps of the last eigensolve
+};
+
+}  // namespace dsvd

@@ -1,0 +1,46 @@
+// Dense tall-skinny kernels: Gaussian sketch, Gram reduction, rescale GEMM,
+// layout conversions.
+#pragma once
+
+#include "common.cuh"
+
+namespace dsvd {
+
+// Omega(i, j) = normal_at(seed, j*rows + i) (random.cpp:29-36), written
+// row-major with stride ld; columns [l, ld) are zero.
+// For a row shard, rows [row_offset, row_offset + rows) of the global
+// global_rows x l sketch are generated (global_rows < 0 means rows).
+void gaussian_rowmajor(double* out, int64_t rows, int64_t l, int64_t ld, uint64_t seed,
+                       cudaStream_t stream, int64_t global_rows = -1, int64_t row_offset = 0);
+
+// t = fma(-alpha, q, t) elementwise unless *alpha == 0 (add_scaled,
+// dense_kernels.cpp:128-136, as applied at solver.cpp:94). Used after the
+// multi-GPU partial sum, where the shift cannot ride the SpMM epilogue.
+void shift_update(double* t, const double* q, int64_t count, const double* alpha,
+                  const int32_t* gate, cudaStream_t stream);
+
+// G = C^T C for row-major C (n x l, stride ld): split-K partial 64x64 tiles
+// over the upper triangle, then a fixed-order reduction across row chunks and
+// an exact mirror (dense_kernels.cpp:91-108 makes G exactly symmetric too).
+// G is l x l (row-major == column-major, it is symmetric).
+size_t gram_workspace_bytes(int64_t n, int64_t l);
+void gram(const double* c, int64_t n, int64_t l, int64_t ld, double* g, void* ws,
+          size_t ws_bytes, const int32_t* gate, cudaStream_t stream);
+
+// out(r, j) = (sum_t c(r, t) * w(t, j)) * scale[j] for j < ncol, the sum one
+// FMA chain over t ascending from 0.0 (the matmul order of
+// dense_kernels.cpp:34-53, scale as scale_columns :118-126).
+//   c: row-major n x K (stride ldc); w: row-major K x ldw; scale may be null.
+//   out_colmajor == 0: row-major with stride ld_out, columns [ncol, ld_out) zeroed.
+//   out_colmajor != 0: column-major n x ncol.
+void rescale(const double* c, int64_t n, int64_t K, int64_t ldc, const double* w, int64_t ldw,
+             const double* scale, int64_t ncol, double* out, int64_t ld_out, int out_colmajor,
+             const int32_t* gate, cudaStream_t stream);
+
+// Column-major (rows x cols) <-> row-major (stride ld, pad columns zeroed).
+void colmajor_to_rowmajor(const double* src, int64_t rows, int64_t cols, double* dst, int64_t ld,
+                          cudaStream_t stream);
+void rowmajor_to_colmajor(const double* src, int64_t rows, int64_t cols, int64_t ld, double* dst,
+                          cudaStream_t stream);
+
+}  // namespace dsvd

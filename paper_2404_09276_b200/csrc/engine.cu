@@ -1,0 +1,1069 @@
+// Engine + C ABI of the B200 dashSVD hot path.
+//
+// The solve mirrors run_shifted_iterations + finalize_row_basis
+// (solver.cpp:76-116, :159-164) with every step on the device:
+//
+//   Omega (m x l, seeded)            gaussian_rowmajor
+//   T = A^T Omega                    spmm (CSR of A^T)
+//   Q = eigSVD(T).u                  gram -> jacobi -> finish -> rescale
+//   loop j = 1..p (or until the PVE rule fires):
+//     Y = A Q                        spmm pass 1
+//     T = A^T Y - alpha Q            spmm pass 2, shift fused in the epilogue
+//     (s, V) = eigSVD(T)             gram -> jacobi -> finish (+ trace, stop rule, shift)
+//     Q = T V diag(1/s)              rescale
+//   B = A Q; U, s, V' = eigSVD(B); V = Q V'[:, :k]
+//
+// Loop control never waits on the host in fixed-p mode; in accuracy-control
+// mode the host reads a 4-byte stop flag with a lookahead of two iterations
+// (iterations enqueued past the stop are skipped on the device through
+// Control::stopped), so the GPU never idles on the check.
+#include <atomic>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <limits>
+#include <map>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "dense.cuh"
+#include "engine.cuh"
+#include "eig.cuh"
+#include "rng.cuh"
+#include "sparse.cuh"
+
+namespace dsvd {
+
+std::atomic<int64_t> g_launches{0};
+
+}  // namespace dsvd
+
+namespace dsvd {
+namespace {
+
+thread_local std::string t_err;
+thread_local long long t_err_index = -1;
+
+constexpr int kMaxSweeps = 60;
+constexpr int kLookahead = 2;
+
+}  // namespace
+
+void set_error(const char* msg, long long index) {
+    t_err = msg;
+    t_err_index = index;
+}
+
+namespace {
+
+void set_device(dsvd_ctx* ctx) { DSVD_CUDA_CHECK(cudaSetDevice(ctx->device)); }
+
+void count_launch(int n = 1) { g_launches += n; }
+
+// ---- matrix construction --------------------------------------------------
+
+struct CsrAlloc {
+    // allocate through the context arena (prefix) or as owned buffers
+    dsvd_ctx* ctx;
+    std::string prefix;
+    std::vector<void*>* owned;
+    void* get(const std::string& name, size_t bytes) {
+        if (owned) {
+            void* p = nullptr;
+            DSVD_CUDA_CHECK(cudaMalloc(&p, bytes > 0 ? bytes : 1));
+            owned->push_back(p);
+            return p;
+        }
+        return ctx->buf(prefix + name, bytes);
+    }
+};
+
+// Device CSR (+ transpose + row orders) from int64 offsets / indices and
+// values already on the device.
+void build_pair(dsvd_ctx* ctx, CsrAlloc& al, int64_t rows, int64_t cols, int64_t nnz,
+                const int64_t* d_off, const int64_t* d_idx64, const double* d_val, DevCsr& a,
+                DevCsr& at, bool copy_inputs) {
+    cudaStream_t st = ctx->stream;
+    if (rows < 0 || cols < 0 || nnz < 0) fail(DSVD_SHAPE, "sparse matrix with negative dimension");
+    if (rows > 0x7fffffffLL || cols > 0x7fffffffLL)
+        fail(DSVD_UNSUPPORTED, "dimensions >= 2^31 are not supported on the device path");
+    a.rows = rows;
+    a.cols = cols;
+    a.nnz = nnz;
+    if (copy_inputs) {
+        a.off = static_cast<int64_t*>(al.get("a.off", sizeof(int64_t) * (rows + 1)));
+        DSVD_CUDA_CHECK(cudaMemcpyAsync(a.off, d_off, sizeof(int64_t) * (rows + 1),
+                                        cudaMemcpyDeviceToDevice, st));
+        a.val = static_cast<double*>(al.get("a.val", sizeof(double) * nnz));
+        if (nnz)
+            DSVD_CUDA_CHECK(cudaMemcpyAsync(a.val, d_val, sizeof(double) * nnz,
+                                            cudaMemcpyDeviceToDevice, st));
+    } else {
+        a.off = const_cast<int64_t*>(d_off);
+        a.val = const_cast<double*>(d_val);
+    }
+    a.idx = static_cast<int32_t*>(al.get("a.idx", sizeof(int32_t) * nnz));
+    a.order = static_cast<int32_t*>(al.get("a.order", sizeof(int32_t) * (rows > 0 ? rows : 1)));
+    int32_t* bad = ctx->tbuf<int32_t>("bad", 2);
+    DSVD_CUDA_CHECK(cudaMemsetAsync(bad, 0, sizeof(int32_t) * 2, st));
+    check_offsets(a.off, rows, nnz, bad, st);
+    count_launch();
+    narrow_indices(d_idx64, a.idx, nnz, cols, bad + 1, st);
+    count_launch(nnz > 0);
+    int32_t hbad[2] = {0, 0};
+    DSVD_CUDA_CHECK(cudaMemcpyAsync(hbad, bad, sizeof(hbad), cudaMemcpyDeviceToHost, st));
+    DSVD_CUDA_CHECK(cudaStreamSynchronize(st));
+    if (hbad[0]) fail(DSVD_SHAPE, "offsets must be non-decreasing and span [0, nnz]");
+    if (hbad[1]) fail(DSVD_SHAPE, "column index out of range");
+
+    at.rows = cols;
+    at.cols = rows;
+    at.nnz = nnz;
+    at.off = static_cast<int64_t*>(al.get("at.off", sizeof(int64_t) * (cols + 1)));
+    at.idx = static_cast<int32_t*>(al.get("at.idx", sizeof(int32_t) * nnz));
+    at.val = static_cast<double*>(al.get("at.val", sizeof(double) * nnz));
+    at.order = static_cast<int32_t*>(al.get("at.order", sizeof(int32_t) * (cols > 0 ? cols : 1)));
+    const size_t scratch_bytes =
+        std::max({csc_scratch_bytes(rows, cols, nnz), order_scratch_bytes(rows), order_scratch_bytes(cols)});
+    void* scratch = ctx->buf("csc.scratch", scratch_bytes);
+    build_transpose(a, at, scratch, scratch_bytes, st);
+    count_launch(nnz > 0 ? 8 : 1);  // 4 own kernels + CUB radix sort passes (estimate)
+    build_row_order(a, scratch, scratch_bytes, st);
+    count_launch(rows > 0 ? 3 : 0);
+    build_row_order(at, scratch, scratch_bytes, st);
+    count_launch(cols > 0 ? 3 : 0);
+}
+
+void upload_pair(dsvd_ctx* ctx, CsrAlloc& al, int64_t rows, int64_t cols, int64_t nnz,
+                 const int64_t* off, const int64_t* idx, const double* val, DevCsr& a, DevCsr& at) {
+    cudaStream_t st = ctx->stream;
+    int64_t* d_off = static_cast<int64_t*>(al.get("a.off", sizeof(int64_t) * (rows + 1)));
+    int64_t* d_idx64 = ctx->tbuf<int64_t>("upload.idx64", nnz);
+    double* d_val = static_cast<double*>(al.get("a.val", sizeof(double) * nnz));
+    DSVD_CUDA_CHECK(cudaMemcpyAsync(d_off, off, sizeof(int64_t) * (rows + 1), cudaMemcpyHostToDevice, st));
+    if (nnz) {
+        DSVD_CUDA_CHECK(cudaMemcpyAsync(d_idx64, idx, sizeof(int64_t) * nnz, cudaMemcpyHostToDevice, st));
+        DSVD_CUDA_CHECK(cudaMemcpyAsync(d_val, val, sizeof(double) * nnz, cudaMemcpyHostToDevice, st));
+    }
+    build_pair(ctx, al, rows, cols, nnz, d_off, d_idx64, d_val, a, at, false);
+}
+
+// ---- config validation (solver.cpp:15-32) ---------------------------------
+
+int64_t effective_s(const dsvd_config& c) { return c.s >= 0 ? c.s : (c.k / 2 > 0 ? c.k / 2 : 1); }
+
+void validate(const dsvd_config& cfg, int64_t rows, int64_t cols) {
+    if (rows < 1 || cols < 1) fail(DSVD_SHAPE, "solver needs a non-empty matrix");
+    if (cfg.k < 1) fail(DSVD_CONFIG, "k must be >= 1");
+    const int64_t s = effective_s(cfg);
+    if (cfg.k + s > std::min(rows, cols))
+        fail(DSVD_CONFIG, "k + s = " + std::to_string(cfg.k + s) + " exceeds min(rows, cols) = " +
+                              std::to_string(std::min(rows, cols)));
+    if (cfg.alg == DSVD_ALG_DASH) {
+        if (s < 1) fail(DSVD_CONFIG, "the accuracy-controlled mode needs oversampling s >= 1");
+        if (!(cfg.tol > 0.0)) fail(DSVD_CONFIG, "tol must be positive");
+        if (cfg.p_max < 1) fail(DSVD_CONFIG, "p_max must be >= 1");
+    } else {
+        if (cfg.p < 0) fail(DSVD_CONFIG, "fixed-power algorithms need p >= 0");
+    }
+    if (cfg.alg < DSVD_ALG_BASIC || cfg.alg > DSVD_ALG_DASH) fail(DSVD_CONFIG, "unknown algorithm");
+}
+
+void raise_device_status(const Control& c) {
+    if (c.status == DSVD_OK) return;
+    if (c.status == DSVD_RANK_DEFICIENT)
+        fail(DSVD_RANK_DEFICIENT, "eig_svd: singular value at or below the rank floor", c.status_index);
+    if (c.status == DSVD_NUMERICAL)
+        fail(DSVD_NUMERICAL, "eigensolver did not converge or produced non-finite values");
+    fail(c.status, "device error");
+}
+
+// ---- eigSVD on a device block ----------------------------------------------
+
+struct EigSvdOut {
+    double* W;      // l x l row-major (V with the sign convention)
+    double* s;      // l
+    double* inv_s;  // l
+};
+
+// (s, V) of the row-major block c (rows x l, stride ld); U is left to the caller.
+void eig_svd_factors(dsvd_ctx* ctx, const double* c, int64_t rows, int64_t l, int64_t ld,
+                     EigSvdOut& o, Control* ctrl, const LoopStep* loop, const int32_t* gate,
+                     bool reduce_gram = false, int64_t floor_rows = -1) {
+    cudaStream_t st = ctx->stream;
+    double* G = ctx->tbuf<double>("eig.G", l * l);
+    const size_t gws = gram_workspace_bytes(rows, l);
+    void* gw = ctx->buf("gram.ws." + std::to_string(rows), gws);
+    int sp = ctx->span_begin(K_GRAM);
+    gram(c, rows, l, ld, G, gw, gws, gate, st);
+    count_launch(2);
+    ctx->span_end(sp);
+    if (reduce_gram) {  // row-sharded B: G = sum_g B_g^T B_g
+        sp = ctx->span_begin(K_COMM);
+        comm_allreduce_sum(ctx, G, static_cast<size_t>(l * l));
+        ctx->span_end(sp);
+    }
+    EigWorkspace ew;
+    void* em = ctx->buf("eig.ws", eig_workspace_bytes(static_cast<int>(l), kMaxSweeps));
+    eig_workspace_bind(ew, static_cast<int>(l), kMaxSweeps, em);
+    sp = ctx->span_begin(K_EIG);
+    jacobi_eig(G, ew, ctrl, gate, st);
+    count_launch(2);
+    eig_svd_finish(ew, floor_rows >= 0 ? floor_rows : rows, o.W, l, o.s, o.inv_s, ctrl, loop, gate, st);
+    count_launch(1);
+    ctx->span_end(sp);
+}
+
+Control read_control(dsvd_ctx* ctx, const Control* d) {
+    Control h;
+    DSVD_CUDA_CHECK(cudaMemcpyAsync(&h, d, sizeof(Control), cudaMemcpyDeviceToHost, ctx->stream));
+    DSVD_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+    return h;
+}
+
+// Host copy of a row-major device block as column-major (rows x l).
+std::vector<double> to_host_colmajor(dsvd_ctx* ctx, const double* d, int64_t rows, int64_t l,
+                                     int64_t ld) {
+    double* tmp = ctx->tbuf<double>("obs.cm", rows * l);
+    rowmajor_to_colmajor(d, rows, l, ld, tmp, ctx->stream);
+    count_launch();
+    std::vector<double> h(static_cast<size_t>(rows * l));
+    DSVD_CUDA_CHECK(cudaMemcpyAsync(h.data(), tmp, sizeof(double) * rows * l, cudaMemcpyDeviceToHost,
+                                    ctx->stream));
+    DSVD_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+    return h;
+}
+
+// ---- the solve ---------------------------------------------------------------
+
+struct SolveIO {
+    // outputs (device or host per on_device); u is rows(A) x k, v is cols(A) x k
+    double* u;
+    double* s;
+    double* v;
+    bool on_device;
+    double* alphas;
+    double* s_hat;
+    int64_t cap;
+    int64_t iterations = 0;
+    int stop_reason = 0;
+};
+
+// Shifted power iteration on the pair (A, AT) = (m x n, n x m) as given
+// (solve_direct, solver.cpp:143-155): Q is a basis of A's row space.
+// With a communicator attached, A is this rank's row shard (rows
+// [row_offset, row_offset + m) of a global_m x n matrix): partial products are
+// summed across ranks after each A^T pass and the finalize Gram; everything
+// else runs redundantly on identical data, so every rank takes the same
+// decisions without further exchange.
+void solve_tall(dsvd_ctx* ctx, const DevCsr& A, const DevCsr& AT, const dsvd_config& cfg,
+                SolveIO& io, dsvd_observer_fn observer, void* user, int64_t row_offset = 0,
+                int64_t global_m = -1) {
+    cudaStream_t st = ctx->stream;
+    const int64_t m = A.rows, n = A.cols;
+    const bool sharded = ctx->comm != nullptr;
+    if (global_m < 0) global_m = m;
+    const int64_t k = cfg.k;
+    const int64_t l = k + effective_s(cfg);
+    const int64_t ld = padded_ld(l);
+    const bool dash = cfg.alg == DSVD_ALG_DASH;
+    const int64_t max_iters = dash ? cfg.p_max : cfg.p;
+    if (l > 512) fail(DSVD_UNSUPPORTED, "sketch width l > 512 is not supported");
+
+    double* Y = ctx->tbuf<double>("Y", m * ld);  // Omega, then A Q, then B
+    double* T = ctx->tbuf<double>("T", n * ld);
+    double* Qb[2] = {ctx->tbuf<double>("Q0", n * ld), ctx->tbuf<double>("Q1", n * ld)};
+    double* W = ctx->tbuf<double>("W", l * l);
+    double* sv = ctx->tbuf<double>("s", l);
+    double* inv_s = ctx->tbuf<double>("inv_s", l);
+    double* s_stored = ctx->tbuf<double>("s_stored", l);
+    Control* ctrl = ctx->tbuf<Control>("ctrl", 1);
+    const int64_t cap = max_iters > 0 ? max_iters : 1;
+    double* d_alphas = ctx->tbuf<double>("trace.alphas", cap);
+    double* d_shat = ctx->tbuf<double>("trace.s_hat", cap * l);
+    EigSvdOut eo{W, sv, inv_s};
+    const int32_t* gate = &ctrl->stopped;
+
+    control_init(ctrl, s_stored, static_cast<int>(l), st);
+    count_launch();
+
+    // Omega = gaussian_matrix(m, l, seed) (solver.cpp:83)
+    int sp = ctx->span_begin(K_OTHER);
+    gaussian_rowmajor(Y, m, l, ld, cfg.seed, st, global_m, row_offset);
+    count_launch();
+    ctx->span_end(sp);
+
+    // Q = eigSVD(A^T Omega).u
+    sp = ctx->span_begin(K_SPMM2);
+    spmm(SpmmArgs{&AT, Y, T, ld, l, nullptr, nullptr, nullptr}, st, ctx->spmm_variant);
+    count_launch();
+    ctx->span_end(sp);
+    if (sharded) {
+        sp = ctx->span_begin(K_COMM);
+        comm_allreduce_sum(ctx, T, static_cast<size_t>(n * ld));
+        ctx->span_end(sp);
+    }
+    eig_svd_factors(ctx, T, n, l, ld, eo, ctrl, nullptr, nullptr);
+    sp = ctx->span_begin(K_RESCALE);
+    rescale(T, n, l, ld, W, l, inv_s, l, Qb[0], ld, 0, nullptr, st);
+    count_launch();
+    ctx->span_end(sp);
+
+    LoopStep ls;
+    ls.k = k;
+    ls.tol = cfg.tol;
+    ls.alg = cfg.alg;
+    ls.alphas = d_alphas;
+    ls.s_hat = d_shat;
+    ls.cap = cap;
+    ls.s_stored = s_stored;
+
+    if (dash && ctx->host_flags == nullptr) {
+        DSVD_CUDA_CHECK(cudaMallocHost(&ctx->host_flags, sizeof(int32_t) * (kLookahead + 1)));
+    }
+    std::vector<cudaEvent_t> flag_ev(kLookahead + 1, nullptr);
+    int cur = 0;
+    for (int64_t j = 1; j <= max_iters; ++j) {
+        if (dash && !observer && j > kLookahead) {
+            const int slot = static_cast<int>((j - kLookahead) % (kLookahead + 1));
+            DSVD_CUDA_CHECK(cudaEventSynchronize(flag_ev[slot]));
+            if (ctx->host_flags[slot]) break;
+        }
+        loop_begin(ctrl, st);
+        count_launch();
+        // Y = A Q
+        sp = ctx->span_begin(K_SPMM1);
+        spmm(SpmmArgs{&A, Qb[cur], Y, ld, l, nullptr, nullptr, gate}, st, ctx->spmm_variant);
+        count_launch();
+        ctx->span_end(sp);
+        // T = A^T Y - alpha Q  (add_scaled skipped when alpha == 0)
+        sp = ctx->span_begin(K_SPMM2);
+        spmm(SpmmArgs{&AT, Y, T, ld, l, sharded ? nullptr : Qb[cur], sharded ? nullptr : &ctrl->alpha,
+                      gate},
+             st, ctx->spmm_variant);
+        count_launch();
+        ctx->span_end(sp);
+        if (sharded) {
+            // sum the partials first, then apply the shift once (solver.cpp:94)
+            sp = ctx->span_begin(K_COMM);
+            comm_allreduce_sum(ctx, T, static_cast<size_t>(n * ld));
+            ctx->span_end(sp);
+            shift_update(T, Qb[cur], n * ld, &ctrl->alpha, gate, st);
+            count_launch();
+        }
+        eig_svd_factors(ctx, T, n, l, ld, eo, ctrl, &ls, gate);
+        sp = ctx->span_begin(K_RESCALE);
+        rescale(T, n, l, ld, W, l, inv_s, l, Qb[1 - cur], ld, 0, gate, st);
+        count_launch();
+        ctx->span_end(sp);
+        if (dash) {
+            const int slot = static_cast<int>(j % (kLookahead + 1));
+            if (flag_ev[slot] == nullptr) flag_ev[slot] = ctx->event();
+            DSVD_CUDA_CHECK(cudaMemcpyAsync(&ctx->host_flags[slot], &ctrl->stop_pending,
+                                            sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+            DSVD_CUDA_CHECK(cudaEventRecord(flag_ev[slot], st));
+        }
+        if (observer) {
+            Control hc = read_control(ctx, ctrl);
+            raise_device_status(hc);
+            std::vector<double> qb = to_host_colmajor(ctx, Qb[cur], n, l, ld);
+            std::vector<double> qa = to_host_colmajor(ctx, Qb[1 - cur], n, l, ld);
+            std::vector<double> sh(static_cast<size_t>(l));
+            double alpha_used = 0.0;
+            DSVD_CUDA_CHECK(cudaMemcpy(sh.data(), d_shat + (j - 1) * l, sizeof(double) * l,
+                                       cudaMemcpyDeviceToHost));
+            DSVD_CUDA_CHECK(cudaMemcpy(&alpha_used, d_alphas + (j - 1), sizeof(double),
+                                       cudaMemcpyDeviceToHost));
+            observer(j, alpha_used, sh.data(), l, qb.data(), qa.data(), n, user);
+            if (hc.stop_pending) {
+                cur = 1 - cur;
+                break;
+            }
+        }
+        cur = 1 - cur;
+    }
+    Control hc = read_control(ctx, ctrl);
+    raise_device_status(hc);
+    io.iterations = hc.iteration;
+    io.stop_reason = dash ? (hc.stop_pending ? DSVD_STOP_TOL_MET : DSVD_STOP_P_MAX_REACHED)
+                          : DSVD_STOP_FIXED_P;
+    ctx->stats.eig_sweeps = hc.total_sweeps;
+    const double* Qf = Qb[hc.iteration % 2];
+
+    // finalize_row_basis: B = A Q, eigSVD(B), U = B V' diag(1/s) [:, :k], V = Q V'[:, :k]
+    control_init(ctrl, s_stored, static_cast<int>(l), st);
+    count_launch();
+    sp = ctx->span_begin(K_SPMM1);
+    spmm(SpmmArgs{&A, Qf, Y, ld, l, nullptr, nullptr, nullptr}, st, ctx->spmm_variant);
+    count_launch();
+    ctx->span_end(sp);
+    eig_svd_factors(ctx, Y, m, l, ld, eo, ctrl, nullptr, nullptr, sharded, global_m);
+    hc = read_control(ctx, ctrl);
+    raise_device_status(hc);
+    ctx->stats.eig_sweeps += hc.total_sweeps;
+
+    double* du = io.on_device ? io.u : ctx->tbuf<double>("out.u", m * k);
+    double* dv = io.on_device ? io.v : ctx->tbuf<double>("out.v", n * k);
+    sp = ctx->span_begin(K_RESCALE);
+    rescale(Y, m, l, ld, W, l, inv_s, k, du, 0, 1, nullptr, st);
+    rescale(Qf, n, l, ld, W, l, nullptr, k, dv, 0, 1, nullptr, st);
+    count_launch(2);
+    ctx->span_end(sp);
+    if (io.on_device) {
+        DSVD_CUDA_CHECK(cudaMemcpyAsync(io.s, sv, sizeof(double) * k, cudaMemcpyDeviceToDevice, st));
+    } else {
+        sp = ctx->span_begin(K_OTHER);
+        DSVD_CUDA_CHECK(cudaMemcpyAsync(io.u, du, sizeof(double) * m * k, cudaMemcpyDeviceToHost, st));
+        DSVD_CUDA_CHECK(cudaMemcpyAsync(io.v, dv, sizeof(double) * n * k, cudaMemcpyDeviceToHost, st));
+        DSVD_CUDA_CHECK(cudaMemcpyAsync(io.s, sv, sizeof(double) * k, cudaMemcpyDeviceToHost, st));
+        ctx->span_end(sp);
+    }
+    const int64_t nrec = std::min(io.iterations, io.cap);
+    if (nrec > 0 && io.alphas)
+        DSVD_CUDA_CHECK(cudaMemcpyAsync(io.alphas, d_alphas, sizeof(double) * nrec,
+                                        cudaMemcpyDeviceToHost, st));
+    if (nrec > 0 && io.s_hat)
+        DSVD_CUDA_CHECK(cudaMemcpyAsync(io.s_hat, d_shat, sizeof(double) * nrec * l,
+                                        cudaMemcpyDeviceToHost, st));
+    DSVD_CUDA_CHECK(cudaStreamSynchronize(st));
+}
+
+void begin_profile(dsvd_ctx* ctx) {
+    ctx->stats = dsvd_stats{};
+    ctx->spans.clear();
+    ctx->event_next = 0;
+}
+
+void end_profile(dsvd_ctx* ctx, int64_t launches_before) {
+    dsvd_stats& s = ctx->stats;
+    s.kernel_launches = g_launches.load() - launches_before;
+    if (!ctx->profiling) return;
+    for (const auto& sp : ctx->spans) {
+        float ms = 0.f;
+        DSVD_CUDA_CHECK(cudaEventElapsedTime(&ms, sp.a, sp.b));
+        switch (sp.cls) {
+            case K_SPMM1:
+                s.spmm_pass_ms[0] += ms;
+                s.spmm_pass_launches[0] += 1;
+                s.spmm_ms += ms;
+                s.spmm_launches += 1;
+                break;
+            case K_SPMM2:
+                s.spmm_pass_ms[1] += ms;
+                s.spmm_pass_launches[1] += 1;
+                s.spmm_ms += ms;
+                s.spmm_launches += 1;
+                break;
+            case K_GRAM: s.gram_ms += ms; break;
+            case K_EIG: s.eig_ms += ms; break;
+            case K_RESCALE: s.rescale_ms += ms; break;
+            default: break;
+        }
+    }
+}
+
+// Run `f` with the boundary contract: Failure -> status code + message.
+template <class F>
+int guarded(F&& f) {
+    try {
+        f();
+        return DSVD_OK;
+    } catch (const Failure& e) {
+        t_err = e.what();
+        t_err_index = e.index;
+        return e.code;
+    } catch (const std::bad_alloc& e) {
+        t_err = "host allocation failed";
+        return DSVD_OOM;
+    } catch (const std::exception& e) {
+        t_err = e.what();
+        return DSVD_OTHER;
+    }
+}
+
+void solve_pair(dsvd_ctx* ctx, const DevCsr& a, const DevCsr& at, const dsvd_config& cfg,
+                dsvd_outputs* out, dsvd_observer_fn observer, void* user, int64_t row_offset = 0,
+                int64_t global_rows = -1) {
+    if (ctx->comm != nullptr) {
+        // row-sharded solve: validate against the global shape
+        const int64_t gm = global_rows >= 0 ? global_rows : a.rows;
+        validate(cfg, gm, a.cols);
+        if (cfg.alg == DSVD_ALG_BASIC)
+            fail(DSVD_UNSUPPORTED, "the basic algorithm is not on the B200 path (shifted family only)");
+        if (gm < a.cols) fail(DSVD_UNSUPPORTED, "row-sharded solves need rows >= cols");
+        SolveIO io;
+        io.on_device = out->outputs_on_device != 0;
+        io.alphas = out->alphas;
+        io.s_hat = out->s_hat;
+        io.cap = out->trace_cap;
+        io.u = out->u;
+        io.v = out->v;
+        io.s = out->s;
+        solve_tall(ctx, a, at, cfg, io, observer, user, row_offset, gm);
+        out->iterations = io.iterations;
+        out->stop_reason = io.stop_reason;
+        return;
+    }
+    validate(cfg, a.rows, a.cols);
+    if (cfg.alg == DSVD_ALG_BASIC)
+        fail(DSVD_UNSUPPORTED, "the basic algorithm is not on the B200 path (shifted family only)");
+    const int64_t l = cfg.k + effective_s(cfg);
+    const bool direct = (cfg.flags & DSVD_FLAG_DIRECT) != 0;
+    SolveIO io;
+    io.on_device = out->outputs_on_device != 0;
+    io.alphas = out->alphas;
+    io.s_hat = out->s_hat;
+    io.cap = out->trace_cap;
+    if (a.rows < a.cols && !direct) {
+        // solve on the transpose and swap U/V (solver.cpp:217-220)
+        io.u = out->v;
+        io.v = out->u;
+        io.s = out->s;
+        solve_tall(ctx, at, a, cfg, io, observer, user);
+    } else {
+        io.u = out->u;
+        io.v = out->v;
+        io.s = out->s;
+        solve_tall(ctx, a, at, cfg, io, observer, user);
+    }
+    (void)l;
+    out->iterations = io.iterations;
+    out->stop_reason = io.stop_reason;
+}
+
+// Algorithmic SpMM bytes of one solve: per pass
+// 12 nnz + 8 (rows+1) + 8 X + 8 Y (+ 8 Q for the shifted pass 2).
+void account_spmm_bytes(dsvd_ctx* ctx, const DevCsr& a, const dsvd_config& cfg, int64_t iters) {
+    const DevCsr* tall = &a;
+    int64_t m = tall->rows, n = tall->cols;
+    if (m < n) std::swap(m, n);
+    const int64_t l = cfg.k + effective_s(cfg);
+    const int64_t b1 = 12 * a.nnz + 8 * (m + 1) + 8 * n * l + 8 * m * l;
+    const int64_t b2 = 12 * a.nnz + 8 * (n + 1) + 8 * m * l + 8 * n * l + 8 * n * l;
+    const int64_t b2_first = 12 * a.nnz + 8 * (n + 1) + 8 * m * l + 8 * n * l;
+    ctx->stats.spmm_pass_bytes[0] = b1 * (iters + 1);
+    ctx->stats.spmm_pass_bytes[1] = b2 * iters + b2_first;
+    ctx->stats.spmm_bytes = ctx->stats.spmm_pass_bytes[0] + ctx->stats.spmm_pass_bytes[1];
+}
+
+}  // namespace
+}  // namespace dsvd
+
+using namespace dsvd;
+
+extern "C" {
+
+const char* dsvd_last_error(void) { return t_err.c_str(); }
+long long dsvd_last_error_index(void) { return t_err_index; }
+const char* dsvd_version(void) { return "dashsvd-b200 0.1 (sm_100a)"; }
+
+int dsvd_ctx_create(int device, dsvd_ctx** out) {
+    return guarded([&] {
+        int count = 0;
+        DSVD_CUDA_CHECK(cudaGetDeviceCount(&count));
+        if (device < 0 || device >= count) fail(DSVD_CUDA, "no such CUDA device");
+        std::unique_ptr<dsvd_ctx> c(new dsvd_ctx());
+        c->device = device;
+        DSVD_CUDA_CHECK(cudaSetDevice(device));
+        DSVD_CUDA_CHECK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+        *out = c.release();
+    });
+}
+
+int dsvd_ctx_destroy(dsvd_ctx* ctx) {
+    return guarded([&] {
+        if (!ctx) return;
+        cudaSetDevice(ctx->device);
+        cudaStreamSynchronize(ctx->stream);
+        for (auto& kv : ctx->arena)
+            if (kv.second.ptr) cudaFree(kv.second.ptr);
+        for (auto e : ctx->event_pool) cudaEventDestroy(e);
+        if (ctx->timer[0]) {
+            cudaEventDestroy(ctx->timer[0]);
+            cudaEventDestroy(ctx->timer[1]);
+        }
+        if (ctx->host_flags) cudaFreeHost(ctx->host_flags);
+        comm_release(ctx);
+        cudaStreamDestroy(ctx->stream);
+        delete ctx;
+    });
+}
+
+int dsvd_ctx_set_profiling(dsvd_ctx* ctx, int on) {
+    return guarded([&] { ctx->profiling = on != 0; });
+}
+
+int dsvd_ctx_get_stats(const dsvd_ctx* ctx, dsvd_stats* out) {
+    return guarded([&] { *out = ctx->stats; });
+}
+
+int dsvd_ctx_synchronize(dsvd_ctx* ctx) {
+    return guarded([&] {
+        set_device(ctx);
+        DSVD_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+int dsvd_ctx_set_option(dsvd_ctx* ctx, const char* name, int64_t value) {
+    return guarded([&] {
+        const std::string n = name ? name : "";
+        if (n == "spmm_variant") {
+            ctx->spmm_variant = static_cast<int>(value);
+        } else {
+            fail(DSVD_CONFIG, "unknown option '" + n + "'");
+        }
+    });
+}
+
+int dsvd_host_register(void* ptr, size_t bytes) {
+    return guarded([&] { DSVD_CUDA_CHECK(cudaHostRegister(ptr, bytes, cudaHostRegisterDefault)); });
+}
+
+int dsvd_host_unregister(void* ptr) {
+    return guarded([&] { DSVD_CUDA_CHECK(cudaHostUnregister(ptr)); });
+}
+
+int dsvd_matrix_upload(dsvd_ctx* ctx, int64_t rows, int64_t cols, int64_t nnz,
+                       const int64_t* offsets, const int64_t* col_indices, const double* values,
+                       dsvd_matrix** out) {
+    return guarded([&] {
+        set_device(ctx);
+        std::unique_ptr<dsvd_matrix> m(new dsvd_matrix());
+        m->ctx = ctx;
+        CsrAlloc al{ctx, "", &m->owned};
+        try {
+            // upload_pair allocates a.off / a.val through `al` (owned)
+            upload_pair(ctx, al, rows, cols, nnz, offsets, col_indices, values, m->a, m->at);
+        } catch (...) {
+            for (void* p : m->owned) cudaFree(p);
+            throw;
+        }
+        *out = m.release();
+    });
+}
+
+int dsvd_matrix_from_device(dsvd_ctx* ctx, int64_t rows, int64_t cols, int64_t nnz,
+                            const int64_t* d_offsets, const int64_t* d_col_indices,
+                            const double* d_values, dsvd_matrix** out) {
+    return guarded([&] {
+        set_device(ctx);
+        std::unique_ptr<dsvd_matrix> m(new dsvd_matrix());
+        m->ctx = ctx;
+        CsrAlloc al{ctx, "", &m->owned};
+        try {
+            build_pair(ctx, al, rows, cols, nnz, d_offsets, d_col_indices, d_values, m->a, m->at,
+                       true);
+        } catch (...) {
+            for (void* p : m->owned) cudaFree(p);
+            throw;
+        }
+        *out = m.release();
+    });
+}
+
+int dsvd_matrix_destroy(dsvd_matrix* m) {
+    return guarded([&] {
+        if (!m) return;
+        cudaSetDevice(m->ctx->device);
+        cudaStreamSynchronize(m->ctx->stream);
+        for (void* p : m->owned) cudaFree(p);
+        delete m;
+    });
+}
+
+int dsvd_matrix_set_shard(dsvd_matrix* m, int64_t row_offset, int64_t global_rows) {
+    return guarded([&] {
+        if (row_offset < 0 || global_rows < row_offset + m->a.rows)
+            fail(DSVD_SHAPE, "shard rows exceed the global row count");
+        m->row_offset = row_offset;
+        m->global_rows = global_rows;
+    });
+}
+
+int dsvd_matrix_shape(const dsvd_matrix* m, int64_t* rows, int64_t* cols, int64_t* nnz) {
+    return guarded([&] {
+        *rows = m->a.rows;
+        *cols = m->a.cols;
+        *nnz = m->a.nnz;
+    });
+}
+
+int dsvd_matrix_download_transpose(const dsvd_matrix* m, int64_t* t_off, int64_t* t_idx,
+                                   double* t_val) {
+    return guarded([&] {
+        dsvd_ctx* ctx = m->ctx;
+        set_device(ctx);
+        cudaStream_t st = ctx->stream;
+        const DevCsr& at = m->at;
+        int64_t* w = ctx->tbuf<int64_t>("dl.idx64", at.nnz);
+        widen_indices(at.idx, w, at.nnz, st);
+        DSVD_CUDA_CHECK(cudaMemcpyAsync(t_off, at.off, sizeof(int64_t) * (at.rows + 1),
+                                        cudaMemcpyDeviceToHost, st));
+        if (at.nnz) {
+            DSVD_CUDA_CHECK(cudaMemcpyAsync(t_idx, w, sizeof(int64_t) * at.nnz, cudaMemcpyDeviceToHost, st));
+            DSVD_CUDA_CHECK(cudaMemcpyAsync(t_val, at.val, sizeof(double) * at.nnz, cudaMemcpyDeviceToHost, st));
+        }
+        DSVD_CUDA_CHECK(cudaStreamSynchronize(st));
+    });
+}
+
+int dsvd_solve(dsvd_ctx* ctx, const dsvd_matrix* a, const dsvd_config* cfg, dsvd_outputs* out,
+               dsvd_observer_fn observer, void* user) {
+    return guarded([&] {
+        set_device(ctx);
+        const int64_t l0 = g_launches.load();
+        begin_profile(ctx);
+        cudaEvent_t e0 = ctx->event(), e1 = ctx->event();
+        DSVD_CUDA_CHECK(cudaEventRecord(e0, ctx->stream));
+        solve_pair(ctx, a->a, a->at, *cfg, out, observer, user, a->row_offset, a->global_rows);
+        DSVD_CUDA_CHECK(cudaEventRecord(e1, ctx->stream));
+        DSVD_CUDA_CHECK(cudaEventSynchronize(e1));
+        float ms = 0.f;
+        DSVD_CUDA_CHECK(cudaEventElapsedTime(&ms, e0, e1));
+        end_profile(ctx, l0);
+        ctx->stats.total_ms = ms;
+        account_spmm_bytes(ctx, a->a, *cfg, out->iterations);
+    });
+}
+
+int dsvd_solve_csr(dsvd_ctx* ctx, int64_t rows, int64_t cols, int64_t nnz, const int64_t* offsets,
+                   const int64_t* col_indices, const double* values, const dsvd_config* cfg,
+                   dsvd_outputs* out) {
+    return guarded([&] {
+        set_device(ctx);
+        if (ctx->comm == nullptr) validate(*cfg, rows, cols);
+        const int64_t l0 = g_launches.load();
+        begin_profile(ctx);
+        cudaEvent_t e0 = ctx->event(), e1 = ctx->event(), e2 = ctx->event();
+        DSVD_CUDA_CHECK(cudaEventRecord(e0, ctx->stream));
+        DevCsr a, at;
+        CsrAlloc al{ctx, "csr.", nullptr};
+        upload_pair(ctx, al, rows, cols, nnz, offsets, col_indices, values, a, at);
+        DSVD_CUDA_CHECK(cudaEventRecord(e1, ctx->stream));
+        solve_pair(ctx, a, at, *cfg, out, nullptr, nullptr, ctx->shard_row_offset,
+                   ctx->shard_global_rows);
+        DSVD_CUDA_CHECK(cudaEventRecord(e2, ctx->stream));
+        DSVD_CUDA_CHECK(cudaEventSynchronize(e2));
+        float ms = 0.f, ms_up = 0.f;
+        DSVD_CUDA_CHECK(cudaEventElapsedTime(&ms, e0, e2));
+        DSVD_CUDA_CHECK(cudaEventElapsedTime(&ms_up, e0, e1));
+        end_profile(ctx, l0);
+        ctx->stats.total_ms = ms;
+        ctx->stats.csc_ms = ms_up;
+        account_spmm_bytes(ctx, a, *cfg, out->iterations);
+    });
+}
+
+int dsvd_solve_csr_device(dsvd_ctx* ctx, int64_t rows, int64_t cols, int64_t nnz,
+                          const int64_t* d_off, const int64_t* d_idx, const double* d_val,
+                          const dsvd_config* cfg, dsvd_outputs* out) {
+    return guarded([&] {
+        set_device(ctx);
+        if (ctx->comm == nullptr) validate(*cfg, rows, cols);
+        const int64_t l0 = g_launches.load();
+        begin_profile(ctx);
+        cudaEvent_t e0 = ctx->event(), e1 = ctx->event(), e2 = ctx->event();
+        DSVD_CUDA_CHECK(cudaEventRecord(e0, ctx->stream));
+        DevCsr a, at;
+        CsrAlloc al{ctx, "csr.", nullptr};
+        build_pair(ctx, al, rows, cols, nnz, d_off, d_idx, d_val, a, at, false);
+        DSVD_CUDA_CHECK(cudaEventRecord(e1, ctx->stream));
+        solve_pair(ctx, a, at, *cfg, out, nullptr, nullptr, ctx->shard_row_offset,
+                   ctx->shard_global_rows);
+        DSVD_CUDA_CHECK(cudaEventRecord(e2, ctx->stream));
+        DSVD_CUDA_CHECK(cudaEventSynchronize(e2));
+        float ms = 0.f, ms_up = 0.f;
+        DSVD_CUDA_CHECK(cudaEventElapsedTime(&ms, e0, e2));
+        DSVD_CUDA_CHECK(cudaEventElapsedTime(&ms_up, e0, e1));
+        end_profile(ctx, l0);
+        ctx->stats.total_ms = ms;
+        ctx->stats.csc_ms = ms_up;
+        account_spmm_bytes(ctx, a, *cfg, out->iterations);
+    });
+}
+
+int dsvd_ctx_set_shard(dsvd_ctx* ctx, int64_t row_offset, int64_t global_rows) {
+    return guarded([&] {
+        if (row_offset < 0) fail(DSVD_SHAPE, "negative shard offset");
+        ctx->shard_row_offset = row_offset;
+        ctx->shard_global_rows = global_rows;
+    });
+}
+
+int dsvd_ctx_timer_start(dsvd_ctx* ctx) {
+    return guarded([&] {
+        set_device(ctx);
+        if (!ctx->timer[0]) {
+            DSVD_CUDA_CHECK(cudaEventCreate(&ctx->timer[0]));
+            DSVD_CUDA_CHECK(cudaEventCreate(&ctx->timer[1]));
+        }
+        DSVD_CUDA_CHECK(cudaEventRecord(ctx->timer[0], ctx->stream));
+    });
+}
+
+int dsvd_ctx_timer_stop(dsvd_ctx* ctx, double* elapsed_ms) {
+    return guarded([&] {
+        set_device(ctx);
+        if (!ctx->timer[0]) fail(DSVD_CONFIG, "timer not started");
+        DSVD_CUDA_CHECK(cudaEventRecord(ctx->timer[1], ctx->stream));
+        DSVD_CUDA_CHECK(cudaEventSynchronize(ctx->timer[1]));
+        float ms = 0.f;
+        DSVD_CUDA_CHECK(cudaEventElapsedTime(&ms, ctx->timer[0], ctx->timer[1]));
+        *elapsed_ms = ms;
+    });
+}
+
+int dsvd_finalize_row_basis(dsvd_ctx* ctx, const dsvd_matrix* a, const double* q, int64_t l,
+                            int64_t k, double* u, double* s, double* v) {
+    return guarded([&] {
+        set_device(ctx);
+        cudaStream_t st = ctx->stream;
+        const DevCsr& A = a->a;
+        const int64_t m = A.rows, n = A.cols;
+        if (k < 1 || k > l) fail(DSVD_SHAPE, "finalize_row_basis: k out of range");
+        if (l > m) fail(DSVD_SHAPE, "eig_svd: needs rows >= cols (factor the transpose instead)");
+        const int64_t ld = padded_ld(l);
+        double* qh = ctx->tbuf<double>("fin.qcm", n * l);
+        double* Q = ctx->tbuf<double>("fin.Q", n * ld);
+        double* B = ctx->tbuf<double>("fin.B", m * ld);
+        double* W = ctx->tbuf<double>("W", l * l);
+        double* sv = ctx->tbuf<double>("s", l);
+        double* inv_s = ctx->tbuf<double>("inv_s", l);
+        double* s_stored = ctx->tbuf<double>("s_stored", l);
+        Control* ctrl = ctx->tbuf<Control>("ctrl", 1);
+        DSVD_CUDA_CHECK(cudaMemcpyAsync(qh, q, sizeof(double) * n * l, cudaMemcpyHostToDevice, st));
+        colmajor_to_rowmajor(qh, n, l, Q, ld, st);
+        control_init(ctrl, s_stored, static_cast<int>(l), st);
+        spmm(SpmmArgs{&A, Q, B, ld, l, nullptr, nullptr, nullptr}, st, ctx->spmm_variant);
+        EigSvdOut eo{W, sv, inv_s};
+        eig_svd_factors(ctx, B, m, l, ld, eo, ctrl, nullptr, nullptr);
+        raise_device_status(read_control(ctx, ctrl));
+        double* du = ctx->tbuf<double>("out.u", m * k);
+        double* dv = ctx->tbuf<double>("out.v", n * k);
+        rescale(B, m, l, ld, W, l, inv_s, k, du, 0, 1, nullptr, st);
+        rescale(Q, n, l, ld, W, l, nullptr, k, dv, 0, 1, nullptr, st);
+        DSVD_CUDA_CHECK(cudaMemcpyAsync(u, du, sizeof(double) * m * k, cudaMemcpyDeviceToHost, st));
+        DSVD_CUDA_CHECK(cudaMemcpyAsync(v, dv, sizeof(double) * n * k, cudaMemcpyDeviceToHost, st));
+        DSVD_CUDA_CHECK(cudaMemcpyAsync(s, sv, sizeof(double) * k, cudaMemcpyDeviceToHost, st));
+        DSVD_CUDA_CHECK(cudaStreamSynchronize(st));
+    });
+}
+
+int dsvd_validate_config(const dsvd_config* cfg, int64_t rows, int64_t cols) {
+    return guarded([&] { validate(*cfg, rows, cols); });
+}
+
+double dsvd_update_shift(double alpha, double s_ll) {
+    return s_ll > alpha ? (s_ll + alpha) / 2.0 : alpha;
+}
+
+int dsvd_pve_stop_check(const double* prev, int64_t n_prev, double alpha_prev, const double* cur,
+                        int64_t n, double alpha, int64_t k, double tol, int* stop) {
+    return guarded([&] {
+        if (k < 1) fail(DSVD_SHAPE, "pve_stop_check: k must be >= 1");
+        if (n_prev < k + 1 || n < k + 1)
+            fail(DSVD_SHAPE, "pve_stop_check: surrogate arrays must hold at least k+1 values");
+        const double denom = cur[k] + alpha;
+        *stop = 1;
+        for (int64_t i = 0; i < k; ++i) {
+            const double change = std::fabs(prev[i] + alpha_prev - cur[i] - alpha);
+            if (!(change / denom <= tol)) {
+                *stop = 0;
+                return;
+            }
+        }
+    });
+}
+
+uint64_t dsvd_splitmix64_at(uint64_t seed, uint64_t i) { return splitmix64_at(seed, i); }
+
+// ---- kernel-level entry points ------------------------------------------------
+
+int dsvd_spmm(dsvd_ctx* ctx, int64_t rows, int64_t cols, int64_t nnz, const int64_t* offsets,
+              const int64_t* col_indices, const double* values, const double* x, int64_t l,
+              double* y) {
+    return dsvd_spmm_shift(ctx, rows, cols, nnz, offsets, col_indices, values, x, l, 0.0, nullptr, y);
+}
+
+int dsvd_spmm_shift(dsvd_ctx* ctx, int64_t rows, int64_t cols, int64_t nnz, const int64_t* offsets,
+                    const int64_t* col_indices, const double* values, const double* x, int64_t l,
+                    double alpha, const double* q, double* y) {
+    return guarded([&] {
+        set_device(ctx);
+        cudaStream_t st = ctx->stream;
+        if (l < 0) fail(DSVD_SHAPE, "spmm: negative width");
+        DevCsr a, at;
+        CsrAlloc al{ctx, "k.", nullptr};
+        upload_pair(ctx, al, rows, cols, nnz, offsets, col_indices, values, a, at);
+        if (l == 0 || rows == 0) return;
+        const int64_t ld = padded_ld(l);
+        double* xc = ctx->tbuf<double>("k.xcm", std::max(cols * l, rows * l));
+        double* X = ctx->tbuf<double>("k.X", cols * ld);
+        double* Yd = ctx->tbuf<double>("k.Y", rows * ld);
+        double* Qd = nullptr;
+        double* d_alpha = ctx->tbuf<double>("k.alpha", 1);
+        if (cols > 0) {
+            DSVD_CUDA_CHECK(cudaMemcpyAsync(xc, x, sizeof(double) * cols * l, cudaMemcpyHostToDevice, st));
+            colmajor_to_rowmajor(xc, cols, l, X, ld, st);
+        }
+        if (q != nullptr) {
+            Qd = ctx->tbuf<double>("k.Q", rows * ld);
+            double* qc = ctx->tbuf<double>("k.qcm", rows * l);
+            DSVD_CUDA_CHECK(cudaMemcpyAsync(qc, q, sizeof(double) * rows * l, cudaMemcpyHostToDevice, st));
+            colmajor_to_rowmajor(qc, rows, l, Qd, ld, st);
+            DSVD_CUDA_CHECK(cudaMemcpyAsync(d_alpha, &alpha, sizeof(double), cudaMemcpyHostToDevice, st));
+        }
+        spmm(SpmmArgs{&a, X, Yd, ld, l, Qd, Qd ? d_alpha : nullptr, nullptr}, st, ctx->spmm_variant);
+        rowmajor_to_colmajor(Yd, rows, l, ld, xc, st);
+        DSVD_CUDA_CHECK(cudaMemcpyAsync(y, xc, sizeof(double) * rows * l, cudaMemcpyDeviceToHost, st));
+        DSVD_CUDA_CHECK(cudaStreamSynchronize(st));
+    });
+}
+
+int dsvd_transpose(dsvd_ctx* ctx, int64_t rows, int64_t cols, int64_t nnz, const int64_t* offsets,
+                   const int64_t* col_indices, const double* values, int64_t* t_off,
+                   int64_t* t_idx, double* t_val) {
+    return guarded([&] {
+        set_device(ctx);
+        cudaStream_t st = ctx->stream;
+        DevCsr a, at;
+        CsrAlloc al{ctx, "k.", nullptr};
+        upload_pair(ctx, al, rows, cols, nnz, offsets, col_indices, values, a, at);
+        int64_t* w = ctx->tbuf<int64_t>("dl.idx64", nnz);
+        widen_indices(at.idx, w, nnz, st);
+        DSVD_CUDA_CHECK(cudaMemcpyAsync(t_off, at.off, sizeof(int64_t) * (cols + 1), cudaMemcpyDeviceToHost, st));
+        if (nnz) {
+            DSVD_CUDA_CHECK(cudaMemcpyAsync(t_idx, w, sizeof(int64_t) * nnz, cudaMemcpyDeviceToHost, st));
+            DSVD_CUDA_CHECK(cudaMemcpyAsync(t_val, at.val, sizeof(double) * nnz, cudaMemcpyDeviceToHost, st));
+        }
+        DSVD_CUDA_CHECK(cudaStreamSynchronize(st));
+    });
+}
+
+int dsvd_gram(dsvd_ctx* ctx, int64_t rows, int64_t cols, const double* c, double* g) {
+    return guarded([&] {
+        set_device(ctx);
+        cudaStream_t st = ctx->stream;
+        if (cols == 0) return;
+        const int64_t ld = padded_ld(cols);
+        double* cc = ctx->tbuf<double>("k.ccm", rows * cols);
+        double* C = ctx->tbuf<double>("k.C", rows * ld);
+        double* G = ctx->tbuf<double>("k.G", cols * cols);
+        DSVD_CUDA_CHECK(cudaMemcpyAsync(cc, c, sizeof(double) * rows * cols, cudaMemcpyHostToDevice, st));
+        colmajor_to_rowmajor(cc, rows, cols, C, ld, st);
+        const size_t gws = gram_workspace_bytes(rows, cols);
+        gram(C, rows, cols, ld, G, ctx->buf("k.gws", gws), gws, nullptr, st);
+        DSVD_CUDA_CHECK(cudaMemcpyAsync(g, G, sizeof(double) * cols * cols, cudaMemcpyDeviceToHost, st));
+        DSVD_CUDA_CHECK(cudaStreamSynchronize(st));
+    });
+}
+
+int dsvd_sym_eig(dsvd_ctx* ctx, int64_t n, const double* g, double* values, double* vectors) {
+    return guarded([&] {
+        set_device(ctx);
+        cudaStream_t st = ctx->stream;
+        if (n == 0) return;
+        if (n > 512) fail(DSVD_UNSUPPORTED, "sym_eig: n > 512 is not supported");
+        // symmetry check exactly as sym_eig.cpp:139-146
+        double scale = 0.0, asym = 0.0;
+        for (int64_t j = 0; j < n; ++j)
+            for (int64_t i = 0; i < n; ++i) {
+                scale = std::max(scale, std::fabs(g[j * n + i]));
+                asym = std::max(asym, std::fabs(g[j * n + i] - g[i * n + j]));
+            }
+        if (asym > 1e-10 * std::max(scale, 1e-300)) fail(DSVD_SHAPE, "sym_eig: matrix is not symmetric");
+        double* G = ctx->tbuf<double>("k.G", n * n);
+        // row-major copy of a column-major matrix: transpose on the host side of the copy
+        std::vector<double> rm(static_cast<size_t>(n * n));
+        for (int64_t i = 0; i < n; ++i)
+            for (int64_t j = 0; j < n; ++j) rm[i * n + j] = g[j * n + i];
+        DSVD_CUDA_CHECK(cudaMemcpyAsync(G, rm.data(), sizeof(double) * n * n, cudaMemcpyHostToDevice, st));
+        Control* ctrl = ctx->tbuf<Control>("ctrl", 1);
+        double* s_stored = ctx->tbuf<double>("s_stored", n);
+        control_init(ctrl, s_stored, static_cast<int>(n), st);
+        EigWorkspace ew;
+        eig_workspace_bind(ew, static_cast<int>(n), kMaxSweeps,
+                           ctx->buf("eig.ws", eig_workspace_bytes(static_cast<int>(n), kMaxSweeps)));
+        jacobi_eig(G, ew, ctrl, nullptr, st);
+        double* dv = ctx->tbuf<double>("k.vals", n);
+        double* dV = ctx->tbuf<double>("k.vecs", n * n);
+        sym_eig_finish(ew, dv, dV, st);
+        Control hc = read_control(ctx, ctrl);
+        if (hc.status == DSVD_NUMERICAL) fail(DSVD_NUMERICAL, "symmetric Jacobi iteration did not converge");
+        DSVD_CUDA_CHECK(cudaMemcpyAsync(values, dv, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
+        DSVD_CUDA_CHECK(cudaMemcpyAsync(vectors, dV, sizeof(double) * n * n, cudaMemcpyDeviceToHost, st));
+        DSVD_CUDA_CHECK(cudaStreamSynchronize(st));
+    });
+}
+
+int dsvd_eig_svd(dsvd_ctx* ctx, int64_t rows, int64_t cols, const double* c, double* u, double* s,
+                 double* v) {
+    return guarded([&] {
+        set_device(ctx);
+        cudaStream_t st = ctx->stream;
+        if (rows < cols) fail(DSVD_SHAPE, "eig_svd: needs rows >= cols (factor the transpose instead)");
+        if (cols == 0) return;
+        if (cols > 512) fail(DSVD_UNSUPPORTED, "eig_svd: cols > 512 is not supported");
+        const int64_t l = cols, ld = padded_ld(cols);
+        double* cc = ctx->tbuf<double>("k.ccm", rows * l);
+        double* C = ctx->tbuf<double>("k.C", rows * ld);
+        DSVD_CUDA_CHECK(cudaMemcpyAsync(cc, c, sizeof(double) * rows * l, cudaMemcpyHostToDevice, st));
+        colmajor_to_rowmajor(cc, rows, l, C, ld, st);
+        double* W = ctx->tbuf<double>("W", l * l);
+        double* sv = ctx->tbuf<double>("s", l);
+        double* inv_s = ctx->tbuf<double>("inv_s", l);
+        double* s_stored = ctx->tbuf<double>("s_stored", l);
+        Control* ctrl = ctx->tbuf<Control>("ctrl", 1);
+        control_init(ctrl, s_stored, static_cast<int>(l), st);
+        EigSvdOut eo{W, sv, inv_s};
+        eig_svd_factors(ctx, C, rows, l, ld, eo, ctrl, nullptr, nullptr);
+        raise_device_status(read_control(ctx, ctrl));
+        rescale(C, rows, l, ld, W, l, inv_s, l, cc, 0, 1, nullptr, st);
+        double* vcm = ctx->tbuf<double>("k.vcm", l * l);
+        rowmajor_to_colmajor(W, l, l, l, vcm, st);
+        DSVD_CUDA_CHECK(cudaMemcpyAsync(u, cc, sizeof(double) * rows * l, cudaMemcpyDeviceToHost, st));
+        DSVD_CUDA_CHECK(cudaMemcpyAsync(s, sv, sizeof(double) * l, cudaMemcpyDeviceToHost, st));
+        DSVD_CUDA_CHECK(cudaMemcpyAsync(v, vcm, sizeof(double) * l * l, cudaMemcpyDeviceToHost, st));
+        DSVD_CUDA_CHECK(cudaStreamSynchronize(st));
+    });
+}
+
+int dsvd_matmul(dsvd_ctx* ctx, int64_t m, int64_t kk, int64_t n, const double* a, const double* b,
+                double* c) {
+    return guarded([&] {
+        set_device(ctx);
+        cudaStream_t st = ctx->stream;
+        if (m == 0 || n == 0) return;
+        const int64_t lda = padded_ld(kk), ldb = padded_ld(n);
+        double* ac = ctx->tbuf<double>("k.acm", std::max(m * kk, m * n));
+        double* A = ctx->tbuf<double>("k.A", m * lda);
+        double* bc = ctx->tbuf<double>("k.bcm", kk * n);
+        double* B = ctx->tbuf<double>("k.B", kk * ldb);
+        DSVD_CUDA_CHECK(cudaMemcpyAsync(ac, a, sizeof(double) * m * kk, cudaMemcpyHostToDevice, st));
+        DSVD_CUDA_CHECK(cudaMemcpyAsync(bc, b, sizeof(double) * kk * n, cudaMemcpyHostToDevice, st));
+        colmajor_to_rowmajor(ac, m, kk, A, lda, st);
+        colmajor_to_rowmajor(bc, kk, n, B, ldb, st);
+        rescale(A, m, kk, lda, B, ldb, nullptr, n, ac, 0, 1, nullptr, st);
+        DSVD_CUDA_CHECK(cudaMemcpyAsync(c, ac, sizeof(double) * m * n, cudaMemcpyDeviceToHost, st));
+        DSVD_CUDA_CHECK(cudaStreamSynchronize(st));
+    });
+}
+
+int dsvd_gaussian_matrix(dsvd_ctx* ctx, int64_t rows, int64_t cols, uint64_t seed, double* out) {
+    return guarded([&] {
+        set_device(ctx);
+        cudaStream_t st = ctx->stream;
+        if (rows * cols == 0) return;
+        const int64_t ld = padded_ld(cols);
+        double* R = ctx->tbuf<double>("k.omega", rows * ld);
+        double* Cm = ctx->tbuf<double>("k.omegacm", rows * cols);
+        gaussian_rowmajor(R, rows, cols, ld, seed, st);
+        rowmajor_to_colmajor(R, rows, cols, ld, Cm, st);
+        DSVD_CUDA_CHECK(cudaMemcpyAsync(out, Cm, sizeof(double) * rows * cols, cudaMemcpyDeviceToHost, st));
+        DSVD_CUDA_CHECK(cudaStreamSynchronize(st));
+    });
+}
+
+}  // extern "C"

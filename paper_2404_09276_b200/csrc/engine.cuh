@@ -1,0 +1,100 @@
+// Context / matrix-handle types shared by engine.cu and comm.cu.
+#pragma once
+
+#include <atomic>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "sparse.cuh"
+
+struct dsvd_ctx;
+
+namespace dsvd {
+
+extern std::atomic<int64_t> g_launches;
+
+struct DevBuf {
+    void* ptr = nullptr;
+    size_t bytes = 0;
+};
+
+enum KernelClass { K_SPMM1 = 0, K_SPMM2, K_GRAM, K_EIG, K_RESCALE, K_COMM, K_OTHER, K_NCLASS };
+
+struct TimedSpan {
+    int cls;
+    cudaEvent_t a, b;
+};
+
+// Multi-GPU hooks (comm.cu). With one rank they are no-ops.
+void comm_allreduce_sum(dsvd_ctx* ctx, double* buf, size_t count);
+void comm_release(dsvd_ctx* ctx);
+// thread-local last-error state of the C ABI (engine.cu)
+void set_error(const char* msg, long long index);
+
+}  // namespace dsvd
+
+struct dsvd_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool profiling = false;
+    dsvd_stats stats{};
+    std::map<std::string, dsvd::DevBuf> arena;
+    std::vector<cudaEvent_t> event_pool;
+    size_t event_next = 0;
+    std::vector<dsvd::TimedSpan> spans;
+    int spmm_variant = 0;
+    int32_t* host_flags = nullptr;  // pinned ring for stop flags
+    cudaEvent_t timer[2] = {nullptr, nullptr};
+    // multi-GPU state (comm.cu): NCCL communicator when nranks > 1
+    void* comm = nullptr;
+    int nranks = 1, rank = 0;
+    int64_t shard_row_offset = 0, shard_global_rows = -1;  // for the CSR entry points
+
+    void* buf(const std::string& name, size_t bytes) {
+        auto& b = arena[name];
+        if (b.bytes < bytes) {
+            if (b.ptr) DSVD_CUDA_CHECK(cudaFree(b.ptr));
+            b.ptr = nullptr;
+            b.bytes = 0;
+            DSVD_CUDA_CHECK(cudaMalloc(&b.ptr, bytes > 0 ? bytes : 1));
+            b.bytes = bytes;
+        }
+        return b.ptr;
+    }
+    template <class T>
+    T* tbuf(const std::string& name, size_t count) {
+        return static_cast<T*>(buf(name, sizeof(T) * (count > 0 ? count : 1)));
+    }
+    cudaEvent_t event() {
+        if (event_next == event_pool.size()) {
+            cudaEvent_t e;
+            DSVD_CUDA_CHECK(cudaEventCreate(&e));
+            event_pool.push_back(e);
+        }
+        return event_pool[event_next++];
+    }
+    // Profiling spans: a CUDA-event pair around a group of launches.
+    int span_begin(int cls) {
+        if (!profiling) return -1;
+        dsvd::TimedSpan s{cls, event(), event()};
+        DSVD_CUDA_CHECK(cudaEventRecord(s.a, stream));
+        spans.push_back(s);
+        return static_cast<int>(spans.size()) - 1;
+    }
+    void span_end(int id) {
+        if (id < 0) return;
+        DSVD_CUDA_CHECK(cudaEventRecord(spans[id].b, stream));
+    }
+};
+
+struct dsvd_matrix {
+    dsvd_ctx* ctx = nullptr;
+    dsvd::DevCsr a, at;
+    std::vector<void*> owned;
+    // row shard of a larger matrix (multi-GPU): global row offset and count
+    int64_t row_offset = 0;
+    int64_t global_rows = -1;
+};
+

@@ -1,0 +1,53 @@
+// Device CSR storage and the sparse kernels of the power loop.
+#pragma once
+
+#include "common.cuh"
+
+namespace dsvd {
+
+// Canonical CSR on the device. Offsets stay int64 (nnz may exceed 2^31 at
+// config 5); column indices are int32 (every dimension here is < 2^31), which
+// cuts the per-nonzero stream from 16 to 12 bytes. `order` lists the rows by
+// nonzero count, longest first, so SpMM starts hub rows first.
+struct DevCsr {
+    int64_t rows = 0, cols = 0, nnz = 0;
+    int64_t* off = nullptr;
+    int32_t* idx = nullptr;
+    double* val = nullptr;
+    int32_t* order = nullptr;
+    int64_t max_row_nnz = 0;
+};
+
+// SpMM launch description. X and Y (and Q) are row-major with row stride ld.
+struct SpmmArgs {
+    const DevCsr* a;
+    const double* x;      // a.cols x ld
+    double* y;            // a.rows x ld
+    int64_t ld;
+    int64_t l;            // logical width (<= ld)
+    const double* q;      // shift operand (a.rows x ld) or nullptr
+    const double* alpha;  // device scalar: y = fma(-alpha, q, A x) unless alpha == 0
+    const int32_t* gate;  // device flag: skip the launch's work when *gate != 0 (or nullptr)
+};
+
+void spmm(const SpmmArgs& args, cudaStream_t stream, int variant);
+
+// CSR(A^T) from CSR(A), bitwise equal to the reference transpose().
+// Temporaries come from `scratch` (bytes given by csc_scratch_bytes).
+size_t csc_scratch_bytes(int64_t rows, int64_t cols, int64_t nnz);
+void build_transpose(const DevCsr& a, DevCsr& at, void* scratch, size_t scratch_bytes,
+                     cudaStream_t stream);
+// Row order by nonzero count (descending, ties by row index) into m.order.
+size_t order_scratch_bytes(int64_t rows);
+void build_row_order(DevCsr& m, void* scratch, size_t scratch_bytes, cudaStream_t stream);
+
+// int64 -> int32 column indices with a bounds check; *bad is set to 1 when an
+// index falls outside [0, cols) (the entry is clamped so no kernel faults).
+void narrow_indices(const int64_t* src, int32_t* dst, int64_t nnz, int64_t cols, int32_t* bad,
+                    cudaStream_t stream);
+void widen_indices(const int32_t* src, int64_t* dst, int64_t nnz, cudaStream_t stream);
+// Offset checks: off[0] == 0, off[rows] == nnz, non-decreasing -> *bad = 1 otherwise.
+void check_offsets(const int64_t* off, int64_t rows, int64_t nnz, int32_t* bad,
+                   cudaStream_t stream);
+
+}  // namespace dsvd

@@ -51,3 +51,7 @@ class HypothesisError(Error):
 class DeviceError(Error):
     """CUDA / NCCL / out-of-memory failure inside the B200 path (no reference analogue;
     the reference maps these to its base Error)."""
+
+
+class UnsupportedOnDevice(Error):
+    """A configuration the B200 path does not implement (e.g. the basic algorithm, l > 512)."""

@@ -1,0 +1,400 @@
+"""GPU parity: every device kernel and the full solve, through the C ABI,
+against the oracle (oracle/dashsvd_oracle.c, pinned bitwise to the reference)
+on the same seeded inputs.
+
+Bars (north_star / SURVEY 8d):
+  - integer/byte work and every FMA-chain kernel whose order the device
+    reproduces (CSR transpose, SpMM, SpMM+shift, matmul): BITWISE;
+  - Gram: relative 1e-13 (split-K order differs from the reference's single chain);
+  - eigensolver: relative 1e-12 on eigenvalues (Jacobi vs Householder+QL);
+  - solve: singular values relative 1e-8, principal angles of U and V
+    subspaces <= 1e-6, equal iteration count, PVE ratio at termination
+    relative 1e-6.
+"""
+import numpy as np
+import pytest
+
+import paper_2404_09276_b200 as d
+from oracle_lib import Csr, transpose_np
+
+pytestmark = pytest.mark.gpu
+
+
+def to_dev(a: Csr) -> d.SparseMatrix:
+    return d.SparseMatrix(a.rows, a.cols, a.offsets, a.col_indices, a.values)
+
+
+def bits(x):
+    return np.ascontiguousarray(x).view(np.uint64)
+
+
+def assert_bitwise(x, y):
+    x = np.asarray(x)
+    y = np.asarray(y)
+    assert x.shape == y.shape
+    diff = np.flatnonzero(bits(x.ravel(order="F")) != bits(y.ravel(order="F")))
+    assert diff.size == 0, f"{diff.size} entries differ, first at {diff[:5]}"
+
+
+def sin_theta(u_ref, u):
+    """sine of the largest principal angle between span(u_ref) and span(u)."""
+    q1, _ = np.linalg.qr(u_ref)
+    q2, _ = np.linalg.qr(u)
+    r = q2 - q1 @ (q1.T @ q2)
+    return float(np.linalg.norm(r, 2))
+
+
+@pytest.fixture(scope="module")
+def c1(oracle):
+    return oracle.sparse_random(10000, 5000, 25, 0, True)
+
+
+# ---- CSR transpose (bit-exact) ------------------------------------------------
+
+def test_transpose_bitwise_config1(dev, oracle, c1):
+    t_ref = oracle.transpose(c1)
+    t = d.transpose(to_dev(c1), device=dev)
+    assert np.array_equal(t.offsets, t_ref.offsets)
+    assert np.array_equal(t.col_indices, t_ref.col_indices)
+    assert_bitwise(t.values, t_ref.values)
+
+
+@pytest.mark.parametrize("shape", [(1, 1, 1), (7, 3, 2), (50, 80, 6), (300, 20, 9), (1, 500, 40)])
+def test_transpose_bitwise_shapes(dev, oracle, shape):
+    rows, cols, npr = shape
+    a = oracle.sparse_random(rows, cols, min(npr, cols), 11 + rows, False)
+    t_ref = oracle.transpose(a)
+    t = d.transpose(to_dev(a), device=dev)
+    assert np.array_equal(t.offsets, t_ref.offsets)
+    assert np.array_equal(t.col_indices, t_ref.col_indices)
+    assert_bitwise(t.values, t_ref.values)
+
+
+def test_transpose_empty_rows_and_zero_nnz(dev, oracle):
+    # rows with no entries and an all-empty matrix
+    off = np.array([0, 0, 2, 2, 3, 3], dtype=np.int64)
+    a = Csr(5, 4, off, np.array([1, 3, 0], dtype=np.int64), np.array([1.5, -2.0, 3.0]))
+    t_ref = oracle.transpose(a)
+    t = d.transpose(to_dev(a), device=dev)
+    assert np.array_equal(t.offsets, t_ref.offsets)
+    assert np.array_equal(t.col_indices, t_ref.col_indices)
+    assert_bitwise(t.values, t_ref.values)
+    z = Csr(3, 6, np.zeros(4, dtype=np.int64), np.zeros(0, dtype=np.int64), np.zeros(0))
+    tz = d.transpose(to_dev(z), device=dev)
+    assert np.array_equal(tz.offsets, np.zeros(7, dtype=np.int64)) and tz.nnz == 0
+
+
+def test_transpose_power_law_hub_columns(dev, oracle):
+    a = d.powerlaw(3000, 1500, 3.0, 1.0, 1.1, 5)
+    ca = Csr(a.rows, a.cols, a.offsets, a.col_indices, a.values)
+    t_ref = oracle.transpose(ca)
+    t = d.transpose(a, device=dev)
+    assert np.array_equal(t.offsets, t_ref.offsets)
+    assert np.array_equal(t.col_indices, t_ref.col_indices)
+    assert_bitwise(t.values, t_ref.values)
+
+
+def test_transpose_rejects_bad_index(dev):
+    a = d.SparseMatrix(2, 3, np.array([0, 1, 2]), np.array([0, 7]), np.array([1.0, 2.0]))
+    with pytest.raises(d.ShapeError):
+        d.transpose(a, device=dev)
+
+
+# ---- SpMM (bit-exact) -----------------------------------------------------------
+
+@pytest.mark.parametrize("l", [1, 3, 47, 48, 49, 64, 75, 97, 150, 300])
+def test_spmm_bitwise_widths(dev, oracle, c1, l):
+    rng = np.random.default_rng(l)
+    x = np.asfortranarray(rng.standard_normal((c1.cols, l)))
+    y_ref = oracle.spmm(c1, x)
+    y = d.spmm(to_dev(c1), x, device=dev)
+    assert_bitwise(y, y_ref)
+
+
+def test_spmm_transpose_pass_bitwise(dev, oracle, c1):
+    at = oracle.transpose(c1)
+    y = np.asfortranarray(np.random.default_rng(3).standard_normal((c1.rows, 75)))
+    assert_bitwise(d.spmm(to_dev(at), y, device=dev), oracle.spmm(at, y))
+
+
+@pytest.mark.parametrize("alpha", [0.0, 0.17816024588547713, -2.5])
+def test_spmm_shift_bitwise(dev, oracle, c1, alpha):
+    at = oracle.transpose(c1)
+    rng = np.random.default_rng(9)
+    y = np.asfortranarray(rng.standard_normal((c1.rows, 75)))
+    q = np.asfortranarray(rng.standard_normal((c1.cols, 75)))
+    t_ref = oracle.spmm(at, y)
+    if alpha != 0.0:
+        t_ref = oracle.add_scaled(t_ref, -alpha, q)
+    t = d.spmm_shift(to_dev(at), y, alpha, q, device=dev)
+    assert_bitwise(t, t_ref)
+
+
+def test_spmm_power_law_long_rows_bitwise(dev, oracle):
+    a = d.powerlaw(4000, 2000, 3.5, 1.0, 1.1, 8)
+    ca = Csr(a.rows, a.cols, a.offsets, a.col_indices, a.values)
+    at = transpose_np(ca)
+    x = np.asfortranarray(np.random.default_rng(1).standard_normal((ca.rows, 150)))
+    assert_bitwise(d.spmm(to_dev(at), x, device=dev), oracle.spmm(at, x))
+
+
+# ---- RNG ------------------------------------------------------------------------
+
+def test_splitmix_pins():
+    # test_dense_core.cpp:23-30
+    assert d.splitmix64_at(0, 0) == 0xe220a8397b1dcdaf
+    assert d.splitmix64_at(0, 1) == 0x6e789e6aa1b965f4
+    assert d.splitmix64_at(42, 0) == 0xbdd732262feb6e95
+    assert d.splitmix64_at(2026, 0) == 0xdb9c559891948d23
+    assert d.splitmix64_at(0x8000000000000000, 5) == 0x4d7e6a268a67c5ff
+
+
+def test_gaussian_pins(dev):
+    # normal_at pins (test_dense_core.cpp:36-41) through the device generator
+    g = d.gaussian_matrix(4, 1, 42, device=dev)
+    assert g[0, 0] == float.fromhex("0x1.a8ac4b546f505p-2")
+    assert g[1, 0] == float.fromhex("-0x1.c8a54f4e91a80p-1")
+    assert g[2, 0] == float.fromhex("0x1.bac69cd4142c4p+0")
+    assert g[3, 0] == float.fromhex("0x1.175b8fd2de8c7p-1")
+    assert d.gaussian_matrix(1, 1, 7, device=dev)[0, 0] == float.fromhex("0x1.5d70229cdee62p+0")
+    assert d.gaussian_matrix(1, 1, 2026, device=dev)[0, 0] == float.fromhex("-0x1.170735b18c9d6p-1")
+    # checksum pin (test_dense_core.cpp:59-61)
+    g = d.gaussian_matrix(8, 4, 2026, device=dev)
+    assert int(bits(g.ravel(order="F")).sum(dtype=np.uint64)) == 0x7bb02d1fc95596ff
+
+
+def test_gaussian_config1_sketch_agreement(dev, oracle):
+    g_ref = oracle.gaussian_matrix(10000, 75, 0)
+    g = d.gaussian_matrix(10000, 75, 0, device=dev)
+    mism = int(np.count_nonzero(bits(g.ravel(order="F")) != bits(g_ref.ravel(order="F"))))
+    # every entry within 2 ulp; the count of 1-ulp differences is reported
+    np.testing.assert_allclose(g, g_ref, rtol=5e-16, atol=0)
+    print(f"config-1 Omega: {mism} of {g.size} entries differ from glibc by <= 1 ulp")
+    assert int(bits(g_ref.ravel(order="F")).sum(dtype=np.uint64)) == 0xab4330ec8cf8afc5
+
+
+# ---- dense kernels -----------------------------------------------------------------
+
+@pytest.mark.parametrize("shape", [(10000, 75), (777, 150), (5000, 300), (40, 3)])
+def test_gram_matches_oracle(dev, oracle, shape):
+    c = np.asfortranarray(np.random.default_rng(shape[1]).standard_normal(shape))
+    g_ref = oracle.gram(c)
+    g = d.gram(c, device=dev)
+    assert np.array_equal(g, g.T)  # exactly symmetric
+    np.testing.assert_allclose(g, g_ref, rtol=1e-13, atol=1e-13 * np.abs(g_ref).max())
+
+
+@pytest.mark.parametrize("shape", [(300, 75, 75), (1000, 150, 100), (17, 5, 3)])
+def test_matmul_bitwise(dev, oracle, shape):
+    m, kk, n = shape
+    rng = np.random.default_rng(m)
+    a = np.asfortranarray(rng.standard_normal((m, kk)))
+    b = np.asfortranarray(rng.standard_normal((kk, n)))
+    assert_bitwise(d.matmul(a, b, device=dev), oracle.matmul(a, b))
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 20, 75, 150, 300])
+def test_sym_eig_matches_oracle(dev, oracle, n):
+    g0 = np.random.default_rng(n).standard_normal((n, n))
+    g = np.asfortranarray(g0 + g0.T)
+    w_ref, v_ref = oracle.sym_eig(g)
+    e = d.sym_eig(g, device=dev)
+    scale = np.abs(w_ref).max()
+    np.testing.assert_allclose(e.values, w_ref, rtol=0, atol=1e-12 * scale)
+    assert np.all(np.diff(e.values) >= 0)
+    np.testing.assert_allclose(e.vectors.T @ e.vectors, np.eye(n), atol=1e-12)
+    np.testing.assert_allclose(g @ e.vectors, e.vectors * e.values, atol=1e-11 * scale)
+
+
+def test_sym_eig_known_cases(dev):
+    # test_dense_core.cpp:88-104
+    e = d.sym_eig(np.array([[2.0, 0.0], [0.0, 5.0]]), device=dev)
+    assert e.values[0] == pytest.approx(2.0, rel=1e-14) and e.values[1] == pytest.approx(5.0, rel=1e-14)
+    e = d.sym_eig(np.array([[0.0, 1.0], [1.0, 0.0]]), device=dev)
+    assert e.values[0] == pytest.approx(-1.0, rel=1e-14) and e.values[1] == pytest.approx(1.0, rel=1e-14)
+    e = d.sym_eig(np.array([[4.0]]), device=dev)
+    assert e.values[0] == 4.0 and abs(e.vectors[0, 0]) == 1.0
+    with pytest.raises(d.ShapeError):
+        d.sym_eig(np.array([[1.0, 2.0], [1.0, 1.0]]), device=dev)
+
+
+def test_eig_svd_known_cases(dev):
+    # test_dense_core.cpp:134-154
+    f = d.eig_svd(np.array([[3.0, 0.0], [0.0, 4.0], [0.0, 0.0]]), device=dev)
+    np.testing.assert_allclose(f.s, [4.0, 3.0], rtol=1e-14)
+    np.testing.assert_allclose(f.v, [[0.0, 1.0], [1.0, 0.0]], atol=1e-14)
+    np.testing.assert_allclose(f.u, [[0.0, 1.0], [1.0, 0.0], [0.0, 0.0]], atol=1e-14)
+    f = d.eig_svd(np.array([[3.0, 0.0], [4.0, 5.0]]), device=dev)
+    np.testing.assert_allclose(f.s, [np.sqrt(45.0), np.sqrt(5.0)], rtol=1e-13)
+
+
+def test_eig_svd_rank_deficient(dev):
+    # test_dense_core.cpp:173-193
+    from oracle_lib import Oracle
+    c = Oracle().gaussian_matrix(6, 2, 1)
+    c[:, 1] = 0.0
+    with pytest.raises(d.RankDeficient) as ei:
+        d.eig_svd(c, device=dev)
+    assert ei.value.index == 1
+    with pytest.raises(d.RankDeficient) as ei:
+        d.eig_svd(np.zeros((5, 2)), device=dev)
+    assert ei.value.index == 0
+    with pytest.raises(d.ShapeError):
+        d.eig_svd(np.zeros((2, 3)), device=dev)
+
+
+@pytest.mark.parametrize("shape", [(10000, 75), (5000, 150), (2000, 300)])
+def test_eig_svd_matches_oracle(dev, oracle, shape):
+    c = np.asfortranarray(np.random.default_rng(shape[0]).standard_normal(shape))
+    u_ref, s_ref, v_ref = oracle.eig_svd(c)
+    f = d.eig_svd(c, device=dev)
+    np.testing.assert_allclose(f.s, s_ref, rtol=1e-12)
+    # same sign convention -> same vectors up to roundoff
+    np.testing.assert_allclose(f.v, v_ref, atol=1e-10)
+    np.testing.assert_allclose(f.u, u_ref, atol=1e-10)
+
+
+# ---- solver (tolerance parity, north_star bars) --------------------------------------
+
+def _pve_ratio(res, k):
+    s = res["s_hat"] if isinstance(res, dict) else np.array(res.trace.s_hat_history)
+    a = res["alphas"] if isinstance(res, dict) else np.array(res.trace.alphas)
+    n = len(a)
+    if n < 2:
+        return None
+    prev, cur = s[n - 2], s[n - 1]
+    ap = a[n - 1]  # alpha_stored after iteration n-1 == alpha used in iteration n
+    denom = cur[k] + a[n - 1]
+    return float(np.max(np.abs(prev[:k] + ap - cur[:k] - a[n - 1]) / denom))
+
+
+def check_solve(res, ref, k, sv_rtol=1e-8, angle=1e-6):
+    np.testing.assert_allclose(res.svd.s, ref["s"], rtol=sv_rtol)
+    assert sin_theta(ref["u"], res.svd.u) <= angle
+    assert sin_theta(ref["v"], res.svd.v) <= angle
+    assert res.trace.iterations == ref["iterations"]
+    assert res.trace.stop_reason.name == ref["stop_reason"]
+    np.testing.assert_allclose(res.trace.alphas, ref["alphas"], rtol=1e-8, atol=1e-300)
+    np.testing.assert_allclose(np.array(res.trace.s_hat_history), ref["s_hat"], rtol=1e-8)
+
+
+def test_solve_config1_shifted(dev, oracle, c1):
+    ref = oracle.solve(c1, 50, 25, p=10, alg="shifted", seed=0)
+    res = d.solve(to_dev(c1), d.SolverConfig(k=50, s=25, p=10, alg=d.Algorithm.shifted, seed=0),
+                  device=dev)
+    check_solve(res, ref, 50)
+    # the published probe values
+    assert res.svd.s[0] == pytest.approx(4.3734243453278507, rel=1e-12)
+    assert res.svd.s[49] == pytest.approx(0.73000858905607624, rel=1e-10)
+
+
+def test_solve_config1_dash(dev, oracle, c1):
+    ref = oracle.solve(c1, 50, 25, tol=1e-2, alg="dash", seed=0)
+    res = d.dash_svd(to_dev(c1), d.SolverConfig(k=50, s=25, tol=1e-2, seed=0), device=dev)
+    check_solve(res, ref, 50)
+    assert res.trace.iterations == 7
+    r_ref = _pve_ratio(ref, 50)
+    r = _pve_ratio(res, 50)
+    assert r == pytest.approx(r_ref, rel=1e-6)
+
+
+def test_solve_fixed_shift(dev, oracle):
+    a = oracle.sparse_random(50, 35, 6, 21, True)
+    ref = oracle.solve(a, 5, 3, p=4, alg="fixed_shift")
+    res = d.shifted_rsvd(to_dev(a), d.SolverConfig(k=5, s=3, p=4, alg=d.Algorithm.fixed_shift),
+                         device=dev)
+    check_solve(res, ref, 5)
+    assert res.trace.alphas[2] == res.trace.alphas[1] == res.trace.alphas[3]
+
+
+def test_solve_wide_orientation(dev, oracle):
+    wide = oracle.sparse_random(60, 100, 8, 44, True)
+    cfg = d.SolverConfig(k=8, s=4, seed=2)
+    ref = oracle.solve(wide, 8, 4, tol=1e-2, alg="dash", seed=2)
+    res = d.solve(to_dev(wide), cfg, device=dev)
+    assert res.svd.u.shape == (60, 8) and res.svd.v.shape == (100, 8)
+    check_solve(res, ref, 8)
+
+
+def test_solve_p0_and_tiny(dev, oracle):
+    a = oracle.sparse_random(40, 25, 6, 77, True)
+    ref = oracle.solve(a, 5, 5, p=0, alg="shifted")
+    res = d.solve(to_dev(a), d.SolverConfig(k=5, s=5, p=0, alg=d.Algorithm.shifted), device=dev)
+    check_solve(res, ref, 5)
+
+
+def test_solve_stop_reasons(dev, oracle):
+    a = oracle.sparse_random(60, 40, 6, 5, True)
+    r = d.dash_svd(to_dev(a), d.SolverConfig(k=5, s=3, tol=1e9), device=dev)
+    assert r.trace.iterations == 1 and r.trace.stop_reason == d.StopReason.tol_met
+    r = d.dash_svd(to_dev(a), d.SolverConfig(k=5, s=3, tol=1e-15, p_max=3), device=dev)
+    assert r.trace.iterations == 3 and r.trace.stop_reason == d.StopReason.p_max_reached
+
+
+def test_solve_dash_equals_shifted_at_stop(dev):
+    # test_rsvd.cpp:317-339: the accuracy-controlled run is bitwise the
+    # fixed-count run at the same iteration count (same device path)
+    from oracle_lib import Oracle
+    a = to_dev(Oracle().sparse_random(150, 90, 8, 6, True))
+    dr = d.dash_svd(a, d.SolverConfig(k=12, s=6, tol=1e-2, seed=17), device=dev)
+    assert dr.trace.stop_reason == d.StopReason.tol_met
+    fr = d.shifted_rsvd(a, d.SolverConfig(k=12, s=6, p=dr.trace.iterations, seed=17), device=dev)
+    assert_bitwise(dr.svd.u, fr.svd.u)
+    assert_bitwise(dr.svd.s, fr.svd.s)
+    assert_bitwise(dr.svd.v, fr.svd.v)
+    assert_bitwise(dr.trace.alphas, fr.trace.alphas)
+
+
+def test_solve_deterministic(dev, c1):
+    cfg = d.SolverConfig(k=50, s=25, p=4, alg=d.Algorithm.shifted)
+    r1 = d.solve(to_dev(c1), cfg, device=dev)
+    r2 = d.solve(to_dev(c1), cfg, device=dev)
+    assert_bitwise(r1.svd.u, r2.svd.u)
+    assert_bitwise(r1.svd.v, r2.svd.v)
+    assert_bitwise(r1.svd.s, r2.svd.s)
+
+
+def test_observer_and_snapshot_finalize(dev, oracle):
+    # test_rsvd.cpp:341-389 + :424-458 on the device path
+    a = oracle.sparse_random(60, 40, 6, 33, True)
+    seen = []
+    cfg = d.SolverConfig(k=6, s=3, p=5, alg=d.Algorithm.shifted)
+    full = d.shifted_rsvd(to_dev(a), cfg, observer=lambda st: seen.append(st), device=dev)
+    assert [s.iteration for s in seen] == [1, 2, 3, 4, 5]
+    for c, st in enumerate(seen):
+        assert st.alpha == full.trace.alphas[c]
+        assert_bitwise(st.s_hat, full.trace.s_hat_history[c])
+        assert st.q_after.shape == (40, 9)
+        np.testing.assert_allclose(st.q_after.T @ st.q_after, np.eye(9), atol=1e-9)
+        if c:
+            assert_bitwise(st.q_before, seen[c - 1].q_after)
+    short = d.shifted_rsvd(to_dev(a), d.SolverConfig(k=6, s=3, p=3, alg=d.Algorithm.shifted),
+                           device=dev)
+    fin = d.finalize_row_basis(to_dev(a), seen[2].q_after, 6, device=dev)
+    assert_bitwise(fin.u, short.svd.u)
+    assert_bitwise(fin.s, short.svd.s)
+    assert_bitwise(fin.v, short.svd.v)
+
+
+def test_config_errors(dev):
+    a = d.SparseMatrix(40, 30, np.arange(41) * 0, np.zeros(0), np.zeros(0))
+    with pytest.raises(d.ConfigError):
+        d.solve(a, d.SolverConfig(k=25, s=10, p=4, alg=d.Algorithm.shifted), device=dev)
+    with pytest.raises(d.ConfigError):
+        d.solve(a, d.SolverConfig(k=4, s=0), device=dev)
+    with pytest.raises(d.ConfigError):
+        d.solve(a, d.SolverConfig(k=4, s=2, alg=d.Algorithm.shifted), device=dev)
+
+
+def test_rank_one_raises_rank_deficient(dev):
+    # test_rsvd.cpp:152-175: a wider sketch than the rank hits the rank floor
+    u = np.array([[2 / 3], [-1 / 3], [2 / 3]])
+    v = np.array([[0.6], [0.8]])
+    dense = 6.0 * u @ v.T
+    rows, cols = np.nonzero(dense)
+    off = np.zeros(4, dtype=np.int64)
+    np.add.at(off, rows + 1, 1)
+    off = np.cumsum(off)
+    a = d.SparseMatrix(3, 2, off, cols, dense[rows, cols])
+    with pytest.raises(d.RankDeficient):
+        d.solve(a, d.SolverConfig(k=1, s=1, p=1, alg=d.Algorithm.shifted), device=dev)

@@ -1,0 +1,246 @@
+"""CPU: pin the oracle (oracle/dashsvd_oracle.c) before trusting it.
+
+1. Known-answer values from the reference's own tests
+   (proj/tests/test_dense_core.cpp, test_rsvd.cpp), restated here.
+2. Golden vectors produced by the unmodified reference (oracle/_ref) and
+   committed in tests/golden/reference_golden.npz (tests/golden/make_golden.py):
+   the oracle must reproduce them BIT FOR BIT.
+3. When oracle/_ref is present, oracle == reference on fresh random cases.
+"""
+import os
+
+import numpy as np
+import pytest
+
+from oracle_lib import Csr
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden", "reference_golden.npz")
+
+
+@pytest.fixture(scope="module")
+def gold():
+    return np.load(GOLD)
+
+
+def bitsum(x):
+    return np.uint64(np.ascontiguousarray(np.asarray(x).ravel(order="F")).view(np.uint64).sum(dtype=np.uint64))
+
+
+def same_bits(x, y):
+    x, y = np.asarray(x), np.asarray(y)
+    return x.shape == y.shape and np.array_equal(
+        np.ascontiguousarray(x.ravel(order="F")).view(np.uint64),
+        np.ascontiguousarray(y.ravel(order="F")).view(np.uint64))
+
+
+# ---- reference known answers ----------------------------------------------------
+
+def test_splitmix_pins(oracle):
+    # test_dense_core.cpp:20-31
+    assert oracle.splitmix64_at(0, 0) == 0xe220a8397b1dcdaf
+    assert oracle.splitmix64_at(0, 1) == 0x6e789e6aa1b965f4
+    assert oracle.splitmix64_at(42, 0) == 0xbdd732262feb6e95
+    assert oracle.splitmix64_at(42, 1) == 0x28efe333b266f103
+    assert oracle.splitmix64_at(2026, 0) == 0xdb9c559891948d23
+    assert oracle.splitmix64_at(0x8000000000000000, 5) == 0x4d7e6a268a67c5ff
+
+
+def test_normal_pins(oracle):
+    # test_dense_core.cpp:33-42
+    assert oracle.normal_at(42, 0) == float.fromhex("0x1.a8ac4b546f505p-2")
+    assert oracle.normal_at(42, 1) == float.fromhex("-0x1.c8a54f4e91a80p-1")
+    assert oracle.normal_at(42, 2) == float.fromhex("0x1.bac69cd4142c4p+0")
+    assert oracle.normal_at(42, 3) == float.fromhex("0x1.175b8fd2de8c7p-1")
+    assert oracle.normal_at(7, 0) == float.fromhex("0x1.5d70229cdee62p+0")
+    assert oracle.normal_at(2026, 0) == float.fromhex("-0x1.170735b18c9d6p-1")
+
+
+def test_gaussian_matrix_pins(oracle):
+    # test_dense_core.cpp:44-67
+    g = oracle.gaussian_matrix(8, 4, 2026)
+    assert g[0, 0] == oracle.normal_at(2026, 0)
+    assert g[3, 2] == oracle.normal_at(2026, 19)
+    assert bitsum(g) == np.uint64(0x7bb02d1fc95596ff)
+    assert not same_bits(oracle.gaussian_matrix(5, 3, 42), oracle.gaussian_matrix(5, 3, 43))
+
+
+def test_gaussian_moments(oracle):
+    # test_dense_core.cpp:69-86
+    g = oracle.gaussian_matrix(1000, 1000, 31337)
+    assert abs(g.mean()) < 0.01 and 0.99 < g.var(ddof=1) < 1.01
+
+
+def test_update_shift_kats(oracle):
+    # test_rsvd.cpp:33-53
+    assert oracle.update_shift(0.0, 0.5) == 0.25
+    assert oracle.update_shift(0.3, 0.2) == 0.3
+    assert oracle.update_shift(0.25, 0.35) == pytest.approx(0.30, rel=1e-15)
+    for i in range(200):
+        alpha, s_ll = 0.01 * i, 0.017 * ((i * 7919) % 200)
+        nxt = oracle.update_shift(alpha, s_ll)
+        assert nxt >= alpha
+        if s_ll > alpha:
+            assert alpha < nxt < s_ll
+        else:
+            assert nxt == alpha
+
+
+def test_pve_stop_kats(oracle):
+    # test_rsvd.cpp:55-84
+    from paper_2404_09276_b200 import ShapeError
+    assert not oracle.pve_stop_check([3.90, 1.00], 0.0, [4.00, 1.00], 0.05, 1, 0.01)
+    assert oracle.pve_stop_check([4.0, 1.0], 0.05, [4.0, 1.0], 0.05, 1, 1e-12)
+    assert oracle.pve_stop_check([4.0, 1.0], 0.0, [4.0, 1.0], 0.0, 1, 1e-300)
+    assert oracle.pve_stop_check([4.00, 1.00], 0.05, [4.005, 1.00], 0.05, 1, 0.01)
+    with pytest.raises(ShapeError):
+        oracle.pve_stop_check([4.0], 0.0, [4.0], 0.0, 1, 0.01)
+    with pytest.raises(ShapeError):
+        oracle.pve_stop_check([3.9, 1.0], 0.0, [4.0, 1.0], 0.0, 0, 0.01)
+    assert not oracle.pve_stop_check([2.0, 0.0], 0.0, [1.0, 0.0], 0.0, 1, 0.01)
+    assert not oracle.pve_stop_check([1.0, 0.0], 0.0, [1.0, 0.0], 0.0, 1, 0.01)
+
+
+def test_validate_config_kats(oracle):
+    # test_rsvd.cpp:86-133 (minus the qr orthonormalizer, which the oracle does not model)
+    from paper_2404_09276_b200 import ConfigError, ShapeError
+    bad = [dict(k=0, s=1, alg="dash"), dict(k=25, s=10, p=4, alg="shifted"),
+           dict(k=4, s=0, alg="dash"), dict(k=4, s=2, p=-1, alg="shifted"),
+           dict(k=4, s=2, p=-1, alg="fixed_shift"), dict(k=4, s=2, tol=0.0, alg="dash"),
+           dict(k=4, s=2, tol=-1.0, alg="dash"), dict(k=4, s=2, p_max=0, alg="dash")]
+    for kw in bad:
+        with pytest.raises(ConfigError):
+            oracle.validate_config(40, 30, **kw)
+    oracle.validate_config(40, 30, k=4, s=2, alg="dash")
+    with pytest.raises(ShapeError):
+        oracle.validate_config(0, 30, k=4, s=2, alg="dash")
+
+
+def test_sym_eig_kats(oracle):
+    # test_dense_core.cpp:88-132
+    w, v = oracle.sym_eig(np.array([[2.0, 0.0], [0.0, 5.0]]))
+    assert w[0] == pytest.approx(2.0, rel=1e-14) and w[1] == pytest.approx(5.0, rel=1e-14)
+    w, v = oracle.sym_eig(np.array([[0.0, 1.0], [1.0, 0.0]]))
+    assert w[0] == pytest.approx(-1.0, rel=1e-14) and w[1] == pytest.approx(1.0, rel=1e-14)
+    from paper_2404_09276_b200 import ShapeError
+    with pytest.raises(ShapeError):
+        oracle.sym_eig(np.array([[1.0, 2.0], [1.0, 1.0]]))
+
+
+def test_eig_svd_kats(oracle):
+    # test_dense_core.cpp:134-193
+    u, s, v = oracle.eig_svd(np.array([[3.0, 0.0], [0.0, 4.0], [0.0, 0.0]]))
+    np.testing.assert_allclose(s, [4.0, 3.0], rtol=1e-14)
+    np.testing.assert_allclose(v, [[0.0, 1.0], [1.0, 0.0]], atol=1e-14)
+    np.testing.assert_allclose(u, [[0.0, 1.0], [1.0, 0.0], [0.0, 0.0]], atol=1e-14)
+    u, s, v = oracle.eig_svd(np.array([[3.0, 0.0], [4.0, 5.0]]))
+    np.testing.assert_allclose(s, [np.sqrt(45.0), np.sqrt(5.0)], rtol=1e-13)
+    from paper_2404_09276_b200 import RankDeficient
+    c = oracle.gaussian_matrix(6, 2, 1)
+    c[:, 1] = 0.0
+    with pytest.raises(RankDeficient) as ei:
+        oracle.eig_svd(c)
+    assert ei.value.index == 1
+    with pytest.raises(RankDeficient) as ei:
+        oracle.eig_svd(np.zeros((5, 2)))
+    assert ei.value.index == 0
+
+
+def test_transpose_involution(oracle):
+    # test_sparse_core.cpp:263-293
+    a = oracle.sparse_random(70, 40, 5, 3, False)
+    tt = oracle.transpose(oracle.transpose(a))
+    assert np.array_equal(tt.offsets, a.offsets) and np.array_equal(tt.col_indices, a.col_indices)
+    assert same_bits(tt.values, a.values)
+
+
+def test_spmm_identity_expansion_exact(oracle):
+    # test_sparse_core.cpp:310-313: A * I reproduces A's dense form exactly
+    a = oracle.sparse_random(30, 20, 4, 9, True)
+    y = oracle.spmm(a, np.eye(20, order="F"))
+    dense = np.zeros((30, 20))
+    for i in range(30):
+        for p in range(a.offsets[i], a.offsets[i + 1]):
+            dense[i, a.col_indices[p]] = a.values[p]
+    assert same_bits(y, np.asfortranarray(dense))
+
+
+# ---- golden vectors from the unmodified reference -----------------------------------
+
+def test_golden_config1_inputs(oracle, gold):
+    a = oracle.sparse_random(10000, 5000, 25, 0, True)
+    assert a.nnz == int(gold["c1_nnz"]) == 249377
+    assert bitsum(a.offsets) == gold["c1_offsets_bitsum"]
+    assert bitsum(a.col_indices) == gold["c1_idx_bitsum"]
+    assert bitsum(a.values) == gold["c1_val_bitsum"]
+    at = oracle.transpose(a)
+    assert bitsum(at.offsets) == gold["c1t_offsets_bitsum"]
+    assert bitsum(at.col_indices) == gold["c1t_idx_bitsum"]
+    assert bitsum(at.values) == gold["c1t_val_bitsum"]
+    om = oracle.gaussian_matrix(10000, 75, 0)
+    assert bitsum(om) == gold["c1_omega_bitsum"] == np.uint64(0xab4330ec8cf8afc5)
+    t0 = oracle.spmm(at, om)
+    assert bitsum(t0) == gold["c1_at_omega_bitsum"]
+    assert same_bits(oracle.gram(t0), gold["c1_gram0"])
+
+
+def test_golden_config1_shifted_solve(oracle, gold):
+    a = oracle.sparse_random(10000, 5000, 25, 0, True)
+    r = oracle.solve(a, 50, 25, p=10, alg="shifted", seed=0)
+    assert same_bits(r["s"], gold["c1_shifted_s"])
+    assert same_bits(r["alphas"], gold["c1_shifted_alphas"])
+    assert same_bits(r["s_hat"], gold["c1_shifted_s_hat"])
+    assert bitsum(r["u"]) == gold["c1_shifted_u_bitsum"]
+    assert bitsum(r["v"]) == gold["c1_shifted_v_bitsum"]
+    # SURVEY 8c probe values
+    assert r["s"][0] == 4.3734243453278507 and r["alphas"][9] == 0.17816024588547713
+    assert bitsum(r["s"]) == np.uint64(0x7d5cf9e4d3614a86)
+
+
+def test_golden_config1_dash_solve(oracle, gold):
+    a = oracle.sparse_random(10000, 5000, 25, 0, True)
+    r = oracle.solve(a, 50, 25, tol=1e-2, alg="dash", seed=0)
+    assert r["iterations"] == int(gold["c1_dash_iterations"]) == 7
+    assert r["stop_reason"] == "tol_met"
+    assert same_bits(r["s"], gold["c1_dash_s"])
+    assert same_bits(r["alphas"], gold["c1_dash_alphas"])
+
+
+def test_golden_small_cases(oracle, gold):
+    b = Csr(150, 90, gold["b_off"], gold["b_idx"], gold["b_val"])
+    r = oracle.solve(b, 12, 6, tol=1e-2, alg="dash", seed=17)
+    assert r["iterations"] == int(gold["b_dash_iterations"])
+    for key in ("u", "s", "v", "alphas", "s_hat"):
+        assert same_bits(r[key], gold["b_dash_" + key]), key
+    w = Csr(60, 100, gold["w_off"], gold["w_idx"], gold["w_val"])
+    r = oracle.solve(w, 8, 4, tol=1e-2, alg="dash", seed=2)
+    for key in ("u", "s", "v", "alphas"):
+        assert same_bits(r[key], gold["w_dash_" + key]), key
+    r = oracle.solve(b, 12, 6, p=4, alg="fixed_shift", seed=3)
+    assert same_bits(r["s"], gold["b_fixed_s"]) and same_bits(r["alphas"], gold["b_fixed_alphas"])
+
+
+def test_golden_dense_kernels(oracle, gold):
+    c = gold["dense_c"]
+    assert same_bits(oracle.gaussian_matrix(200, 20, 808), c)
+    assert same_bits(oracle.gram(c), gold["dense_gram"])
+    u, s, v = oracle.eig_svd(c)
+    assert same_bits(u, gold["dense_eig_u"]) and same_bits(s, gold["dense_eig_s"])
+    assert same_bits(v, gold["dense_eig_v"])
+    w, vec = oracle.sym_eig(gold["sym_g"])
+    assert same_bits(w, gold["sym_w"]) and same_bits(vec, gold["sym_v"])
+    b = Csr(150, 90, gold["b_off"], gold["b_idx"], gold["b_val"])
+    assert same_bits(oracle.spmm(b, gold["spmm_x"]), gold["spmm_y"])
+
+
+# ---- oracle == reference on fresh cases (needs oracle/_ref) ------------------------
+
+@pytest.mark.parametrize("seed", [1, 2, 3])
+def test_oracle_equals_reference_random(oracle, reference, seed):
+    a = reference.sparse_random(120 + 17 * seed, 80, 7, seed, True)
+    assert same_bits(oracle.sparse_random(120 + 17 * seed, 80, 7, seed, True).values, a.values)
+    for alg, kw in (("dash", dict(tol=1e-2)), ("shifted", dict(p=3)), ("fixed_shift", dict(p=3))):
+        r1 = reference.solve(a, 9, 5, alg=alg, seed=seed, **kw)
+        r2 = oracle.solve(a, 9, 5, alg=alg, seed=seed, **kw)
+        for key in ("u", "s", "v", "alphas", "s_hat"):
+            assert same_bits(r1[key], r2[key]), (alg, key)
+        assert r1["iterations"] == r2["iterations"]
