@@ -55,12 +55,18 @@ jacobi_kernel(const double* __restrict__ g_in, int l, int lp, double* __restrict
     double* G = use_smem ? smem : gbuf;
     const int tid = threadIdx.x;
     const int half = lp / 2;
+    const int nblocks = half * (half + 1) / 2;
+    // (kp, kr) of every upper 2x2 block, decoded once (fixed across rounds)
+    uint16_t* blk = reinterpret_cast<uint16_t*>(use_smem ? smem + lp * lp : smem);
     for (int e = tid; e < lp * lp; e += blockDim.x) {
         const int i = e / lp, j = e % lp;
         G[e] = (i < l && j < l) ? g_in[i * l + j] : 0.0;
     }
+    for (int kp = tid; kp < half; kp += blockDim.x) {
+        const int base = kp * half - kp * (kp - 1) / 2;  // blocks before row kp
+        for (int kr = kp; kr < half; ++kr) blk[base + (kr - kp)] = static_cast<uint16_t>((kp << 8) | kr);
+    }
     __syncthreads();
-    const int nblocks = half * (half + 1) / 2;
     int sweep = 0;
     bool converged = false;
     for (; sweep < max_sweeps; ++sweep) {
@@ -92,13 +98,8 @@ jacobi_kernel(const double* __restrict__ g_in, int l, int lp, double* __restrict
             }
             __syncthreads();
             for (int e = tid; e < nblocks; e += blockDim.x) {
-                // decode (kp, kr), kp <= kr, row-major over the upper triangle
-                int kp = 0, rem = e;
-                while (rem >= half - kp) {
-                    rem -= half - kp;
-                    ++kp;
-                }
-                const int kr = kp + rem;
+                const int code = blk[e];
+                const int kp = code >> 8, kr = code & 0xff;
                 const double s1 = cs_s[kp], s2 = cs_s[kr];
                 const int p = pp[kp], q = qq[kp];
                 if (kp == kr) {
@@ -378,8 +379,11 @@ void eig_workspace_bind(EigWorkspace& w, int l, int max_sweeps, void* mem) {
 void jacobi_eig(const double* g, EigWorkspace& w, Control* ctrl, const int32_t* gate,
                 cudaStream_t stream) {
     if (w.lp > 2 * kMaxPairs) fail(DSVD_UNSUPPORTED, "eigensolver: l > 512 is not supported");
-    const size_t smem = sizeof(double) * w.lp * w.lp;
-    const int use_smem = smem <= static_cast<size_t>(kSmemLimit) - 16 * 1024;
+    const size_t half = w.lp / 2;
+    const size_t table = sizeof(uint16_t) * half * (half + 1) / 2;
+    const size_t gbytes = sizeof(double) * w.lp * w.lp;
+    const int use_smem = gbytes + table <= static_cast<size_t>(kSmemLimit) - 16 * 1024;
+    const size_t smem = (use_smem ? gbytes : 0) + table;
     DSVD_CUDA_CHECK(cudaFuncSetAttribute(jacobi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          kSmemLimit - 16 * 1024));
     jacobi_kernel<<<1, kEigThreads, use_smem ? smem : 0, stream>>>(

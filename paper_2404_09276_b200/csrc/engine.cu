@@ -130,10 +130,21 @@ void build_pair(dsvd_ctx* ctx, CsrAlloc& al, int64_t rows, int64_t cols, int64_t
     void* scratch = ctx->buf("csc.scratch", scratch_bytes);
     build_transpose(a, at, scratch, scratch_bytes, st);
     count_launch(nnz > 0 ? 8 : 1);  // 4 own kernels + CUB radix sort passes (estimate)
+    int32_t* hubs = static_cast<int32_t*>(al.get("hub_counts", sizeof(int32_t) * 2));
+    a.hub_threshold = at.hub_threshold = ctx->hub_threshold;
+    a.d_hub_rows = hubs;
+    at.d_hub_rows = hubs + 1;
     build_row_order(a, scratch, scratch_bytes, st);
-    count_launch(rows > 0 ? 3 : 0);
+    count_launch(rows > 0 ? 4 : 0);
     build_row_order(at, scratch, scratch_bytes, st);
-    count_launch(cols > 0 ? 3 : 0);
+    count_launch(cols > 0 ? 4 : 0);
+    int32_t hh[2] = {0, 0};
+    if (rows > 0 && cols > 0) {
+        DSVD_CUDA_CHECK(cudaMemcpyAsync(hh, hubs, sizeof(hh), cudaMemcpyDeviceToHost, st));
+        DSVD_CUDA_CHECK(cudaStreamSynchronize(st));
+    }
+    a.hub_rows = rows > 0 ? hh[0] : 0;
+    at.hub_rows = cols > 0 ? hh[1] : 0;
 }
 
 void upload_pair(dsvd_ctx* ctx, CsrAlloc& al, int64_t rows, int64_t cols, int64_t nnz,
@@ -297,7 +308,7 @@ void solve_tall(dsvd_ctx* ctx, const DevCsr& A, const DevCsr& AT, const dsvd_con
 
     // Q = eigSVD(A^T Omega).u
     sp = ctx->span_begin(K_SPMM2);
-    spmm(SpmmArgs{&AT, Y, T, ld, l, nullptr, nullptr, nullptr}, st, ctx->spmm_variant);
+    spmm(SpmmArgs{&AT, Y, T, ld, l, nullptr, nullptr, nullptr}, st, ctx->spmm_variant, ctx->side, ctx->fork, ctx->join);
     count_launch();
     ctx->span_end(sp);
     if (sharded) {
@@ -335,14 +346,14 @@ void solve_tall(dsvd_ctx* ctx, const DevCsr& A, const DevCsr& AT, const dsvd_con
         count_launch();
         // Y = A Q
         sp = ctx->span_begin(K_SPMM1);
-        spmm(SpmmArgs{&A, Qb[cur], Y, ld, l, nullptr, nullptr, gate}, st, ctx->spmm_variant);
+        spmm(SpmmArgs{&A, Qb[cur], Y, ld, l, nullptr, nullptr, gate}, st, ctx->spmm_variant, ctx->side, ctx->fork, ctx->join);
         count_launch();
         ctx->span_end(sp);
         // T = A^T Y - alpha Q  (add_scaled skipped when alpha == 0)
         sp = ctx->span_begin(K_SPMM2);
         spmm(SpmmArgs{&AT, Y, T, ld, l, sharded ? nullptr : Qb[cur], sharded ? nullptr : &ctrl->alpha,
                       gate},
-             st, ctx->spmm_variant);
+             st, ctx->spmm_variant, ctx->side, ctx->fork, ctx->join);
         count_launch();
         ctx->span_end(sp);
         if (sharded) {
@@ -396,7 +407,7 @@ void solve_tall(dsvd_ctx* ctx, const DevCsr& A, const DevCsr& AT, const dsvd_con
     control_init(ctrl, s_stored, static_cast<int>(l), st);
     count_launch();
     sp = ctx->span_begin(K_SPMM1);
-    spmm(SpmmArgs{&A, Qf, Y, ld, l, nullptr, nullptr, nullptr}, st, ctx->spmm_variant);
+    spmm(SpmmArgs{&A, Qf, Y, ld, l, nullptr, nullptr, nullptr}, st, ctx->spmm_variant, ctx->side, ctx->fork, ctx->join);
     count_launch();
     ctx->span_end(sp);
     eig_svd_factors(ctx, Y, m, l, ld, eo, ctrl, nullptr, nullptr, sharded, global_m);
@@ -568,6 +579,9 @@ int dsvd_ctx_create(int device, dsvd_ctx** out) {
         c->device = device;
         DSVD_CUDA_CHECK(cudaSetDevice(device));
         DSVD_CUDA_CHECK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+        DSVD_CUDA_CHECK(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
+        DSVD_CUDA_CHECK(cudaEventCreateWithFlags(&c->fork, cudaEventDisableTiming));
+        DSVD_CUDA_CHECK(cudaEventCreateWithFlags(&c->join, cudaEventDisableTiming));
         *out = c.release();
     });
 }
@@ -586,6 +600,9 @@ int dsvd_ctx_destroy(dsvd_ctx* ctx) {
         }
         if (ctx->host_flags) cudaFreeHost(ctx->host_flags);
         comm_release(ctx);
+        cudaStreamDestroy(ctx->side);
+        cudaEventDestroy(ctx->fork);
+        cudaEventDestroy(ctx->join);
         cudaStreamDestroy(ctx->stream);
         delete ctx;
     });
@@ -611,6 +628,8 @@ int dsvd_ctx_set_option(dsvd_ctx* ctx, const char* name, int64_t value) {
         const std::string n = name ? name : "";
         if (n == "spmm_variant") {
             ctx->spmm_variant = static_cast<int>(value);
+        } else if (n == "hub_threshold") {
+            ctx->hub_threshold = value;
         } else {
             fail(DSVD_CONFIG, "unknown option '" + n + "'");
         }
@@ -836,7 +855,7 @@ int dsvd_finalize_row_basis(dsvd_ctx* ctx, const dsvd_matrix* a, const double* q
         DSVD_CUDA_CHECK(cudaMemcpyAsync(qh, q, sizeof(double) * n * l, cudaMemcpyHostToDevice, st));
         colmajor_to_rowmajor(qh, n, l, Q, ld, st);
         control_init(ctrl, s_stored, static_cast<int>(l), st);
-        spmm(SpmmArgs{&A, Q, B, ld, l, nullptr, nullptr, nullptr}, st, ctx->spmm_variant);
+        spmm(SpmmArgs{&A, Q, B, ld, l, nullptr, nullptr, nullptr}, st, ctx->spmm_variant, ctx->side, ctx->fork, ctx->join);
         EigSvdOut eo{W, sv, inv_s};
         eig_svd_factors(ctx, B, m, l, ld, eo, ctrl, nullptr, nullptr);
         raise_device_status(read_control(ctx, ctrl));
@@ -915,7 +934,7 @@ int dsvd_spmm_shift(dsvd_ctx* ctx, int64_t rows, int64_t cols, int64_t nnz, cons
             colmajor_to_rowmajor(qc, rows, l, Qd, ld, st);
             DSVD_CUDA_CHECK(cudaMemcpyAsync(d_alpha, &alpha, sizeof(double), cudaMemcpyHostToDevice, st));
         }
-        spmm(SpmmArgs{&a, X, Yd, ld, l, Qd, Qd ? d_alpha : nullptr, nullptr}, st, ctx->spmm_variant);
+        spmm(SpmmArgs{&a, X, Yd, ld, l, Qd, Qd ? d_alpha : nullptr, nullptr}, st, ctx->spmm_variant, ctx->side, ctx->fork, ctx->join);
         rowmajor_to_colmajor(Yd, rows, l, ld, xc, st);
         DSVD_CUDA_CHECK(cudaMemcpyAsync(y, xc, sizeof(double) * rows * l, cudaMemcpyDeviceToHost, st));
         DSVD_CUDA_CHECK(cudaStreamSynchronize(st));

@@ -45,6 +45,9 @@ struct dsvd_ctx {
     size_t event_next = 0;
     std::vector<dsvd::TimedSpan> spans;
     int spmm_variant = 0;
+    int64_t hub_threshold = 4096;   // rows with >= this many nonzeros take the hub SpMM path
+    cudaStream_t side = nullptr;    // second stream: hub-row SpMM runs beside the bulk kernel
+    cudaEvent_t fork = nullptr, join = nullptr;
     int32_t* host_flags = nullptr;  // pinned ring for stop flags
     cudaEvent_t timer[2] = {nullptr, nullptr};
     // multi-GPU state (comm.cu): NCCL communicator when nranks > 1

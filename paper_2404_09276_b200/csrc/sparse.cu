@@ -31,15 +31,15 @@ template <bool kShift>
 __global__ void __launch_bounds__(256)
 spmm_rowslab_kernel(const int64_t* __restrict__ off, const int32_t* __restrict__ idx,
                     const double* __restrict__ val, const int32_t* __restrict__ order,
-                    int64_t rows, int nslab, const double* __restrict__ x,
+                    int64_t row_start, int64_t rows, int nslab, const double* __restrict__ x,
                     double* __restrict__ y, int64_t ld, const double* __restrict__ q,
                     const double* __restrict__ alpha_p, const int32_t* __restrict__ gate) {
     if (gate != nullptr && *gate != 0) return;
     const int lane = threadIdx.x & 31;
     const int64_t item = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    if (item >= rows * nslab) return;
-    const int64_t rpos = item / nslab;
-    const int slab = static_cast<int>(item - rpos * nslab);
+    if (item >= (rows - row_start) * nslab) return;
+    const int64_t rpos = row_start + item / nslab;
+    const int slab = static_cast<int>(item % nslab);
     const int64_t row = order != nullptr ? static_cast<int64_t>(order[rpos]) : rpos;
     const int64_t col = static_cast<int64_t>(slab) * kSlab + 2 * lane;
     const bool active = col < ld;  // ld is a multiple of 4, so col+1 < ld as well
@@ -88,6 +88,123 @@ spmm_rowslab_kernel(const int64_t* __restrict__ off, const int32_t* __restrict__
         }
     }
     *reinterpret_cast<double2*>(y + row * ld + col) = make_double2(a0, a1);
+}
+
+
+// ---- hub rows ------------------------------------------------------------------
+// One warp per (hub row, 32-column slab); one lane per column, so each lane
+// runs its column's FMA chain over the row in CSR order (bitwise as above).
+// Gathered X values and the (index, value) stream move through a per-warp
+// shared-memory ring with cp.async: kHubNB batches of 32 nonzeros are in
+// flight while the chain consumes the oldest, so a 200k-nonzero row runs at
+// the FMA-latency bound instead of one L2/DRAM round trip per few nonzeros.
+constexpr int kHubNB = 4;                 // gather batches in flight (ring depth)
+constexpr int kHubWarps = 2;              // warps per block
+constexpr int kHubWarpDoubles = kHubNB * 32 * 32 + 2 * kHubNB * 32;  // gathers + values
+constexpr int kHubWarpInts = 2 * kHubNB * 32;                        // indices
+constexpr size_t kHubSmem =
+    kHubWarps * (sizeof(double) * kHubWarpDoubles + sizeof(int32_t) * kHubWarpInts);
+
+__device__ __forceinline__ void cp_async8(void* smem_dst, const void* gsrc) {
+    const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(smem_dst));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(gsrc));
+}
+__device__ __forceinline__ void cp_async4(void* smem_dst, const void* gsrc) {
+    const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(smem_dst));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(d), "l"(gsrc));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+template <bool kShift>
+__global__ void __launch_bounds__(32 * kHubWarps)
+spmm_hub_kernel(const int64_t* __restrict__ off, const int32_t* __restrict__ idx,
+                const double* __restrict__ val, const int32_t* __restrict__ order,
+                const int32_t* __restrict__ n_hub_p, int nslab, const double* __restrict__ x,
+                double* __restrict__ y, int64_t ld, const double* __restrict__ q,
+                const double* __restrict__ alpha_p, const int32_t* __restrict__ gate) {
+    if (gate != nullptr && *gate != 0) return;
+    extern __shared__ double hub_smem[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t item = static_cast<int64_t>(blockIdx.x) * kHubWarps + warp;
+    if (item >= static_cast<int64_t>(*n_hub_p) * nslab) return;
+    const int64_t row = order[item / nslab];
+    const int64_t col = static_cast<int64_t>(item % nslab) * 32 + lane;
+    const bool active = col < ld;
+    double* ring = hub_smem + warp * kHubWarpDoubles;        // [NB][32 nnz][32 lanes]
+    double* vring = ring + kHubNB * 32 * 32;                  // [2NB][32]
+    int32_t* iring = reinterpret_cast<int32_t*>(hub_smem + kHubWarps * kHubWarpDoubles) +
+                     warp * kHubWarpInts;                     // [2NB][32]
+    const int64_t beg = off[row], end = off[row + 1];
+    const int64_t nb = (end - beg + 31) / 32;
+    const double* xc = x + (active ? col : 0);
+
+    // (index, value) batch b -> slot b % 2NB
+    auto fetch_iv = [&](int64_t b) {
+        const int64_t p = beg + b * 32 + lane;
+        if (b < nb && p < end) {
+            cp_async4(iring + (b % (2 * kHubNB)) * 32 + lane, idx + p);
+            cp_async8(vring + (b % (2 * kHubNB)) * 32 + lane, val + p);
+        }
+    };
+    // gathers of batch b -> ring slot b % NB (indices must already be in smem)
+    auto gather = [&](int64_t b) {
+        if (b >= nb || !active) return;
+        const int cnt = static_cast<int>(min(static_cast<int64_t>(32), end - beg - b * 32));
+        const int32_t* ib = iring + (b % (2 * kHubNB)) * 32;
+        double* slot = ring + (b % kHubNB) * 1024;
+        for (int j = 0; j < cnt; ++j) cp_async8(slot + j * 32 + lane, xc + static_cast<int64_t>(ib[j]) * ld);
+    };
+
+    // prologue: indices of batches 0..NB-1 first (one group), then gathers 0..NB-2
+    for (int b = 0; b < kHubNB; ++b) fetch_iv(b);
+    cp_async_commit();
+    cp_async_wait<0>();
+    __syncwarp();
+    for (int b = 0; b < kHubNB - 1; ++b) {
+        gather(b);
+        fetch_iv(b + kHubNB);
+        cp_async_commit();
+    }
+    double acc = 0.0;
+    for (int64_t b = 0; b < nb; ++b) {
+        gather(b + kHubNB - 1);      // its indices arrived with an older group
+        fetch_iv(b + 2 * kHubNB - 1);
+        cp_async_commit();
+        cp_async_wait<kHubNB - 1>();  // batch b (gathers and values) has landed
+        __syncwarp();
+        const double* slot = ring + (b % kHubNB) * 1024;
+        const double* vb = vring + (b % (2 * kHubNB)) * 32;
+        const int cnt = static_cast<int>(min(static_cast<int64_t>(32), end - beg - b * 32));
+        if (cnt == 32) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) acc = fma(vb[j], slot[j * 32 + lane], acc);
+        } else {
+            for (int j = 0; j < cnt; ++j) acc = fma(vb[j], slot[j * 32 + lane], acc);
+        }
+        __syncwarp();
+    }
+    cp_async_wait<0>();
+    if (!active) return;
+    if (kShift) {
+        const double alpha = *alpha_p;
+        if (alpha != 0.0) acc = fma(-alpha, q[row * ld + col], acc);
+    }
+    y[row * ld + col] = acc;
+}
+
+__global__ void count_ge_kernel(const int32_t* __restrict__ sorted_desc, int64_t n, int64_t t,
+                                int32_t* out) {
+    // number of leading entries >= t in a descending array (binary search)
+    int64_t lo = 0, hi = n;
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) / 2;
+        if (sorted_desc[mid] >= t) lo = mid + 1; else hi = mid;
+    }
+    *out = static_cast<int32_t>(lo);
 }
 
 __global__ void narrow_kernel(const int64_t* __restrict__ src, int32_t* __restrict__ dst,
@@ -192,22 +309,52 @@ size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 
 }  // namespace
 
-void spmm(const SpmmArgs& s, cudaStream_t stream, int variant) {
+void spmm(const SpmmArgs& s, cudaStream_t stream, int variant, cudaStream_t side,
+          cudaEvent_t fork, cudaEvent_t join) {
     (void)variant;
     const DevCsr& a = *s.a;
     if (a.rows == 0) return;
-    const int nslab = static_cast<int>(ceil_div(s.ld, kSlab));
-    const int64_t items = a.rows * nslab;
-    const int warps_per_block = 8;
-    const int64_t blocks = ceil_div(items, warps_per_block);
-    if (s.q != nullptr) {
-        spmm_rowslab_kernel<true><<<static_cast<unsigned>(blocks), 32 * warps_per_block, 0, stream>>>(
-            a.off, a.idx, a.val, a.order, a.rows, nslab, s.x, s.y, s.ld, s.q, s.alpha, s.gate);
-    } else {
-        spmm_rowslab_kernel<false><<<static_cast<unsigned>(blocks), 32 * warps_per_block, 0, stream>>>(
-            a.off, a.idx, a.val, a.order, a.rows, nslab, s.x, s.y, s.ld, nullptr, nullptr, s.gate);
+    const int64_t hub = (side != nullptr && a.d_hub_rows != nullptr) ? a.hub_rows : 0;
+    if (hub > 0) {
+        static bool attr = false;
+        if (!attr) {
+            DSVD_CUDA_CHECK(cudaFuncSetAttribute(spmm_hub_kernel<true>,
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, kHubSmem));
+            DSVD_CUDA_CHECK(cudaFuncSetAttribute(spmm_hub_kernel<false>,
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, kHubSmem));
+            attr = true;
+        }
+        DSVD_CUDA_CHECK(cudaEventRecord(fork, stream));
+        DSVD_CUDA_CHECK(cudaStreamWaitEvent(side, fork, 0));
+        const int nslab32 = static_cast<int>(ceil_div(s.ld, 32));
+        const unsigned blocks = static_cast<unsigned>(ceil_div(hub * nslab32, kHubWarps));
+        if (s.q != nullptr)
+            spmm_hub_kernel<true><<<blocks, 32 * kHubWarps, kHubSmem, side>>>(
+                a.off, a.idx, a.val, a.order, a.d_hub_rows, nslab32, s.x, s.y, s.ld, s.q, s.alpha, s.gate);
+        else
+            spmm_hub_kernel<false><<<blocks, 32 * kHubWarps, kHubSmem, side>>>(
+                a.off, a.idx, a.val, a.order, a.d_hub_rows, nslab32, s.x, s.y, s.ld, nullptr, nullptr,
+                s.gate);
+        DSVD_LAUNCH_CHECK();
     }
-    DSVD_LAUNCH_CHECK();
+    const int nslab = static_cast<int>(ceil_div(s.ld, kSlab));
+    const int64_t items = (a.rows - hub) * nslab;
+    if (items > 0) {
+        const int warps_per_block = 8;
+        const int64_t blocks = ceil_div(items, warps_per_block);
+        if (s.q != nullptr) {
+            spmm_rowslab_kernel<true><<<static_cast<unsigned>(blocks), 32 * warps_per_block, 0, stream>>>(
+                a.off, a.idx, a.val, a.order, hub, a.rows, nslab, s.x, s.y, s.ld, s.q, s.alpha, s.gate);
+        } else {
+            spmm_rowslab_kernel<false><<<static_cast<unsigned>(blocks), 32 * warps_per_block, 0, stream>>>(
+                a.off, a.idx, a.val, a.order, hub, a.rows, nslab, s.x, s.y, s.ld, nullptr, nullptr, s.gate);
+        }
+        DSVD_LAUNCH_CHECK();
+    }
+    if (hub > 0) {
+        DSVD_CUDA_CHECK(cudaEventRecord(join, side));
+        DSVD_CUDA_CHECK(cudaStreamWaitEvent(stream, join, 0));
+    }
 }
 
 void narrow_indices(const int64_t* src, int32_t* dst, int64_t nnz, int64_t cols, int32_t* bad,
@@ -298,6 +445,12 @@ void build_row_order(DevCsr& m, void* scratch, size_t scratch_bytes, cudaStream_
     DSVD_LAUNCH_CHECK();
     DSVD_CUDA_CHECK(cub::DeviceRadixSort::SortPairsDescending(temp, temp_bytes, len, len_sorted,
                                                               ids, m.order, m.rows, 0, 32, stream));
+    if (m.d_hub_rows != nullptr) {
+        count_ge_kernel<<<1, 1, 0, stream>>>(len_sorted, m.rows,
+                                             m.hub_threshold > 0 ? m.hub_threshold : (int64_t(1) << 40),
+                                             m.d_hub_rows);
+        DSVD_LAUNCH_CHECK();
+    }
 }
 
 }  // namespace dsvd

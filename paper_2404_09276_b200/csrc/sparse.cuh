@@ -16,6 +16,11 @@ struct DevCsr {
     double* val = nullptr;
     int32_t* order = nullptr;
     int64_t max_row_nnz = 0;
+    // rows order[0 .. hub_rows) hold >= hub_threshold nonzeros and take the
+    // deep-pipelined hub path of spmm (counted on the device at build time)
+    int64_t hub_rows = 0;
+    int64_t hub_threshold = 0;
+    int32_t* d_hub_rows = nullptr;  // device copy written by build_row_order
 };
 
 // SpMM launch description. X and Y (and Q) are row-major with row stride ld.
@@ -30,14 +35,18 @@ struct SpmmArgs {
     const int32_t* gate;  // device flag: skip the launch's work when *gate != 0 (or nullptr)
 };
 
-void spmm(const SpmmArgs& args, cudaStream_t stream, int variant);
+// Launches the hub-row kernel on `side` (when the matrix has hub rows) and the
+// kernel for all other rows on `stream`; `fork`/`join` order the two streams.
+void spmm(const SpmmArgs& args, cudaStream_t stream, int variant, cudaStream_t side = nullptr,
+          cudaEvent_t fork = nullptr, cudaEvent_t join = nullptr);
 
 // CSR(A^T) from CSR(A), bitwise equal to the reference transpose().
 // Temporaries come from `scratch` (bytes given by csc_scratch_bytes).
 size_t csc_scratch_bytes(int64_t rows, int64_t cols, int64_t nnz);
 void build_transpose(const DevCsr& a, DevCsr& at, void* scratch, size_t scratch_bytes,
                      cudaStream_t stream);
-// Row order by nonzero count (descending, ties by row index) into m.order.
+// Row order by nonzero count (descending, ties by row index) into m.order,
+// and the number of rows with >= m.hub_threshold nonzeros into *m.d_hub_rows.
 size_t order_scratch_bytes(int64_t rows);
 void build_row_order(DevCsr& m, void* scratch, size_t scratch_bytes, cudaStream_t stream);
 
