@@ -386,7 +386,7 @@ void jacobi_eig(const double* g, EigWorkspace& w, Control* ctrl, const int32_t* 
     const size_t smem = (use_smem ? gbytes : 0) + table;
     DSVD_CUDA_CHECK(cudaFuncSetAttribute(jacobi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          kSmemLimit - 16 * 1024));
-    jacobi_kernel<<<1, kEigThreads, use_smem ? smem : 0, stream>>>(
+    jacobi_kernel<<<1, kEigThreads, smem, stream>>>(
         g, w.l, w.lp, w.gbuf, use_smem, w.rot_log, w.max_sweeps, w.lam, ctrl, gate);
     DSVD_LAUNCH_CHECK();
     const int warps = 8;
