@@ -214,10 +214,12 @@ constexpr int kTmaW = 64;
 constexpr int kTmaStageNnz = 32;
 constexpr int kTmaStages = 6;
 constexpr int kTmaConsumers = kTmaW / 32;
+constexpr int kTmaPf = 4;                           // index/value prefetch distance (stages)
+constexpr int kTmaRing = kTmaStages + kTmaPf;       // index/value ring slots
 constexpr int kTmaThreads = 32 * (1 + kTmaConsumers);
 constexpr size_t kTmaStageBytes = sizeof(double) * kTmaStageNnz * kTmaW;
 constexpr size_t kTmaSmem = 1024 + kTmaStages * kTmaStageBytes +
-                            kTmaStages * kTmaStageNnz * sizeof(double) +
+                            kTmaRing * kTmaStageNnz * (sizeof(double) + sizeof(int32_t)) +
                             2 * kTmaStages * sizeof(uint64_t);
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
@@ -267,9 +269,10 @@ spmm_hub_tma_kernel(const __grid_constant__ CUtensorMap xmap, const int64_t* __r
     unsigned char* base = reinterpret_cast<unsigned char*>(
         (reinterpret_cast<uintptr_t>(tma_raw) + 1023) & ~uintptr_t(1023));
     double* data = reinterpret_cast<double*>(base);                        // [S][32][64]
-    double* vals = data + kTmaStages * kTmaStageNnz * kTmaW;                // [S][32]
-    uint64_t* full = reinterpret_cast<uint64_t*>(vals + kTmaStages * kTmaStageNnz);
+    double* vring = data + kTmaStages * kTmaStageNnz * kTmaW;               // [R][32]
+    uint64_t* full = reinterpret_cast<uint64_t*>(vring + kTmaRing * kTmaStageNnz);
     uint64_t* empty = full + kTmaStages;
+    int32_t* iring = reinterpret_cast<int32_t*>(empty + kTmaStages);       // [R][32]
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t items = static_cast<int64_t>(*n_hub_p) * nslab;
     if (threadIdx.x == 0) {
@@ -281,38 +284,86 @@ spmm_hub_tma_kernel(const __grid_constant__ CUtensorMap xmap, const int64_t* __r
         asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
     }
     __syncthreads();
-    int stage = 0;
-    unsigned phase = 0;
     if (warp == 0) {
-        for (int64_t item = blockIdx.x; item < items; item += gridDim.x) {
-            const int64_t row = order[item / nslab];
-            const int col0 = static_cast<int>(item % nslab) * kTmaW;
-            const int64_t beg = off[row], end = off[row + 1];
-            for (int64_t p0 = beg; p0 < end; p0 += kTmaStageNnz) {
-                const int cnt = static_cast<int>(end - p0 < kTmaStageNnz ? end - p0 : kTmaStageNnz);
-                mbar_wait(&empty[stage], phase ^ 1);
-                const int src = lane < cnt ? lane : cnt - 1;  // pad the last gather4 group
-                const int c = __ldg(idx + p0 + src);
-                vals[stage * kTmaStageNnz + lane] = lane < cnt ? __ldg(val + p0 + lane) : 0.0;
-                const int ngather = (cnt + 3) / 4;
-                __syncwarp();
-                if (lane == 0)
-                    mbar_expect_tx(&full[stage], static_cast<unsigned>(ngather * 4 * kTmaW * sizeof(double)));
-                __syncwarp();
-                const int g = lane & 7;
-                const int r0 = __shfl_sync(kFull, c, 4 * g), r1 = __shfl_sync(kFull, c, 4 * g + 1);
-                const int r2 = __shfl_sync(kFull, c, 4 * g + 2), r3 = __shfl_sync(kFull, c, 4 * g + 3);
-                if (lane < ngather)
-                    tma_gather4(data + (static_cast<size_t>(stage) * kTmaStageNnz + 4 * lane) * kTmaW,
-                                &xmap, col0, r0, r1, r2, r3, &full[stage]);
-                if (++stage == kTmaStages) {
-                    stage = 0;
-                    phase ^= 1;
+        // Producer. Two cursors walk the same flat stage sequence: `pf` fetches
+        // the (index, value) pairs kTmaPf stages ahead with cp.async, `is`
+        // turns landed indices into TMA gathers.
+        struct Cursor {
+            int64_t item, beg, end, p0;
+            int col0;
+            bool valid;
+        };
+        auto seek = [&](Cursor& c) {
+            c.valid = false;
+            while (c.item < items) {
+                const int64_t row = order[c.item / nslab];
+                c.beg = off[row];
+                c.end = off[row + 1];
+                c.col0 = static_cast<int>(c.item % nslab) * kTmaW;
+                if (c.end > c.beg) {
+                    c.p0 = c.beg;
+                    c.valid = true;
+                    return;
                 }
+                c.item += gridDim.x;
             }
+        };
+        auto advance = [&](Cursor& c) {
+            c.p0 += kTmaStageNnz;
+            if (c.p0 >= c.end) {
+                c.item += gridDim.x;
+                seek(c);
+            }
+        };
+        auto fetch = [&](const Cursor& c, int64_t fs) {
+            const int64_t n = c.end - c.p0;
+            if (lane < n && lane < kTmaStageNnz) {
+                const int r = static_cast<int>(fs % kTmaRing) * kTmaStageNnz + lane;
+                cp_async4(iring + r, idx + c.p0 + lane);
+                cp_async8(vring + r, val + c.p0 + lane);
+            }
+        };
+        Cursor pf{blockIdx.x, 0, 0, 0, 0, false};
+        seek(pf);
+        Cursor is = pf;
+        int64_t fs_pf = 0, fs = 0;
+        for (int k = 0; k < kTmaPf; ++k) {
+            if (pf.valid) {
+                fetch(pf, fs_pf++);
+                advance(pf);
+            }
+            cp_async_commit();
         }
+        while (is.valid) {
+            if (pf.valid) {
+                fetch(pf, fs_pf++);
+                advance(pf);
+            }
+            cp_async_commit();
+            cp_async_wait<kTmaPf>();  // indices of stage fs have landed
+            __syncwarp();
+            const int cnt = static_cast<int>(is.end - is.p0 < kTmaStageNnz ? is.end - is.p0 : kTmaStageNnz);
+            const int slot = static_cast<int>(fs % kTmaStages);
+            const unsigned ph = static_cast<unsigned>((fs / kTmaStages) & 1);
+            mbar_wait(&empty[slot], ph ^ 1);
+            const int c = iring[static_cast<int>(fs % kTmaRing) * kTmaStageNnz + (lane < cnt ? lane : cnt - 1)];
+            const int ngather = (cnt + 3) / 4;
+            if (lane == 0)
+                mbar_expect_tx(&full[slot], static_cast<unsigned>(ngather * 4 * kTmaW * sizeof(double)));
+            __syncwarp();
+            const int g = lane & 7;
+            const int r0 = __shfl_sync(kFull, c, 4 * g), r1 = __shfl_sync(kFull, c, 4 * g + 1);
+            const int r2 = __shfl_sync(kFull, c, 4 * g + 2), r3 = __shfl_sync(kFull, c, 4 * g + 3);
+            if (lane < ngather)
+                tma_gather4(data + (static_cast<size_t>(slot) * kTmaStageNnz + 4 * lane) * kTmaW, &xmap,
+                            is.col0, r0, r1, r2, r3, &full[slot]);
+            advance(is);
+            ++fs;
+        }
+        cp_async_wait<0>();
     } else {
         const int cw = warp - 1;
+        int64_t fs = 0;
         for (int64_t item = blockIdx.x; item < items; item += gridDim.x) {
             const int64_t row = order[item / nslab];
             const int64_t col = static_cast<int64_t>(item % nslab) * kTmaW + cw * 32 + lane;
@@ -320,9 +371,10 @@ spmm_hub_tma_kernel(const __grid_constant__ CUtensorMap xmap, const int64_t* __r
             double acc = 0.0;
             for (int64_t p0 = beg; p0 < end; p0 += kTmaStageNnz) {
                 const int cnt = static_cast<int>(end - p0 < kTmaStageNnz ? end - p0 : kTmaStageNnz);
-                mbar_wait(&full[stage], phase);
-                const double* d = data + static_cast<size_t>(stage) * kTmaStageNnz * kTmaW + cw * 32 + lane;
-                const double* v = vals + stage * kTmaStageNnz;
+                const int slot = static_cast<int>(fs % kTmaStages);
+                mbar_wait(&full[slot], static_cast<unsigned>((fs / kTmaStages) & 1));
+                const double* d = data + static_cast<size_t>(slot) * kTmaStageNnz * kTmaW + cw * 32 + lane;
+                const double* v = vring + static_cast<int>(fs % kTmaRing) * kTmaStageNnz;
                 if (cnt == kTmaStageNnz) {
 #pragma unroll
                     for (int j = 0; j < kTmaStageNnz; ++j) acc = fma(v[j], d[j * kTmaW], acc);
@@ -330,11 +382,8 @@ spmm_hub_tma_kernel(const __grid_constant__ CUtensorMap xmap, const int64_t* __r
                     for (int j = 0; j < cnt; ++j) acc = fma(v[j], d[j * kTmaW], acc);
                 }
                 __syncwarp();
-                if (lane == 0) mbar_arrive(&empty[stage]);
-                if (++stage == kTmaStages) {
-                    stage = 0;
-                    phase ^= 1;
-                }
+                if (lane == 0) mbar_arrive(&empty[slot]);
+                ++fs;
             }
             if (col < ld) {
                 if (kShift) {
