@@ -323,6 +323,8 @@ spmm_hub_tma_kernel(const __grid_constant__ CUtensorMap xmap, const int64_t* __r
                 cp_async8(vring + r, val + c.p0 + lane);
             }
         };
+        if (lane == 0)
+            asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&xmap)) : "memory");
         Cursor pf{blockIdx.x, 0, 0, 0, 0, false};
         seek(pf);
         Cursor is = pf;
@@ -346,17 +348,22 @@ spmm_hub_tma_kernel(const __grid_constant__ CUtensorMap xmap, const int64_t* __r
             const int slot = static_cast<int>(fs % kTmaStages);
             const unsigned ph = static_cast<unsigned>((fs / kTmaStages) & 1);
             mbar_wait(&empty[slot], ph ^ 1);
-            const int c = iring[static_cast<int>(fs % kTmaRing) * kTmaStageNnz + (lane < cnt ? lane : cnt - 1)];
-            const int ngather = (cnt + 3) / 4;
-            if (lane == 0)
+            if (lane == 0) {
+                // one thread issues the stage: ceil(cnt/4) gather4 copies with
+                // uniform operands (row indices read back as int4). Index slots
+                // past cnt may hold stale values; TMA zero-fills any out-of-range
+                // row and the consumers never read those rows.
+                const int ngather = (cnt + 3) / 4;
                 mbar_expect_tx(&full[slot], static_cast<unsigned>(ngather * 4 * kTmaW * sizeof(double)));
+                const int4* rows4 = reinterpret_cast<const int4*>(
+                    iring + static_cast<int>(fs % kTmaRing) * kTmaStageNnz);
+                double* dst = data + static_cast<size_t>(slot) * kTmaStageNnz * kTmaW;
+                for (int g = 0; g < ngather; ++g) {
+                    const int4 r = rows4[g];
+                    tma_gather4(dst + 4 * g * kTmaW, &xmap, is.col0, r.x, r.y, r.z, r.w, &full[slot]);
+                }
+            }
             __syncwarp();
-            const int g = lane & 7;
-            const int r0 = __shfl_sync(kFull, c, 4 * g), r1 = __shfl_sync(kFull, c, 4 * g + 1);
-            const int r2 = __shfl_sync(kFull, c, 4 * g + 2), r3 = __shfl_sync(kFull, c, 4 * g + 3);
-            if (lane < ngather)
-                tma_gather4(data + (static_cast<size_t>(slot) * kTmaStageNnz + 4 * lane) * kTmaW, &xmap,
-                            is.col0, r0, r1, r2, r3, &full[slot]);
             advance(is);
             ++fs;
         }
