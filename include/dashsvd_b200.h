@@ -169,6 +169,14 @@ DSVD_API int dsvd_matrix_destroy(dsvd_matrix* m);
  * global_rows x cols matrix (multi-GPU solves; see dsvd_ctx_attach_comm). */
 DSVD_API int dsvd_matrix_set_shard(dsvd_matrix* m, int64_t row_offset, int64_t global_rows);
 DSVD_API int dsvd_matrix_shape(const dsvd_matrix* m, int64_t* rows, int64_t* cols, int64_t* nnz);
+/* Microbenchmark the SpMM of A (transpose = 0) or A^T (transpose = 1) on a
+ * random l-column block: average milliseconds over `iters` launches.
+ * variant: 0 = TMA gather4 hub kernel, 1 = cp.async hub kernel; +16 times only
+ * the hub rows, +32 only the bulk rows. dsvd_matrix_hub_rows reports how many
+ * rows of A / A^T take the hub path (option "hub_threshold"). */
+DSVD_API int dsvd_matrix_bench_spmm(dsvd_matrix* m, int transpose, int64_t l, int variant,
+                                    int iters, double* ms_out);
+DSVD_API int dsvd_matrix_hub_rows(const dsvd_matrix* m, int64_t* hub_a, int64_t* hub_at);
 /* Download the device-built transpose (int64 offsets/indices, host buffers). */
 DSVD_API int dsvd_matrix_download_transpose(const dsvd_matrix* m, int64_t* t_offsets,
                                    int64_t* t_col_indices, double* t_values);

@@ -79,6 +79,8 @@ SIGNATURES = [
     ("dsvd_matrix_set_shard", C.c_int, [P, I64, I64]),
     ("dsvd_matrix_shape", C.c_int, [P, C.POINTER(I64), C.POINTER(I64), C.POINTER(I64)]),
     ("dsvd_matrix_download_transpose", C.c_int, [P, P, P, P]),
+    ("dsvd_matrix_bench_spmm", C.c_int, [P, C.c_int, I64, C.c_int, C.c_int, C.POINTER(D)]),
+    ("dsvd_matrix_hub_rows", C.c_int, [P, C.POINTER(I64), C.POINTER(I64)]),
     ("dsvd_solve", C.c_int, [P, P, C.POINTER(dsvd_config), C.POINTER(dsvd_outputs), OBSERVER, P]),
     ("dsvd_solve_csr", C.c_int, [P, I64, I64, I64, P, P, P, C.POINTER(dsvd_config),
                                  C.POINTER(dsvd_outputs)]),

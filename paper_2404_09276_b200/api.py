@@ -297,6 +297,18 @@ class DeviceMatrix:
     def set_shard(self, row_offset: int, global_rows: int) -> None:
         check(lib().dsvd_matrix_set_shard(self._h, int(row_offset), int(global_rows)))
 
+    def bench_spmm(self, transpose: bool, l: int, variant: int = 0, iters: int = 5) -> float:
+        """Average ms of one SpMM launch on a random l-column block (see header)."""
+        ms = C.c_double()
+        check(lib().dsvd_matrix_bench_spmm(self._h, 1 if transpose else 0, int(l), int(variant),
+                                           int(iters), C.byref(ms)))
+        return float(ms.value)
+
+    def hub_rows(self):
+        a, t = C.c_int64(), C.c_int64()
+        check(lib().dsvd_matrix_hub_rows(self._h, C.byref(a), C.byref(t)))
+        return int(a.value), int(t.value)
+
     def transpose(self) -> SparseMatrix:
         off = np.empty(self.cols + 1, dtype=np.int64)
         idx = np.empty(self.nnz, dtype=np.int64)

@@ -709,6 +709,40 @@ int dsvd_matrix_shape(const dsvd_matrix* m, int64_t* rows, int64_t* cols, int64_
     });
 }
 
+int dsvd_matrix_bench_spmm(dsvd_matrix* m, int transpose, int64_t l, int variant, int iters,
+                           double* ms_out) {
+    return guarded([&] {
+        dsvd_ctx* ctx = m->ctx;
+        set_device(ctx);
+        cudaStream_t st = ctx->stream;
+        const DevCsr& A = transpose ? m->at : m->a;
+        const int64_t ld = padded_ld(l);
+        double* X = ctx->tbuf<double>("bench.X", A.cols * ld);
+        double* Y = ctx->tbuf<double>("bench.Y", A.rows * ld);
+        gaussian_rowmajor(X, A.cols, l, ld, 1234, st);
+        spmm(SpmmArgs{&A, X, Y, ld, l, nullptr, nullptr, nullptr}, st, variant, ctx->side, ctx->fork,
+             ctx->join);
+        cudaEvent_t e0 = ctx->event(), e1 = ctx->event();
+        DSVD_CUDA_CHECK(cudaEventRecord(e0, st));
+        for (int i = 0; i < iters; ++i)
+            spmm(SpmmArgs{&A, X, Y, ld, l, nullptr, nullptr, nullptr}, st, variant, ctx->side,
+                 ctx->fork, ctx->join);
+        DSVD_CUDA_CHECK(cudaEventRecord(e1, st));
+        DSVD_CUDA_CHECK(cudaEventSynchronize(e1));
+        float ms = 0.f;
+        DSVD_CUDA_CHECK(cudaEventElapsedTime(&ms, e0, e1));
+        *ms_out = ms / (iters > 0 ? iters : 1);
+        ctx->event_next = 0;
+    });
+}
+
+int dsvd_matrix_hub_rows(const dsvd_matrix* m, int64_t* hub_a, int64_t* hub_at) {
+    return guarded([&] {
+        *hub_a = m->a.hub_rows;
+        *hub_at = m->at.hub_rows;
+    });
+}
+
 int dsvd_matrix_download_transpose(const dsvd_matrix* m, int64_t* t_off, int64_t* t_idx,
                                    double* t_val) {
     return guarded([&] {

@@ -348,20 +348,18 @@ spmm_hub_tma_kernel(const __grid_constant__ CUtensorMap xmap, const int64_t* __r
             const int slot = static_cast<int>(fs % kTmaStages);
             const unsigned ph = static_cast<unsigned>((fs / kTmaStages) & 1);
             mbar_wait(&empty[slot], ph ^ 1);
-            if (lane == 0) {
-                // one thread issues the stage: ceil(cnt/4) gather4 copies with
-                // uniform operands (row indices read back as int4). Index slots
-                // past cnt may hold stale values; TMA zero-fills any out-of-range
-                // row and the consumers never read those rows.
-                const int ngather = (cnt + 3) / 4;
+            // lanes 0..ngather-1 each issue one gather4 (four X rows of the slab).
+            // Index slots past cnt may hold stale values; TMA zero-fills any
+            // out-of-range row and the consumers never read those rows.
+            const int ngather = (cnt + 3) / 4;
+            if (lane == 0)
                 mbar_expect_tx(&full[slot], static_cast<unsigned>(ngather * 4 * kTmaW * sizeof(double)));
-                const int4* rows4 = reinterpret_cast<const int4*>(
-                    iring + static_cast<int>(fs % kTmaRing) * kTmaStageNnz);
-                double* dst = data + static_cast<size_t>(slot) * kTmaStageNnz * kTmaW;
-                for (int g = 0; g < ngather; ++g) {
-                    const int4 r = rows4[g];
-                    tma_gather4(dst + 4 * g * kTmaW, &xmap, is.col0, r.x, r.y, r.z, r.w, &full[slot]);
-                }
+            __syncwarp();
+            if (lane < ngather) {
+                const int4 r = reinterpret_cast<const int4*>(
+                    iring + static_cast<int>(fs % kTmaRing) * kTmaStageNnz)[lane];
+                tma_gather4(data + (static_cast<size_t>(slot) * kTmaStageNnz + 4 * lane) * kTmaW, &xmap,
+                            is.col0, r.x, r.y, r.z, r.w, &full[slot]);
             }
             __syncwarp();
             advance(is);
@@ -545,6 +543,10 @@ void spmm(const SpmmArgs& s, cudaStream_t stream, int variant, cudaStream_t side
           cudaEvent_t fork, cudaEvent_t join) {
     const DevCsr& a = *s.a;
     if (a.rows == 0) return;
+    // variant bits: low nibble selects the hub kernel; 16 skips the bulk rows,
+    // 32 skips the hub rows (benchmarking the two halves separately)
+    const bool skip_bulk = (variant & 16) != 0, skip_hub = (variant & 32) != 0;
+    variant &= 15;
     const int64_t hub = (side != nullptr && a.d_hub_rows != nullptr) ? a.hub_rows : 0;
     if (hub > 0) {
         static bool attr = false;
@@ -558,7 +560,7 @@ void spmm(const SpmmArgs& s, cudaStream_t stream, int variant, cudaStream_t side
         DSVD_CUDA_CHECK(cudaEventRecord(fork, stream));
         DSVD_CUDA_CHECK(cudaStreamWaitEvent(side, fork, 0));
     }
-    if (hub > 0 && variant == 0) {
+    if (hub > 0 && !skip_hub && variant == 0) {
         static bool tattr = false;
         if (!tattr) {
             DSVD_CUDA_CHECK(cudaFuncSetAttribute(spmm_hub_tma_kernel<true>,
@@ -579,7 +581,7 @@ void spmm(const SpmmArgs& s, cudaStream_t stream, int variant, cudaStream_t side
                 xmap, a.off, a.idx, a.val, a.order, a.d_hub_rows, nslab64, s.y, s.ld, nullptr, nullptr,
                 s.gate);
         DSVD_LAUNCH_CHECK();
-    } else if (hub > 0) {
+    } else if (hub > 0 && !skip_hub) {
         const int nslab32 = static_cast<int>(ceil_div(s.ld, 32));
         const unsigned blocks = static_cast<unsigned>(ceil_div(hub * nslab32, kHubWarps));
         if (s.q != nullptr)
@@ -592,7 +594,7 @@ void spmm(const SpmmArgs& s, cudaStream_t stream, int variant, cudaStream_t side
         DSVD_LAUNCH_CHECK();
     }
     const int nslab = static_cast<int>(ceil_div(s.ld, kSlab));
-    const int64_t items = (a.rows - hub) * nslab;
+    const int64_t items = skip_bulk ? 0 : (a.rows - hub) * nslab;
     if (items > 0) {
         const int warps_per_block = 8;
         const int64_t blocks = ceil_div(items, warps_per_block);
