@@ -185,6 +185,221 @@ __global__ void jacobi_replay_kernel(const double2* __restrict__ rot_log, int l,
     for (int j = lane; j < lp; j += 32) vecs[static_cast<int64_t>(row) * lp + j] = v[j];
 }
 
+
+// ---- two-CTA cluster variant -----------------------------------------------------
+// CTA 0 runs the Jacobi rounds on G (shared memory) exactly as jacobi_kernel;
+// after computing a round's rotations it writes them straight into CTA 1's
+// shared memory (DSMEM) and signals an mbarrier there. CTA 1 holds V and applies
+// each round's rotations V <- V J while CTA 0 is already on the next rounds: the
+// accumulation of eigenvectors runs concurrently on a second SM instead of in a
+// replay kernel afterwards. A kClRing-slot ring with full/empty mbarriers (the
+// empty ones live in CTA 0 and are signalled remotely) decouples the two.
+constexpr int kClRing = 8;
+
+__device__ __forceinline__ unsigned s_u32(const void* p) {
+    return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ unsigned cl_rank() {
+    unsigned r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ unsigned cl_map(const void* p, unsigned rank) {
+    unsigned r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(r) : "r"(s_u32(p)), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void cl_st_v2(unsigned addr, double a, double b) {
+    asm volatile("st.shared::cluster.v2.f64 [%0], {%1, %2};\n" ::"r"(addr), "d"(a), "d"(b) : "memory");
+}
+__device__ __forceinline__ void cl_st_s32(unsigned addr, int v) {
+    asm volatile("st.shared::cluster.s32 [%0], %1;\n" ::"r"(addr), "r"(v) : "memory");
+}
+__device__ __forceinline__ void cl_arrive(unsigned addr) {
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];\n" ::"r"(addr) : "memory");
+}
+__device__ __forceinline__ void cl_wait(uint64_t* bar, unsigned parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(s_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void cl_sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::
+                     : "memory");
+}
+
+size_t cluster_smem_bytes(int lp) {
+    const size_t half = lp / 2;
+    return sizeof(double) * lp * lp + sizeof(double2) * kClRing * half + 2 * kClRing * sizeof(uint64_t) +
+           kClRing * sizeof(int) + sizeof(uint16_t) * half * (half + 1) / 2 + 64;
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kEigThreads, 1)
+jacobi_cluster_kernel(const double* __restrict__ g_in, int l, int lp, int max_sweeps,
+                      double* __restrict__ lam, double* __restrict__ vecs, Control* ctrl,
+                      const int32_t* __restrict__ gate) {
+    // the gate is read by both CTAs before any cluster traffic, so both exit together
+    if (gate != nullptr && *gate != 0) return;
+    extern __shared__ __align__(16) double cl_smem[];
+    __shared__ double cs_c[kMaxPairs], cs_s[kMaxPairs], cs_t[kMaxPairs];
+    __shared__ int pp[kMaxPairs], qq[kMaxPairs];
+    __shared__ int rotated;
+    const int half = lp / 2;
+    double* M = cl_smem;                                               // G (rank 0) or V (rank 1)
+    double2* ring = reinterpret_cast<double2*>(M + lp * lp);           // [kClRing][half] (rank 1)
+    uint64_t* full = reinterpret_cast<uint64_t*>(ring + kClRing * half);  // rank 1
+    uint64_t* empty = full + kClRing;                                  // rank 0
+    int* ctrlw = reinterpret_cast<int*>(empty + kClRing);              // rank 1
+    uint16_t* blk = reinterpret_cast<uint16_t*>(ctrlw + kClRing);      // rank 0
+    const unsigned rank = cl_rank();
+    const int tid = threadIdx.x;
+    if (tid == 0) {
+        for (int sl = 0; sl < kClRing; ++sl) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(s_u32(&full[sl])), "r"(half));
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(s_u32(&empty[sl])), "r"(1));
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    cl_sync();
+
+    if (rank == 0) {
+        const int nblocks = half * (half + 1) / 2;
+        for (int e = tid; e < lp * lp; e += blockDim.x) {
+            const int i = e / lp, j = e % lp;
+            M[e] = (i < l && j < l) ? g_in[i * l + j] : 0.0;
+        }
+        for (int kp = tid; kp < half; kp += blockDim.x) {
+            const int base = kp * half - kp * (kp - 1) / 2;
+            for (int kr = kp; kr < half; ++kr) blk[base + (kr - kp)] = static_cast<uint16_t>((kp << 8) | kr);
+        }
+        __syncthreads();
+        int64_t rg = 0;
+        int sweep = 0;
+        bool converged = false;
+        for (; sweep < max_sweeps && !converged; ++sweep) {
+            if (tid == 0) rotated = 0;
+            __syncthreads();
+            for (int round = 0; round < lp - 1; ++round, ++rg) {
+                const int sl = static_cast<int>(rg % kClRing);
+                for (int k = tid; k < half; k += blockDim.x) {
+                    int p, q;
+                    pair_of(round, k, lp, p, q);
+                    const double a = M[p * lp + p], d = M[q * lp + q], b = M[p * lp + q];
+                    double c = 1.0, s = 0.0, t = 0.0;
+                    if (fabs(b) > kJacobiTol * sqrt(fabs(a)) * sqrt(fabs(d)) && fabs(b) > 1e-300) {
+                        const double theta = (d - a) / (2.0 * b);
+                        if (fabs(theta) > 1e150) {
+                            t = 0.5 / theta;
+                        } else {
+                            t = (theta >= 0.0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(fma(theta, theta, 1.0)));
+                        }
+                        c = 1.0 / sqrt(fma(t, t, 1.0));
+                        s = t * c;
+                        if (s != 0.0) rotated = 1;
+                    }
+                    cs_c[k] = c;
+                    cs_s[k] = s;
+                    cs_t[k] = t;
+                    pp[k] = p;
+                    qq[k] = q;
+                    // hand the rotation to the V-CTA
+                    cl_wait(&empty[sl], static_cast<unsigned>(((rg / kClRing) & 1) ^ 1));
+                    cl_st_v2(cl_map(&ring[sl * half + k], 1), c, s);
+                    if (k == 0) cl_st_s32(cl_map(&ctrlw[sl], 1), 1);
+                    cl_arrive(cl_map(&full[sl], 1));
+                }
+                __syncthreads();
+                for (int e = tid; e < nblocks; e += blockDim.x) {
+                    const int code = blk[e];
+                    const int kp = code >> 8, kr = code & 0xff;
+                    const double s1 = cs_s[kp], s2 = cs_s[kr];
+                    const int p = pp[kp], q = qq[kp];
+                    if (kp == kr) {
+                        if (s1 != 0.0) {
+                            const double t = cs_t[kp];
+                            const double b = M[p * lp + q];
+                            M[p * lp + p] -= t * b;
+                            M[q * lp + q] += t * b;
+                            M[p * lp + q] = 0.0;
+                            M[q * lp + p] = 0.0;
+                        }
+                        continue;
+                    }
+                    if (s1 == 0.0 && s2 == 0.0) continue;
+                    const double c1 = cs_c[kp], c2 = cs_c[kr];
+                    const int r = pp[kr], s = qq[kr];
+                    const double xpr = M[p * lp + r], xps = M[p * lp + s];
+                    const double xqr = M[q * lp + r], xqs = M[q * lp + s];
+                    const double ypr = c2 * xpr - s2 * xps, yps = s2 * xpr + c2 * xps;
+                    const double yqr = c2 * xqr - s2 * xqs, yqs = s2 * xqr + c2 * xqs;
+                    const double zpr = c1 * ypr - s1 * yqr, zqr = s1 * ypr + c1 * yqr;
+                    const double zps = c1 * yps - s1 * yqs, zqs = s1 * yps + c1 * yqs;
+                    M[p * lp + r] = zpr;
+                    M[r * lp + p] = zpr;
+                    M[p * lp + s] = zps;
+                    M[s * lp + p] = zps;
+                    M[q * lp + r] = zqr;
+                    M[r * lp + q] = zqr;
+                    M[q * lp + s] = zqs;
+                    M[s * lp + q] = zqs;
+                }
+                __syncthreads();
+            }
+            converged = rotated == 0;
+            __syncthreads();
+        }
+        // stop marker for the V-CTA
+        {
+            const int sl = static_cast<int>(rg % kClRing);
+            for (int k = tid; k < half; k += blockDim.x) {
+                cl_wait(&empty[sl], static_cast<unsigned>(((rg / kClRing) & 1) ^ 1));
+                if (k == 0) cl_st_s32(cl_map(&ctrlw[sl], 1), 0);
+                cl_arrive(cl_map(&full[sl], 1));
+            }
+        }
+        for (int i = tid; i < lp; i += blockDim.x) lam[i] = M[i * lp + i];
+        if (tid == 0) {
+            ctrl->eig_sweeps = sweep;
+            ctrl->total_sweeps += sweep;
+            if (!converged && ctrl->status == DSVD_OK) {
+                ctrl->status = DSVD_NUMERICAL;
+                ctrl->stopped = 1;
+            }
+        }
+    } else {
+        for (int e = tid; e < lp * lp; e += blockDim.x) M[e] = (e / lp == e % lp) ? 1.0 : 0.0;
+        __syncthreads();
+        for (int64_t rg = 0;; ++rg) {
+            const int sl = static_cast<int>(rg % kClRing);
+            cl_wait(&full[sl], static_cast<unsigned>((rg / kClRing) & 1));
+            if (ctrlw[sl] == 0) break;
+            const int round = static_cast<int>(rg % (lp - 1));
+            const double2* rot = ring + sl * half;
+            for (int e = tid; e < lp * half; e += blockDim.x) {
+                const int r = e / half, k = e - (e / half) * half;
+                const double2 cs = rot[k];
+                if (cs.y != 0.0) {
+                    int p, q;
+                    pair_of(round, k, lp, p, q);
+                    const double vp = M[r * lp + p], vq = M[r * lp + q];
+                    M[r * lp + p] = cs.x * vp - cs.y * vq;
+                    M[r * lp + q] = cs.y * vp + cs.x * vq;
+                }
+            }
+            __syncthreads();
+            if (tid == 0) cl_arrive(cl_map(&empty[sl], 0));
+        }
+        for (int e = tid; e < lp * lp; e += blockDim.x) vecs[e] = M[e];
+    }
+    cl_sync();  // keep both CTAs' shared memory alive until all remote traffic is done
+}
+
 constexpr int kFinishThreads = 512;
 
 __global__ void __launch_bounds__(kFinishThreads)
@@ -379,6 +594,16 @@ void eig_workspace_bind(EigWorkspace& w, int l, int max_sweeps, void* mem) {
 void jacobi_eig(const double* g, EigWorkspace& w, Control* ctrl, const int32_t* gate,
                 cudaStream_t stream) {
     if (w.lp > 2 * kMaxPairs) fail(DSVD_UNSUPPORTED, "eigensolver: l > 512 is not supported");
+    const size_t csmem = cluster_smem_bytes(w.lp);
+    if (csmem <= static_cast<size_t>(kSmemLimit) - 12 * 1024 && w.lp >= 4) {
+        DSVD_CUDA_CHECK(cudaFuncSetAttribute(jacobi_cluster_kernel,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             static_cast<int>(csmem)));
+        jacobi_cluster_kernel<<<2, kEigThreads, csmem, stream>>>(g, w.l, w.lp, w.max_sweeps, w.lam,
+                                                                 w.vecs, ctrl, gate);
+        DSVD_LAUNCH_CHECK();
+        return;
+    }
     const size_t half = w.lp / 2;
     const size_t table = sizeof(uint16_t) * half * (half + 1) / 2;
     const size_t gbytes = sizeof(double) * w.lp * w.lp;
