@@ -381,15 +381,22 @@ jacobi_cluster_kernel(const double* __restrict__ g_in, int l, int lp, int max_sw
             if (ctrlw[sl] == 0) break;
             const int round = static_cast<int>(rg % (lp - 1));
             const double2* rot = ring + sl * half;
-            for (int e = tid; e < lp * half; e += blockDim.x) {
-                const int r = e / half, k = e - (e / half) * half;
+            // thread -> (pair k, block of rows): the rotation is loaded once and
+            // applied to a strip of rows (no per-element index arithmetic)
+            const int groups = blockDim.x / half;  // row groups (>= 1: half <= 82 here)
+            const int k = tid % half, grp = tid / half;
+            if (grp < groups) {
                 const double2 cs = rot[k];
                 if (cs.y != 0.0) {
                     int p, q;
                     pair_of(round, k, lp, p, q);
-                    const double vp = M[r * lp + p], vq = M[r * lp + q];
-                    M[r * lp + p] = cs.x * vp - cs.y * vq;
-                    M[r * lp + q] = cs.y * vp + cs.x * vq;
+                    const int rows_per = (lp + groups - 1) / groups;
+                    const int r0 = grp * rows_per, r1 = min(lp, r0 + rows_per);
+                    for (int r = r0; r < r1; ++r) {
+                        const double vp = M[r * lp + p], vq = M[r * lp + q];
+                        M[r * lp + p] = cs.x * vp - cs.y * vq;
+                        M[r * lp + q] = cs.y * vp + cs.x * vq;
+                    }
                 }
             }
             __syncthreads();

@@ -401,6 +401,141 @@ spmm_hub_tma_kernel(const __grid_constant__ CUtensorMap xmap, const int64_t* __r
     }
 }
 
+
+// ---- hub rows, deep cp.async variant --------------------------------------------------
+// One warp per CTA, persistent over (hub row, 32-column slab) items, one lane
+// per column. The warp keeps kDeepDc chunks of 32 nonzeros (kDeepDc*8 KB of
+// gathered X) in flight with cp.async into its own shared-memory ring — about
+// one DRAM latency's worth of bytes at the FMA-chain rate — so a hub row runs
+// at ~8 cycles per nonzero (the DFMA latency of its chain) instead of being
+// bound by per-request TMA or LDG limits. Indices/values are fetched 2*kDeepDc
+// chunks ahead. Bitwise identical to the CSR-order chain.
+constexpr int kDeepDc = 10;                       // gather chunks in flight
+constexpr int kDeepIc = 2 * kDeepDc + 2;          // index/value ring (chunks)
+constexpr size_t kDeepSmem = sizeof(double) * kDeepDc * 32 * 32 +
+                             kDeepIc * 32 * (sizeof(double) + sizeof(int32_t)) + 128;
+
+template <bool kShift>
+__global__ void __launch_bounds__(32)
+spmm_hub_deep_kernel(const int64_t* __restrict__ off, const int32_t* __restrict__ idx,
+                     const double* __restrict__ val, const int32_t* __restrict__ order,
+                     const int32_t* __restrict__ n_hub_p, int nslab, const double* __restrict__ x,
+                     double* __restrict__ y, int64_t ld, const double* __restrict__ q,
+                     const double* __restrict__ alpha_p, const int32_t* __restrict__ gate) {
+    if (gate != nullptr && *gate != 0) return;
+    extern __shared__ __align__(16) double deep_smem[];
+    double* ring = deep_smem;                                   // [Dc][32 nnz][32 lanes]
+    double* vring = ring + kDeepDc * 32 * 32;                   // [Ic][32]
+    int32_t* iring = reinterpret_cast<int32_t*>(vring + kDeepIc * 32);  // [Ic][32]
+    const int lane = threadIdx.x;
+    const int64_t items = static_cast<int64_t>(*n_hub_p) * nslab;
+
+    // a cursor walks the flat sequence of 32-nonzero chunks of this CTA's items
+    struct Cursor {
+        int64_t item, beg, end, p0;
+        int64_t col;
+        bool valid;
+    };
+    auto seek = [&](Cursor& c) {
+        c.valid = false;
+        while (c.item < items) {
+            const int64_t row = order[c.item / nslab];
+            c.beg = off[row];
+            c.end = off[row + 1];
+            c.col = (c.item % nslab) * 32 + lane;
+            if (c.end > c.beg) {
+                c.p0 = c.beg;
+                c.valid = true;
+                return;
+            }
+            c.item += gridDim.x;
+        }
+    };
+    auto advance = [&](Cursor& c) {
+        c.p0 += 32;
+        if (c.p0 >= c.end) {
+            c.item += gridDim.x;
+            seek(c);
+        }
+    };
+    auto fetch_iv = [&](const Cursor& c, int64_t k) {
+        if (!c.valid) return;
+        const int64_t p = c.p0 + lane;
+        if (p < c.end) {
+            const int r = static_cast<int>(k % kDeepIc) * 32 + lane;
+            cp_async4(iring + r, idx + p);
+            cp_async8(vring + r, val + p);
+        }
+    };
+    auto gather = [&](const Cursor& c, int64_t k) {
+        if (!c.valid || c.col >= ld) return;
+        const int32_t* ib = iring + static_cast<int>(k % kDeepIc) * 32;
+        double* slot = ring + static_cast<int>(k % kDeepDc) * 1024 + lane;
+        const double* xc = x + c.col;
+        const int cnt = static_cast<int>(c.end - c.p0 < 32 ? c.end - c.p0 : 32);
+        if (cnt == 32) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) cp_async8(slot + j * 32, xc + static_cast<int64_t>(ib[j]) * ld);
+        } else {
+            for (int j = 0; j < cnt; ++j) cp_async8(slot + j * 32, xc + static_cast<int64_t>(ib[j]) * ld);
+        }
+    };
+
+    Cursor ci{blockIdx.x, 0, 0, 0, 0, false};  // index fetch cursor (2*Dc ahead)
+    seek(ci);
+    Cursor cg = ci, cc = ci;                    // gather cursor (Dc-1 ahead), consume cursor
+    int64_t ki = 0, kg = 0, kc = 0;
+    for (int k = 0; k < 2 * kDeepDc; ++k) {
+        fetch_iv(ci, ki++);
+        if (ci.valid) advance(ci);
+    }
+    cp_async_commit();
+    cp_async_wait<0>();
+    __syncwarp();
+    for (int k = 0; k < kDeepDc - 1; ++k) {
+        gather(cg, kg++);
+        if (cg.valid) advance(cg);
+        cp_async_commit();
+    }
+    double acc = 0.0;
+    while (cc.valid) {
+        gather(cg, kg++);
+        if (cg.valid) advance(cg);
+        fetch_iv(ci, ki++);
+        if (ci.valid) advance(ci);
+        cp_async_commit();
+        cp_async_wait<kDeepDc - 1>();  // chunk kc has landed
+        __syncwarp();
+        const double* slot = ring + static_cast<int>(kc % kDeepDc) * 1024 + lane;
+        const double* vb = vring + static_cast<int>(kc % kDeepIc) * 32;
+        const int cnt = static_cast<int>(cc.end - cc.p0 < 32 ? cc.end - cc.p0 : 32);
+        if (cnt == 32) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) acc = fma(vb[j], slot[j * 32], acc);
+        } else {
+            for (int j = 0; j < cnt; ++j) acc = fma(vb[j], slot[j * 32], acc);
+        }
+        __syncwarp();
+        ++kc;
+        const int64_t row_item = cc.item;
+        const int64_t col = cc.col;
+        const bool last = cc.p0 + 32 >= cc.end;
+        advance(cc);
+        if (last) {  // item finished: write its column
+            if (col < ld) {
+                const int64_t row = order[row_item / nslab];
+                if (kShift) {
+                    const double alpha = *alpha_p;
+                    if (alpha != 0.0) acc = fma(-alpha, q[row * ld + col], acc);
+                }
+                y[row * ld + col] = acc;
+            }
+            acc = 0.0;
+        }
+    }
+    cp_async_wait<0>();
+}
+
 // 2-D tensor map over the row-major X block (rows x ld doubles) with a
 // 64-column x 1-row box: the shape tile::gather4 expects.
 CUtensorMap make_xmap(const double* x, int64_t rows, int64_t ld) {
@@ -560,7 +695,27 @@ void spmm(const SpmmArgs& s, cudaStream_t stream, int variant, cudaStream_t side
         DSVD_CUDA_CHECK(cudaEventRecord(fork, stream));
         DSVD_CUDA_CHECK(cudaStreamWaitEvent(side, fork, 0));
     }
-    if (hub > 0 && !skip_hub && variant == 0) {
+    if (hub > 0 && !skip_hub && variant == 2) {
+        static bool dattr = false;
+        if (!dattr) {
+            DSVD_CUDA_CHECK(cudaFuncSetAttribute(spmm_hub_deep_kernel<true>,
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, kDeepSmem));
+            DSVD_CUDA_CHECK(cudaFuncSetAttribute(spmm_hub_deep_kernel<false>,
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, kDeepSmem));
+            dattr = true;
+        }
+        const int nslab32 = static_cast<int>(ceil_div(s.ld, 32));
+        const int64_t items = hub * nslab32;
+        const unsigned blocks = static_cast<unsigned>(items < 2 * kNumSMs ? items : 2 * kNumSMs);
+        if (s.q != nullptr)
+            spmm_hub_deep_kernel<true><<<blocks, 32, kDeepSmem, side>>>(
+                a.off, a.idx, a.val, a.order, a.d_hub_rows, nslab32, s.x, s.y, s.ld, s.q, s.alpha, s.gate);
+        else
+            spmm_hub_deep_kernel<false><<<blocks, 32, kDeepSmem, side>>>(
+                a.off, a.idx, a.val, a.order, a.d_hub_rows, nslab32, s.x, s.y, s.ld, nullptr, nullptr,
+                s.gate);
+        DSVD_LAUNCH_CHECK();
+    } else if (hub > 0 && !skip_hub && variant == 0) {
         static bool tattr = false;
         if (!tattr) {
             DSVD_CUDA_CHECK(cudaFuncSetAttribute(spmm_hub_tma_kernel<true>,

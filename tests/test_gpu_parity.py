@@ -147,7 +147,7 @@ def hub_dev():
     dv.close()
 
 
-@pytest.mark.parametrize("variant", [0, 1])  # 0: TMA gather4 ring, 1: cp.async ring
+@pytest.mark.parametrize("variant", [0, 1, 2])  # 0: TMA gather4 ring, 1/2: cp.async rings
 @pytest.mark.parametrize("threshold", [1, 9, 33, 200])
 @pytest.mark.parametrize("l", [1, 31, 75, 150])
 def test_spmm_hub_path_bitwise(hub_dev, oracle, c1, threshold, l, variant):
@@ -162,7 +162,7 @@ def test_spmm_hub_path_bitwise(hub_dev, oracle, c1, threshold, l, variant):
     assert_bitwise(d.spmm_shift(to_dev(at), y, 0.37, q, device=hub_dev), t_ref)
 
 
-@pytest.mark.parametrize("variant", [0, 1])
+@pytest.mark.parametrize("variant", [0, 1, 2])
 def test_spmm_hub_power_law_bitwise(hub_dev, oracle, variant):
     hub_dev.set_option("hub_threshold", 64)
     hub_dev.set_option("spmm_variant", variant)

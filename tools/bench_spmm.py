@@ -15,7 +15,7 @@ for thr in (4096, 16384):
     ha, hat = m.hub_rows()
     print(f"threshold {thr}: hub rows A={ha} A^T={hat}")
     for tr in (0, 1):
-        for var in (0, 1):
+        for var in (0, 2):
             full = m.bench_spmm(tr, l, var)
             hub = m.bench_spmm(tr, l, var + 16)
             bulk = m.bench_spmm(tr, l, var + 32)
