@@ -80,6 +80,53 @@ struct CsrAlloc {
     }
 };
 
+// Chunk list of the rows longer than m.split_chunk (the prefix m.hub_rows of
+// m.order): each split row is cut into ceil(len / C) near-equal CSR ranges.
+void build_chunks(dsvd_ctx* ctx, CsrAlloc& al, DevCsr& m, const std::string& tag) {
+    cudaStream_t st = ctx->stream;
+    const int64_t ns = m.hub_rows, C = m.split_chunk;
+    m.nsplit = 0;
+    m.nchunks = 0;
+    m.hub_rows = 0;  // split mode does not use the hub kernels
+    if (ns == 0) return;
+    int64_t* dbe = ctx->tbuf<int64_t>("chunk.bounds", 2 * ns);
+    prefix_row_bounds(m, ns, dbe, dbe + ns, st);
+    count_launch();
+    std::vector<int64_t> be(static_cast<size_t>(2 * ns));
+    DSVD_CUDA_CHECK(cudaMemcpyAsync(be.data(), dbe, sizeof(int64_t) * 2 * ns, cudaMemcpyDeviceToHost, st));
+    DSVD_CUDA_CHECK(cudaStreamSynchronize(st));
+    std::vector<int64_t> p0, p1;
+    std::vector<int32_t> first(static_cast<size_t>(ns + 1), 0);
+    for (int64_t i = 0; i < ns; ++i) {
+        const int64_t b = be[i], e = be[ns + i], len = e - b;
+        const int64_t nch = (len + C - 1) / C;
+        const int64_t cs = (len + nch - 1) / nch;
+        first[i] = static_cast<int32_t>(p0.size());
+        for (int64_t j = 0; j < nch; ++j) {
+            p0.push_back(b + j * cs);
+            p1.push_back(std::min(e, b + (j + 1) * cs));
+        }
+    }
+    first[ns] = static_cast<int32_t>(p0.size());
+    const int64_t nc = static_cast<int64_t>(p0.size());
+    m.chunk_p0 = static_cast<int64_t*>(al.get(tag + ".chunk_p0", sizeof(int64_t) * nc));
+    m.chunk_p1 = static_cast<int64_t*>(al.get(tag + ".chunk_p1", sizeof(int64_t) * nc));
+    m.split_first = static_cast<int32_t*>(al.get(tag + ".split_first", sizeof(int32_t) * (ns + 1)));
+    DSVD_CUDA_CHECK(cudaMemcpyAsync(m.chunk_p0, p0.data(), sizeof(int64_t) * nc, cudaMemcpyHostToDevice, st));
+    DSVD_CUDA_CHECK(cudaMemcpyAsync(m.chunk_p1, p1.data(), sizeof(int64_t) * nc, cudaMemcpyHostToDevice, st));
+    DSVD_CUDA_CHECK(cudaMemcpyAsync(m.split_first, first.data(), sizeof(int32_t) * (ns + 1),
+                                    cudaMemcpyHostToDevice, st));
+    DSVD_CUDA_CHECK(cudaStreamSynchronize(st));  // the host vectors die here
+    m.nsplit = ns;
+    m.nchunks = nc;
+}
+
+// Partial-row workspace for the split chunks of `a` at width ld.
+double* partial_for(dsvd_ctx* ctx, const DevCsr& a, int64_t ld) {
+    if (a.nchunks == 0) return nullptr;
+    return ctx->tbuf<double>("spmm.partial", a.nchunks * ld);
+}
+
 // Device CSR (+ transpose + row orders) from int64 offsets / indices and
 // values already on the device.
 void build_pair(dsvd_ctx* ctx, CsrAlloc& al, int64_t rows, int64_t cols, int64_t nnz,
@@ -131,7 +178,11 @@ void build_pair(dsvd_ctx* ctx, CsrAlloc& al, int64_t rows, int64_t cols, int64_t
     build_transpose(a, at, scratch, scratch_bytes, st);
     count_launch(nnz > 0 ? 8 : 1);  // 4 own kernels + CUB radix sort passes (estimate)
     int32_t* hubs = static_cast<int32_t*>(al.get("hub_counts", sizeof(int32_t) * 2));
-    a.hub_threshold = at.hub_threshold = ctx->hub_threshold;
+    // split mode: the "hub" prefix of the row order is the set of rows longer
+    // than split_chunk, which are cut into chunks below
+    const int64_t C = ctx->split_chunk;
+    a.hub_threshold = at.hub_threshold = C > 0 ? C + 1 : ctx->hub_threshold;
+    a.split_chunk = at.split_chunk = C;
     a.d_hub_rows = hubs;
     at.d_hub_rows = hubs + 1;
     build_row_order(a, scratch, scratch_bytes, st);
@@ -145,6 +196,10 @@ void build_pair(dsvd_ctx* ctx, CsrAlloc& al, int64_t rows, int64_t cols, int64_t
     }
     a.hub_rows = rows > 0 ? hh[0] : 0;
     at.hub_rows = cols > 0 ? hh[1] : 0;
+    if (C > 0) {
+        build_chunks(ctx, al, a, "a");
+        build_chunks(ctx, al, at, "at");
+    }
 }
 
 void upload_pair(dsvd_ctx* ctx, CsrAlloc& al, int64_t rows, int64_t cols, int64_t nnz,
@@ -308,7 +363,8 @@ void solve_tall(dsvd_ctx* ctx, const DevCsr& A, const DevCsr& AT, const dsvd_con
 
     // Q = eigSVD(A^T Omega).u
     sp = ctx->span_begin(K_SPMM2);
-    spmm(SpmmArgs{&AT, Y, T, ld, l, nullptr, nullptr, nullptr}, st, ctx->spmm_variant, ctx->side, ctx->fork, ctx->join);
+    spmm(SpmmArgs{&AT, Y, T, ld, l, nullptr, nullptr, nullptr}, st, ctx->spmm_variant, ctx->side, ctx->fork,
+         ctx->join, partial_for(ctx, AT, ld));
     count_launch();
     ctx->span_end(sp);
     if (sharded) {
@@ -346,14 +402,15 @@ void solve_tall(dsvd_ctx* ctx, const DevCsr& A, const DevCsr& AT, const dsvd_con
         count_launch();
         // Y = A Q
         sp = ctx->span_begin(K_SPMM1);
-        spmm(SpmmArgs{&A, Qb[cur], Y, ld, l, nullptr, nullptr, gate}, st, ctx->spmm_variant, ctx->side, ctx->fork, ctx->join);
+        spmm(SpmmArgs{&A, Qb[cur], Y, ld, l, nullptr, nullptr, gate}, st, ctx->spmm_variant, ctx->side,
+             ctx->fork, ctx->join, partial_for(ctx, A, ld));
         count_launch();
         ctx->span_end(sp);
         // T = A^T Y - alpha Q  (add_scaled skipped when alpha == 0)
         sp = ctx->span_begin(K_SPMM2);
         spmm(SpmmArgs{&AT, Y, T, ld, l, sharded ? nullptr : Qb[cur], sharded ? nullptr : &ctrl->alpha,
                       gate},
-             st, ctx->spmm_variant, ctx->side, ctx->fork, ctx->join);
+             st, ctx->spmm_variant, ctx->side, ctx->fork, ctx->join, partial_for(ctx, AT, ld));
         count_launch();
         ctx->span_end(sp);
         if (sharded) {
@@ -407,7 +464,8 @@ void solve_tall(dsvd_ctx* ctx, const DevCsr& A, const DevCsr& AT, const dsvd_con
     control_init(ctrl, s_stored, static_cast<int>(l), st);
     count_launch();
     sp = ctx->span_begin(K_SPMM1);
-    spmm(SpmmArgs{&A, Qf, Y, ld, l, nullptr, nullptr, nullptr}, st, ctx->spmm_variant, ctx->side, ctx->fork, ctx->join);
+    spmm(SpmmArgs{&A, Qf, Y, ld, l, nullptr, nullptr, nullptr}, st, ctx->spmm_variant, ctx->side, ctx->fork,
+         ctx->join, partial_for(ctx, A, ld));
     count_launch();
     ctx->span_end(sp);
     eig_svd_factors(ctx, Y, m, l, ld, eo, ctrl, nullptr, nullptr, sharded, global_m);
@@ -630,6 +688,9 @@ int dsvd_ctx_set_option(dsvd_ctx* ctx, const char* name, int64_t value) {
             ctx->spmm_variant = static_cast<int>(value);
         } else if (n == "hub_threshold") {
             ctx->hub_threshold = value;
+        } else if (n == "split_chunk") {
+            if (value < 0) fail(DSVD_CONFIG, "split_chunk must be >= 0");
+            ctx->split_chunk = value;
         } else {
             fail(DSVD_CONFIG, "unknown option '" + n + "'");
         }
@@ -721,12 +782,12 @@ int dsvd_matrix_bench_spmm(dsvd_matrix* m, int transpose, int64_t l, int variant
         double* Y = ctx->tbuf<double>("bench.Y", A.rows * ld);
         gaussian_rowmajor(X, A.cols, l, ld, 1234, st);
         spmm(SpmmArgs{&A, X, Y, ld, l, nullptr, nullptr, nullptr}, st, variant, ctx->side, ctx->fork,
-             ctx->join);
+             ctx->join, partial_for(ctx, A, ld));
         cudaEvent_t e0 = ctx->event(), e1 = ctx->event();
         DSVD_CUDA_CHECK(cudaEventRecord(e0, st));
         for (int i = 0; i < iters; ++i)
             spmm(SpmmArgs{&A, X, Y, ld, l, nullptr, nullptr, nullptr}, st, variant, ctx->side,
-                 ctx->fork, ctx->join);
+                 ctx->fork, ctx->join, partial_for(ctx, A, ld));
         DSVD_CUDA_CHECK(cudaEventRecord(e1, st));
         DSVD_CUDA_CHECK(cudaEventSynchronize(e1));
         float ms = 0.f;
@@ -889,7 +950,8 @@ int dsvd_finalize_row_basis(dsvd_ctx* ctx, const dsvd_matrix* a, const double* q
         DSVD_CUDA_CHECK(cudaMemcpyAsync(qh, q, sizeof(double) * n * l, cudaMemcpyHostToDevice, st));
         colmajor_to_rowmajor(qh, n, l, Q, ld, st);
         control_init(ctrl, s_stored, static_cast<int>(l), st);
-        spmm(SpmmArgs{&A, Q, B, ld, l, nullptr, nullptr, nullptr}, st, ctx->spmm_variant, ctx->side, ctx->fork, ctx->join);
+        spmm(SpmmArgs{&A, Q, B, ld, l, nullptr, nullptr, nullptr}, st, ctx->spmm_variant, ctx->side,
+             ctx->fork, ctx->join, partial_for(ctx, A, ld));
         EigSvdOut eo{W, sv, inv_s};
         eig_svd_factors(ctx, B, m, l, ld, eo, ctrl, nullptr, nullptr);
         raise_device_status(read_control(ctx, ctrl));
@@ -968,7 +1030,8 @@ int dsvd_spmm_shift(dsvd_ctx* ctx, int64_t rows, int64_t cols, int64_t nnz, cons
             colmajor_to_rowmajor(qc, rows, l, Qd, ld, st);
             DSVD_CUDA_CHECK(cudaMemcpyAsync(d_alpha, &alpha, sizeof(double), cudaMemcpyHostToDevice, st));
         }
-        spmm(SpmmArgs{&a, X, Yd, ld, l, Qd, Qd ? d_alpha : nullptr, nullptr}, st, ctx->spmm_variant, ctx->side, ctx->fork, ctx->join);
+        spmm(SpmmArgs{&a, X, Yd, ld, l, Qd, Qd ? d_alpha : nullptr, nullptr}, st, ctx->spmm_variant, ctx->side, ctx->fork, ctx->join,
+             partial_for(ctx, a, ld));
         rowmajor_to_colmajor(Yd, rows, l, ld, xc, st);
         DSVD_CUDA_CHECK(cudaMemcpyAsync(y, xc, sizeof(double) * rows * l, cudaMemcpyDeviceToHost, st));
         DSVD_CUDA_CHECK(cudaStreamSynchronize(st));

@@ -30,59 +30,77 @@ __device__ __forceinline__ double2 ld_x(const double* p) {
     return __ldg(reinterpret_cast<const double2*>(p));
 }
 
-// One warp = one (row, slab) item. Lanes own two adjacent columns each.
-template <bool kShift>
+// One warp = one (row, slab) item. Lanes own two adjacent columns each. Per
+// 32-nonzero batch the warp issues all 32 X-row gathers before the first FMA
+// and fetches the next batch's (index, value) pairs at the same time, so a
+// warp has ~32 128-bit loads in flight instead of waiting on each group.
+// kChunk: the item is a CSR range [chunk_p0, chunk_p1) of a split row and the
+// result goes to row `rpos` of `partial` (no shift; added in the combine).
+template <bool kShift, bool kChunk>
 __global__ void __launch_bounds__(256)
-spmm_rowslab_kernel(const int64_t* __restrict__ off, const int32_t* __restrict__ idx,
-                    const double* __restrict__ val, const int32_t* __restrict__ order,
-                    int64_t row_start, int64_t rows, int nslab, const double* __restrict__ x,
-                    double* __restrict__ y, int64_t ld, const double* __restrict__ q,
-                    const double* __restrict__ alpha_p, const int32_t* __restrict__ gate) {
+spmm_bulk_kernel(const int64_t* __restrict__ off, const int32_t* __restrict__ idx,
+                 const double* __restrict__ val, const int32_t* __restrict__ order,
+                 int64_t row_start, int64_t rows, int nslab, const double* __restrict__ x,
+                 double* __restrict__ y, int64_t ld, const double* __restrict__ q,
+                 const double* __restrict__ alpha_p, const int32_t* __restrict__ gate,
+                 const int64_t* __restrict__ chunk_p0, const int64_t* __restrict__ chunk_p1) {
     if (gate != nullptr && *gate != 0) return;
     const int lane = threadIdx.x & 31;
     const int64_t item = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
     if (item >= (rows - row_start) * nslab) return;
     const int64_t rpos = row_start + item / nslab;
     const int slab = static_cast<int>(item % nslab);
-    const int64_t row = order != nullptr ? static_cast<int64_t>(order[rpos]) : rpos;
+    int64_t row, beg, end;
+    if (kChunk) {
+        row = rpos;
+        beg = chunk_p0[rpos];
+        end = chunk_p1[rpos];
+    } else {
+        row = static_cast<int64_t>(order[rpos]);
+        beg = off[row];
+        end = off[row + 1];
+    }
     const int64_t col = static_cast<int64_t>(slab) * kSlab + 2 * lane;
     const bool active = col < ld;  // ld is a multiple of 4, so col+1 < ld as well
-    const int64_t beg = off[row], end = off[row + 1];
     const double* xc = x + (active ? col : 0);
 
     double a0 = 0.0, a1 = 0.0;
+    int c = 0;
+    double v = 0.0;
+    if (beg + lane < end) {
+        c = __ldg(idx + beg + lane);
+        v = __ldg(val + beg + lane);
+    }
     for (int64_t p0 = beg; p0 < end; p0 += 32) {
         const int cnt = static_cast<int>(end - p0 < 32 ? end - p0 : 32);
-        int c = 0;
-        double v = 0.0;
-        if (lane < cnt) {
-            c = __ldg(idx + p0 + lane);
-            v = __ldg(val + p0 + lane);
+        int cn = 0;
+        double vn = 0.0;
+        if (p0 + 32 + lane < end) {  // next batch, in flight during this one
+            cn = __ldg(idx + p0 + 32 + lane);
+            vn = __ldg(val + p0 + 32 + lane);
         }
-        if (cnt == 32) {
-#pragma unroll 8
-            for (int j = 0; j < 32; ++j) {
-                const int cj = __shfl_sync(kFull, c, j);
-                const double vj = __shfl_sync(kFull, v, j);
-                if (active) {
-                    const double2 xv = ld_x(xc + static_cast<int64_t>(cj) * ld);
-                    a0 = fma(vj, xv.x, a0);
-                    a1 = fma(vj, xv.y, a1);
-                }
-            }
-        } else {
-            for (int j = 0; j < cnt; ++j) {
-                const int cj = __shfl_sync(kFull, c, j);
-                const double vj = __shfl_sync(kFull, v, j);
-                if (active) {
-                    const double2 xv = ld_x(xc + static_cast<int64_t>(cj) * ld);
-                    a0 = fma(vj, xv.x, a0);
-                    a1 = fma(vj, xv.y, a1);
-                }
+        double2 xs[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+            const int cj = __shfl_sync(kFull, c, j);
+            xs[j] = (j < cnt && active) ? ld_x(xc + static_cast<int64_t>(cj) * ld) : make_double2(0.0, 0.0);
+        }
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+            const double vj = __shfl_sync(kFull, v, j);
+            if (j < cnt) {
+                a0 = fma(vj, xs[j].x, a0);
+                a1 = fma(vj, xs[j].y, a1);
             }
         }
+        c = cn;
+        v = vn;
     }
     if (!active) return;
+    if (kChunk) {
+        *reinterpret_cast<double2*>(y + rpos * ld + col) = make_double2(a0, a1);
+        return;
+    }
     if (kShift) {
         const double alpha = *alpha_p;
         if (alpha != 0.0) {  // solver.cpp:94 skips the update when alpha == 0
@@ -94,6 +112,38 @@ spmm_rowslab_kernel(const int64_t* __restrict__ off, const int32_t* __restrict__
     *reinterpret_cast<double2*>(y + row * ld + col) = make_double2(a0, a1);
 }
 
+// y(row_i, :) = sum over the row's chunks, in chunk order, of partial(chunk, :),
+// then the shift epilogue.
+template <bool kShift>
+__global__ void split_combine_kernel(const double* __restrict__ partial,
+                                     const int32_t* __restrict__ split_first,
+                                     const int32_t* __restrict__ order, int64_t nsplit,
+                                     double* __restrict__ y, int64_t ld, const double* __restrict__ q,
+                                     const double* __restrict__ alpha_p,
+                                     const int32_t* __restrict__ gate) {
+    if (gate != nullptr && *gate != 0) return;
+    const int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (e >= nsplit * ld) return;
+    const int64_t i = e / ld, col = e - (e / ld) * ld;
+    const int64_t row = order[i];
+    double acc = 0.0;
+    for (int32_t c = split_first[i]; c < split_first[i + 1]; ++c) acc += partial[c * ld + col];
+    if (kShift) {
+        const double alpha = *alpha_p;
+        if (alpha != 0.0) acc = fma(-alpha, q[row * ld + col], acc);
+    }
+    y[row * ld + col] = acc;
+}
+
+__global__ void prefix_bounds_kernel(const int32_t* __restrict__ order, const int64_t* __restrict__ off,
+                                     int64_t n, int64_t* beg, int64_t* end) {
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i < n) {
+        const int64_t r = order[i];
+        beg[i] = off[r];
+        end[i] = off[r + 1];
+    }
+}
 
 // ---- hub rows ------------------------------------------------------------------
 // One warp per (hub row, 32-column slab); one lane per column, so each lane
@@ -675,14 +725,29 @@ size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 }  // namespace
 
 void spmm(const SpmmArgs& s, cudaStream_t stream, int variant, cudaStream_t side,
-          cudaEvent_t fork, cudaEvent_t join) {
+          cudaEvent_t fork, cudaEvent_t join, double* partial) {
     const DevCsr& a = *s.a;
     if (a.rows == 0) return;
     // variant bits: low nibble selects the hub kernel; 16 skips the bulk rows,
     // 32 skips the hub rows (benchmarking the two halves separately)
     const bool skip_bulk = (variant & 16) != 0, skip_hub = (variant & 32) != 0;
     variant &= 15;
-    const int64_t hub = (side != nullptr && a.d_hub_rows != nullptr) ? a.hub_rows : 0;
+    const bool split = a.nsplit > 0 && partial != nullptr && side != nullptr;
+    const int64_t hub = (!split && side != nullptr && a.d_hub_rows != nullptr) ? a.hub_rows : 0;
+    if (split) {
+        // chunks of the long rows (longest work first) on the side stream,
+        // beside the bulk rows on the main stream; combined in chunk order
+        DSVD_CUDA_CHECK(cudaEventRecord(fork, stream));
+        DSVD_CUDA_CHECK(cudaStreamWaitEvent(side, fork, 0));
+        const int nslab64 = static_cast<int>(ceil_div(s.ld, kSlab));
+        const int64_t citems = skip_hub ? 0 : a.nchunks * nslab64;
+        if (citems > 0) {
+            spmm_bulk_kernel<false, true><<<static_cast<unsigned>(ceil_div(citems, 8)), 256, 0, side>>>(
+                a.off, a.idx, a.val, a.order, 0, a.nchunks, nslab64, s.x, partial, s.ld, nullptr, nullptr,
+                s.gate, a.chunk_p0, a.chunk_p1);
+            DSVD_LAUNCH_CHECK();
+        }
+    }
     if (hub > 0) {
         static bool attr = false;
         if (!attr) {
@@ -749,23 +814,47 @@ void spmm(const SpmmArgs& s, cudaStream_t stream, int variant, cudaStream_t side
         DSVD_LAUNCH_CHECK();
     }
     const int nslab = static_cast<int>(ceil_div(s.ld, kSlab));
-    const int64_t items = skip_bulk ? 0 : (a.rows - hub) * nslab;
+    const int warps_per_block = 8;
+    const int64_t first = split ? a.nsplit : hub;  // rows handled above / in chunks
+    const int64_t items = skip_bulk ? 0 : (a.rows - first) * nslab;
     if (items > 0) {
-        const int warps_per_block = 8;
         const int64_t blocks = ceil_div(items, warps_per_block);
         if (s.q != nullptr) {
-            spmm_rowslab_kernel<true><<<static_cast<unsigned>(blocks), 32 * warps_per_block, 0, stream>>>(
-                a.off, a.idx, a.val, a.order, hub, a.rows, nslab, s.x, s.y, s.ld, s.q, s.alpha, s.gate);
+            spmm_bulk_kernel<true, false><<<static_cast<unsigned>(blocks), 32 * warps_per_block, 0, stream>>>(
+                a.off, a.idx, a.val, a.order, first, a.rows, nslab, s.x, s.y, s.ld, s.q, s.alpha, s.gate,
+                nullptr, nullptr);
         } else {
-            spmm_rowslab_kernel<false><<<static_cast<unsigned>(blocks), 32 * warps_per_block, 0, stream>>>(
-                a.off, a.idx, a.val, a.order, hub, a.rows, nslab, s.x, s.y, s.ld, nullptr, nullptr, s.gate);
+            spmm_bulk_kernel<false, false><<<static_cast<unsigned>(blocks), 32 * warps_per_block, 0, stream>>>(
+                a.off, a.idx, a.val, a.order, first, a.rows, nslab, s.x, s.y, s.ld, nullptr, nullptr,
+                s.gate, nullptr, nullptr);
         }
         DSVD_LAUNCH_CHECK();
+    }
+    if (split) {
+        DSVD_CUDA_CHECK(cudaEventRecord(join, side));
+        DSVD_CUDA_CHECK(cudaStreamWaitEvent(stream, join, 0));
+        const int64_t n = a.nsplit * s.ld;
+        if (s.q != nullptr)
+            split_combine_kernel<true><<<static_cast<unsigned>(ceil_div(n, 256)), 256, 0, stream>>>(
+                partial, a.split_first, a.order, a.nsplit, s.y, s.ld, s.q, s.alpha, s.gate);
+        else
+            split_combine_kernel<false><<<static_cast<unsigned>(ceil_div(n, 256)), 256, 0, stream>>>(
+                partial, a.split_first, a.order, a.nsplit, s.y, s.ld, nullptr, nullptr, s.gate);
+        DSVD_LAUNCH_CHECK();
+        return;
     }
     if (hub > 0) {
         DSVD_CUDA_CHECK(cudaEventRecord(join, side));
         DSVD_CUDA_CHECK(cudaStreamWaitEvent(stream, join, 0));
     }
+}
+
+void prefix_row_bounds(const DevCsr& m, int64_t n, int64_t* d_beg, int64_t* d_end,
+                       cudaStream_t stream) {
+    if (n == 0) return;
+    prefix_bounds_kernel<<<static_cast<unsigned>(ceil_div(n, 256)), 256, 0, stream>>>(m.order, m.off, n,
+                                                                                    d_beg, d_end);
+    DSVD_LAUNCH_CHECK();
 }
 
 void narrow_indices(const int64_t* src, int32_t* dst, int64_t nnz, int64_t cols, int32_t* bad,

@@ -21,6 +21,17 @@ struct DevCsr {
     int64_t hub_rows = 0;
     int64_t hub_threshold = 0;
     int32_t* d_hub_rows = nullptr;  // device copy written by build_row_order
+    // Split mode (split_chunk > 0): rows order[0 .. nsplit) hold more than
+    // split_chunk nonzeros and are cut into nchunks CSR ranges of at most
+    // split_chunk nonzeros; each chunk's FMA chain goes to a partial row and the
+    // partials of a row are summed in chunk order (deterministic, not the
+    // reference's single chain). split_chunk == 0 keeps every chain whole
+    // (bit-exact, hub rows take the hub kernel).
+    int64_t split_chunk = 0;
+    int64_t nsplit = 0, nchunks = 0;
+    int64_t* chunk_p0 = nullptr;     // nchunks: first nonzero of the chunk
+    int64_t* chunk_p1 = nullptr;     // nchunks: one past the last nonzero
+    int32_t* split_first = nullptr;  // nsplit+1: chunk range of split row i
 };
 
 // SpMM launch description. X and Y (and Q) are row-major with row stride ld.
@@ -38,7 +49,12 @@ struct SpmmArgs {
 // Launches the hub-row kernel on `side` (when the matrix has hub rows) and the
 // kernel for all other rows on `stream`; `fork`/`join` order the two streams.
 void spmm(const SpmmArgs& args, cudaStream_t stream, int variant, cudaStream_t side = nullptr,
-          cudaEvent_t fork = nullptr, cudaEvent_t join = nullptr);
+          cudaEvent_t fork = nullptr, cudaEvent_t join = nullptr, double* partial = nullptr);
+
+// Row bounds (offsets) of the first n rows of m.order, for the host-side
+// construction of the split chunk list.
+void prefix_row_bounds(const DevCsr& m, int64_t n, int64_t* d_beg, int64_t* d_end,
+                       cudaStream_t stream);
 
 // CSR(A^T) from CSR(A), bitwise equal to the reference transpose().
 // Temporaries come from `scratch` (bytes given by csc_scratch_bytes).

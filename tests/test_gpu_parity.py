@@ -130,12 +130,54 @@ def test_spmm_shift_bitwise(dev, oracle, c1, alpha):
     assert_bitwise(t, t_ref)
 
 
-def test_spmm_power_law_long_rows_bitwise(dev, oracle):
+def test_spmm_power_law_long_rows_bitwise(oracle):
+    dv = d.Device(0)
+    dv.set_option("split_chunk", 0)  # whole chains: bit-exact
     a = d.powerlaw(4000, 2000, 3.5, 1.0, 1.1, 8)
     ca = Csr(a.rows, a.cols, a.offsets, a.col_indices, a.values)
     at = transpose_np(ca)
     x = np.asfortranarray(np.random.default_rng(1).standard_normal((ca.rows, 150)))
-    assert_bitwise(d.spmm(to_dev(at), x, device=dev), oracle.spmm(at, x))
+    assert_bitwise(d.spmm(to_dev(at), x, device=dv), oracle.spmm(at, x))
+
+
+@pytest.mark.parametrize("chunk", [7, 32, 100, 2048])
+@pytest.mark.parametrize("l", [1, 75, 150])
+def test_spmm_split_rows_match(oracle, chunk, l):
+    """Split mode: long rows as chunk partials summed in chunk order. Not the
+    reference's single chain, so checked against the rounding-error scale
+    (|A| |X|) rather than bitwise."""
+    dv = d.Device(0)
+    dv.set_option("split_chunk", chunk)
+    a = d.powerlaw(6000, 2500, 3.5, 1.0, 1.1, 21)
+    ca = Csr(a.rows, a.cols, a.offsets, a.col_indices, a.values)
+    at = transpose_np(ca)
+    rng = np.random.default_rng(chunk + l)
+    for m, x in ((ca, rng.standard_normal((ca.cols, l))), (at, rng.standard_normal((ca.rows, l)))):
+        x = np.asfortranarray(x)
+        y_ref = oracle.spmm(m, x)
+        scale = oracle.spmm(Csr(m.rows, m.cols, m.offsets, m.col_indices, np.abs(m.values)),
+                            np.asfortranarray(np.abs(x)))
+        y = d.spmm(to_dev(m), x, device=dv)
+        assert np.all(np.abs(y - y_ref) <= 1e-13 * scale + 1e-300)
+        q = np.asfortranarray(rng.standard_normal((m.rows, l)))
+        t = d.spmm_shift(to_dev(m), x, 0.25, q, device=dv)
+        t_ref = oracle.add_scaled(y_ref, -0.25, q)
+        assert np.all(np.abs(t - t_ref) <= 1e-13 * (scale + 0.25 * np.abs(q)) + 1e-300)
+        # rows that were not split keep their exact chains
+        short = np.diff(m.offsets) <= chunk
+        assert_bitwise(y[short], y_ref[short])
+
+
+def test_solve_power_law_split_vs_bitwise(oracle):
+    a = d.powerlaw(8000, 3000, 3.5, 1.0, 1.1, 4)
+    ca = Csr(a.rows, a.cols, a.offsets, a.col_indices, a.values)
+    ref = oracle.solve(ca, 20, 10, p=6, alg="shifted", seed=1)
+    cfg = d.SolverConfig(k=20, s=10, p=6, alg=d.Algorithm.shifted, seed=1)
+    for chunk in (0, 64):
+        dv = d.Device(0)
+        dv.set_option("split_chunk", chunk)
+        res = d.solve(a, cfg, device=dv)
+        check_solve(res, ref, 20)
 
 
 @pytest.fixture()
@@ -143,6 +185,7 @@ def hub_dev():
     """A context whose SpMM sends every row with >= threshold nonzeros down the
     hub (cp.async ring) path, so small matrices exercise it."""
     dv = d.Device(0)
+    dv.set_option("split_chunk", 0)
     yield dv
     dv.close()
 
