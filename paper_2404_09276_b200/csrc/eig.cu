@@ -234,10 +234,28 @@ __device__ __forceinline__ void cl_sync() {
                      : "memory");
 }
 
+__device__ __forceinline__ void cl_expect_tx_remote(unsigned addr, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.release.cluster.shared::cluster.b64 _, [%0], %1;\n" ::"r"(addr),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void cl_bulk_copy(unsigned remote_dst, const void* local_src, unsigned bytes,
+                                             unsigned remote_bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+            remote_dst),
+        "r"(s_u32(local_src)), "r"(bytes), "r"(remote_bar)
+        : "memory");
+}
+
+// Shared memory of each CTA: M (lp x lds, lds = lp + 1 odd so row and column
+// strides hit distinct banks), the rotation ring (payload per round: half
+// (c, s) pairs + a header {continue?, 0}), the local staging ring of CTA 0,
+// mbarriers, and the block table.
 size_t cluster_smem_bytes(int lp) {
-    const size_t half = lp / 2;
-    return sizeof(double) * lp * lp + sizeof(double2) * kClRing * half + 2 * kClRing * sizeof(uint64_t) +
-           kClRing * sizeof(int) + sizeof(uint16_t) * half * (half + 1) / 2 + 64;
+    const size_t half = lp / 2, lds = lp + 1;
+    return sizeof(double) * lp * lds + 2 * sizeof(double2) * kClRing * (half + 1) +
+           2 * kClRing * sizeof(uint64_t) + sizeof(uint16_t) * half * (half + 1) / 2 + 128;
 }
 
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kEigThreads, 1)
@@ -250,18 +268,20 @@ jacobi_cluster_kernel(const double* __restrict__ g_in, int l, int lp, int max_sw
     __shared__ double cs_c[kMaxPairs], cs_s[kMaxPairs], cs_t[kMaxPairs];
     __shared__ int pp[kMaxPairs], qq[kMaxPairs];
     __shared__ int rotated;
-    const int half = lp / 2;
-    double* M = cl_smem;                                               // G (rank 0) or V (rank 1)
-    double2* ring = reinterpret_cast<double2*>(M + lp * lp);           // [kClRing][half] (rank 1)
-    uint64_t* full = reinterpret_cast<uint64_t*>(ring + kClRing * half);  // rank 1
-    uint64_t* empty = full + kClRing;                                  // rank 0
-    int* ctrlw = reinterpret_cast<int*>(empty + kClRing);              // rank 1
-    uint16_t* blk = reinterpret_cast<uint16_t*>(ctrlw + kClRing);      // rank 0
+    const int half = lp / 2, lds = lp + 1;
+    const int pay = half + 1;                                           // double2 per round
+    double* M = cl_smem;                                                // G (rank 0) or V (rank 1)
+    double2* ring = reinterpret_cast<double2*>(M + ((lp * lds + 1) & ~1));  // [kClRing][pay] (rank 1)
+    double2* stage = ring + kClRing * pay;                              // [kClRing][pay] (rank 0)
+    uint64_t* full = reinterpret_cast<uint64_t*>(stage + kClRing * pay);  // rank 1
+    uint64_t* empty = full + kClRing;                                   // rank 0
+    uint16_t* blk = reinterpret_cast<uint16_t*>(empty + kClRing);       // rank 0
     const unsigned rank = cl_rank();
     const int tid = threadIdx.x;
+    const unsigned pay_bytes = static_cast<unsigned>(sizeof(double2) * pay);
     if (tid == 0) {
         for (int sl = 0; sl < kClRing; ++sl) {
-            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(s_u32(&full[sl])), "r"(half));
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(s_u32(&full[sl])), "r"(1));
             asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(s_u32(&empty[sl])), "r"(1));
         }
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
@@ -272,13 +292,22 @@ jacobi_cluster_kernel(const double* __restrict__ g_in, int l, int lp, int max_sw
         const int nblocks = half * (half + 1) / 2;
         for (int e = tid; e < lp * lp; e += blockDim.x) {
             const int i = e / lp, j = e % lp;
-            M[e] = (i < l && j < l) ? g_in[i * l + j] : 0.0;
+            M[i * lds + j] = (i < l && j < l) ? g_in[i * l + j] : 0.0;
         }
         for (int kp = tid; kp < half; kp += blockDim.x) {
             const int base = kp * half - kp * (kp - 1) / 2;
             for (int kr = kp; kr < half; ++kr) blk[base + (kr - kp)] = static_cast<uint16_t>((kp << 8) | kr);
         }
         __syncthreads();
+        // hand round rg's payload (already in stage[sl]) to the V-CTA
+        auto send = [&](int64_t rg) {
+            const int sl = static_cast<int>(rg % kClRing);
+            cl_wait(&empty[sl], static_cast<unsigned>(((rg / kClRing) & 1) ^ 1));
+            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+            const unsigned bar = cl_map(&full[sl], 1);
+            cl_expect_tx_remote(bar, pay_bytes);
+            cl_bulk_copy(cl_map(&ring[sl * pay], 1), &stage[sl * pay], pay_bytes, bar);
+        };
         int64_t rg = 0;
         int sweep = 0;
         bool converged = false;
@@ -287,10 +316,17 @@ jacobi_cluster_kernel(const double* __restrict__ g_in, int l, int lp, int max_sw
             __syncthreads();
             for (int round = 0; round < lp - 1; ++round, ++rg) {
                 const int sl = static_cast<int>(rg % kClRing);
+                if (tid == 0) {
+                    // the staging slot is reusable once the V-CTA released it
+                    cl_wait(&empty[sl], static_cast<unsigned>(((rg / kClRing) & 1) ^ 1));
+                    stage[sl * pay + half] = make_double2(1.0, 0.0);  // header: continue
+                    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+                }
+                __syncthreads();
                 for (int k = tid; k < half; k += blockDim.x) {
                     int p, q;
                     pair_of(round, k, lp, p, q);
-                    const double a = M[p * lp + p], d = M[q * lp + q], b = M[p * lp + q];
+                    const double a = M[p * lds + p], d = M[q * lds + q], b = M[p * lds + q];
                     double c = 1.0, s = 0.0, t = 0.0;
                     if (fabs(b) > kJacobiTol * sqrt(fabs(a)) * sqrt(fabs(d)) && fabs(b) > 1e-300) {
                         const double theta = (d - a) / (2.0 * b);
@@ -308,13 +344,12 @@ jacobi_cluster_kernel(const double* __restrict__ g_in, int l, int lp, int max_sw
                     cs_t[k] = t;
                     pp[k] = p;
                     qq[k] = q;
-                    // hand the rotation to the V-CTA
-                    cl_wait(&empty[sl], static_cast<unsigned>(((rg / kClRing) & 1) ^ 1));
-                    cl_st_v2(cl_map(&ring[sl * half + k], 1), c, s);
-                    if (k == 0) cl_st_s32(cl_map(&ctrlw[sl], 1), 1);
-                    cl_arrive(cl_map(&full[sl], 1));
+                    stage[sl * pay + k] = make_double2(c, s);
+                    // make the generic-proxy writes visible to the bulk copy (async proxy)
+                    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
                 }
                 __syncthreads();
+                if (tid == 0) send(rg);
                 for (int e = tid; e < nblocks; e += blockDim.x) {
                     const int code = blk[e];
                     const int kp = code >> 8, kr = code & 0xff;
@@ -323,47 +358,44 @@ jacobi_cluster_kernel(const double* __restrict__ g_in, int l, int lp, int max_sw
                     if (kp == kr) {
                         if (s1 != 0.0) {
                             const double t = cs_t[kp];
-                            const double b = M[p * lp + q];
-                            M[p * lp + p] -= t * b;
-                            M[q * lp + q] += t * b;
-                            M[p * lp + q] = 0.0;
-                            M[q * lp + p] = 0.0;
+                            const double b = M[p * lds + q];
+                            M[p * lds + p] -= t * b;
+                            M[q * lds + q] += t * b;
+                            M[p * lds + q] = 0.0;
+                            M[q * lds + p] = 0.0;
                         }
                         continue;
                     }
                     if (s1 == 0.0 && s2 == 0.0) continue;
                     const double c1 = cs_c[kp], c2 = cs_c[kr];
                     const int r = pp[kr], s = qq[kr];
-                    const double xpr = M[p * lp + r], xps = M[p * lp + s];
-                    const double xqr = M[q * lp + r], xqs = M[q * lp + s];
+                    const double xpr = M[p * lds + r], xps = M[p * lds + s];
+                    const double xqr = M[q * lds + r], xqs = M[q * lds + s];
                     const double ypr = c2 * xpr - s2 * xps, yps = s2 * xpr + c2 * xps;
                     const double yqr = c2 * xqr - s2 * xqs, yqs = s2 * xqr + c2 * xqs;
                     const double zpr = c1 * ypr - s1 * yqr, zqr = s1 * ypr + c1 * yqr;
                     const double zps = c1 * yps - s1 * yqs, zqs = s1 * yps + c1 * yqs;
-                    M[p * lp + r] = zpr;
-                    M[r * lp + p] = zpr;
-                    M[p * lp + s] = zps;
-                    M[s * lp + p] = zps;
-                    M[q * lp + r] = zqr;
-                    M[r * lp + q] = zqr;
-                    M[q * lp + s] = zqs;
-                    M[s * lp + q] = zqs;
+                    M[p * lds + r] = zpr;
+                    M[r * lds + p] = zpr;
+                    M[p * lds + s] = zps;
+                    M[s * lds + p] = zps;
+                    M[q * lds + r] = zqr;
+                    M[r * lds + q] = zqr;
+                    M[q * lds + s] = zqs;
+                    M[s * lds + q] = zqs;
                 }
                 __syncthreads();
             }
             converged = rotated == 0;
             __syncthreads();
         }
-        // stop marker for the V-CTA
-        {
+        if (tid == 0) {  // stop marker
             const int sl = static_cast<int>(rg % kClRing);
-            for (int k = tid; k < half; k += blockDim.x) {
-                cl_wait(&empty[sl], static_cast<unsigned>(((rg / kClRing) & 1) ^ 1));
-                if (k == 0) cl_st_s32(cl_map(&ctrlw[sl], 1), 0);
-                cl_arrive(cl_map(&full[sl], 1));
-            }
+            cl_wait(&empty[sl], static_cast<unsigned>(((rg / kClRing) & 1) ^ 1));
+            stage[sl * pay + half] = make_double2(0.0, 0.0);
+            send(rg);
         }
-        for (int i = tid; i < lp; i += blockDim.x) lam[i] = M[i * lp + i];
+        for (int i = tid; i < lp; i += blockDim.x) lam[i] = M[i * lds + i];
         if (tid == 0) {
             ctrl->eig_sweeps = sweep;
             ctrl->total_sweeps += sweep;
@@ -373,36 +405,41 @@ jacobi_cluster_kernel(const double* __restrict__ g_in, int l, int lp, int max_sw
             }
         }
     } else {
-        for (int e = tid; e < lp * lp; e += blockDim.x) M[e] = (e / lp == e % lp) ? 1.0 : 0.0;
+        for (int e = tid; e < lp * lp; e += blockDim.x) {
+            const int i = e / lp, j = e % lp;
+            M[i * lds + j] = (i == j) ? 1.0 : 0.0;
+        }
         __syncthreads();
+        const int groups = blockDim.x / half;  // row groups (>= 1: half <= 82 here)
+        const int k = tid % half, grp = tid / half;
+        const int rows_per = (lp + groups - 1) / groups;
         for (int64_t rg = 0;; ++rg) {
             const int sl = static_cast<int>(rg % kClRing);
             cl_wait(&full[sl], static_cast<unsigned>((rg / kClRing) & 1));
-            if (ctrlw[sl] == 0) break;
+            const double2* rot = ring + sl * pay;
+            if (rot[half].x == 0.0) break;
             const int round = static_cast<int>(rg % (lp - 1));
-            const double2* rot = ring + sl * half;
-            // thread -> (pair k, block of rows): the rotation is loaded once and
-            // applied to a strip of rows (no per-element index arithmetic)
-            const int groups = blockDim.x / half;  // row groups (>= 1: half <= 82 here)
-            const int k = tid % half, grp = tid / half;
+            // thread -> (pair k, strip of rows): one rotation, several rows
             if (grp < groups) {
                 const double2 cs = rot[k];
                 if (cs.y != 0.0) {
                     int p, q;
                     pair_of(round, k, lp, p, q);
-                    const int rows_per = (lp + groups - 1) / groups;
                     const int r0 = grp * rows_per, r1 = min(lp, r0 + rows_per);
                     for (int r = r0; r < r1; ++r) {
-                        const double vp = M[r * lp + p], vq = M[r * lp + q];
-                        M[r * lp + p] = cs.x * vp - cs.y * vq;
-                        M[r * lp + q] = cs.y * vp + cs.x * vq;
+                        const double vp = M[r * lds + p], vq = M[r * lds + q];
+                        M[r * lds + p] = cs.x * vp - cs.y * vq;
+                        M[r * lds + q] = cs.y * vp + cs.x * vq;
                     }
                 }
             }
             __syncthreads();
             if (tid == 0) cl_arrive(cl_map(&empty[sl], 0));
         }
-        for (int e = tid; e < lp * lp; e += blockDim.x) vecs[e] = M[e];
+        for (int e = tid; e < lp * lp; e += blockDim.x) {
+            const int i = e / lp, j = e % lp;
+            vecs[e] = M[i * lds + j];
+        }
     }
     cl_sync();  // keep both CTAs' shared memory alive until all remote traffic is done
 }

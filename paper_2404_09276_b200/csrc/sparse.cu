@@ -30,10 +30,10 @@ __device__ __forceinline__ double2 ld_x(const double* p) {
     return __ldg(reinterpret_cast<const double2*>(p));
 }
 
-// One warp = one (row, slab) item. Lanes own two adjacent columns each. Per
-// 32-nonzero batch the warp issues all 32 X-row gathers before the first FMA
-// and fetches the next batch's (index, value) pairs at the same time, so a
-// warp has ~32 128-bit loads in flight instead of waiting on each group.
+// One warp = one (row, slab) item. Lanes own two adjacent columns each; the
+// next batch's (index, value) pairs are fetched while the current batch's
+// gathers run. Bulk throughput is bound by random 512-byte gathers
+// (tools/micro/gather_bw.cu), hence the slab-major order below.
 // kChunk: the item is a CSR range [chunk_p0, chunk_p1) of a split row and the
 // result goes to row `rpos` of `partial` (no shift; added in the combine).
 template <bool kShift, bool kChunk>
@@ -46,10 +46,13 @@ spmm_bulk_kernel(const int64_t* __restrict__ off, const int32_t* __restrict__ id
                  const int64_t* __restrict__ chunk_p0, const int64_t* __restrict__ chunk_p1) {
     if (gate != nullptr && *gate != 0) return;
     const int lane = threadIdx.x & 31;
+    // slab-major order: all rows' first 64 columns, then the next 64, ... so
+    // the X columns being gathered (rows x 512 B) stay resident in L2
+    const int64_t nrows = rows - row_start;
     const int64_t item = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    if (item >= (rows - row_start) * nslab) return;
-    const int64_t rpos = row_start + item / nslab;
-    const int slab = static_cast<int>(item % nslab);
+    if (item >= nrows * nslab) return;
+    const int slab = static_cast<int>(item / nrows);
+    const int64_t rpos = row_start + item % nrows;
     int64_t row, beg, end;
     if (kChunk) {
         row = rpos;
@@ -75,22 +78,30 @@ spmm_bulk_kernel(const int64_t* __restrict__ off, const int32_t* __restrict__ id
         const int cnt = static_cast<int>(end - p0 < 32 ? end - p0 : 32);
         int cn = 0;
         double vn = 0.0;
-        if (p0 + 32 + lane < end) {  // next batch, in flight during this one
+        if (p0 + 32 + lane < end) {  // next batch's pairs, in flight during this one
             cn = __ldg(idx + p0 + 32 + lane);
             vn = __ldg(val + p0 + 32 + lane);
         }
-        double2 xs[32];
-#pragma unroll
-        for (int j = 0; j < 32; ++j) {
-            const int cj = __shfl_sync(kFull, c, j);
-            xs[j] = (j < cnt && active) ? ld_x(xc + static_cast<int64_t>(cj) * ld) : make_double2(0.0, 0.0);
-        }
-#pragma unroll
-        for (int j = 0; j < 32; ++j) {
-            const double vj = __shfl_sync(kFull, v, j);
-            if (j < cnt) {
-                a0 = fma(vj, xs[j].x, a0);
-                a1 = fma(vj, xs[j].y, a1);
+        if (cnt == 32) {
+#pragma unroll 8
+            for (int j = 0; j < 32; ++j) {
+                const int cj = __shfl_sync(kFull, c, j);
+                const double vj = __shfl_sync(kFull, v, j);
+                if (active) {
+                    const double2 xv = ld_x(xc + static_cast<int64_t>(cj) * ld);
+                    a0 = fma(vj, xv.x, a0);
+                    a1 = fma(vj, xv.y, a1);
+                }
+            }
+        } else {
+            for (int j = 0; j < cnt; ++j) {
+                const int cj = __shfl_sync(kFull, c, j);
+                const double vj = __shfl_sync(kFull, v, j);
+                if (active) {
+                    const double2 xv = ld_x(xc + static_cast<int64_t>(cj) * ld);
+                    a0 = fma(vj, xv.x, a0);
+                    a1 = fma(vj, xv.y, a1);
+                }
             }
         }
         c = cn;
