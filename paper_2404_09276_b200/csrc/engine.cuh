@@ -48,7 +48,7 @@ struct dsvd_ctx {
     int64_t hub_threshold = 4096;   // rows with >= this many nonzeros take the hub SpMM path
     // rows longer than split_chunk nonzeros are computed as chunk partials summed
     // in a fixed order (deterministic; 0 = whole chains, bit-exact vs reference)
-    int64_t split_chunk = 2048;
+    int64_t split_chunk = 512;
     cudaStream_t side = nullptr;    // second stream: hub-row SpMM runs beside the bulk kernel
     cudaEvent_t fork = nullptr, join = nullptr;
     int32_t* host_flags = nullptr;  // pinned ring for stop flags
