@@ -200,6 +200,196 @@ __global__ void rm_to_cm_kernel(const double* __restrict__ src, int64_t rows, in
     }
 }
 
+
+// ---- register-tiled kernels (8x8 accumulators per thread) -----------------------------
+// Gram v2: one block per row chunk computes the whole upper triangle of its
+// chunk's C^T C; thread t owns one 8x8 tile (ti <= tj) in registers, C rows
+// are staged 8 at a time in shared memory (double buffered with cp.async),
+// a (8 values, shared by most lanes of a warp -> broadcast) and b (8 values)
+// give 64 DFMA per 16 loads. Chunk partials are reduced in a fixed order.
+constexpr int kG2Rows = 8;        // rows per stage
+constexpr int kG2MaxTiles = 1024; // tile pairs per block (l_pad8 <= 8*44)
+
+__device__ __forceinline__ void cpa16(void* dst, const void* src) {
+    const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(src));
+}
+__device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cpa_wait1() { asm volatile("cp.async.wait_group 1;\n" ::); }
+__device__ __forceinline__ void cpa_wait0() { asm volatile("cp.async.wait_group 0;\n" ::); }
+
+__global__ void __launch_bounds__(256)
+gram2_kernel(const double* __restrict__ c, int64_t n, int64_t ld, int lp8, int ntile,
+             int64_t rows_per_block, double* __restrict__ partial, const int32_t* __restrict__ gate) {
+    if (gate != nullptr && *gate != 0) return;
+    extern __shared__ __align__(16) double g2s[];  // [2][kG2Rows][lp8]
+    const int npair = ntile * (ntile + 1) / 2;
+    // tile pair of this thread (row-major over ti <= tj)
+    int ti = 0, rem = threadIdx.x;
+    while (ti < ntile && rem >= ntile - ti) {
+        rem -= ntile - ti;
+        ++ti;
+    }
+    const int tj = ti + rem;
+    const bool owner = threadIdx.x < npair;
+    const int64_t r_beg = static_cast<int64_t>(blockIdx.x) * rows_per_block;
+    const int64_t r_end = min(n, r_beg + rows_per_block);
+    double acc[8][8];
+#pragma unroll
+    for (int a = 0; a < 8; ++a)
+#pragma unroll
+        for (int b = 0; b < 8; ++b) acc[a][b] = 0.0;
+    const int vec_per_row = static_cast<int>(ld / 2);  // 16-byte vectors per row
+    auto stage = [&](int buf, int64_t r0) {
+        double* dst = g2s + buf * kG2Rows * lp8;
+        for (int e = threadIdx.x; e < kG2Rows * (lp8 / 2); e += blockDim.x) {
+            const int rr = e / (lp8 / 2), v = e % (lp8 / 2);
+            const int64_t r = r0 + rr;
+            if (r < r_end && v < vec_per_row)
+                cpa16(dst + rr * lp8 + 2 * v, c + r * ld + 2 * v);
+            else
+                *reinterpret_cast<double2*>(dst + rr * lp8 + 2 * v) = make_double2(0.0, 0.0);
+        }
+    };
+    if (r_beg < r_end) stage(0, r_beg);
+    cpa_commit();
+    int buf = 0;
+    for (int64_t r0 = r_beg; r0 < r_end; r0 += kG2Rows) {
+        if (r0 + kG2Rows < r_end) stage(buf ^ 1, r0 + kG2Rows);
+        cpa_commit();
+        cpa_wait1();
+        __syncthreads();
+        if (owner) {
+            const double* cs = g2s + buf * kG2Rows * lp8;
+#pragma unroll
+            for (int k = 0; k < kG2Rows; ++k) {
+                double av[8], bv[8];
+                const double2* ap = reinterpret_cast<const double2*>(cs + k * lp8 + 8 * ti);
+                const double2* bp = reinterpret_cast<const double2*>(cs + k * lp8 + 8 * tj);
+#pragma unroll
+                for (int h = 0; h < 4; ++h) {
+                    const double2 x = ap[h], y = bp[h];
+                    av[2 * h] = x.x;
+                    av[2 * h + 1] = x.y;
+                    bv[2 * h] = y.x;
+                    bv[2 * h + 1] = y.y;
+                }
+#pragma unroll
+                for (int a = 0; a < 8; ++a)
+#pragma unroll
+                    for (int b = 0; b < 8; ++b) acc[a][b] = fma(av[a], bv[b], acc[a][b]);
+            }
+        }
+        __syncthreads();
+        buf ^= 1;
+    }
+    cpa_wait0();
+    if (owner) {
+        double* out = partial + (static_cast<int64_t>(blockIdx.x) * npair + threadIdx.x) * 64;
+#pragma unroll
+        for (int a = 0; a < 8; ++a)
+#pragma unroll
+            for (int b = 0; b < 8; b += 2)
+                *reinterpret_cast<double2*>(out + a * 8 + b) = make_double2(acc[a][b], acc[a][b + 1]);
+    }
+}
+
+// G(i, j) = G(j, i) = sum over blocks (fixed order) of the tile entry; one thread per upper entry.
+__global__ void gram2_reduce_kernel(const double* __restrict__ partial, int nblk, int ntile,
+                                    int64_t l, double* __restrict__ g, const int32_t* __restrict__ gate) {
+    if (gate != nullptr && *gate != 0) return;
+    const int npair = ntile * (ntile + 1) / 2;
+    const int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (e >= static_cast<int64_t>(npair) * 64) return;
+    const int t = static_cast<int>(e / 64), w = static_cast<int>(e % 64);
+    int ti = 0, rem = t;
+    while (rem >= ntile - ti) {
+        rem -= ntile - ti;
+        ++ti;
+    }
+    const int tj = ti + rem;
+    const int64_t i = 8 * ti + w / 8, j = 8 * tj + w % 8;
+    if (i >= l || j >= l || i > j) return;
+    double s = 0.0;
+    for (int b = 0; b < nblk; ++b) s += partial[(static_cast<int64_t>(b) * npair + t) * 64 + w];
+    g[i * l + j] = s;
+    g[j * l + i] = s;
+}
+
+// Rescale v2: out(r, j) = (sum_t c(r,t) w(t,j)) * scale[j], t ascending from 0.0
+// (bitwise the reference matmul order). Block = 64 rows x all ncol columns;
+// thread owns an 8x8 output tile; C (transposed) and W are staged 8 t at a time.
+constexpr int kR2Rows = 64;
+constexpr int kR2K = 8;
+
+__global__ void __launch_bounds__(256)
+rescale2_kernel(const double* __restrict__ c, int64_t n, int64_t K, int64_t ldc,
+                const double* __restrict__ w, int64_t ldw, const double* __restrict__ scale,
+                int64_t ncol, int np8, double* __restrict__ out, int64_t ld_out, int out_colmajor,
+                const int32_t* __restrict__ gate) {
+    if (gate != nullptr && *gate != 0) return;
+    extern __shared__ __align__(16) double r2s[];
+    double* As = r2s;                       // [kR2K][kR2Rows]   (transposed C tile)
+    double* Ws = r2s + kR2K * kR2Rows;      // [kR2K][np8]
+    const int ntc = np8 / 8;                // column tiles
+    const int tr = threadIdx.x / ntc, tc = threadIdx.x % ntc;  // 8 row tiles x ntc col tiles
+    const bool owner = tr < kR2Rows / 8;
+    const int64_t r0 = static_cast<int64_t>(blockIdx.x) * kR2Rows;
+    double acc[8][8];
+#pragma unroll
+    for (int a = 0; a < 8; ++a)
+#pragma unroll
+        for (int b = 0; b < 8; ++b) acc[a][b] = 0.0;
+    for (int64_t t0 = 0; t0 < K; t0 += kR2K) {
+        const int kmax = static_cast<int>(K - t0 < kR2K ? K - t0 : kR2K);
+        for (int e = threadIdx.x; e < kR2K * kR2Rows; e += blockDim.x) {
+            const int rr = e / kR2K, kk = e % kR2K;
+            const int64_t r = r0 + rr;
+            As[kk * kR2Rows + rr] = (r < n && kk < kmax) ? c[r * ldc + t0 + kk] : 0.0;
+        }
+        for (int e = threadIdx.x; e < kR2K * np8; e += blockDim.x) {
+            const int kk = e / np8, jj = e % np8;
+            Ws[kk * np8 + jj] = (kk < kmax && jj < ncol) ? w[(t0 + kk) * ldw + jj] : 0.0;
+        }
+        __syncthreads();
+        if (owner) {
+            for (int kk = 0; kk < kmax; ++kk) {
+                double av[8], bv[8];
+#pragma unroll
+                for (int h = 0; h < 4; ++h) {
+                    const double2 x = reinterpret_cast<const double2*>(As + kk * kR2Rows + 8 * tr)[h];
+                    const double2 y = reinterpret_cast<const double2*>(Ws + kk * np8 + 8 * tc)[h];
+                    av[2 * h] = x.x;
+                    av[2 * h + 1] = x.y;
+                    bv[2 * h] = y.x;
+                    bv[2 * h + 1] = y.y;
+                }
+#pragma unroll
+                for (int a = 0; a < 8; ++a)
+#pragma unroll
+                    for (int b = 0; b < 8; ++b) acc[a][b] = fma(av[a], bv[b], acc[a][b]);
+            }
+        }
+        __syncthreads();
+    }
+    if (!owner) return;
+#pragma unroll
+    for (int a = 0; a < 8; ++a) {
+        const int64_t r = r0 + 8 * tr + a;
+        if (r >= n) continue;
+#pragma unroll
+        for (int b = 0; b < 8; ++b) {
+            const int64_t j = 8 * tc + b;
+            const double v = j < ncol ? (scale != nullptr ? acc[a][b] * scale[j] : acc[a][b]) : 0.0;
+            if (out_colmajor) {
+                if (j < ncol) out[j * n + r] = v;
+            } else if (j < ld_out) {
+                out[r * ld_out + j] = v;
+            }
+        }
+    }
+}
+
 int grid_for(int64_t n) {
     const int64_t g = ceil_div(n, 256);
     return static_cast<int>(g < 1 ? 1 : (g > 148 * 32 ? 148 * 32 : g));
@@ -237,15 +427,52 @@ void gram_plan(int64_t n, int64_t l, int& ntiles, int& nchunk, int64_t& rows_per
 }
 }  // namespace
 
+namespace {
+// v2 plan: lp8 = l rounded to 8, tile pairs must fit one block
+struct Gram2Plan {
+    int lp8, ntile, npair, nblk;
+    int64_t rows_per_block;
+    bool ok;
+};
+Gram2Plan gram2_plan(int64_t n, int64_t l, int64_t ld) {
+    Gram2Plan p{};
+    p.lp8 = static_cast<int>((l + 7) / 8 * 8);
+    p.ntile = p.lp8 / 8;
+    p.npair = p.ntile * (p.ntile + 1) / 2;
+    p.ok = p.npair <= kG2MaxTiles && ld % 2 == 0 && p.lp8 >= ld - 3;
+    const int64_t target = 2 * kNumSMs;
+    int64_t rpb = ceil_div(n, target);
+    rpb = std::max<int64_t>(kG2Rows, ceil_div(rpb, kG2Rows) * kG2Rows);
+    p.rows_per_block = rpb;
+    p.nblk = static_cast<int>(std::max<int64_t>(1, ceil_div(n, rpb)));
+    return p;
+}
+}  // namespace
+
 size_t gram_workspace_bytes(int64_t n, int64_t l) {
+    const Gram2Plan p2 = gram2_plan(n, l, padded_ld(l));
+    const size_t v2 = sizeof(double) * static_cast<size_t>(p2.nblk) * p2.npair * 64;
     int ntiles, nchunk;
     int64_t rpc;
     gram_plan(n, l, ntiles, nchunk, rpc);
-    return sizeof(double) * static_cast<size_t>(ntiles) * nchunk * kTile * kTile;
+    return std::max(v2, sizeof(double) * static_cast<size_t>(ntiles) * nchunk * kTile * kTile);
 }
 
 void gram(const double* c, int64_t n, int64_t l, int64_t ld, double* g, void* ws,
           size_t ws_bytes, const int32_t* gate, cudaStream_t stream) {
+    const Gram2Plan p2 = gram2_plan(n, l, ld);
+    if (p2.ok && n > 0) {
+        const size_t smem = sizeof(double) * 2 * kG2Rows * p2.lp8;
+        const int threads = std::max(64, (p2.npair + 31) / 32 * 32);
+        gram2_kernel<<<p2.nblk, threads, smem, stream>>>(c, n, ld, p2.lp8, p2.ntile, p2.rows_per_block,
+                                                         static_cast<double*>(ws), gate);
+        DSVD_LAUNCH_CHECK();
+        const int64_t ne = static_cast<int64_t>(p2.npair) * 64;
+        gram2_reduce_kernel<<<static_cast<unsigned>(ceil_div(ne, 256)), 256, 0, stream>>>(
+            static_cast<const double*>(ws), p2.nblk, p2.ntile, l, g, gate);
+        DSVD_LAUNCH_CHECK();
+        return;
+    }
     int ntiles, nchunk;
     int64_t rpc;
     gram_plan(n, l, ntiles, nchunk, rpc);
@@ -263,6 +490,15 @@ void rescale(const double* c, int64_t n, int64_t K, int64_t ldc, const double* w
              const int32_t* gate, cudaStream_t stream) {
     if (n == 0) return;
     const int64_t width = out_colmajor ? ncol : ld_out;
+    const int np8 = static_cast<int>((width + 7) / 8 * 8);
+    const int threads = (kR2Rows / 8) * (np8 / 8);
+    if (threads <= 1024 && np8 > 0) {
+        const size_t smem = sizeof(double) * kR2K * (kR2Rows + np8);
+        rescale2_kernel<<<static_cast<unsigned>(ceil_div(n, kR2Rows)), (threads + 31) / 32 * 32, smem, stream>>>(
+            c, n, K, ldc, w, ldw, scale, ncol, np8, out, ld_out, out_colmajor, gate);
+        DSVD_LAUNCH_CHECK();
+        return;
+    }
     dim3 grid(static_cast<unsigned>(ceil_div(n, kTile)), static_cast<unsigned>(ceil_div(width, kTile)));
     rescale_kernel<<<grid, 256, 0, stream>>>(c, n, K, ldc, w, ldw, scale, ncol, out, ld_out,
                                              out_colmajor, gate);

@@ -316,12 +316,8 @@ jacobi_cluster_kernel(const double* __restrict__ g_in, int l, int lp, int max_sw
             __syncthreads();
             for (int round = 0; round < lp - 1; ++round, ++rg) {
                 const int sl = static_cast<int>(rg % kClRing);
-                if (tid == 0) {
-                    // the staging slot is reusable once the V-CTA released it
+                if (tid == 0)  // the staging slot is reusable once the V-CTA released it
                     cl_wait(&empty[sl], static_cast<unsigned>(((rg / kClRing) & 1) ^ 1));
-                    stage[sl * pay + half] = make_double2(1.0, 0.0);  // header: continue
-                    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-                }
                 __syncthreads();
                 for (int k = tid; k < half; k += blockDim.x) {
                     int p, q;
@@ -329,13 +325,11 @@ jacobi_cluster_kernel(const double* __restrict__ g_in, int l, int lp, int max_sw
                     const double a = M[p * lds + p], d = M[q * lds + q], b = M[p * lds + q];
                     double c = 1.0, s = 0.0, t = 0.0;
                     if (fabs(b) > kJacobiTol * sqrt(fabs(a)) * sqrt(fabs(d)) && fabs(b) > 1e-300) {
-                        const double theta = (d - a) / (2.0 * b);
-                        if (fabs(theta) > 1e150) {
-                            t = 0.5 / theta;
-                        } else {
-                            t = (theta >= 0.0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(fma(theta, theta, 1.0)));
-                        }
-                        c = 1.0 / sqrt(fma(t, t, 1.0));
+                        // t = tan(phi) = sgn(d - a) 2b / (|d - a| + sqrt((d - a)^2 + 4b^2))
+                        const double dm = d - a, b2 = 2.0 * b;
+                        const double den = fabs(dm) + sqrt(fma(dm, dm, b2 * b2));
+                        t = (dm >= 0.0 ? b2 : -b2) / den;
+                        c = rsqrt(fma(t, t, 1.0));
                         s = t * c;
                         if (s != 0.0) rotated = 1;
                     }
@@ -345,44 +339,48 @@ jacobi_cluster_kernel(const double* __restrict__ g_in, int l, int lp, int max_sw
                     pp[k] = p;
                     qq[k] = q;
                     stage[sl * pay + k] = make_double2(c, s);
+                    if (k == 0) stage[sl * pay + half] = make_double2(1.0, 0.0);  // header: continue
                     // make the generic-proxy writes visible to the bulk copy (async proxy)
                     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
                 }
                 __syncthreads();
-                if (tid == 0) send(rg);
-                for (int e = tid; e < nblocks; e += blockDim.x) {
-                    const int code = blk[e];
-                    const int kp = code >> 8, kr = code & 0xff;
-                    const double s1 = cs_s[kp], s2 = cs_s[kr];
-                    const int p = pp[kp], q = qq[kp];
-                    if (kp == kr) {
-                        if (s1 != 0.0) {
-                            const double t = cs_t[kp];
-                            const double b = M[p * lds + q];
-                            M[p * lds + p] -= t * b;
-                            M[q * lds + q] += t * b;
-                            M[p * lds + q] = 0.0;
-                            M[q * lds + p] = 0.0;
+                if (tid == kEigThreads - 32) {
+                    send(rg);  // the last warp forwards the round while the others update G
+                } else if (tid < kEigThreads - 32) {
+                    for (int e = tid; e < nblocks; e += kEigThreads - 32) {
+                        const int code = blk[e];
+                        const int kp = code >> 8, kr = code & 0xff;
+                        const double s1 = cs_s[kp], s2 = cs_s[kr];
+                        const int p = pp[kp], q = qq[kp];
+                        if (kp == kr) {
+                            if (s1 != 0.0) {
+                                const double t = cs_t[kp];
+                                const double b = M[p * lds + q];
+                                M[p * lds + p] -= t * b;
+                                M[q * lds + q] += t * b;
+                                M[p * lds + q] = 0.0;
+                                M[q * lds + p] = 0.0;
+                            }
+                            continue;
                         }
-                        continue;
+                        if (s1 == 0.0 && s2 == 0.0) continue;
+                        const double c1 = cs_c[kp], c2 = cs_c[kr];
+                        const int r = pp[kr], s = qq[kr];
+                        const double xpr = M[p * lds + r], xps = M[p * lds + s];
+                        const double xqr = M[q * lds + r], xqs = M[q * lds + s];
+                        const double ypr = c2 * xpr - s2 * xps, yps = s2 * xpr + c2 * xps;
+                        const double yqr = c2 * xqr - s2 * xqs, yqs = s2 * xqr + c2 * xqs;
+                        const double zpr = c1 * ypr - s1 * yqr, zqr = s1 * ypr + c1 * yqr;
+                        const double zps = c1 * yps - s1 * yqs, zqs = s1 * yps + c1 * yqs;
+                        M[p * lds + r] = zpr;
+                        M[r * lds + p] = zpr;
+                        M[p * lds + s] = zps;
+                        M[s * lds + p] = zps;
+                        M[q * lds + r] = zqr;
+                        M[r * lds + q] = zqr;
+                        M[q * lds + s] = zqs;
+                        M[s * lds + q] = zqs;
                     }
-                    if (s1 == 0.0 && s2 == 0.0) continue;
-                    const double c1 = cs_c[kp], c2 = cs_c[kr];
-                    const int r = pp[kr], s = qq[kr];
-                    const double xpr = M[p * lds + r], xps = M[p * lds + s];
-                    const double xqr = M[q * lds + r], xqs = M[q * lds + s];
-                    const double ypr = c2 * xpr - s2 * xps, yps = s2 * xpr + c2 * xps;
-                    const double yqr = c2 * xqr - s2 * xqs, yqs = s2 * xqr + c2 * xqs;
-                    const double zpr = c1 * ypr - s1 * yqr, zqr = s1 * ypr + c1 * yqr;
-                    const double zps = c1 * yps - s1 * yqs, zqs = s1 * yps + c1 * yqs;
-                    M[p * lds + r] = zpr;
-                    M[r * lds + p] = zpr;
-                    M[p * lds + s] = zps;
-                    M[s * lds + p] = zps;
-                    M[q * lds + r] = zqr;
-                    M[r * lds + q] = zqr;
-                    M[q * lds + s] = zqs;
-                    M[s * lds + q] = zqs;
                 }
                 __syncthreads();
             }
