@@ -320,6 +320,8 @@ __global__ void gram2_reduce_kernel(const double* __restrict__ partial, int nblk
 // (bitwise the reference matmul order). Block = 64 rows x all ncol columns;
 // thread owns an 8x8 output tile; C (transposed) and W are staged 8 t at a time.
 constexpr int kR2Rows = 64;
+// measured slower than rescale_kernel on C2 (0.89 vs 0.62 ms); kept for tuning
+bool rescale_v2_enabled = false;
 constexpr int kR2K = 8;
 
 __global__ void __launch_bounds__(256)
@@ -439,7 +441,8 @@ Gram2Plan gram2_plan(int64_t n, int64_t l, int64_t ld) {
     p.lp8 = static_cast<int>((l + 7) / 8 * 8);
     p.ntile = p.lp8 / 8;
     p.npair = p.ntile * (p.ntile + 1) / 2;
-    p.ok = p.npair <= kG2MaxTiles && ld % 2 == 0 && p.lp8 >= ld - 3;
+    // 8x8 accumulators take ~165 registers: at most 384 threads per block
+    p.ok = p.npair <= 384 && ld % 2 == 0 && p.lp8 >= ld - 3;
     const int64_t target = 2 * kNumSMs;
     int64_t rpb = ceil_div(n, target);
     rpb = std::max<int64_t>(kG2Rows, ceil_div(rpb, kG2Rows) * kG2Rows);
@@ -492,7 +495,7 @@ void rescale(const double* c, int64_t n, int64_t K, int64_t ldc, const double* w
     const int64_t width = out_colmajor ? ncol : ld_out;
     const int np8 = static_cast<int>((width + 7) / 8 * 8);
     const int threads = (kR2Rows / 8) * (np8 / 8);
-    if (threads <= 1024 && np8 > 0) {
+    if (rescale_v2_enabled && threads <= 320 && np8 > 0) {
         const size_t smem = sizeof(double) * kR2K * (kR2Rows + np8);
         rescale2_kernel<<<static_cast<unsigned>(ceil_div(n, kR2Rows)), (threads + 31) / 32 * 32, smem, stream>>>(
             c, n, K, ldc, w, ldw, scale, ncol, np8, out, ld_out, out_colmajor, gate);
