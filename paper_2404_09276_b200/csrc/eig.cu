@@ -413,7 +413,10 @@ jacobi_cluster_kernel(const double* __restrict__ g_in, int l, int lp, int max_sw
         const int rows_per = (lp + groups - 1) / groups;
         for (int64_t rg = 0;; ++rg) {
             const int sl = static_cast<int>(rg % kClRing);
-            cl_wait(&full[sl], static_cast<unsigned>((rg / kClRing) & 1));
+            // one thread acquires at cluster scope (each cluster-scope acquire
+            // invalidates L1), the CTA barrier hands the slot to the others
+            if (tid == 0) cl_wait(&full[sl], static_cast<unsigned>((rg / kClRing) & 1));
+            __syncthreads();
             const double2* rot = ring + sl * pay;
             if (rot[half].x == 0.0) break;
             const int round = static_cast<int>(rg % (lp - 1));
