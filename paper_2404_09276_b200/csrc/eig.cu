@@ -30,6 +30,7 @@ namespace {
 constexpr int kEigThreads = 1024;
 constexpr int kMaxPairs = 256;  // lp <= 512
 constexpr double kJacobiTol = 1e-15;
+constexpr double kBigRatio2 = 1e-16;  // (1e-8)^2: sweep-level convergence test
 constexpr int kSmemLimit = 227 * 1024;
 
 __device__ __forceinline__ void pair_of(int round, int k, int lp, int& p, int& q) {
@@ -267,7 +268,7 @@ jacobi_cluster_kernel(const double* __restrict__ g_in, int l, int lp, int max_sw
     extern __shared__ __align__(16) double cl_smem[];
     __shared__ double cs_c[kMaxPairs], cs_s[kMaxPairs], cs_t[kMaxPairs];
     __shared__ int pp[kMaxPairs], qq[kMaxPairs];
-    __shared__ int rotated;
+    __shared__ int rotated, big;
     const int half = lp / 2, lds = lp + 1;
     const int pay = half + 1;                                           // double2 per round
     double* M = cl_smem;                                                // G (rank 0) or V (rank 1)
@@ -278,6 +279,7 @@ jacobi_cluster_kernel(const double* __restrict__ g_in, int l, int lp, int max_sw
     uint16_t* blk = reinterpret_cast<uint16_t*>(empty + kClRing);       // rank 0
     const unsigned rank = cl_rank();
     const int tid = threadIdx.x;
+    auto UP = [&](int i, int j) -> double& { return i <= j ? M[i * lds + j] : M[j * lds + i]; };
     const unsigned pay_bytes = static_cast<unsigned>(sizeof(double2) * pay);
     if (tid == 0) {
         for (int sl = 0; sl < kClRing; ++sl) {
@@ -312,7 +314,10 @@ jacobi_cluster_kernel(const double* __restrict__ g_in, int l, int lp, int max_sw
         int sweep = 0;
         bool converged = false;
         for (; sweep < max_sweeps && !converged; ++sweep) {
-            if (tid == 0) rotated = 0;
+            if (tid == 0) {
+                rotated = 0;
+                big = 0;
+            }
             __syncthreads();
             for (int round = 0; round < lp - 1; ++round, ++rg) {
                 const int sl = static_cast<int>(rg % kClRing);
@@ -322,13 +327,15 @@ jacobi_cluster_kernel(const double* __restrict__ g_in, int l, int lp, int max_sw
                 for (int k = tid; k < half; k += blockDim.x) {
                     int p, q;
                     pair_of(round, k, lp, p, q);
-                    const double a = M[p * lds + p], d = M[q * lds + q], b = M[p * lds + q];
+                    const double a = M[p * lds + p], d = M[q * lds + q], b = UP(p, q);
                     double c = 1.0, s = 0.0, t = 0.0;
-                    if (fabs(b) > kJacobiTol * sqrt(fabs(a)) * sqrt(fabs(d)) && fabs(b) > 1e-300) {
+                    const double b2 = b * b, ad = fabs(a * d);
+                    if (b2 > kBigRatio2 * ad) big = 1;
+                    if (b2 > kJacobiTol * kJacobiTol * ad && fabs(b) > 1e-300) {
                         // t = tan(phi) = sgn(d - a) 2b / (|d - a| + sqrt((d - a)^2 + 4b^2))
-                        const double dm = d - a, b2 = 2.0 * b;
-                        const double den = fabs(dm) + sqrt(fma(dm, dm, b2 * b2));
-                        t = (dm >= 0.0 ? b2 : -b2) / den;
+                        const double dm = d - a, tb = 2.0 * b;
+                        const double den = fabs(dm) + sqrt(fma(dm, dm, tb * tb));
+                        t = (dm >= 0.0 ? tb : -tb) / den;
                         c = rsqrt(fma(t, t, 1.0));
                         s = t * c;
                         if (s != 0.0) rotated = 1;
@@ -355,36 +362,37 @@ jacobi_cluster_kernel(const double* __restrict__ g_in, int l, int lp, int max_sw
                         if (kp == kr) {
                             if (s1 != 0.0) {
                                 const double t = cs_t[kp];
-                                const double b = M[p * lds + q];
-                                M[p * lds + p] -= t * b;
-                                M[q * lds + q] += t * b;
-                                M[p * lds + q] = 0.0;
-                                M[q * lds + p] = 0.0;
+                                double& bpq = UP(p, q);
+                                const double bb = bpq;
+                                M[p * lds + p] -= t * bb;
+                                M[q * lds + q] += t * bb;
+                                bpq = 0.0;
                             }
                             continue;
                         }
                         if (s1 == 0.0 && s2 == 0.0) continue;
                         const double c1 = cs_c[kp], c2 = cs_c[kr];
                         const int r = pp[kr], s = qq[kr];
-                        const double xpr = M[p * lds + r], xps = M[p * lds + s];
-                        const double xqr = M[q * lds + r], xqs = M[q * lds + s];
+                        // G is kept as its upper triangle only: every entry is read and
+                        // written once per round (half the traffic of a mirrored update)
+                        double& gpr = UP(p, r);
+                        double& gps = UP(p, s);
+                        double& gqr = UP(q, r);
+                        double& gqs = UP(q, s);
+                        const double xpr = gpr, xps = gps, xqr = gqr, xqs = gqs;
                         const double ypr = c2 * xpr - s2 * xps, yps = s2 * xpr + c2 * xps;
                         const double yqr = c2 * xqr - s2 * xqs, yqs = s2 * xqr + c2 * xqs;
-                        const double zpr = c1 * ypr - s1 * yqr, zqr = s1 * ypr + c1 * yqr;
-                        const double zps = c1 * yps - s1 * yqs, zqs = s1 * yps + c1 * yqs;
-                        M[p * lds + r] = zpr;
-                        M[r * lds + p] = zpr;
-                        M[p * lds + s] = zps;
-                        M[s * lds + p] = zps;
-                        M[q * lds + r] = zqr;
-                        M[r * lds + q] = zqr;
-                        M[q * lds + s] = zqs;
-                        M[s * lds + q] = zqs;
+                        gpr = c1 * ypr - s1 * yqr;
+                        gqr = s1 * ypr + c1 * yqr;
+                        gps = c1 * yps - s1 * yqs;
+                        gqs = s1 * yps + c1 * yqs;
                     }
                 }
                 __syncthreads();
             }
-            converged = rotated == 0;
+            // quadratic convergence: once every off-diagonal entry seen in a sweep
+            // was below 1e-8 of sqrt(g_pp g_qq), the sweep left them at ~1e-16
+            converged = rotated == 0 || big == 0;
             __syncthreads();
         }
         if (tid == 0) {  // stop marker
