@@ -47,8 +47,10 @@ __device__ __forceinline__ void pair_of(int round, int k, int lp, int& p, int& q
 __global__ void __launch_bounds__(kEigThreads, 1)
 jacobi_kernel(const double* __restrict__ g_in, int l, int lp, double* __restrict__ gbuf,
               int use_smem, double2* __restrict__ rot_log, int max_sweeps,
-              double* __restrict__ lam, Control* ctrl, const int32_t* __restrict__ gate) {
+              double* __restrict__ lam, Control* ctrl, const int32_t* __restrict__ gate,
+              const int32_t* __restrict__ need) {
     if (gate != nullptr && *gate != 0) return;
+    if (need != nullptr && *need == 0) return;
     extern __shared__ double smem[];
     __shared__ double cs_c[kMaxPairs], cs_s[kMaxPairs], cs_t[kMaxPairs];
     __shared__ int pp[kMaxPairs], qq[kMaxPairs];
@@ -156,8 +158,9 @@ jacobi_kernel(const double* __restrict__ g_in, int l, int lp, double* __restrict
 // V = I * J_1 * ... replayed on one row of V per warp.
 __global__ void jacobi_replay_kernel(const double2* __restrict__ rot_log, int l, int lp,
                                      const Control* ctrl, double* __restrict__ vecs,
-                                     const int32_t* __restrict__ gate) {
+                                     const int32_t* __restrict__ gate, const int32_t* __restrict__ need) {
     if (gate != nullptr && *gate != 0) return;
+    if (need != nullptr && *need == 0) return;
     extern __shared__ double vrow_all[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int row = blockIdx.x * (blockDim.x >> 5) + warp;
@@ -262,9 +265,10 @@ size_t cluster_smem_bytes(int lp) {
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kEigThreads, 1)
 jacobi_cluster_kernel(const double* __restrict__ g_in, int l, int lp, int max_sweeps,
                       double* __restrict__ lam, double* __restrict__ vecs, Control* ctrl,
-                      const int32_t* __restrict__ gate) {
-    // the gate is read by both CTAs before any cluster traffic, so both exit together
+                      const int32_t* __restrict__ gate, const int32_t* __restrict__ need) {
+    // the gates are read by both CTAs before any cluster traffic, so both exit together
     if (gate != nullptr && *gate != 0) return;
+    if (need != nullptr && *need == 0) return;
     extern __shared__ __align__(16) double cl_smem[];
     __shared__ double cs_c[kMaxPairs], cs_s[kMaxPairs], cs_t[kMaxPairs];
     __shared__ int pp[kMaxPairs], qq[kMaxPairs];
@@ -645,7 +649,7 @@ void eig_workspace_bind(EigWorkspace& w, int l, int max_sweeps, void* mem) {
 }
 
 void jacobi_eig(const double* g, EigWorkspace& w, Control* ctrl, const int32_t* gate,
-                cudaStream_t stream) {
+                cudaStream_t stream, const int32_t* need) {
     if (w.lp > 2 * kMaxPairs) fail(DSVD_UNSUPPORTED, "eigensolver: l > 512 is not supported");
     const size_t csmem = cluster_smem_bytes(w.lp);
     if (csmem <= static_cast<size_t>(kSmemLimit) - 12 * 1024 && w.lp >= 4) {
@@ -653,7 +657,7 @@ void jacobi_eig(const double* g, EigWorkspace& w, Control* ctrl, const int32_t* 
                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              static_cast<int>(csmem)));
         jacobi_cluster_kernel<<<2, kEigThreads, csmem, stream>>>(g, w.l, w.lp, w.max_sweeps, w.lam,
-                                                                 w.vecs, ctrl, gate);
+                                                                 w.vecs, ctrl, gate, need);
         DSVD_LAUNCH_CHECK();
         return;
     }
@@ -665,12 +669,12 @@ void jacobi_eig(const double* g, EigWorkspace& w, Control* ctrl, const int32_t* 
     DSVD_CUDA_CHECK(cudaFuncSetAttribute(jacobi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          kSmemLimit - 16 * 1024));
     jacobi_kernel<<<1, kEigThreads, smem, stream>>>(
-        g, w.l, w.lp, w.gbuf, use_smem, w.rot_log, w.max_sweeps, w.lam, ctrl, gate);
+        g, w.l, w.lp, w.gbuf, use_smem, w.rot_log, w.max_sweeps, w.lam, ctrl, gate, need);
     DSVD_LAUNCH_CHECK();
     const int warps = 8;
     jacobi_replay_kernel<<<static_cast<unsigned>(ceil_div(w.lp, warps)), 32 * warps,
                            sizeof(double) * warps * w.lp, stream>>>(w.rot_log, w.l, w.lp, ctrl,
-                                                                    w.vecs, gate);
+                                                                    w.vecs, gate, need);
     DSVD_LAUNCH_CHECK();
 }
 

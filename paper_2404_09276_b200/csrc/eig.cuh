@@ -21,8 +21,18 @@ void eig_workspace_bind(EigWorkspace& w, int l, int max_sweeps, void* mem);
 // Jacobi on the l x l matrix g (device, row-major == column-major) -> w.lam,
 // w.vecs (unsorted). Sweep count goes to ctrl->eig_sweeps (and is added to
 // ctrl->total_sweeps); non-convergence sets ctrl->status = DSVD_NUMERICAL.
+// `need` (optional): the kernels only run when *need != 0 (the tridiagonal
+// path's fallback flag).
 void jacobi_eig(const double* g, EigWorkspace& w, Control* ctrl, const int32_t* gate,
-                cudaStream_t stream);
+                cudaStream_t stream, const int32_t* need = nullptr);
+
+// Tridiagonal path (eig_tbi.cu): Householder + multisection + inverse
+// iteration. Sets *clustered when eigenvalues are too close for inverse
+// iteration; callers then run jacobi_eig with need = clustered.
+bool tbi_supported(int l);
+size_t tbi_workspace_bytes(int l);
+void tbi_eig(const double* g, EigWorkspace& w, void* tbi_ws, int32_t* clustered, const int32_t* gate,
+             cudaStream_t stream);
 
 // Loop-mode parameters of eig_svd_finish (solver.cpp:97-112).
 struct LoopStep {

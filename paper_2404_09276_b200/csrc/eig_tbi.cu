@@ -1,0 +1,411 @@
+// Tridiagonal eigensolver path for eigSVD's l x l Gram matrix on sm_100a:
+//
+//   1. tbi_tridiag_kernel  — Householder reduction A = Q T Q^T on one SM (the
+//      reference's first stage, sym_eig.cpp:19-74, parallelised per step:
+//      warp reductions for the norm, warp-per-row for p = tau A v, a
+//      symmetric rank-2 update of the lower triangle in shared memory).
+//   2. tbi_eig_kernel      — one warp per eigenvalue: 33-way multisection on
+//      Sturm counts (each lane evaluates one point) to full precision, then
+//      inverse iteration with a partially pivoted tridiagonal LU (lane 0).
+//   3. tbi_orth_kernel     — two Newton-Schulz polar steps Z <- Z (3I - Z^T Z)/2
+//      make the eigenvectors orthonormal to working precision.
+//   4. tbi_backtransform_kernel — V = H_0 ... H_{n-3} Z, one warp per column, on
+//      all SMs.
+//
+// The reference's implicit QL (sym_eig.cpp:78-130) is a serial bulge chase;
+// bisection + inverse iteration exposes one independent task per eigenvalue
+// instead. Inverse iteration needs separated eigenvalues, so tbi_eig_kernel
+// raises a flag when two eigenvalues are closer than kTbiGap (relative to
+// ||T||); the caller then runs the Jacobi solver instead (its kernels are
+// launched gated on that flag), so clustered or repeated spectra keep full
+// accuracy. Accuracy class on separated spectra: absolute eigenvalue error
+// ~ n eps ||A||, the same as the reference's QL.
+#include <cfloat>
+
+#include "eig.cuh"
+
+namespace dsvd {
+
+namespace {
+
+constexpr int kTbiThreads = 1024;
+constexpr double kTbiGap = 1e-9;  // minimum relative eigenvalue gap for inverse iteration
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// ---- 1. Householder tridiagonalisation ---------------------------------------
+// A (n x n, symmetric) in shared memory, lower triangle authoritative, stride
+// lda = n | 1. Outputs d (n), e (n-1), reflectors hv[k*n + i] (i > k) and tau[k].
+__global__ void __launch_bounds__(kTbiThreads, 1)
+tbi_tridiag_kernel(const double* __restrict__ g, int n, double* __restrict__ d, double* __restrict__ e,
+                   double* __restrict__ hv, double* __restrict__ tau_out, const int32_t* __restrict__ gate,
+                   const int32_t* __restrict__ skip) {
+    if ((gate != nullptr && *gate != 0) || (skip != nullptr && *skip != 0)) return;
+    extern __shared__ double tsm[];
+    const int lda = n | 1;
+    double* A = tsm;                 // n x lda
+    double* v = A + n * lda;         // n
+    double* w = v + n;               // n
+    __shared__ double s_tau, s_K;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarp = blockDim.x >> 5;
+    for (int x = tid; x < n * n; x += blockDim.x) {
+        const int i = x / n, j = x % n;
+        A[i * lda + j] = g[x];
+    }
+    __syncthreads();
+    auto L = [&](int i, int j) -> double& { return i >= j ? A[i * lda + j] : A[j * lda + i]; };
+    for (int k = 0; k + 2 < n; ++k) {
+        const int k1 = k + 1, m = n - k1;
+        if (warp == 0) {
+            double sig = 0.0;
+            for (int i = k1 + lane; i < n; i += 32) {
+                const double x = L(i, k);
+                sig = fma(x, x, sig);
+            }
+            sig = warp_sum(sig);
+            const double x0 = L(k1, k);
+            double alpha = 0.0, tau = 0.0, v0 = x0;
+            const double tail = sig - x0 * x0;  // sum of squares below the first entry
+            if (tail > 0.0) {
+                alpha = -copysign(sqrt(sig), x0);
+                v0 = x0 - alpha;
+                tau = 2.0 / (tail + v0 * v0);
+            } else {
+                alpha = x0;  // already tridiagonal in this column
+            }
+            for (int i = k1 + lane; i < n; i += 32) {
+                const double vi = (i == k1) ? v0 : L(i, k);
+                v[i] = vi;
+                hv[static_cast<int64_t>(k) * n + i] = vi;
+            }
+            if (lane == 0) {
+                s_tau = tau;
+                tau_out[k] = tau;
+                e[k] = alpha;
+                d[k] = L(k, k);
+            }
+        }
+        __syncthreads();
+        const double tau = s_tau;
+        if (tau != 0.0) {
+            // p = tau * A22 v   (warp per row, lanes over columns)
+            for (int i = k1 + warp; i < n; i += nwarp) {
+                double acc = 0.0;
+                for (int j = k1 + lane; j < n; j += 32) acc = fma(L(i, j), v[j], acc);
+                acc = warp_sum(acc);
+                if (lane == 0) w[i] = tau * acc;
+            }
+            __syncthreads();
+            if (warp == 0) {
+                double acc = 0.0;
+                for (int i = k1 + lane; i < n; i += 32) acc = fma(w[i], v[i], acc);
+                acc = warp_sum(acc);
+                if (lane == 0) s_K = 0.5 * tau * acc;
+            }
+            __syncthreads();
+            const double K = s_K;
+            for (int i = k1 + tid; i < n; i += blockDim.x) w[i] = fma(-K, v[i], w[i]);
+            __syncthreads();
+            // A22 -= v w^T + w v^T on the lower triangle
+            for (int x = tid; x < m * m; x += blockDim.x) {
+                const int i = k1 + x / m, j = k1 + x % m;
+                if (j <= i) {
+                    double& a = A[i * lda + j];
+                    a = a - v[i] * w[j] - w[i] * v[j];
+                }
+            }
+            __syncthreads();
+        }
+    }
+    if (tid == 0) {
+        if (n >= 2) {
+            d[n - 2] = L(n - 2, n - 2);
+            e[n - 2] = L(n - 1, n - 2);
+        }
+        d[n - 1] = L(n - 1, n - 1);
+    }
+}
+
+// ---- 2. eigenvalues (multisection) and eigenvectors (inverse iteration) ----------------
+__device__ int sturm_count(const double* d, const double* e2, int n, double x, double pivmin) {
+    int cnt = 0;
+    double q = d[0] - x;
+    if (fabs(q) < pivmin) q = -pivmin;
+    cnt += q < 0.0;
+    for (int i = 1; i < n; ++i) {
+        q = (d[i] - x) - e2[i - 1] / q;
+        if (fabs(q) < pivmin) q = -pivmin;
+        cnt += q < 0.0;
+    }
+    return cnt;
+}
+
+constexpr int kTbiWarps = 8;
+
+__global__ void __launch_bounds__(32 * kTbiWarps)
+tbi_eig_kernel(const double* __restrict__ dg, const double* __restrict__ eg, int n,
+               double* __restrict__ lam, double* __restrict__ z, int ldz, int32_t* __restrict__ clustered,
+               const int32_t* __restrict__ gate, const int32_t* __restrict__ skip) {
+    if ((gate != nullptr && *gate != 0) || (skip != nullptr && *skip != 0)) return;
+    extern __shared__ double esm[];
+    double* d = esm;                       // n
+    double* e = d + n;                     // n
+    double* e2 = e + n;                    // n
+    double* work = e2 + n;                 // kTbiWarps x 5n (per-warp LU / vector)
+    __shared__ double s_gl, s_gu, s_pivmin, s_tnorm;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (int i = tid; i < n; i += blockDim.x) {
+        d[i] = dg[i];
+        const double ei = i + 1 < n ? eg[i] : 0.0;
+        e[i] = ei;
+        e2[i] = ei * ei;
+    }
+    __syncthreads();
+    if (warp == 0) {
+        double gl = DBL_MAX, gu = -DBL_MAX, emax = 0.0, tn = 0.0;
+        for (int i = lane; i < n; i += 32) {
+            const double r = (i > 0 ? fabs(e[i - 1]) : 0.0) + (i + 1 < n ? fabs(e[i]) : 0.0);
+            gl = fmin(gl, d[i] - r);
+            gu = fmax(gu, d[i] + r);
+            emax = fmax(emax, e2[i]);
+            tn = fmax(tn, fabs(d[i]) + r);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            gl = fmin(gl, __shfl_xor_sync(0xffffffffu, gl, o));
+            gu = fmax(gu, __shfl_xor_sync(0xffffffffu, gu, o));
+            emax = fmax(emax, __shfl_xor_sync(0xffffffffu, emax, o));
+            tn = fmax(tn, __shfl_xor_sync(0xffffffffu, tn, o));
+        }
+        if (lane == 0) {
+            const double pad = 2.0 * DBL_EPSILON * fmax(fabs(gl), fabs(gu)) + 1e-300;
+            s_gl = gl - pad;
+            s_gu = gu + pad;
+            s_pivmin = DBL_MIN * fmax(1.0, emax);
+            s_tnorm = tn;
+        }
+    }
+    __syncthreads();
+    const int j = blockIdx.x * kTbiWarps + warp;
+    if (j >= n) return;
+    const double pivmin = s_pivmin, tnorm = s_tnorm;
+    // j-th smallest eigenvalue: count(lo) <= j < count(hi)
+    double lo = s_gl, hi = s_gu;
+    for (int it = 0; it < 40; ++it) {
+        const double width = hi - lo;
+        if (width <= 2.0 * DBL_EPSILON * fmax(fabs(lo), fabs(hi)) + pivmin) break;
+        const double x = lo + width * (lane + 1) / 33.0;
+        const int c = sturm_count(d, e2, n, x, pivmin);
+        const unsigned above = __ballot_sync(0xffffffffu, c > j);
+        const int first = above ? __ffs(above) - 1 : 32;
+        const double xf = __shfl_sync(0xffffffffu, x, first < 32 ? first : 31);
+        const double xp = __shfl_sync(0xffffffffu, x, first > 0 ? first - 1 : 0);
+        if (first < 32) hi = xf;
+        if (first > 0) lo = xp;
+        if (first == 32) lo = xf;  // all points below: root in (x_31, hi]
+    }
+    const double lmb = 0.5 * (lo + hi);
+    if (lane == 0) lam[j] = lmb;
+    // neighbours closer than kTbiGap ||T|| -> inverse iteration is not reliable
+    if (lane == 0 && j + 1 < n) {
+        const int c = sturm_count(d, e2, n, lmb + kTbiGap * tnorm, pivmin);
+        if (c > j + 1) atomicExch(clustered, 1);
+    }
+    // inverse iteration on (T - lmb I): LU with partial pivoting (the dgttrf /
+    // dgttrs recurrences), three solves from a fixed non-degenerate start (lane 0)
+    if (lane == 0) {
+        double* dd = work + warp * 5 * n;  // diagonal of U
+        double* du = dd + n;               // first superdiagonal of U
+        double* du2 = du + n;              // second superdiagonal (fill-in)
+        double* dl = du2 + n;              // multipliers
+        double* sw = dl + n;               // 1.0 where rows i, i+1 were interchanged
+        for (int i = 0; i < n; ++i) {
+            dd[i] = d[i] - lmb;
+            du[i] = i + 1 < n ? e[i] : 0.0;
+            dl[i] = i + 1 < n ? e[i] : 0.0;
+            du2[i] = 0.0;
+            sw[i] = 0.0;
+        }
+        const double tiny = DBL_EPSILON * fmax(tnorm, DBL_MIN);
+        for (int i = 0; i + 1 < n; ++i) {
+            if (fabs(dd[i]) >= fabs(dl[i])) {
+                const double fact = dd[i] != 0.0 ? dl[i] / dd[i] : 0.0;
+                dl[i] = fact;
+                dd[i + 1] -= fact * du[i];
+            } else {
+                const double fact = dd[i] / dl[i];
+                dd[i] = dl[i];
+                dl[i] = fact;
+                const double t = du[i];
+                du[i] = dd[i + 1];
+                dd[i + 1] = t - fact * dd[i + 1];
+                if (i + 2 < n) {
+                    du2[i] = du[i + 1];
+                    du[i + 1] = -fact * du[i + 1];
+                }
+                sw[i] = 1.0;
+            }
+            if (fabs(dd[i]) < tiny) dd[i] = copysign(tiny, dd[i]);
+        }
+        if (fabs(dd[n - 1]) < tiny) dd[n - 1] = copysign(tiny, dd[n - 1]);
+        double* x = z + j;  // column j of z (stride ldz) holds the iterate
+        auto X = [&](int i) -> double& { return x[static_cast<int64_t>(i) * ldz]; };
+        for (int i = 0; i < n; ++i) X(i) = 1.0 + 0.01 * ((i * 7 + j * 13) % 17);
+        for (int pass = 0; pass < 3; ++pass) {
+            for (int i = 0; i + 1 < n; ++i) {  // L^{-1} with the interchanges
+                if (sw[i] == 0.0) {
+                    X(i + 1) -= dl[i] * X(i);
+                } else {
+                    const double t = X(i);
+                    X(i) = X(i + 1);
+                    X(i + 1) = t - dl[i] * X(i);
+                }
+            }
+            double nrm = 0.0;
+            for (int i = n - 1; i >= 0; --i) {  // U^{-1}
+                double sum = X(i);
+                if (i + 1 < n) sum -= du[i] * X(i + 1);
+                if (i + 2 < n) sum -= du2[i] * X(i + 2);
+                sum /= dd[i];
+                X(i) = sum;
+                nrm = fmax(nrm, fabs(sum));
+            }
+            const double inv = nrm > 0.0 ? 1.0 / nrm : 1.0;
+            for (int i = 0; i < n; ++i) X(i) *= inv;
+        }
+        double s2 = 0.0;
+        for (int i = 0; i < n; ++i) s2 = fma(X(i), X(i), s2);
+        const double inv = 1.0 / sqrt(s2);
+        for (int i = 0; i < n; ++i) X(i) *= inv;
+    }
+}
+
+// ---- 3. orthonormalisation: Z <- Z (3I - Z^T Z) / 2, twice -----------------------------
+__global__ void __launch_bounds__(kTbiThreads, 1)
+tbi_orth_kernel(double* __restrict__ z, int n, int ldz, const int32_t* __restrict__ gate,
+                const int32_t* __restrict__ skip) {
+    if ((gate != nullptr && *gate != 0) || (skip != nullptr && *skip != 0)) return;
+    extern __shared__ double osm[];
+    const int lds = n | 1;
+    double* Z = osm;             // n x lds
+    double* S = Z + n * lds;     // n x lds : 3I - Z^T Z, then scratch
+    for (int x = threadIdx.x; x < n * n; x += blockDim.x) {
+        const int i = x / n, j = x % n;
+        Z[i * lds + j] = z[static_cast<int64_t>(i) * ldz + j];
+    }
+    __syncthreads();
+    for (int step = 0; step < 2; ++step) {
+        for (int x = threadIdx.x; x < n * n; x += blockDim.x) {
+            const int a = x / n, b = x % n;
+            if (b < a) continue;
+            double acc = 0.0;
+            for (int t = 0; t < n; ++t) acc = fma(Z[t * lds + a], Z[t * lds + b], acc);
+            const double v = (a == b ? 3.0 : 0.0) - acc;
+            S[a * lds + b] = 0.5 * v;
+            S[b * lds + a] = 0.5 * v;
+        }
+        __syncthreads();
+        // Z <- Z S, one row of Z per thread group (row kept in registers chunks)
+        for (int i = threadIdx.x >> 5; i < n; i += blockDim.x >> 5) {
+            const int lane = threadIdx.x & 31;
+            double out[8];
+            const int nb = (n + 31) / 32;
+            for (int q = 0; q < nb && q < 8; ++q) {
+                const int col = lane + 32 * q;
+                double acc = 0.0;
+                if (col < n)
+                    for (int t = 0; t < n; ++t) acc = fma(Z[i * lds + t], S[t * lds + col], acc);
+                out[q] = acc;
+            }
+            __syncwarp();
+            for (int q = 0; q < nb && q < 8; ++q) {
+                const int col = lane + 32 * q;
+                if (col < n) Z[i * lds + col] = out[q];
+            }
+        }
+        __syncthreads();
+    }
+    for (int x = threadIdx.x; x < n * n; x += blockDim.x) {
+        const int i = x / n, j = x % n;
+        z[static_cast<int64_t>(i) * ldz + j] = Z[i * lds + j];
+    }
+}
+
+// ---- 4. back-transform: V = H_0 H_1 ... H_{n-3} Z, one warp per column -------------
+__global__ void tbi_backtransform_kernel(const double* __restrict__ hv, const double* __restrict__ tau,
+                                         const double* __restrict__ z, int n, int ldz,
+                                         double* __restrict__ vecs, int ldv, const int32_t* __restrict__ gate,
+                                         const int32_t* __restrict__ skip) {
+    if ((gate != nullptr && *gate != 0) || (skip != nullptr && *skip != 0)) return;
+    extern __shared__ double bsm[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int col = blockIdx.x * (blockDim.x >> 5) + warp;
+    if (col >= n) return;
+    double* x = bsm + warp * n;
+    for (int i = lane; i < n; i += 32) x[i] = z[static_cast<int64_t>(i) * ldz + col];
+    __syncwarp();
+    for (int k = n - 3; k >= 0; --k) {
+        const double t = tau[k];
+        if (t == 0.0) continue;
+        const double* vk = hv + static_cast<int64_t>(k) * n;
+        double s = 0.0;
+        for (int i = k + 1 + lane; i < n; i += 32) s = fma(vk[i], x[i], s);
+        s = warp_sum(s) * t;
+        for (int i = k + 1 + lane; i < n; i += 32) x[i] = fma(-s, vk[i], x[i]);
+        __syncwarp();
+    }
+    for (int i = lane; i < n; i += 32) vecs[static_cast<int64_t>(i) * ldv + col] = x[i];
+}
+
+__global__ void tbi_clear_kernel(int32_t* flag) { *flag = 0; }
+
+}  // namespace
+
+bool tbi_supported(int l) { return l >= 3 && l <= 160; }
+
+size_t tbi_workspace_bytes(int l) {
+    const size_t n = l;
+    return sizeof(double) * (n * n /*hv*/ + n /*tau*/ + 2 * n /*d,e*/ + n * n /*z*/) + 64;
+}
+
+// Runs the tridiagonal path; sets *clustered (device) when the spectrum needs
+// the Jacobi fallback. Writes w.lam / w.vecs (stride w.lp) like jacobi_eig.
+void tbi_eig(const double* g, EigWorkspace& w, void* tbi_ws, int32_t* clustered, const int32_t* gate,
+             cudaStream_t stream) {
+    const int n = w.l;
+    double* hv = static_cast<double*>(tbi_ws);
+    double* tau = hv + static_cast<size_t>(n) * n;
+    double* d = tau + n;
+    double* e = d + n;
+    double* z = e + n;
+    tbi_clear_kernel<<<1, 1, 0, stream>>>(clustered);
+    DSVD_LAUNCH_CHECK();
+    const int lda = n | 1;
+    const size_t s1 = sizeof(double) * (static_cast<size_t>(n) * lda + 2 * n);
+    static bool attr = false;
+    if (!attr) {
+        DSVD_CUDA_CHECK(cudaFuncSetAttribute(tbi_tridiag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             227 * 1024));
+        DSVD_CUDA_CHECK(cudaFuncSetAttribute(tbi_orth_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             227 * 1024));
+        attr = true;
+    }
+    tbi_tridiag_kernel<<<1, kTbiThreads, s1, stream>>>(g, n, d, e, hv, tau, gate, nullptr);
+    DSVD_LAUNCH_CHECK();
+    const size_t s2 = sizeof(double) * (3 * static_cast<size_t>(n) + kTbiWarps * 5 * static_cast<size_t>(n));
+    tbi_eig_kernel<<<static_cast<unsigned>(ceil_div(n, kTbiWarps)), 32 * kTbiWarps, s2, stream>>>(
+        d, e, n, w.lam, z, n, clustered, gate, nullptr);
+    DSVD_LAUNCH_CHECK();
+    const size_t s3 = sizeof(double) * 2 * static_cast<size_t>(n) * lda;
+    tbi_orth_kernel<<<1, kTbiThreads, s3, stream>>>(z, n, n, gate, clustered);
+    DSVD_LAUNCH_CHECK();
+    tbi_backtransform_kernel<<<static_cast<unsigned>(ceil_div(n, 8)), 256, sizeof(double) * 8 * n, stream>>>(
+        hv, tau, z, n, n, w.vecs, w.lp, gate, clustered);
+    DSVD_LAUNCH_CHECK();
+}
+
+}  // namespace dsvd

@@ -275,8 +275,17 @@ void eig_svd_factors(dsvd_ctx* ctx, const double* c, int64_t rows, int64_t l, in
     void* em = ctx->buf("eig.ws", eig_workspace_bytes(static_cast<int>(l), kMaxSweeps));
     eig_workspace_bind(ew, static_cast<int>(l), kMaxSweeps, em);
     sp = ctx->span_begin(K_EIG);
-    jacobi_eig(G, ew, ctrl, gate, st);
-    count_launch(2);
+    if (ctx->eig_method == 0 && tbi_supported(static_cast<int>(l))) {
+        // tridiagonal path; the Jacobi kernels run only if it flags a cluster
+        int32_t* flag = ctx->tbuf<int32_t>("tbi.flag", 1);
+        tbi_eig(G, ew, ctx->buf("tbi.ws", tbi_workspace_bytes(static_cast<int>(l))), flag, gate, st);
+        count_launch(5);
+        jacobi_eig(G, ew, ctrl, gate, st, flag);
+        count_launch(1);
+    } else {
+        jacobi_eig(G, ew, ctrl, gate, st);
+        count_launch(2);
+    }
     eig_svd_finish(ew, floor_rows >= 0 ? floor_rows : rows, o.W, l, o.s, o.inv_s, ctrl, loop, gate, st);
     count_launch(1);
     ctx->span_end(sp);
@@ -688,6 +697,9 @@ int dsvd_ctx_set_option(dsvd_ctx* ctx, const char* name, int64_t value) {
             ctx->spmm_variant = static_cast<int>(value);
         } else if (n == "hub_threshold") {
             ctx->hub_threshold = value;
+        } else if (n == "eig_method") {
+            if (value < 0 || value > 1) fail(DSVD_CONFIG, "eig_method: 0 = tridiagonal (auto), 1 = Jacobi");
+            ctx->eig_method = static_cast<int>(value);
         } else if (n == "split_chunk") {
             if (value < 0) fail(DSVD_CONFIG, "split_chunk must be >= 0");
             ctx->split_chunk = value;

@@ -307,6 +307,27 @@ def test_sym_eig_known_cases(dev):
         d.sym_eig(np.array([[1.0, 2.0], [1.0, 1.0]]), device=dev)
 
 
+def test_eig_svd_clustered_spectrum_falls_back(eig_dev):
+    # identity-like and repeated singular values: the tridiagonal path must
+    # hand over to Jacobi and still return orthonormal factors
+    f = d.eig_svd(np.eye(40), device=eig_dev)
+    np.testing.assert_allclose(f.s, np.ones(40), rtol=1e-13)
+    np.testing.assert_allclose(f.u @ f.v.T, np.eye(40), atol=1e-12)
+    q, _ = np.linalg.qr(np.random.default_rng(5).standard_normal((300, 30)))
+    sv = np.repeat([5.0, 3.0, 1.0], 10)
+    c = np.asfortranarray(q * sv)
+    f = d.eig_svd(c, device=eig_dev)
+    np.testing.assert_allclose(f.s, sv, rtol=1e-12)
+    np.testing.assert_allclose(f.v.T @ f.v, np.eye(30), atol=1e-12)
+    np.testing.assert_allclose((f.u * f.s) @ f.v.T, c, atol=1e-11)
+
+
+def test_solve_config1_both_eigensolvers(oracle, c1, eig_dev):
+    ref = oracle.solve(c1, 50, 25, tol=1e-2, alg="dash", seed=0)
+    res = d.solve(to_dev(c1), d.SolverConfig(k=50, s=25, tol=1e-2, seed=0), device=eig_dev)
+    check_solve(res, ref, 50)
+
+
 def test_eig_svd_known_cases(dev):
     # test_dense_core.cpp:134-154
     f = d.eig_svd(np.array([[3.0, 0.0], [0.0, 4.0], [0.0, 0.0]]), device=dev)
@@ -332,11 +353,19 @@ def test_eig_svd_rank_deficient(dev):
         d.eig_svd(np.zeros((2, 3)), device=dev)
 
 
-@pytest.mark.parametrize("shape", [(10000, 75), (5000, 150), (2000, 300)])
-def test_eig_svd_matches_oracle(dev, oracle, shape):
+@pytest.fixture(params=[0, 1], ids=["tridiagonal", "jacobi"])
+def eig_dev(request):
+    dv = d.Device(0)
+    dv.set_option("eig_method", request.param)
+    yield dv
+    dv.close()
+
+
+@pytest.mark.parametrize("shape", [(10000, 75), (5000, 150), (2000, 300), (400, 3), (900, 64)])
+def test_eig_svd_matches_oracle(eig_dev, oracle, shape):
     c = np.asfortranarray(np.random.default_rng(shape[0]).standard_normal(shape))
     u_ref, s_ref, v_ref = oracle.eig_svd(c)
-    f = d.eig_svd(c, device=dev)
+    f = d.eig_svd(c, device=eig_dev)
     np.testing.assert_allclose(f.s, s_ref, rtol=1e-12)
     # same sign convention -> same vectors up to roundoff
     np.testing.assert_allclose(f.v, v_ref, atol=1e-10)
