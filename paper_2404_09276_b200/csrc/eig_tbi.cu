@@ -386,21 +386,17 @@ void tbi_eig(const double* g, EigWorkspace& w, void* tbi_ws, int32_t* clustered,
     DSVD_LAUNCH_CHECK();
     const int lda = n | 1;
     const size_t s1 = sizeof(double) * (static_cast<size_t>(n) * lda + 2 * n);
-    static bool attr = false;
-    if (!attr) {
-        DSVD_CUDA_CHECK(cudaFuncSetAttribute(tbi_tridiag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             227 * 1024));
-        DSVD_CUDA_CHECK(cudaFuncSetAttribute(tbi_orth_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             227 * 1024));
-        attr = true;
-    }
+    const size_t s3 = sizeof(double) * 2 * static_cast<size_t>(n) * lda;
+    DSVD_CUDA_CHECK(cudaFuncSetAttribute(tbi_tridiag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(s1)));
+    DSVD_CUDA_CHECK(cudaFuncSetAttribute(tbi_orth_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(s3)));
     tbi_tridiag_kernel<<<1, kTbiThreads, s1, stream>>>(g, n, d, e, hv, tau, gate, nullptr);
     DSVD_LAUNCH_CHECK();
     const size_t s2 = sizeof(double) * (3 * static_cast<size_t>(n) + kTbiWarps * 5 * static_cast<size_t>(n));
     tbi_eig_kernel<<<static_cast<unsigned>(ceil_div(n, kTbiWarps)), 32 * kTbiWarps, s2, stream>>>(
         d, e, n, w.lam, z, n, clustered, gate, nullptr);
     DSVD_LAUNCH_CHECK();
-    const size_t s3 = sizeof(double) * 2 * static_cast<size_t>(n) * lda;
     tbi_orth_kernel<<<1, kTbiThreads, s3, stream>>>(z, n, n, gate, clustered);
     DSVD_LAUNCH_CHECK();
     tbi_backtransform_kernel<<<static_cast<unsigned>(ceil_div(n, 8)), 256, sizeof(double) * 8 * n, stream>>>(
