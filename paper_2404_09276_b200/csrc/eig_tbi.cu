@@ -286,13 +286,12 @@ tbi_eig_kernel(const double* __restrict__ dg, const double* __restrict__ eg, int
 
 // ---- 3. orthonormalisation: Z <- Z (3I - Z^T Z) / 2, twice -----------------------------
 __global__ void __launch_bounds__(kTbiThreads, 1)
-tbi_orth_kernel(double* __restrict__ z, int n, int ldz, const int32_t* __restrict__ gate,
-                const int32_t* __restrict__ skip) {
+tbi_orth_kernel(double* __restrict__ z, int n, int ldz, double* __restrict__ S,
+                const int32_t* __restrict__ gate, const int32_t* __restrict__ skip) {
     if ((gate != nullptr && *gate != 0) || (skip != nullptr && *skip != 0)) return;
     extern __shared__ double osm[];
     const int lds = n | 1;
-    double* Z = osm;             // n x lds
-    double* S = Z + n * lds;     // n x lds : 3I - Z^T Z, then scratch
+    double* Z = osm;  // n x lds in shared memory; S = (3I - Z^T Z)/2 lives in global (L2)
     for (int x = threadIdx.x; x < n * n; x += blockDim.x) {
         const int i = x / n, j = x % n;
         Z[i * lds + j] = z[static_cast<int64_t>(i) * ldz + j];
@@ -304,27 +303,30 @@ tbi_orth_kernel(double* __restrict__ z, int n, int ldz, const int32_t* __restric
             if (b < a) continue;
             double acc = 0.0;
             for (int t = 0; t < n; ++t) acc = fma(Z[t * lds + a], Z[t * lds + b], acc);
-            const double v = (a == b ? 3.0 : 0.0) - acc;
-            S[a * lds + b] = 0.5 * v;
-            S[b * lds + a] = 0.5 * v;
+            const double v = 0.5 * ((a == b ? 3.0 : 0.0) - acc);
+            S[a * n + b] = v;
+            S[b * n + a] = v;
         }
         __syncthreads();
-        // Z <- Z S, one row of Z per thread group (row kept in registers chunks)
+        // Z <- Z S: a warp per row of Z, lanes over columns; the row is read
+        // completely before it is overwritten
+        const int lane = threadIdx.x & 31;
         for (int i = threadIdx.x >> 5; i < n; i += blockDim.x >> 5) {
-            const int lane = threadIdx.x & 31;
             double out[8];
             const int nb = (n + 31) / 32;
-            for (int q = 0; q < nb && q < 8; ++q) {
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
                 const int col = lane + 32 * q;
                 double acc = 0.0;
-                if (col < n)
-                    for (int t = 0; t < n; ++t) acc = fma(Z[i * lds + t], S[t * lds + col], acc);
+                if (q < nb && col < n)
+                    for (int t = 0; t < n; ++t) acc = fma(Z[i * lds + t], S[t * n + col], acc);
                 out[q] = acc;
             }
             __syncwarp();
-            for (int q = 0; q < nb && q < 8; ++q) {
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
                 const int col = lane + 32 * q;
-                if (col < n) Z[i * lds + col] = out[q];
+                if (q < nb && col < n) Z[i * lds + col] = out[q];
             }
         }
         __syncthreads();
@@ -369,7 +371,7 @@ bool tbi_supported(int l) { return l >= 3 && l <= 160; }
 
 size_t tbi_workspace_bytes(int l) {
     const size_t n = l;
-    return sizeof(double) * (n * n /*hv*/ + n /*tau*/ + 2 * n /*d,e*/ + n * n /*z*/) + 64;
+    return sizeof(double) * (n * n /*hv*/ + n /*tau*/ + 2 * n /*d,e*/ + 2 * n * n /*z, S*/) + 64;
 }
 
 // Runs the tridiagonal path; sets *clustered (device) when the spectrum needs
@@ -386,7 +388,7 @@ void tbi_eig(const double* g, EigWorkspace& w, void* tbi_ws, int32_t* clustered,
     DSVD_LAUNCH_CHECK();
     const int lda = n | 1;
     const size_t s1 = sizeof(double) * (static_cast<size_t>(n) * lda + 2 * n);
-    const size_t s3 = sizeof(double) * 2 * static_cast<size_t>(n) * lda;
+    const size_t s3 = sizeof(double) * static_cast<size_t>(n) * lda;
     DSVD_CUDA_CHECK(cudaFuncSetAttribute(tbi_tridiag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(s1)));
     DSVD_CUDA_CHECK(cudaFuncSetAttribute(tbi_orth_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -397,7 +399,8 @@ void tbi_eig(const double* g, EigWorkspace& w, void* tbi_ws, int32_t* clustered,
     tbi_eig_kernel<<<static_cast<unsigned>(ceil_div(n, kTbiWarps)), 32 * kTbiWarps, s2, stream>>>(
         d, e, n, w.lam, z, n, clustered, gate, nullptr);
     DSVD_LAUNCH_CHECK();
-    tbi_orth_kernel<<<1, kTbiThreads, s3, stream>>>(z, n, n, gate, clustered);
+    tbi_orth_kernel<<<1, kTbiThreads, s3, stream>>>(z, n, n, z + static_cast<size_t>(n) * n, gate,
+                                                    clustered);
     DSVD_LAUNCH_CHECK();
     tbi_backtransform_kernel<<<static_cast<unsigned>(ceil_div(n, 8)), 256, sizeof(double) * 8 * n, stream>>>(
         hv, tau, z, n, n, w.vecs, w.lp, gate, clustered);
