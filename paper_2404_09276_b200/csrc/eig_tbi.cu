@@ -396,6 +396,8 @@ void tbi_eig(const double* g, EigWorkspace& w, void* tbi_ws, int32_t* clustered,
     tbi_tridiag_kernel<<<1, kTbiThreads, s1, stream>>>(g, n, d, e, hv, tau, gate, nullptr);
     DSVD_LAUNCH_CHECK();
     const size_t s2 = sizeof(double) * (3 * static_cast<size_t>(n) + kTbiWarps * 5 * static_cast<size_t>(n));
+    DSVD_CUDA_CHECK(cudaFuncSetAttribute(tbi_eig_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(s2)));
     tbi_eig_kernel<<<static_cast<unsigned>(ceil_div(n, kTbiWarps)), 32 * kTbiWarps, s2, stream>>>(
         d, e, n, w.lam, z, n, clustered, gate, nullptr);
     DSVD_LAUNCH_CHECK();
