@@ -95,7 +95,9 @@ tbi_tridiag_kernel(const double* __restrict__ g, int n, double* __restrict__ d, 
             // p = tau * A22 v   (warp per row, lanes over columns)
             for (int i = k1 + warp; i < n; i += nwarp) {
                 double acc = 0.0;
-                for (int j = k1 + lane; j < n; j += 32) acc = fma(L(i, j), v[j], acc);
+                const double* row = A + i * lda;
+                for (int j = k1 + lane; j <= i; j += 32) acc = fma(row[j], v[j], acc);
+                for (int j = i + 1 + lane; j < n; j += 32) acc = fma(A[j * lda + i], v[j], acc);
                 acc = warp_sum(acc);
                 if (lane == 0) w[i] = tau * acc;
             }
@@ -110,13 +112,11 @@ tbi_tridiag_kernel(const double* __restrict__ g, int n, double* __restrict__ d, 
             const double K = s_K;
             for (int i = k1 + tid; i < n; i += blockDim.x) w[i] = fma(-K, v[i], w[i]);
             __syncthreads();
-            // A22 -= v w^T + w v^T on the lower triangle
-            for (int x = tid; x < m * m; x += blockDim.x) {
-                const int i = k1 + x / m, j = k1 + x % m;
-                if (j <= i) {
-                    double& a = A[i * lda + j];
-                    a = a - v[i] * w[j] - w[i] * v[j];
-                }
+            // A22 -= v w^T + w v^T on the lower triangle (warp per row, lanes over j <= i)
+            for (int i = k1 + warp; i < n; i += nwarp) {
+                const double vi = v[i], wi = w[i];
+                double* row = A + i * lda;
+                for (int j = k1 + lane; j <= i; j += 32) row[j] = row[j] - vi * w[j] - wi * v[j];
             }
             __syncthreads();
         }
@@ -131,13 +131,19 @@ tbi_tridiag_kernel(const double* __restrict__ g, int n, double* __restrict__ d, 
 }
 
 // ---- 2. eigenvalues (multisection) and eigenvectors (inverse iteration) ----------------
+__device__ __forceinline__ double rcp_fast(double q) {
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(q));
+    return r * fma(-q, r, 2.0);  // one Newton step: ~2^-56; counts only need signs
+}
+
 __device__ int sturm_count(const double* d, const double* e2, int n, double x, double pivmin) {
     int cnt = 0;
     double q = d[0] - x;
     if (fabs(q) < pivmin) q = -pivmin;
     cnt += q < 0.0;
     for (int i = 1; i < n; ++i) {
-        q = (d[i] - x) - e2[i - 1] / q;
+        q = (d[i] - x) - e2[i - 1] * rcp_fast(q);
         if (fabs(q) < pivmin) q = -pivmin;
         cnt += q < 0.0;
     }
@@ -155,7 +161,7 @@ tbi_eig_kernel(const double* __restrict__ dg, const double* __restrict__ eg, int
     double* d = esm;                       // n
     double* e = d + n;                     // n
     double* e2 = e + n;                    // n
-    double* work = e2 + n;                 // kTbiWarps x 5n (per-warp LU / vector)
+    double* work = e2 + n;                 // kTbiWarps x 6n (per-warp LU + iterate)
     __shared__ double s_gl, s_gu, s_pivmin, s_tnorm;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     for (int i = tid; i < n; i += blockDim.x) {
@@ -218,7 +224,7 @@ tbi_eig_kernel(const double* __restrict__ dg, const double* __restrict__ eg, int
     // inverse iteration on (T - lmb I): LU with partial pivoting (the dgttrf /
     // dgttrs recurrences), three solves from a fixed non-degenerate start (lane 0)
     if (lane == 0) {
-        double* dd = work + warp * 5 * n;  // diagonal of U
+        double* dd = work + warp * 6 * n;  // diagonal of U
         double* du = dd + n;               // first superdiagonal of U
         double* du2 = du + n;              // second superdiagonal (fill-in)
         double* dl = du2 + n;              // multipliers
@@ -252,8 +258,8 @@ tbi_eig_kernel(const double* __restrict__ dg, const double* __restrict__ eg, int
             if (fabs(dd[i]) < tiny) dd[i] = copysign(tiny, dd[i]);
         }
         if (fabs(dd[n - 1]) < tiny) dd[n - 1] = copysign(tiny, dd[n - 1]);
-        double* x = z + j;  // column j of z (stride ldz) holds the iterate
-        auto X = [&](int i) -> double& { return x[static_cast<int64_t>(i) * ldz]; };
+        double* xs = sw + n;  // the iterate, in shared memory
+        auto X = [&](int i) -> double& { return xs[i]; };
         for (int i = 0; i < n; ++i) X(i) = 1.0 + 0.01 * ((i * 7 + j * 13) % 17);
         for (int pass = 0; pass < 3; ++pass) {
             for (int i = 0; i + 1 < n; ++i) {  // L^{-1} with the interchanges
@@ -282,78 +288,107 @@ tbi_eig_kernel(const double* __restrict__ dg, const double* __restrict__ eg, int
         const double inv = 1.0 / sqrt(s2);
         for (int i = 0; i < n; ++i) X(i) *= inv;
     }
+    __syncwarp();
+    for (int i = lane; i < n; i += 32) z[static_cast<int64_t>(i) * ldz + j] = work[warp * 6 * n + 5 * n + i];
 }
 
 // ---- 3. orthonormalisation: Z <- Z (3I - Z^T Z) / 2, twice -----------------------------
+// Z (n x n, global, row stride ldz) <- Z (3I - Z^T Z) / 2, twice. Phase a holds
+// Z in shared memory to form S = (3I - Z^T Z)/2 (written to global scratch);
+// phase b holds S in shared memory while each warp streams one row of Z
+// through registers. A step whose S is already I to 1e-15 is skipped.
 __global__ void __launch_bounds__(kTbiThreads, 1)
 tbi_orth_kernel(double* __restrict__ z, int n, int ldz, double* __restrict__ S,
                 const int32_t* __restrict__ gate, const int32_t* __restrict__ skip) {
     if ((gate != nullptr && *gate != 0) || (skip != nullptr && *skip != 0)) return;
     extern __shared__ double osm[];
+    __shared__ int s_dev;
     const int lds = n | 1;
-    double* Z = osm;  // n x lds in shared memory; S = (3I - Z^T Z)/2 lives in global (L2)
-    for (int x = threadIdx.x; x < n * n; x += blockDim.x) {
-        const int i = x / n, j = x % n;
-        Z[i * lds + j] = z[static_cast<int64_t>(i) * ldz + j];
-    }
-    __syncthreads();
+    double* M = osm;  // Z (phase a) or S (phase b), n x lds
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
     for (int step = 0; step < 2; ++step) {
+        if (threadIdx.x == 0) s_dev = 0;
         for (int x = threadIdx.x; x < n * n; x += blockDim.x) {
-            const int a = x / n, b = x % n;
-            if (b < a) continue;
-            double acc = 0.0;
-            for (int t = 0; t < n; ++t) acc = fma(Z[t * lds + a], Z[t * lds + b], acc);
-            const double v = 0.5 * ((a == b ? 3.0 : 0.0) - acc);
-            S[a * n + b] = v;
-            S[b * n + a] = v;
+            const int i = x / n, j = x - (x / n) * n;
+            M[i * lds + j] = z[static_cast<int64_t>(i) * ldz + j];
         }
         __syncthreads();
-        // Z <- Z S: a warp per row of Z, lanes over columns; the row is read
-        // completely before it is overwritten
-        const int lane = threadIdx.x & 31;
-        for (int i = threadIdx.x >> 5; i < n; i += blockDim.x >> 5) {
-            double out[8];
-            const int nb = (n + 31) / 32;
-#pragma unroll
-            for (int q = 0; q < 8; ++q) {
-                const int col = lane + 32 * q;
+        // S(a, b) for b >= a: warp per a, lanes over b
+        for (int a = warp; a < n; a += nwarp) {
+            for (int b = a + lane; b < n; b += 32) {
                 double acc = 0.0;
-                if (q < nb && col < n)
-                    for (int t = 0; t < n; ++t) acc = fma(Z[i * lds + t], S[t * n + col], acc);
-                out[q] = acc;
-            }
-            __syncwarp();
-#pragma unroll
-            for (int q = 0; q < 8; ++q) {
-                const int col = lane + 32 * q;
-                if (q < nb && col < n) Z[i * lds + col] = out[q];
+                for (int t = 0; t < n; ++t) acc = fma(M[t * lds + a], M[t * lds + b], acc);
+                const double v = 0.5 * ((a == b ? 3.0 : 0.0) - acc);
+                if (fabs(v - (a == b ? 1.0 : 0.0)) > 1e-15) s_dev = 1;
+                S[a * n + b] = v;
+                S[b * n + a] = v;
             }
         }
         __syncthreads();
-    }
-    for (int x = threadIdx.x; x < n * n; x += blockDim.x) {
-        const int i = x / n, j = x % n;
-        z[static_cast<int64_t>(i) * ldz + j] = Z[i * lds + j];
+        if (s_dev == 0) break;
+        for (int x = threadIdx.x; x < n * n; x += blockDim.x) {
+            const int i = x / n, j = x - (x / n) * n;
+            M[i * lds + j] = S[x];
+        }
+        __syncthreads();
+        const int nb = (n + 31) / 32;
+        for (int i = warp; i < n; i += nwarp) {
+            double zr[8], out[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const int col = lane + 32 * q;
+                zr[q] = (q < nb && col < n) ? z[static_cast<int64_t>(i) * ldz + col] : 0.0;
+                out[q] = 0.0;
+            }
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                if (q >= nb) break;
+                for (int tl = 0; tl < 32; ++tl) {
+                    const int t = 32 * q + tl;
+                    if (t >= n) break;
+                    const double zt = __shfl_sync(0xffffffffu, zr[q], tl);
+#pragma unroll
+                    for (int c = 0; c < 8; ++c) {
+                        const int col = lane + 32 * c;
+                        if (c < nb && col < n) out[c] = fma(zt, M[t * lds + col], out[c]);
+                    }
+                }
+            }
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+                const int col = lane + 32 * c;
+                if (c < nb && col < n) z[static_cast<int64_t>(i) * ldz + col] = out[c];
+            }
+        }
+        __syncthreads();
     }
 }
 
 // ---- 4. back-transform: V = H_0 H_1 ... H_{n-3} Z, one warp per column -------------
-__global__ void tbi_backtransform_kernel(const double* __restrict__ hv, const double* __restrict__ tau,
-                                         const double* __restrict__ z, int n, int ldz,
-                                         double* __restrict__ vecs, int ldv, const int32_t* __restrict__ gate,
-                                         const int32_t* __restrict__ skip) {
+constexpr int kBtWarps = 16;
+
+__global__ void __launch_bounds__(32 * kBtWarps, 1)
+tbi_backtransform_kernel(const double* __restrict__ hv, const double* __restrict__ tau,
+                         const double* __restrict__ z, int n, int ldz, double* __restrict__ vecs, int ldv,
+                         const int32_t* __restrict__ gate, const int32_t* __restrict__ skip) {
     if ((gate != nullptr && *gate != 0) || (skip != nullptr && *skip != 0)) return;
     extern __shared__ double bsm[];
+    double* H = bsm;                     // all reflectors, n x n (row k = v_k)
+    double* T = H + static_cast<size_t>(n) * n;  // tau, n
+    double* X = T + n;                   // kBtWarps x n columns being transformed
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int col = blockIdx.x * (blockDim.x >> 5) + warp;
+    for (int x = threadIdx.x; x < n * n; x += blockDim.x) H[x] = hv[x];
+    for (int x = threadIdx.x; x < n; x += blockDim.x) T[x] = tau[x];
+    const int col = blockIdx.x * kBtWarps + warp;
+    double* x = X + warp * n;
+    if (col < n)
+        for (int i = lane; i < n; i += 32) x[i] = z[static_cast<int64_t>(i) * ldz + col];
+    __syncthreads();
     if (col >= n) return;
-    double* x = bsm + warp * n;
-    for (int i = lane; i < n; i += 32) x[i] = z[static_cast<int64_t>(i) * ldz + col];
-    __syncwarp();
     for (int k = n - 3; k >= 0; --k) {
-        const double t = tau[k];
+        const double t = T[k];
         if (t == 0.0) continue;
-        const double* vk = hv + static_cast<int64_t>(k) * n;
+        const double* vk = H + static_cast<size_t>(k) * n;
         double s = 0.0;
         for (int i = k + 1 + lane; i < n; i += 32) s = fma(vk[i], x[i], s);
         s = warp_sum(s) * t;
@@ -395,7 +430,7 @@ void tbi_eig(const double* g, EigWorkspace& w, void* tbi_ws, int32_t* clustered,
                                          static_cast<int>(s3)));
     tbi_tridiag_kernel<<<1, kTbiThreads, s1, stream>>>(g, n, d, e, hv, tau, gate, nullptr);
     DSVD_LAUNCH_CHECK();
-    const size_t s2 = sizeof(double) * (3 * static_cast<size_t>(n) + kTbiWarps * 5 * static_cast<size_t>(n));
+    const size_t s2 = sizeof(double) * (3 * static_cast<size_t>(n) + kTbiWarps * 6 * static_cast<size_t>(n));
     DSVD_CUDA_CHECK(cudaFuncSetAttribute(tbi_eig_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(s2)));
     tbi_eig_kernel<<<static_cast<unsigned>(ceil_div(n, kTbiWarps)), 32 * kTbiWarps, s2, stream>>>(
@@ -404,7 +439,10 @@ void tbi_eig(const double* g, EigWorkspace& w, void* tbi_ws, int32_t* clustered,
     tbi_orth_kernel<<<1, kTbiThreads, s3, stream>>>(z, n, n, z + static_cast<size_t>(n) * n, gate,
                                                     clustered);
     DSVD_LAUNCH_CHECK();
-    tbi_backtransform_kernel<<<static_cast<unsigned>(ceil_div(n, 8)), 256, sizeof(double) * 8 * n, stream>>>(
+    const size_t s4 = sizeof(double) * (static_cast<size_t>(n) * n + n + kBtWarps * static_cast<size_t>(n));
+    DSVD_CUDA_CHECK(cudaFuncSetAttribute(tbi_backtransform_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(s4)));
+    tbi_backtransform_kernel<<<static_cast<unsigned>(ceil_div(n, kBtWarps)), 32 * kBtWarps, s4, stream>>>(
         hv, tau, z, n, n, w.vecs, w.lp, gate, clustered);
     DSVD_LAUNCH_CHECK();
 }
