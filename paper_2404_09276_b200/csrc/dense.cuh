@@ -37,6 +37,19 @@ void rescale(const double* c, int64_t n, int64_t K, int64_t ldc, const double* w
              const double* scale, int64_t ncol, double* out, int64_t ld_out, int out_colmajor,
              const int32_t* gate, cudaStream_t stream);
 
+// FP64 tensor-core versions used inside the solve (dmma.cu): same contracts as
+// gram / rescale (rescale's scale folded into W), summation order not the
+// reference's FMA chain. Workspace from the *_workspace_bytes functions.
+bool gram_dmma_supported(int64_t l, int64_t ld);
+size_t gram_dmma_workspace_bytes(int64_t n, int64_t l);
+void gram_dmma(const double* c, int64_t n, int64_t l, int64_t ld, double* g, void* ws, const int32_t* gate,
+               cudaStream_t stream);
+bool rescale_dmma_supported(int64_t K, int64_t ldc, int64_t ld_out, int out_colmajor);
+size_t rescale_dmma_workspace_bytes(int64_t K, int64_t width);
+void rescale_dmma(const double* c, int64_t n, int64_t K, int64_t ldc, const double* w, int64_t ldw,
+                  const double* scale, int64_t ncol, double* out, int64_t ld_out, int out_colmajor, void* ws,
+                  const int32_t* gate, cudaStream_t stream);
+
 // Column-major (rows x cols) <-> row-major (stride ld, pad columns zeroed).
 void colmajor_to_rowmajor(const double* src, int64_t rows, int64_t cols, double* dst, int64_t ld,
                           cudaStream_t stream);

@@ -1,0 +1,340 @@
+// FP64 tensor-core (DMMA, mma.sync m8n8k4 f64) kernels for the two dense
+// products of every power iteration (eigSVD, decompositions.cpp:52-73):
+//
+//   gram_dmma    G = C^T C for row-major C (n x l): one warp per pair of
+//                block rows (a, NB-1-a) of the 8x8-blocked upper triangle, so
+//                every warp issues NB+1 DMMAs per 4-row k-step; C is staged
+//                16 rows at a time by cp.async; per-CTA partial triangles are
+//                summed in a fixed order (deterministic, not the reference's
+//                single FMA chain; the eigensolver is not bitwise either).
+//   rescale_dmma out = C (W diag(scale)) for the 150-wide tall-skinny blocks:
+//                CTA tile 128 rows x 32 columns, the W column block resident
+//                in shared memory (pre-transposed, scale folded in), C staged
+//                16 k at a time through a 4-deep cp.async ring with an XOR
+//                swizzle so every fragment load is one conflict-free LDS.128.
+//
+// B200 runs DMMA and DFMA at the same peak (~37 TFLOP/s measured,
+// tools/micro/dmma_tput.cu) but one DMMA carries 256 FMAs, which leaves issue
+// slots for the operand loads; the register-tiled DFMA kernels these replace
+// reached ~26% of the FP64 pipe.
+#include "dense.cuh"
+
+namespace dsvd {
+
+namespace {
+
+__device__ __forceinline__ void dmma884(double2& d, double a, double b) {
+    asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+        : "+d"(d.x), "+d"(d.y)
+        : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ void cpa16z(void* dst, const void* src, bool valid) {
+    const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+    const int sz = valid ? 16 : 0;
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(src), "r"(sz));
+}
+__device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cpa_wait() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+// ---- rescale ----------------------------------------------------------------------
+constexpr int kRsBM = 128, kRsBN = 32, kRsBK = 16, kRsStages = 4, kRsThreads = 256;
+constexpr int kRsMaxK = 160;
+
+// wt[nn][k] = (k < K && nn < ncol) ? w[k][nn] * scale[nn] : 0, nn < npad, k < ldb
+__global__ void rescale_prep_kernel(const double* __restrict__ w, int64_t ldw, const double* __restrict__ scale,
+                                    int K, int ncol, int npad, int ldb, double* __restrict__ wt,
+                                    const int32_t* __restrict__ gate) {
+    if (gate != nullptr && *gate != 0) return;
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < npad * ldb; e += gridDim.x * blockDim.x) {
+        const int nn = e / ldb, k = e - nn * ldb;
+        double v = 0.0;
+        if (k < K && nn < ncol) v = w[static_cast<int64_t>(k) * ldw + nn] * (scale != nullptr ? scale[nn] : 1.0);
+        wt[e] = v;
+    }
+}
+
+__global__ void __launch_bounds__(kRsThreads, 2)
+rescale_dmma_kernel(const double* __restrict__ c, int64_t n, int K, int64_t ldc, const double* __restrict__ wt,
+                    int ldb, int ncol, double* __restrict__ out, int64_t ld_out, int out_colmajor,
+                    const int32_t* __restrict__ gate) {
+    if (gate != nullptr && *gate != 0) return;
+    extern __shared__ __align__(16) double rsm[];
+    double* Bt = rsm;                // [32][ldb]: W block, transposed
+    double* As = rsm + kRsBN * ldb;  // [stages][128][16], 8-double halves XOR-swizzled by row parity
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int q = lane & 3, g = lane >> 2;
+    const int j0 = blockIdx.x * kRsBN;
+    const int nk = (K + kRsBK - 1) / kRsBK;
+    const int64_t nrb = (n + kRsBM - 1) / kRsBM;
+    for (int e = tid; e < kRsBN * ldb / 2; e += kRsThreads)
+        cpa16z(Bt + 2 * e, wt + static_cast<int64_t>(j0) * ldb + 2 * e, true);
+    cpa_commit();
+    for (int64_t rb = blockIdx.y; rb < nrb; rb += gridDim.y) {
+        const int64_t r0 = rb * kRsBM;
+        auto load_a = [&](int slot, int kc) {
+            double* dst = As + slot * (kRsBM * kRsBK);
+            const int k0 = kc * kRsBK;
+            for (int e = tid; e < kRsBM * (kRsBK / 2); e += kRsThreads) {
+                const int r = e >> 3, ch = e & 7;
+                const int64_t gr = r0 + r;
+                const int k = k0 + 2 * ch;
+                const bool ok = gr < n && k < ldc;
+                double* d = dst + r * kRsBK + ((((ch >> 2) ^ (r & 1)) << 3) | ((2 * ch) & 7));
+                cpa16z(d, ok ? c + gr * ldc + k : c, ok);
+            }
+        };
+        for (int s = 0; s < kRsStages - 1; ++s) {
+            if (s < nk) load_a(s, s);
+            cpa_commit();
+        }
+        double2 acc[2][4];
+#pragma unroll
+        for (int a = 0; a < 2; ++a)
+#pragma unroll
+            for (int b = 0; b < 4; ++b) acc[a][b] = make_double2(0.0, 0.0);
+        for (int kc = 0; kc < nk; ++kc) {
+            cpa_wait<kRsStages - 2>();
+            __syncthreads();
+            const int pf = kc + kRsStages - 1;
+            if (pf < nk) load_a(pf % kRsStages, pf);
+            cpa_commit();
+            const double* A = As + (kc % kRsStages) * (kRsBM * kRsBK);
+#pragma unroll
+            for (int p = 0; p < 2; ++p) {
+                double2 af[2], bf[4];
+#pragma unroll
+                for (int mb = 0; mb < 2; ++mb) {
+                    const int r = warp * 16 + mb * 8 + g;
+                    af[mb] = *reinterpret_cast<const double2*>(A + r * kRsBK + ((p ^ (r & 1)) << 3) + 2 * q);
+                }
+                const int kg = kc * kRsBK + p * 8 + 2 * q;
+#pragma unroll
+                for (int nb = 0; nb < 4; ++nb)
+                    bf[nb] = *reinterpret_cast<const double2*>(Bt + (nb * 8 + g) * ldb + kg);
+#pragma unroll
+                for (int mb = 0; mb < 2; ++mb)
+#pragma unroll
+                    for (int nb = 0; nb < 4; ++nb) {
+                        dmma884(acc[mb][nb], af[mb].x, bf[nb].x);
+                        dmma884(acc[mb][nb], af[mb].y, bf[nb].y);
+                    }
+            }
+        }
+        cpa_wait<0>();
+        __syncthreads();  // the ring is reused by the next row block
+#pragma unroll
+        for (int mb = 0; mb < 2; ++mb) {
+            const int64_t r = r0 + warp * 16 + mb * 8 + g;
+            if (r >= n) continue;
+#pragma unroll
+            for (int nb = 0; nb < 4; ++nb) {
+                const int j = j0 + nb * 8 + 2 * q;
+                const double2 v = acc[mb][nb];
+                if (out_colmajor) {
+                    if (j < ncol) out[static_cast<int64_t>(j) * n + r] = v.x;
+                    if (j + 1 < ncol) out[static_cast<int64_t>(j + 1) * n + r] = v.y;
+                } else if (j + 1 < ld_out) {
+                    *reinterpret_cast<double2*>(out + r * ld_out + j) = v;
+                } else if (j < ld_out) {
+                    out[r * ld_out + j] = v.x;
+                }
+            }
+        }
+    }
+}
+
+// ---- gram -------------------------------------------------------------------------
+constexpr int kGmRows = 16, kGmStages = 3;
+
+__host__ __device__ constexpr int gm_pairs(int nb) { return nb * (nb + 1) / 2; }
+__host__ __device__ constexpr int gm_stride(int nb) { return nb % 2 ? nb * 8 : nb * 8 + 8; }
+__device__ __forceinline__ int gm_tri(int a, int j, int nb) { return a * nb - a * (a - 1) / 2 + (j - a); }
+
+template <int NB>
+__global__ void __launch_bounds__(32 * ((NB + 1) / 2))
+gram_dmma_kernel(const double* __restrict__ c, int64_t n, int64_t ld, int64_t rows_per_block,
+                 double* __restrict__ partial, const int32_t* __restrict__ gate) {
+    if (gate != nullptr && *gate != 0) return;
+    constexpr int S = gm_stride(NB);
+    extern __shared__ __align__(16) double gsm[];  // [stages][kGmRows][S]
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int q = lane & 3, g = lane >> 2;
+    const int a = warp, b = NB - 1 - warp;  // block rows of this warp (a == b: middle row)
+    const int64_t r_beg = static_cast<int64_t>(blockIdx.x) * rows_per_block;
+    const int64_t r_end = min(n, r_beg + rows_per_block);
+    const int vec = static_cast<int>(ld / 2);
+    // columns [ld, S) are never written by cp.async: zero them once
+    for (int e = tid; e < kGmStages * kGmRows * (S - 2 * vec); e += blockDim.x) {
+        const int row = e / (S - 2 * vec), col = 2 * vec + e % (S - 2 * vec);
+        gsm[row * S + col] = 0.0;
+    }
+    auto stage = [&](int slot, int64_t rr0) {
+        double* dst = gsm + slot * kGmRows * S;
+        for (int e = tid; e < kGmRows * vec; e += blockDim.x) {
+            const int r = e / vec, v = e - r * vec;
+            const int64_t gr = rr0 + r;
+            const bool ok = gr < r_end;
+            cpa16z(dst + r * S + 2 * v, ok ? c + gr * ld + 2 * v : c, ok);
+        }
+    };
+    const int nst = static_cast<int>(((r_end > r_beg ? r_end - r_beg : int64_t(0)) + kGmRows - 1) / kGmRows);
+    for (int s = 0; s < kGmStages - 1; ++s) {
+        if (s < nst) stage(s, r_beg + s * kGmRows);
+        cpa_commit();
+    }
+    double2 accA[NB], accB[NB];
+#pragma unroll
+    for (int j = 0; j < NB; ++j) accA[j] = accB[j] = make_double2(0.0, 0.0);
+    for (int st = 0; st < nst; ++st) {
+        cpa_wait<kGmStages - 2>();
+        __syncthreads();
+        const int pf = st + kGmStages - 1;
+        if (pf < nst) stage(pf % kGmStages, r_beg + static_cast<int64_t>(pf) * kGmRows);
+        cpa_commit();
+        const double* C = gsm + (st % kGmStages) * kGmRows * S;
+#pragma unroll
+        for (int ks = 0; ks < kGmRows / 4; ++ks) {
+            const double* row = C + (4 * ks + q) * S + g;
+            const double fa = row[8 * a], fb = row[8 * b];
+#pragma unroll
+            for (int j = 0; j < NB; ++j) {
+                if (j >= a) {
+                    const double fj = row[8 * j];
+                    dmma884(accA[j], fa, fj);
+                    if (j >= b && b != a) dmma884(accB[j], fb, fj);
+                }
+            }
+        }
+    }
+    cpa_wait<0>();
+    double* out = partial + static_cast<int64_t>(blockIdx.x) * gm_pairs(NB) * 64;
+#pragma unroll
+    for (int j = 0; j < NB; ++j) {
+        if (j >= a)
+            *reinterpret_cast<double2*>(out + gm_tri(a, j, NB) * 64 + g * 8 + 2 * q) = accA[j];
+        if (j >= b && b != a)
+            *reinterpret_cast<double2*>(out + gm_tri(b, j, NB) * 64 + g * 8 + 2 * q) = accB[j];
+    }
+}
+
+// G(i, j) = G(j, i) = sum over CTAs of the partial block entry: 256 threads per
+// 8x8 block, four interleaved partial sums combined in a fixed order.
+__global__ void __launch_bounds__(256)
+gram_dmma_reduce_kernel(const double* __restrict__ partial, int nblk, int nb, int64_t l, double* __restrict__ g,
+                        const int32_t* __restrict__ gate) {
+    if (gate != nullptr && *gate != 0) return;
+    __shared__ double red[4][64];
+    const int t = blockIdx.x, npair = nb * (nb + 1) / 2;
+    const int w = threadIdx.x & 63, part = threadIdx.x >> 6;
+    double s0 = 0.0, s1 = 0.0;
+    int bb = part;
+    for (; bb + 4 < nblk; bb += 8) {
+        s0 += partial[(static_cast<int64_t>(bb) * npair + t) * 64 + w];
+        s1 += partial[(static_cast<int64_t>(bb + 4) * npair + t) * 64 + w];
+    }
+    if (bb < nblk) s0 += partial[(static_cast<int64_t>(bb) * npair + t) * 64 + w];
+    red[part][w] = s0 + s1;
+    __syncthreads();
+    if (part != 0) return;
+    const double s = (red[0][w] + red[1][w]) + (red[2][w] + red[3][w]);
+    int ta = 0, rem = t;
+    while (rem >= nb - ta) {
+        rem -= nb - ta;
+        ++ta;
+    }
+    const int64_t i = 8 * ta + w / 8, j = 8 * (ta + rem) + w % 8;
+    if (i >= l || j >= l || i > j) return;
+    g[i * l + j] = s;
+    g[j * l + i] = s;
+}
+
+template <int NB>
+void launch_gram_dmma(const double* c, int64_t n, int64_t ld, int nblk, int64_t rpb, double* partial,
+                      const int32_t* gate, cudaStream_t stream) {
+    const size_t smem = sizeof(double) * kGmStages * kGmRows * gm_stride(NB);
+    DSVD_CUDA_CHECK(cudaFuncSetAttribute(gram_dmma_kernel<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem)));
+    gram_dmma_kernel<NB><<<nblk, 32 * ((NB + 1) / 2), smem, stream>>>(c, n, ld, rpb, partial, gate);
+    DSVD_LAUNCH_CHECK();
+}
+
+struct GramDmmaPlan {
+    int nb = 0, nblk = 0;
+    int64_t rpb = 0;
+};
+GramDmmaPlan gram_dmma_plan(int64_t n, int64_t l) {
+    GramDmmaPlan p;
+    p.nb = static_cast<int>((l + 7) / 8);
+    const int warps = (p.nb + 1) / 2;  // ~150 registers per thread: one CTA per SM at 10 warps
+    p.nblk = static_cast<int>(
+        std::max<int64_t>(1, std::min<int64_t>(kNumSMs * std::max(1, 10 / warps), ceil_div(n, 64))));
+    p.rpb = ceil_div(ceil_div(n, p.nblk), kGmRows) * kGmRows;
+    p.nblk = static_cast<int>(std::max<int64_t>(1, ceil_div(n, p.rpb)));
+    return p;
+}
+
+}  // namespace
+
+bool gram_dmma_supported(int64_t l, int64_t ld) { return l >= 1 && (l + 7) / 8 <= 20 && ld % 2 == 0 && ld >= l; }
+
+size_t gram_dmma_workspace_bytes(int64_t n, int64_t l) {
+    const GramDmmaPlan p = gram_dmma_plan(n, l);
+    return sizeof(double) * static_cast<size_t>(p.nblk) * gm_pairs(p.nb) * 64;
+}
+
+void gram_dmma(const double* c, int64_t n, int64_t l, int64_t ld, double* g, void* ws, const int32_t* gate,
+               cudaStream_t stream) {
+    const GramDmmaPlan p = gram_dmma_plan(n, l);
+    double* partial = static_cast<double*>(ws);
+    switch (p.nb) {
+#define DSVD_GRAM_CASE(NB) \
+    case NB: launch_gram_dmma<NB>(c, n, ld, p.nblk, p.rpb, partial, gate, stream); break;
+        DSVD_GRAM_CASE(1) DSVD_GRAM_CASE(2) DSVD_GRAM_CASE(3) DSVD_GRAM_CASE(4) DSVD_GRAM_CASE(5)
+        DSVD_GRAM_CASE(6) DSVD_GRAM_CASE(7) DSVD_GRAM_CASE(8) DSVD_GRAM_CASE(9) DSVD_GRAM_CASE(10)
+        DSVD_GRAM_CASE(11) DSVD_GRAM_CASE(12) DSVD_GRAM_CASE(13) DSVD_GRAM_CASE(14) DSVD_GRAM_CASE(15)
+        DSVD_GRAM_CASE(16) DSVD_GRAM_CASE(17) DSVD_GRAM_CASE(18) DSVD_GRAM_CASE(19) DSVD_GRAM_CASE(20)
+#undef DSVD_GRAM_CASE
+        default: fail(DSVD_OTHER, "gram_dmma: unsupported width");
+    }
+    gram_dmma_reduce_kernel<<<gm_pairs(p.nb), 256, 0, stream>>>(partial, p.nblk, p.nb, l, g, gate);
+    DSVD_LAUNCH_CHECK();
+}
+
+bool rescale_dmma_supported(int64_t K, int64_t ldc, int64_t ld_out, int out_colmajor) {
+    return K >= 1 && K <= kRsMaxK && ldc % 2 == 0 && ldc >= K && (out_colmajor || ld_out % 2 == 0);
+}
+
+size_t rescale_dmma_workspace_bytes(int64_t K, int64_t width) {
+    const int64_t kpad = ceil_div(K, kRsBK) * kRsBK;
+    const int64_t ldb = kpad + 8;
+    return sizeof(double) * static_cast<size_t>(ceil_div(width, kRsBN) * kRsBN * ldb);
+}
+
+void rescale_dmma(const double* c, int64_t n, int64_t K, int64_t ldc, const double* w, int64_t ldw,
+                  const double* scale, int64_t ncol, double* out, int64_t ld_out, int out_colmajor, void* ws,
+                  const int32_t* gate, cudaStream_t stream) {
+    if (n == 0) return;
+    const int64_t width = out_colmajor ? ncol : ld_out;
+    const int ncb = static_cast<int>(ceil_div(width, kRsBN));
+    const int ldb = static_cast<int>(ceil_div(K, kRsBK) * kRsBK + 8);  // == 8 (mod 16): conflict-free B loads
+    double* wt = static_cast<double*>(ws);
+    const int npad = ncb * kRsBN;
+    rescale_prep_kernel<<<static_cast<unsigned>(ceil_div(static_cast<int64_t>(npad) * ldb, 256)), 256, 0, stream>>>(
+        w, ldw, scale, static_cast<int>(K), static_cast<int>(ncol), npad, ldb, wt, gate);
+    DSVD_LAUNCH_CHECK();
+    const size_t smem = sizeof(double) * (static_cast<size_t>(kRsBN) * ldb + kRsStages * kRsBM * kRsBK);
+    DSVD_CUDA_CHECK(cudaFuncSetAttribute(rescale_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem)));
+    const int64_t nrb = ceil_div(n, kRsBM);
+    const dim3 grid(static_cast<unsigned>(ncb), static_cast<unsigned>(std::min<int64_t>(nrb, 65535)));
+    rescale_dmma_kernel<<<grid, kRsThreads, smem, stream>>>(c, n, static_cast<int>(K), ldc, wt, ldb,
+                                                            static_cast<int>(ncol), out, ld_out, out_colmajor,
+                                                            gate);
+    DSVD_LAUNCH_CHECK();
+}
+
+}  // namespace dsvd

@@ -7,8 +7,9 @@
 //   2. tbi_eig_kernel      — one warp per eigenvalue: 33-way multisection on
 //      Sturm counts (each lane evaluates one point) to full precision, then
 //      inverse iteration with a partially pivoted tridiagonal LU (lane 0).
-//   3. tbi_orth_kernel     — two Newton-Schulz polar steps Z <- Z (3I - Z^T Z)/2
-//      make the eigenvectors orthonormal to working precision.
+//   3. tbi_ns_kernel       — two Newton-Schulz polar steps Z <- Z (3I - Z^T Z)/2
+//      (four small GEMMs on all SMs) make the eigenvectors orthonormal to
+//      working precision.
 //   4. tbi_backtransform_kernel — V = H_0 ... H_{n-3} Z, one warp per column, on
 //      all SMs.
 //
@@ -28,7 +29,6 @@ namespace dsvd {
 
 namespace {
 
-constexpr int kTbiThreads = 1024;
 constexpr double kTbiGap = 1e-9;  // minimum relative eigenvalue gap for inverse iteration
 
 __device__ __forceinline__ double warp_sum(double v) {
@@ -61,7 +61,45 @@ __device__ __forceinline__ void load_square(double* __restrict__ dst, int lds, c
 // ---- 1. Householder tridiagonalisation ---------------------------------------
 // A (n x n, symmetric) in shared memory, lower triangle authoritative, stride
 // lda = n | 1. Outputs d (n), e (n-1), reflectors hv[k*n + i] (i > k) and tau[k].
-__global__ void __launch_bounds__(kTbiThreads, 1)
+//
+// Two block barriers per step and no redundant scalar work on the critical
+// path:
+//   (b) p = A22 x with x = column k as stored (T threads per row); the row
+//       owner applies the v0 substitution, v_{k1} = v0 instead of x0, as
+//       p += (v0 - x0) A(:, k1), and scales by tau;
+//   (c) K = tau/2 w.v per warp, then A22 -= v w^T + (w - 2K v) v^T. Warp 0
+//       updates column k1 first and immediately derives the next reflector
+//       (alpha, tau, v0) from it while warps 1.. update the columns right of k1.
+// The reflector scalars are double-buffered by step parity.
+constexpr int kTridThreads = 512;
+
+struct Reflector {
+    double tau, v0, x0, alpha;
+};
+
+// Householder reflector of column c (rows c+1 .. n-1), evaluated by one warp.
+__device__ __forceinline__ Reflector make_reflector(const double* A, int lda, int n, int c, int lane) {
+    double sig = 0.0;
+    for (int i = c + 1 + lane; i < n; i += 32) {
+        const double x = A[i * lda + c];
+        sig = fma(x, x, sig);
+    }
+    sig = warp_sum(sig);
+    Reflector r;
+    r.x0 = A[(c + 1) * lda + c];
+    r.alpha = r.x0;
+    r.tau = 0.0;
+    r.v0 = r.x0;
+    const double tail = sig - r.x0 * r.x0;  // sum of squares below the first entry
+    if (tail > 0.0) {
+        r.alpha = -copysign(sqrt(sig), r.x0);
+        r.v0 = r.x0 - r.alpha;
+        r.tau = 2.0 / (tail + r.v0 * r.v0);
+    }
+    return r;
+}
+
+__global__ void __launch_bounds__(kTridThreads, 1)
 tbi_tridiag_kernel(const double* __restrict__ g, int n, double* __restrict__ d, double* __restrict__ e,
                    double* __restrict__ hv, double* __restrict__ tau_out, const int32_t* __restrict__ gate,
                    const int32_t* __restrict__ skip) {
@@ -69,90 +107,124 @@ tbi_tridiag_kernel(const double* __restrict__ g, int n, double* __restrict__ d, 
     extern __shared__ double tsm[];
     const int lda = n | 1;
     double* A = tsm;                 // n x lda
-    double* v = A + n * lda;         // n
-    double* w = v + n;               // n
-    __shared__ double s_tau, s_K;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarp = blockDim.x >> 5;
+    double* v = A + n * lda;         // n: v of the current step
+    double* w = v + n;               // n: p = tau A22 v
+    __shared__ Reflector s_ref[2];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nthr = blockDim.x;
     load_square(A, lda, g, n, n);
     __syncthreads();
-    auto L = [&](int i, int j) -> double& { return i >= j ? A[i * lda + j] : A[j * lda + i]; };
-    // four threads per row for the O(m^2) parts: row = tid / 4, quarter q = tid % 4
-    const int rq = tid & 3, rgrp = tid >> 2, ngrp = blockDim.x >> 2;
+    if (warp == 0) {
+        const Reflector r = make_reflector(A, lda, n, 0, lane);
+        if (lane == 0) s_ref[0] = r;
+    }
+    __syncthreads();
     for (int k = 0; k + 2 < n; ++k) {
         const int k1 = k + 1, m = n - k1;
-        if (warp == 0) {
-            double sig = 0.0;
-            for (int i = k1 + lane; i < n; i += 32) {
-                const double x = L(i, k);
-                sig = fma(x, x, sig);
+        const Reflector ref = s_ref[k & 1];
+        if (tid == 0) {
+            tau_out[k] = ref.tau;
+            e[k] = ref.alpha;
+            d[k] = A[k * lda + k];
+        }
+        if (ref.tau == 0.0) {  // column already reduced (uniform across the block)
+            for (int i = k1 + tid; i < n; i += nthr) hv[static_cast<int64_t>(k) * n + i] = A[i * lda + k];
+            if (warp == 0 && k1 + 2 < n) {
+                const Reflector r = make_reflector(A, lda, n, k1, lane);
+                if (lane == 0) s_ref[k1 & 1] = r;
             }
-            sig = warp_sum(sig);
-            const double x0 = L(k1, k);
-            double alpha = 0.0, tau = 0.0, v0 = x0;
-            const double tail = sig - x0 * x0;  // sum of squares below the first entry
-            if (tail > 0.0) {
-                alpha = -copysign(sqrt(sig), x0);
-                v0 = x0 - alpha;
-                tau = 2.0 / (tail + v0 * v0);
-            } else {
-                alpha = x0;  // already tridiagonal in this column
+            __syncthreads();
+            continue;
+        }
+        // (b)
+        {
+            int lg = 5;
+            while (lg > 0 && (m << lg) > nthr) --lg;
+            const int T = 1 << lg, r = tid >> lg, sub = tid & (T - 1);
+            const int i = k1 + r;
+            double a0 = 0.0, a1 = 0.0;
+            if (r < m) {
+                const double* row = A + i * lda;
+                int j = k1 + sub;
+                for (; j + T <= i; j += 2 * T) {
+                    a0 = fma(row[j], A[j * lda + k], a0);
+                    a1 = fma(row[j + T], A[(j + T) * lda + k], a1);
+                }
+                if (j <= i) {
+                    a0 = fma(row[j], A[j * lda + k], a0);
+                    j += T;
+                }
+                for (; j + T < n; j += 2 * T) {
+                    a0 = fma(A[j * lda + i], A[j * lda + k], a0);
+                    a1 = fma(A[(j + T) * lda + i], A[(j + T) * lda + k], a1);
+                }
+                if (j < n) a0 = fma(A[j * lda + i], A[j * lda + k], a0);
             }
-            for (int i = k1 + lane; i < n; i += 32) {
-                const double vi = (i == k1) ? v0 : L(i, k);
+            double acc = a0 + a1;
+            for (int o = 1; o < T; o <<= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+            if (r < m && sub == 0) {
+                acc = fma(ref.v0 - ref.x0, A[i * lda + k1], acc);
+                const double vi = i == k1 ? ref.v0 : A[i * lda + k];
+                w[i] = ref.tau * acc;
                 v[i] = vi;
                 hv[static_cast<int64_t>(k) * n + i] = vi;
             }
-            if (lane == 0) {
-                s_tau = tau;
-                tau_out[k] = tau;
-                e[k] = alpha;
-                d[k] = L(k, k);
+        }
+        __syncthreads();
+        // (c)
+        {
+            double kk = 0.0;
+            for (int i = k1 + lane; i < n; i += 32) kk = fma(w[i], v[i], kk);
+            const double K2 = ref.tau * warp_sum(kk);  // 2K
+            if (warp == 0) {
+                const double vj = v[k1], wj = w[k1];
+                for (int i = k1 + lane; i < n; i += 32) {
+                    const double vi = v[i], wi = fma(-K2, vi, w[i]);
+                    double& a = A[i * lda + k1];
+                    a = fma(-vi, wj, fma(-wi, vj, a));
+                }
+                __syncwarp();
+                if (k1 + 2 < n) {
+                    const Reflector r = make_reflector(A, lda, n, k1, lane);
+                    if (lane == 0) s_ref[k1 & 1] = r;
+                }
+            } else {
+                // rows k1 + r (r = 1 .. m-1) hold r entries right of column k1;
+                // rows r and m - r are paired (m entries per pair)
+                const int npair = m >> 1;
+                if (npair > 0) {
+                    const int t = tid - 32, nt = nthr - 32;
+                    const int T2 = nt / npair;
+                    const int p = static_cast<int>((t + 0.5f) / static_cast<float>(T2));
+                    const int sub = t - p * T2;
+                    if (p < npair) {
+                        const int r1 = p + 1;
+                        int i = k1 + r1;
+                        double vi = v[i], wi = fma(-K2, vi, w[i]);
+                        double* row = A + i * lda + k1 + 1;
+                        const double* vv = v + k1 + 1;
+                        const double* ww = w + k1 + 1;
+                        int q = sub;
+                        for (; q < r1; q += T2) row[q] = fma(-vi, ww[q], fma(-wi, vv[q], row[q]));
+                        const int r2 = m - r1;
+                        if (r2 != r1) {
+                            i = k1 + r2;
+                            vi = v[i];
+                            wi = fma(-K2, vi, w[i]);
+                            row = A + i * lda + k1 + 1;
+                            for (q -= r1; q < r2; q += T2) row[q] = fma(-vi, ww[q], fma(-wi, vv[q], row[q]));
+                        }
+                    }
+                }
             }
         }
         __syncthreads();
-        const double tau = s_tau;
-        if (tau != 0.0) {
-            // p = tau * A22 v: four threads per row (n <= 160 < 256 groups), each a
-            // quarter of the columns; every lane reaches the shuffles
-            {
-                const int i = k1 + rgrp;
-                double acc = 0.0;
-                if (i < n) {
-                    const double* row = A + i * lda;
-                    for (int j = k1 + rq; j <= i; j += 4) acc = fma(row[j], v[j], acc);
-                    for (int j = i + 1 + ((rq - (i + 1 - k1)) & 3); j < n; j += 4)
-                        acc = fma(A[j * lda + i], v[j], acc);
-                }
-                acc += __shfl_xor_sync(0xffffffffu, acc, 1);
-                acc += __shfl_xor_sync(0xffffffffu, acc, 2);
-                if (i < n && rq == 0) w[i] = tau * acc;
-            }
-            __syncthreads();
-            if (warp == 0) {
-                double acc = 0.0;
-                for (int i = k1 + lane; i < n; i += 32) acc = fma(w[i], v[i], acc);
-                acc = warp_sum(acc);
-                if (lane == 0) s_K = 0.5 * tau * acc;
-            }
-            __syncthreads();
-            const double K = s_K;
-            for (int i = k1 + tid; i < n; i += blockDim.x) w[i] = fma(-K, v[i], w[i]);
-            __syncthreads();
-            // A22 -= v w^T + w v^T on the lower triangle, four threads per row
-            for (int i = k1 + rgrp; i < n; i += ngrp) {
-                const double vi = v[i], wi = w[i];
-                double* row = A + i * lda;
-                for (int j = k1 + rq; j <= i; j += 4) row[j] = row[j] - vi * w[j] - wi * v[j];
-            }
-            __syncthreads();
-        }
     }
     if (tid == 0) {
         if (n >= 2) {
-            d[n - 2] = L(n - 2, n - 2);
-            e[n - 2] = L(n - 1, n - 2);
+            d[n - 2] = A[(n - 2) * lda + (n - 2)];
+            e[n - 2] = A[(n - 1) * lda + (n - 2)];
         }
-        d[n - 1] = L(n - 1, n - 1);
+        d[n - 1] = A[(n - 1) * lda + (n - 1)];
     }
 }
 
@@ -320,74 +392,50 @@ tbi_eig_kernel(const double* __restrict__ dg, const double* __restrict__ eg, int
 }
 
 // ---- 3. orthonormalisation: Z <- Z (3I - Z^T Z) / 2, twice -----------------------------
-// Z (n x n, global, row stride ldz) <- Z (3I - Z^T Z) / 2, twice. Phase a holds
-// Z in shared memory to form S = (3I - Z^T Z)/2 (written to global scratch);
-// phase b holds S in shared memory while each warp streams one row of Z
-// through registers. A step whose S is already I to 1e-15 is skipped.
-__global__ void __launch_bounds__(kTbiThreads, 1)
-tbi_orth_kernel(double* __restrict__ z, int n, int ldz, double* __restrict__ S,
-                const int32_t* __restrict__ gate, const int32_t* __restrict__ skip) {
+// Each Newton-Schulz step is two small GEMMs over all SMs: 16 x 16 output tiles,
+// the two n x 16 operand panels staged in shared memory. mode 0: C = A B;
+// mode 1: C = (3I - A^T B) / 2 (the polar step's S). The operand layout:
+// A(t, i) = trans_a ? a[t * n + i] : a[i * n + t], B(t, j) = b[t * n + j].
+constexpr int kNsTile = 16;
+constexpr int kNsMaxN = 160;
+
+__global__ void __launch_bounds__(kNsTile * kNsTile)
+tbi_ns_kernel(const double* __restrict__ a, int trans_a, const double* __restrict__ b, double* __restrict__ c,
+              int n, int mode, const int32_t* __restrict__ gate, const int32_t* __restrict__ skip) {
     if ((gate != nullptr && *gate != 0) || (skip != nullptr && *skip != 0)) return;
-    extern __shared__ double osm[];
-    __shared__ int s_dev;
-    const int lds = n | 1;
-    double* M = osm;  // Z (phase a) or S (phase b), n x lds
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
-    for (int step = 0; step < 2; ++step) {
-        if (threadIdx.x == 0) s_dev = 0;
-        load_square(M, lds, z, ldz, n);
-        __syncthreads();
-        // S(a, b) for b >= a: warp per a, lanes over b
-        for (int a = warp; a < n; a += nwarp) {
-            for (int b = a + lane; b < n; b += 32) {
-                double acc = 0.0;
-                for (int t = 0; t < n; ++t) acc = fma(M[t * lds + a], M[t * lds + b], acc);
-                const double v = 0.5 * ((a == b ? 3.0 : 0.0) - acc);
-                const double dev = fabs(v - (a == b ? 1.0 : 0.0));
-                if (dev > (step == 0 ? 1e-15 : 1e-10)) s_dev = 1;
-                S[a * n + b] = v;
-                S[b * n + a] = v;
-            }
-        }
-        __syncthreads();
-        if (s_dev == 0) break;
-        load_square(M, lds, S, n, n);
-        __syncthreads();
-        const int nb = (n + 31) / 32;
-        for (int i = warp; i < n; i += nwarp) {
-            double zr[8], out[8];
-#pragma unroll
-            for (int q = 0; q < 8; ++q) {
-                const int col = lane + 32 * q;
-                zr[q] = (q < nb && col < n) ? z[static_cast<int64_t>(i) * ldz + col] : 0.0;
-                out[q] = 0.0;
-            }
-#pragma unroll
-            for (int q = 0; q < 8; ++q) {
-                if (q >= nb) break;
-                for (int tl = 0; tl < 32; ++tl) {
-                    const int t = 32 * q + tl;
-                    if (t >= n) break;
-                    const double zt = __shfl_sync(0xffffffffu, zr[q], tl);
-#pragma unroll
-                    for (int c = 0; c < 8; ++c) {
-                        const int col = lane + 32 * c;
-                        if (c < nb && col < n) out[c] = fma(zt, M[t * lds + col], out[c]);
-                    }
-                }
-            }
-#pragma unroll
-            for (int c = 0; c < 8; ++c) {
-                const int col = lane + 32 * c;
-                if (c < nb && col < n) z[static_cast<int64_t>(i) * ldz + col] = out[c];
-            }
-        }
-        __syncthreads();
+    __shared__ double as[kNsMaxN][kNsTile + 1];
+    __shared__ double bs[kNsMaxN][kNsTile];
+    const int i0 = blockIdx.y * kNsTile, j0 = blockIdx.x * kNsTile, tid = threadIdx.x;
+    for (int x = tid; x < n * kNsTile; x += blockDim.x) {
+        int t, ii;
+        if (trans_a) { t = x / kNsTile; ii = x % kNsTile; }
+        else { ii = x / n; t = x % n; }
+        const int i = i0 + ii;
+        as[t][ii] = i < n ? (trans_a ? a[t * n + i] : a[i * n + t]) : 0.0;
+        const int tb = x / kNsTile, jj = x % kNsTile, j = j0 + jj;
+        bs[tb][jj] = j < n ? b[tb * n + j] : 0.0;
+    }
+    __syncthreads();
+    const int ty = tid / kNsTile, tx = tid % kNsTile;
+    double a0 = 0.0, a1 = 0.0;
+    int t = 0;
+    for (; t + 1 < n; t += 2) {
+        a0 = fma(as[t][ty], bs[t][tx], a0);
+        a1 = fma(as[t + 1][ty], bs[t + 1][tx], a1);
+    }
+    if (t < n) a0 = fma(as[t][ty], bs[t][tx], a0);
+    const int i = i0 + ty, j = j0 + tx;
+    if (i < n && j < n) {
+        const double acc = a0 + a1;
+        c[i * n + j] = mode == 0 ? acc : 0.5 * ((i == j ? 3.0 : 0.0) - acc);
     }
 }
 
 // ---- 4. back-transform: V = H_0 H_1 ... H_{n-3} Z, one warp per column -------------
-constexpr int kBtWarps = 16;
+// The column lives in registers (lane owns rows lane + 32q); the reflectors are
+// staged in shared memory once per CTA.
+constexpr int kBtWarps = 8;
+constexpr int kBtRegs = (kNsMaxN + 31) / 32;
 
 __global__ void __launch_bounds__(32 * kBtWarps, 1)
 tbi_backtransform_kernel(const double* __restrict__ hv, const double* __restrict__ tau,
@@ -395,29 +443,41 @@ tbi_backtransform_kernel(const double* __restrict__ hv, const double* __restrict
                          const int32_t* __restrict__ gate, const int32_t* __restrict__ skip) {
     if ((gate != nullptr && *gate != 0) || (skip != nullptr && *skip != 0)) return;
     extern __shared__ double bsm[];
-    double* H = bsm;                     // all reflectors, n x n (row k = v_k)
-    double* T = H + static_cast<size_t>(n) * n;  // tau, n
-    double* X = T + n;                   // kBtWarps x n columns being transformed
+    double* H = bsm;                              // all reflectors, n x n (row k = v_k)
+    double* T = H + static_cast<size_t>(n) * n;   // tau, n
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     load_square(H, n, hv, n, n);
     for (int x = threadIdx.x; x < n; x += blockDim.x) T[x] = tau[x];
     const int col = blockIdx.x * kBtWarps + warp;
-    double* x = X + warp * n;
-    if (col < n)
-        for (int i = lane; i < n; i += 32) x[i] = z[static_cast<int64_t>(i) * ldz + col];
+    double x[kBtRegs];
+#pragma unroll
+    for (int q = 0; q < kBtRegs; ++q) {
+        const int i = lane + 32 * q;
+        x[q] = (col < n && i < n) ? z[static_cast<int64_t>(i) * ldz + col] : 0.0;
+    }
     __syncthreads();
     if (col >= n) return;
     for (int k = n - 3; k >= 0; --k) {
         const double t = T[k];
         if (t == 0.0) continue;
         const double* vk = H + static_cast<size_t>(k) * n;
+        double vr[kBtRegs];
         double s = 0.0;
-        for (int i = k + 1 + lane; i < n; i += 32) s = fma(vk[i], x[i], s);
+#pragma unroll
+        for (int q = 0; q < kBtRegs; ++q) {
+            const int i = lane + 32 * q;
+            vr[q] = (i > k && i < n) ? vk[i] : 0.0;
+            s = fma(vr[q], x[q], s);
+        }
         s = warp_sum(s) * t;
-        for (int i = k + 1 + lane; i < n; i += 32) x[i] = fma(-s, vk[i], x[i]);
-        __syncwarp();
+#pragma unroll
+        for (int q = 0; q < kBtRegs; ++q) x[q] = fma(-s, vr[q], x[q]);
     }
-    for (int i = lane; i < n; i += 32) vecs[static_cast<int64_t>(i) * ldv + col] = x[i];
+#pragma unroll
+    for (int q = 0; q < kBtRegs; ++q) {
+        const int i = lane + 32 * q;
+        if (i < n) vecs[static_cast<int64_t>(i) * ldv + col] = x[q];
+    }
 }
 
 __global__ void tbi_clear_kernel(int32_t* flag) { *flag = 0; }
@@ -428,7 +488,7 @@ bool tbi_supported(int l) { return l >= 3 && l <= 160; }
 
 size_t tbi_workspace_bytes(int l) {
     const size_t n = l;
-    return sizeof(double) * (n * n /*hv*/ + n /*tau*/ + 2 * n /*d,e*/ + 2 * n * n /*z, S*/) + 64;
+    return sizeof(double) * (n * n /*hv*/ + n /*tau*/ + 2 * n /*d,e*/ + 3 * n * n /*z, S, z2*/) + 64;
 }
 
 // Runs the tridiagonal path; sets *clustered (device) when the spectrum needs
@@ -441,16 +501,15 @@ void tbi_eig(const double* g, EigWorkspace& w, void* tbi_ws, int32_t* clustered,
     double* d = tau + n;
     double* e = d + n;
     double* z = e + n;
+    double* S = z + static_cast<size_t>(n) * n;
+    double* z2 = S + static_cast<size_t>(n) * n;
     tbi_clear_kernel<<<1, 1, 0, stream>>>(clustered);
     DSVD_LAUNCH_CHECK();
     const int lda = n | 1;
     const size_t s1 = sizeof(double) * (static_cast<size_t>(n) * lda + 2 * n);
-    const size_t s3 = sizeof(double) * static_cast<size_t>(n) * lda;
     DSVD_CUDA_CHECK(cudaFuncSetAttribute(tbi_tridiag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(s1)));
-    DSVD_CUDA_CHECK(cudaFuncSetAttribute(tbi_orth_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(s3)));
-    tbi_tridiag_kernel<<<1, kTbiThreads, s1, stream>>>(g, n, d, e, hv, tau, gate, nullptr);
+    tbi_tridiag_kernel<<<1, kTridThreads, s1, stream>>>(g, n, d, e, hv, tau, gate, nullptr);
     DSVD_LAUNCH_CHECK();
     const size_t s2 = sizeof(double) * (3 * static_cast<size_t>(n) + kTbiWarps * 6 * static_cast<size_t>(n));
     DSVD_CUDA_CHECK(cudaFuncSetAttribute(tbi_eig_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -458,10 +517,16 @@ void tbi_eig(const double* g, EigWorkspace& w, void* tbi_ws, int32_t* clustered,
     tbi_eig_kernel<<<static_cast<unsigned>(ceil_div(n, kTbiWarps)), 32 * kTbiWarps, s2, stream>>>(
         d, e, n, w.lam, z, n, clustered, gate, nullptr);
     DSVD_LAUNCH_CHECK();
-    tbi_orth_kernel<<<1, kTbiThreads, s3, stream>>>(z, n, n, z + static_cast<size_t>(n) * n, gate,
-                                                    clustered);
-    DSVD_LAUNCH_CHECK();
-    const size_t s4 = sizeof(double) * (static_cast<size_t>(n) * n + n + kBtWarps * static_cast<size_t>(n));
+    const dim3 ns_grid(static_cast<unsigned>(ceil_div(n, kNsTile)), static_cast<unsigned>(ceil_div(n, kNsTile)));
+    for (int step = 0; step < 2; ++step) {
+        double* zi = step == 0 ? z : z2;
+        double* zo = step == 0 ? z2 : z;
+        tbi_ns_kernel<<<ns_grid, kNsTile * kNsTile, 0, stream>>>(zi, 1, zi, S, n, 1, gate, clustered);
+        DSVD_LAUNCH_CHECK();
+        tbi_ns_kernel<<<ns_grid, kNsTile * kNsTile, 0, stream>>>(zi, 0, S, zo, n, 0, gate, clustered);
+        DSVD_LAUNCH_CHECK();
+    }
+    const size_t s4 = sizeof(double) * (static_cast<size_t>(n) * n + n);
     DSVD_CUDA_CHECK(cudaFuncSetAttribute(tbi_backtransform_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(s4)));
     tbi_backtransform_kernel<<<static_cast<unsigned>(ceil_div(n, kBtWarps)), 32 * kBtWarps, s4, stream>>>(

@@ -254,16 +254,37 @@ struct EigSvdOut {
     double* inv_s;  // l
 };
 
+// rescale() of the solve path: FP64 tensor cores when the shape allows
+// (dmma.cu), else the DFMA kernel. Two launches either way on the DMMA path.
+void solve_rescale(dsvd_ctx* ctx, const double* c, int64_t n, int64_t K, int64_t ldc, const double* w,
+                   int64_t ldw, const double* scale, int64_t ncol, double* out, int64_t ld_out, int out_colmajor,
+                   const int32_t* gate) {
+    if (ctx->dense_method == 0 && rescale_dmma_supported(K, ldc, ld_out, out_colmajor)) {
+        const size_t ws = rescale_dmma_workspace_bytes(K, out_colmajor ? ncol : ld_out);
+        rescale_dmma(c, n, K, ldc, w, ldw, scale, ncol, out, ld_out, out_colmajor, ctx->buf("rescale.ws", ws), gate,
+                     ctx->stream);
+        count_launch(2);
+    } else {
+        rescale(c, n, K, ldc, w, ldw, scale, ncol, out, ld_out, out_colmajor, gate, ctx->stream);
+        count_launch();
+    }
+}
+
 // (s, V) of the row-major block c (rows x l, stride ld); U is left to the caller.
 void eig_svd_factors(dsvd_ctx* ctx, const double* c, int64_t rows, int64_t l, int64_t ld,
                      EigSvdOut& o, Control* ctrl, const LoopStep* loop, const int32_t* gate,
                      bool reduce_gram = false, int64_t floor_rows = -1) {
     cudaStream_t st = ctx->stream;
     double* G = ctx->tbuf<double>("eig.G", l * l);
-    const size_t gws = gram_workspace_bytes(rows, l);
-    void* gw = ctx->buf("gram.ws." + std::to_string(rows), gws);
     int sp = ctx->span_begin(K_GRAM);
-    gram(c, rows, l, ld, G, gw, gws, gate, st);
+    if (ctx->dense_method == 0 && gram_dmma_supported(l, ld)) {
+        const size_t gws = gram_dmma_workspace_bytes(rows, l);
+        gram_dmma(c, rows, l, ld, G, ctx->buf("gram.dws." + std::to_string(rows), gws), gate, st);
+    } else {
+        const size_t gws = gram_workspace_bytes(rows, l);
+        void* gw = ctx->buf("gram.ws." + std::to_string(rows), gws);
+        gram(c, rows, l, ld, G, gw, gws, gate, st);
+    }
     count_launch(2);
     ctx->span_end(sp);
     if (reduce_gram) {  // row-sharded B: G = sum_g B_g^T B_g
@@ -383,8 +404,7 @@ void solve_tall(dsvd_ctx* ctx, const DevCsr& A, const DevCsr& AT, const dsvd_con
     }
     eig_svd_factors(ctx, T, n, l, ld, eo, ctrl, nullptr, nullptr);
     sp = ctx->span_begin(K_RESCALE);
-    rescale(T, n, l, ld, W, l, inv_s, l, Qb[0], ld, 0, nullptr, st);
-    count_launch();
+    solve_rescale(ctx, T, n, l, ld, W, l, inv_s, l, Qb[0], ld, 0, nullptr);
     ctx->span_end(sp);
 
     LoopStep ls;
@@ -432,8 +452,7 @@ void solve_tall(dsvd_ctx* ctx, const DevCsr& A, const DevCsr& AT, const dsvd_con
         }
         eig_svd_factors(ctx, T, n, l, ld, eo, ctrl, &ls, gate);
         sp = ctx->span_begin(K_RESCALE);
-        rescale(T, n, l, ld, W, l, inv_s, l, Qb[1 - cur], ld, 0, gate, st);
-        count_launch();
+        solve_rescale(ctx, T, n, l, ld, W, l, inv_s, l, Qb[1 - cur], ld, 0, gate);
         ctx->span_end(sp);
         if (dash) {
             const int slot = static_cast<int>(j % (kLookahead + 1));
@@ -485,9 +504,8 @@ void solve_tall(dsvd_ctx* ctx, const DevCsr& A, const DevCsr& AT, const dsvd_con
     double* du = io.on_device ? io.u : ctx->tbuf<double>("out.u", m * k);
     double* dv = io.on_device ? io.v : ctx->tbuf<double>("out.v", n * k);
     sp = ctx->span_begin(K_RESCALE);
-    rescale(Y, m, l, ld, W, l, inv_s, k, du, 0, 1, nullptr, st);
-    rescale(Qf, n, l, ld, W, l, nullptr, k, dv, 0, 1, nullptr, st);
-    count_launch(2);
+    solve_rescale(ctx, Y, m, l, ld, W, l, inv_s, k, du, 0, 1, nullptr);
+    solve_rescale(ctx, Qf, n, l, ld, W, l, nullptr, k, dv, 0, 1, nullptr);
     ctx->span_end(sp);
     if (io.on_device) {
         DSVD_CUDA_CHECK(cudaMemcpyAsync(io.s, sv, sizeof(double) * k, cudaMemcpyDeviceToDevice, st));
@@ -700,6 +718,9 @@ int dsvd_ctx_set_option(dsvd_ctx* ctx, const char* name, int64_t value) {
         } else if (n == "eig_method") {
             if (value < 0 || value > 1) fail(DSVD_CONFIG, "eig_method: 0 = tridiagonal (auto), 1 = Jacobi");
             ctx->eig_method = static_cast<int>(value);
+        } else if (n == "dense_method") {
+            if (value < 0 || value > 1) fail(DSVD_CONFIG, "dense_method: 0 = FP64 tensor cores, 1 = DFMA");
+            ctx->dense_method = static_cast<int>(value);
         } else if (n == "split_chunk") {
             if (value < 0) fail(DSVD_CONFIG, "split_chunk must be >= 0");
             ctx->split_chunk = value;
@@ -969,8 +990,8 @@ int dsvd_finalize_row_basis(dsvd_ctx* ctx, const dsvd_matrix* a, const double* q
         raise_device_status(read_control(ctx, ctrl));
         double* du = ctx->tbuf<double>("out.u", m * k);
         double* dv = ctx->tbuf<double>("out.v", n * k);
-        rescale(B, m, l, ld, W, l, inv_s, k, du, 0, 1, nullptr, st);
-        rescale(Q, n, l, ld, W, l, nullptr, k, dv, 0, 1, nullptr, st);
+        solve_rescale(ctx, B, m, l, ld, W, l, inv_s, k, du, 0, 1, nullptr);
+        solve_rescale(ctx, Q, n, l, ld, W, l, nullptr, k, dv, 0, 1, nullptr);
         DSVD_CUDA_CHECK(cudaMemcpyAsync(u, du, sizeof(double) * m * k, cudaMemcpyDeviceToHost, st));
         DSVD_CUDA_CHECK(cudaMemcpyAsync(v, dv, sizeof(double) * n * k, cudaMemcpyDeviceToHost, st));
         DSVD_CUDA_CHECK(cudaMemcpyAsync(s, sv, sizeof(double) * k, cudaMemcpyDeviceToHost, st));
@@ -1081,8 +1102,12 @@ int dsvd_gram(dsvd_ctx* ctx, int64_t rows, int64_t cols, const double* c, double
         double* G = ctx->tbuf<double>("k.G", cols * cols);
         DSVD_CUDA_CHECK(cudaMemcpyAsync(cc, c, sizeof(double) * rows * cols, cudaMemcpyHostToDevice, st));
         colmajor_to_rowmajor(cc, rows, cols, C, ld, st);
-        const size_t gws = gram_workspace_bytes(rows, cols);
-        gram(C, rows, cols, ld, G, ctx->buf("k.gws", gws), gws, nullptr, st);
+        if (ctx->dense_method == 0 && gram_dmma_supported(cols, ld)) {
+            gram_dmma(C, rows, cols, ld, G, ctx->buf("k.gdws", gram_dmma_workspace_bytes(rows, cols)), nullptr, st);
+        } else {
+            const size_t gws = gram_workspace_bytes(rows, cols);
+            gram(C, rows, cols, ld, G, ctx->buf("k.gws", gws), gws, nullptr, st);
+        }
         DSVD_CUDA_CHECK(cudaMemcpyAsync(g, G, sizeof(double) * cols * cols, cudaMemcpyDeviceToHost, st));
         DSVD_CUDA_CHECK(cudaStreamSynchronize(st));
     });

@@ -49,6 +49,7 @@ struct dsvd_ctx {
     // rows longer than split_chunk nonzeros are computed as chunk partials summed
     // in a fixed order (deterministic; 0 = whole chains, bit-exact vs reference)
     int64_t split_chunk = 512;
+    int dense_method = 0;           // 0: FP64 tensor-core Gram / rescale (dmma.cu), 1: DFMA kernels
     int eig_method = 0;             // 0: tridiagonal + inverse iteration (Jacobi fallback), 1: Jacobi
     cudaStream_t side = nullptr;    // second stream: hub-row SpMM runs beside the bulk kernel
     cudaEvent_t fork = nullptr, join = nullptr;

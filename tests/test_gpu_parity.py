@@ -264,11 +264,21 @@ def test_gaussian_config1_sketch_agreement(dev, oracle):
 
 # ---- dense kernels -----------------------------------------------------------------
 
-@pytest.mark.parametrize("shape", [(10000, 75), (777, 150), (5000, 300), (40, 3)])
-def test_gram_matches_oracle(dev, oracle, shape):
+@pytest.fixture(params=[0, 1], ids=["dmma", "dfma"])
+def dense_dev(request):
+    """Gram / rescale on FP64 tensor cores (dense_method 0) or DFMA (1)."""
+    dv = d.Device(0)
+    dv.set_option("dense_method", request.param)
+    yield dv
+    dv.close()
+
+
+@pytest.mark.parametrize("shape", [(10000, 75), (777, 150), (5000, 300), (40, 3), (200003, 150), (9, 160),
+                                   (1000, 8), (1000, 1)])
+def test_gram_matches_oracle(dense_dev, oracle, shape):
     c = np.asfortranarray(np.random.default_rng(shape[1]).standard_normal(shape))
     g_ref = oracle.gram(c)
-    g = d.gram(c, device=dev)
+    g = d.gram(c, device=dense_dev)
     assert np.array_equal(g, g.T)  # exactly symmetric
     np.testing.assert_allclose(g, g_ref, rtol=1e-13, atol=1e-13 * np.abs(g_ref).max())
 
@@ -326,6 +336,14 @@ def test_solve_config1_both_eigensolvers(oracle, c1, eig_dev):
     ref = oracle.solve(c1, 50, 25, tol=1e-2, alg="dash", seed=0)
     res = d.solve(to_dev(c1), d.SolverConfig(k=50, s=25, tol=1e-2, seed=0), device=eig_dev)
     check_solve(res, ref, 50)
+
+
+@pytest.mark.parametrize("k,s", [(50, 25), (100, 50), (7, 3), (140, 20)])
+def test_solve_config1_dense_methods(oracle, c1, dense_dev, k, s):
+    # l = k + s spans the tensor-core shapes: odd widths, l = 160, tiny l
+    ref = oracle.solve(c1, k, s, p=6, alg="shifted", seed=3)
+    res = d.solve(to_dev(c1), d.SolverConfig(k=k, s=s, p=6, alg=d.Algorithm.shifted, seed=3), device=dense_dev)
+    check_solve(res, ref, k)
 
 
 def test_eig_svd_known_cases(dev):
