@@ -123,6 +123,115 @@ spmm_bulk_kernel(const int64_t* __restrict__ off, const int32_t* __restrict__ id
     *reinterpret_cast<double2*>(y + row * ld + col) = make_double2(a0, a1);
 }
 
+// Whole-row variant of spmm_bulk_kernel for ld <= 192: one warp = one row
+// (or chunk) and all its columns. Lane L owns columns [4L, 4L+4) (one
+// 256-bit load per nonzero) and [128+2L, 128+2L+2) (a 128-bit load, lanes
+// with 128+2L < ld). The batch's (value, index) pairs are staged in shared
+// memory and read back with one broadcast LDS.128 per nonzero; gathers are
+// issued U nonzeros ahead of their FMAs, which stay in CSR order (bitwise
+// the same chains as the slab kernel). Per nonzero a warp issues ~10
+// instructions for 8*ld bytes instead of ~8 per 512-byte slab. U = 2 keeps
+// the kernel at 85 registers / 24 warps per SM, which measured fastest on C2
+// (pass 1 bulk rows 1.17 ms vs 1.56 ms for the slab kernel).
+constexpr int kRowWarps = 8;
+
+__device__ __forceinline__ void ld256(const double* p, double (&r)[4]) {
+    asm("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(r[0]), "=d"(r[1]), "=d"(r[2]), "=d"(r[3]) : "l"(p));
+}
+
+template <bool kShift, bool kChunk, int U>
+__global__ void __launch_bounds__(32 * kRowWarps, U == 2 ? 3 : (U == 4 ? 2 : 1))
+spmm_row_kernel(const int64_t* __restrict__ off, const int32_t* __restrict__ idx, const double* __restrict__ val,
+                const int32_t* __restrict__ order, int64_t row_start, int64_t rows, const double* __restrict__ x,
+                double* __restrict__ y, int64_t ld, const double* __restrict__ q,
+                const double* __restrict__ alpha_p, const int32_t* __restrict__ gate,
+                const int64_t* __restrict__ chunk_p0, const int64_t* __restrict__ chunk_p1) {
+    if (gate != nullptr && *gate != 0) return;
+    __shared__ __align__(16) double2 cv[kRowWarps][32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t rpos = row_start + static_cast<int64_t>(blockIdx.x) * kRowWarps + warp;
+    if (rpos >= rows) return;
+    int64_t row, beg, end;
+    if (kChunk) {
+        row = rpos;
+        beg = chunk_p0[rpos];
+        end = chunk_p1[rpos];
+    } else {
+        row = static_cast<int64_t>(order[rpos]);
+        beg = off[row];
+        end = off[row + 1];
+    }
+    const bool act4 = 4 * lane < ld, act2 = 128 + 2 * lane < ld;
+    const double* x4 = x + (act4 ? 4 * lane : 0);
+    const double* x2 = x + (act2 ? 128 + 2 * lane : 0);
+    double acc[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+    int c = 0;
+    double v = 0.0;
+    if (beg + lane < end) {
+        c = __ldg(idx + beg + lane);
+        v = __ldg(val + beg + lane);
+    }
+    double2* slot = cv[warp];
+    for (int64_t p0 = beg; p0 < end; p0 += 32) {
+        const int cnt = static_cast<int>(end - p0 < 32 ? end - p0 : 32);
+        __syncwarp();
+        slot[lane] = make_double2(v, __longlong_as_double(static_cast<long long>(c)));
+        __syncwarp();
+        if (p0 + 32 + lane < end) {  // next batch, in flight during this one
+            c = __ldg(idx + p0 + 32 + lane);
+            v = __ldg(val + p0 + 32 + lane);
+        }
+        for (int j0 = 0; j0 < cnt; j0 += U) {
+            double xa[U][4], xb[U][2], vj[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int j = j0 + u;
+                vj[u] = 0.0;
+                if (j < cnt) {
+                    const double2 e = slot[j];
+                    vj[u] = e.x;
+                    const int64_t cj = __double_as_longlong(e.y);
+                    if (act4) ld256(x4 + cj * ld, xa[u]);
+                    if (act2) {
+                        const double2 t = __ldg(reinterpret_cast<const double2*>(x2 + cj * ld));
+                        xb[u][0] = t.x;
+                        xb[u][1] = t.y;
+                    }
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                if (j0 + u < cnt) {
+#pragma unroll
+                    for (int t = 0; t < 4; ++t) acc[t] = fma(vj[u], xa[u][t], acc[t]);
+                    acc[4] = fma(vj[u], xb[u][0], acc[4]);
+                    acc[5] = fma(vj[u], xb[u][1], acc[5]);
+                }
+            }
+        }
+    }
+    double* yr = y + (kChunk ? rpos : row) * ld;
+    if (kShift && !kChunk) {
+        const double alpha = *alpha_p;
+        if (alpha != 0.0) {  // solver.cpp:94 skips the update when alpha == 0
+            const double* qr = q + row * ld;
+            if (act4) {
+#pragma unroll
+                for (int t = 0; t < 4; ++t) acc[t] = fma(-alpha, qr[4 * lane + t], acc[t]);
+            }
+            if (act2) {
+                acc[4] = fma(-alpha, qr[128 + 2 * lane], acc[4]);
+                acc[5] = fma(-alpha, qr[128 + 2 * lane + 1], acc[5]);
+            }
+        }
+    }
+    if (act4) {
+        *reinterpret_cast<double2*>(yr + 4 * lane) = make_double2(acc[0], acc[1]);
+        *reinterpret_cast<double2*>(yr + 4 * lane + 2) = make_double2(acc[2], acc[3]);
+    }
+    if (act2) *reinterpret_cast<double2*>(yr + 128 + 2 * lane) = make_double2(acc[4], acc[5]);
+}
+
 // y(row_i, :) = sum over the row's chunks, in chunk order, of partial(chunk, :),
 // then the shift epilogue.
 template <bool kShift>
@@ -742,6 +851,11 @@ void spmm(const SpmmArgs& s, cudaStream_t stream, int variant, cudaStream_t side
     // variant bits: low nibble selects the hub kernel; 16 skips the bulk rows,
     // 32 skips the hub rows (benchmarking the two halves separately)
     const bool skip_bulk = (variant & 16) != 0, skip_hub = (variant & 32) != 0;
+    // the whole-row kernel takes the bulk rows and the split chunks when
+    // ld <= 192; bits 64 / 128 force the 64-column slab kernel for them, bits
+    // 256 / 512 raise the whole-row kernel's gather lookahead from 2 to 4 / 8
+    const bool row_bulk = (variant & 64) == 0 && s.ld <= 192, row_chunk = (variant & 128) == 0 && s.ld <= 192;
+    const int ru = (variant & 256) ? 4 : (variant & 512) ? 8 : 2;
     variant &= 15;
     const bool split = a.nsplit > 0 && partial != nullptr && side != nullptr;
     const int64_t hub = (!split && side != nullptr && a.d_hub_rows != nullptr) ? a.hub_rows : 0;
@@ -752,7 +866,14 @@ void spmm(const SpmmArgs& s, cudaStream_t stream, int variant, cudaStream_t side
         DSVD_CUDA_CHECK(cudaStreamWaitEvent(side, fork, 0));
         const int nslab64 = static_cast<int>(ceil_div(s.ld, kSlab));
         const int64_t citems = skip_hub ? 0 : a.nchunks * nslab64;
-        if (citems > 0) {
+        if (citems > 0 && row_chunk) {
+            auto k = ru == 4 ? spmm_row_kernel<false, true, 4>
+                     : ru == 8 ? spmm_row_kernel<false, true, 8> : spmm_row_kernel<false, true, 2>;
+            k<<<static_cast<unsigned>(ceil_div(a.nchunks, kRowWarps)), 32 * kRowWarps, 0, side>>>(
+                a.off, a.idx, a.val, a.order, 0, a.nchunks, s.x, partial, s.ld, nullptr, nullptr, s.gate, a.chunk_p0,
+                a.chunk_p1);
+            DSVD_LAUNCH_CHECK();
+        } else if (citems > 0) {
             spmm_bulk_kernel<false, true><<<static_cast<unsigned>(ceil_div(citems, 8)), 256, 0, side>>>(
                 a.off, a.idx, a.val, a.order, 0, a.nchunks, nslab64, s.x, partial, s.ld, nullptr, nullptr,
                 s.gate, a.chunk_p0, a.chunk_p1);
@@ -828,7 +949,21 @@ void spmm(const SpmmArgs& s, cudaStream_t stream, int variant, cudaStream_t side
     const int warps_per_block = 8;
     const int64_t first = split ? a.nsplit : hub;  // rows handled above / in chunks
     const int64_t items = skip_bulk ? 0 : (a.rows - first) * nslab;
-    if (items > 0) {
+    if (items > 0 && row_bulk) {
+        const unsigned blocks = static_cast<unsigned>(ceil_div(a.rows - first, kRowWarps));
+        if (s.q != nullptr) {
+            auto k = ru == 4 ? spmm_row_kernel<true, false, 4>
+                     : ru == 8 ? spmm_row_kernel<true, false, 8> : spmm_row_kernel<true, false, 2>;
+            k<<<blocks, 32 * kRowWarps, 0, stream>>>(a.off, a.idx, a.val, a.order, first, a.rows, s.x, s.y, s.ld, s.q,
+                                                     s.alpha, s.gate, nullptr, nullptr);
+        } else {
+            auto k = ru == 4 ? spmm_row_kernel<false, false, 4>
+                     : ru == 8 ? spmm_row_kernel<false, false, 8> : spmm_row_kernel<false, false, 2>;
+            k<<<blocks, 32 * kRowWarps, 0, stream>>>(a.off, a.idx, a.val, a.order, first, a.rows, s.x, s.y, s.ld,
+                                                     nullptr, nullptr, s.gate, nullptr, nullptr);
+        }
+        DSVD_LAUNCH_CHECK();
+    } else if (items > 0) {
         const int64_t blocks = ceil_div(items, warps_per_block);
         if (s.q != nullptr) {
             spmm_bulk_kernel<true, false><<<static_cast<unsigned>(blocks), 32 * warps_per_block, 0, stream>>>(

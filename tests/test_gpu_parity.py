@@ -102,13 +102,35 @@ def test_transpose_rejects_bad_index(dev):
 
 # ---- SpMM (bit-exact) -----------------------------------------------------------
 
-@pytest.mark.parametrize("l", [1, 3, 47, 48, 49, 64, 75, 97, 150, 300])
+@pytest.mark.parametrize("l", [1, 3, 47, 48, 49, 64, 75, 97, 128, 129, 150, 190, 192, 193, 300])
 def test_spmm_bitwise_widths(dev, oracle, c1, l):
     rng = np.random.default_rng(l)
     x = np.asfortranarray(rng.standard_normal((c1.cols, l)))
     y_ref = oracle.spmm(c1, x)
     y = d.spmm(to_dev(c1), x, device=dev)
     assert_bitwise(y, y_ref)
+
+
+# spmm_variant bits: 64/128 force the 64-column slab kernel for the bulk rows /
+# split chunks, 256/512 deepen the whole-row kernel's gather lookahead
+@pytest.mark.parametrize("variant", [64, 128, 192, 256, 512])
+@pytest.mark.parametrize("l", [2, 75, 150])
+def test_spmm_kernel_variants_bitwise(oracle, variant, l):
+    dv = d.Device(0)
+    dv.set_option("spmm_variant", variant)
+    a = d.powerlaw(6000, 2500, 3.5, 1.0, 1.1, 21)
+    ca = Csr(a.rows, a.cols, a.offsets, a.col_indices, a.values)
+    at = transpose_np(ca)
+    rng = np.random.default_rng(variant + l)
+    for m, x in ((ca, rng.standard_normal((ca.cols, l))), (at, rng.standard_normal((ca.rows, l)))):
+        x = np.asfortranarray(x)
+        q = np.asfortranarray(rng.standard_normal((m.rows, l)))
+        short = np.diff(m.offsets) <= 512  # rows the default split mode keeps whole
+        y_ref = oracle.spmm(m, x)
+        assert_bitwise(d.spmm(to_dev(m), x, device=dv)[short], y_ref[short])
+        t_ref = oracle.add_scaled(y_ref, -0.25, q)
+        assert_bitwise(d.spmm_shift(to_dev(m), x, 0.25, q, device=dv)[short], t_ref[short])
+    dv.close()
 
 
 def test_spmm_transpose_pass_bitwise(dev, oracle, c1):
