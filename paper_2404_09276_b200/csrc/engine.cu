@@ -81,34 +81,62 @@ struct CsrAlloc {
 };
 
 // Chunk list of the rows longer than m.split_chunk (the prefix m.hub_rows of
-// m.order): each split row is cut into ceil(len / C) near-equal CSR ranges.
-void build_chunks(dsvd_ctx* ctx, CsrAlloc& al, DevCsr& m, const std::string& tag) {
+// m.order): each split row is cut into near-equal CSR ranges of at most
+// split_chunk nonzeros. With panel_rows > 0 (rows with sorted indices only,
+// i.e. the transpose) the ranges are also cut where the gathered X row index
+// crosses a multiple of panel_rows, and the chunk list is ordered by panel:
+// chunks that run together then gather from one panel_rows-row slice of X
+// (~40 MB at ld 152, L2-resident) instead of all of it. Each row's chunks are
+// still summed in CSR order (chunk_slot maps them to list positions).
+void build_chunks(dsvd_ctx* ctx, CsrAlloc& al, DevCsr& m, const std::string& tag, int64_t panel_rows) {
     cudaStream_t st = ctx->stream;
     const int64_t ns = m.hub_rows, C = m.split_chunk;
     m.nsplit = 0;
     m.nchunks = 0;
     m.hub_rows = 0;  // split mode does not use the hub kernels
+    m.chunk_slot = nullptr;
     if (ns == 0) return;
-    int64_t* dbe = ctx->tbuf<int64_t>("chunk.bounds", 2 * ns);
-    prefix_row_bounds(m, ns, dbe, dbe + ns, st);
+    const int npanel = panel_rows > 0 ? static_cast<int>(std::max<int64_t>(1, ceil_div(m.cols, panel_rows))) : 1;
+    const int64_t nb = ns * (npanel + 1);
+    int64_t* dbe = ctx->tbuf<int64_t>("chunk.bounds", nb);
+    panel_bounds(m, ns, npanel, npanel > 1 ? panel_rows : m.cols + 1, dbe, st);
     count_launch();
-    std::vector<int64_t> be(static_cast<size_t>(2 * ns));
-    DSVD_CUDA_CHECK(cudaMemcpyAsync(be.data(), dbe, sizeof(int64_t) * 2 * ns, cudaMemcpyDeviceToHost, st));
+    std::vector<int64_t> be(static_cast<size_t>(nb));
+    DSVD_CUDA_CHECK(cudaMemcpyAsync(be.data(), dbe, sizeof(int64_t) * nb, cudaMemcpyDeviceToHost, st));
     DSVD_CUDA_CHECK(cudaStreamSynchronize(st));
-    std::vector<int64_t> p0, p1;
+    struct Chunk {
+        int64_t p0, p1;
+        int32_t panel;
+    };
+    std::vector<Chunk> chunks;  // CSR order: row by row, panel by panel
     std::vector<int32_t> first(static_cast<size_t>(ns + 1), 0);
     for (int64_t i = 0; i < ns; ++i) {
-        const int64_t b = be[i], e = be[ns + i], len = e - b;
-        const int64_t nch = (len + C - 1) / C;
-        const int64_t cs = (len + nch - 1) / nch;
-        first[i] = static_cast<int32_t>(p0.size());
-        for (int64_t j = 0; j < nch; ++j) {
-            p0.push_back(b + j * cs);
-            p1.push_back(std::min(e, b + (j + 1) * cs));
+        first[i] = static_cast<int32_t>(chunks.size());
+        for (int p = 0; p < npanel; ++p) {
+            const int64_t b = be[i * (npanel + 1) + p], e = be[i * (npanel + 1) + p + 1], len = e - b;
+            if (len <= 0) continue;
+            const int64_t nch = (len + C - 1) / C;
+            const int64_t cs = (len + nch - 1) / nch;
+            for (int64_t j = 0; j < nch; ++j)
+                chunks.push_back({b + j * cs, std::min(e, b + (j + 1) * cs), static_cast<int32_t>(p)});
         }
     }
-    first[ns] = static_cast<int32_t>(p0.size());
-    const int64_t nc = static_cast<int64_t>(p0.size());
+    first[ns] = static_cast<int32_t>(chunks.size());
+    const int64_t nc = static_cast<int64_t>(chunks.size());
+    // list position of each chunk: stable by panel
+    std::vector<int32_t> slot(static_cast<size_t>(nc));
+    std::vector<int64_t> p0(static_cast<size_t>(nc)), p1(static_cast<size_t>(nc));
+    {
+        std::vector<int64_t> start(static_cast<size_t>(npanel + 1), 0);
+        for (const Chunk& c : chunks) ++start[c.panel + 1];
+        for (int p = 0; p < npanel; ++p) start[p + 1] += start[p];
+        for (int64_t c = 0; c < nc; ++c) {
+            const int64_t pos = start[chunks[c].panel]++;
+            slot[c] = static_cast<int32_t>(pos);
+            p0[pos] = chunks[c].p0;
+            p1[pos] = chunks[c].p1;
+        }
+    }
     m.chunk_p0 = static_cast<int64_t*>(al.get(tag + ".chunk_p0", sizeof(int64_t) * nc));
     m.chunk_p1 = static_cast<int64_t*>(al.get(tag + ".chunk_p1", sizeof(int64_t) * nc));
     m.split_first = static_cast<int32_t*>(al.get(tag + ".split_first", sizeof(int32_t) * (ns + 1)));
@@ -116,6 +144,10 @@ void build_chunks(dsvd_ctx* ctx, CsrAlloc& al, DevCsr& m, const std::string& tag
     DSVD_CUDA_CHECK(cudaMemcpyAsync(m.chunk_p1, p1.data(), sizeof(int64_t) * nc, cudaMemcpyHostToDevice, st));
     DSVD_CUDA_CHECK(cudaMemcpyAsync(m.split_first, first.data(), sizeof(int32_t) * (ns + 1),
                                     cudaMemcpyHostToDevice, st));
+    if (npanel > 1) {
+        m.chunk_slot = static_cast<int32_t*>(al.get(tag + ".chunk_slot", sizeof(int32_t) * nc));
+        DSVD_CUDA_CHECK(cudaMemcpyAsync(m.chunk_slot, slot.data(), sizeof(int32_t) * nc, cudaMemcpyHostToDevice, st));
+    }
     DSVD_CUDA_CHECK(cudaStreamSynchronize(st));  // the host vectors die here
     m.nsplit = ns;
     m.nchunks = nc;
@@ -197,8 +229,10 @@ void build_pair(dsvd_ctx* ctx, CsrAlloc& al, int64_t rows, int64_t cols, int64_t
     a.hub_rows = rows > 0 ? hh[0] : 0;
     at.hub_rows = cols > 0 ? hh[1] : 0;
     if (C > 0) {
-        build_chunks(ctx, al, a, "a");
-        build_chunks(ctx, al, at, "at");
+        // no panels for A: pass 1 gathers (Zipf columns) are L2-friendly already
+        // and the caller's rows need not be sorted
+        build_chunks(ctx, al, a, "a", 0);
+        build_chunks(ctx, al, at, "at", ctx->split_panel_rows);
     }
 }
 
@@ -721,6 +755,9 @@ int dsvd_ctx_set_option(dsvd_ctx* ctx, const char* name, int64_t value) {
         } else if (n == "dense_method") {
             if (value < 0 || value > 1) fail(DSVD_CONFIG, "dense_method: 0 = FP64 tensor cores, 1 = DFMA");
             ctx->dense_method = static_cast<int>(value);
+        } else if (n == "split_panel_rows") {
+            if (value < 0) fail(DSVD_CONFIG, "split_panel_rows must be >= 0");
+            ctx->split_panel_rows = value;
         } else if (n == "split_chunk") {
             if (value < 0) fail(DSVD_CONFIG, "split_chunk must be >= 0");
             ctx->split_chunk = value;

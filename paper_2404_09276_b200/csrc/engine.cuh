@@ -49,6 +49,8 @@ struct dsvd_ctx {
     // rows longer than split_chunk nonzeros are computed as chunk partials summed
     // in a fixed order (deterministic; 0 = whole chains, bit-exact vs reference)
     int64_t split_chunk = 512;
+    // transpose chunks are also cut / ordered by X-row panels of this many rows (0: off)
+    int64_t split_panel_rows = 32768;
     int dense_method = 0;           // 0: FP64 tensor-core Gram / rescale (dmma.cu), 1: DFMA kernels
     int eig_method = 0;             // 0: tridiagonal + inverse iteration (Jacobi fallback), 1: Jacobi
     cudaStream_t side = nullptr;    // second stream: hub-row SpMM runs beside the bulk kernel

@@ -237,6 +237,7 @@ spmm_row_kernel(const int64_t* __restrict__ off, const int32_t* __restrict__ idx
 template <bool kShift>
 __global__ void split_combine_kernel(const double* __restrict__ partial,
                                      const int32_t* __restrict__ split_first,
+                                     const int32_t* __restrict__ slot,
                                      const int32_t* __restrict__ order, int64_t nsplit,
                                      double* __restrict__ y, int64_t ld, const double* __restrict__ q,
                                      const double* __restrict__ alpha_p,
@@ -247,12 +248,35 @@ __global__ void split_combine_kernel(const double* __restrict__ partial,
     const int64_t i = e / ld, col = e - (e / ld) * ld;
     const int64_t row = order[i];
     double acc = 0.0;
-    for (int32_t c = split_first[i]; c < split_first[i + 1]; ++c) acc += partial[c * ld + col];
+    for (int32_t c = split_first[i]; c < split_first[i + 1]; ++c)
+        acc += partial[static_cast<int64_t>(slot != nullptr ? slot[c] : c) * ld + col];
     if (kShift) {
         const double alpha = *alpha_p;
         if (alpha != 0.0) acc = fma(-alpha, q[row * ld + col], acc);
     }
     y[row * ld + col] = acc;
+}
+
+__global__ void panel_bounds_kernel(const int32_t* __restrict__ order, const int64_t* __restrict__ off,
+                                    const int32_t* __restrict__ idx, int64_t n, int npanel, int64_t panel_rows,
+                                    int64_t* __restrict__ bounds) {
+    const int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (t >= n * (npanel + 1)) return;
+    const int64_t r = t / (npanel + 1);
+    const int p = static_cast<int>(t - r * (npanel + 1));
+    const int64_t row = order[r];
+    int64_t lo = off[row], hi = off[row + 1];
+    if (p == npanel) {
+        bounds[t] = hi;
+        return;
+    }
+    const int64_t key = p * panel_rows;
+    while (lo < hi) {  // first position with idx >= key
+        const int64_t mid = lo + (hi - lo) / 2;
+        if (idx[mid] < key) lo = mid + 1;
+        else hi = mid;
+    }
+    bounds[t] = lo;
 }
 
 __global__ void prefix_bounds_kernel(const int32_t* __restrict__ order, const int64_t* __restrict__ off,
@@ -982,10 +1006,10 @@ void spmm(const SpmmArgs& s, cudaStream_t stream, int variant, cudaStream_t side
         const int64_t n = a.nsplit * s.ld;
         if (s.q != nullptr)
             split_combine_kernel<true><<<static_cast<unsigned>(ceil_div(n, 256)), 256, 0, stream>>>(
-                partial, a.split_first, a.order, a.nsplit, s.y, s.ld, s.q, s.alpha, s.gate);
+                partial, a.split_first, a.chunk_slot, a.order, a.nsplit, s.y, s.ld, s.q, s.alpha, s.gate);
         else
             split_combine_kernel<false><<<static_cast<unsigned>(ceil_div(n, 256)), 256, 0, stream>>>(
-                partial, a.split_first, a.order, a.nsplit, s.y, s.ld, nullptr, nullptr, s.gate);
+                partial, a.split_first, a.chunk_slot, a.order, a.nsplit, s.y, s.ld, nullptr, nullptr, s.gate);
         DSVD_LAUNCH_CHECK();
         return;
     }
@@ -993,6 +1017,15 @@ void spmm(const SpmmArgs& s, cudaStream_t stream, int variant, cudaStream_t side
         DSVD_CUDA_CHECK(cudaEventRecord(join, side));
         DSVD_CUDA_CHECK(cudaStreamWaitEvent(stream, join, 0));
     }
+}
+
+void panel_bounds(const DevCsr& m, int64_t nrows, int npanel, int64_t panel_rows, int64_t* bounds,
+                  cudaStream_t stream) {
+    const int64_t n = nrows * (npanel + 1);
+    if (n == 0) return;
+    panel_bounds_kernel<<<static_cast<unsigned>(ceil_div(n, 256)), 256, 0, stream>>>(m.order, m.off, m.idx, nrows,
+                                                                                   npanel, panel_rows, bounds);
+    DSVD_LAUNCH_CHECK();
 }
 
 void prefix_row_bounds(const DevCsr& m, int64_t n, int64_t* d_beg, int64_t* d_end,

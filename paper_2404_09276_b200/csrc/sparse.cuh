@@ -32,6 +32,11 @@ struct DevCsr {
     int64_t* chunk_p0 = nullptr;     // nchunks: first nonzero of the chunk
     int64_t* chunk_p1 = nullptr;     // nchunks: one past the last nonzero
     int32_t* split_first = nullptr;  // nsplit+1: chunk range of split row i
+    // chunk_slot[split_first[i] + t] = position in chunk_p0/p1 (and in the
+    // partial rows) of split row i's t-th chunk; null = identity. The chunk
+    // list itself is ordered by X-row panel (see build_chunks) so chunks
+    // running together gather from an L2-resident slice of X.
+    int32_t* chunk_slot = nullptr;
 };
 
 // SpMM launch description. X and Y (and Q) are row-major with row stride ld.
@@ -48,6 +53,12 @@ struct SpmmArgs {
 
 // Launches the hub-row kernel on `side` (when the matrix has hub rows) and the
 // kernel for all other rows on `stream`; `fork`/`join` order the two streams.
+// bounds[r * (npanel + 1) + p] = first nonzero of split row r (the r-th row of
+// m.order) whose index is >= p * panel_rows; p = npanel gives the row end.
+// Requires sorted indices within each row (true for the transpose).
+void panel_bounds(const DevCsr& m, int64_t nrows, int npanel, int64_t panel_rows, int64_t* bounds,
+                  cudaStream_t stream);
+
 void spmm(const SpmmArgs& args, cudaStream_t stream, int variant, cudaStream_t side = nullptr,
           cudaEvent_t fork = nullptr, cudaEvent_t join = nullptr, double* partial = nullptr);
 

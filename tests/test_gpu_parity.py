@@ -162,14 +162,17 @@ def test_spmm_power_law_long_rows_bitwise(oracle):
     assert_bitwise(d.spmm(to_dev(at), x, device=dv), oracle.spmm(at, x))
 
 
+@pytest.mark.parametrize("panel", [0, 777])
 @pytest.mark.parametrize("chunk", [7, 32, 100, 2048])
 @pytest.mark.parametrize("l", [1, 75, 150])
-def test_spmm_split_rows_match(oracle, chunk, l):
+def test_spmm_split_rows_match(oracle, chunk, l, panel):
     """Split mode: long rows as chunk partials summed in chunk order. Not the
     reference's single chain, so checked against the rounding-error scale
-    (|A| |X|) rather than bitwise."""
+    (|A| |X|) rather than bitwise. panel: the transpose's chunks are also cut
+    at multiples of `panel` gathered rows and listed panel by panel."""
     dv = d.Device(0)
     dv.set_option("split_chunk", chunk)
+    dv.set_option("split_panel_rows", panel)  # no effect here: panels apply to the transpose of a solve
     a = d.powerlaw(6000, 2500, 3.5, 1.0, 1.1, 21)
     ca = Csr(a.rows, a.cols, a.offsets, a.col_indices, a.values)
     at = transpose_np(ca)
@@ -195,9 +198,12 @@ def test_solve_power_law_split_vs_bitwise(oracle):
     ca = Csr(a.rows, a.cols, a.offsets, a.col_indices, a.values)
     ref = oracle.solve(ca, 20, 10, p=6, alg="shifted", seed=1)
     cfg = d.SolverConfig(k=20, s=10, p=6, alg=d.Algorithm.shifted, seed=1)
-    for chunk in (0, 64):
+    # (split_chunk, split_panel_rows): whole chains; chunks; chunks cut and
+    # ordered by 500- / 333-row panels of the gathered Y (pass 2)
+    for chunk, panel in ((0, 0), (64, 0), (64, 500), (7, 333)):
         dv = d.Device(0)
         dv.set_option("split_chunk", chunk)
+        dv.set_option("split_panel_rows", panel)
         res = d.solve(a, cfg, device=dv)
         check_solve(res, ref, 20)
 
