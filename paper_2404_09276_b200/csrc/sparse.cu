@@ -130,9 +130,10 @@ spmm_bulk_kernel(const int64_t* __restrict__ off, const int32_t* __restrict__ id
 // memory and read back with one broadcast LDS.128 per nonzero; gathers are
 // issued U nonzeros ahead of their FMAs, which stay in CSR order (bitwise
 // the same chains as the slab kernel). Per nonzero a warp issues ~10
-// instructions for 8*ld bytes instead of ~8 per 512-byte slab. U = 2 keeps
-// the kernel at 85 registers / 24 warps per SM, which measured fastest on C2
-// (pass 1 bulk rows 1.17 ms vs 1.56 ms for the slab kernel).
+// instructions for 8*ld bytes instead of ~8 per 512-byte slab. The kernel is
+// bound by gathers in flight per SM: U = 2 at 64 registers (32 warps per SM;
+// ptxas spills ~40 bytes outside the inner loop) measured fastest on C2
+// (pass 1 bulk rows 1.11 ms; 24 warps: 1.17 ms; slab kernel: 1.56 ms).
 constexpr int kRowWarps = 8;
 
 __device__ __forceinline__ void ld256(const double* p, double (&r)[4]) {
@@ -140,7 +141,7 @@ __device__ __forceinline__ void ld256(const double* p, double (&r)[4]) {
 }
 
 template <bool kShift, bool kChunk, int U>
-__global__ void __launch_bounds__(32 * kRowWarps, U == 2 ? 3 : (U == 4 ? 2 : 1))
+__global__ void __launch_bounds__(32 * kRowWarps, U == 2 ? 4 : (U == 4 ? 2 : 1))
 spmm_row_kernel(const int64_t* __restrict__ off, const int32_t* __restrict__ idx, const double* __restrict__ val,
                 const int32_t* __restrict__ order, int64_t row_start, int64_t rows, const double* __restrict__ x,
                 double* __restrict__ y, int64_t ld, const double* __restrict__ q,
