@@ -2,6 +2,8 @@
 
     python tools/profile_solve.py [c2|c1] [warm]
 
+DSVD_OPTIONS="name=value,..." sets context options first (e.g. eig_method=1).
+
 With "warm", one untimed solve runs first so the profiled launches are the
 second solve's (ncu -s skips the first solve's launches).
 """
@@ -21,6 +23,9 @@ def main():
     a = bench.make_matrix(cfg)
     scfg = bench.solver_config(cfg)
     dev = d.Device(0, profiling=True)
+    for kv in filter(None, os.environ.get("DSVD_OPTIONS", "").split(",")):  # e.g. eig_method=1
+        k, v = kv.split("=")
+        dev.set_option(k, int(v))
     if "warm" in sys.argv[2:]:
         d.solve(a, scfg, device=dev)
     r = d.solve(a, scfg, device=dev)
