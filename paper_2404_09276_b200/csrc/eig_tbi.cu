@@ -75,10 +75,14 @@ constexpr int kTridThreads = 512;
 
 #ifdef DSVD_TRID_PROBE  // tools/micro/tridiag_probe.cu: per-step phase clocks
 __device__ long long g_trid_probe[192][4];
-#define TRID_PROBE(k, slot) \
-    if (threadIdx.x == 0 || (slot) == 3) g_trid_probe[k][slot] = clock64();
+#define TRID_PROBE(k, slot)                                                   \
+    do {                                                                      \
+        if (threadIdx.x == 0 || (slot) == 3) g_trid_probe[k][slot] = clock64(); \
+    } while (0)
 #else
-#define TRID_PROBE(k, slot)
+#define TRID_PROBE(k, slot) \
+    do {                    \
+    } while (0)
 #endif
 
 struct Reflector {
@@ -129,7 +133,7 @@ tbi_tridiag_kernel(const double* __restrict__ g, int n, double* __restrict__ d, 
     for (int k = 0; k + 2 < n; ++k) {
         const int k1 = k + 1, m = n - k1;
         const Reflector ref = s_ref[k & 1];
-        TRID_PROBE(k, 0)
+        TRID_PROBE(k, 0);
         if (tid == 0) {
             tau_out[k] = ref.tau;
             e[k] = ref.alpha;
@@ -179,7 +183,7 @@ tbi_tridiag_kernel(const double* __restrict__ g, int n, double* __restrict__ d, 
             }
         }
         __syncthreads();
-        TRID_PROBE(k, 1)
+        TRID_PROBE(k, 1);
         // (c)
         {
             double kk = 0.0;
@@ -197,7 +201,7 @@ tbi_tridiag_kernel(const double* __restrict__ g, int n, double* __restrict__ d, 
                     const Reflector r = make_reflector(A, lda, n, k1, lane);
                     if (lane == 0) s_ref[k1 & 1] = r;
                 }
-                if (lane == 0) TRID_PROBE(k, 3)
+                if (lane == 0) TRID_PROBE(k, 3);
             } else {
                 // rows k1 + r (r = 1 .. m-1) hold r entries right of column k1;
                 // rows r and m - r are paired (m entries per pair)
