@@ -60,18 +60,20 @@ __device__ __forceinline__ void load_square(double* __restrict__ dst, int lds, c
 
 // ---- 1. Householder tridiagonalisation ---------------------------------------
 // A (n x n, symmetric) in shared memory, lower triangle authoritative, stride
-// lda = n | 1. Outputs d (n), e (n-1), reflectors hv[k*n + i] (i > k) and tau[k].
-//
-// Two block barriers per step and no redundant scalar work on the critical
-// path:
-//   (b) p = A22 x with x = column k as stored (T threads per row); the row
-//       owner applies the v0 substitution, v_{k1} = v0 instead of x0, as
-//       p += (v0 - x0) A(:, k1), and scales by tau;
-//   (c) K = tau/2 w.v per warp, then A22 -= v w^T + (w - 2K v) v^T. Warp 0
-//       updates column k1 first and immediately derives the next reflector
-//       (alpha, tau, v0) from it while warps 1.. update the columns right of k1.
-// The reflector scalars are double-buffered by step parity.
+// lda = n | 1 (odd: a warp reading 32 consecutive rows of one column hits 32
+// distinct banks pairs). Outputs d (n), e (n-1), reflectors hv[k*n + i]
+// (i > k) and tau[k]. Step k, three block barriers:
+//   B  warp 0 derives the reflector of column k (alpha, tau, v0) while warps
+//      1..15 form p = A22 x with x = column k as stored: one lane per row,
+//      the columns split into chunks across warps (partial sums per chunk);
+//   C1 one thread per row: p += (v0 - x0) A(:, k+1) (the v0 substitution),
+//      w = tau p, v; the products w_i v_i are warp-reduced for K;
+//   C2 A22 -= v w^T + (w - 2K v) v^T, one warp per 32 x 32 lower tile, one
+//      lane per row (column k+1, the next reflector's source, included).
+// The per-step fixed latency (reflector: norm, sqrt, division) overlaps the
+// matvec instead of serialising with the update (tools/micro/tridiag_probe.cu).
 constexpr int kTridThreads = 512;
+constexpr int kTridWarps = kTridThreads / 32;
 
 #ifdef DSVD_TRID_PROBE  // tools/micro/tridiag_probe.cu: per-step phase clocks
 __device__ long long g_trid_probe[192][4];
@@ -116,118 +118,112 @@ tbi_tridiag_kernel(const double* __restrict__ g, int n, double* __restrict__ d, 
                    double* __restrict__ hv, double* __restrict__ tau_out, const int32_t* __restrict__ gate,
                    const int32_t* __restrict__ skip) {
     if ((gate != nullptr && *gate != 0) || (skip != nullptr && *skip != 0)) return;
-    extern __shared__ double tsm[];
+    extern __shared__ __align__(16) double tsm[];
     const int lda = n | 1;
-    double* A = tsm;                 // n x lda
-    double* v = A + n * lda;         // n: v of the current step
-    double* w = v + n;               // n: p = tau A22 v
-    __shared__ Reflector s_ref[2];
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nthr = blockDim.x;
+    double* A = tsm;                                   // n x lda
+    double2* vw = reinterpret_cast<double2*>(A + n * lda + (n * lda & 1));  // n: (v_i, w_i)
+    double* part = reinterpret_cast<double*>(vw + n);  // (kTridWarps - 1) x n matvec partials
+    __shared__ Reflector s_ref;
+    __shared__ double s_ksum[kTridWarps];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     load_square(A, lda, g, n, n);
-    __syncthreads();
-    if (warp == 0) {
-        const Reflector r = make_reflector(A, lda, n, 0, lane);
-        if (lane == 0) s_ref[0] = r;
-    }
     __syncthreads();
     for (int k = 0; k + 2 < n; ++k) {
         const int k1 = k + 1, m = n - k1;
-        const Reflector ref = s_ref[k & 1];
+        const int G = (m + 31) >> 5;  // 32-row groups of the trailing block
         TRID_PROBE(k, 0);
-        if (tid == 0) {
-            tau_out[k] = ref.tau;
-            e[k] = ref.alpha;
-            d[k] = A[k * lda + k];
-        }
-        if (ref.tau == 0.0) {  // column already reduced (uniform across the block)
-            for (int i = k1 + tid; i < n; i += nthr) hv[static_cast<int64_t>(k) * n + i] = A[i * lda + k];
-            if (warp == 0 && k1 + 2 < n) {
-                const Reflector r = make_reflector(A, lda, n, k1, lane);
-                if (lane == 0) s_ref[k1 & 1] = r;
+        // ---- B ----
+        __syncwarp();  // reconverge (lanes past row n - 1 skipped parts of C2)
+        if (warp == 0) {
+            const Reflector r = make_reflector(A, lda, n, k, lane);
+            if (lane == 0) {
+                s_ref = r;
+                tau_out[k] = r.tau;
+                e[k] = r.alpha;
+                d[k] = A[k * lda + k];
             }
-            __syncthreads();
-            continue;
-        }
-        // (b)
-        {
-            int lg = 5;
-            while (lg > 0 && (m << lg) > nthr) --lg;
-            const int T = 1 << lg, r = tid >> lg, sub = tid & (T - 1);
-            const int i = k1 + r;
-            double a0 = 0.0, a1 = 0.0;
-            if (r < m) {
-                const double* row = A + i * lda;
-                int j = k1 + sub;
-                for (; j + T <= i; j += 2 * T) {
-                    a0 = fma(row[j], A[j * lda + k], a0);
-                    a1 = fma(row[j + T], A[(j + T) * lda + k], a1);
+            TRID_PROBE(k, 3);
+        } else {
+            const int C = (kTridWarps - 1) / G;  // column chunks
+            const int item = warp - 1, grp = item % G, c = item / G;
+            if (c < C) {
+                const int i = k1 + 32 * grp + lane;
+                const int len = (m + C - 1) / C;
+                const int j0 = k1 + c * len, j1 = min(n, j0 + len);
+                double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+                if (i < n) {
+                    const double* xk = A + k;  // x_j = A(j, k)
+                    auto el = [&](int j) { return j <= i ? A[i * lda + j] : A[j * lda + i]; };
+                    int j = j0;
+                    for (; j + 3 < j1; j += 4) {
+                        a0 = fma(el(j), xk[j * lda], a0);
+                        a1 = fma(el(j + 1), xk[(j + 1) * lda], a1);
+                        a2 = fma(el(j + 2), xk[(j + 2) * lda], a2);
+                        a3 = fma(el(j + 3), xk[(j + 3) * lda], a3);
+                    }
+                    for (; j < j1; ++j) a0 = fma(el(j), xk[j * lda], a0);
+                    part[c * n + i] = (a0 + a1) + (a2 + a3);
                 }
-                if (j <= i) {
-                    a0 = fma(row[j], A[j * lda + k], a0);
-                    j += T;
-                }
-                for (; j + T < n; j += 2 * T) {
-                    a0 = fma(A[j * lda + i], A[j * lda + k], a0);
-                    a1 = fma(A[(j + T) * lda + i], A[(j + T) * lda + k], a1);
-                }
-                if (j < n) a0 = fma(A[j * lda + i], A[j * lda + k], a0);
-            }
-            double acc = a0 + a1;
-            for (int o = 1; o < T; o <<= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-            if (r < m && sub == 0) {
-                acc = fma(ref.v0 - ref.x0, A[i * lda + k1], acc);
-                const double vi = i == k1 ? ref.v0 : A[i * lda + k];
-                w[i] = ref.tau * acc;
-                v[i] = vi;
-                hv[static_cast<int64_t>(k) * n + i] = vi;
             }
         }
         __syncthreads();
         TRID_PROBE(k, 1);
-        // (c)
+        // ---- C1 ----
+        __syncwarp();
+        const Reflector ref = s_ref;
         {
-            double kk = 0.0;
-            for (int i = k1 + lane; i < n; i += 32) kk = fma(w[i], v[i], kk);
-            const double K2 = ref.tau * warp_sum(kk);  // 2K
-            if (warp == 0) {
-                const double vj = v[k1], wj = w[k1];
-                for (int i = k1 + lane; i < n; i += 32) {
-                    const double vi = v[i], wi = fma(-K2, vi, w[i]);
-                    double& a = A[i * lda + k1];
-                    a = fma(-vi, wj, fma(-wi, vj, a));
-                }
-                __syncwarp();
-                if (k1 + 2 < n) {
-                    const Reflector r = make_reflector(A, lda, n, k1, lane);
-                    if (lane == 0) s_ref[k1 & 1] = r;
-                }
-                if (lane == 0) TRID_PROBE(k, 3);
-            } else {
-                // rows k1 + r (r = 1 .. m-1) hold r entries right of column k1;
-                // rows r and m - r are paired (m entries per pair)
-                const int npair = m >> 1;
-                if (npair > 0) {
-                    const int t = tid - 32, nt = nthr - 32;
-                    const int T2 = nt / npair;
-                    const int p = static_cast<int>((t + 0.5f) / static_cast<float>(T2));
-                    const int sub = t - p * T2;
-                    if (p < npair) {
-                        const int r1 = p + 1;
-                        int i = k1 + r1;
-                        double vi = v[i], wi = fma(-K2, vi, w[i]);
-                        double* row = A + i * lda + k1 + 1;
-                        const double* vv = v + k1 + 1;
-                        const double* ww = w + k1 + 1;
-                        int q = sub;
-                        for (; q < r1; q += T2) row[q] = fma(-vi, ww[q], fma(-wi, vv[q], row[q]));
-                        const int r2 = m - r1;
-                        if (r2 != r1) {
-                            i = k1 + r2;
-                            vi = v[i];
-                            wi = fma(-K2, vi, w[i]);
-                            row = A + i * lda + k1 + 1;
-                            for (q -= r1; q < r2; q += T2) row[q] = fma(-vi, ww[q], fma(-wi, vv[q], row[q]));
-                        }
+            double t = 0.0;
+            if (tid < m) {
+                const int i = k1 + tid;
+                const int C = (kTridWarps - 1) / G;
+                double p = 0.0;
+                for (int c = 0; c < C; ++c) p += part[c * n + i];
+                p = fma(ref.v0 - ref.x0, A[i * lda + k1], p);
+                const double vi = i == k1 ? ref.v0 : A[i * lda + k];
+                const double wi = ref.tau * p;
+                vw[i] = make_double2(vi, wi);
+                hv[static_cast<int64_t>(k) * n + i] = vi;
+                t = wi * vi;
+            }
+            if (warp < G) {
+                t = warp_sum(t);
+                if (lane == 0) s_ksum[warp] = t;
+            }
+        }
+        __syncthreads();
+        TRID_PROBE(k, 2);
+        // ---- C2 ----
+        {
+            double ks = 0.0;
+            for (int q = 0; q < G; ++q) ks += s_ksum[q];
+            const double K2 = ref.tau * ks;  // 2K
+            // lower 32 x 32 tiles (gr >= gc) of the trailing block, one per warp
+            int gr = 0, t = warp;
+            while (gr < G && t > gr) {
+                t -= gr + 1;
+                ++gr;
+            }
+            if (gr < G) {
+                const int gc = t;
+                const int i = k1 + 32 * gr + lane;
+                if (i < n) {
+                    const double2 pi = vw[i];
+                    const double vi = pi.x, wi = fma(-K2, pi.x, pi.y);
+                    double* row = A + i * lda;
+                    const int jb = k1 + 32 * gc;
+                    const int je = min(gr == gc ? i + 1 : jb + 32, n);
+                    int j = jb;
+                    for (; j + 3 < je; j += 4) {
+                        const double2 q0 = vw[j], q1 = vw[j + 1], q2 = vw[j + 2], q3 = vw[j + 3];
+                        const double e0 = row[j], e1 = row[j + 1], e2 = row[j + 2], e3 = row[j + 3];
+                        row[j] = fma(-vi, q0.y, fma(-wi, q0.x, e0));
+                        row[j + 1] = fma(-vi, q1.y, fma(-wi, q1.x, e1));
+                        row[j + 2] = fma(-vi, q2.y, fma(-wi, q2.x, e2));
+                        row[j + 3] = fma(-vi, q3.y, fma(-wi, q3.x, e3));
+                    }
+                    for (; j < je; ++j) {
+                        const double2 q0 = vw[j];
+                        row[j] = fma(-vi, q0.y, fma(-wi, q0.x, row[j]));
                     }
                 }
             }
@@ -241,6 +237,11 @@ tbi_tridiag_kernel(const double* __restrict__ g, int n, double* __restrict__ d, 
         }
         d[n - 1] = A[(n - 1) * lda + (n - 1)];
     }
+}
+
+size_t tridiag_smem_bytes(int n) {
+    const size_t lda = n | 1;
+    return sizeof(double) * (n * lda + 1 + 2 * n + (kTridWarps - 1) * static_cast<size_t>(n));
 }
 
 // ---- 2. eigenvalues (multisection) and eigenvectors (inverse iteration) ----------------
@@ -520,8 +521,7 @@ void tbi_eig(const double* g, EigWorkspace& w, void* tbi_ws, int32_t* clustered,
     double* z2 = S + static_cast<size_t>(n) * n;
     tbi_clear_kernel<<<1, 1, 0, stream>>>(clustered);
     DSVD_LAUNCH_CHECK();
-    const int lda = n | 1;
-    const size_t s1 = sizeof(double) * (static_cast<size_t>(n) * lda + 2 * n);
+    const size_t s1 = tridiag_smem_bytes(n);
     DSVD_CUDA_CHECK(cudaFuncSetAttribute(tbi_tridiag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(s1)));
     tbi_tridiag_kernel<<<1, kTridThreads, s1, stream>>>(g, n, d, e, hv, tau, gate, nullptr);

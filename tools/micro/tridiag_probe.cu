@@ -28,8 +28,7 @@ int main(int argc, char** argv) {
     cudaMalloc(&hv, sizeof(double) * n * n);
     cudaMalloc(&tau, sizeof(double) * n);
     cudaMemcpy(dg, g.data(), sizeof(double) * n * n, cudaMemcpyHostToDevice);
-    const int lda = n | 1;
-    const size_t s1 = sizeof(double) * (static_cast<size_t>(n) * lda + 2 * n);
+    const size_t s1 = dsvd::tridiag_smem_bytes(n);
     cudaFuncSetAttribute(dsvd::tbi_tridiag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(s1));
     cudaEvent_t a0, a1;
     cudaEventCreate(&a0);
@@ -45,18 +44,19 @@ int main(int argc, char** argv) {
     printf("n %d: %.1f us (%s)\n", n, ms * 1e3, cudaGetErrorString(cudaGetLastError()));
     long long pr[192][4];
     cudaMemcpyFromSymbol(pr, dsvd::g_trid_probe, sizeof(pr));
-    long long sb = 0, sc = 0, sw = 0;
+    long long sb = 0, sc1 = 0, sc2 = 0, sw = 0;
     for (int k = 0; k + 2 < n; ++k) {
-        const long long b_ = pr[k][1] - pr[k][0];
-        const long long next = (k + 3 < n) ? pr[k + 1][0] : pr[k][1];
-        const long long c_ = next - pr[k][1], w0 = pr[k][3] - pr[k][1];
+        const long long b_ = pr[k][1] - pr[k][0], c1 = pr[k][2] - pr[k][1];
+        const long long next = (k + 3 < n) ? pr[k + 1][0] : pr[k][2];
+        const long long c2 = next - pr[k][2], w0 = pr[k][3] - pr[k][0];
         sb += b_;
-        sc += c_;
+        sc1 += c1;
+        sc2 += c2;
         sw += w0;
         if (k % 16 == 0 || k + 3 == n)
-            printf("step %3d (m=%3d): matvec+bar %6lld  update+bar %6lld  (warp0 col+reflector %6lld) cycles\n", k,
-                   n - k - 1, b_, c_, w0);
+            printf("step %3d (m=%3d): B (reflector | matvec) %6lld  C1 %6lld  C2 update %6lld  (reflector %6lld) cycles\n",
+                   k, n - k - 1, b_, c1, c2, w0);
     }
-    printf("sum: matvec+bar %lld  update+bar %lld  warp0 %lld cycles\n", sb, sc, sw);
+    printf("sum: B %lld  C1 %lld  C2 %lld  reflector %lld cycles\n", sb, sc1, sc2, sw);
     return 0;
 }
