@@ -110,15 +110,25 @@ void build_chunks(dsvd_ctx* ctx, CsrAlloc& al, DevCsr& m, const std::string& tag
     };
     std::vector<Chunk> chunks;  // CSR order: row by row, panel by panel
     std::vector<int32_t> first(static_cast<size_t>(ns + 1), 0);
+    auto cut = [&](int64_t b, int64_t e, int32_t panel) {
+        const int64_t len = e - b;
+        if (len <= 0) return;
+        const int64_t nch = (len + C - 1) / C;
+        const int64_t cs = (len + nch - 1) / nch;
+        for (int64_t j = 0; j < nch; ++j) chunks.push_back({b + j * cs, std::min(e, b + (j + 1) * cs), panel});
+    };
     for (int64_t i = 0; i < ns; ++i) {
         first[i] = static_cast<int32_t>(chunks.size());
-        for (int p = 0; p < npanel; ++p) {
-            const int64_t b = be[i * (npanel + 1) + p], e = be[i * (npanel + 1) + p + 1], len = e - b;
-            if (len <= 0) continue;
-            const int64_t nch = (len + C - 1) / C;
-            const int64_t cs = (len + nch - 1) / nch;
-            for (int64_t j = 0; j < nch; ++j)
-                chunks.push_back({b + j * cs, std::min(e, b + (j + 1) * cs), static_cast<int32_t>(p)});
+        const int64_t* bi = be.data() + i * (npanel + 1);
+        // a row of L nonzeros is cut at every gs-th panel boundary, gs chosen so
+        // the pieces stay about split_chunk long (L / C groups of panels); each
+        // piece is listed under the middle panel of its group
+        const int64_t L = bi[npanel] - bi[0];
+        const int64_t groups = std::max<int64_t>(1, std::min<int64_t>(npanel, L / C));
+        const int gs = static_cast<int>((npanel + groups - 1) / groups);
+        for (int p = 0; p < npanel; p += gs) {
+            const int pe = std::min(npanel, p + gs);
+            cut(bi[p], bi[pe], static_cast<int32_t>((p + pe - 1) / 2));
         }
     }
     first[ns] = static_cast<int32_t>(chunks.size());
