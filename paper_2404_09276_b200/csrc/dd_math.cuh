@@ -69,9 +69,106 @@ __host__ __device__ __forceinline__ dd div(dd a, dd b) {
     return add(q, dd{q3, 0.0});
 }
 
+// Table entries (hi, lo) of dd_consts.cuh: device copies through the
+// read-only cache, host copies in host code.
+__host__ __device__ __forceinline__ dd tab_ld(const double* host, const double* dev, int i) {
+#ifdef __CUDA_ARCH__
+    const double2 v = __ldg(reinterpret_cast<const double2*>(dev) + i);
+    return {v.x, v.y};
+#else
+    (void)dev;
+    return {host[2 * i], host[2 * i + 1]};
+#endif
+}
+#ifdef __CUDA_ARCH__
+#define DSVD_TAB(name) nullptr, ddc::name##D
+#else
+#define DSVD_TAB(name) ddc::name##H, nullptr
+#endif
+
 // log(u) for finite u > 0, correctly rounded (ties to even) up to the
-// ~2^-104 accuracy of the double-double evaluation.
+// ~2^-104 accuracy of the double-double evaluation. Table-driven: f = c (1+t)
+// with c = i/64 the nearest table point, log c from a double-double table, and
+// log(f/c) = 2 atanh(z), z = (f-c)/(f+c), |z| <= 2^-7.5, so the series needs
+// three double-double Horner steps plus a plain-double tail (the w^4 .. w^7
+// terms, below 2^-60 relative, whose rounding stays under 2^-113). Same value as
+// log_cr_series (the 23-term reference evaluation) except with probability
+// ~2^-50 per draw; tests/test_ddm.py checks both against each other.
 __host__ __device__ inline double log_cr(double u) {
+    int e;
+    double f = frexp(u, &e);  // u = f * 2^e, f in [0.5, 1)
+    if (f < 0.70710678118654752440) {
+        f *= 2.0;
+        e -= 1;
+    }
+    const int i = static_cast<int>(rint(f * 64.0));  // 45 .. 91
+    const double c = i * 0.015625;
+    const dd z = div(dd{f - c, 0.0}, two_sum(f, c));  // f - c exact (Sterbenz)
+    const dd w = mul(z, z);
+    const double wh = w.hi;
+    const double tail = ddc::kAtanhHi(4) + wh * (ddc::kAtanhHi(5) + wh * (ddc::kAtanhHi(6) + wh * ddc::kAtanhHi(7)));
+    dd p = add(dd{ddc::kAtanhHi(3), ddc::kAtanhLo(3)}, mul_d(w, tail));
+    p = add(dd{ddc::kAtanhHi(2), ddc::kAtanhLo(2)}, mul(w, p));
+    p = add(dd{ddc::kAtanhHi(1), ddc::kAtanhLo(1)}, mul(w, p));
+    p = add(dd{1.0, 0.0}, mul(w, p));
+    const dd lg = mul(mul_d(z, 2.0), p);
+    const double ed = static_cast<double>(e);
+    dd el = add(dd{ed * ddc::kLn2Hi, 0.0}, two_prod(ed, ddc::kLn2Mid));
+    el = add(el, dd{ed * ddc::kLn2Lo, 0.0});
+    const dd lc = tab_ld(DSVD_TAB(kLogCTab), i - ddc::kLogCFirst);
+    const dd r = add(add(el, lc), lg);
+    return r.hi + r.lo;
+}
+
+// cos(x) for 0 <= x <= 8, correctly rounded (same caveat as log_cr).
+// Table-driven: x = k pi/2 + r, r = a + s with a = j/32, |s| <= 1/64, and
+// cos/sin(a + s) from double-double cos a, sin a and short cos s, sin s series
+// (three double-double Horner steps each, plain-double tails).
+__host__ __device__ inline double cos_cr(double x) {
+    const double kq = rint(x * ddc::kTwoOverPi);
+    const int k = static_cast<int>(kq);
+    dd r = two_sum(x, -kq * ddc::kPio2_1);
+    r = add(r, dd{-kq * ddc::kPio2_2, 0.0});
+    r = add(r, dd{-kq * ddc::kPio2_3, 0.0});
+    r = add(r, two_prod(-kq, ddc::kPio2_4));
+    const int j = static_cast<int>(rint(r.hi * 32.0));  // -25 .. 25
+    const int ja = j < 0 ? -j : j;
+    const dd s = two_sum(r.hi - j * 0.03125, r.lo);     // r.hi - j/32 exact (Sterbenz)
+    const dd w = mul(s, s);
+    const double wh = w.hi;
+    // cos s = 1 + w (c1 + w (c2 + w (c3 + w tail_c)))
+    const double tc = ddc::kCosHi(4) + wh * (ddc::kCosHi(5) + wh * ddc::kCosHi(6));
+    dd pc = add(dd{ddc::kCosHi(3), ddc::kCosLo(3)}, mul_d(w, tc));
+    pc = add(dd{ddc::kCosHi(2), ddc::kCosLo(2)}, mul(w, pc));
+    pc = add(dd{ddc::kCosHi(1), ddc::kCosLo(1)}, mul(w, pc));
+    const dd cs = add(dd{1.0, 0.0}, mul(w, pc));
+    // sin s = s (1 + w (d1 + w (d2 + w (d3 + w tail_s))))
+    const double ts = ddc::kSinHi(4) + wh * (ddc::kSinHi(5) + wh * ddc::kSinHi(6));
+    dd ps = add(dd{ddc::kSinHi(3), ddc::kSinLo(3)}, mul_d(w, ts));
+    ps = add(dd{ddc::kSinHi(2), ddc::kSinLo(2)}, mul(w, ps));
+    ps = add(dd{ddc::kSinHi(1), ddc::kSinLo(1)}, mul(w, ps));
+    const dd sn = mul(s, add(dd{1.0, 0.0}, mul(w, ps)));
+    dd res;
+    if (ja == 0) {
+        res = (k & 1) == 0 ? cs : sn;
+    } else {
+        const dd ca = tab_ld(DSVD_TAB(kCosTab), ja);
+        dd sa = tab_ld(DSVD_TAB(kSinTab), ja);
+        if (j < 0) sa = dd{-sa.hi, -sa.lo};
+        if ((k & 1) == 0) {
+            res = add(mul(ca, cs), mul(dd{-sa.hi, -sa.lo}, sn));  // cos(a+s)
+        } else {
+            res = add(mul(sa, cs), mul(ca, sn));  // sin(a+s)
+        }
+    }
+    const int q = k & 3;
+    const double v = res.hi + res.lo;
+    return (q == 1 || q == 2) ? -v : v;
+}
+
+// The series evaluations the table-driven versions above replace (kept as the
+// cross-check of tests/test_ddm.py).
+__host__ __device__ inline double log_cr_series(double u) {
     int e;
     double f = frexp(u, &e);  // u = f * 2^e, f in [0.5, 1)
     if (f < 0.70710678118654752440) {
@@ -94,8 +191,7 @@ __host__ __device__ inline double log_cr(double u) {
     return r.hi + r.lo;
 }
 
-// cos(x) for 0 <= x <= 8, correctly rounded (same caveat as log_cr).
-__host__ __device__ inline double cos_cr(double x) {
+__host__ __device__ inline double cos_cr_series(double x) {
     const double kq = rint(x * ddc::kTwoOverPi);
     const int k = static_cast<int>(kq);
     // r = x - kq*pi/2 with pi/2 in four pieces (kq*piece_i exact for the first three)
