@@ -91,7 +91,8 @@ def committed_traffic(config_key):
     """dram bytes per SpMM launch from the committed ncu capture, if any."""
     try:
         with open(os.path.join(ROOT, "profiles", "spmm_traffic.json")) as f:
-            return json.load(f).get(config_key)
+            entry = json.load(f).get(config_key)
+        return entry.get("traffic") if isinstance(entry, dict) else entry
     except Exception:
         return None
 
@@ -347,7 +348,8 @@ def run_b200(args, rank, world, local_rank):
                 "d2h_bytes_per_step": int(d2h)},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": (achieved / peak) if achieved else None,
-                     "traffic": traffic, "peak_source": peak_kind,
+                     "traffic": traffic, "traffic_source": "profiles/spmm_traffic.json" if traffic else None,
+                     "peak_source": peak_kind,
                      "kernel": "csr_spmm_f64 (both passes)",
                      "pass_gbs": pass_gbs,
                      "algorithmic_bytes_per_launch": sp_bytes / max(sp_launch, 1)},
