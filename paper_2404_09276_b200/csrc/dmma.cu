@@ -115,13 +115,15 @@ rescale_dmma_kernel(const double* __restrict__ c, int64_t n, int K, int64_t ldc,
 #pragma unroll
                 for (int nb = 0; nb < 4; ++nb)
                     bf[nb] = *reinterpret_cast<const double2*>(Bt + (nb * 8 + g) * ldb + kg);
+                // the two k-halves of each accumulator are eight DMMAs apart
 #pragma unroll
                 for (int mb = 0; mb < 2; ++mb)
 #pragma unroll
-                    for (int nb = 0; nb < 4; ++nb) {
-                        dmma884(acc[mb][nb], af[mb].x, bf[nb].x);
-                        dmma884(acc[mb][nb], af[mb].y, bf[nb].y);
-                    }
+                    for (int nb = 0; nb < 4; ++nb) dmma884(acc[mb][nb], af[mb].x, bf[nb].x);
+#pragma unroll
+                for (int mb = 0; mb < 2; ++mb)
+#pragma unroll
+                    for (int nb = 0; nb < 4; ++nb) dmma884(acc[mb][nb], af[mb].y, bf[nb].y);
             }
         }
         cpa_wait<0>();
@@ -148,7 +150,7 @@ rescale_dmma_kernel(const double* __restrict__ c, int64_t n, int K, int64_t ldc,
 }
 
 // ---- gram -------------------------------------------------------------------------
-constexpr int kGmRows = 16, kGmStages = 3;
+constexpr int kGmRows = 32, kGmStages = 4;
 
 __host__ __device__ constexpr int gm_pairs(int nb) { return nb * (nb + 1) / 2; }
 __host__ __device__ constexpr int gm_stride(int nb) { return nb % 2 ? nb * 8 : nb * 8 + 8; }
@@ -172,13 +174,14 @@ gram_dmma_kernel(const double* __restrict__ c, int64_t n, int64_t ld, int64_t ro
         const int row = e / (S - 2 * vec), col = 2 * vec + e % (S - 2 * vec);
         gsm[row * S + col] = 0.0;
     }
-    auto stage = [&](int slot, int64_t rr0) {
+    const int nwarp = blockDim.x >> 5;
+    auto stage = [&](int slot, int64_t rr0) {  // warp per row, lanes along the row
         double* dst = gsm + slot * kGmRows * S;
-        for (int e = tid; e < kGmRows * vec; e += blockDim.x) {
-            const int r = e / vec, v = e - r * vec;
+        for (int r = warp; r < kGmRows; r += nwarp) {
             const int64_t gr = rr0 + r;
             const bool ok = gr < r_end;
-            cpa16z(dst + r * S + 2 * v, ok ? c + gr * ld + 2 * v : c, ok);
+            const double* src = c + (ok ? gr * ld : 0);
+            for (int v = lane; v < vec; v += 32) cpa16z(dst + r * S + 2 * v, src + 2 * v, ok);
         }
     };
     const int nst = static_cast<int>(((r_end > r_beg ? r_end - r_beg : int64_t(0)) + kGmRows - 1) / kGmRows);
