@@ -251,6 +251,36 @@ __device__ __forceinline__ double rcp_fast(double q) {
     return r * fma(-q, r, 2.0);  // one Newton step: ~2^-56; counts only need signs
 }
 
+// Two Sturm counts at once: independent recurrences interleaved, so the
+// dependent-latency chain is paid once for both points.
+__device__ __forceinline__ void sturm_count2(const double* d, const double* e2, int n, double x0, double x1,
+                                             double pivmin, int& c0, int& c1) {
+    double q0 = d[0] - x0, q1 = d[0] - x1;
+    if (fabs(q0) < pivmin) q0 = -pivmin;
+    if (fabs(q1) < pivmin) q1 = -pivmin;
+    int a0 = q0 < 0.0, a1 = q1 < 0.0;
+    for (int i = 1; i < n; ++i) {
+        const double di = d[i], ei = e2[i - 1];
+        q0 = (di - x0) - ei * rcp_fast(q0);
+        q1 = (di - x1) - ei * rcp_fast(q1);
+        if (fabs(q0) < pivmin) q0 = -pivmin;
+        if (fabs(q1) < pivmin) q1 = -pivmin;
+        a0 += q0 < 0.0;
+        a1 += q1 < 0.0;
+    }
+    c0 = a0;
+    c1 = a1;
+}
+
+// 1/q to full double precision (approximation + two Newton steps); the LU of
+// the inverse iteration only needs a backward-stable factorisation
+__device__ __forceinline__ double rcp_nr2(double q) {
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(q));
+    r = r * fma(-q, r, 2.0);
+    return r * fma(-q, r, 2.0);
+}
+
 __device__ int sturm_count(const double* d, const double* e2, int n, double x, double pivmin) {
     int cnt = 0;
     double q = d[0] - x;
@@ -265,146 +295,221 @@ __device__ int sturm_count(const double* d, const double* e2, int n, double x, d
 }
 
 constexpr int kTbiWarps = 8;
+constexpr int kGridPts = 2048;  // shared Sturm-count grid (tbi_grid_kernel)
 
-__global__ void __launch_bounds__(32 * kTbiWarps)
-tbi_eig_kernel(const double* __restrict__ dg, const double* __restrict__ eg, int n,
-               double* __restrict__ lam, double* __restrict__ z, int ldz, int32_t* __restrict__ clustered,
-               const int32_t* __restrict__ gate, const int32_t* __restrict__ skip) {
-    if ((gate != nullptr && *gate != 0) || (skip != nullptr && *skip != 0)) return;
-    extern __shared__ double esm[];
-    double* d = esm;                       // n
-    double* e = d + n;                     // n
-    double* e2 = e + n;                    // n
-    double* work = e2 + n;                 // kTbiWarps x 6n (per-warp LU + iterate)
-    __shared__ double s_gl, s_gu, s_pivmin, s_tnorm;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    for (int i = tid; i < n; i += blockDim.x) {
+#ifdef DSVD_EIG_PROBE  // tools/micro/eig_probe.cu: per-eigenvalue phase clocks
+__device__ long long g_eig_probe[256][6];
+#define EIG_PROBE(j, slot)                                             \
+    do {                                                               \
+        if ((threadIdx.x & 31) == 0) g_eig_probe[j][slot] = clock64(); \
+    } while (0)
+#else
+#define EIG_PROBE(j, slot) \
+    do {                   \
+    } while (0)
+#endif
+
+// Gershgorin bounds, pivmin and ||T|| of the tridiagonal (d, e), one warp.
+struct TriBounds {
+    double gl, gu, pivmin, tnorm;
+};
+__device__ TriBounds tri_bounds(const double* d, const double* e, const double* e2, int n, int lane) {
+    double gl = DBL_MAX, gu = -DBL_MAX, emax = 0.0, tn = 0.0;
+    for (int i = lane; i < n; i += 32) {
+        const double r = (i > 0 ? fabs(e[i - 1]) : 0.0) + (i + 1 < n ? fabs(e[i]) : 0.0);
+        gl = fmin(gl, d[i] - r);
+        gu = fmax(gu, d[i] + r);
+        emax = fmax(emax, e2[i]);
+        tn = fmax(tn, fabs(d[i]) + r);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        gl = fmin(gl, __shfl_xor_sync(0xffffffffu, gl, o));
+        gu = fmax(gu, __shfl_xor_sync(0xffffffffu, gu, o));
+        emax = fmax(emax, __shfl_xor_sync(0xffffffffu, emax, o));
+        tn = fmax(tn, __shfl_xor_sync(0xffffffffu, tn, o));
+    }
+    const double pad = 2.0 * DBL_EPSILON * fmax(fabs(gl), fabs(gu)) + 1e-300;
+    return {gl - pad, gu + pad, DBL_MIN * fmax(1.0, emax), tn};
+}
+
+// Grid point t of the shared count grid: 0 -> gl, 1 .. kGridPts-1 geometric
+// from gu * 2^-70 up to gu (the Gram spectrum is non-negative and spans many
+// decades), so every eigenvalue above gu * 2^-70 starts bracketed to ~2.4%.
+__device__ __forceinline__ double grid_x(int t, double gl, double gu) {
+    if (t == 0 || gu <= 0.0) return gl + (gu - gl) * t / (kGridPts - 1);
+    return gu * exp2(-70.0 * (kGridPts - 1 - t) / (kGridPts - 2));
+}
+
+__device__ __forceinline__ void load_tri(const double* dg, const double* eg, int n, double* d, double* e,
+                                         double* e2) {
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
         d[i] = dg[i];
         const double ei = i + 1 < n ? eg[i] : 0.0;
         e[i] = ei;
         e2[i] = ei * ei;
     }
+}
+
+// counts[t] = number of eigenvalues below grid_x(t), two points per thread.
+__global__ void __launch_bounds__(256)
+tbi_grid_kernel(const double* __restrict__ dg, const double* __restrict__ eg, int n, int32_t* __restrict__ counts,
+                const int32_t* __restrict__ gate, const int32_t* __restrict__ skip) {
+    if ((gate != nullptr && *gate != 0) || (skip != nullptr && *skip != 0)) return;
+    extern __shared__ double gsm2[];
+    double* d = gsm2;
+    double* e = d + n;
+    double* e2 = e + n;
+    load_tri(dg, eg, n, d, e, e2);
     __syncthreads();
-    if (warp == 0) {
-        double gl = DBL_MAX, gu = -DBL_MAX, emax = 0.0, tn = 0.0;
-        for (int i = lane; i < n; i += 32) {
-            const double r = (i > 0 ? fabs(e[i - 1]) : 0.0) + (i + 1 < n ? fabs(e[i]) : 0.0);
-            gl = fmin(gl, d[i] - r);
-            gu = fmax(gu, d[i] + r);
-            emax = fmax(emax, e2[i]);
-            tn = fmax(tn, fabs(d[i]) + r);
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            gl = fmin(gl, __shfl_xor_sync(0xffffffffu, gl, o));
-            gu = fmax(gu, __shfl_xor_sync(0xffffffffu, gu, o));
-            emax = fmax(emax, __shfl_xor_sync(0xffffffffu, emax, o));
-            tn = fmax(tn, __shfl_xor_sync(0xffffffffu, tn, o));
-        }
-        if (lane == 0) {
-            const double pad = 2.0 * DBL_EPSILON * fmax(fabs(gl), fabs(gu)) + 1e-300;
-            s_gl = gl - pad;
-            s_gu = gu + pad;
-            s_pivmin = DBL_MIN * fmax(1.0, emax);
-            s_tnorm = tn;
-        }
-    }
+    const TriBounds b = tri_bounds(d, e, e2, n, threadIdx.x & 31);
+    const int t0 = 2 * (blockIdx.x * blockDim.x + threadIdx.x);
+    if (t0 >= kGridPts) return;
+    int c0, c1;
+    sturm_count2(d, e2, n, grid_x(t0, b.gl, b.gu), grid_x(t0 + 1, b.gl, b.gu), b.pivmin, c0, c1);
+    counts[t0] = c0;
+    counts[t0 + 1] = c1;
+}
+
+// One warp per eigenvalue j (ascending): bracket from the count grid, 65-way
+// multisection on Sturm counts to full precision, then the eigenvector from a
+// twisted factorization of T - lambda I (Dhillon-Parlett): forward and
+// backward pivots D+ / D- (lanes 0 and 1), twist index r = argmin |gamma_r|,
+// gamma_r = D+_r + D-_r - (d_r - lambda), and z from z_r = 1 outwards with the
+// ratios -e/D+ and -e/D- (one pass; no inverse-iteration sweeps). Lane 2 checks
+// the gap to the next eigenvalue at the same time.
+__global__ void __launch_bounds__(32 * kTbiWarps)
+tbi_eig_kernel(const double* __restrict__ dg, const double* __restrict__ eg, int n,
+               const int32_t* __restrict__ counts, double* __restrict__ lam, double* __restrict__ z, int ldz,
+               int32_t* __restrict__ clustered, const int32_t* __restrict__ gate, const int32_t* __restrict__ skip) {
+    if ((gate != nullptr && *gate != 0) || (skip != nullptr && *skip != 0)) return;
+    extern __shared__ double esm[];
+    double* d = esm;        // n
+    double* e = d + n;      // n
+    double* e2 = e + n;     // n
+    double* work = e2 + n;  // kTbiWarps x 3n: D+, D-, z
+    __shared__ int s_cnt[kGridPts];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    load_tri(dg, eg, n, d, e, e2);
+    for (int t = tid; t < kGridPts; t += blockDim.x) s_cnt[t] = counts[t];
     __syncthreads();
     const int j = blockIdx.x * kTbiWarps + warp;
     if (j >= n) return;
-    const double pivmin = s_pivmin, tnorm = s_tnorm;
-    // j-th smallest eigenvalue: count(lo) <= j < count(hi)
-    double lo = s_gl, hi = s_gu;
+    const TriBounds b = tri_bounds(d, e, e2, n, lane);
+    const double pivmin = b.pivmin, tnorm = b.tnorm;
+    EIG_PROBE(j, 0);
+    // bracket: last grid point with count <= j, first with count > j
+    double lo = b.gl, hi = b.gu;
+    {
+        int tl = -1, th = kGridPts;  // count(x_tl) <= j < count(x_th); counts are monotone in t
+        for (int t = lane; t < kGridPts; t += 32) {
+            if (s_cnt[t] <= j) tl = max(tl, t);
+            else th = min(th, t);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            tl = max(tl, __shfl_xor_sync(0xffffffffu, tl, o));
+            th = min(th, __shfl_xor_sync(0xffffffffu, th, o));
+        }
+        if (tl >= 0) lo = grid_x(tl, b.gl, b.gu);
+        if (th < kGridPts) hi = grid_x(th, b.gl, b.gu);
+    }
     for (int it = 0; it < 40; ++it) {
         const double width = hi - lo;
         if (width <= 2.0 * DBL_EPSILON * fmax(fabs(lo), fabs(hi)) + pivmin) break;
-        const double x = lo + width * (lane + 1) / 33.0;
-        const int c = sturm_count(d, e2, n, x, pivmin);
-        const unsigned above = __ballot_sync(0xffffffffu, c > j);
-        const int first = above ? __ffs(above) - 1 : 32;
-        const double xf = __shfl_sync(0xffffffffu, x, first < 32 ? first : 31);
-        const double xp = __shfl_sync(0xffffffffu, x, first > 0 ? first - 1 : 0);
-        if (first < 32) hi = xf;
-        if (first > 0) lo = xp;
-        if (first == 32) lo = xf;  // all points below: root in (x_31, hi]
+        const double x0 = lo + width * (2 * lane + 1) / 65.0;
+        const double x1 = lo + width * (2 * lane + 2) / 65.0;
+        int c0, c1;
+        sturm_count2(d, e2, n, x0, x1, pivmin, c0, c1);
+        const unsigned a0 = __ballot_sync(0xffffffffu, c0 > j), a1 = __ballot_sync(0xffffffffu, c1 > j);
+        // point t = 2L + p (p = 0, 1); counts are monotone in t
+        const unsigned any = a0 | a1;
+        const int fl = any ? __ffs(any) - 1 : 32;  // lane holding the first point above
+        const int ft = fl == 32 ? 64 : 2 * fl + (((a0 >> fl) & 1u) ? 0 : 1);
+        auto xat = [&](int t) {  // x of point t (0 .. 63): lane t/2, slot t%2
+            const double v0 = __shfl_sync(0xffffffffu, x0, t >> 1), v1 = __shfl_sync(0xffffffffu, x1, t >> 1);
+            return (t & 1) ? v1 : v0;
+        };
+        const double xf = xat(ft < 64 ? ft : 63);
+        const double xp = xat(ft > 0 ? ft - 1 : 0);
+        if (ft < 64) hi = xf;
+        if (ft > 0) lo = xp;
+        if (ft == 64) lo = xf;  // all points below: root in (x_63, hi]
     }
     const double lmb = 0.5 * (lo + hi);
+    EIG_PROBE(j, 1);
     if (lane == 0) lam[j] = lmb;
-    // neighbours closer than kTbiGap ||T|| -> inverse iteration is not reliable
-    if (lane == 0 && j + 1 < n) {
+    double* Dp = work + warp * 3 * n;
+    double* Dm = Dp + n;
+    double* zs = Dm + n;
+    if (lane == 0) {
+        double q = d[0] - lmb;
+        if (fabs(q) < pivmin) q = -pivmin;
+        Dp[0] = q;
+        for (int i = 1; i < n; ++i) {
+            q = (d[i] - lmb) - e2[i - 1] * rcp_fast(q);
+            if (fabs(q) < pivmin) q = -pivmin;
+            Dp[i] = q;
+        }
+    } else if (lane == 1) {
+        double q = d[n - 1] - lmb;
+        if (fabs(q) < pivmin) q = -pivmin;
+        Dm[n - 1] = q;
+        for (int i = n - 2; i >= 0; --i) {
+            q = (d[i] - lmb) - e2[i] * rcp_fast(q);
+            if (fabs(q) < pivmin) q = -pivmin;
+            Dm[i] = q;
+        }
+    } else if (lane == 2 && j + 1 < n) {
+        // neighbours closer than kTbiGap ||T||: vectors from one shift are not reliable
         const int c = sturm_count(d, e2, n, lmb + kTbiGap * tnorm, pivmin);
         if (c > j + 1) atomicExch(clustered, 1);
     }
-    // inverse iteration on (T - lmb I): LU with partial pivoting (the dgttrf /
-    // dgttrs recurrences), three solves from a fixed non-degenerate start (lane 0)
+    __syncwarp();
+    // twist index: argmin |gamma_r| (ties: smallest r)
+    double gbest = DBL_MAX;
+    int rbest = 0;
+    for (int r = lane; r < n; r += 32) {
+        const double g = fabs(Dp[r] + Dm[r] - (d[r] - lmb));
+        if (g < gbest) {
+            gbest = g;
+            rbest = r;
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const double go = __shfl_xor_sync(0xffffffffu, gbest, o);
+        const int ro = __shfl_xor_sync(0xffffffffu, rbest, o);
+        if (go < gbest || (go == gbest && ro < rbest)) {
+            gbest = go;
+            rbest = ro;
+        }
+    }
+    const int r = rbest;
+    // ratios in parallel: z_i = ratio_i z_{i+1} (i < r), z_i = ratio_i z_{i-1} (i > r)
+    for (int i = lane; i < n; i += 32)
+        zs[i] = i < r ? -e[i] * rcp_nr2(Dp[i]) : (i > r ? -e[i - 1] * rcp_nr2(Dm[i]) : 1.0);
+    __syncwarp();
     if (lane == 0) {
-        double* dd = work + warp * 6 * n;  // diagonal of U
-        double* du = dd + n;               // first superdiagonal of U
-        double* du2 = du + n;              // second superdiagonal (fill-in)
-        double* dl = du2 + n;              // multipliers
-        double* sw = dl + n;               // 1.0 where rows i, i+1 were interchanged
-        for (int i = 0; i < n; ++i) {
-            dd[i] = d[i] - lmb;
-            du[i] = i + 1 < n ? e[i] : 0.0;
-            dl[i] = i + 1 < n ? e[i] : 0.0;
-            du2[i] = 0.0;
-            sw[i] = 0.0;
+        double zi = 1.0;
+        for (int i = r - 1; i >= 0; --i) {
+            zi *= zs[i];
+            zs[i] = zi;
         }
-        const double tiny = DBL_EPSILON * fmax(tnorm, DBL_MIN);
-        for (int i = 0; i + 1 < n; ++i) {
-            if (fabs(dd[i]) >= fabs(dl[i])) {
-                const double fact = dd[i] != 0.0 ? dl[i] / dd[i] : 0.0;
-                dl[i] = fact;
-                dd[i + 1] -= fact * du[i];
-            } else {
-                const double fact = dd[i] / dl[i];
-                dd[i] = dl[i];
-                dl[i] = fact;
-                const double t = du[i];
-                du[i] = dd[i + 1];
-                dd[i + 1] = t - fact * dd[i + 1];
-                if (i + 2 < n) {
-                    du2[i] = du[i + 1];
-                    du[i + 1] = -fact * du[i + 1];
-                }
-                sw[i] = 1.0;
-            }
-            if (fabs(dd[i]) < tiny) dd[i] = copysign(tiny, dd[i]);
+    } else if (lane == 1) {
+        double zi = 1.0;
+        for (int i = r + 1; i < n; ++i) {
+            zi *= zs[i];
+            zs[i] = zi;
         }
-        if (fabs(dd[n - 1]) < tiny) dd[n - 1] = copysign(tiny, dd[n - 1]);
-        for (int i = 0; i < n; ++i) dd[i] = 1.0 / dd[i];  // solves multiply by 1/pivot
-        double* xs = sw + n;  // the iterate, in shared memory
-        auto X = [&](int i) -> double& { return xs[i]; };
-        for (int i = 0; i < n; ++i) X(i) = 1.0 + 0.01 * ((i * 7 + j * 13) % 17);
-        for (int pass = 0; pass < 3; ++pass) {
-            for (int i = 0; i + 1 < n; ++i) {  // L^{-1} with the interchanges
-                if (sw[i] == 0.0) {
-                    X(i + 1) -= dl[i] * X(i);
-                } else {
-                    const double t = X(i);
-                    X(i) = X(i + 1);
-                    X(i + 1) = t - dl[i] * X(i);
-                }
-            }
-            double nrm = 0.0;
-            for (int i = n - 1; i >= 0; --i) {  // U^{-1}
-                double sum = X(i);
-                if (i + 1 < n) sum -= du[i] * X(i + 1);
-                if (i + 2 < n) sum -= du2[i] * X(i + 2);
-                sum *= dd[i];
-                X(i) = sum;
-                nrm = fmax(nrm, fabs(sum));
-            }
-            const double inv = nrm > 0.0 ? 1.0 / nrm : 1.0;
-            for (int i = 0; i < n; ++i) X(i) *= inv;
-        }
-        double s2 = 0.0;
-        for (int i = 0; i < n; ++i) s2 = fma(X(i), X(i), s2);
-        const double inv = 1.0 / sqrt(s2);
-        for (int i = 0; i < n; ++i) X(i) *= inv;
     }
     __syncwarp();
-    for (int i = lane; i < n; i += 32) z[static_cast<int64_t>(i) * ldz + j] = work[warp * 6 * n + 5 * n + i];
+    double s2 = 0.0;
+    for (int i = lane; i < n; i += 32) s2 = fma(zs[i], zs[i], s2);
+    s2 = warp_sum(s2);
+    const double inv = 1.0 / sqrt(s2);
+    EIG_PROBE(j, 2);
+    for (int i = lane; i < n; i += 32) z[static_cast<int64_t>(i) * ldz + j] = zs[i] * inv;
 }
 
 // ---- 3. orthonormalisation: Z <- Z (3I - Z^T Z) / 2, twice -----------------------------
@@ -504,7 +609,8 @@ bool tbi_supported(int l) { return l >= 3 && l <= 160; }
 
 size_t tbi_workspace_bytes(int l) {
     const size_t n = l;
-    return sizeof(double) * (n * n /*hv*/ + n /*tau*/ + 2 * n /*d,e*/ + 3 * n * n /*z, S, z2*/) + 64;
+    return sizeof(double) * (n * n /*hv*/ + n /*tau*/ + 2 * n /*d,e*/ + 3 * n * n /*z, S, z2*/) +
+           sizeof(int32_t) * kGridPts /*count grid*/ + 64;
 }
 
 // Runs the tridiagonal path; sets *clustered (device) when the spectrum needs
@@ -526,11 +632,14 @@ void tbi_eig(const double* g, EigWorkspace& w, void* tbi_ws, int32_t* clustered,
                                          static_cast<int>(s1)));
     tbi_tridiag_kernel<<<1, kTridThreads, s1, stream>>>(g, n, d, e, hv, tau, gate, nullptr);
     DSVD_LAUNCH_CHECK();
-    const size_t s2 = sizeof(double) * (3 * static_cast<size_t>(n) + kTbiWarps * 6 * static_cast<size_t>(n));
+    int32_t* counts = reinterpret_cast<int32_t*>(z2 + static_cast<size_t>(n) * n);
+    tbi_grid_kernel<<<kGridPts / 512, 256, sizeof(double) * 3 * n, stream>>>(d, e, n, counts, gate, nullptr);
+    DSVD_LAUNCH_CHECK();
+    const size_t s2 = sizeof(double) * (3 * static_cast<size_t>(n) + kTbiWarps * 3 * static_cast<size_t>(n));
     DSVD_CUDA_CHECK(cudaFuncSetAttribute(tbi_eig_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(s2)));
     tbi_eig_kernel<<<static_cast<unsigned>(ceil_div(n, kTbiWarps)), 32 * kTbiWarps, s2, stream>>>(
-        d, e, n, w.lam, z, n, clustered, gate, nullptr);
+        d, e, n, counts, w.lam, z, n, clustered, gate, nullptr);
     DSVD_LAUNCH_CHECK();
     const dim3 ns_grid(static_cast<unsigned>(ceil_div(n, kNsTile)), static_cast<unsigned>(ceil_div(n, kNsTile)));
     for (int step = 0; step < 2; ++step) {
