@@ -324,6 +324,12 @@ def run_b200(args, rank, world, local_rank):
         pass_gbs.append(b / (t * 1e-3) / 1e9 if t > 0 else None)
     st0 = stats_list[-1]
     traffic = committed_traffic(args.config)
+    # the row gathers actually moved through L1/L2: nnz * 8 * ld bytes per pass
+    # (ld = l rounded up to 4), against the measured random-gather ceiling
+    ld = (l + 3) // 4 * 4
+    gather_bytes_pass = a_full.nnz * 8 * ld
+    sp_passes = sum(s["spmm_launches"] for s in stats_list)
+    gather_tbs = gather_bytes_pass * sp_passes / (sp_ms * 1e-3) / 1e12 if sp_ms > 0 else None
     breakdown = {key: round(st0[key], 3) for key in ("total_ms", "csc_ms", "spmm_ms", "gram_ms",
                                                       "eig_ms", "rescale_ms")}
     breakdown["spmm_pass_ms"] = [round(x, 3) for x in st0["spmm_pass_ms"]]
@@ -352,7 +358,11 @@ def run_b200(args, rank, world, local_rank):
                      "peak_source": peak_kind,
                      "kernel": "csr_spmm_f64 (both passes)",
                      "pass_gbs": pass_gbs,
-                     "algorithmic_bytes_per_launch": sp_bytes / max(sp_launch, 1)},
+                     "algorithmic_bytes_per_launch": sp_bytes / max(sp_launch, 1),
+                     "gather": {"bytes_per_launch": gather_bytes_pass, "achieved_tbs": gather_tbs,
+                                "ceiling_tbs": 24.1,
+                                "ceiling_source": "tools/micro/gather2.cu: 1 KB Zipf(1.1) row gathers over "
+                                                  "a 122 MB X, no FMAs, 8 loads in flight per warp"}},
         "gpu_launches": int(st0["kernel_launches"]) * args.steps,
         "breakdown_last_step": breakdown,
         "iterations": e2e_res.trace.iterations,
