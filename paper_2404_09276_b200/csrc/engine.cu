@@ -429,10 +429,16 @@ void solve_tall(dsvd_ctx* ctx, const DevCsr& A, const DevCsr& AT, const dsvd_con
     control_init(ctrl, s_stored, static_cast<int>(l), st);
     count_launch();
 
-    // Omega = gaussian_matrix(m, l, seed) (solver.cpp:83)
+    // Omega = gaussian_matrix(m, l, seed) (solver.cpp:83), unless it was already
+    // generated beside the host upload (pregenerate_omega)
     int sp = ctx->span_begin(K_OTHER);
-    gaussian_rowmajor(Y, m, l, ld, cfg.seed, st, global_m, row_offset);
-    count_launch();
+    if (ctx->omega_pending && !sharded && ctx->omega_m == m && ctx->omega_l == l && ctx->omega_seed == cfg.seed) {
+        DSVD_CUDA_CHECK(cudaStreamWaitEvent(st, ctx->omega_ev, 0));
+    } else {
+        gaussian_rowmajor(Y, m, l, ld, cfg.seed, st, global_m, row_offset);
+        count_launch();
+    }
+    ctx->omega_pending = false;
     ctx->span_end(sp);
 
     // Q = eigSVD(A^T Omega).u
@@ -623,6 +629,29 @@ int guarded(F&& f) {
     }
 }
 
+// Starts Omega for the solve of an m x n host matrix on the side stream, so it
+// overlaps the CSR upload that follows on the main stream (single-GPU solves).
+void pregenerate_omega(dsvd_ctx* ctx, int64_t rows, int64_t cols, const dsvd_config& cfg) {
+    ctx->omega_pending = false;
+    if (ctx->comm != nullptr || cfg.k < 1 || cfg.alg == DSVD_ALG_BASIC) return;
+    const bool direct = (cfg.flags & DSVD_FLAG_DIRECT) != 0;
+    const int64_t m = (rows < cols && !direct) ? cols : rows;  // the tall orientation (solve_pair)
+    const int64_t l = cfg.k + effective_s(cfg);
+    if (l > 512 || m < 1) return;
+    const int64_t ld = padded_ld(l);
+    double* Y = ctx->tbuf<double>("Y", m * ld);
+    if (!ctx->omega_ev) DSVD_CUDA_CHECK(cudaEventCreateWithFlags(&ctx->omega_ev, cudaEventDisableTiming));
+    DSVD_CUDA_CHECK(cudaEventRecord(ctx->fork, ctx->stream));  // earlier work on Y is done
+    DSVD_CUDA_CHECK(cudaStreamWaitEvent(ctx->side, ctx->fork, 0));
+    gaussian_rowmajor(Y, m, l, ld, cfg.seed, ctx->side);
+    count_launch();
+    DSVD_CUDA_CHECK(cudaEventRecord(ctx->omega_ev, ctx->side));
+    ctx->omega_pending = true;
+    ctx->omega_m = m;
+    ctx->omega_l = l;
+    ctx->omega_seed = cfg.seed;
+}
+
 void solve_pair(dsvd_ctx* ctx, const DevCsr& a, const DevCsr& at, const dsvd_config& cfg,
                 dsvd_outputs* out, dsvd_observer_fn observer, void* user, int64_t row_offset = 0,
                 int64_t global_rows = -1) {
@@ -732,6 +761,7 @@ int dsvd_ctx_destroy(dsvd_ctx* ctx) {
         cudaStreamDestroy(ctx->side);
         cudaEventDestroy(ctx->fork);
         cudaEventDestroy(ctx->join);
+        if (ctx->omega_ev) cudaEventDestroy(ctx->omega_ev);
         cudaStreamDestroy(ctx->stream);
         delete ctx;
     });
@@ -907,6 +937,7 @@ int dsvd_solve(dsvd_ctx* ctx, const dsvd_matrix* a, const dsvd_config* cfg, dsvd
                dsvd_observer_fn observer, void* user) {
     return guarded([&] {
         set_device(ctx);
+        ctx->omega_pending = false;
         const int64_t l0 = g_launches.load();
         begin_profile(ctx);
         cudaEvent_t e0 = ctx->event(), e1 = ctx->event();
@@ -934,6 +965,7 @@ int dsvd_solve_csr(dsvd_ctx* ctx, int64_t rows, int64_t cols, int64_t nnz, const
         DSVD_CUDA_CHECK(cudaEventRecord(e0, ctx->stream));
         DevCsr a, at;
         CsrAlloc al{ctx, "csr.", nullptr};
+        pregenerate_omega(ctx, rows, cols, *cfg);
         upload_pair(ctx, al, rows, cols, nnz, offsets, col_indices, values, a, at);
         DSVD_CUDA_CHECK(cudaEventRecord(e1, ctx->stream));
         solve_pair(ctx, a, at, *cfg, out, nullptr, nullptr, ctx->shard_row_offset,
@@ -955,6 +987,7 @@ int dsvd_solve_csr_device(dsvd_ctx* ctx, int64_t rows, int64_t cols, int64_t nnz
                           const dsvd_config* cfg, dsvd_outputs* out) {
     return guarded([&] {
         set_device(ctx);
+        ctx->omega_pending = false;
         if (ctx->comm == nullptr) validate(*cfg, rows, cols);
         const int64_t l0 = g_launches.load();
         begin_profile(ctx);

@@ -54,6 +54,13 @@ struct dsvd_ctx {
     int dense_method = 0;           // 0: FP64 tensor-core Gram / rescale (dmma.cu), 1: DFMA kernels
     int eig_method = 0;             // 0: tridiagonal + inverse iteration (Jacobi fallback), 1: Jacobi
     cudaStream_t side = nullptr;    // second stream: hub-row SpMM runs beside the bulk kernel
+    // Omega generated on `side` while the host CSR uploads (host-input solves):
+    // the next solve_tall with the same (m, l, seed) waits on omega_ev instead
+    // of generating it
+    bool omega_pending = false;
+    int64_t omega_m = 0, omega_l = 0;
+    uint64_t omega_seed = 0;
+    cudaEvent_t omega_ev = nullptr;
     cudaEvent_t fork = nullptr, join = nullptr;
     int32_t* host_flags = nullptr;  // pinned ring for stop flags
     cudaEvent_t timer[2] = {nullptr, nullptr};
