@@ -1,12 +1,12 @@
 // FP64 tensor-core (DMMA, mma.sync m8n8k4 f64) kernels for the two dense
 // products of every power iteration (eigSVD, decompositions.cpp:52-73):
 //
-//   gram_dmma    G = C^T C for row-major C (n x l): one warp per pair of
-//                block rows (a, NB-1-a) of the 8x8-blocked upper triangle, so
-//                every warp issues NB+1 DMMAs per 4-row k-step; C is staged
-//                16 rows at a time by cp.async; per-CTA partial triangles are
-//                summed in a fixed order (deterministic, not the reference's
-//                single FMA chain; the eigensolver is not bitwise either).
+//   gram_dmma    G = C^T C for row-major C (n x l): one warp per 4x4 tile of
+//                8x8 blocks on and above the diagonal (16 DMMAs per 8 fragment
+//                loads per 4-row k-step); C is staged 32 rows at a time by
+//                cp.async; per-CTA partial triangles are summed in a fixed
+//                order (deterministic, not the reference's single FMA chain;
+//                the eigensolver is not bitwise either).
 //   rescale_dmma out = C (W diag(scale)) for the 150-wide tall-skinny blocks:
 //                CTA tile 128 rows x 32 columns, the W column block resident
 //                in shared memory (pre-transposed, scale folded in), C staged
@@ -153,19 +153,30 @@ rescale_dmma_kernel(const double* __restrict__ c, int64_t n, int K, int64_t ldc,
 constexpr int kGmRows = 32, kGmStages = 4;
 
 __host__ __device__ constexpr int gm_pairs(int nb) { return nb * (nb + 1) / 2; }
-__host__ __device__ constexpr int gm_stride(int nb) { return nb % 2 ? nb * 8 : nb * 8 + 8; }
 __device__ __forceinline__ int gm_tri(int a, int j, int nb) { return a * nb - a * (a - 1) / 2 + (j - a); }
 
-template <int NB>
-__global__ void __launch_bounds__(32 * ((NB + 1) / 2))
-gram_dmma_kernel(const double* __restrict__ c, int64_t n, int64_t ld, int64_t rows_per_block,
+// 4x4 register-blocked Gram: the 8x8-block grid (padded to NB4*4 blocks) is
+// covered by NB4(NB4+1)/2 tiles of 4x4 blocks on and above the diagonal, one
+// warp each; per 4-row k-step a warp loads 8 fragments (4 on diagonal tiles)
+// for 16 DMMAs. Shared-memory rows are 32*NB4 + 8 doubles (2*S == 16 mod 32
+// banks: the four rows of a fragment load fall in two wavefronts).
+__host__ __device__ constexpr int gm4_stride(int nb4) { return 32 * nb4 + 8; }
+
+template <int NB4>
+__global__ void __launch_bounds__(32 * NB4 * (NB4 + 1) / 2, NB4 >= 5 ? 1 : (NB4 == 4 ? 2 : (NB4 == 3 ? 3 : 4)))
+gram_dmma_kernel(const double* __restrict__ c, int64_t n, int64_t ld, int nb, int64_t rows_per_block,
                  double* __restrict__ partial, const int32_t* __restrict__ gate) {
     if (gate != nullptr && *gate != 0) return;
-    constexpr int S = gm_stride(NB);
+    constexpr int S = gm4_stride(NB4);
     extern __shared__ __align__(16) double gsm[];  // [stages][kGmRows][S]
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int q = lane & 3, g = lane >> 2;
-    const int a = warp, b = NB - 1 - warp;  // block rows of this warp (a == b: middle row)
+    int I = 0, t = warp;  // tile (I, J), I <= J, row-major over the upper triangle
+    while (t >= NB4 - I) {
+        t -= NB4 - I;
+        ++I;
+    }
+    const int J = I + t;
     const int64_t r_beg = static_cast<int64_t>(blockIdx.x) * rows_per_block;
     const int64_t r_end = min(n, r_beg + rows_per_block);
     const int vec = static_cast<int>(ld / 2);
@@ -185,13 +196,16 @@ gram_dmma_kernel(const double* __restrict__ c, int64_t n, int64_t ld, int64_t ro
         }
     };
     const int nst = static_cast<int>(((r_end > r_beg ? r_end - r_beg : int64_t(0)) + kGmRows - 1) / kGmRows);
-    for (int s = 0; s < kGmStages - 1; ++s) {
-        if (s < nst) stage(s, r_beg + s * kGmRows);
+    for (int st = 0; st < kGmStages - 1; ++st) {
+        if (st < nst) stage(st, r_beg + st * kGmRows);
         cpa_commit();
     }
-    double2 accA[NB], accB[NB];
+    double2 acc[4][4];
 #pragma unroll
-    for (int j = 0; j < NB; ++j) accA[j] = accB[j] = make_double2(0.0, 0.0);
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) acc[u][v] = make_double2(0.0, 0.0);
+    const bool diag = I == J;
     for (int st = 0; st < nst; ++st) {
         cpa_wait<kGmStages - 2>();
         __syncthreads();
@@ -199,29 +213,35 @@ gram_dmma_kernel(const double* __restrict__ c, int64_t n, int64_t ld, int64_t ro
         if (pf < nst) stage(pf % kGmStages, r_beg + static_cast<int64_t>(pf) * kGmRows);
         cpa_commit();
         const double* C = gsm + (st % kGmStages) * kGmRows * S;
-#pragma unroll
+#pragma unroll 2
         for (int ks = 0; ks < kGmRows / 4; ++ks) {
             const double* row = C + (4 * ks + q) * S + g;
-            const double fa = row[8 * a], fb = row[8 * b];
+            double fa[4], fb[4];
 #pragma unroll
-            for (int j = 0; j < NB; ++j) {
-                if (j >= a) {
-                    const double fj = row[8 * j];
-                    dmma884(accA[j], fa, fj);
-                    if (j >= b && b != a) dmma884(accB[j], fb, fj);
-                }
+            for (int u = 0; u < 4; ++u) fa[u] = row[8 * (4 * I + u)];
+            if (diag) {
+#pragma unroll
+                for (int v = 0; v < 4; ++v) fb[v] = fa[v];
+            } else {
+#pragma unroll
+                for (int v = 0; v < 4; ++v) fb[v] = row[8 * (4 * J + v)];
             }
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+#pragma unroll
+                for (int v = 0; v < 4; ++v) dmma884(acc[u][v], fa[u], fb[v]);
         }
     }
     cpa_wait<0>();
-    double* out = partial + static_cast<int64_t>(blockIdx.x) * gm_pairs(NB) * 64;
+    double* out = partial + static_cast<int64_t>(blockIdx.x) * gm_pairs(nb) * 64;
 #pragma unroll
-    for (int j = 0; j < NB; ++j) {
-        if (j >= a)
-            *reinterpret_cast<double2*>(out + gm_tri(a, j, NB) * 64 + g * 8 + 2 * q) = accA[j];
-        if (j >= b && b != a)
-            *reinterpret_cast<double2*>(out + gm_tri(b, j, NB) * 64 + g * 8 + 2 * q) = accB[j];
-    }
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+            const int bi = 4 * I + u, bj = 4 * J + v;
+            if (bi <= bj && bj < nb)
+                *reinterpret_cast<double2*>(out + gm_tri(bi, bj, nb) * 64 + g * 8 + 2 * q) = acc[u][v];
+        }
 }
 
 // G(i, j) = G(j, i) = sum over CTAs of the partial block entry: 256 threads per
@@ -255,13 +275,13 @@ gram_dmma_reduce_kernel(const double* __restrict__ partial, int nblk, int nb, in
     g[j * l + i] = s;
 }
 
-template <int NB>
-void launch_gram_dmma(const double* c, int64_t n, int64_t ld, int nblk, int64_t rpb, double* partial,
+template <int NB4>
+void launch_gram_dmma(const double* c, int64_t n, int64_t ld, int nb, int nblk, int64_t rpb, double* partial,
                       const int32_t* gate, cudaStream_t stream) {
-    const size_t smem = sizeof(double) * kGmStages * kGmRows * gm_stride(NB);
-    DSVD_CUDA_CHECK(cudaFuncSetAttribute(gram_dmma_kernel<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    const size_t smem = sizeof(double) * kGmStages * kGmRows * gm4_stride(NB4);
+    DSVD_CUDA_CHECK(cudaFuncSetAttribute(gram_dmma_kernel<NB4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem)));
-    gram_dmma_kernel<NB><<<nblk, 32 * ((NB + 1) / 2), smem, stream>>>(c, n, ld, rpb, partial, gate);
+    gram_dmma_kernel<NB4><<<nblk, 32 * NB4 * (NB4 + 1) / 2, smem, stream>>>(c, n, ld, nb, rpb, partial, gate);
     DSVD_LAUNCH_CHECK();
 }
 
@@ -272,9 +292,9 @@ struct GramDmmaPlan {
 GramDmmaPlan gram_dmma_plan(int64_t n, int64_t l) {
     GramDmmaPlan p;
     p.nb = static_cast<int>((l + 7) / 8);
-    const int warps = (p.nb + 1) / 2;  // ~150 registers per thread: one CTA per SM at 10 warps
-    p.nblk = static_cast<int>(
-        std::max<int64_t>(1, std::min<int64_t>(kNumSMs * std::max(1, 10 / warps), ceil_div(n, 64))));
+    const int nb4 = (p.nb + 3) / 4;  // CTAs per SM as in the launch bounds
+    p.nblk = static_cast<int>(std::max<int64_t>(
+        1, std::min<int64_t>(kNumSMs * (nb4 >= 5 ? 1 : (nb4 == 4 ? 2 : (nb4 == 3 ? 3 : 4))), ceil_div(n, 64))));
     p.rpb = ceil_div(ceil_div(n, p.nblk), kGmRows) * kGmRows;
     p.nblk = static_cast<int>(std::max<int64_t>(1, ceil_div(n, p.rpb)));
     return p;
@@ -293,14 +313,12 @@ void gram_dmma(const double* c, int64_t n, int64_t l, int64_t ld, double* g, voi
                cudaStream_t stream) {
     const GramDmmaPlan p = gram_dmma_plan(n, l);
     double* partial = static_cast<double*>(ws);
-    switch (p.nb) {
-#define DSVD_GRAM_CASE(NB) \
-    case NB: launch_gram_dmma<NB>(c, n, ld, p.nblk, p.rpb, partial, gate, stream); break;
-        DSVD_GRAM_CASE(1) DSVD_GRAM_CASE(2) DSVD_GRAM_CASE(3) DSVD_GRAM_CASE(4) DSVD_GRAM_CASE(5)
-        DSVD_GRAM_CASE(6) DSVD_GRAM_CASE(7) DSVD_GRAM_CASE(8) DSVD_GRAM_CASE(9) DSVD_GRAM_CASE(10)
-        DSVD_GRAM_CASE(11) DSVD_GRAM_CASE(12) DSVD_GRAM_CASE(13) DSVD_GRAM_CASE(14) DSVD_GRAM_CASE(15)
-        DSVD_GRAM_CASE(16) DSVD_GRAM_CASE(17) DSVD_GRAM_CASE(18) DSVD_GRAM_CASE(19) DSVD_GRAM_CASE(20)
-#undef DSVD_GRAM_CASE
+    switch ((p.nb + 3) / 4) {
+        case 1: launch_gram_dmma<1>(c, n, ld, p.nb, p.nblk, p.rpb, partial, gate, stream); break;
+        case 2: launch_gram_dmma<2>(c, n, ld, p.nb, p.nblk, p.rpb, partial, gate, stream); break;
+        case 3: launch_gram_dmma<3>(c, n, ld, p.nb, p.nblk, p.rpb, partial, gate, stream); break;
+        case 4: launch_gram_dmma<4>(c, n, ld, p.nb, p.nblk, p.rpb, partial, gate, stream); break;
+        case 5: launch_gram_dmma<5>(c, n, ld, p.nb, p.nblk, p.rpb, partial, gate, stream); break;
         default: fail(DSVD_OTHER, "gram_dmma: unsupported width");
     }
     gram_dmma_reduce_kernel<<<gm_pairs(p.nb), 256, 0, stream>>>(partial, p.nblk, p.nb, l, g, gate);
