@@ -17,6 +17,9 @@
 // tools/micro/dmma_tput.cu) but one DMMA carries 256 FMAs, which leaves issue
 // slots for the operand loads; the register-tiled DFMA kernels these replace
 // reached ~26% of the FP64 pipe.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include "dense.cuh"
 
 namespace dsvd {
@@ -38,6 +41,40 @@ __device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_gro
 template <int N>
 __device__ __forceinline__ void cpa_wait() {
     asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+__device__ __forceinline__ unsigned su32(const void* p) { return static_cast<unsigned>(__cvta_generic_to_shared(p)); }
+__device__ __forceinline__ void bar_init(uint64_t* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(su32(bar)), "r"(count));
+}
+__device__ __forceinline__ void bar_expect_tx(uint64_t* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(su32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bar_wait(uint64_t* bar, unsigned parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(su32(bar)),
+        "r"(parity)
+        : "memory");
+}
+// 2-D TMA tile load (box of the tensor map at column x, row y) into shared memory
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int x, int y, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(
+            su32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(su32(bar))
+        : "memory");
+}
+// 1-D bulk copy global -> shared (bytes a multiple of 16)
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(su32(dst)),
+        "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(su32(bar))
+        : "memory");
 }
 
 // ---- rescale ----------------------------------------------------------------------
@@ -147,6 +184,133 @@ rescale_dmma_kernel(const double* __restrict__ c, int64_t n, int K, int64_t ldc,
             }
         }
     }
+}
+
+// TMA-fed variant: one thread streams the C tiles (128 rows x 16 k, 128-byte
+// swizzle) into a kRsStages ring with mbarriers and bulk-copies the W block;
+// fragment addresses follow the swizzle (16-byte chunk c of row r lives at
+// chunk c ^ (r & 7)). Removes the per-thread cp.async address arithmetic,
+// which was ~45% of the issued instructions of rescale_dmma_kernel.
+__global__ void __launch_bounds__(kRsThreads, 2)
+rescale_tma_kernel(const __grid_constant__ CUtensorMap cmap, int64_t n, int K, const double* __restrict__ wt,
+                   int ldb, int ncol, double* __restrict__ out, int64_t ld_out, int out_colmajor,
+                   const int32_t* __restrict__ gate) {
+    if (gate != nullptr && *gate != 0) return;
+    extern __shared__ __align__(1024) unsigned char rsm_raw[];
+    // 1024-byte aligned ring first (128B-swizzle requirement), then W, then barriers
+    double* As = reinterpret_cast<double*>(rsm_raw + ((1024 - (su32(rsm_raw) & 1023)) & 1023));
+    double* Bt = As + kRsStages * kRsBM * kRsBK;
+    uint64_t* full = reinterpret_cast<uint64_t*>(Bt + kRsBN * ldb);
+    uint64_t* wbar = full + kRsStages;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int q = lane & 3, g = lane >> 2;
+    const int j0 = blockIdx.x * kRsBN;
+    const int nk = (K + kRsBK - 1) / kRsBK;
+    const int64_t nrb = (n + kRsBM - 1) / kRsBM;
+    constexpr unsigned kTileBytes = kRsBM * kRsBK * sizeof(double);
+    if (tid == 0) {
+        for (int s = 0; s < kRsStages; ++s) bar_init(&full[s], 1);
+        bar_init(wbar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+    }
+    __syncthreads();
+    if (tid == 0) {
+        const unsigned wbytes = static_cast<unsigned>(kRsBN * ldb * sizeof(double));
+        bar_expect_tx(wbar, wbytes);
+        bulk_load(Bt, wt + static_cast<int64_t>(j0) * ldb, wbytes, wbar);
+    }
+    bar_wait(wbar, 0);
+    unsigned use = 0;  // chunks consumed so far (ring position and mbarrier phase)
+    for (int64_t rb = blockIdx.y; rb < nrb; rb += gridDim.y) {
+        const int y0 = static_cast<int>(rb * kRsBM);
+        if (tid == 0) {
+            for (int s = 0; s < kRsStages - 1 && s < nk; ++s) {
+                const unsigned slot = (use + s) % kRsStages;
+                bar_expect_tx(&full[slot], kTileBytes);
+                tma_load_2d(As + slot * (kRsBM * kRsBK), &cmap, s * kRsBK, y0, &full[slot]);
+            }
+        }
+        double2 acc[2][4];
+#pragma unroll
+        for (int a = 0; a < 2; ++a)
+#pragma unroll
+            for (int b = 0; b < 4; ++b) acc[a][b] = make_double2(0.0, 0.0);
+        for (int kc = 0; kc < nk; ++kc, ++use) {
+            __syncthreads();  // every warp is done with the slot refilled below
+            if (tid == 0 && kc + kRsStages - 1 < nk) {
+                const unsigned slot = (use + kRsStages - 1) % kRsStages;
+                bar_expect_tx(&full[slot], kTileBytes);
+                tma_load_2d(As + slot * (kRsBM * kRsBK), &cmap, (kc + kRsStages - 1) * kRsBK, y0, &full[slot]);
+            }
+            const unsigned slot = use % kRsStages;
+            bar_wait(&full[slot], (use / kRsStages) & 1);
+            const double* A = As + slot * (kRsBM * kRsBK);
+#pragma unroll
+            for (int p = 0; p < 2; ++p) {
+                double2 af[2], bf[4];
+#pragma unroll
+                for (int mb = 0; mb < 2; ++mb) {
+                    const int r = warp * 16 + mb * 8 + g;
+                    af[mb] = *reinterpret_cast<const double2*>(A + r * kRsBK + (((4 * p + q) ^ (r & 7)) << 1));
+                }
+                const int kg = kc * kRsBK + p * 8 + 2 * q;
+#pragma unroll
+                for (int nb = 0; nb < 4; ++nb)
+                    bf[nb] = *reinterpret_cast<const double2*>(Bt + (nb * 8 + g) * ldb + kg);
+#pragma unroll
+                for (int mb = 0; mb < 2; ++mb)
+#pragma unroll
+                    for (int nb = 0; nb < 4; ++nb) dmma884(acc[mb][nb], af[mb].x, bf[nb].x);
+#pragma unroll
+                for (int mb = 0; mb < 2; ++mb)
+#pragma unroll
+                    for (int nb = 0; nb < 4; ++nb) dmma884(acc[mb][nb], af[mb].y, bf[nb].y);
+            }
+        }
+        const int64_t r0 = rb * kRsBM;
+#pragma unroll
+        for (int mb = 0; mb < 2; ++mb) {
+            const int64_t r = r0 + warp * 16 + mb * 8 + g;
+            if (r >= n) continue;
+#pragma unroll
+            for (int nb = 0; nb < 4; ++nb) {
+                const int j = j0 + nb * 8 + 2 * q;
+                const double2 v = acc[mb][nb];
+                if (out_colmajor) {
+                    if (j < ncol) out[static_cast<int64_t>(j) * n + r] = v.x;
+                    if (j + 1 < ncol) out[static_cast<int64_t>(j + 1) * n + r] = v.y;
+                } else if (j + 1 < ld_out) {
+                    *reinterpret_cast<double2*>(out + r * ld_out + j) = v;
+                } else if (j < ld_out) {
+                    out[r * ld_out + j] = v.x;
+                }
+            }
+        }
+    }
+}
+
+// 2-D tensor map over a row-major (rows x ld) fp64 block: box of 16 columns x
+// 128 rows, 128-byte swizzle, out-of-range elements read as zero.
+CUtensorMap make_cmap(const double* c, int64_t rows, int64_t ld) {
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+    if (encode == nullptr) {
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult qr;
+        DSVD_CUDA_CHECK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &qr));
+        if (fn == nullptr || qr != cudaDriverEntryPointSuccess) fail(DSVD_CUDA, "cuTensorMapEncodeTiled unavailable");
+        encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }
+    CUtensorMap map;
+    const cuuint64_t dims[2] = {static_cast<cuuint64_t>(ld), static_cast<cuuint64_t>(rows)};
+    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld * sizeof(double))};
+    const cuuint32_t box[2] = {kRsBK, kRsBM};
+    const cuuint32_t estr[2] = {1, 1};
+    const CUresult r = encode(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(c), dims, strides, box,
+                              estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) fail(DSVD_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(r));
+    return map;
 }
 
 // ---- gram -------------------------------------------------------------------------
@@ -325,6 +489,8 @@ void gram_dmma(const double* c, int64_t n, int64_t l, int64_t ld, double* g, voi
     DSVD_LAUNCH_CHECK();
 }
 
+bool rescale_use_tma = true;
+
 bool rescale_dmma_supported(int64_t K, int64_t ldc, int64_t ld_out, int out_colmajor) {
     return K >= 1 && K <= kRsMaxK && ldc % 2 == 0 && ldc >= K && (out_colmajor || ld_out % 2 == 0);
 }
@@ -347,14 +513,26 @@ void rescale_dmma(const double* c, int64_t n, int64_t K, int64_t ldc, const doub
     rescale_prep_kernel<<<static_cast<unsigned>(ceil_div(static_cast<int64_t>(npad) * ldb, 256)), 256, 0, stream>>>(
         w, ldw, scale, static_cast<int>(K), static_cast<int>(ncol), npad, ldb, wt, gate);
     DSVD_LAUNCH_CHECK();
-    const size_t smem = sizeof(double) * (static_cast<size_t>(kRsBN) * ldb + kRsStages * kRsBM * kRsBK);
-    DSVD_CUDA_CHECK(cudaFuncSetAttribute(rescale_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem)));
     const int64_t nrb = ceil_div(n, kRsBM);
     const dim3 grid(static_cast<unsigned>(ncb), static_cast<unsigned>(std::min<int64_t>(nrb, 65535)));
-    rescale_dmma_kernel<<<grid, kRsThreads, smem, stream>>>(c, n, static_cast<int>(K), ldc, wt, ldb,
-                                                            static_cast<int>(ncol), out, ld_out, out_colmajor,
-                                                            gate);
+    const bool tma = rescale_use_tma && (reinterpret_cast<uintptr_t>(c) % 16) == 0 && (ldc * 8) % 16 == 0;
+    if (tma) {
+        const size_t smem = 1024 + sizeof(double) * (kRsStages * kRsBM * kRsBK + static_cast<size_t>(kRsBN) * ldb) +
+                            sizeof(uint64_t) * (kRsStages + 1);
+        DSVD_CUDA_CHECK(cudaFuncSetAttribute(rescale_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             static_cast<int>(smem)));
+        const CUtensorMap cmap = make_cmap(c, n, ldc);
+        rescale_tma_kernel<<<grid, kRsThreads, smem, stream>>>(cmap, n, static_cast<int>(K), wt, ldb,
+                                                               static_cast<int>(ncol), out, ld_out, out_colmajor,
+                                                               gate);
+    } else {
+        const size_t smem = sizeof(double) * (static_cast<size_t>(kRsBN) * ldb + kRsStages * kRsBM * kRsBK);
+        DSVD_CUDA_CHECK(cudaFuncSetAttribute(rescale_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             static_cast<int>(smem)));
+        rescale_dmma_kernel<<<grid, kRsThreads, smem, stream>>>(c, n, static_cast<int>(K), ldc, wt, ldb,
+                                                                static_cast<int>(ncol), out, ld_out, out_colmajor,
+                                                                gate);
+    }
     DSVD_LAUNCH_CHECK();
 }
 
