@@ -144,7 +144,7 @@ tbi_tridiag_kernel(const double* __restrict__ g, int n, double* __restrict__ d, 
             }
             TRID_PROBE(k, 3);
         } else {
-            const int C = (kTridWarps - 1) / G;  // column chunks
+            const int C = min((kTridWarps - 1) / G, max(1, (m + 15) / 16));  // column chunks of >= ~16
             const int item = warp - 1, grp = item % G, c = item / G;
             if (c < C) {
                 const int i = k1 + 32 * grp + lane;
@@ -175,7 +175,7 @@ tbi_tridiag_kernel(const double* __restrict__ g, int n, double* __restrict__ d, 
             double t = 0.0;
             if (tid < m) {
                 const int i = k1 + tid;
-                const int C = (kTridWarps - 1) / G;
+                const int C = min((kTridWarps - 1) / G, max(1, (m + 15) / 16));
                 double p = 0.0;
                 for (int c = 0; c < C; ++c) p += part[c * n + i];
                 p = fma(ref.v0 - ref.x0, A[i * lda + k1], p);
@@ -186,6 +186,7 @@ tbi_tridiag_kernel(const double* __restrict__ g, int n, double* __restrict__ d, 
                 t = wi * vi;
             }
             if (warp < G) {
+                __syncwarp();  // lanes past row n - 1 skipped the block above
                 t = warp_sum(t);
                 if (lane == 0) s_ksum[warp] = t;
             }
