@@ -133,6 +133,8 @@ void build_chunks(dsvd_ctx* ctx, CsrAlloc& al, DevCsr& m, const std::string& tag
     }
     first[ns] = static_cast<int32_t>(chunks.size());
     const int64_t nc = static_cast<int64_t>(chunks.size());
+    m.max_row_chunks = 0;
+    for (int64_t i = 0; i < ns; ++i) m.max_row_chunks = std::max<int64_t>(m.max_row_chunks, first[i + 1] - first[i]);
     // list position of each chunk: stable by panel
     std::vector<int32_t> slot(static_cast<size_t>(nc));
     std::vector<int64_t> p0(static_cast<size_t>(nc)), p1(static_cast<size_t>(nc));

@@ -235,22 +235,92 @@ spmm_row_kernel(const int64_t* __restrict__ off, const int32_t* __restrict__ idx
 
 // y(row_i, :) = sum over the row's chunks, in chunk order, of partial(chunk, :),
 // then the shift epilogue.
+// y(row_i, :) = sum of the row's chunk partials (chunk_slot maps its chunks, in
+// CSR order, to partial rows), then the shift epilogue. One block per (split
+// row, 64-column group): warp w sums a contiguous eighth of the chunks in
+// order, the eight warp sums are added in warp order (a fixed tree:
+// deterministic), so a hub row with hundreds of chunks is not one thread's
+// serial chain.
 template <bool kShift>
-__global__ void split_combine_kernel(const double* __restrict__ partial,
-                                     const int32_t* __restrict__ split_first,
-                                     const int32_t* __restrict__ slot,
-                                     const int32_t* __restrict__ order, int64_t nsplit,
-                                     double* __restrict__ y, int64_t ld, const double* __restrict__ q,
-                                     const double* __restrict__ alpha_p,
-                                     const int32_t* __restrict__ gate) {
+__global__ void __launch_bounds__(256)
+split_combine_tree_kernel(const double* __restrict__ partial, const int32_t* __restrict__ split_first,
+                     const int32_t* __restrict__ slot, const int32_t* __restrict__ order, int64_t nsplit,
+                     double* __restrict__ y, int64_t ld, const double* __restrict__ q,
+                     const double* __restrict__ alpha_p, const int32_t* __restrict__ gate) {
+    if (gate != nullptr && *gate != 0) return;
+    __shared__ double2 red[8][32];
+    const int64_t i = blockIdx.x;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t col = static_cast<int64_t>(blockIdx.y) * 64 + 2 * lane;
+    const bool act = col < ld;  // ld is a multiple of 4
+    const int32_t c0 = split_first[i], c1 = split_first[i + 1];
+    const int32_t per = (c1 - c0 + 7) / 8;
+    const int32_t a = c0 + warp * per, b = min(c1, a + per);
+    double2 acc = make_double2(0.0, 0.0);
+    if (act) {
+        auto at = [&](int32_t c) {
+            const int64_t r = slot != nullptr ? slot[c] : c;
+            return *reinterpret_cast<const double2*>(partial + r * ld + col);
+        };
+        int32_t c = a;
+        for (; c + 4 <= b; c += 4) {
+            const double2 v0 = at(c), v1 = at(c + 1), v2 = at(c + 2), v3 = at(c + 3);
+            acc.x += v0.x; acc.y += v0.y;
+            acc.x += v1.x; acc.y += v1.y;
+            acc.x += v2.x; acc.y += v2.y;
+            acc.x += v3.x; acc.y += v3.y;
+        }
+        for (; c < b; ++c) {
+            const double2 v = at(c);
+            acc.x += v.x;
+            acc.y += v.y;
+        }
+    }
+    red[warp][lane] = acc;
+    __syncthreads();
+    if (warp != 0 || !act) return;
+    double2 s = red[0][lane];
+#pragma unroll
+    for (int w = 1; w < 8; ++w) {
+        s.x += red[w][lane].x;
+        s.y += red[w][lane].y;
+    }
+    const int64_t row = order[i];
+    if (kShift) {
+        const double alpha = *alpha_p;
+        if (alpha != 0.0) {
+            const double2 qv = *reinterpret_cast<const double2*>(q + row * ld + col);
+            s.x = fma(-alpha, qv.x, s.x);
+            s.y = fma(-alpha, qv.y, s.y);
+        }
+    }
+    *reinterpret_cast<double2*>(y + row * ld + col) = s;
+}
+
+// Flat variant for rows with few chunks: one thread per output element, the
+// chunk rows fetched eight ahead of the in-order additions.
+template <bool kShift>
+__global__ void split_combine_kernel(const double* __restrict__ partial, const int32_t* __restrict__ split_first,
+                                     const int32_t* __restrict__ slot, const int32_t* __restrict__ order,
+                                     int64_t nsplit, double* __restrict__ y, int64_t ld, const double* __restrict__ q,
+                                     const double* __restrict__ alpha_p, const int32_t* __restrict__ gate) {
     if (gate != nullptr && *gate != 0) return;
     const int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
     if (e >= nsplit * ld) return;
     const int64_t i = e / ld, col = e - (e / ld) * ld;
     const int64_t row = order[i];
     double acc = 0.0;
-    for (int32_t c = split_first[i]; c < split_first[i + 1]; ++c)
-        acc += partial[static_cast<int64_t>(slot != nullptr ? slot[c] : c) * ld + col];
+    const int32_t c0 = split_first[i], c1 = split_first[i + 1];
+    int32_t c = c0;
+    for (; c + 8 <= c1; c += 8) {
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+            v[u] = partial[static_cast<int64_t>(slot != nullptr ? slot[c + u] : c + u) * ld + col];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) acc += v[u];
+    }
+    for (; c < c1; ++c) acc += partial[static_cast<int64_t>(slot != nullptr ? slot[c] : c) * ld + col];
     if (kShift) {
         const double alpha = *alpha_p;
         if (alpha != 0.0) acc = fma(-alpha, q[row * ld + col], acc);
@@ -1004,13 +1074,25 @@ void spmm(const SpmmArgs& s, cudaStream_t stream, int variant, cudaStream_t side
     if (split) {
         DSVD_CUDA_CHECK(cudaEventRecord(join, side));
         DSVD_CUDA_CHECK(cudaStreamWaitEvent(stream, join, 0));
-        const int64_t n = a.nsplit * s.ld;
-        if (s.q != nullptr)
-            split_combine_kernel<true><<<static_cast<unsigned>(ceil_div(n, 256)), 256, 0, stream>>>(
-                partial, a.split_first, a.chunk_slot, a.order, a.nsplit, s.y, s.ld, s.q, s.alpha, s.gate);
-        else
-            split_combine_kernel<false><<<static_cast<unsigned>(ceil_div(n, 256)), 256, 0, stream>>>(
-                partial, a.split_first, a.chunk_slot, a.order, a.nsplit, s.y, s.ld, nullptr, nullptr, s.gate);
+        // rows with many chunks (hub columns of A^T): the 8-warp tree per row
+        if (a.max_row_chunks > 32) {
+            const dim3 cgrid(static_cast<unsigned>(a.nsplit), static_cast<unsigned>(ceil_div(s.ld, 64)));
+            if (s.q != nullptr)
+                split_combine_tree_kernel<true><<<cgrid, 256, 0, stream>>>(partial, a.split_first, a.chunk_slot, a.order,
+                                                                           a.nsplit, s.y, s.ld, s.q, s.alpha, s.gate);
+            else
+                split_combine_tree_kernel<false><<<cgrid, 256, 0, stream>>>(partial, a.split_first, a.chunk_slot,
+                                                                            a.order, a.nsplit, s.y, s.ld, nullptr,
+                                                                            nullptr, s.gate);
+        } else {
+            const int64_t n = a.nsplit * s.ld;
+            if (s.q != nullptr)
+                split_combine_kernel<true><<<static_cast<unsigned>(ceil_div(n, 256)), 256, 0, stream>>>(
+                    partial, a.split_first, a.chunk_slot, a.order, a.nsplit, s.y, s.ld, s.q, s.alpha, s.gate);
+            else
+                split_combine_kernel<false><<<static_cast<unsigned>(ceil_div(n, 256)), 256, 0, stream>>>(
+                    partial, a.split_first, a.chunk_slot, a.order, a.nsplit, s.y, s.ld, nullptr, nullptr, s.gate);
+        }
         DSVD_LAUNCH_CHECK();
         return;
     }

@@ -37,6 +37,7 @@ struct DevCsr {
     // list itself is ordered by X-row panel (see build_chunks) so chunks
     // running together gather from an L2-resident slice of X.
     int32_t* chunk_slot = nullptr;
+    int64_t max_row_chunks = 0;  // most chunks of one split row (picks the combine kernel)
 };
 
 // SpMM launch description. X and Y (and Q) are row-major with row stride ld.
