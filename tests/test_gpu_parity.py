@@ -519,6 +519,32 @@ def test_solve_deterministic(dev, c1):
     assert_bitwise(r1.svd.s, r2.svd.s)
 
 
+@pytest.mark.parametrize("alg", ["shifted", "dash"])
+def test_sharded_path_single_rank(oracle, c1, alg):
+    """The multi-GPU code path (NCCL communicator, shard bookkeeping, all-reduce
+    of the n x l partials, shift after the sum, all-reduced finalize Gram) run
+    with a one-rank communicator on the one GPU: it must reproduce the
+    single-GPU solve bitwise (one rank's all-reduce is the identity and the
+    separate shift kernel does the same fma as the fused epilogue)."""
+    cfg = (d.SolverConfig(k=50, s=25, p=6, alg=d.Algorithm.shifted, seed=0) if alg == "shifted"
+           else d.SolverConfig(k=50, s=25, tol=1e-2, seed=0))
+    plain = d.Device(0)
+    r_ref = d.solve(to_dev(c1), cfg, device=plain)
+    sh = d.Device(0)
+    sh.attach_comm(1, 0, d.comm_unique_id())
+    sh.set_shard(0, c1.rows)
+    r = d.solve(to_dev(c1), cfg, device=sh)
+    assert r.trace.iterations == r_ref.trace.iterations
+    assert_bitwise(r.svd.s, r_ref.svd.s)
+    assert_bitwise(r.svd.u, r_ref.svd.u)
+    assert_bitwise(r.svd.v, r_ref.svd.v)
+    ref = oracle.solve(c1, 50, 25, p=6, alg="shifted", seed=0) if alg == "shifted" else \
+        oracle.solve(c1, 50, 25, tol=1e-2, alg="dash", seed=0)
+    check_solve(r, ref, 50)
+    sh.close()
+    plain.close()
+
+
 def test_observer_and_snapshot_finalize(dev, oracle):
     # test_rsvd.cpp:341-389 + :424-458 on the device path
     a = oracle.sparse_random(60, 40, 6, 33, True)
