@@ -175,7 +175,7 @@ double* partial_for(dsvd_ctx* ctx, const DevCsr& a, int64_t ld) {
 // values already on the device.
 void build_pair(dsvd_ctx* ctx, CsrAlloc& al, int64_t rows, int64_t cols, int64_t nnz,
                 const int64_t* d_off, const int64_t* d_idx64, const double* d_val, DevCsr& a,
-                DevCsr& at, bool copy_inputs) {
+                DevCsr& at, bool copy_inputs, cudaEvent_t values_ready = nullptr) {
     cudaStream_t st = ctx->stream;
     if (rows < 0 || cols < 0 || nnz < 0) fail(DSVD_SHAPE, "sparse matrix with negative dimension");
     if (rows > 0x7fffffffLL || cols > 0x7fffffffLL)
@@ -219,7 +219,7 @@ void build_pair(dsvd_ctx* ctx, CsrAlloc& al, int64_t rows, int64_t cols, int64_t
     const size_t scratch_bytes =
         std::max({csc_scratch_bytes(rows, cols, nnz), order_scratch_bytes(rows), order_scratch_bytes(cols)});
     void* scratch = ctx->buf("csc.scratch", scratch_bytes);
-    build_transpose(a, at, scratch, scratch_bytes, st);
+    build_transpose(a, at, scratch, scratch_bytes, st, values_ready);
     count_launch(nnz > 0 ? 8 : 1);  // 4 own kernels + CUB radix sort passes (estimate)
     int32_t* hubs = static_cast<int32_t*>(al.get("hub_counts", sizeof(int32_t) * 2));
     // split mode: the "hub" prefix of the row order is the set of rows longer
@@ -255,11 +255,20 @@ void upload_pair(dsvd_ctx* ctx, CsrAlloc& al, int64_t rows, int64_t cols, int64_
     int64_t* d_idx64 = ctx->tbuf<int64_t>("upload.idx64", nnz);
     double* d_val = static_cast<double*>(al.get("a.val", sizeof(double) * nnz));
     DSVD_CUDA_CHECK(cudaMemcpyAsync(d_off, off, sizeof(int64_t) * (rows + 1), cudaMemcpyHostToDevice, st));
+    cudaEvent_t vals = nullptr;
     if (nnz) {
         DSVD_CUDA_CHECK(cudaMemcpyAsync(d_idx64, idx, sizeof(int64_t) * nnz, cudaMemcpyHostToDevice, st));
-        DSVD_CUDA_CHECK(cudaMemcpyAsync(d_val, val, sizeof(double) * nnz, cudaMemcpyHostToDevice, st));
+        // the values travel on the copy stream while the structure is checked,
+        // narrowed and sorted on the main stream (needed first by the CSC gather)
+        if (!ctx->copy) DSVD_CUDA_CHECK(cudaStreamCreateWithFlags(&ctx->copy, cudaStreamNonBlocking));
+        if (!ctx->copy_ev) DSVD_CUDA_CHECK(cudaEventCreateWithFlags(&ctx->copy_ev, cudaEventDisableTiming));
+        DSVD_CUDA_CHECK(cudaEventRecord(ctx->copy_ev, st));  // d_val is free (earlier work on st)
+        DSVD_CUDA_CHECK(cudaStreamWaitEvent(ctx->copy, ctx->copy_ev, 0));
+        DSVD_CUDA_CHECK(cudaMemcpyAsync(d_val, val, sizeof(double) * nnz, cudaMemcpyHostToDevice, ctx->copy));
+        DSVD_CUDA_CHECK(cudaEventRecord(ctx->copy_ev, ctx->copy));
+        vals = ctx->copy_ev;
     }
-    build_pair(ctx, al, rows, cols, nnz, d_off, d_idx64, d_val, a, at, false);
+    build_pair(ctx, al, rows, cols, nnz, d_off, d_idx64, d_val, a, at, false, vals);
 }
 
 // ---- config validation (solver.cpp:15-32) ---------------------------------
@@ -764,6 +773,8 @@ int dsvd_ctx_destroy(dsvd_ctx* ctx) {
         cudaEventDestroy(ctx->fork);
         cudaEventDestroy(ctx->join);
         if (ctx->omega_ev) cudaEventDestroy(ctx->omega_ev);
+        if (ctx->copy_ev) cudaEventDestroy(ctx->copy_ev);
+        if (ctx->copy) cudaStreamDestroy(ctx->copy);
         cudaStreamDestroy(ctx->stream);
         delete ctx;
     });

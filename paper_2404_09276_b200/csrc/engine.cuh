@@ -61,6 +61,8 @@ struct dsvd_ctx {
     int64_t omega_m = 0, omega_l = 0;
     uint64_t omega_seed = 0;
     cudaEvent_t omega_ev = nullptr;
+    cudaStream_t copy = nullptr;      // host->device copy of the CSR values (upload_pair)
+    cudaEvent_t copy_ev = nullptr;
     cudaEvent_t fork = nullptr, join = nullptr;
     int32_t* host_flags = nullptr;  // pinned ring for stop flags
     cudaEvent_t timer[2] = {nullptr, nullptr};

@@ -1150,7 +1150,7 @@ size_t csc_scratch_bytes(int64_t rows, int64_t cols, int64_t nnz) {
 }
 
 void build_transpose(const DevCsr& a, DevCsr& at, void* scratch, size_t scratch_bytes,
-                     cudaStream_t stream) {
+                     cudaStream_t stream, cudaEvent_t values_ready) {
     at.rows = a.cols;
     at.cols = a.rows;
     at.nnz = a.nnz;
@@ -1178,6 +1178,8 @@ void build_transpose(const DevCsr& a, DevCsr& at, void* scratch, size_t scratch_
     // exactly the counting sort's placement.
     DSVD_CUDA_CHECK(cub::DeviceRadixSort::SortPairs(temp, temp_bytes, a.idx, keys_out, perm_in,
                                                     perm_out, nnz, 0, key_bits(a.cols), stream));
+    // the values may still be on their way from the host (upload_pair)
+    if (values_ready != nullptr) DSVD_CUDA_CHECK(cudaStreamWaitEvent(stream, values_ready, 0));
     gather_transpose_kernel<<<grid_for(nnz), 256, 0, stream>>>(perm_out, row_of, a.val, at.idx,
                                                                at.val, nnz);
     DSVD_LAUNCH_CHECK();

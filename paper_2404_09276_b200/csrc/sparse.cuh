@@ -72,7 +72,7 @@ void prefix_row_bounds(const DevCsr& m, int64_t n, int64_t* d_beg, int64_t* d_en
 // Temporaries come from `scratch` (bytes given by csc_scratch_bytes).
 size_t csc_scratch_bytes(int64_t rows, int64_t cols, int64_t nnz);
 void build_transpose(const DevCsr& a, DevCsr& at, void* scratch, size_t scratch_bytes,
-                     cudaStream_t stream);
+                     cudaStream_t stream, cudaEvent_t values_ready = nullptr);
 // Row order by nonzero count (descending, ties by row index) into m.order,
 // and the number of rows with >= m.hub_threshold nonzeros into *m.d_hub_rows.
 size_t order_scratch_bytes(int64_t rows);
