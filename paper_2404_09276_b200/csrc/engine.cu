@@ -225,8 +225,12 @@ void build_pair(dsvd_ctx* ctx, CsrAlloc& al, int64_t rows, int64_t cols, int64_t
     // split mode: the "hub" prefix of the row order is the set of rows longer
     // than split_chunk, which are cut into chunks below
     const int64_t C = ctx->split_chunk;
-    a.hub_threshold = at.hub_threshold = C > 0 ? C + 1 : ctx->hub_threshold;
-    a.split_chunk = at.split_chunk = C;
+    // the transpose (pass 2) may split shorter rows than A (split_chunk_t)
+    const int64_t Ct = C > 0 && ctx->split_chunk_t > 0 ? ctx->split_chunk_t : C;
+    a.hub_threshold = C > 0 ? C + 1 : ctx->hub_threshold;
+    at.hub_threshold = Ct > 0 ? Ct + 1 : ctx->hub_threshold;
+    a.split_chunk = C;
+    at.split_chunk = Ct;
     a.d_hub_rows = hubs;
     at.d_hub_rows = hubs + 1;
     build_row_order(a, scratch, scratch_bytes, st);
@@ -808,6 +812,9 @@ int dsvd_ctx_set_option(dsvd_ctx* ctx, const char* name, int64_t value) {
         } else if (n == "dense_method") {
             if (value < 0 || value > 1) fail(DSVD_CONFIG, "dense_method: 0 = FP64 tensor cores, 1 = DFMA");
             ctx->dense_method = static_cast<int>(value);
+        } else if (n == "split_chunk_t") {
+            if (value < 0) fail(DSVD_CONFIG, "split_chunk_t must be >= 0");
+            ctx->split_chunk_t = value;
         } else if (n == "split_panel_rows") {
             if (value < 0) fail(DSVD_CONFIG, "split_panel_rows must be >= 0");
             ctx->split_panel_rows = value;

@@ -49,6 +49,7 @@ struct dsvd_ctx {
     // rows longer than split_chunk nonzeros are computed as chunk partials summed
     // in a fixed order (deterministic; 0 = whole chains, bit-exact vs reference)
     int64_t split_chunk = 512;
+    int64_t split_chunk_t = 0;        // transpose (pass 2) chunk length; 0: split_chunk
     // transpose chunks are also cut / ordered by X-row panels of this many rows (0: off)
     int64_t split_panel_rows = 32768;
     int dense_method = 0;           // 0: FP64 tensor-core Gram / rescale (dmma.cu), 1: DFMA kernels
