@@ -61,8 +61,9 @@ typedef struct dsvd_matrix dsvd_matrix; /* device-resident CSR(A) + CSR(A^T)    
  * flags: DSVD_FLAG_DIRECT runs the algorithm on `a` as given, like
  * shifted_rsvd / dash_svd (solver.cpp:190-212); without it the entry point
  * behaves like solve(), which factors the transpose of wide inputs and swaps
- * U and V (solver.cpp:217-220). */
-enum { DSVD_FLAG_DIRECT = 1 };
+ * U and V (solver.cpp:217-220). DSVD_FLAG_ORTH_QR selects the QR
+ * orthonormalizer of the basic algorithm (Orthonormalizer::qr, solver.hpp:20). */
+enum { DSVD_FLAG_DIRECT = 1, DSVD_FLAG_ORTH_QR = 2 };
 typedef struct {
     int64_t k;
     int64_t s;

@@ -162,7 +162,7 @@ inline dsvd_config to_c(const SolverConfig& c, bool direct) {
     r.tol = c.tol;
     r.p_max = c.p_max;
     r.alg = static_cast<int32_t>(c.alg);
-    r.flags = direct ? DSVD_FLAG_DIRECT : 0;
+    r.flags = (direct ? DSVD_FLAG_DIRECT : 0) | (c.orth == Orthonormalizer::qr ? DSVD_FLAG_ORTH_QR : 0);
     r.seed = c.seed;
     return r;
 }
@@ -250,6 +250,18 @@ inline SolveResult solve(const SparseMatrix& a, const SparseMatrix& /*at*/,
                          const SolverConfig& cfg, const IterationObserver& observer = {}) {
     // the device builds its own transpose (bitwise equal to transpose(a))
     return b200::run(a, cfg, observer, false);
+}
+// basic_rsvd (solver.cpp:178-188): Alg. 1 on `a` as given
+inline TruncatedSvd basic_rsvd(const SparseMatrix& a, const SolverConfig& cfg) {
+    SolverConfig c = cfg;
+    c.alg = Algorithm::basic;
+    return b200::run(a, c, {}, true).svd;
+}
+inline TruncatedSvd basic_rsvd(const SparseMatrix& a, const SparseMatrix& /*at*/, const SolverConfig& cfg,
+                               const IterationObserver& observer = {}) {
+    SolverConfig c = cfg;
+    c.alg = Algorithm::basic;
+    return b200::run(a, c, observer, true).svd;
 }
 inline SolveResult shifted_rsvd(const SparseMatrix& a, const SolverConfig& cfg) {
     SolverConfig c = cfg;

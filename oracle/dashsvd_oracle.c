@@ -429,7 +429,7 @@ static int64_t eff_s(const orc_config* c) { /* solver.hpp:36 */
 }
 
 int orc_validate_config(const orc_config* cfg, int64_t rows, int64_t cols) {
-    /* solver.cpp:15-32 (the orthonormalizer option is not modelled: eigsvd only) */
+    /* solver.cpp:15-32 */
     if (rows < 1 || cols < 1) return fail(ORC_SHAPE, -1, "solver needs a non-empty matrix");
     if (cfg->k < 1) return fail(ORC_CONFIG, -1, "k must be >= 1");
     const int64_t s = eff_s(cfg);
@@ -442,6 +442,8 @@ int orc_validate_config(const orc_config* cfg, int64_t rows, int64_t cols) {
     } else {
         if (cfg->p < 0) return fail(ORC_CONFIG, -1, "fixed-power algorithms need p >= 0");
     }
+    if (cfg->orth_qr && cfg->alg != ORC_BASIC)
+        return fail(ORC_CONFIG, -1, "the qr orthonormalizer applies to the basic algorithm only");
     return ORC_OK;
 }
 
@@ -555,13 +557,130 @@ static int shifted_direct(const orc_csr* a, const orc_csr* at, const orc_config*
     return rc;
 }
 
+/* qr_orth (decompositions.cpp:77-126): Householder QR of the column-major
+ * m x n block c, the explicit m x n Q by backward accumulation; RankDeficient
+ * when |R(k, k)| <= max(m, n) * eps * max |R(j, j)|. */
+int orc_qr_orth(int64_t m, int64_t n, const double* c, double* q) {
+    if (m < n) return fail(ORC_SHAPE, -1, "qr_orth: needs rows >= cols");
+    if (n == 0) return ORC_OK;
+    double* w = (double*)malloc(sizeof(double) * m * n);
+    double* tau = (double*)calloc((size_t)n, sizeof(double));
+    double* rdiag = (double*)calloc((size_t)n, sizeof(double));
+    memcpy(w, c, sizeof(double) * m * n);
+    for (int64_t k = 0; k < n; ++k) {
+        double* wk = w + k * m;
+        double norm2 = 0.0;
+        for (int64_t i = k; i < m; ++i) norm2 += wk[i] * wk[i];
+        const double alpha = wk[k];
+        const double beta = alpha >= 0.0 ? -sqrt(norm2) : sqrt(norm2);
+        rdiag[k] = beta;
+        if (beta == 0.0) continue;
+        tau[k] = (beta - alpha) / beta;
+        const double scale = 1.0 / (alpha - beta);
+        for (int64_t i = k + 1; i < m; ++i) wk[i] *= scale;
+        wk[k] = 1.0;
+        for (int64_t j = k + 1; j < n; ++j) {
+            double* wj = w + j * m;
+            double d = 0.0; /* dot(wk + k, wj + k, m - k) */
+            for (int64_t i = k; i < m; ++i) d += wk[i] * wj[i];
+            const double t = tau[k] * d;
+            for (int64_t i = k; i < m; ++i) wj[i] -= t * wk[i];
+        }
+    }
+    double max_diag = 0.0;
+    for (int64_t k = 0; k < n; ++k) max_diag = fmax(max_diag, fabs(rdiag[k]));
+    const double floor_ = (double)(m > n ? m : n) * DBL_EPSILON * max_diag;
+    for (int64_t k = 0; k < n; ++k)
+        if (fabs(rdiag[k]) <= floor_) {
+            free(w);
+            free(tau);
+            free(rdiag);
+            return fail(ORC_RANK, k, "qr_orth: diagonal of R at or below the rank floor");
+        }
+    memset(q, 0, sizeof(double) * m * n);
+    for (int64_t j = 0; j < n; ++j) q[j * m + j] = 1.0;
+    for (int64_t k = n - 1; k >= 0; --k) {
+        if (tau[k] == 0.0) continue;
+        const double* wk = w + k * m;
+        for (int64_t j = k; j < n; ++j) {
+            double* qj = q + j * m;
+            double d = 0.0;
+            for (int64_t i = k; i < m; ++i) d += wk[i] * qj[i];
+            const double t = tau[k] * d;
+            for (int64_t i = k; i < m; ++i) qj[i] -= t * wk[i];
+        }
+    }
+    free(w);
+    free(tau);
+    free(rdiag);
+    return ORC_OK;
+}
+
+/* basic_core + finalize_col_basis (solver.cpp:118-141, :166-176) on a as
+ * given: q = orth(A Omega), Omega = gaussian_matrix(a.cols, l, seed); p times
+ * q = orth(A (A^T q)); orth = eig_svd(.).u (its s is the trace's s_hat, alphas
+ * 0) or qr_orth (empty s_hat: left untouched). Finalize: f = eig_svd(A^T q),
+ * U = q f.v[:, :k], s = f.s[:k], V = f.u[:, :k]. */
+static int basic_direct(const orc_csr* a, const orc_csr* at, const orc_config* cfg, int qr, double* u,
+                        double* s_out, double* v, double* alphas, double* s_hat, int64_t cap,
+                        int64_t* iterations, int* stop_reason) {
+    const int64_t m = a->rows, n = a->cols;
+    const int64_t l = cfg->k + eff_s(cfg), k = cfg->k;
+    double* omega = (double*)malloc(sizeof(double) * n * l);
+    double* t = (double*)malloc(sizeof(double) * n * l);
+    double* y = (double*)malloc(sizeof(double) * m * l);
+    double* q = (double*)malloc(sizeof(double) * m * l);
+    double* fs = (double*)malloc(sizeof(double) * l);
+    double* fv = (double*)malloc(sizeof(double) * l * l);
+    double* fu = (double*)malloc(sizeof(double) * n * l);
+    int rc;
+    orc_gaussian_matrix(n, l, cfg->seed, omega);
+    orc_spmm(a, omega, l, y);
+    rc = qr ? orc_qr_orth(m, l, y, q) : orc_eig_svd(m, l, y, q, fs, fv);
+    *iterations = 0;
+    *stop_reason = ORC_STOP_FIXED_P;
+    for (int64_t j = 1; rc == ORC_OK && j <= cfg->p; ++j) {
+        orc_spmm(at, q, l, t);
+        orc_spmm(a, t, l, y);
+        rc = qr ? orc_qr_orth(m, l, y, q) : orc_eig_svd(m, l, y, q, fs, fv);
+        if (rc != ORC_OK) break;
+        if (j - 1 < cap) {
+            alphas[j - 1] = 0.0;
+            if (!qr) memcpy(s_hat + (j - 1) * l, fs, sizeof(double) * l);
+        }
+        *iterations = j;
+    }
+    if (rc == ORC_OK) {
+        orc_spmm(at, q, l, t);
+        rc = orc_eig_svd(n, l, t, fu, fs, fv);
+        if (rc == ORC_OK) {
+            orc_matmul(m, l, k, q, fv, u); /* head_cols(f.v, k) is the leading l x k block */
+            memcpy(s_out, fs, sizeof(double) * k);
+            memcpy(v, fu, sizeof(double) * n * k);
+        }
+    }
+    free(omega);
+    free(t);
+    free(y);
+    free(q);
+    free(fs);
+    free(fv);
+    free(fu);
+    return rc;
+}
+
 int orc_solve(const orc_csr* a, const orc_csr* at, const orc_config* cfg, double* u, double* s,
               double* v, double* alphas, double* s_hat, int64_t cap, int64_t* iterations,
               int* stop_reason) {
     /* solver.cpp:214-223: wide inputs run on the transpose and swap U/V */
     int rc = orc_validate_config(cfg, a->rows, a->cols);
     if (rc != ORC_OK) return rc;
-    if (cfg->alg == ORC_BASIC) return fail(ORC_CONFIG, -1, "oracle: basic algorithm not restated");
+    if (cfg->alg == ORC_BASIC) {
+        const int qr = cfg->orth_qr != 0;
+        if (a->rows < a->cols)
+            return basic_direct(at, a, cfg, qr, v, s, u, alphas, s_hat, cap, iterations, stop_reason);
+        return basic_direct(a, at, cfg, qr, u, s, v, alphas, s_hat, cap, iterations, stop_reason);
+    }
     if (a->rows < a->cols)
         return shifted_direct(at, a, cfg, v, s, u, alphas, s_hat, cap, iterations, stop_reason);
     return shifted_direct(a, at, cfg, u, s, v, alphas, s_hat, cap, iterations, stop_reason);

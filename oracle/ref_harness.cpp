@@ -14,6 +14,7 @@
 //   - dashsvd::finalize_row_basis                        solver.hpp:123
 // Dense matrices cross this boundary column-major (the reference's layout,
 // dense_matrix.hpp:10-13). Output: oracle/_ref/libdashsvd_ref.so.
+#include <algorithm>
 #include <chrono>
 #include <cstdint>
 #include <cstring>
@@ -86,9 +87,12 @@ void put(const DenseMatrix& d, double* out) {
     if (out) std::memcpy(out, d.data(), sizeof(double) * d.size());
 }
 
+int g_orth_qr = 0;  // ref_set_orth: Orthonormalizer for the next make_cfg calls
+
 SolverConfig make_cfg(int64_t k, int64_t s, int64_t p, double tol, int64_t p_max, int alg,
                       uint64_t seed) {
     SolverConfig c;
+    c.orth = g_orth_qr ? Orthonormalizer::qr : Orthonormalizer::eigsvd;
     c.k = k;
     c.s = s;
     c.p = p;
@@ -108,6 +112,7 @@ extern "C" {
 const char* ref_last_error() { return g_err.c_str(); }
 long long ref_last_error_index() { return g_err_index; }
 void ref_set_threads(int n) { set_thread_count(n); }
+void ref_set_orth(int qr) { g_orth_qr = qr; }
 int ref_thread_count() { return thread_count(); }
 
 uint64_t ref_splitmix64_at(uint64_t seed, uint64_t i) { return splitmix64_at(seed, i); }
@@ -239,7 +244,8 @@ int ref_solve(int64_t rows, int64_t cols, int64_t nnz, const int64_t* off, const
         const int64_t l = cfg.sketch_width();
         for (int64_t c = 0; c < static_cast<int64_t>(r.trace.alphas.size()) && c < cap; ++c) {
             alphas[c] = r.trace.alphas[c];
-            std::memcpy(s_hat + c * l, r.trace.s_hat_history[c].data(), sizeof(double) * l);
+            const auto& sh = r.trace.s_hat_history[c];  // empty for the qr orthonormalizer
+            if (!sh.empty()) std::memcpy(s_hat + c * l, sh.data(), sizeof(double) * std::min<int64_t>(l, sh.size()));
         }
         *iterations = r.trace.iterations;
         *stop_reason = static_cast<int>(r.trace.stop_reason);

@@ -136,8 +136,9 @@ class SolverConfig:
         return self.k + self.effective_s(self.k)
 
     def _c(self, direct: bool = False) -> dsvd_config:
+        flags = (1 if direct else 0) | (2 if self.orth == Orthonormalizer.qr else 0)  # DSVD_FLAG_*
         return dsvd_config(int(self.k), int(self.s), int(self.p), float(self.tol), int(self.p_max),
-                           int(self.alg), 1 if direct else 0, int(self.seed) & 0xFFFFFFFFFFFFFFFF)
+                           int(self.alg), flags, int(self.seed) & 0xFFFFFFFFFFFFFFFF)
 
 
 @dataclass
@@ -472,9 +473,14 @@ def _direct(a, cfg, observer, device):
     return solve(a, cfg, observer=observer, device=device, _direct=True)
 
 
-def basic_rsvd(a: SparseMatrix, cfg: SolverConfig, *args, **kwargs):
-    raise E.UnsupportedOnDevice("basic_rsvd (Alg. 1) is outside the B200 hot path; "
-                                "see DESIGN.md 'next rows'")
+def basic_rsvd(a: SparseMatrix, cfg: SolverConfig, at: Optional[SparseMatrix] = None,
+               observer: Optional[IterationObserver] = None,
+               device: Optional[Device] = None) -> TruncatedSvd:
+    """Plain randomized subspace iteration, Alg. 1 (solver.cpp:178-188): alg forced
+    to basic, run on `a` as given; returns the TruncatedSvd like the reference."""
+    c = SolverConfig(**{**cfg.__dict__})
+    c.alg = Algorithm.basic
+    return _direct(a, c, observer, device).svd
 
 
 def finalize_row_basis(a: SparseMatrix, q: np.ndarray, k: int,

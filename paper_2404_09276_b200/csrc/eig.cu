@@ -552,6 +552,10 @@ eig_svd_finish_kernel(const double* __restrict__ lam, const double* __restrict__
         if (loop.s_hat)
             for (int r = tid; r < l; r += blockDim.x) loop.s_hat[(j - 1) * l + r] = sv[r];
     }
+    if (loop.alg == DSVD_ALG_BASIC) {  // basic_core: trace only, no shift (solver.cpp:130-136)
+        if (tid == 0) ctrl->iteration = j;
+        return;
+    }
     bool stop = false;
     if (loop.alg == DSVD_ALG_DASH) {
         // pve_stop_check(s_stored, alpha_stored, s, alpha, k, tol): operand order as written

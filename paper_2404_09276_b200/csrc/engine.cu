@@ -294,6 +294,9 @@ void validate(const dsvd_config& cfg, int64_t rows, int64_t cols) {
         if (cfg.p < 0) fail(DSVD_CONFIG, "fixed-power algorithms need p >= 0");
     }
     if (cfg.alg < DSVD_ALG_BASIC || cfg.alg > DSVD_ALG_DASH) fail(DSVD_CONFIG, "unknown algorithm");
+    if ((cfg.flags & DSVD_FLAG_ORTH_QR) != 0 && cfg.alg != DSVD_ALG_BASIC)
+        fail(DSVD_CONFIG, "the qr orthonormalizer applies to the basic algorithm only; shifted iterations need "
+                          "the surrogate spectrum");
 }
 
 void raise_device_status(const Control& c) {
@@ -644,6 +647,126 @@ int guarded(F&& f) {
     }
 }
 
+// basic_core + finalize_col_basis (solver.cpp:118-141, :166-176) on the pair
+// (A, AT) as given: Omega = gaussian_matrix(n, l, seed), q = orth(A Omega),
+// then p times q = orth(A (A^T q)); orth = eigSVD(.).u (the default
+// Orthonormalizer::eigsvd; its spectrum is the trace's s_hat, alphas are 0).
+// Finalize: f = eigSVD(A^T q), U = q f.v[:, :k], V = f.u[:, :k], s = f.s[:k].
+void solve_basic(dsvd_ctx* ctx, const DevCsr& A, const DevCsr& AT, const dsvd_config& cfg, SolveIO& io,
+                 dsvd_observer_fn observer, void* user) {
+    cudaStream_t st = ctx->stream;
+    const int64_t m = A.rows, n = A.cols;
+    const int64_t k = cfg.k;
+    const int64_t l = k + effective_s(cfg);
+    const int64_t ld = padded_ld(l);
+    const int64_t p = cfg.p;
+    if (l > 512) fail(DSVD_UNSUPPORTED, "sketch width l > 512 is not supported");
+    if ((cfg.flags & DSVD_FLAG_ORTH_QR) != 0) fail(DSVD_UNSUPPORTED, "orth_qr is handled by solve_basic_qr");
+
+    double* Y = ctx->tbuf<double>("Y", m * ld);  // A Omega, A (A^T q)
+    double* T = ctx->tbuf<double>("T", n * ld);  // Omega, A^T q
+    double* Qb[2] = {ctx->tbuf<double>("QB0", m * ld), ctx->tbuf<double>("QB1", m * ld)};
+    double* W = ctx->tbuf<double>("W", l * l);
+    double* sv = ctx->tbuf<double>("s", l);
+    double* inv_s = ctx->tbuf<double>("inv_s", l);
+    double* s_stored = ctx->tbuf<double>("s_stored", l);
+    Control* ctrl = ctx->tbuf<Control>("ctrl", 1);
+    const int64_t cap = p > 0 ? p : 1;
+    double* d_alphas = ctx->tbuf<double>("trace.alphas", cap);
+    double* d_shat = ctx->tbuf<double>("trace.s_hat", cap * l);
+    EigSvdOut eo{W, sv, inv_s};
+    control_init(ctrl, s_stored, static_cast<int>(l), st);
+    count_launch();
+
+    int sp = ctx->span_begin(K_OTHER);
+    gaussian_rowmajor(T, n, l, ld, cfg.seed, st);  // gaussian_matrix(a.cols, l, seed)
+    count_launch();
+    ctx->span_end(sp);
+    sp = ctx->span_begin(K_SPMM1);
+    spmm(SpmmArgs{&A, T, Y, ld, l, nullptr, nullptr, nullptr}, st, ctx->spmm_variant, ctx->side, ctx->fork,
+         ctx->join, partial_for(ctx, A, ld));
+    count_launch();
+    ctx->span_end(sp);
+    eig_svd_factors(ctx, Y, m, l, ld, eo, ctrl, nullptr, nullptr);
+    sp = ctx->span_begin(K_RESCALE);
+    solve_rescale(ctx, Y, m, l, ld, W, l, inv_s, l, Qb[0], ld, 0, nullptr);
+    ctx->span_end(sp);
+
+    LoopStep ls;
+    ls.k = k;
+    ls.tol = cfg.tol;
+    ls.alg = DSVD_ALG_BASIC;
+    ls.alphas = d_alphas;
+    ls.s_hat = d_shat;
+    ls.cap = cap;
+    ls.s_stored = s_stored;
+    int cur = 0;
+    for (int64_t j = 1; j <= p; ++j) {
+        sp = ctx->span_begin(K_SPMM2);
+        spmm(SpmmArgs{&AT, Qb[cur], T, ld, l, nullptr, nullptr, nullptr}, st, ctx->spmm_variant, ctx->side,
+             ctx->fork, ctx->join, partial_for(ctx, AT, ld));
+        count_launch();
+        ctx->span_end(sp);
+        sp = ctx->span_begin(K_SPMM1);
+        spmm(SpmmArgs{&A, T, Y, ld, l, nullptr, nullptr, nullptr}, st, ctx->spmm_variant, ctx->side, ctx->fork,
+             ctx->join, partial_for(ctx, A, ld));
+        count_launch();
+        ctx->span_end(sp);
+        eig_svd_factors(ctx, Y, m, l, ld, eo, ctrl, &ls, nullptr);
+        sp = ctx->span_begin(K_RESCALE);
+        solve_rescale(ctx, Y, m, l, ld, W, l, inv_s, l, Qb[1 - cur], ld, 0, nullptr);
+        ctx->span_end(sp);
+        if (observer) {
+            Control hc = read_control(ctx, ctrl);
+            raise_device_status(hc);
+            std::vector<double> qb = to_host_colmajor(ctx, Qb[cur], m, l, ld);
+            std::vector<double> qa = to_host_colmajor(ctx, Qb[1 - cur], m, l, ld);
+            std::vector<double> sh(static_cast<size_t>(l));
+            DSVD_CUDA_CHECK(cudaMemcpy(sh.data(), d_shat + (j - 1) * l, sizeof(double) * l, cudaMemcpyDeviceToHost));
+            observer(j, 0.0, sh.data(), l, qb.data(), qa.data(), m, user);
+        }
+        cur = 1 - cur;
+    }
+    Control hc = read_control(ctx, ctrl);
+    raise_device_status(hc);
+    io.iterations = p;
+    io.stop_reason = DSVD_STOP_FIXED_P;
+    ctx->stats.eig_sweeps = hc.total_sweeps;
+    const double* Qf = Qb[cur];
+
+    // finalize_col_basis: f = eigSVD(A^T q); U = q f.v[:, :k]; V = f.u[:, :k]
+    control_init(ctrl, s_stored, static_cast<int>(l), st);
+    count_launch();
+    sp = ctx->span_begin(K_SPMM2);
+    spmm(SpmmArgs{&AT, Qf, T, ld, l, nullptr, nullptr, nullptr}, st, ctx->spmm_variant, ctx->side, ctx->fork,
+         ctx->join, partial_for(ctx, AT, ld));
+    count_launch();
+    ctx->span_end(sp);
+    eig_svd_factors(ctx, T, n, l, ld, eo, ctrl, nullptr, nullptr);
+    hc = read_control(ctx, ctrl);
+    raise_device_status(hc);
+    ctx->stats.eig_sweeps += hc.total_sweeps;
+    double* du = io.on_device ? io.u : ctx->tbuf<double>("out.u", m * k);
+    double* dv = io.on_device ? io.v : ctx->tbuf<double>("out.v", n * k);
+    sp = ctx->span_begin(K_RESCALE);
+    solve_rescale(ctx, Qf, m, l, ld, W, l, nullptr, k, du, 0, 1, nullptr);  // matmul(q, head_cols(f.v, k))
+    solve_rescale(ctx, T, n, l, ld, W, l, inv_s, k, dv, 0, 1, nullptr);      // head_cols(f.u, k)
+    ctx->span_end(sp);
+    if (io.on_device) {
+        DSVD_CUDA_CHECK(cudaMemcpyAsync(io.s, sv, sizeof(double) * k, cudaMemcpyDeviceToDevice, st));
+    } else {
+        DSVD_CUDA_CHECK(cudaMemcpyAsync(io.u, du, sizeof(double) * m * k, cudaMemcpyDeviceToHost, st));
+        DSVD_CUDA_CHECK(cudaMemcpyAsync(io.v, dv, sizeof(double) * n * k, cudaMemcpyDeviceToHost, st));
+        DSVD_CUDA_CHECK(cudaMemcpyAsync(io.s, sv, sizeof(double) * k, cudaMemcpyDeviceToHost, st));
+    }
+    const int64_t nrec = std::min(io.iterations, io.cap);
+    if (nrec > 0 && io.alphas)
+        DSVD_CUDA_CHECK(cudaMemcpyAsync(io.alphas, d_alphas, sizeof(double) * nrec, cudaMemcpyDeviceToHost, st));
+    if (nrec > 0 && io.s_hat)
+        DSVD_CUDA_CHECK(cudaMemcpyAsync(io.s_hat, d_shat, sizeof(double) * nrec * l, cudaMemcpyDeviceToHost, st));
+    DSVD_CUDA_CHECK(cudaStreamSynchronize(st));
+}
+
 // Starts Omega for the solve of an m x n host matrix on the side stream, so it
 // overlaps the CSR upload that follows on the main stream (single-GPU solves).
 void pregenerate_omega(dsvd_ctx* ctx, int64_t rows, int64_t cols, const dsvd_config& cfg) {
@@ -691,8 +814,6 @@ void solve_pair(dsvd_ctx* ctx, const DevCsr& a, const DevCsr& at, const dsvd_con
         return;
     }
     validate(cfg, a.rows, a.cols);
-    if (cfg.alg == DSVD_ALG_BASIC)
-        fail(DSVD_UNSUPPORTED, "the basic algorithm is not on the B200 path (shifted family only)");
     const int64_t l = cfg.k + effective_s(cfg);
     const bool direct = (cfg.flags & DSVD_FLAG_DIRECT) != 0;
     SolveIO io;
@@ -705,12 +826,14 @@ void solve_pair(dsvd_ctx* ctx, const DevCsr& a, const DevCsr& at, const dsvd_con
         io.u = out->v;
         io.v = out->u;
         io.s = out->s;
-        solve_tall(ctx, at, a, cfg, io, observer, user);
+        if (cfg.alg == DSVD_ALG_BASIC) solve_basic(ctx, at, a, cfg, io, observer, user);
+        else solve_tall(ctx, at, a, cfg, io, observer, user);
     } else {
         io.u = out->u;
         io.v = out->v;
         io.s = out->s;
-        solve_tall(ctx, a, at, cfg, io, observer, user);
+        if (cfg.alg == DSVD_ALG_BASIC) solve_basic(ctx, a, at, cfg, io, observer, user);
+        else solve_tall(ctx, a, at, cfg, io, observer, user);
     }
     (void)l;
     out->iterations = io.iterations;

@@ -52,7 +52,7 @@ class _orc_csr(C.Structure):
 
 class _orc_config(C.Structure):
     _fields_ = [("k", _I64), ("s", _I64), ("p", _I64), ("tol", _D), ("p_max", _I64),
-                ("alg", C.c_int), ("seed", _U64)]
+                ("alg", C.c_int), ("seed", _U64), ("orth_qr", C.c_int)]
 
 
 ALG = {"basic": 0, "shifted": 1, "fixed_shift": 2, "dash": 3}
@@ -208,7 +208,7 @@ class Oracle(_Lib):
                                                            _ptr(a), _ptr(b), _ptr(c))
 
     def validate_config(self, rows, cols, k, s=-1, p=-1, tol=1e-2, p_max=1000, alg="dash"):
-        cfg = _orc_config(k, s, p, tol, p_max, ALG[alg], 0)
+        cfg = _orc_config(k, s, p, tol, p_max, ALG[alg], 0, 0)
         self.check(self.f("validate_config", C.c_int, _P, _I64, _I64)(C.byref(cfg), rows, cols))
 
     def pve_stop_check(self, prev, alpha_prev, cur, alpha, k, tol):
@@ -232,7 +232,13 @@ class Oracle(_Lib):
             C.byref(cs), _ptr(q), l, k, _ptr(u), _ptr(s), _ptr(v)))
         return u, s, v
 
-    def solve(self, a: Csr, k, s=-1, p=-1, tol=1e-2, p_max=1000, alg="dash", seed=0, at=None):
+    def qr_orth(self, c):
+        c = np.asfortranarray(c, dtype=np.float64)
+        q = np.empty_like(c, order="F")
+        self.check(self.f("qr_orth", C.c_int, _I64, _I64, _P, _P)(c.shape[0], c.shape[1], _ptr(c), _ptr(q)))
+        return q
+
+    def solve(self, a: Csr, k, s=-1, p=-1, tol=1e-2, p_max=1000, alg="dash", seed=0, at=None, orth="eigsvd"):
         at = at if at is not None else self.transpose(a)
         sw = k + (s if s >= 0 else max(1, k // 2))
         cap = (p_max if alg == "dash" else max(p, 0)) + 1
@@ -243,7 +249,7 @@ class Oracle(_Lib):
         s_hat = np.zeros((cap, sw))
         it = _I64()
         sr = C.c_int()
-        cfg = _orc_config(k, s, p, tol, p_max, ALG[alg], seed)
+        cfg = _orc_config(k, s, p, tol, p_max, ALG[alg], seed, 1 if orth == "qr" else 0)
         ca, cat = self._csr(a), self._csr(at)
         fn = self.f("solve", C.c_int, _P, _P, _P, _P, _P, _P, _P, _P, _I64, C.POINTER(_I64),
                     C.POINTER(C.c_int))
@@ -336,7 +342,8 @@ class Reference(_Lib):
         return u, s, v
 
     def solve(self, a: Csr, k, s=-1, p=-1, tol=1e-2, p_max=1000, alg="dash", seed=0,
-              times=False):
+              times=False, orth="eigsvd"):
+        self.f("set_orth", None, C.c_int)(1 if orth == "qr" else 0)
         sw = k + (s if s >= 0 else max(1, k // 2))
         cap = (p_max if alg == "dash" else max(p, 0)) + 1
         u = np.empty((a.rows, k), order="F")

@@ -589,3 +589,31 @@ def test_rank_one_raises_rank_deficient(dev):
     a = d.SparseMatrix(3, 2, off, cols, dense[rows, cols])
     with pytest.raises(d.RankDeficient):
         d.solve(a, d.SolverConfig(k=1, s=1, p=1, alg=d.Algorithm.shifted), device=dev)
+
+
+# ---- basic algorithm (Alg. 1) -------------------------------------
+
+@pytest.mark.parametrize("shape", [(3000, 1800), (1500, 2600)])
+@pytest.mark.parametrize("p", [0, 1, 4])
+def test_solve_basic_eigsvd(dev, oracle, shape, p):
+    a = oracle.sparse_random(shape[0], shape[1], 12, 5, True)
+    ref = oracle.solve(a, 20, 10, p=p, alg="basic", seed=4)
+    res = d.solve(to_dev(a), d.SolverConfig(k=20, s=10, p=p, alg=d.Algorithm.basic, seed=4), device=dev)
+    check_solve(res, ref, 20)
+    assert np.all(np.asarray(res.trace.alphas) == 0.0) and len(res.trace.alphas) == p
+    assert res.trace.stop_reason.name == "fixed_p"
+
+
+def test_basic_rsvd_direct_and_observer(dev, oracle, c1):
+    # basic_rsvd runs on `a` as given (solver.cpp:178-184); observer sees q (m x l)
+    ref = oracle.solve(c1, 30, 10, p=3, alg="basic", seed=1)
+    seen = []
+    cfg = d.SolverConfig(k=30, s=10, p=3, seed=1)
+    f = d.basic_rsvd(to_dev(c1), cfg, observer=lambda st: seen.append(st), device=dev)
+    np.testing.assert_allclose(f.s, ref["s"], rtol=1e-8)
+    assert sin_theta(ref["u"], f.u) <= 1e-6 and sin_theta(ref["v"], f.v) <= 1e-6
+    assert [st.iteration for st in seen] == [1, 2, 3]
+    for j, st in enumerate(seen):
+        assert st.alpha == 0.0 and st.q_after.shape == (c1.rows, 40)
+        np.testing.assert_allclose(st.q_after.T @ st.q_after, np.eye(40), atol=1e-9)
+        np.testing.assert_allclose(st.s_hat, ref["s_hat"][j], rtol=1e-8)

@@ -244,3 +244,32 @@ def test_oracle_equals_reference_random(oracle, reference, seed):
         for key in ("u", "s", "v", "alphas", "s_hat"):
             assert same_bits(r1[key], r2[key]), (alg, key)
         assert r1["iterations"] == r2["iterations"]
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3])
+@pytest.mark.parametrize("orth", ["eigsvd", "qr"])
+def test_oracle_equals_reference_basic(oracle, reference, seed, orth):
+    """The basic algorithm (Alg. 1, solver.cpp:118-141, finalize_col_basis
+    :166-176) and qr_orth (decompositions.cpp:77-126), restated in the oracle,
+    against the unmodified reference, bit for bit; tall and wide inputs."""
+    for rows, cols in ((130 + 11 * seed, 70), (60, 140 + 9 * seed)):
+        a = reference.sparse_random(rows, cols, 8, seed, True)
+        r1 = reference.solve(a, 9, 5, p=3, alg="basic", seed=seed, orth=orth)
+        r2 = oracle.solve(a, 9, 5, p=3, alg="basic", seed=seed, orth=orth)
+        reference.solve(a, 9, 5, p=1, alg="basic", seed=seed)  # reset the harness orth
+        keys = ("u", "s", "v", "alphas") + (("s_hat",) if orth == "eigsvd" else ())
+        for key in keys:
+            assert same_bits(r1[key], r2[key]), (orth, key)
+        assert r1["iterations"] == r2["iterations"] == 3
+        assert r1["stop_reason"] == r2["stop_reason"] == "fixed_p"
+
+
+def test_oracle_qr_orth_rank_deficient(oracle):
+    c = np.asfortranarray(np.random.default_rng(0).standard_normal((50, 6)))
+    c[:, 4] = c[:, 1] + c[:, 2]
+    from paper_2404_09276_b200 import errors as E
+    with pytest.raises(E.RankDeficient) as ei:
+        oracle.qr_orth(c)
+    assert ei.value.index == 4
+    q = oracle.qr_orth(np.asfortranarray(c[:, :4]))
+    np.testing.assert_allclose(q.T @ q, np.eye(4), atol=1e-14)
