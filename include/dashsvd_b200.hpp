@@ -217,9 +217,11 @@ inline SolveResult run(const SparseMatrix& a, const SolverConfig& cfg,
     }
     r.trace.iterations = out.iterations;
     r.trace.stop_reason = static_cast<StopReason>(out.stop_reason);
+    const bool no_spectrum = cfg.alg == Algorithm::basic && cfg.orth == Orthonormalizer::qr;
     for (index_t j = 0; j < out.iterations && j < cap; ++j) {
         r.trace.alphas.push_back(alphas[j]);
-        r.trace.s_hat_history.emplace_back(s_hat.begin() + j * l, s_hat.begin() + (j + 1) * l);
+        if (no_spectrum) r.trace.s_hat_history.emplace_back();  // qr: no surrogate spectrum
+        else r.trace.s_hat_history.emplace_back(s_hat.begin() + j * l, s_hat.begin() + (j + 1) * l);
     }
     return r;
 }

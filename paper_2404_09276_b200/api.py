@@ -356,11 +356,13 @@ def _make_outputs(rows, cols, cfg, out=None):
     return out, (u, s, v, alphas, s_hat)
 
 
-def _result(out, bufs, device: Device) -> SolveResult:
+def _result(out, bufs, device: Device, cfg: Optional[SolverConfig] = None) -> SolveResult:
     u, s, v, alphas, s_hat = bufs
     n = int(out.iterations)
-    trace = ShiftTrace([float(a) for a in alphas[:n]], [s_hat[c].copy() for c in range(n)], n,
-                       StopReason(int(out.stop_reason)))
+    # the qr orthonormalizer produces no surrogate spectrum: empty entries (solver.cpp:121-126)
+    no_spec = cfg is not None and cfg.alg == Algorithm.basic and cfg.orth == Orthonormalizer.qr
+    hist = [np.empty(0) if no_spec else s_hat[c].copy() for c in range(n)]
+    trace = ShiftTrace([float(a) for a in alphas[:n]], hist, n, StopReason(int(out.stop_reason)))
     return SolveResult(TruncatedSvd(u, s, v), trace, device.stats())
 
 
@@ -393,7 +395,7 @@ def _solve_handle(m: DeviceMatrix, cfg: SolverConfig, observer, out_rows=None,
     check(lib().dsvd_solve(m.device.handle, m.handle, C.byref(c), C.byref(out), cb, None))
     if errs:
         raise errs[0]
-    return _result(out, bufs, m.device)
+    return _result(out, bufs, m.device, cfg)
 
 
 # ---- reference-shaped entry points ---------------------------------------------
@@ -437,7 +439,7 @@ def solve(a: SparseMatrix, cfg: SolverConfig, at: Optional[SparseMatrix] = None,
         c = cfg._c(_direct)
         check(lib().dsvd_solve_csr(dev.handle, a.rows, a.cols, a.nnz, _ptr(a.offsets),
                                    _ptr(a.col_indices), _ptr(a.values), C.byref(c), C.byref(out)))
-        return _result(out, bufs, dev)
+        return _result(out, bufs, dev, cfg)
     validate_config(cfg, a.rows, a.cols)
     m = DeviceMatrix(a, dev)
     try:

@@ -56,6 +56,7 @@ struct Control {
     int32_t stop_pending;  // set by the stop rule; becomes `stopped` at the next iteration
     int32_t status;        // DSVD_OK or an error raised on the device
     int32_t eig_sweeps;    // sweeps of the last eigensolve
+    int32_t status_src;    // 1: the status was raised by the QR orthonormalizer
 };
 
 }  // namespace dsvd

@@ -620,6 +620,7 @@ __global__ void control_init_kernel(Control* ctrl, double* s_stored, int l) {
         ctrl->stopped = 0;
         ctrl->stop_pending = 0;
         ctrl->status = DSVD_OK;
+        ctrl->status_src = 0;
         ctrl->eig_sweeps = 0;
     }
 }
@@ -695,6 +696,17 @@ void eig_svd_finish(const EigWorkspace& w, int64_t rows, double* W, int64_t ldw,
 void sym_eig_finish(const EigWorkspace& w, double* values, double* vectors_colmajor,
                     cudaStream_t stream) {
     sym_finish_kernel<<<1, 256, 0, stream>>>(w.lam, w.vecs, w.l, w.lp, values, vectors_colmajor);
+    DSVD_LAUNCH_CHECK();
+}
+
+__global__ void trace_basic_kernel(Control* ctrl, double* alphas, int64_t cap) {
+    const int64_t j = ctrl->iteration + 1;
+    if (alphas != nullptr && j - 1 < cap) alphas[j - 1] = 0.0;
+    ctrl->iteration = j;
+}
+
+void trace_basic_iteration(Control* ctrl, double* alphas, int64_t cap, cudaStream_t stream) {
+    trace_basic_kernel<<<1, 1, 0, stream>>>(ctrl, alphas, cap);
     DSVD_LAUNCH_CHECK();
 }
 

@@ -59,6 +59,10 @@ void eig_svd_finish(const EigWorkspace& w, int64_t rows, double* W, int64_t ldw,
 void sym_eig_finish(const EigWorkspace& w, double* values, double* vectors_colmajor,
                     cudaStream_t stream);
 
+// Basic-algorithm iteration without a spectrum (qr orthonormalizer): alphas[j-1]
+// = 0 and ctrl->iteration = j.
+void trace_basic_iteration(Control* ctrl, double* alphas, int64_t cap, cudaStream_t stream);
+
 // ctrl->stopped = ctrl->stop_pending (first kernel of each loop iteration).
 void loop_begin(Control* ctrl, cudaStream_t stream);
 void control_init(Control* ctrl, double* s_stored, int l, cudaStream_t stream);

@@ -30,6 +30,7 @@
 #include "common.cuh"
 #include "dense.cuh"
 #include "engine.cuh"
+#include "qr.cuh"
 #include "eig.cuh"
 #include "rng.cuh"
 #include "sparse.cuh"
@@ -301,6 +302,8 @@ void validate(const dsvd_config& cfg, int64_t rows, int64_t cols) {
 
 void raise_device_status(const Control& c) {
     if (c.status == DSVD_OK) return;
+    if (c.status == DSVD_RANK_DEFICIENT && c.status_src == 1)
+        fail(DSVD_RANK_DEFICIENT, "qr_orth: diagonal of R at or below the rank floor", c.status_index);
     if (c.status == DSVD_RANK_DEFICIENT)
         fail(DSVD_RANK_DEFICIENT, "eig_svd: singular value at or below the rank floor", c.status_index);
     if (c.status == DSVD_NUMERICAL)
@@ -661,7 +664,8 @@ void solve_basic(dsvd_ctx* ctx, const DevCsr& A, const DevCsr& AT, const dsvd_co
     const int64_t ld = padded_ld(l);
     const int64_t p = cfg.p;
     if (l > 512) fail(DSVD_UNSUPPORTED, "sketch width l > 512 is not supported");
-    if ((cfg.flags & DSVD_FLAG_ORTH_QR) != 0) fail(DSVD_UNSUPPORTED, "orth_qr is handled by solve_basic_qr");
+    const bool qr = (cfg.flags & DSVD_FLAG_ORTH_QR) != 0;
+    if (qr && l > 160) fail(DSVD_UNSUPPORTED, "the device QR orthonormalizer supports l <= 160");
 
     double* Y = ctx->tbuf<double>("Y", m * ld);  // A Omega, A (A^T q)
     double* T = ctx->tbuf<double>("T", n * ld);  // Omega, A^T q
@@ -677,6 +681,7 @@ void solve_basic(dsvd_ctx* ctx, const DevCsr& A, const DevCsr& AT, const dsvd_co
     EigSvdOut eo{W, sv, inv_s};
     control_init(ctrl, s_stored, static_cast<int>(l), st);
     count_launch();
+    if (qr) DSVD_CUDA_CHECK(cudaMemsetAsync(d_shat, 0, sizeof(double) * cap * l, st));  // no spectrum
 
     int sp = ctx->span_begin(K_OTHER);
     gaussian_rowmajor(T, n, l, ld, cfg.seed, st);  // gaussian_matrix(a.cols, l, seed)
@@ -687,10 +692,51 @@ void solve_basic(dsvd_ctx* ctx, const DevCsr& A, const DevCsr& AT, const dsvd_co
          ctx->join, partial_for(ctx, A, ld));
     count_launch();
     ctx->span_end(sp);
-    eig_svd_factors(ctx, Y, m, l, ld, eo, ctrl, nullptr, nullptr);
-    sp = ctx->span_begin(K_RESCALE);
-    solve_rescale(ctx, Y, m, l, ld, W, l, inv_s, l, Qb[0], ld, 0, nullptr);
-    ctx->span_end(sp);
+    // orth(y): eigSVD(y).u, or qr_orth(y) = CholeskyQR2 + Householder signs (qr.cu)
+    auto orth = [&](const double* y, double* qout, const LoopStep* loop) {
+        if (!qr) {
+            eig_svd_factors(ctx, y, m, l, ld, eo, ctrl, loop, nullptr);
+            const int s2 = ctx->span_begin(K_RESCALE);
+            solve_rescale(ctx, y, m, l, ld, W, l, inv_s, l, qout, ld, 0, nullptr);
+            ctx->span_end(s2);
+            return;
+        }
+        double* G = ctx->tbuf<double>("qr.G", l * l);
+        double* W1 = ctx->tbuf<double>("qr.W1", l * l);
+        double* W2 = ctx->tbuf<double>("qr.W2", l * l);
+        double* r1 = ctx->tbuf<double>("qr.r1", l);
+        double* r2 = ctx->tbuf<double>("qr.r2", l);
+        double* Q1 = ctx->tbuf<double>("qr.Q1", m * ld);
+        double* Ptop = ctx->tbuf<double>("qr.Ptop", l * ld);
+        auto gram_of = [&](const double* c) {
+            const int s2 = ctx->span_begin(K_GRAM);
+            if (gram_dmma_supported(l, ld)) {
+                gram_dmma(c, m, l, ld, G, ctx->buf("gram.dws." + std::to_string(m), gram_dmma_workspace_bytes(m, l)),
+                          nullptr, st);
+            } else {
+                const size_t gws = gram_workspace_bytes(m, l);
+                gram(c, m, l, ld, G, ctx->buf("gram.ws." + std::to_string(m), gws), gws, nullptr, st);
+            }
+            count_launch(2);
+            ctx->span_end(s2);
+        };
+        gram_of(y);
+        chol_inv(G, static_cast<int>(l), W1, r1, ctrl, nullptr, st);
+        count_launch();
+        solve_rescale(ctx, y, m, l, ld, W1, l, nullptr, l, Q1, ld, 0, nullptr);  // Q1 = Y R1^{-1}
+        gram_of(Q1);
+        chol_inv(G, static_cast<int>(l), W2, r2, ctrl, nullptr, st);
+        count_launch();
+        solve_rescale(ctx, Q1, l, l, ld, W2, l, nullptr, l, Ptop, ld, 0, nullptr);  // top l rows of Q_pos
+        qr_signs(Ptop, ld, static_cast<int>(l), W2, W1, r1, r2, m, ctrl, nullptr, st);  // W1 <- W2 diag(s)
+        count_launch();
+        solve_rescale(ctx, Q1, m, l, ld, W1, l, nullptr, l, qout, ld, 0, nullptr);  // Q = Q1 R2^{-1} diag(s)
+        if (loop != nullptr) {  // the qr orthonormalizer has no spectrum: the trace records alpha = 0 only
+            trace_basic_iteration(ctrl, loop->alphas, loop->cap, st);
+            count_launch();
+        }
+    };
+    orth(Y, Qb[0], nullptr);
 
     LoopStep ls;
     ls.k = k;
@@ -712,10 +758,7 @@ void solve_basic(dsvd_ctx* ctx, const DevCsr& A, const DevCsr& AT, const dsvd_co
              ctx->join, partial_for(ctx, A, ld));
         count_launch();
         ctx->span_end(sp);
-        eig_svd_factors(ctx, Y, m, l, ld, eo, ctrl, &ls, nullptr);
-        sp = ctx->span_begin(K_RESCALE);
-        solve_rescale(ctx, Y, m, l, ld, W, l, inv_s, l, Qb[1 - cur], ld, 0, nullptr);
-        ctx->span_end(sp);
+        orth(Y, Qb[1 - cur], &ls);
         if (observer) {
             Control hc = read_control(ctx, ctrl);
             raise_device_status(hc);

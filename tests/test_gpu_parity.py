@@ -617,3 +617,45 @@ def test_basic_rsvd_direct_and_observer(dev, oracle, c1):
         assert st.alpha == 0.0 and st.q_after.shape == (c1.rows, 40)
         np.testing.assert_allclose(st.q_after.T @ st.q_after, np.eye(40), atol=1e-9)
         np.testing.assert_allclose(st.s_hat, ref["s_hat"][j], rtol=1e-8)
+
+
+@pytest.mark.parametrize("shape", [(3000, 1800), (1500, 2600)])
+@pytest.mark.parametrize("p", [0, 2])
+def test_solve_basic_qr(dev, oracle, shape, p):
+    """Basic algorithm with the QR orthonormalizer: CholeskyQR2 + Householder
+    sign reconstruction on the device vs the reference's Householder qr_orth."""
+    a = oracle.sparse_random(shape[0], shape[1], 12, 6, True)
+    ref = oracle.solve(a, 20, 10, p=p, alg="basic", seed=2, orth="qr")
+    cfg = d.SolverConfig(k=20, s=10, p=p, alg=d.Algorithm.basic, seed=2, orth=d.Orthonormalizer.qr)
+    res = d.solve(to_dev(a), cfg, device=dev)
+    np.testing.assert_allclose(res.svd.s, ref["s"], rtol=1e-8)
+    assert sin_theta(ref["u"], res.svd.u) <= 1e-6 and sin_theta(ref["v"], res.svd.v) <= 1e-6
+    assert res.trace.iterations == p and all(len(h) == 0 for h in res.trace.s_hat_history)
+    np.testing.assert_allclose(res.trace.alphas, np.zeros(p))
+
+
+def test_basic_qr_observer_q_matches_householder(dev, oracle):
+    """The iterate q of the device QR orthonormalizer equals the reference's
+    Householder Q column for column (signs included)."""
+    a = oracle.sparse_random(900, 500, 10, 3, True)
+    at = oracle.transpose(a)
+    seen = []
+    cfg = d.SolverConfig(k=12, s=6, p=2, alg=d.Algorithm.basic, seed=5, orth=d.Orthonormalizer.qr)
+    d.basic_rsvd(to_dev(a), cfg, observer=lambda st: seen.append(st), device=dev)
+    assert len(seen) == 2
+    for st in seen:
+        # the reference's qr_orth of the same block (A A^T q_before)
+        y = oracle.spmm(a, oracle.spmm(at, np.asfortranarray(st.q_before)))
+        q_ref = oracle.qr_orth(y)
+        np.testing.assert_allclose(st.q_after, q_ref, atol=1e-10)
+
+
+def test_basic_qr_rank_deficient(dev):
+    # identical columns -> dependent sketch columns -> RankDeficient like qr_orth
+    off = np.arange(0, 2 * 401, 2, dtype=np.int64)
+    idx = np.tile(np.array([0, 1], dtype=np.int64), 400)
+    val = np.ones(800)
+    a = d.SparseMatrix(400, 60, off, idx, val)
+    cfg = d.SolverConfig(k=4, s=2, p=1, alg=d.Algorithm.basic, seed=1, orth=d.Orthonormalizer.qr)
+    with pytest.raises(d.errors.RankDeficient):
+        d.solve(a, cfg, device=dev)
