@@ -47,7 +47,8 @@ enum {
     DSVD_OOM = 6,           /* device allocation failed (reference: Error)  */
     DSVD_NCCL = 7,          /* collective failure (reference: Error)        */
     DSVD_UNSUPPORTED = 8,   /* configuration outside the B200 path          */
-    DSVD_OTHER = 9
+    DSVD_OTHER = 9,
+    DSVD_DEGENERATE = 10    /* DegenerateReference (metrics)                */
 };
 
 /* Algorithm and StopReason keep the reference enum order (solver.hpp:13-18, :45). */
@@ -187,7 +188,9 @@ DSVD_API int dsvd_matrix_download_transpose(const dsvd_matrix* m, int64_t* t_off
  * dsvd_solve_csr         <- solve(a, cfg)                 solver.hpp:104 / solver.cpp:225-227
  *                           (host CSR in, host U/S/V out; transpose built on device)
  * alg == DSVD_ALG_SHIFTED / FIXED_SHIFT / DASH run the shifted family
- * (shifted_rsvd :95 / dash_svd :99). alg == BASIC returns DSVD_UNSUPPORTED. */
+ * (shifted_rsvd :95 / dash_svd :99); alg == BASIC runs basic_core +
+ * finalize_col_basis (solver.cpp:118-141, :166-176), with the QR
+ * orthonormalizer when cfg->flags has DSVD_FLAG_ORTH_QR (l <= 160). */
 DSVD_API int dsvd_solve(dsvd_ctx* ctx, const dsvd_matrix* a, const dsvd_config* cfg, dsvd_outputs* out,
                dsvd_observer_fn observer, void* user);
 DSVD_API int dsvd_solve_csr(dsvd_ctx* ctx, int64_t rows, int64_t cols, int64_t nnz,
@@ -208,6 +211,26 @@ DSVD_API int dsvd_ctx_timer_stop(dsvd_ctx* ctx, double* elapsed_ms);
  * column-major) -> host u[rows*k], s[k], v[cols*k]. */
 DSVD_API int dsvd_finalize_row_basis(dsvd_ctx* ctx, const dsvd_matrix* a, const double* q, int64_t l,
                             int64_t k, double* u, double* s, double* v);
+
+/* ---- validation metrics (metrics.hpp / metrics.cpp:99-206) ----------------
+ * Host factors (column-major u[rows*k], s[k], v[cols*k]) against the device
+ * matrix; reference singular values sigmas[n_ref] descending. Reductions are
+ * deterministic trees (values agree with the reference to rounding).
+ * dsvd_eps_pve              <- eps_pve(a, u_hat, ref)           metrics.cpp:99-117
+ * dsvd_eps_res              <- eps_res(a, approx, ref)          metrics.cpp:119-134
+ * dsvd_eps_spec             <- eps_spec(a, approx, ref, it, seed) metrics.cpp:136-159
+ * dsvd_max_triplet_residual <- max_triplet_residual(a, approx)  metrics.cpp:194-206
+ * A reference that is too short or has a zero where one is divided by returns
+ * DSVD_DEGENERATE (DegenerateReference). */
+DSVD_API int dsvd_eps_pve(dsvd_ctx* ctx, const dsvd_matrix* a, const double* u, int64_t k, const double* sigmas,
+                          int64_t n_ref, double* out);
+DSVD_API int dsvd_eps_res(dsvd_ctx* ctx, const dsvd_matrix* a, const double* u, const double* s, const double* v,
+                          int64_t k, const double* sigmas, int64_t n_ref, double* out);
+DSVD_API int dsvd_eps_spec(dsvd_ctx* ctx, const dsvd_matrix* a, const double* u, const double* s, const double* v,
+                           int64_t k, const double* sigmas, int64_t n_ref, int64_t power_iters, uint64_t seed,
+                           double* out);
+DSVD_API int dsvd_max_triplet_residual(dsvd_ctx* ctx, const dsvd_matrix* a, const double* u, const double* s,
+                                       const double* v, int64_t k, double* out);
 
 /* validate_config (solver.cpp:15-32), update_shift (:34-36), pve_stop_check
  * (:38-50): pure host functions with the reference's semantics; the device

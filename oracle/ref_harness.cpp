@@ -26,6 +26,7 @@
 #include "dashsvd/dense_kernels.hpp"
 #include "dashsvd/errors.hpp"
 #include "dashsvd/random.hpp"
+#include "dashsvd/metrics.hpp"
 #include "dashsvd/solver.hpp"
 #include "dashsvd/sparse_matrix.hpp"
 #include "dashsvd/sym_eig.hpp"
@@ -255,6 +256,28 @@ int ref_solve(int64_t rows, int64_t cols, int64_t nnz, const int64_t* off, const
             for (int64_t c = 0; c < static_cast<int64_t>(stamps.size()) && c < cap; ++c)
                 times[2 + c] = stamps[c];
         }
+    });
+}
+
+// metrics.cpp:99-206 on host factors (column-major): out = {eps_pve, eps_res,
+// eps_spec, max_triplet_residual}
+int ref_metrics(int64_t rows, int64_t cols, int64_t nnz, const int64_t* off, const int64_t* idx, const double* val,
+                const double* u, const double* s, const double* v, int64_t k, const double* sigmas, int64_t n_ref,
+                int64_t power_iters, uint64_t seed, double* out) {
+    return guarded([&] {
+        SparseMatrix a = make_csr(rows, cols, nnz, off, idx, val);
+        TruncatedSvd t;
+        t.u = DenseMatrix(rows, k);
+        t.v = DenseMatrix(cols, k);
+        std::memcpy(t.u.data(), u, sizeof(double) * rows * k);
+        std::memcpy(t.v.data(), v, sizeof(double) * cols * k);
+        t.s.assign(s, s + k);
+        ReferenceSpectrum ref;
+        ref.sigmas.assign(sigmas, sigmas + n_ref);
+        out[0] = eps_pve(a, t.u, ref);
+        out[1] = eps_res(a, t, ref);
+        out[2] = eps_spec(a, t, ref, power_iters, seed);
+        out[3] = max_triplet_residual(a, t);
     });
 }
 

@@ -8,11 +8,12 @@ The public surface mirrors the reference library's dashsvd:: namespace; see
 from . import errors
 from .api import (Algorithm, Device, DeviceMatrix, EigenPair, IterationState, Orthonormalizer,
                   ShiftTrace, SolveResult, SolverConfig, SparseMatrix, StopReason, TruncatedSvd,
-                  basic_rsvd, comm_unique_id, dash_svd, default_device, eig_svd,
-                  finalize_row_basis, gaussian_matrix, gram, matmul, pin, powerlaw, pve_stop_check,
+                  basic_rsvd, comm_unique_id, dash_svd, default_device, eig_svd, eps_pve, eps_res,
+                  eps_spec, finalize_row_basis, gaussian_matrix, gram, matmul, max_triplet_residual,
+                  pin, powerlaw, pve_stop_check,
                   shifted_rsvd, solve, sparse_random, splitmix64_at, spmm, spmm_shift, sym_eig,
                   transpose, unpin, update_shift, validate_config)
-from .errors import (ConfigError, DeviceError, Error, NumericalError, RankDeficient, ShapeError,
-                     UnsupportedOnDevice)
+from .errors import (ConfigError, DegenerateReference, DeviceError, Error, NumericalError, RankDeficient,
+                     ShapeError, UnsupportedOnDevice)
 
 __all__ = [n for n in dir() if not n.startswith("_")]

@@ -23,6 +23,7 @@ U64 = C.c_uint64
 
 DSVD_OK, DSVD_SHAPE, DSVD_CONFIG, DSVD_RANK, DSVD_NUMERICAL = 0, 1, 2, 3, 4
 DSVD_CUDA, DSVD_OOM, DSVD_NCCL, DSVD_UNSUPPORTED, DSVD_OTHER = 5, 6, 7, 8, 9
+DSVD_DEGENERATE = 10
 
 
 class NativeLibraryMissing(E.Error):
@@ -89,6 +90,10 @@ SIGNATURES = [
     ("dsvd_ctx_timer_start", C.c_int, [P]),
     ("dsvd_ctx_timer_stop", C.c_int, [P, C.POINTER(D)]),
     ("dsvd_finalize_row_basis", C.c_int, [P, P, P, I64, I64, P, P, P]),
+    ("dsvd_eps_pve", C.c_int, [P, P, P, I64, P, I64, C.POINTER(D)]),
+    ("dsvd_eps_res", C.c_int, [P, P, P, P, P, I64, P, I64, C.POINTER(D)]),
+    ("dsvd_eps_spec", C.c_int, [P, P, P, P, P, I64, P, I64, I64, U64, C.POINTER(D)]),
+    ("dsvd_max_triplet_residual", C.c_int, [P, P, P, P, P, I64, C.POINTER(D)]),
     ("dsvd_validate_config", C.c_int, [C.POINTER(dsvd_config), I64, I64]),
     ("dsvd_update_shift", D, [D, D]),
     ("dsvd_pve_stop_check", C.c_int, [P, I64, D, P, I64, D, I64, D, C.POINTER(C.c_int)]),
@@ -147,4 +152,6 @@ def check(rc: int) -> None:
         raise E.NumericalError(msg)
     if rc == DSVD_UNSUPPORTED:
         raise E.UnsupportedOnDevice(msg)
+    if rc == DSVD_DEGENERATE:
+        raise E.DegenerateReference(msg)
     raise E.DeviceError(f"[status {rc}] {msg}")

@@ -651,3 +651,60 @@ def solve_device_csr(rows: int, cols: int, nnz: int, d_offsets: int, d_col_indic
     trace = ShiftTrace([float(a) for a in alphas[:n]], [s_hat[i].copy() for i in range(n)], n,
                        StopReason(int(out.stop_reason)))
     return SolveResult(None, trace, dev.stats())
+
+
+# ---- validation metrics (metrics.hpp) ----------------------------
+
+def _metric_matrix(a, device):
+    """A DeviceMatrix for `a` (uploaded when a SparseMatrix is given) and whether we own it."""
+    if isinstance(a, DeviceMatrix):
+        return a, False
+    return DeviceMatrix(a, _dev(device)), True
+
+
+def _metric_call(a, device, fn, *args):
+    m, own = _metric_matrix(a, device)
+    try:
+        out = C.c_double()
+        check(fn(m.device.handle, m.handle, *args, C.byref(out)))
+        return float(out.value)
+    finally:
+        if own:
+            m.close()
+
+
+def _sig(ref):
+    return np.ascontiguousarray(getattr(ref, "sigmas", ref), dtype=np.float64)
+
+
+def eps_pve(a, u_hat: np.ndarray, ref, device: Optional[Device] = None) -> float:
+    """metrics.cpp:99-117 on the device: max_i |sigma_i^2 - ||A^T u_i||^2| / sigma_{k+1}^2."""
+    u = np.asfortranarray(u_hat, dtype=np.float64)
+    sg = _sig(ref)
+    return _metric_call(a, device, lib().dsvd_eps_pve, _ptr(u), u.shape[1], _ptr(sg), sg.size)
+
+
+def eps_res(a, approx: TruncatedSvd, ref, device: Optional[Device] = None) -> float:
+    """metrics.cpp:119-134: max_i ||A^T u_i - s_i v_i|| / sigma_i."""
+    u, v = np.asfortranarray(approx.u, dtype=np.float64), np.asfortranarray(approx.v, dtype=np.float64)
+    s = np.ascontiguousarray(approx.s, dtype=np.float64)
+    sg = _sig(ref)
+    return _metric_call(a, device, lib().dsvd_eps_res, _ptr(u), _ptr(s), _ptr(v), s.size, _ptr(sg), sg.size)
+
+
+def eps_spec(a, approx: TruncatedSvd, ref, power_iters: int = 300, seed: int = 0x5EED,
+             device: Optional[Device] = None) -> float:
+    """metrics.cpp:136-159: (||A - U S V^T||_2 estimate - sigma_{k+1}) / sigma_{k+1}, the norm by
+    power iteration on the matrix-free residual operator."""
+    u, v = np.asfortranarray(approx.u, dtype=np.float64), np.asfortranarray(approx.v, dtype=np.float64)
+    s = np.ascontiguousarray(approx.s, dtype=np.float64)
+    sg = _sig(ref)
+    return _metric_call(a, device, lib().dsvd_eps_spec, _ptr(u), _ptr(s), _ptr(v), s.size, _ptr(sg), sg.size,
+                        int(power_iters), int(seed) & 0xFFFFFFFFFFFFFFFF)
+
+
+def max_triplet_residual(a, approx: TruncatedSvd, device: Optional[Device] = None) -> float:
+    """metrics.cpp:194-206: max_i ||A v_i - s_i u_i||."""
+    u, v = np.asfortranarray(approx.u, dtype=np.float64), np.asfortranarray(approx.v, dtype=np.float64)
+    s = np.ascontiguousarray(approx.s, dtype=np.float64)
+    return _metric_call(a, device, lib().dsvd_max_triplet_residual, _ptr(u), _ptr(s), _ptr(v), s.size)

@@ -111,6 +111,7 @@ struct dsvd_ctx {
 
 struct dsvd_matrix {
     dsvd_ctx* ctx = nullptr;
+    int device = 0;  // destroy() must not touch ctx: it may already be gone
     dsvd::DevCsr a, at;
     std::vector<void*> owned;
     // row shard of a larger matrix (multi-GPU): global row offset and count

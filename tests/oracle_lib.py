@@ -272,6 +272,17 @@ class Reference(_Lib):
     def thread_count(self):
         return int(self.f("thread_count", C.c_int)())
 
+    def metrics(self, a: Csr, u, s, v, sigmas, power_iters=300, seed=0x5EED):
+        """[eps_pve, eps_res, eps_spec, max_triplet_residual] (metrics.cpp:99-206)."""
+        u, v = np.asfortranarray(u, dtype=np.float64), np.asfortranarray(v, dtype=np.float64)
+        s = np.ascontiguousarray(s, dtype=np.float64)
+        sg = np.ascontiguousarray(sigmas, dtype=np.float64)
+        out = np.zeros(4)
+        fn = self.f("metrics", C.c_int, _I64, _I64, _I64, _P, _P, _P, _P, _P, _P, _I64, _P, _I64, _I64, _U64, _P)
+        self.check(fn(*self._a(a), _ptr(u), _ptr(s), _ptr(v), s.size, _ptr(sg), sg.size, power_iters, seed,
+                      _ptr(out)))
+        return out
+
     def sparse_random(self, rows, cols, npr, seed, decay=False) -> Csr:
         nnz = _I64()
         self.check(self.f("sparse_random", C.c_int, _I64, _I64, _I64, _U64, C.c_int,

@@ -659,3 +659,38 @@ def test_basic_qr_rank_deficient(dev):
     cfg = d.SolverConfig(k=4, s=2, p=1, alg=d.Algorithm.basic, seed=1, orth=d.Orthonormalizer.qr)
     with pytest.raises(d.errors.RankDeficient):
         d.solve(a, cfg, device=dev)
+
+
+# ---- validation metrics on the device ---------------------------
+
+def _dense(a):
+    m = np.zeros((a.rows, a.cols))
+    for i in range(a.rows):
+        for p in range(a.offsets[i], a.offsets[i + 1]):
+            m[i, a.col_indices[p]] += a.values[p]
+    return m
+
+
+@pytest.mark.parametrize("p", [0, 2])
+def test_metrics_match_reference(dev, oracle, reference, p):
+    a = oracle.sparse_random(1200, 700, 9, 8, True)
+    sig = np.linalg.svd(_dense(a), compute_uv=False)
+    res = d.solve(to_dev(a), d.SolverConfig(k=20, s=10, p=p, alg=d.Algorithm.shifted, seed=3), device=dev)
+    f = res.svd
+    ref = reference.metrics(a, f.u, f.s, f.v, sig, power_iters=120, seed=11)
+    got = np.array([d.eps_pve(to_dev(a), f.u, sig, device=dev), d.eps_res(to_dev(a), f, sig, device=dev),
+                    d.eps_spec(to_dev(a), f, sig, power_iters=120, seed=11, device=dev),
+                    d.max_triplet_residual(to_dev(a), f, device=dev)])
+    # reductions differ from the reference's sequential sums only by rounding
+    np.testing.assert_allclose(got[[0, 1, 3]], ref[[0, 1, 3]], rtol=1e-7, atol=1e-12)
+    np.testing.assert_allclose(got[2], ref[2], rtol=1e-6, atol=1e-9)
+
+
+def test_metrics_degenerate_reference(dev, oracle):
+    a = oracle.sparse_random(300, 200, 6, 2, True)
+    f = d.solve(to_dev(a), d.SolverConfig(k=5, s=5, p=1, alg=d.Algorithm.shifted), device=dev).svd
+    with pytest.raises(d.DegenerateReference):
+        d.eps_pve(to_dev(a), f.u, f.s, device=dev)  # needs k + 1 values
+    with pytest.raises(d.DegenerateReference):
+        d.eps_spec(to_dev(a), f, np.r_[f.s, 0.0], device=dev)  # sigma_{k+1} == 0
+    assert d.max_triplet_residual(to_dev(a), f, device=dev) < 1e-3 * f.s[0]
