@@ -48,7 +48,9 @@ enum {
     DSVD_NCCL = 7,          /* collective failure (reference: Error)        */
     DSVD_UNSUPPORTED = 8,   /* configuration outside the B200 path          */
     DSVD_OTHER = 9,
-    DSVD_DEGENERATE = 10    /* DegenerateReference (metrics)                */
+    DSVD_DEGENERATE = 10,   /* DegenerateReference (metrics)                */
+    DSVD_FORMAT = 11,       /* UnsupportedFormat (cache / Matrix Market)    */
+    DSVD_PARSE = 12         /* ParseError; dsvd_last_error_index() = line   */
 };
 
 /* Algorithm and StopReason keep the reference enum order (solver.hpp:13-18, :45). */
@@ -179,6 +181,8 @@ DSVD_API int dsvd_matrix_shape(const dsvd_matrix* m, int64_t* rows, int64_t* col
 DSVD_API int dsvd_matrix_bench_spmm(dsvd_matrix* m, int transpose, int64_t l, int variant,
                                     int iters, double* ms_out);
 DSVD_API int dsvd_matrix_hub_rows(const dsvd_matrix* m, int64_t* hub_a, int64_t* hub_at);
+/* Download CSR(A) as stored on the device (int64 offsets/indices, host buffers). */
+DSVD_API int dsvd_matrix_download(const dsvd_matrix* m, int64_t* offsets, int64_t* col_indices, double* values);
 /* Download the device-built transpose (int64 offsets/indices, host buffers). */
 DSVD_API int dsvd_matrix_download_transpose(const dsvd_matrix* m, int64_t* t_offsets,
                                    int64_t* t_col_indices, double* t_values);
@@ -211,6 +215,46 @@ DSVD_API int dsvd_ctx_timer_stop(dsvd_ctx* ctx, double* elapsed_ms);
  * column-major) -> host u[rows*k], s[k], v[cols*k]. */
 DSVD_API int dsvd_finalize_row_basis(dsvd_ctx* ctx, const dsvd_matrix* a, const double* q, int64_t l,
                             int64_t k, double* u, double* s, double* v);
+
+/* ---- inputs -------------------------------------------
+ * dsvd_csr_validate     <- SparseMatrix::validate()        sparse_matrix.cpp:12-33
+ *   (on the device; same first violation and error type: ShapeError for
+ *   offsets / index range / ordering, NumericalError for non-finite or
+ *   explicit-zero values, message naming the row)
+ * dsvd_save_cache       <- save_cache(path, a)             matrix_market.cpp:~241-255 (DSH1)
+ * dsvd_matrix_load_cache<- load_cache(path) + validate()   matrix_market.cpp:257-275,
+ *   read into pinned memory and uploaded; the device matrix handle is built
+ *   directly (dims[3] receives rows, cols, nnz). DSVD_FORMAT: bad magic or
+ *   truncated file.
+ * dsvd_coo_assemble     <- assemble(rows, cols, triplets)  matrix_market.cpp:90-115
+ *   (sort by (row, col), duplicates summed in input order, exact zeros
+ *   dropped; *nnz receives the canonical count); dsvd_coo_fetch copies the
+ *   resulting CSR to host arrays, dsvd_matrix_from_coo builds the device
+ *   matrix handle from it without a host round trip.
+ * dsvd_mtx_assemble     <- load_matrix_market(path)        matrix_market.cpp:117-165
+ *   (text parsed on the host with the reference's errors: DSVD_PARSE with the
+ *   1-based line in dsvd_last_error_index(), DSVD_FORMAT for unsupported
+ *   headers, DSVD_OTHER when the file cannot be opened; the triplets are then
+ *   assembled on the device as dsvd_coo_assemble; dims[3] = rows, cols, nnz)
+ * dsvd_mtx_read / dsvd_mtx_fetch: the host parsing half alone (dims[3] = rows,
+ *   cols, number of triplets after the symmetric expansion; fetch hands the
+ *   0-based triplets out in file order and releases them)
+ * dsvd_write_matrix_market <- write_matrix_market(path, a) matrix_market.cpp:167-177 */
+DSVD_API int dsvd_csr_validate(dsvd_ctx* ctx, int64_t rows, int64_t cols, int64_t nnz, const int64_t* offsets,
+                               const int64_t* col_indices, const double* values);
+DSVD_API int dsvd_save_cache(const char* path, int64_t rows, int64_t cols, int64_t nnz, const int64_t* offsets,
+                             const int64_t* col_indices, const double* values);
+DSVD_API int dsvd_matrix_load_cache(dsvd_ctx* ctx, const char* path, int validate, dsvd_matrix** out,
+                                    int64_t* dims);
+DSVD_API int dsvd_coo_assemble(dsvd_ctx* ctx, int64_t rows, int64_t cols, int64_t n, const int64_t* r,
+                               const int64_t* c, const double* v, int64_t* nnz);
+DSVD_API int dsvd_coo_fetch(dsvd_ctx* ctx, int64_t* offsets, int64_t* col_indices, double* values);
+DSVD_API int dsvd_matrix_from_coo(dsvd_ctx* ctx, dsvd_matrix** out);
+DSVD_API int dsvd_mtx_assemble(dsvd_ctx* ctx, const char* path, int64_t* dims);
+DSVD_API int dsvd_mtx_read(const char* path, int64_t* dims);
+DSVD_API int dsvd_mtx_fetch(int64_t* r, int64_t* c, double* v);
+DSVD_API int dsvd_write_matrix_market(const char* path, int64_t rows, int64_t cols, const int64_t* offsets,
+                                      const int64_t* col_indices, const double* values);
 
 /* ---- validation metrics (metrics.hpp / metrics.cpp:99-206) ----------------
  * Host factors (column-major u[rows*k], s[k], v[cols*k]) against the device

@@ -12,6 +12,9 @@
 //   - dashsvd::gaussian_matrix / normal_at / splitmix64  random.hpp:11-20
 //   - dashsvd::sparse_random                             synthetic.hpp:37-38
 //   - dashsvd::finalize_row_basis                        solver.hpp:123
+//   - SparseMatrix::validate                             sparse_matrix.hpp:22
+//   - load_matrix_market / write_matrix_market / save_cache / load_cache
+//                                                        matrix_market.hpp:14-34
 // Dense matrices cross this boundary column-major (the reference's layout,
 // dense_matrix.hpp:10-13). Output: oracle/_ref/libdashsvd_ref.so.
 #include <algorithm>
@@ -25,6 +28,7 @@
 #include "dashsvd/decompositions.hpp"
 #include "dashsvd/dense_kernels.hpp"
 #include "dashsvd/errors.hpp"
+#include "dashsvd/matrix_market.hpp"
 #include "dashsvd/random.hpp"
 #include "dashsvd/metrics.hpp"
 #include "dashsvd/solver.hpp"
@@ -41,7 +45,7 @@ thread_local std::string g_err;
 thread_local long long g_err_index = -1;
 
 // Status codes shared with include/dashsvd_b200.h (DSVD_*).
-enum { OK = 0, E_SHAPE = 1, E_CONFIG = 2, E_RANK = 3, E_NUMERICAL = 4, E_OTHER = 9 };
+enum { OK = 0, E_SHAPE = 1, E_CONFIG = 2, E_RANK = 3, E_NUMERICAL = 4, E_OTHER = 9, E_FORMAT = 11, E_PARSE = 12 };
 
 template <class F>
 int guarded(F&& f) {
@@ -61,6 +65,13 @@ int guarded(F&& f) {
     } catch (const NumericalError& e) {
         g_err = e.what();
         return E_NUMERICAL;
+    } catch (const ParseError& e) {
+        g_err = e.what();
+        g_err_index = e.line;
+        return E_PARSE;
+    } catch (const UnsupportedFormat& e) {
+        g_err = e.what();
+        return E_FORMAT;
     } catch (const std::exception& e) {
         g_err = e.what();
         return E_OTHER;
@@ -105,6 +116,13 @@ SolverConfig make_cfg(int64_t k, int64_t s, int64_t p, double tol, int64_t p_max
 }
 
 SparseMatrix g_rand;  // last sparse_random result, handed out by ref_sparse_random_fetch
+SparseMatrix g_csr;   // last loaded matrix (ref_load_matrix_market / ref_load_cache)
+
+void put_dims(const SparseMatrix& a, int64_t* dims) {
+    dims[0] = a.rows;
+    dims[1] = a.cols;
+    dims[2] = a.nnz();
+}
 
 }  // namespace
 
@@ -279,6 +297,42 @@ int ref_metrics(int64_t rows, int64_t cols, int64_t nnz, const int64_t* off, con
         out[2] = eps_spec(a, t, ref, power_iters, seed);
         out[3] = max_triplet_residual(a, t);
     });
+}
+
+// SparseMatrix::validate (sparse_matrix.cpp:12-33)
+int ref_validate(int64_t rows, int64_t cols, int64_t nnz, const int64_t* off, const int64_t* idx, const double* val) {
+    return guarded([&] { make_csr(rows, cols, nnz, off, idx, val).validate(); });
+}
+
+// matrix_market.cpp:117-275; the loaded matrix is handed out by ref_csr_fetch
+int ref_load_matrix_market(const char* path, int64_t* dims) {
+    return guarded([&] {
+        g_csr = load_matrix_market(path);
+        put_dims(g_csr, dims);
+    });
+}
+
+int ref_load_cache(const char* path, int64_t* dims) {
+    return guarded([&] {
+        g_csr = load_cache(path);
+        put_dims(g_csr, dims);
+    });
+}
+
+void ref_csr_fetch(int64_t* off, int64_t* idx, double* val) {
+    std::copy(g_csr.offsets.begin(), g_csr.offsets.end(), off);
+    std::copy(g_csr.col_indices.begin(), g_csr.col_indices.end(), idx);
+    std::copy(g_csr.values.begin(), g_csr.values.end(), val);
+}
+
+int ref_save_cache(const char* path, int64_t rows, int64_t cols, int64_t nnz, const int64_t* off, const int64_t* idx,
+                   const double* val) {
+    return guarded([&] { save_cache(path, make_csr(rows, cols, nnz, off, idx, val)); });
+}
+
+int ref_write_matrix_market(const char* path, int64_t rows, int64_t cols, int64_t nnz, const int64_t* off,
+                            const int64_t* idx, const double* val) {
+    return guarded([&] { write_matrix_market(path, make_csr(rows, cols, nnz, off, idx, val)); });
 }
 
 }  // extern "C"

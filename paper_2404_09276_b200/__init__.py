@@ -6,7 +6,7 @@ The public surface mirrors the reference library's dashsvd:: namespace; see
 ``api`` for the mapping.
 """
 from . import errors
-from .api import (Algorithm, Device, DeviceMatrix, EigenPair, IterationState, Orthonormalizer,
+from .api import (Algorithm, assemble, load_cache, load_matrix_market, read_matrix_market_triplets, save_cache, write_matrix_market, Device, DeviceMatrix, EigenPair, IterationState, Orthonormalizer,
                   ShiftTrace, SolveResult, SolverConfig, SparseMatrix, StopReason, TruncatedSvd,
                   basic_rsvd, comm_unique_id, dash_svd, default_device, eig_svd, eps_pve, eps_res,
                   eps_spec, finalize_row_basis, gaussian_matrix, gram, matmul, max_triplet_residual,
@@ -14,6 +14,6 @@ from .api import (Algorithm, Device, DeviceMatrix, EigenPair, IterationState, Or
                   shifted_rsvd, solve, sparse_random, splitmix64_at, spmm, spmm_shift, sym_eig,
                   transpose, unpin, update_shift, validate_config)
 from .errors import (ConfigError, DegenerateReference, DeviceError, Error, NumericalError, RankDeficient,
-                     ShapeError, UnsupportedOnDevice)
+                     ParseError, ShapeError, UnsupportedFormat, UnsupportedOnDevice)
 
 __all__ = [n for n in dir() if not n.startswith("_")]

@@ -23,7 +23,7 @@ U64 = C.c_uint64
 
 DSVD_OK, DSVD_SHAPE, DSVD_CONFIG, DSVD_RANK, DSVD_NUMERICAL = 0, 1, 2, 3, 4
 DSVD_CUDA, DSVD_OOM, DSVD_NCCL, DSVD_UNSUPPORTED, DSVD_OTHER = 5, 6, 7, 8, 9
-DSVD_DEGENERATE = 10
+DSVD_DEGENERATE, DSVD_FORMAT, DSVD_PARSE = 10, 11, 12
 
 
 class NativeLibraryMissing(E.Error):
@@ -80,6 +80,7 @@ SIGNATURES = [
     ("dsvd_matrix_set_shard", C.c_int, [P, I64, I64]),
     ("dsvd_matrix_shape", C.c_int, [P, C.POINTER(I64), C.POINTER(I64), C.POINTER(I64)]),
     ("dsvd_matrix_download_transpose", C.c_int, [P, P, P, P]),
+    ("dsvd_matrix_download", C.c_int, [P, P, P, P]),
     ("dsvd_matrix_bench_spmm", C.c_int, [P, C.c_int, I64, C.c_int, C.c_int, C.POINTER(D)]),
     ("dsvd_matrix_hub_rows", C.c_int, [P, C.POINTER(I64), C.POINTER(I64)]),
     ("dsvd_solve", C.c_int, [P, P, C.POINTER(dsvd_config), C.POINTER(dsvd_outputs), OBSERVER, P]),
@@ -93,6 +94,16 @@ SIGNATURES = [
     ("dsvd_eps_pve", C.c_int, [P, P, P, I64, P, I64, C.POINTER(D)]),
     ("dsvd_eps_res", C.c_int, [P, P, P, P, P, I64, P, I64, C.POINTER(D)]),
     ("dsvd_eps_spec", C.c_int, [P, P, P, P, P, I64, P, I64, I64, U64, C.POINTER(D)]),
+    ("dsvd_csr_validate", C.c_int, [P, I64, I64, I64, P, P, P]),
+    ("dsvd_save_cache", C.c_int, [C.c_char_p, I64, I64, I64, P, P, P]),
+    ("dsvd_matrix_load_cache", C.c_int, [P, C.c_char_p, C.c_int, C.POINTER(P), C.POINTER(I64)]),
+    ("dsvd_coo_assemble", C.c_int, [P, I64, I64, I64, P, P, P, C.POINTER(I64)]),
+    ("dsvd_coo_fetch", C.c_int, [P, P, P, P]),
+    ("dsvd_matrix_from_coo", C.c_int, [P, C.POINTER(P)]),
+    ("dsvd_mtx_assemble", C.c_int, [P, C.c_char_p, C.POINTER(I64)]),
+    ("dsvd_mtx_read", C.c_int, [C.c_char_p, C.POINTER(I64)]),
+    ("dsvd_mtx_fetch", C.c_int, [P, P, P]),
+    ("dsvd_write_matrix_market", C.c_int, [C.c_char_p, I64, I64, P, P, P]),
     ("dsvd_max_triplet_residual", C.c_int, [P, P, P, P, P, I64, C.POINTER(D)]),
     ("dsvd_validate_config", C.c_int, [C.POINTER(dsvd_config), I64, I64]),
     ("dsvd_update_shift", D, [D, D]),
@@ -154,4 +165,10 @@ def check(rc: int) -> None:
         raise E.UnsupportedOnDevice(msg)
     if rc == DSVD_DEGENERATE:
         raise E.DegenerateReference(msg)
+    if rc == DSVD_FORMAT:
+        raise E.UnsupportedFormat(msg)
+    if rc == DSVD_PARSE:
+        raise E.ParseError(int(L.dsvd_last_error_index()), msg)
+    if rc == DSVD_OTHER:
+        raise E.Error(msg)
     raise E.DeviceError(f"[status {rc}] {msg}")

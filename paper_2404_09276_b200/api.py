@@ -35,6 +35,7 @@ from __future__ import annotations
 
 import ctypes as C
 import enum
+import os
 import threading
 from dataclasses import dataclass, field
 from typing import Callable, List, Optional
@@ -45,6 +46,11 @@ from . import errors as E
 from ._native import (OBSERVER, dsvd_config, dsvd_outputs, dsvd_stats, check, lib)
 
 _P = C.c_void_p
+I64 = C.c_int64
+
+
+def _path(path) -> bytes:
+    return os.fsencode(path)
 
 
 def _ptr(a: Optional[np.ndarray]):
@@ -88,7 +94,8 @@ class SparseMatrix:
         return int(self.values.shape[0])
 
     def validate(self) -> None:
-        """Canonical-form check (sparse_matrix.cpp:12-33), ShapeError/NumericalError."""
+        """Canonical-form check on the host (sparse_matrix.cpp:12-33): ShapeError /
+        NumericalError for the first violation in row order, as the reference's loop."""
         if self.rows < 0 or self.cols < 0:
             raise E.ShapeError("sparse matrix with negative dimension")
         if self.offsets.shape[0] != self.rows + 1:
@@ -97,22 +104,41 @@ class SparseMatrix:
             raise E.ShapeError("offsets must span [0, nnz]")
         if self.col_indices.shape[0] != self.values.shape[0]:
             raise E.ShapeError("index/value length mismatch")
-        if np.any(np.diff(self.offsets) < 0):
+        off = self.offsets
+        dec = np.flatnonzero(off[:-1] > off[1:])
+        first_dec = int(dec[0]) if dec.size else self.rows
+        # rows before the first decrease are contiguous from 0 (the loop reaches them first)
+        end = int(min(max(off[first_dec], 0), self.nnz))
+        ci, v = self.col_indices[:end], self.values[:end]
+        row = np.repeat(np.arange(first_dec), np.diff(off[:first_dec + 1]))[:end]
+        code = np.full(end, 5, dtype=np.int8)
+        notinc = np.zeros(end, dtype=bool)
+        if end > 1:
+            notinc[1:] = (row[1:] == row[:-1]) & (ci[:-1] >= ci[1:])
+        for c, bad in ((4, v == 0.0), (3, ~np.isfinite(v)), (2, notinc), (1, (ci < 0) | (ci >= self.cols))):
+            code[bad] = c
+        hit = np.flatnonzero(code < 5)
+        if hit.size:
+            p = int(hit[0])
+            i, c = int(row[p]), int(code[p])
+            if c == 1:
+                raise E.ShapeError(f"column index out of range in row {i}")
+            if c == 2:
+                raise E.ShapeError(f"column indices not strictly increasing in row {i}")
+            if c == 3:
+                raise E.NumericalError(f"non-finite value in row {i}")
+            raise E.NumericalError(f"explicit zero stored in row {i}")
+        if dec.size:
             raise E.ShapeError("offsets must be non-decreasing")
-        ci = self.col_indices
-        if ci.size and (ci.min() < 0 or ci.max() >= self.cols):
-            bad = int(np.searchsorted(self.offsets, int(np.flatnonzero((ci < 0) | (ci >= self.cols))[0]), "right") - 1)
-            raise E.ShapeError(f"column index out of range in row {bad}")
-        if ci.size > 1:
-            same_row = np.repeat(np.arange(self.rows), np.diff(self.offsets))
-            inc = (np.diff(ci) > 0) | (np.diff(same_row) != 0)
-            if not np.all(inc):
-                bad = int(same_row[1:][~inc][0])
-                raise E.ShapeError(f"column indices not strictly increasing in row {bad}")
-        if not np.all(np.isfinite(self.values)):
-            raise E.NumericalError("non-finite value")
-        if np.any(self.values == 0.0):
-            raise E.NumericalError("explicit zero stored")
+
+    def validate_on_device(self, device: Optional["Device"] = None) -> None:
+        """The same check run by the sm_100a library (dsvd_csr_validate)."""
+        if self.offsets.shape[0] != self.rows + 1:
+            raise E.ShapeError("offset array must have rows+1 entries")
+        if self.col_indices.shape[0] != self.values.shape[0]:
+            raise E.ShapeError("index/value length mismatch")
+        check(lib().dsvd_csr_validate(_dev(device).handle, self.rows, self.cols, self.nnz, _ptr(self.offsets),
+                                      _ptr(self.col_indices), _ptr(self.values)))
 
 
 @dataclass
@@ -198,9 +224,44 @@ class Device:
         if profiling:
             self.set_profiling(True)
 
+    @classmethod
+    def _adopt(cls, h, rows: int, cols: int, nnz: int, device: "Device") -> "DeviceMatrix":
+        m = cls(None, device)
+        m._h = h
+        m.rows, m.cols, m.nnz = int(rows), int(cols), int(nnz)
+        return m
+
+    @classmethod
+    def load_cache(cls, path: str, device: Optional[Device] = None, validate: bool = True) -> "DeviceMatrix":
+        """load_cache (matrix_market.cpp:257-275) straight into HBM: the DSH1 file is read
+        into pinned memory, validated on the device and built into the device pair."""
+        dev = _dev(device)
+        h, dims = _P(), (I64 * 3)()
+        check(lib().dsvd_matrix_load_cache(dev.handle, _path(path), 1 if validate else 0, C.byref(h), dims))
+        return cls._adopt(h, dims[0], dims[1], dims[2], dev)
+
+    @classmethod
+    def from_matrix_market(cls, path: str, device: Optional[Device] = None) -> "DeviceMatrix":
+        """load_matrix_market (matrix_market.cpp:117-165) with the assembly on the device
+        and the device pair built from it without a host round trip."""
+        dev = _dev(device)
+        dims = (I64 * 3)()
+        check(lib().dsvd_mtx_assemble(dev.handle, _path(path), dims))
+        h = _P()
+        check(lib().dsvd_matrix_from_coo(dev.handle, C.byref(h)))
+        return cls._adopt(h, dims[0], dims[1], dims[2], dev)
+
     @property
     def handle(self):
         return self._h
+
+    def download(self) -> SparseMatrix:
+        """CSR(A) back to the host (int64 indices)."""
+        off = np.empty(self.rows + 1, dtype=np.int64)
+        idx = np.empty(self.nnz, dtype=np.int64)
+        val = np.empty(self.nnz, dtype=np.float64)
+        check(lib().dsvd_matrix_download(self._h, _ptr(off), _ptr(idx), _ptr(val)))
+        return SparseMatrix(self.rows, self.cols, off, idx, val)
 
     def set_profiling(self, on: bool) -> None:
         check(lib().dsvd_ctx_set_profiling(self._h, 1 if on else 0))
@@ -283,17 +344,55 @@ def _dev(device: Optional[Device]) -> Device:
 class DeviceMatrix:
     """Device-resident CSR(A) + CSR(A^T) (upload once, solve many)."""
 
-    def __init__(self, a: SparseMatrix, device: Optional[Device] = None):
+    def __init__(self, a: Optional[SparseMatrix], device: Optional[Device] = None):
         self.device = _dev(device)
+        if a is None:  # filled in by _adopt
+            self._h = None
+            return
         h = _P()
         check(lib().dsvd_matrix_upload(self.device.handle, a.rows, a.cols, a.nnz, _ptr(a.offsets),
                                        _ptr(a.col_indices), _ptr(a.values), C.byref(h)))
         self._h = h
         self.rows, self.cols, self.nnz = a.rows, a.cols, a.nnz
 
+    @classmethod
+    def _adopt(cls, h, rows: int, cols: int, nnz: int, device: "Device") -> "DeviceMatrix":
+        m = cls(None, device)
+        m._h = h
+        m.rows, m.cols, m.nnz = int(rows), int(cols), int(nnz)
+        return m
+
+    @classmethod
+    def load_cache(cls, path: str, device: Optional[Device] = None, validate: bool = True) -> "DeviceMatrix":
+        """load_cache (matrix_market.cpp:257-275) straight into HBM: the DSH1 file is read
+        into pinned memory, validated on the device and built into the device pair."""
+        dev = _dev(device)
+        h, dims = _P(), (I64 * 3)()
+        check(lib().dsvd_matrix_load_cache(dev.handle, _path(path), 1 if validate else 0, C.byref(h), dims))
+        return cls._adopt(h, dims[0], dims[1], dims[2], dev)
+
+    @classmethod
+    def from_matrix_market(cls, path: str, device: Optional[Device] = None) -> "DeviceMatrix":
+        """load_matrix_market (matrix_market.cpp:117-165) with the assembly on the device
+        and the device pair built from it without a host round trip."""
+        dev = _dev(device)
+        dims = (I64 * 3)()
+        check(lib().dsvd_mtx_assemble(dev.handle, _path(path), dims))
+        h = _P()
+        check(lib().dsvd_matrix_from_coo(dev.handle, C.byref(h)))
+        return cls._adopt(h, dims[0], dims[1], dims[2], dev)
+
     @property
     def handle(self):
         return self._h
+
+    def download(self) -> SparseMatrix:
+        """CSR(A) back to the host (int64 indices)."""
+        off = np.empty(self.rows + 1, dtype=np.int64)
+        idx = np.empty(self.nnz, dtype=np.int64)
+        val = np.empty(self.nnz, dtype=np.float64)
+        check(lib().dsvd_matrix_download(self._h, _ptr(off), _ptr(idx), _ptr(val)))
+        return SparseMatrix(self.rows, self.cols, off, idx, val)
 
     def set_shard(self, row_offset: int, global_rows: int) -> None:
         check(lib().dsvd_matrix_set_shard(self._h, int(row_offset), int(global_rows)))
@@ -708,3 +807,73 @@ def max_triplet_residual(a, approx: TruncatedSvd, device: Optional[Device] = Non
     u, v = np.asfortranarray(approx.u, dtype=np.float64), np.asfortranarray(approx.v, dtype=np.float64)
     s = np.ascontiguousarray(approx.s, dtype=np.float64)
     return _metric_call(a, device, lib().dsvd_max_triplet_residual, _ptr(u), _ptr(s), _ptr(v), s.size)
+
+
+# ---- inputs: DSH1 cache, Matrix Market, COO assembly -----------
+
+def _fetch_coo(dev: Device, rows: int, cols: int, nnz: int) -> SparseMatrix:
+    off = np.empty(rows + 1, dtype=np.int64)
+    idx = np.empty(nnz, dtype=np.int64)
+    val = np.empty(nnz, dtype=np.float64)
+    check(lib().dsvd_coo_fetch(dev.handle, _ptr(off), _ptr(idx), _ptr(val)))
+    return SparseMatrix(rows, cols, off, idx, val)
+
+
+def assemble(rows: int, cols: int, r, c, v, device: Optional[Device] = None) -> SparseMatrix:
+    """assemble (matrix_market.cpp:90-115) on the device: triplets sorted by (row, col),
+    duplicates summed, exact zeros dropped. 0-based coordinates."""
+    dev = _dev(device)
+    r = np.ascontiguousarray(r, dtype=np.int64)
+    c = np.ascontiguousarray(c, dtype=np.int64)
+    v = np.ascontiguousarray(v, dtype=np.float64)
+    if not (r.shape == c.shape == v.shape):
+        raise E.ShapeError("triplet arrays differ in length")
+    nnz = I64()
+    check(lib().dsvd_coo_assemble(dev.handle, int(rows), int(cols), r.size, _ptr(r), _ptr(c), _ptr(v),
+                                  C.byref(nnz)))
+    return _fetch_coo(dev, int(rows), int(cols), int(nnz.value))
+
+
+def load_matrix_market(path: str, device: Optional[Device] = None) -> SparseMatrix:
+    """load_matrix_market (matrix_market.cpp:117-165): parsed on the host, assembled on the
+    device, returned as a host CSR (DeviceMatrix.from_matrix_market keeps it in HBM)."""
+    dev = _dev(device)
+    dims = (I64 * 3)()
+    check(lib().dsvd_mtx_assemble(dev.handle, _path(path), dims))
+    return _fetch_coo(dev, dims[0], dims[1], dims[2])
+
+
+def read_matrix_market_triplets(path: str):
+    """The host parsing half of load_matrix_market (matrix_market.cpp:117-163): returns
+    (rows, cols, r, c, v), 0-based triplets in file order after the symmetric expansion,
+    before assembly. Raises ParseError / UnsupportedFormat / Error like the reference."""
+    dims = (I64 * 3)()
+    check(lib().dsvd_mtx_read(_path(path), dims))
+    n = int(dims[2])
+    r = np.empty(n, dtype=np.int64)
+    c = np.empty(n, dtype=np.int64)
+    v = np.empty(n, dtype=np.float64)
+    check(lib().dsvd_mtx_fetch(_ptr(r), _ptr(c), _ptr(v)))
+    return int(dims[0]), int(dims[1]), r, c, v
+
+
+def write_matrix_market(path: str, a: SparseMatrix) -> None:
+    """write_matrix_market (matrix_market.cpp:167-177)."""
+    check(lib().dsvd_write_matrix_market(_path(path), a.rows, a.cols, _ptr(a.offsets), _ptr(a.col_indices),
+                                         _ptr(a.values)))
+
+
+def save_cache(path: str, a: SparseMatrix) -> None:
+    """save_cache (matrix_market.cpp:241-253): DSH1 binary CSR."""
+    check(lib().dsvd_save_cache(_path(path), a.rows, a.cols, a.nnz, _ptr(a.offsets), _ptr(a.col_indices),
+                                _ptr(a.values)))
+
+
+def load_cache(path: str, device: Optional[Device] = None) -> SparseMatrix:
+    """load_cache (matrix_market.cpp:255-275): read, validated on the device, returned on
+    the host. DeviceMatrix.load_cache keeps the matrix in HBM instead."""
+    m = DeviceMatrix.load_cache(path, device, validate=True)
+    try:
+        return m.download()
+    finally:
+        m.close()

@@ -63,6 +63,7 @@ struct dsvd_ctx {
     uint64_t omega_seed = 0;
     cudaEvent_t omega_ev = nullptr;
     cudaStream_t copy = nullptr;      // host->device copy of the CSR values (upload_pair)
+    int64_t coo_rows = -1, coo_cols = -1, coo_nnz = -1;  // last assembled CSR (dsvd_coo_fetch, _from_coo)
     cudaEvent_t copy_ev = nullptr;
     cudaEvent_t fork = nullptr, join = nullptr;
     int32_t* host_flags = nullptr;  // pinned ring for stop flags

@@ -65,7 +65,9 @@ def _raise(code, msg, index):
         return
     if code == 3:
         raise E.RankDeficient(int(index), msg)
-    raise {1: E.ShapeError, 2: E.ConfigError, 4: E.NumericalError}.get(code, E.Error)(msg)
+    if code == 12:
+        raise E.ParseError(int(index), msg.split(": ", 1)[1] if msg.startswith("parse error") else msg)
+    raise {1: E.ShapeError, 2: E.ConfigError, 4: E.NumericalError, 11: E.UnsupportedFormat}.get(code, E.Error)(msg)
 
 
 def transpose_np(a: Csr) -> Csr:
@@ -282,6 +284,36 @@ class Reference(_Lib):
         self.check(fn(*self._a(a), _ptr(u), _ptr(s), _ptr(v), s.size, _ptr(sg), sg.size, power_iters, seed,
                       _ptr(out)))
         return out
+
+    # --- inputs (matrix_market.cpp, sparse_matrix.cpp:12-33) ---------------
+    def validate(self, a: Csr):
+        self.check(self.f("validate", C.c_int, _I64, _I64, _I64, _P, _P, _P)(*self._a(a)))
+
+    def _fetch_csr(self, dims) -> Csr:
+        rows, cols, n = dims[0], dims[1], dims[2]
+        off = np.empty(rows + 1, dtype=np.int64)
+        idx = np.empty(n, dtype=np.int64)
+        val = np.empty(n, dtype=np.float64)
+        self.f("csr_fetch", None, _P, _P, _P)(_ptr(off), _ptr(idx), _ptr(val))
+        return Csr(rows, cols, off, idx, val)
+
+    def load_matrix_market(self, path) -> Csr:
+        dims = (_I64 * 3)()
+        self.check(self.f("load_matrix_market", C.c_int, C.c_char_p, _P)(os.fsencode(path), dims))
+        return self._fetch_csr(dims)
+
+    def load_cache(self, path) -> Csr:
+        dims = (_I64 * 3)()
+        self.check(self.f("load_cache", C.c_int, C.c_char_p, _P)(os.fsencode(path), dims))
+        return self._fetch_csr(dims)
+
+    def save_cache(self, path, a: Csr):
+        self.check(self.f("save_cache", C.c_int, C.c_char_p, _I64, _I64, _I64, _P, _P, _P)(os.fsencode(path),
+                                                                                       *self._a(a)))
+
+    def write_matrix_market(self, path, a: Csr):
+        self.check(self.f("write_matrix_market", C.c_int, C.c_char_p, _I64, _I64, _I64, _P, _P, _P)(
+            os.fsencode(path), *self._a(a)))
 
     def sparse_random(self, rows, cols, npr, seed, decay=False) -> Csr:
         nnz = _I64()
