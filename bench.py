@@ -44,6 +44,14 @@ CONFIGS = {
     "c3": dict(name="C3 ratings 2000000x500000, lognormal(4.2,1.2), Zipf(1.0), values 1-5",
                rows=2_000_000, cols=500_000, mu=4.2, sigma=1.2, zipf=1.0, ratings=True,
                gen_seed=3, k=100, s=50, p=-1, p_max=100, tol=1e-2, alg="dash", seed=0),
+    # BASELINE.json configs[3]: R-MAT scale 22, ~100M unique edges (104M draws), values 1.0
+    "c4": dict(name="C4 R-MAT scale 22, (a,b,c)=(.57,.19,.19), 104M draws -> ~100M unique, values 1.0",
+               rows=1 << 22, cols=1 << 22, rmat_scale=22, draws=104_000_000, uniform=False,
+               gen_seed=4, k=200, s=100, p=30, alg="shifted", seed=0),
+    # BASELINE.json configs[4]: R-MAT scale 24, ~1B unique edges (1.05B draws), uniform(0,1] values
+    "c5": dict(name="C5 R-MAT scale 24, (a,b,c)=(.57,.19,.19), 1.05B draws -> ~1.0B unique, uniform(0,1]",
+               rows=1 << 24, cols=1 << 24, rmat_scale=24, draws=1_050_000_000, uniform=True,
+               gen_seed=5, k=100, s=50, p=-1, p_max=50, tol=1e-2, alg="dash", seed=0),
 }
 
 CLOCK_FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
@@ -63,10 +71,17 @@ def parse():
     return ap.parse_args()
 
 
-def make_matrix(cfg):
+def make_matrix(cfg, device=None):
     import paper_2404_09276_b200 as d
     if "npr" in cfg:
         return d.sparse_random(cfg["rows"], cfg["cols"], cfg["npr"], cfg["gen_seed"], True)
+    if "rmat_scale" in cfg:  # generated on the device, brought to the host as the input CSR
+        m = d.rmat(cfg["rmat_scale"], cfg["draws"], uniform_values=cfg["uniform"], seed=cfg["gen_seed"],
+                   device=device)
+        try:
+            return m.download()
+        finally:
+            m.close()
     return d.powerlaw(cfg["rows"], cfg["cols"], cfg["mu"], cfg["sigma"], cfg["zipf"],
                       cfg["gen_seed"], ratings=cfg["ratings"])
 
@@ -230,7 +245,8 @@ def run_b200(args, rank, world, local_rank):
     dist = None
     if world > 1:
         import torch.distributed as dist
-    a_full = make_matrix(cfg)
+    dev = d.Device(local_rank)
+    a_full = make_matrix(cfg, dev)
     r0, r1 = shard_rows(a_full, world, rank)
     off = a_full.offsets[r0:r1 + 1] - a_full.offsets[r0]
     sl = slice(int(a_full.offsets[r0]), int(a_full.offsets[r1]))
@@ -239,7 +255,6 @@ def run_b200(args, rank, world, local_rank):
     scfg = solver_config(cfg)
     k, l = scfg.k, scfg.sketch_width()
 
-    dev = d.Device(local_rank)
     if world > 1:
         uid = torch.zeros(128, dtype=torch.uint8, device="cuda")
         if rank == 0:

@@ -255,6 +255,16 @@ DSVD_API int dsvd_mtx_read(const char* path, int64_t* dims);
 DSVD_API int dsvd_mtx_fetch(int64_t* r, int64_t* c, double* v);
 DSVD_API int dsvd_write_matrix_market(const char* path, int64_t rows, int64_t cols, const int64_t* offsets,
                                       const int64_t* col_indices, const double* values);
+/* R-MAT generator on the device (BASELINE.json configs 4/5; no reference
+ * counterpart: the reference ships only sparse_random). Draws `draws` edges of
+ * a 2^scale square graph with quadrant probabilities (a, b, c, 1-a-b-c) at
+ * 16-bit resolution from counter-based SplitMix64 streams (ingest.cuh spells
+ * out the rule), keeps the first draw of every duplicate edge, values 1.0
+ * (value_mode 0) or uniform (0, 1] (value_mode 1), and builds the device pair
+ * directly. *nnz receives the unique edge count; dsvd_matrix_download copies
+ * the CSR to the host (e.g. for the CPU reference). */
+DSVD_API int dsvd_synth_rmat(dsvd_ctx* ctx, int scale, int64_t draws, double a, double b, double c, int value_mode,
+                             uint64_t seed, dsvd_matrix** out, int64_t* nnz);
 
 /* ---- validation metrics (metrics.hpp / metrics.cpp:99-206) ----------------
  * Host factors (column-major u[rows*k], s[k], v[cols*k]) against the device

@@ -10,7 +10,7 @@ from .api import (Algorithm, assemble, load_cache, load_matrix_market, read_matr
                   ShiftTrace, SolveResult, SolverConfig, SparseMatrix, StopReason, TruncatedSvd,
                   basic_rsvd, comm_unique_id, dash_svd, default_device, eig_svd, eps_pve, eps_res,
                   eps_spec, finalize_row_basis, gaussian_matrix, gram, matmul, max_triplet_residual,
-                  pin, powerlaw, pve_stop_check,
+                  pin, powerlaw, pve_stop_check, rmat,
                   shifted_rsvd, solve, sparse_random, splitmix64_at, spmm, spmm_shift, sym_eig,
                   transpose, unpin, update_shift, validate_config)
 from .errors import (ConfigError, DegenerateReference, DeviceError, Error, NumericalError, RankDeficient,

@@ -120,6 +120,7 @@ SIGNATURES = [
     ("dsvd_synth_sparse_random", C.c_int, [I64, I64, I64, U64, C.c_int, C.POINTER(I64)]),
     ("dsvd_synth_powerlaw", C.c_int, [I64, I64, D, D, D, C.c_int, U64, C.POINTER(I64)]),
     ("dsvd_synth_fetch", C.c_int, [P, P, P]),
+    ("dsvd_synth_rmat", C.c_int, [P, C.c_int, I64, D, D, D, C.c_int, U64, C.POINTER(P), C.POINTER(I64)]),
 ]
 
 _lib = None

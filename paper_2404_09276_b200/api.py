@@ -731,6 +731,18 @@ def powerlaw(rows: int, cols: int, mu: float, sigma: float, zipf_s: float, seed:
     return _fetch(rows, cols, nnz.value)
 
 
+def rmat(scale: int, draws: int, a: float = 0.57, b: float = 0.19, c: float = 0.19, uniform_values: bool = False,
+         seed: int = 0, device: Optional[Device] = None) -> "DeviceMatrix":
+    """R-MAT graph generated on the device (BASELINE.json configs 4/5), returned as a device
+    matrix (DeviceMatrix.download() for the host CSR). See dsvd_synth_rmat for the rule."""
+    dev = _dev(device)
+    h, nnz = _P(), I64()
+    check(lib().dsvd_synth_rmat(dev.handle, int(scale), int(draws), float(a), float(b), float(c),
+                                1 if uniform_values else 0, int(seed) & 0xFFFFFFFFFFFFFFFF, C.byref(h), C.byref(nnz)))
+    n = 1 << int(scale)
+    return DeviceMatrix._adopt(h, n, n, nnz.value, dev)
+
+
 def solve_device_csr(rows: int, cols: int, nnz: int, d_offsets: int, d_col_indices: int,
                      d_values: int, cfg: SolverConfig, d_u: int, d_s: int, d_v: int,
                      device: Optional[Device] = None) -> SolveResult:

@@ -1349,6 +1349,48 @@ int dsvd_matrix_from_coo(dsvd_ctx* ctx, dsvd_matrix** out) {
     });
 }
 
+int dsvd_synth_rmat(dsvd_ctx* ctx, int scale, int64_t draws, double a, double b, double c, int value_mode,
+                    uint64_t seed, dsvd_matrix** out, int64_t* nnz_out) {
+    return guarded([&] {
+        set_device(ctx);
+        if (scale < 1 || scale > 30) fail(DSVD_SHAPE, "rmat: scale must be in [1, 30]");
+        if (draws < 0 || draws > 0x7fffffffLL) fail(DSVD_SHAPE, "rmat: draws must be in [0, 2^31)");
+        if (!(a >= 0 && b >= 0 && c >= 0 && a + b + c <= 1.0)) fail(DSVD_CONFIG, "rmat: need a, b, c >= 0, a+b+c <= 1");
+        if (value_mode != 0 && value_mode != 1) fail(DSVD_CONFIG, "rmat: value_mode 0 (ones) or 1 (uniform (0,1])");
+        RmatParams P;
+        P.scale = scale;
+        P.draws = draws;
+        P.t_a = static_cast<uint32_t>(std::llround(a * 65536.0));
+        P.t_ab = static_cast<uint32_t>(std::llround((a + b) * 65536.0));
+        P.t_abc = static_cast<uint32_t>(std::llround((a + b + c) * 65536.0));
+        P.value_mode = value_mode;
+        P.edge_seed = splitmix64_at(seed, 0);
+        P.val_seed = splitmix64_at(seed, 1);
+        const int64_t n = int64_t(1) << scale;
+        int64_t* off = ctx->tbuf<int64_t>("rmat.off", n + 1);
+        int64_t* idx = ctx->tbuf<int64_t>("upload.idx64", draws);
+        double* val = ctx->tbuf<double>("rmat.val", draws);
+        const int64_t nnz = rmat_generate(P, ctx->buf("rmat.scratch", rmat_scratch_bytes(draws)), off, idx, val,
+                                          ctx->stream);
+        ctx->release("rmat.scratch");
+        std::unique_ptr<dsvd_matrix> m(new dsvd_matrix());
+        m->ctx = ctx;
+        m->device = ctx->device;
+        CsrAlloc al{ctx, "", &m->owned};
+        try {
+            build_pair(ctx, al, n, n, nnz, off, idx, val, m->a, m->at, true);
+            DSVD_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+        } catch (...) {
+            for (void* p : m->owned) cudaFree(p);
+            throw;
+        }
+        ctx->release("rmat.off");
+        ctx->release("rmat.val");
+        *nnz_out = nnz;
+        *out = m.release();
+    });
+}
+
 int dsvd_write_matrix_market(const char* path, int64_t rows, int64_t cols, const int64_t* offsets,
                              const int64_t* col_indices, const double* values) {
     return guarded([&] {

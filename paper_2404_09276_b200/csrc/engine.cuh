@@ -84,6 +84,12 @@ struct dsvd_ctx {
         }
         return b.ptr;
     }
+    void release(const std::string& name) {
+        auto it = arena.find(name);
+        if (it == arena.end()) return;
+        if (it->second.ptr) DSVD_CUDA_CHECK(cudaFree(it->second.ptr));
+        arena.erase(it);
+    }
     template <class T>
     T* tbuf(const std::string& name, size_t count) {
         return static_cast<T*>(buf(name, sizeof(T) * (count > 0 ? count : 1)));

@@ -13,6 +13,7 @@
 #include <cub/device/device_scan.cuh>
 
 #include "ingest.cuh"
+#include "rng.cuh"
 
 namespace dsvd {
 
@@ -114,6 +115,46 @@ __global__ void minus_one_kernel(int64_t* x, int64_t n) {
         x[i] -= 1;
 }
 
+__global__ void rmat_keys_kernel(RmatParams P, uint64_t* __restrict__ keys, uint32_t* __restrict__ draw) {
+    const int H = (P.scale + 3) / 4;
+    for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < P.draws;
+         e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        uint64_t row = 0, col = 0, h = 0;
+        for (int t = 0; t < P.scale; ++t) {
+            if ((t & 3) == 0) h = splitmix64_at(P.edge_seed, static_cast<uint64_t>(e) * H + (t >> 2));
+            const uint32_t q = static_cast<uint32_t>(h >> (16 * (t & 3))) & 0xffffu;
+            const uint32_t quad = q < P.t_a ? 0u : (q < P.t_ab ? 1u : (q < P.t_abc ? 2u : 3u));
+            row = (row << 1) | (quad >> 1);
+            col = (col << 1) | (quad & 1u);
+        }
+        keys[e] = (row << P.scale) | col;
+        draw[e] = static_cast<uint32_t>(e);
+    }
+}
+
+__global__ void head_flags_kernel(const uint64_t* __restrict__ keys, int64_t n, int64_t* __restrict__ flag) {
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        flag[i] = (i == 0 || keys[i] != keys[i - 1]) ? 1 : 0;
+}
+
+// first draw of each run of equal keys -> (column, value), row counts
+__global__ void rmat_emit_kernel(RmatParams P, const uint64_t* __restrict__ keys, const uint32_t* __restrict__ draw,
+                                 const int64_t* __restrict__ incl, int64_t n, int64_t* __restrict__ out_idx,
+                                 double* __restrict__ out_val, int64_t* __restrict__ row_count) {
+    const uint64_t mask = (1ull << P.scale) - 1;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        if (i != 0 && keys[i] == keys[i - 1]) continue;
+        const int64_t w = incl[i] - 1;
+        out_idx[w] = static_cast<int64_t>(keys[i] & mask);
+        out_val[w] = P.value_mode == 0 ? 1.0
+                                       : (static_cast<double>(splitmix64_at(P.val_seed, draw[i]) >> 11) + 1.0) *
+                                             0x1p-53;
+        atomicAdd(reinterpret_cast<unsigned long long*>(row_count + (keys[i] >> P.scale) + 1), 1ull);
+    }
+}
+
 unsigned grid_n(int64_t n) {
     const int64_t g = ceil_div(n, 256);
     return static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(g, 148 * 32)));
@@ -191,6 +232,57 @@ int64_t coo_assemble(const int64_t* d_r, const int64_t* d_c, const double* d_v, 
                                                   stream));
     DSVD_CUDA_CHECK(cudaStreamSynchronize(stream));
     return last_scan + last_keep;
+}
+
+size_t rmat_scratch_bytes(int64_t draws) {
+    size_t sort_tmp = 0, scan_tmp = 0;
+    const int nn = static_cast<int>(draws > 0 ? draws : 1);
+    cub::DoubleBuffer<uint64_t> kb(nullptr, nullptr);
+    cub::DoubleBuffer<uint32_t> vb(nullptr, nullptr);
+    cub::DeviceRadixSort::SortPairs(nullptr, sort_tmp, kb, vb, nn);
+    cub::DeviceScan::InclusiveSum(nullptr, scan_tmp, static_cast<const int64_t*>(nullptr),
+                                  static_cast<int64_t*>(nullptr), nn);
+    const size_t n = static_cast<size_t>(draws > 0 ? draws : 1);
+    const size_t a8 = (n * 8 + 255) / 256 * 256, a4 = (n * 4 + 255) / 256 * 256;
+    return 2 * a8 + 2 * a4 + 2 * a8 + std::max(sort_tmp, scan_tmp) + 256;
+}
+
+int64_t rmat_generate(const RmatParams& P, void* scratch, int64_t* d_off, int64_t* d_idx, double* d_val,
+                      cudaStream_t stream) {
+    const int64_t rows = int64_t(1) << P.scale;
+    DSVD_CUDA_CHECK(cudaMemsetAsync(d_off, 0, sizeof(int64_t) * (rows + 1), stream));
+    const int64_t n = P.draws;
+    if (n == 0) return 0;
+    const size_t a8 = (static_cast<size_t>(n) * 8 + 255) / 256 * 256, a4 = (static_cast<size_t>(n) * 4 + 255) / 256 * 256;
+    char* p = static_cast<char*>(scratch);
+    uint64_t* k0 = reinterpret_cast<uint64_t*>(p);
+    uint64_t* k1 = reinterpret_cast<uint64_t*>(p + a8);
+    uint32_t* v0 = reinterpret_cast<uint32_t*>(p + 2 * a8);
+    uint32_t* v1 = reinterpret_cast<uint32_t*>(p + 2 * a8 + a4);
+    int64_t* flag = reinterpret_cast<int64_t*>(p + 2 * a8 + 2 * a4);
+    int64_t* incl = reinterpret_cast<int64_t*>(p + 3 * a8 + 2 * a4);
+    void* tmp = p + 4 * a8 + 2 * a4;
+    size_t tmp_bytes = rmat_scratch_bytes(n) - (4 * a8 + 2 * a4);
+    rmat_keys_kernel<<<grid_n(n), 256, 0, stream>>>(P, k0, v0);
+    DSVD_LAUNCH_CHECK();
+    cub::DoubleBuffer<uint64_t> kb(k0, k1);
+    cub::DoubleBuffer<uint32_t> vb(v0, v1);
+    DSVD_CUDA_CHECK(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, kb, vb, static_cast<int>(n), 0, 2 * P.scale,
+                                                    stream));
+    const uint64_t* keys = kb.Current();
+    const uint32_t* draw = vb.Current();
+    head_flags_kernel<<<grid_n(n), 256, 0, stream>>>(keys, n, flag);
+    DSVD_LAUNCH_CHECK();
+    tmp_bytes = rmat_scratch_bytes(n) - (4 * a8 + 2 * a4);
+    DSVD_CUDA_CHECK(cub::DeviceScan::InclusiveSum(tmp, tmp_bytes, flag, incl, static_cast<int>(n), stream));
+    rmat_emit_kernel<<<grid_n(n), 256, 0, stream>>>(P, keys, draw, incl, n, d_idx, d_val, d_off);
+    DSVD_LAUNCH_CHECK();
+    DSVD_CUDA_CHECK(cub::DeviceScan::InclusiveSum(tmp, tmp_bytes, d_off + 1, d_off + 1, static_cast<int>(rows),
+                                                  stream));
+    int64_t nnz = 0;
+    DSVD_CUDA_CHECK(cudaMemcpyAsync(&nnz, incl + n - 1, sizeof(int64_t), cudaMemcpyDeviceToHost, stream));
+    DSVD_CUDA_CHECK(cudaStreamSynchronize(stream));
+    return nnz;
 }
 
 }  // namespace dsvd

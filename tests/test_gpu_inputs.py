@@ -203,3 +203,28 @@ def test_solve_from_file_equals_upload(tmp_path, dev):
     d.write_matrix_market(mtx, a)
     r3 = d.DeviceMatrix.from_matrix_market(mtx, device=dev).solve(cfg)
     assert np.array_equal(r3.svd.v.view(np.uint64), r2.svd.v.view(np.uint64))
+
+
+# ---- R-MAT generator (BASELINE.json configs 4/5) ----------------------------------
+
+@pytest.mark.parametrize("scale,draws,uniform,seed", [(1, 5, False, 0), (6, 300, True, 3), (10, 20000, False, 1),
+                                                      (13, 150000, True, 7), (17, 2000000, True, 2)])
+def test_rmat_matches_numpy_restatement(dev, scale, draws, uniform, seed):
+    from input_cases import rmat_np
+    m = d.rmat(scale, draws, uniform_values=uniform, seed=seed, device=dev)
+    got = m.download()
+    same_csr(got, rmat_np(scale, draws, uniform=uniform, seed=seed))
+    got.validate()
+    assert np.all(got.values > 0.0) and np.all(got.values <= 1.0)
+    m.close()
+
+
+def test_rmat_skewed_quadrants(dev):
+    from input_cases import rmat_np
+    for a, b, c in ((1.0, 0.0, 0.0), (0.25, 0.25, 0.25), (0.0, 0.0, 1.0), (0.45, 0.15, 0.15)):
+        got = d.rmat(9, 5000, a, b, c, seed=4, device=dev).download()
+        same_csr(got, rmat_np(9, 5000, a, b, c, seed=4))
+    with pytest.raises(E.ConfigError):
+        d.rmat(5, 10, 0.6, 0.3, 0.3, device=dev)
+    with pytest.raises(E.ShapeError):
+        d.rmat(31, 10, device=dev)
