@@ -79,7 +79,7 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned b
 
 // ---- rescale ----------------------------------------------------------------------
 constexpr int kRsBM = 128, kRsBN = 32, kRsBK = 16, kRsStages = 4, kRsThreads = 256;
-constexpr int kRsMaxK = 160;
+constexpr int kRsMaxK = 320;  // W block (32 x (K+8)) + the ring fit in shared memory
 
 // wt[nn][k] = (k < K && nn < ncol) ? w[k][nn] * scale[nn] : 0, nn < npad, k < ldb
 __global__ void rescale_prep_kernel(const double* __restrict__ w, int64_t ldw, const double* __restrict__ scale,
@@ -439,6 +439,90 @@ gram_dmma_reduce_kernel(const double* __restrict__ partial, int nblk, int nb, in
     g[j * l + i] = s;
 }
 
+// Wide Gram (l > 160, e.g. C4's l = 300): the 32-column strips are grouped in
+// fours (128 columns); CTA (pair of strip groups a <= b, row slab) computes the
+// 4x4 tiles (I, J), I in group a, J in group b, I <= J, one warp per tile (16
+// warps), staging only the columns of its two groups. blockIdx.x (the group
+// pair) varies fastest so the CTAs of one slab share the slab in L2. Same
+// partial layout as gram_dmma_kernel (one triangle of 8x8 blocks per slab).
+constexpr int kGwRows = 16, kGwStages = 4, kGwStride = 264;  // 2 * 264 == 16 (mod 32) banks
+
+__global__ void __launch_bounds__(512, 1)
+gram_dmma_wide_kernel(const double* __restrict__ c, int64_t n, int64_t ld, int nb, int64_t rows_per_block,
+                      double* __restrict__ partial, const int32_t* __restrict__ gate) {
+    if (gate != nullptr && *gate != 0) return;
+    extern __shared__ __align__(16) double wsm[];  // [stages][kGwRows][kGwStride]
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int q = lane & 3, g = lane >> 2;
+    int a = 0, t = blockIdx.x;
+    const int ngrp = (nb + 15) / 16;
+    while (t >= ngrp - a) {
+        t -= ngrp - a;
+        ++a;
+    }
+    const int b = a + t;
+    const int I = 4 * a + (warp >> 2), J = 4 * b + (warp & 3);
+    const bool active = I <= J && 4 * I < nb && 4 * J < nb;
+    const int64_t r_beg = static_cast<int64_t>(blockIdx.y) * rows_per_block;
+    const int64_t r_end = min(n, r_beg + rows_per_block);
+    const int64_t c0a = 128 * a, c0b = 128 * b;
+    const bool same = a == b;
+    auto stage = [&](int slot, int64_t rr0) {  // 16 rows x (64 + 64) 16-byte chunks
+        double* dst = wsm + slot * kGwRows * kGwStride;
+        for (int e = tid; e < kGwRows * 128; e += 512) {
+            const int r = e >> 7, ch = e & 127;
+            const int64_t gr = rr0 + r;
+            const int64_t col = (ch < 64 ? c0a : c0b) + 2 * (ch & 63);
+            const bool ok = gr < r_end && col < ld && (ch < 64 || !same);
+            cpa16z(dst + r * kGwStride + 2 * ch, ok ? c + gr * ld + col : c, ok);
+        }
+    };
+    const int nst = static_cast<int>(((r_end > r_beg ? r_end - r_beg : int64_t(0)) + kGwRows - 1) / kGwRows);
+    for (int st = 0; st < kGwStages - 1; ++st) {
+        if (st < nst) stage(st, r_beg + st * kGwRows);
+        cpa_commit();
+    }
+    double2 acc[4][4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) acc[u][v] = make_double2(0.0, 0.0);
+    const int ia = 32 * (I - 4 * a), jb = (same ? 0 : 128) + 32 * (J - 4 * b);
+    for (int st = 0; st < nst; ++st) {
+        cpa_wait<kGwStages - 2>();
+        __syncthreads();
+        const int pf = st + kGwStages - 1;
+        if (pf < nst) stage(pf % kGwStages, r_beg + static_cast<int64_t>(pf) * kGwRows);
+        cpa_commit();
+        if (!active) continue;
+        const double* C = wsm + (st % kGwStages) * kGwRows * kGwStride;
+#pragma unroll
+        for (int ks = 0; ks < kGwRows / 4; ++ks) {
+            const double* row = C + (4 * ks + q) * kGwStride + g;
+            double fa[4], fb[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) fa[u] = row[ia + 8 * u];
+#pragma unroll
+            for (int v = 0; v < 4; ++v) fb[v] = row[jb + 8 * v];
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+#pragma unroll
+                for (int v = 0; v < 4; ++v) dmma884(acc[u][v], fa[u], fb[v]);
+        }
+    }
+    cpa_wait<0>();
+    if (!active) return;
+    double* out = partial + static_cast<int64_t>(blockIdx.y) * gm_pairs(nb) * 64;
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+            const int bi = 4 * I + u, bj = 4 * J + v;
+            if (bi <= bj && bj < nb)
+                *reinterpret_cast<double2*>(out + gm_tri(bi, bj, nb) * 64 + g * 8 + 2 * q) = acc[u][v];
+        }
+}
+
 template <int NB4>
 void launch_gram_dmma(const double* c, int64_t n, int64_t ld, int nb, int nblk, int64_t rpb, double* partial,
                       const int32_t* gate, cudaStream_t stream) {
@@ -453,9 +537,21 @@ struct GramDmmaPlan {
     int nb = 0, nblk = 0;
     int64_t rpb = 0;
 };
+constexpr int kGramNarrowMaxNb = 20;  // gram_dmma_kernel<NB4 <= 5>: l <= 160
+constexpr int kGramWideMaxNb = 64;    // gram_dmma_wide_kernel: l <= 512
+
 GramDmmaPlan gram_dmma_plan(int64_t n, int64_t l) {
     GramDmmaPlan p;
     p.nb = static_cast<int>((l + 7) / 8);
+    if (p.nb > kGramNarrowMaxNb) {
+        // wide: group pairs x slabs, ~2 waves of one CTA per SM
+        const int ngrp = (p.nb + 15) / 16, npairs = ngrp * (ngrp + 1) / 2;
+        p.nblk = static_cast<int>(std::max<int64_t>(
+            1, std::min<int64_t>(ceil_div(2 * kNumSMs, npairs), ceil_div(n, 4 * kGwRows))));
+        p.rpb = ceil_div(ceil_div(n, p.nblk), kGwRows) * kGwRows;
+        p.nblk = static_cast<int>(std::max<int64_t>(1, ceil_div(n, p.rpb)));
+        return p;
+    }
     const int nb4 = (p.nb + 3) / 4;  // CTAs per SM as in the launch bounds
     p.nblk = static_cast<int>(std::max<int64_t>(
         1, std::min<int64_t>(kNumSMs * (nb4 >= 5 ? 1 : (nb4 == 4 ? 2 : (nb4 == 3 ? 3 : 4))), ceil_div(n, 64))));
@@ -466,7 +562,9 @@ GramDmmaPlan gram_dmma_plan(int64_t n, int64_t l) {
 
 }  // namespace
 
-bool gram_dmma_supported(int64_t l, int64_t ld) { return l >= 1 && (l + 7) / 8 <= 20 && ld % 2 == 0 && ld >= l; }
+bool gram_dmma_supported(int64_t l, int64_t ld) {
+    return l >= 1 && (l + 7) / 8 <= kGramWideMaxNb && ld % 2 == 0 && ld >= l;
+}
 
 size_t gram_dmma_workspace_bytes(int64_t n, int64_t l) {
     const GramDmmaPlan p = gram_dmma_plan(n, l);
@@ -477,6 +575,18 @@ void gram_dmma(const double* c, int64_t n, int64_t l, int64_t ld, double* g, voi
                cudaStream_t stream) {
     const GramDmmaPlan p = gram_dmma_plan(n, l);
     double* partial = static_cast<double*>(ws);
+    if (p.nb > kGramNarrowMaxNb) {
+        const int ngrp = (p.nb + 15) / 16;
+        const size_t smem = sizeof(double) * kGwStages * kGwRows * kGwStride;
+        DSVD_CUDA_CHECK(cudaFuncSetAttribute(gram_dmma_wide_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             static_cast<int>(smem)));
+        const dim3 grid(static_cast<unsigned>(ngrp * (ngrp + 1) / 2), static_cast<unsigned>(p.nblk));
+        gram_dmma_wide_kernel<<<grid, 512, smem, stream>>>(c, n, ld, p.nb, p.rpb, partial, gate);
+        DSVD_LAUNCH_CHECK();
+        gram_dmma_reduce_kernel<<<gm_pairs(p.nb), 256, 0, stream>>>(partial, p.nblk, p.nb, l, g, gate);
+        DSVD_LAUNCH_CHECK();
+        return;
+    }
     switch ((p.nb + 3) / 4) {
         case 1: launch_gram_dmma<1>(c, n, ld, p.nb, p.nblk, p.rpb, partial, gate, stream); break;
         case 2: launch_gram_dmma<2>(c, n, ld, p.nb, p.nblk, p.rpb, partial, gate, stream); break;
