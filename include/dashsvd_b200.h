@@ -139,6 +139,10 @@ DSVD_API int dsvd_ctx_destroy(dsvd_ctx* ctx);
 DSVD_API int dsvd_ctx_set_profiling(dsvd_ctx* ctx, int on);
 DSVD_API int dsvd_ctx_get_stats(const dsvd_ctx* ctx, dsvd_stats* out);
 DSVD_API int dsvd_ctx_synchronize(dsvd_ctx* ctx);
+/* Free the context's cached device workspaces (they are re-allocated on the
+ * next call); matrix handles keep their own buffers. For very large inputs
+ * that alternate between entry points. */
+DSVD_API int dsvd_ctx_trim(dsvd_ctx* ctx);
 /* Tuning knobs (testing/benchmarking); unknown names -> DSVD_CONFIG. */
 DSVD_API int dsvd_ctx_set_option(dsvd_ctx* ctx, const char* name, int64_t value);
 

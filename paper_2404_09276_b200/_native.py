@@ -68,6 +68,7 @@ SIGNATURES = [
     ("dsvd_ctx_set_profiling", C.c_int, [P, C.c_int]),
     ("dsvd_ctx_get_stats", C.c_int, [P, C.POINTER(dsvd_stats)]),
     ("dsvd_ctx_synchronize", C.c_int, [P]),
+    ("dsvd_ctx_trim", C.c_int, [P]),
     ("dsvd_ctx_set_option", C.c_int, [P, C.c_char_p, I64]),
     ("dsvd_comm_unique_id", C.c_int, [C.POINTER(C.c_uint8)]),
     ("dsvd_ctx_attach_comm", C.c_int, [P, C.c_int, C.c_int, C.POINTER(C.c_uint8)]),

@@ -277,6 +277,10 @@ class Device:
     def synchronize(self) -> None:
         check(lib().dsvd_ctx_synchronize(self._h))
 
+    def trim(self) -> None:
+        """Free the cached device workspaces (dsvd_ctx_trim)."""
+        check(lib().dsvd_ctx_trim(self._h))
+
     def attach_comm(self, nranks: int, rank: int, unique_id: bytes) -> None:
         buf = (C.c_uint8 * 128).from_buffer_copy(unique_id)
         check(lib().dsvd_ctx_attach_comm(self._h, int(nranks), int(rank), buf))

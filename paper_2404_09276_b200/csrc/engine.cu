@@ -979,6 +979,18 @@ int dsvd_ctx_synchronize(dsvd_ctx* ctx) {
     });
 }
 
+int dsvd_ctx_trim(dsvd_ctx* ctx) {
+    return guarded([&] {
+        set_device(ctx);
+        DSVD_CUDA_CHECK(cudaDeviceSynchronize());
+        for (auto& kv : ctx->arena)
+            if (kv.second.ptr) DSVD_CUDA_CHECK(cudaFree(kv.second.ptr));
+        ctx->arena.clear();
+        ctx->omega_pending = false;
+        ctx->coo_rows = ctx->coo_cols = ctx->coo_nnz = -1;
+    });
+}
+
 int dsvd_ctx_set_option(dsvd_ctx* ctx, const char* name, int64_t value) {
     return guarded([&] {
         const std::string n = name ? name : "";
