@@ -259,6 +259,19 @@ DSVD_API int dsvd_mtx_read(const char* path, int64_t* dims);
 DSVD_API int dsvd_mtx_fetch(int64_t* r, int64_t* c, double* v);
 DSVD_API int dsvd_write_matrix_market(const char* path, int64_t rows, int64_t cols, const int64_t* offsets,
                                       const int64_t* col_indices, const double* values);
+/* Dense factor files and reference spectra (host text, used by the CLI):
+ * dsvd_dense_read/_fetch   <- load_dense_array(path)          matrix_market.cpp:179-213
+ *                             (dims[2] = rows, cols; fetch copies column-major)
+ * dsvd_dense_write         <- write_dense_array(path, a)      :215-223
+ * dsvd_spectrum_read/_fetch<- load_reference_spectrum(path)   metrics.cpp:71-90
+ * dsvd_spectrum_write      <- write_reference_spectrum(path)  :92-97
+ * Errors as the reference: DSVD_PARSE (line), DSVD_FORMAT, DSVD_OTHER (I/O). */
+DSVD_API int dsvd_dense_read(const char* path, int64_t* dims);
+DSVD_API int dsvd_dense_fetch(double* colmajor);
+DSVD_API int dsvd_dense_write(const char* path, int64_t rows, int64_t cols, const double* colmajor);
+DSVD_API int dsvd_spectrum_read(const char* path, int64_t* n);
+DSVD_API int dsvd_spectrum_fetch(double* sigmas);
+DSVD_API int dsvd_spectrum_write(const char* path, const double* sigmas, int64_t n);
 /* R-MAT generator on the device (BASELINE.json configs 4/5; no reference
  * counterpart: the reference ships only sparse_random). Draws `draws` edges of
  * a 2^scale square graph with quadrant probabilities (a, b, c, 1-a-b-c) at

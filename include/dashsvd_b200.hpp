@@ -10,6 +10,7 @@
 // Header-only; needs C++17.
 #pragma once
 
+#include <algorithm>
 #include <cstdint>
 #include <cstring>
 #include <functional>
@@ -42,6 +43,20 @@ struct RankDeficient : Error {
 struct NumericalError : Error {
     using Error::Error;
 };
+struct ParseError : Error {
+    ParseError(std::int64_t line_, const std::string& what_)
+        : Error("parse error at line " + std::to_string(line_) + ": " + what_), line(line_) {}
+    std::int64_t line = 0;
+};
+struct UnsupportedFormat : Error {
+    using Error::Error;
+};
+struct DegenerateReference : Error {
+    using Error::Error;
+};
+struct HypothesisError : Error {
+    using Error::Error;
+};
 
 namespace b200 {
 inline void check(int rc) {
@@ -55,6 +70,10 @@ inline void check(int rc) {
             throw RankDeficient(dsvd_last_error_index(), msg.substr(0, cut));
         }
         case DSVD_NUMERICAL: throw NumericalError(msg);
+        case DSVD_PARSE: throw ParseError(dsvd_last_error_index(), msg);
+        case DSVD_FORMAT: throw UnsupportedFormat(msg);
+        case DSVD_DEGENERATE: throw DegenerateReference(msg);
+        case DSVD_OTHER: throw Error(msg);
         default: throw Error("[dashsvd_b200 status " + std::to_string(rc) + "] " + msg);
     }
 }
@@ -90,6 +109,20 @@ class DenseMatrix {
     const double* col(index_t j) const { return data_.data() + j * rows_; }
     double* data() { return data_.data(); }
     const double* data() const { return data_.data(); }
+    // dense_matrix.cpp:16-27
+    static DenseMatrix from_data(index_t rows, index_t cols, std::vector<double> entries) {
+        if (rows < 0 || cols < 0) throw ShapeError("negative matrix dimension");
+        if (static_cast<index_t>(entries.size()) != rows * cols)
+            throw ShapeError("entry count " + std::to_string(entries.size()) + " does not match " +
+                             std::to_string(rows) + "x" + std::to_string(cols));
+        for (double v : entries)
+            if (!(v - v == 0.0)) throw NumericalError("non-finite entry in dense input");
+        DenseMatrix m;
+        m.rows_ = rows;
+        m.cols_ = cols;
+        m.data_ = std::move(entries);
+        return m;
+    }
 
   private:
     index_t rows_ = 0, cols_ = 0;
@@ -346,6 +379,240 @@ inline DenseMatrix gaussian_matrix(index_t rows, index_t cols, std::uint64_t see
 }
 inline std::uint64_t splitmix64_at(std::uint64_t seed, std::uint64_t i) {
     return dsvd_splitmix64_at(seed, i);
+}
+
+
+// ---- matrix_market.hpp:14-34 (text parsing on the host, assembly / validation on the GPU)
+inline SparseMatrix load_matrix_market(const std::string& path) {
+    dsvd_ctx* ctx = b200::context();
+    int64_t dims[3];
+    b200::check(dsvd_mtx_assemble(ctx, path.c_str(), dims));
+    SparseMatrix a;
+    a.rows = dims[0];
+    a.cols = dims[1];
+    a.offsets.resize(a.rows + 1);
+    a.col_indices.resize(dims[2]);
+    a.values.resize(dims[2]);
+    b200::check(dsvd_coo_fetch(ctx, a.offsets.data(), a.col_indices.data(), a.values.data()));
+    return a;
+}
+inline void write_matrix_market(const std::string& path, const SparseMatrix& a) {
+    b200::check(dsvd_write_matrix_market(path.c_str(), a.rows, a.cols, a.offsets.data(), a.col_indices.data(),
+                                         a.values.data()));
+}
+inline void save_cache(const std::string& path, const SparseMatrix& a) {
+    b200::check(dsvd_save_cache(path.c_str(), a.rows, a.cols, a.nnz(), a.offsets.data(), a.col_indices.data(),
+                                a.values.data()));
+}
+inline DenseMatrix load_dense_array(const std::string& path) {
+    int64_t dims[2];
+    b200::check(dsvd_dense_read(path.c_str(), dims));
+    DenseMatrix d(dims[0], dims[1]);
+    b200::check(dsvd_dense_fetch(d.data()));
+    return d;
+}
+inline void write_dense_array(const std::string& path, const DenseMatrix& a) {
+    b200::check(dsvd_dense_write(path.c_str(), a.rows(), a.cols(), a.data()));
+}
+
+namespace b200 {
+// A CSR(A) + CSR(A^T) pair resident on the GPU: load once, solve / measure many times.
+class DeviceMatrix {
+  public:
+    DeviceMatrix() = default;
+    explicit DeviceMatrix(const SparseMatrix& a) {
+        dsvd_matrix* m = nullptr;
+        check(dsvd_matrix_upload(context(), a.rows, a.cols, a.nnz(), a.offsets.data(), a.col_indices.data(),
+                                 a.values.data(), &m));
+        reset(m, a.rows, a.cols, a.nnz());
+    }
+    // ".dsh" -> load_cache (validated on the device), otherwise Matrix Market
+    // assembled on the device (the CLI's load_input, dashsvd.cpp:78-82)
+    static DeviceMatrix load(const std::string& path) {
+        DeviceMatrix d;
+        dsvd_matrix* m = nullptr;
+        int64_t dims[3];
+        if (path.size() > 4 && path.compare(path.size() - 4, 4, ".dsh") == 0) {
+            check(dsvd_matrix_load_cache(context(), path.c_str(), 1, &m, dims));
+        } else {
+            check(dsvd_mtx_assemble(context(), path.c_str(), dims));
+            check(dsvd_matrix_from_coo(context(), &m));
+        }
+        d.reset(m, dims[0], dims[1], dims[2]);
+        return d;
+    }
+    index_t rows() const { return rows_; }
+    index_t cols() const { return cols_; }
+    index_t nnz() const { return nnz_; }
+    const dsvd_matrix* handle() const { return m_.get(); }
+    SparseMatrix download() const {
+        SparseMatrix a;
+        a.rows = rows_;
+        a.cols = cols_;
+        a.offsets.resize(rows_ + 1);
+        a.col_indices.resize(nnz_);
+        a.values.resize(nnz_);
+        check(dsvd_matrix_download(m_.get(), a.offsets.data(), a.col_indices.data(), a.values.data()));
+        return a;
+    }
+    // solve(a, at, cfg) (solver.cpp:214-223) on the resident pair; `stats`
+    // (optional) receives the device timing breakdown of the call
+    SolveResult solve(const SolverConfig& cfg, dsvd_stats* stats = nullptr) const {
+        if (cfg.orth == Orthonormalizer::qr && cfg.alg != Algorithm::basic)
+            throw ConfigError(
+                "the qr orthonormalizer applies to the basic algorithm only; shifted iterations need "
+                "the surrogate spectrum");
+        dsvd_ctx* ctx = context();
+        const dsvd_config c = to_c(cfg, false);
+        check(dsvd_validate_config(&c, rows_, cols_));
+        const index_t l = cfg.sketch_width();
+        const index_t cap = std::max<index_t>(1, cfg.alg == Algorithm::dash ? cfg.p_max : cfg.p);
+        SolveResult r;
+        r.svd.u = DenseMatrix(rows_, cfg.k);
+        r.svd.s.assign(cfg.k, 0.0);
+        r.svd.v = DenseMatrix(cols_, cfg.k);
+        std::vector<double> alphas(cap), s_hat(static_cast<std::size_t>(cap * l));
+        dsvd_outputs out{};
+        out.u = r.svd.u.data();
+        out.s = r.svd.s.data();
+        out.v = r.svd.v.data();
+        out.alphas = alphas.data();
+        out.s_hat = s_hat.data();
+        out.trace_cap = cap;
+        if (stats) check(dsvd_ctx_set_profiling(ctx, 1));
+        check(dsvd_solve(ctx, m_.get(), &c, &out, nullptr, nullptr));
+        if (stats) check(dsvd_ctx_get_stats(ctx, stats));
+        r.trace.iterations = out.iterations;
+        r.trace.stop_reason = static_cast<StopReason>(out.stop_reason);
+        const bool no_spectrum = cfg.alg == Algorithm::basic && cfg.orth == Orthonormalizer::qr;
+        for (index_t j = 0; j < out.iterations && j < cap; ++j) {
+            r.trace.alphas.push_back(alphas[j]);
+            if (no_spectrum) r.trace.s_hat_history.emplace_back();
+            else r.trace.s_hat_history.emplace_back(s_hat.begin() + j * l, s_hat.begin() + (j + 1) * l);
+        }
+        return r;
+    }
+
+  private:
+    void reset(dsvd_matrix* m, index_t r, index_t c, index_t n) {
+        m_.reset(m, [](dsvd_matrix* p) {
+            if (p) dsvd_matrix_destroy(p);
+        });
+        rows_ = r;
+        cols_ = c;
+        nnz_ = n;
+    }
+    std::shared_ptr<dsvd_matrix> m_;
+    index_t rows_ = 0, cols_ = 0, nnz_ = 0;
+};
+}  // namespace b200
+
+inline SparseMatrix load_cache(const std::string& path) {
+    if (!(path.size() > 4 && path.compare(path.size() - 4, 4, ".dsh") == 0)) {
+        // load_cache does not look at the extension
+        dsvd_matrix* m = nullptr;
+        int64_t dims[3];
+        b200::check(dsvd_matrix_load_cache(b200::context(), path.c_str(), 1, &m, dims));
+        std::unique_ptr<dsvd_matrix, int (*)(dsvd_matrix*)> hold(m, dsvd_matrix_destroy);
+        SparseMatrix a;
+        a.rows = dims[0];
+        a.cols = dims[1];
+        a.offsets.resize(a.rows + 1);
+        a.col_indices.resize(dims[2]);
+        a.values.resize(dims[2]);
+        b200::check(dsvd_matrix_download(m, a.offsets.data(), a.col_indices.data(), a.values.data()));
+        return a;
+    }
+    return b200::DeviceMatrix::load(path).download();
+}
+
+// ---- metrics.hpp:13-69 ---------------------------------------------------------------
+enum class ReferenceSource { oracle, file };
+struct ReferenceSpectrum {
+    std::vector<double> sigmas;
+    ReferenceSource source = ReferenceSource::oracle;
+};
+inline ReferenceSpectrum load_reference_spectrum(const std::string& path) {
+    int64_t n = 0;
+    b200::check(dsvd_spectrum_read(path.c_str(), &n));
+    ReferenceSpectrum r;
+    r.sigmas.resize(n);
+    r.source = ReferenceSource::file;
+    b200::check(dsvd_spectrum_fetch(r.sigmas.data()));
+    return r;
+}
+inline void write_reference_spectrum(const std::string& path, const std::vector<double>& sigmas) {
+    b200::check(dsvd_spectrum_write(path.c_str(), sigmas.data(), static_cast<int64_t>(sigmas.size())));
+}
+inline double eps_pve(const b200::DeviceMatrix& a, const DenseMatrix& u_hat, const ReferenceSpectrum& ref) {
+    double out = 0.0;
+    b200::check(dsvd_eps_pve(b200::context(), a.handle(), u_hat.data(), u_hat.cols(), ref.sigmas.data(),
+                             static_cast<int64_t>(ref.sigmas.size()), &out));
+    return out;
+}
+inline double eps_res(const b200::DeviceMatrix& a, const TruncatedSvd& f, const ReferenceSpectrum& ref) {
+    double out = 0.0;
+    b200::check(dsvd_eps_res(b200::context(), a.handle(), f.u.data(), f.s.data(), f.v.data(), f.rank(),
+                             ref.sigmas.data(), static_cast<int64_t>(ref.sigmas.size()), &out));
+    return out;
+}
+inline double eps_spec(const b200::DeviceMatrix& a, const TruncatedSvd& f, const ReferenceSpectrum& ref,
+                       index_t power_iters = 300, std::uint64_t seed = 0x5eed) {
+    double out = 0.0;
+    b200::check(dsvd_eps_spec(b200::context(), a.handle(), f.u.data(), f.s.data(), f.v.data(), f.rank(),
+                              ref.sigmas.data(), static_cast<int64_t>(ref.sigmas.size()), power_iters, seed,
+                              &out));
+    return out;
+}
+inline double max_triplet_residual(const b200::DeviceMatrix& a, const TruncatedSvd& f) {
+    double out = 0.0;
+    b200::check(dsvd_max_triplet_residual(b200::context(), a.handle(), f.u.data(), f.s.data(), f.v.data(),
+                                          f.rank(), &out));
+    return out;
+}
+inline double eps_pve(const SparseMatrix& a, const DenseMatrix& u_hat, const ReferenceSpectrum& ref) {
+    return eps_pve(b200::DeviceMatrix(a), u_hat, ref);
+}
+inline double eps_res(const SparseMatrix& a, const TruncatedSvd& f, const ReferenceSpectrum& ref) {
+    return eps_res(b200::DeviceMatrix(a), f, ref);
+}
+inline double eps_spec(const SparseMatrix& a, const TruncatedSvd& f, const ReferenceSpectrum& ref,
+                       index_t power_iters = 300, std::uint64_t seed = 0x5eed) {
+    return eps_spec(b200::DeviceMatrix(a), f, ref, power_iters, seed);
+}
+inline double max_triplet_residual(const SparseMatrix& a, const TruncatedSvd& f) {
+    return max_triplet_residual(b200::DeviceMatrix(a), f);
+}
+// metrics.cpp:160-170 (k values; host arithmetic)
+inline double eps_sigma(const std::vector<double>& s_hat, const ReferenceSpectrum& ref) {
+    const index_t k = static_cast<index_t>(s_hat.size());
+    if (k < 1) throw ShapeError("eps_sigma: no singular values supplied");
+    if (static_cast<index_t>(ref.sigmas.size()) < k)
+        throw DegenerateReference("reference provides " + std::to_string(ref.sigmas.size()) +
+                                  " singular values, need " + std::to_string(k));
+    double worst = 0.0;
+    for (index_t i = 0; i < k; ++i) {
+        if (ref.sigmas[i] == 0.0) throw DegenerateReference("sigma_i is zero");
+        const double e = (ref.sigmas[i] - s_hat[i] < 0 ? s_hat[i] - ref.sigmas[i] : ref.sigmas[i] - s_hat[i]) /
+                         ref.sigmas[i];
+        worst = e > worst ? e : worst;
+    }
+    return worst;
+}
+
+// synthetic.hpp:37-38 (sparse_random, generated on the host by the library)
+inline SparseMatrix sparse_random(index_t rows, index_t cols, index_t nnz_per_row, std::uint64_t seed,
+                                  bool row_decay = false) {
+    int64_t nnz = 0;
+    b200::check(dsvd_synth_sparse_random(rows, cols, nnz_per_row, seed, row_decay ? 1 : 0, &nnz));
+    SparseMatrix a;
+    a.rows = rows;
+    a.cols = cols;
+    a.offsets.resize(rows + 1);
+    a.col_indices.resize(nnz);
+    a.values.resize(nnz);
+    b200::check(dsvd_synth_fetch(a.offsets.data(), a.col_indices.data(), a.values.data()));
+    return a;
 }
 
 }  // namespace dashsvd

@@ -117,6 +117,8 @@ SolverConfig make_cfg(int64_t k, int64_t s, int64_t p, double tol, int64_t p_max
 
 SparseMatrix g_rand;  // last sparse_random result, handed out by ref_sparse_random_fetch
 SparseMatrix g_csr;   // last loaded matrix (ref_load_matrix_market / ref_load_cache)
+DenseMatrix g_dense;  // last ref_load_dense_array result
+std::vector<double> g_spec;  // last ref_load_spectrum result
 
 void put_dims(const SparseMatrix& a, int64_t* dims) {
     dims[0] = a.rows;
@@ -333,6 +335,31 @@ int ref_save_cache(const char* path, int64_t rows, int64_t cols, int64_t nnz, co
 int ref_write_matrix_market(const char* path, int64_t rows, int64_t cols, int64_t nnz, const int64_t* off,
                             const int64_t* idx, const double* val) {
     return guarded([&] { write_matrix_market(path, make_csr(rows, cols, nnz, off, idx, val)); });
+}
+
+// load_dense_array / write_dense_array (matrix_market.cpp:179-223)
+int ref_load_dense_array(const char* path, int64_t* dims) {
+    return guarded([&] {
+        g_dense = load_dense_array(path);
+        dims[0] = g_dense.rows();
+        dims[1] = g_dense.cols();
+    });
+}
+void ref_dense_fetch(double* out) { put(g_dense, out); }
+int ref_write_dense_array(const char* path, int64_t rows, int64_t cols, const double* colmajor) {
+    return guarded([&] { write_dense_array(path, make_dense(rows, cols, colmajor)); });
+}
+
+// load_reference_spectrum / write_reference_spectrum (metrics.cpp:71-97)
+int ref_load_spectrum(const char* path, int64_t* n) {
+    return guarded([&] {
+        g_spec = load_reference_spectrum(path).sigmas;
+        *n = static_cast<int64_t>(g_spec.size());
+    });
+}
+void ref_spectrum_fetch(double* out) { std::copy(g_spec.begin(), g_spec.end(), out); }
+int ref_write_spectrum(const char* path, const double* s, int64_t n) {
+    return guarded([&] { write_reference_spectrum(path, std::vector<double>(s, s + n)); });
 }
 
 }  // extern "C"

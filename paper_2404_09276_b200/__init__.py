@@ -6,7 +6,8 @@ The public surface mirrors the reference library's dashsvd:: namespace; see
 ``api`` for the mapping.
 """
 from . import errors
-from .api import (Algorithm, assemble, load_cache, load_matrix_market, read_matrix_market_triplets, save_cache, write_matrix_market, Device, DeviceMatrix, EigenPair, IterationState, Orthonormalizer,
+from .api import (Algorithm, assemble, eps_sigma, load_dense_array, load_reference_spectrum, write_dense_array,
+                  write_reference_spectrum, load_cache, load_matrix_market, read_matrix_market_triplets, save_cache, write_matrix_market, Device, DeviceMatrix, EigenPair, IterationState, Orthonormalizer,
                   ShiftTrace, SolveResult, SolverConfig, SparseMatrix, StopReason, TruncatedSvd,
                   basic_rsvd, comm_unique_id, dash_svd, default_device, eig_svd, eps_pve, eps_res,
                   eps_spec, finalize_row_basis, gaussian_matrix, gram, matmul, max_triplet_residual,

@@ -105,6 +105,12 @@ SIGNATURES = [
     ("dsvd_mtx_read", C.c_int, [C.c_char_p, C.POINTER(I64)]),
     ("dsvd_mtx_fetch", C.c_int, [P, P, P]),
     ("dsvd_write_matrix_market", C.c_int, [C.c_char_p, I64, I64, P, P, P]),
+    ("dsvd_dense_read", C.c_int, [C.c_char_p, C.POINTER(I64)]),
+    ("dsvd_dense_fetch", C.c_int, [P]),
+    ("dsvd_dense_write", C.c_int, [C.c_char_p, I64, I64, P]),
+    ("dsvd_spectrum_read", C.c_int, [C.c_char_p, C.POINTER(I64)]),
+    ("dsvd_spectrum_fetch", C.c_int, [P]),
+    ("dsvd_spectrum_write", C.c_int, [C.c_char_p, P, I64]),
     ("dsvd_max_triplet_residual", C.c_int, [P, P, P, P, P, I64, C.POINTER(D)]),
     ("dsvd_validate_config", C.c_int, [C.POINTER(dsvd_config), I64, I64]),
     ("dsvd_update_shift", D, [D, D]),

@@ -893,3 +893,50 @@ def load_cache(path: str, device: Optional[Device] = None) -> SparseMatrix:
         return m.download()
     finally:
         m.close()
+
+
+def load_dense_array(path: str) -> np.ndarray:
+    """load_dense_array (matrix_market.cpp:179-213): column-major rows x cols array."""
+    dims = (I64 * 2)()
+    check(lib().dsvd_dense_read(_path(path), dims))
+    out = np.empty((dims[0], dims[1]), order="F")
+    check(lib().dsvd_dense_fetch(_ptr(out)))
+    return out
+
+
+def write_dense_array(path: str, a: np.ndarray) -> None:
+    """write_dense_array (matrix_market.cpp:215-223)."""
+    a = np.asfortranarray(a, dtype=np.float64)
+    check(lib().dsvd_dense_write(_path(path), a.shape[0], a.shape[1], _ptr(a)))
+
+
+def load_reference_spectrum(path: str) -> np.ndarray:
+    """load_reference_spectrum (metrics.cpp:71-90): descending singular values."""
+    n = I64()
+    check(lib().dsvd_spectrum_read(_path(path), C.byref(n)))
+    out = np.empty(n.value)
+    check(lib().dsvd_spectrum_fetch(_ptr(out)))
+    return out
+
+
+def write_reference_spectrum(path: str, sigmas) -> None:
+    """write_reference_spectrum (metrics.cpp:92-97)."""
+    s = np.ascontiguousarray(sigmas, dtype=np.float64)
+    check(lib().dsvd_spectrum_write(_path(path), _ptr(s), s.size))
+
+
+def eps_sigma(s_hat, ref) -> float:
+    """metrics.cpp:160-170: worst relative error of the leading k singular values."""
+    s_hat = np.asarray(s_hat, dtype=np.float64)
+    sg = _sig(ref)
+    k = s_hat.size
+    if k < 1:
+        raise E.ShapeError("eps_sigma: no singular values supplied")
+    if sg.size < k:
+        raise E.DegenerateReference(f"reference provides {sg.size} singular values, need {k}")
+    worst = 0.0
+    for i in range(k):
+        if sg[i] == 0.0:
+            raise E.DegenerateReference("sigma_i is zero")
+        worst = max(worst, abs(sg[i] - s_hat[i]) / sg[i])
+    return worst

@@ -1341,6 +1341,53 @@ int dsvd_mtx_fetch(int64_t* r, int64_t* c, double* v) {
     });
 }
 
+namespace {
+thread_local DenseArray t_dense;          // dsvd_dense_read -> dsvd_dense_fetch
+thread_local std::vector<double> t_spec;  // dsvd_spectrum_read -> dsvd_spectrum_fetch
+void raise_mtx(const MtxStatus& stt) {
+    if (stt.code != DSVD_OK) fail(stt.code, stt.what, stt.code == DSVD_PARSE ? stt.line : -1);
+}
+}  // namespace
+
+int dsvd_dense_read(const char* path, int64_t* dims) {
+    return guarded([&] {
+        t_dense = DenseArray{};
+        raise_mtx(dense_read(path, t_dense));
+        dims[0] = t_dense.rows;
+        dims[1] = t_dense.cols;
+    });
+}
+
+int dsvd_dense_fetch(double* colmajor) {
+    return guarded([&] {
+        std::copy(t_dense.data.begin(), t_dense.data.end(), colmajor);
+        t_dense = DenseArray{};
+    });
+}
+
+int dsvd_dense_write(const char* path, int64_t rows, int64_t cols, const double* colmajor) {
+    return guarded([&] { raise_mtx(dense_write(path, rows, cols, colmajor)); });
+}
+
+int dsvd_spectrum_read(const char* path, int64_t* n) {
+    return guarded([&] {
+        t_spec.clear();
+        raise_mtx(spectrum_read(path, t_spec));
+        *n = static_cast<int64_t>(t_spec.size());
+    });
+}
+
+int dsvd_spectrum_fetch(double* sigmas) {
+    return guarded([&] {
+        std::copy(t_spec.begin(), t_spec.end(), sigmas);
+        t_spec.clear();
+    });
+}
+
+int dsvd_spectrum_write(const char* path, const double* sigmas, int64_t n) {
+    return guarded([&] { raise_mtx(spectrum_write(path, sigmas, n)); });
+}
+
 int dsvd_matrix_from_coo(dsvd_ctx* ctx, dsvd_matrix** out) {
     return guarded([&] {
         set_device(ctx);

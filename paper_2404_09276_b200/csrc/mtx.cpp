@@ -140,50 +140,67 @@ struct Lines {
 MtxStatus parse_error(int64_t line, std::string what) { return MtxStatus{DSVD_PARSE, line, std::move(what)}; }
 MtxStatus format_error(std::string what) { return MtxStatus{DSVD_FORMAT, 0, std::move(what)}; }
 
+enum Field { kReal, kInteger, kPattern };
+enum Symmetry { kGeneral, kSymmetric, kSkew };
+struct Header {
+    bool coordinate = true;
+    Field field = kReal;
+    Symmetry sym = kGeneral;
+};
+
+// parse_header (matrix_market.cpp:38-70)
+MtxStatus parse_header(const Cursor& line, Header& h) {
+    std::string banner, object, format, fld, symmetry;
+    Cursor c = line;
+    read_token(c, banner) && read_token(c, object) && read_token(c, format) && read_token(c, fld) &&
+        read_token(c, symmetry);
+    if (banner != "%%MatrixMarket") return parse_error(1, "missing %%MatrixMarket banner");
+    if (lower(object) != "matrix") return format_error("unsupported object: " + object);
+    const std::string fm = lower(format);
+    if (fm == "coordinate") h.coordinate = true;
+    else if (fm == "array") h.coordinate = false;
+    else return format_error("unsupported format: " + format);
+    const std::string fl = lower(fld);
+    if (fl == "real") h.field = kReal;
+    else if (fl == "integer") h.field = kInteger;
+    else if (fl == "pattern") h.field = kPattern;
+    else return format_error("unsupported field: " + fld);
+    const std::string sy = lower(symmetry);
+    if (sy == "general") h.sym = kGeneral;
+    else if (sy == "symmetric") h.sym = kSymmetric;
+    else if (sy == "skew-symmetric") h.sym = kSkew;
+    else return format_error("unsupported symmetry: " + symmetry);
+    return MtxStatus{};
+}
+
+bool read_file(const char* path, std::string& buf) {
+    std::FILE* f = std::fopen(path, "rb");
+    if (!f) return false;
+    char chunk[1 << 16];
+    size_t got;
+    while ((got = std::fread(chunk, 1, sizeof(chunk), f)) > 0) buf.append(chunk, got);
+    std::fclose(f);
+    return true;
+}
+
 }  // namespace
 
 MtxStatus mtx_read(const char* path, MtxTriplets& out) {
-    std::FILE* f = std::fopen(path, "rb");
-    if (!f) return MtxStatus{DSVD_OTHER, 0, std::string("cannot open ") + path};
     std::string buf;
-    {
-        char chunk[1 << 16];
-        size_t got;
-        while ((got = std::fread(chunk, 1, sizeof(chunk), f)) > 0) buf.append(chunk, got);
-        std::fclose(f);
-    }
+    if (!read_file(path, buf)) return MtxStatus{DSVD_OTHER, 0, std::string("cannot open ") + path};
     Lines in{buf.data(), buf.data() + buf.size()};
     Cursor line{};
     if (!in.getline(line)) return parse_error(1, "empty file");
     in.lineno = 1;
     // parse_header (:38-70)
-    enum { kReal, kInteger, kPattern } field = kReal;
-    enum { kGeneral, kSymmetric, kSkew } sym = kGeneral;
+    Header hd;
     {
-        std::string banner, object, format, fld, symmetry;
-        Cursor h = line;
-        read_token(h, banner) && read_token(h, object) && read_token(h, format) && read_token(h, fld) &&
-            read_token(h, symmetry);
-        if (banner != "%%MatrixMarket") return parse_error(1, "missing %%MatrixMarket banner");
-        if (lower(object) != "matrix") return format_error("unsupported object: " + object);
-        const std::string fm = lower(format);
-        bool coordinate;
-        if (fm == "coordinate") coordinate = true;
-        else if (fm == "array") coordinate = false;
-        else return format_error("unsupported format: " + format);
-        const std::string fl = lower(fld);
-        if (fl == "real") field = kReal;
-        else if (fl == "integer") field = kInteger;
-        else if (fl == "pattern") field = kPattern;
-        else return format_error("unsupported field: " + fld);
-        const std::string sy = lower(symmetry);
-        if (sy == "general") sym = kGeneral;
-        else if (sy == "symmetric") sym = kSymmetric;
-        else if (sy == "skew-symmetric") sym = kSkew;
-        else return format_error("unsupported symmetry: " + symmetry);
-        if (!coordinate) return format_error("array format holds a dense matrix; use load_dense_array");
+        const MtxStatus hs = parse_header(line, hd);
+        if (hs.code != DSVD_OK) return hs;
+        if (!hd.coordinate) return format_error("array format holds a dense matrix; use load_dense_array");
     }
-    (void)kInteger;
+    const auto field = hd.field;
+    const auto sym = hd.sym;
     if (!in.next_data(line)) return parse_error(in.lineno + 1, "missing size line");
     int64_t rows, cols, nnz;
     {
@@ -242,6 +259,88 @@ MtxStatus mtx_write(const char* path, int64_t rows, int64_t cols, const int64_t*
     for (int64_t i = 0; i < rows; ++i)
         for (int64_t p = offsets[i]; p < offsets[i + 1]; ++p)
             std::fprintf(f, "%" PRId64 " %" PRId64 " %.17g\n", i + 1, col_indices[p] + 1, values[p]);
+    if (std::fclose(f) != 0) return MtxStatus{DSVD_OTHER, 0, std::string("failed writing ") + path};
+    return MtxStatus{};
+}
+
+MtxStatus dense_read(const char* path, DenseArray& out) {
+    std::string buf;
+    if (!read_file(path, buf)) return MtxStatus{DSVD_OTHER, 0, std::string("cannot open ") + path};
+    Lines in{buf.data(), buf.data() + buf.size()};
+    Cursor line{};
+    if (!in.getline(line)) return parse_error(1, "empty file");
+    in.lineno = 1;
+    Header hd;
+    {
+        const MtxStatus hs = parse_header(line, hd);
+        if (hs.code != DSVD_OK) return hs;
+    }
+    if (hd.coordinate) return format_error("coordinate file; use load_matrix_market");
+    if (hd.field == kPattern) return format_error("pattern array is not a matrix");
+    if (!in.next_data(line)) return parse_error(in.lineno + 1, "missing size line");
+    int64_t rows, cols;
+    {
+        Cursor s = line;
+        if (!(read_int(s, rows) && read_int(s, cols)) || rows < 0 || cols < 0)
+            return parse_error(in.lineno, "size line must be 'rows cols'");
+    }
+    const int64_t total = rows * cols;
+    out.rows = rows;
+    out.cols = cols;
+    out.data.clear();
+    out.data.reserve(static_cast<size_t>(total));
+    while (static_cast<int64_t>(out.data.size()) < total) {
+        if (!in.next_data(line)) return parse_error(in.lineno + 1, "file ended before all entries were read");
+        Cursor s = line;
+        double v;
+        // `while (ss >> v) push; if (!ss.eof()) malformed`: a failed extraction is
+        // fine only when it ran into the end of the line
+        while (read_double(s, v)) out.data.push_back(v);
+        if (s.p != s.end) return parse_error(in.lineno, "malformed value");
+    }
+    if (static_cast<int64_t>(out.data.size()) != total) return parse_error(in.lineno, "more entries than rows*cols");
+    for (double v : out.data)
+        if (!std::isfinite(v)) return parse_error(in.lineno, "non-finite value in array");
+    return MtxStatus{};
+}
+
+MtxStatus dense_write(const char* path, int64_t rows, int64_t cols, const double* colmajor) {
+    std::FILE* f = std::fopen(path, "w");
+    if (!f) return MtxStatus{DSVD_OTHER, 0, std::string("cannot open ") + path + " for writing"};
+    std::fprintf(f, "%%%%MatrixMarket matrix array real general\n");
+    std::fprintf(f, "%" PRId64 " %" PRId64 "\n", rows, cols);
+    for (int64_t e = 0; e < rows * cols; ++e) std::fprintf(f, "%.17g\n", colmajor[e]);
+    if (std::fclose(f) != 0) return MtxStatus{DSVD_OTHER, 0, std::string("failed writing ") + path};
+    return MtxStatus{};
+}
+
+MtxStatus spectrum_read(const char* path, std::vector<double>& out) {
+    std::string buf;
+    if (!read_file(path, buf)) return MtxStatus{DSVD_OTHER, 0, std::string("cannot open ") + path};
+    Lines in{buf.data(), buf.data() + buf.size()};
+    Cursor line{};
+    out.clear();
+    while (in.getline(line)) {
+        ++in.lineno;
+        const char* q = line.p;
+        while (q < line.end && (*q == ' ' || *q == '\t' || *q == '\r')) ++q;
+        if (q == line.end || *q == '#') continue;
+        Cursor s = line;
+        double v;
+        if (!read_double(s, v) || !std::isfinite(v) || v < 0.0)
+            return parse_error(in.lineno, "expected a non-negative singular value");
+        if (!out.empty() && v > out.back() * (1.0 + 1e-12) + 1e-300)
+            return parse_error(in.lineno, "singular values must be non-increasing");
+        out.push_back(v);
+    }
+    if (out.empty()) return parse_error(in.lineno, "no singular values in file");
+    return MtxStatus{};
+}
+
+MtxStatus spectrum_write(const char* path, const double* sigmas, int64_t n) {
+    std::FILE* f = std::fopen(path, "w");
+    if (!f) return MtxStatus{DSVD_OTHER, 0, std::string("cannot open ") + path + " for writing"};
+    for (int64_t i = 0; i < n; ++i) std::fprintf(f, "%.17g\n", sigmas[i]);
     if (std::fclose(f) != 0) return MtxStatus{DSVD_OTHER, 0, std::string("failed writing ") + path};
     return MtxStatus{};
 }

@@ -311,6 +311,29 @@ class Reference(_Lib):
         self.check(self.f("save_cache", C.c_int, C.c_char_p, _I64, _I64, _I64, _P, _P, _P)(os.fsencode(path),
                                                                                        *self._a(a)))
 
+    def load_dense_array(self, path):
+        dims = (_I64 * 2)()
+        self.check(self.f("load_dense_array", C.c_int, C.c_char_p, _P)(os.fsencode(path), dims))
+        out = np.empty((dims[0], dims[1]), order="F")
+        self.f("dense_fetch", None, _P)(_ptr(out))
+        return out
+
+    def write_dense_array(self, path, a):
+        a = np.asfortranarray(a, dtype=np.float64)
+        self.check(self.f("write_dense_array", C.c_int, C.c_char_p, _I64, _I64, _P)(os.fsencode(path), a.shape[0],
+                                                                                 a.shape[1], _ptr(a)))
+
+    def load_spectrum(self, path):
+        n = _I64()
+        self.check(self.f("load_spectrum", C.c_int, C.c_char_p, C.POINTER(_I64))(os.fsencode(path), C.byref(n)))
+        out = np.empty(n.value)
+        self.f("spectrum_fetch", None, _P)(_ptr(out))
+        return out
+
+    def write_spectrum(self, path, s):
+        s = np.ascontiguousarray(s, dtype=np.float64)
+        self.check(self.f("write_spectrum", C.c_int, C.c_char_p, _P, _I64)(os.fsencode(path), _ptr(s), s.size))
+
     def write_matrix_market(self, path, a: Csr):
         self.check(self.f("write_matrix_market", C.c_int, C.c_char_p, _I64, _I64, _I64, _P, _P, _P)(
             os.fsencode(path), *self._a(a)))

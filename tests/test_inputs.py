@@ -127,3 +127,80 @@ def test_write_then_parse_round_trip(tmp_path):
     assert b.offsets.tolist() == a.offsets.tolist()
     assert b.col_indices.tolist() == a.col_indices.tolist()
     assert b.values.view(np.uint64).tolist() == a.values.view(np.uint64).tolist()
+
+
+# ---- dense factor files and reference spectra (CLI inputs) -----------------------------
+
+DENSE_CASES = {
+    "ok_one_per_line": "%%MatrixMarket matrix array real general\n2 2\n1\n2\n3\n4\n",
+    "ok_many_per_line": "%%MatrixMarket matrix array real general\n% c\n2 3\n1 2 3\n\n4 5 6\n",
+    "ok_trailing_ws_crlf": "%%MatrixMarket matrix array real general\r\n1 2\r\n1.5  \r\n-2e3\t\r\n",
+    "ok_integer_field": "%%MatrixMarket matrix array integer general\n1 1\n7\n",
+    "ok_empty": "%%MatrixMarket matrix array real general\n0 3\n",
+    "ok_overflow_at_line_end": "%%MatrixMarket matrix array real general\n1 2\n1e999\n1\n2\n",
+    "malformed_word": "%%MatrixMarket matrix array real general\n2 2\n1.0\n2.0\nnope\n4.0\n",
+    "malformed_suffix": "%%MatrixMarket matrix array real general\n1 2\n1.5x 2\n",
+    "malformed_overflow_mid": "%%MatrixMarket matrix array real general\n1 2\n1e999 2\n",
+    "too_many": "%%MatrixMarket matrix array real general\n1 2\n1 2 3\n",
+    "too_few": "%%MatrixMarket matrix array real general\n2 2\n1 2 3\n",
+    "bad_size": "%%MatrixMarket matrix array real general\n2\n1\n",
+    "negative_size": "%%MatrixMarket matrix array real general\n-1 2\n",
+    "missing_size": "%%MatrixMarket matrix array real general\n% only\n",
+    "coordinate": "%%MatrixMarket matrix coordinate real general\n1 1 1\n1 1 1.0\n",
+    "pattern": "%%MatrixMarket matrix array pattern general\n1 1\n",
+    "bad_banner": "%MatrixMarket matrix array real general\n1 1\n1\n",
+    "empty": "",
+}
+
+SPECTRUM_CASES = {
+    "ok": "3\n2.5\n1\n",
+    "ok_comments": "# exact\n\n  5 trailing words ignored\n\t# x\n4\n4\n0\n",
+    "ok_tolerance": "1\n1.0000000000005\n",
+    "increasing": "1\n2\n",
+    "negative": "1\n-0.5\n",
+    "word": "1\nabc\n",
+    "empty": "# nothing\n\n",
+    "inf_text": "inf\n",
+}
+
+
+def _dense_outcome(fn):
+    try:
+        a = fn()
+    except E.ParseError as e:
+        return ("ParseError", e.line, str(e))
+    except E.Error as e:
+        return (type(e).__name__, str(e))
+    return ("ok", a.shape, np.asarray(a).ravel(order="F").tobytes())
+
+
+@pytest.mark.parametrize("name", sorted(DENSE_CASES))
+def test_dense_array_parser_matches_reference(tmp_path, reference, name):
+    p = tmp_path / "d.mtx"
+    with open(p, "w", newline="") as f:
+        f.write(DENSE_CASES[name])
+    assert _dense_outcome(lambda: d.load_dense_array(str(p))) == \
+        _dense_outcome(lambda: reference.load_dense_array(str(p)))
+
+
+@pytest.mark.parametrize("name", sorted(SPECTRUM_CASES))
+def test_spectrum_parser_matches_reference(tmp_path, reference, name):
+    p = tmp_path / "s.txt"
+    p.write_text(SPECTRUM_CASES[name])
+    assert _dense_outcome(lambda: d.load_reference_spectrum(str(p))) == \
+        _dense_outcome(lambda: reference.load_spectrum(str(p)))
+
+
+def test_dense_and_spectrum_writers_match_reference(tmp_path, reference):
+    rng = np.random.default_rng(9)
+    a = np.asfortranarray(rng.standard_normal((7, 3)) * 10.0 ** rng.integers(-200, 200, (7, 3)))
+    d.write_dense_array(str(tmp_path / "o.mtx"), a)
+    reference.write_dense_array(str(tmp_path / "r.mtx"), a)
+    assert (tmp_path / "o.mtx").read_bytes() == (tmp_path / "r.mtx").read_bytes()
+    assert np.array_equal(d.load_dense_array(str(tmp_path / "o.mtx")), a)
+    s = np.sort(np.abs(rng.standard_normal(9)))[::-1]
+    d.write_reference_spectrum(str(tmp_path / "o.txt"), s)
+    reference.write_spectrum(str(tmp_path / "r.txt"), s)
+    assert (tmp_path / "o.txt").read_bytes() == (tmp_path / "r.txt").read_bytes()
+    assert np.array_equal(d.load_reference_spectrum(str(tmp_path / "o.txt")), s)
+    assert d.eps_sigma(s[:4] * (1 + 1e-9), s) == pytest.approx(1e-9, rel=1e-6)
