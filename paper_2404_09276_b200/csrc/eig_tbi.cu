@@ -240,6 +240,138 @@ tbi_tridiag_kernel(const double* __restrict__ g, int n, double* __restrict__ d, 
     }
 }
 
+// Wide variant (n > kTridSmemMaxN, up to 320): A no longer fits in shared
+// memory, so the full symmetric matrix lives in global memory (L2-resident,
+// 0.8 MB at n = 320), element (i, j) at A[j * n + i], and every access is
+// lane-per-row, i.e. coalesced. Same three phases per step with 32 warps:
+// B (reflector on warp 0, p = A22 x on the rest: 32-row groups x column
+// chunks, eight loads in flight per lane), C1 (v, w, K), C2 (the symmetric
+// rank-2 update A22 -= v u^T + u v^T, u = w - K v, on all m x m entries with
+// the two products added before the subtraction, so A stays exactly
+// symmetric).
+constexpr int kTridBigThreads = 1024;
+constexpr int kTridBigWarps = kTridBigThreads / 32;
+
+__global__ void __launch_bounds__(kTridBigThreads, 1)
+tbi_tridiag_big_kernel(const double* __restrict__ g, int n, double* __restrict__ A, double* __restrict__ d,
+                       double* __restrict__ e, double* __restrict__ hv, double* __restrict__ tau_out,
+                       const int32_t* __restrict__ gate, const int32_t* __restrict__ skip) {
+    if ((gate != nullptr && *gate != 0) || (skip != nullptr && *skip != 0)) return;
+    extern __shared__ __align__(16) double tbm[];
+    double2* vw = reinterpret_cast<double2*>(tbm);     // n: (v_i, u_i)
+    double* xk = tbm + 2 * n;                          // n: column k (x)
+    double* part = xk + n;                             // (kTridBigWarps - 1) x n matvec partials
+    __shared__ Reflector s_ref;
+    __shared__ double s_ksum[kTridBigWarps];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (int x = tid; x < n * n; x += blockDim.x) A[x] = g[x];  // g row-major symmetric: same layout
+    __syncthreads();
+    for (int k = 0; k + 2 < n; ++k) {
+        const int k1 = k + 1, m = n - k1;
+        const int G = (m + 31) >> 5;
+        const int C = min((kTridBigWarps - 1) / G, max(1, (m + 15) / 16));
+        for (int j = k1 + tid; j < n; j += blockDim.x) xk[j] = A[k * n + j];
+        __syncthreads();
+        // ---- B ----
+        if (warp == 0) {
+            double sig = 0.0;
+            for (int i = k1 + lane; i < n; i += 32) sig = fma(xk[i], xk[i], sig);
+            sig = warp_sum(sig);
+            if (lane == 0) {
+                Reflector r;
+                r.x0 = xk[k1];
+                r.alpha = r.x0;
+                r.tau = 0.0;
+                r.v0 = r.x0;
+                const double tail = sig - r.x0 * r.x0;
+                if (tail > 0.0) {
+                    r.alpha = -copysign(sqrt(sig), r.x0);
+                    r.v0 = r.x0 - r.alpha;
+                    r.tau = 2.0 / (tail + r.v0 * r.v0);
+                }
+                s_ref = r;
+                tau_out[k] = r.tau;
+                e[k] = r.alpha;
+                d[k] = A[k * n + k];
+            }
+        } else {
+            const int item = warp - 1, grp = item % G, c = item / G;
+            if (c < C) {
+                const int i = k1 + 32 * grp + lane;
+                const int len = (m + C - 1) / C;
+                const int j0 = k1 + c * len, j1 = min(n, j0 + len);
+                double acc[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) acc[u] = 0.0;
+                if (i < n) {
+                    int j = j0;
+                    for (; j + 7 < j1; j += 8) {
+                        double a[8];
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) a[u] = A[(j + u) * n + i];
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) acc[u] = fma(a[u], xk[j + u], acc[u]);
+                    }
+                    for (; j < j1; ++j) acc[0] = fma(A[j * n + i], xk[j], acc[0]);
+                    part[c * n + i] = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
+                }
+            }
+        }
+        __syncthreads();
+        // ---- C1 ----
+        const Reflector ref = s_ref;
+        {
+            double t = 0.0;
+            if (tid < m) {
+                const int i = k1 + tid;
+                double p = 0.0;
+                for (int c = 0; c < C; ++c) p += part[c * n + i];
+                p = fma(ref.v0 - ref.x0, A[k1 * n + i], p);  // x -> v: first entry v0
+                const double vi = i == k1 ? ref.v0 : xk[i];
+                const double wi = ref.tau * p;
+                vw[i] = make_double2(vi, wi);
+                hv[static_cast<int64_t>(k) * n + i] = vi;
+                t = wi * vi;
+            }
+            if (warp < G) {
+                t = warp_sum(t);
+                if (lane == 0) s_ksum[warp] = t;
+            }
+        }
+        __syncthreads();
+        // ---- C2: A22 -= v u^T + u v^T, u = w - (tau K / 2) v -------------------------
+        {
+            double ks = 0.0;
+            for (int q = 0; q < G; ++q) ks += s_ksum[q];
+            const double hk = 0.5 * ref.tau * ks;
+            const int ntile = G * G;
+            for (int tile = warp; tile < ntile; tile += kTridBigWarps) {
+                const int gr = tile % G, gc = tile / G;
+                const int i = k1 + 32 * gr + lane;
+                if (i >= n) continue;
+                const double2 pi = vw[i];
+                const double vi = pi.x, ui = fma(-hk, pi.x, pi.y);
+                const int jb = k1 + 32 * gc, je = min(jb + 32, n);
+                for (int j = jb; j < je; ++j) {
+                    const double2 q = vw[j];
+                    const double uj = fma(-hk, q.x, q.y);
+                    A[j * n + i] -= vi * uj + ui * q.x;
+                }
+            }
+        }
+        __syncthreads();
+    }
+    if (tid == 0) {
+        if (n >= 2) {
+            d[n - 2] = A[(n - 2) * n + (n - 2)];
+            e[n - 2] = A[(n - 2) * n + (n - 1)];
+        }
+        d[n - 1] = A[(n - 1) * n + (n - 1)];
+    }
+}
+
+size_t tridiag_big_smem_bytes(int n) { return sizeof(double) * (3 * static_cast<size_t>(n) + (kTridBigWarps - 1) * static_cast<size_t>(n)); }
+
 size_t tridiag_smem_bytes(int n) {
     const size_t lda = n | 1;
     return sizeof(double) * (n * lda + 1 + 2 * n + (kTridWarps - 1) * static_cast<size_t>(n));
@@ -519,33 +651,38 @@ tbi_eig_kernel(const double* __restrict__ dg, const double* __restrict__ eg, int
 // mode 1: C = (3I - A^T B) / 2 (the polar step's S). The operand layout:
 // A(t, i) = trans_a ? a[t * n + i] : a[i * n + t], B(t, j) = b[t * n + j].
 constexpr int kNsTile = 16;
-constexpr int kNsMaxN = 160;
+constexpr int kNsChunk = 160;  // t-panel staged per pass (n <= 160: one pass)
+constexpr int kNsMaxN = 320;
 
 __global__ void __launch_bounds__(kNsTile * kNsTile)
 tbi_ns_kernel(const double* __restrict__ a, int trans_a, const double* __restrict__ b, double* __restrict__ c,
               int n, int mode, const int32_t* __restrict__ gate, const int32_t* __restrict__ skip) {
     if ((gate != nullptr && *gate != 0) || (skip != nullptr && *skip != 0)) return;
-    __shared__ double as[kNsMaxN][kNsTile + 1];
-    __shared__ double bs[kNsMaxN][kNsTile];
+    __shared__ double as[kNsChunk][kNsTile + 1];
+    __shared__ double bs[kNsChunk][kNsTile];
     const int i0 = blockIdx.y * kNsTile, j0 = blockIdx.x * kNsTile, tid = threadIdx.x;
-    for (int x = tid; x < n * kNsTile; x += blockDim.x) {
-        int t, ii;
-        if (trans_a) { t = x / kNsTile; ii = x % kNsTile; }
-        else { ii = x / n; t = x % n; }
-        const int i = i0 + ii;
-        as[t][ii] = i < n ? (trans_a ? a[t * n + i] : a[i * n + t]) : 0.0;
-        const int tb = x / kNsTile, jj = x % kNsTile, j = j0 + jj;
-        bs[tb][jj] = j < n ? b[tb * n + j] : 0.0;
-    }
-    __syncthreads();
     const int ty = tid / kNsTile, tx = tid % kNsTile;
     double a0 = 0.0, a1 = 0.0;
-    int t = 0;
-    for (; t + 1 < n; t += 2) {
-        a0 = fma(as[t][ty], bs[t][tx], a0);
-        a1 = fma(as[t + 1][ty], bs[t + 1][tx], a1);
+    for (int t0 = 0; t0 < n; t0 += kNsChunk) {
+        const int tn = min(kNsChunk, n - t0);
+        if (t0 > 0) __syncthreads();
+        for (int x = tid; x < tn * kNsTile; x += blockDim.x) {
+            int t, ii;
+            if (trans_a) { t = x / kNsTile; ii = x % kNsTile; }
+            else { ii = x / tn; t = x % tn; }
+            const int i = i0 + ii;
+            as[t][ii] = i < n ? (trans_a ? a[(t0 + t) * n + i] : a[i * n + t0 + t]) : 0.0;
+            const int tb = x / kNsTile, jj = x % kNsTile, j = j0 + jj;
+            bs[tb][jj] = j < n ? b[(t0 + tb) * n + j] : 0.0;
+        }
+        __syncthreads();
+        int t = 0;
+        for (; t + 1 < tn; t += 2) {
+            a0 = fma(as[t][ty], bs[t][tx], a0);
+            a1 = fma(as[t + 1][ty], bs[t + 1][tx], a1);
+        }
+        if (t < tn) a0 = fma(as[t][ty], bs[t][tx], a0);
     }
-    if (t < n) a0 = fma(as[t][ty], bs[t][tx], a0);
     const int i = i0 + ty, j = j0 + tx;
     if (i < n && j < n) {
         const double acc = a0 + a1;
@@ -557,46 +694,54 @@ tbi_ns_kernel(const double* __restrict__ a, int trans_a, const double* __restric
 // The column lives in registers (lane owns rows lane + 32q); the reflectors are
 // staged in shared memory once per CTA.
 constexpr int kBtWarps = 8;
-constexpr int kBtRegs = (kNsMaxN + 31) / 32;
 
-__global__ void __launch_bounds__(32 * kBtWarps, 1)
+// R: registers per lane (n <= 32 R); SMEM: reflectors staged in shared memory
+// (n <= 160) or read from global / L2 (wider n, 0.8 MB of reflectors at 320)
+template <int R, bool SMEM>
+__global__ void __launch_bounds__(32 * kBtWarps)
 tbi_backtransform_kernel(const double* __restrict__ hv, const double* __restrict__ tau,
                          const double* __restrict__ z, int n, int ldz, double* __restrict__ vecs, int ldv,
                          const int32_t* __restrict__ gate, const int32_t* __restrict__ skip) {
     if ((gate != nullptr && *gate != 0) || (skip != nullptr && *skip != 0)) return;
     extern __shared__ double bsm[];
-    double* H = bsm;                              // all reflectors, n x n (row k = v_k)
-    double* T = H + static_cast<size_t>(n) * n;   // tau, n
+    const double* H = hv;  // all reflectors, n x n (row k = v_k)
+    const double* T = tau;
+    if (SMEM) {
+        double* Hs = bsm;
+        double* Ts = Hs + static_cast<size_t>(n) * n;
+        load_square(Hs, n, hv, n, n);
+        for (int x = threadIdx.x; x < n; x += blockDim.x) Ts[x] = tau[x];
+        H = Hs;
+        T = Ts;
+    }
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    load_square(H, n, hv, n, n);
-    for (int x = threadIdx.x; x < n; x += blockDim.x) T[x] = tau[x];
     const int col = blockIdx.x * kBtWarps + warp;
-    double x[kBtRegs];
+    double x[R];
 #pragma unroll
-    for (int q = 0; q < kBtRegs; ++q) {
+    for (int q = 0; q < R; ++q) {
         const int i = lane + 32 * q;
         x[q] = (col < n && i < n) ? z[static_cast<int64_t>(i) * ldz + col] : 0.0;
     }
-    __syncthreads();
+    if (SMEM) __syncthreads();
     if (col >= n) return;
     for (int k = n - 3; k >= 0; --k) {
         const double t = T[k];
         if (t == 0.0) continue;
         const double* vk = H + static_cast<size_t>(k) * n;
-        double vr[kBtRegs];
+        double vr[R];
         double s = 0.0;
 #pragma unroll
-        for (int q = 0; q < kBtRegs; ++q) {
+        for (int q = 0; q < R; ++q) {
             const int i = lane + 32 * q;
             vr[q] = (i > k && i < n) ? vk[i] : 0.0;
             s = fma(vr[q], x[q], s);
         }
         s = warp_sum(s) * t;
 #pragma unroll
-        for (int q = 0; q < kBtRegs; ++q) x[q] = fma(-s, vr[q], x[q]);
+        for (int q = 0; q < R; ++q) x[q] = fma(-s, vr[q], x[q]);
     }
 #pragma unroll
-    for (int q = 0; q < kBtRegs; ++q) {
+    for (int q = 0; q < R; ++q) {
         const int i = lane + 32 * q;
         if (i < n) vecs[static_cast<int64_t>(i) * ldv + col] = x[q];
     }
@@ -606,11 +751,14 @@ __global__ void tbi_clear_kernel(int32_t* flag) { *flag = 0; }
 
 }  // namespace
 
-bool tbi_supported(int l) { return l >= 3 && l <= 160; }
+constexpr int kTridSmemMaxN = 160;  // tbi_tridiag_kernel / the staged back-transform
+
+bool tbi_supported(int l) { return l >= 3 && l <= kNsMaxN; }
 
 size_t tbi_workspace_bytes(int l) {
     const size_t n = l;
-    return sizeof(double) * (n * n /*hv*/ + n /*tau*/ + 2 * n /*d,e*/ + 3 * n * n /*z, S, z2*/) +
+    return sizeof(double) * (n * n /*hv*/ + n /*tau*/ + 2 * n /*d,e*/ + 3 * n * n /*z, S, z2*/ +
+                             (l > kTridSmemMaxN ? n * n : 0) /*A for the wide tridiagonalisation*/) +
            sizeof(int32_t) * kGridPts /*count grid*/ + 64;
 }
 
@@ -628,12 +776,20 @@ void tbi_eig(const double* g, EigWorkspace& w, void* tbi_ws, int32_t* clustered,
     double* z2 = S + static_cast<size_t>(n) * n;
     tbi_clear_kernel<<<1, 1, 0, stream>>>(clustered);
     DSVD_LAUNCH_CHECK();
-    const size_t s1 = tridiag_smem_bytes(n);
-    DSVD_CUDA_CHECK(cudaFuncSetAttribute(tbi_tridiag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(s1)));
-    tbi_tridiag_kernel<<<1, kTridThreads, s1, stream>>>(g, n, d, e, hv, tau, gate, nullptr);
-    DSVD_LAUNCH_CHECK();
     int32_t* counts = reinterpret_cast<int32_t*>(z2 + static_cast<size_t>(n) * n);
+    if (n <= kTridSmemMaxN) {
+        const size_t s1 = tridiag_smem_bytes(n);
+        DSVD_CUDA_CHECK(cudaFuncSetAttribute(tbi_tridiag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             static_cast<int>(s1)));
+        tbi_tridiag_kernel<<<1, kTridThreads, s1, stream>>>(g, n, d, e, hv, tau, gate, nullptr);
+    } else {
+        double* Aw = reinterpret_cast<double*>(counts + kGridPts);  // n x n, after the count grid
+        const size_t s1 = tridiag_big_smem_bytes(n);
+        DSVD_CUDA_CHECK(cudaFuncSetAttribute(tbi_tridiag_big_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             static_cast<int>(s1)));
+        tbi_tridiag_big_kernel<<<1, kTridBigThreads, s1, stream>>>(g, n, Aw, d, e, hv, tau, gate, nullptr);
+    }
+    DSVD_LAUNCH_CHECK();
     tbi_grid_kernel<<<kGridPts / 512, 256, sizeof(double) * 3 * n, stream>>>(d, e, n, counts, gate, nullptr);
     DSVD_LAUNCH_CHECK();
     const size_t s2 = sizeof(double) * (3 * static_cast<size_t>(n) + kTbiWarps * 3 * static_cast<size_t>(n));
@@ -651,11 +807,17 @@ void tbi_eig(const double* g, EigWorkspace& w, void* tbi_ws, int32_t* clustered,
         tbi_ns_kernel<<<ns_grid, kNsTile * kNsTile, 0, stream>>>(zi, 0, S, zo, n, 0, gate, clustered);
         DSVD_LAUNCH_CHECK();
     }
-    const size_t s4 = sizeof(double) * (static_cast<size_t>(n) * n + n);
-    DSVD_CUDA_CHECK(cudaFuncSetAttribute(tbi_backtransform_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(s4)));
-    tbi_backtransform_kernel<<<static_cast<unsigned>(ceil_div(n, kBtWarps)), 32 * kBtWarps, s4, stream>>>(
-        hv, tau, z, n, n, w.vecs, w.lp, gate, clustered);
+    const unsigned bt_grid = static_cast<unsigned>(ceil_div(n, kBtWarps));
+    if (n <= kTridSmemMaxN) {
+        const size_t s4 = sizeof(double) * (static_cast<size_t>(n) * n + n);
+        DSVD_CUDA_CHECK(cudaFuncSetAttribute(tbi_backtransform_kernel<5, true>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(s4)));
+        tbi_backtransform_kernel<5, true><<<bt_grid, 32 * kBtWarps, s4, stream>>>(hv, tau, z, n, n, w.vecs, w.lp,
+                                                                                  gate, clustered);
+    } else {
+        tbi_backtransform_kernel<10, false><<<bt_grid, 32 * kBtWarps, 0, stream>>>(hv, tau, z, n, n, w.vecs, w.lp,
+                                                                                   gate, clustered);
+    }
     DSVD_LAUNCH_CHECK();
 }
 

@@ -321,7 +321,7 @@ def test_matmul_bitwise(dev, oracle, shape):
     assert_bitwise(d.matmul(a, b, device=dev), oracle.matmul(a, b))
 
 
-@pytest.mark.parametrize("n", [1, 2, 3, 20, 75, 150, 300])
+@pytest.mark.parametrize("n", [1, 2, 3, 20, 75, 150, 161, 200, 257, 300, 320])
 def test_sym_eig_matches_oracle(dev, oracle, n):
     g0 = np.random.default_rng(n).standard_normal((n, n))
     g = np.asfortranarray(g0 + g0.T)
@@ -408,7 +408,8 @@ def eig_dev(request):
     dv.close()
 
 
-@pytest.mark.parametrize("shape", [(10000, 75), (5000, 150), (2000, 300), (400, 3), (900, 64)])
+@pytest.mark.parametrize("shape", [(10000, 75), (5000, 150), (2000, 300), (400, 3), (900, 64), (3000, 200),
+                                   (4000, 320)])
 def test_eig_svd_matches_oracle(eig_dev, oracle, shape):
     c = np.asfortranarray(np.random.default_rng(shape[0]).standard_normal(shape))
     u_ref, s_ref, v_ref = oracle.eig_svd(c)
