@@ -29,7 +29,13 @@ namespace dsvd {
 
 namespace {
 
-constexpr double kTbiGap = 1e-9;  // minimum relative eigenvalue gap for inverse iteration
+// Minimum eigenvalue gap (relative to ||T||) for the twisted-factorisation
+// vectors: a pair closer than gap has its two vectors accurate only to an angle
+// ~ eps / gap inside the pair's 2-D eigenspace; at 1e-12 that is ~1e-4, which
+// the two Newton-Schulz steps remove (1e-4 -> 1e-8 -> 1e-16), and the mixing
+// inside the pair changes the factorisation by ~angle x gap ~ 1e-16 ||T||.
+// Tighter clusters (e.g. repeated eigenvalues) take the Jacobi fallback.
+constexpr double kTbiGap = 1e-12;
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll

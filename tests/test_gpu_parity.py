@@ -361,6 +361,28 @@ def test_eig_svd_clustered_spectrum_falls_back(eig_dev):
     np.testing.assert_allclose((f.u * f.s) @ f.v.T, c, atol=1e-11)
 
 
+@pytest.mark.parametrize("gap", [1e-9, 1e-10, 1e-11, 3e-12])
+def test_eig_svd_close_pairs_stay_accurate(dev, oracle, gap):
+    # nearly repeated pairs (relative gaps 1e-9 .. 3e-12, as the R-MAT Gram
+    # matrices of C4 have): the tridiagonal path keeps them (no fallback above
+    # 1e-12) and the factors stay orthonormal and accurate
+    rng = np.random.default_rng(int(-np.log10(gap) * 10))
+    n, l = 3000, 200
+    q, _ = np.linalg.qr(rng.standard_normal((n, l)))
+    w, _ = np.linalg.qr(rng.standard_normal((l, l)))
+    sv = np.sort(rng.uniform(1.0, 10.0, l))[::-1]
+    for i in range(0, 40, 4):  # ten pairs whose squares differ by gap * sigma_1^2
+        sv[i + 1] = np.sqrt(sv[i] ** 2 - gap * sv[0] ** 2)
+    c = np.asfortranarray((q * sv) @ w.T)
+    f = d.eig_svd(c, device=dev)
+    u_ref, s_ref, v_ref = oracle.eig_svd(c)
+    # eigenvalues of the Gram to ~l eps ||G||: sigma to ~1e-12 relative at sigma_1 / sigma_l = 10
+    np.testing.assert_allclose(f.s, s_ref, rtol=1e-11)
+    np.testing.assert_allclose(f.v.T @ f.v, np.eye(l), atol=1e-12)
+    np.testing.assert_allclose(f.u.T @ f.u, np.eye(l), atol=1e-10)
+    np.testing.assert_allclose((f.u * f.s) @ f.v.T, c, atol=1e-11 * sv[0])
+
+
 def test_solve_config1_both_eigensolvers(oracle, c1, eig_dev):
     ref = oracle.solve(c1, 50, 25, tol=1e-2, alg="dash", seed=0)
     res = d.solve(to_dev(c1), d.SolverConfig(k=50, s=25, tol=1e-2, seed=0), device=eig_dev)
