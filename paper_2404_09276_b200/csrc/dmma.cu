@@ -445,7 +445,7 @@ gram_dmma_reduce_kernel(const double* __restrict__ partial, int nblk, int nb, in
 // warps), staging only the columns of its two groups. blockIdx.x (the group
 // pair) varies fastest so the CTAs of one slab share the slab in L2. Same
 // partial layout as gram_dmma_kernel (one triangle of 8x8 blocks per slab).
-constexpr int kGwRows = 16, kGwStages = 4, kGwStride = 264;  // 2 * 264 == 16 (mod 32) banks
+constexpr int kGwRows = 32, kGwStages = 3, kGwStride = 264;  // 2 * 264 == 16 (mod 32) banks
 
 __global__ void __launch_bounds__(512, 1)
 gram_dmma_wide_kernel(const double* __restrict__ c, int64_t n, int64_t ld, int nb, int64_t rows_per_block,
@@ -467,14 +467,20 @@ gram_dmma_wide_kernel(const double* __restrict__ c, int64_t n, int64_t ld, int n
     const int64_t r_end = min(n, r_beg + rows_per_block);
     const int64_t c0a = 128 * a, c0b = 128 * b;
     const bool same = a == b;
-    auto stage = [&](int slot, int64_t rr0) {  // 16 rows x (64 + 64) 16-byte chunks
-        double* dst = wsm + slot * kGwRows * kGwStride;
-        for (int e = tid; e < kGwRows * 128; e += 512) {
-            const int r = e >> 7, ch = e & 127;
-            const int64_t gr = rr0 + r;
-            const int64_t col = (ch < 64 ? c0a : c0b) + 2 * (ch & 63);
-            const bool ok = gr < r_end && col < ld && (ch < 64 || !same);
-            cpa16z(dst + r * kGwStride + 2 * ch, ok ? c + gr * ld + col : c, ok);
+    // staging: 16 rows x (64 + 64) 16-byte chunks per stage, four per thread at
+    // rows (tid >> 7) + 4u of one fixed chunk, so the addresses are set up once
+    const int ch = tid & 127, r0t = tid >> 7;
+    const int64_t col = (ch < 64 ? c0a : c0b) + 2 * (ch & 63);
+    const bool col_ok = col < ld && (ch < 64 || !same);
+    const double* src0 = c + (col_ok ? col : 0);
+    double* dst0 = wsm + r0t * kGwStride + 2 * ch;
+    auto stage = [&](int slot, int64_t rr0) {
+        double* dst = dst0 + slot * kGwRows * kGwStride;
+#pragma unroll
+        for (int u = 0; u < kGwRows / 4; ++u) {
+            const int64_t gr = rr0 + r0t + 4 * u;
+            const bool ok = col_ok && gr < r_end;
+            cpa16z(dst + 4 * u * kGwStride, ok ? src0 + gr * ld : c, ok);
         }
     };
     const int nst = static_cast<int>(((r_end > r_beg ? r_end - r_beg : int64_t(0)) + kGwRows - 1) / kGwRows);
@@ -544,10 +550,12 @@ GramDmmaPlan gram_dmma_plan(int64_t n, int64_t l) {
     GramDmmaPlan p;
     p.nb = static_cast<int>((l + 7) / 8);
     if (p.nb > kGramNarrowMaxNb) {
-        // wide: group pairs x slabs, ~2 waves of one CTA per SM
+        // wide: group pairs x slabs. The pairs carry unequal tile counts (a
+        // diagonal pair 10 of 16, an edge pair as few as 1), so ~12 waves of
+        // one CTA per SM let the block scheduler even the load out
         const int ngrp = (p.nb + 15) / 16, npairs = ngrp * (ngrp + 1) / 2;
         p.nblk = static_cast<int>(std::max<int64_t>(
-            1, std::min<int64_t>(ceil_div(2 * kNumSMs, npairs), ceil_div(n, 4 * kGwRows))));
+            1, std::min<int64_t>(ceil_div(12 * kNumSMs, npairs), ceil_div(n, 16 * kGwRows))));
         p.rpb = ceil_div(ceil_div(n, p.nblk), kGwRows) * kGwRows;
         p.nblk = static_cast<int>(std::max<int64_t>(1, ceil_div(n, p.rpb)));
         return p;

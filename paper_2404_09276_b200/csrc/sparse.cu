@@ -233,6 +233,118 @@ spmm_row_kernel(const int64_t* __restrict__ off, const int32_t* __restrict__ idx
     if (act2) *reinterpret_cast<double2*>(yr + 128 + 2 * lane) = make_double2(acc[4], acc[5]);
 }
 
+// Whole-row kernel for 192 < ld <= 320 (C4's l = 300): lane L owns columns
+// [8L, 8L+8) (two 256-bit loads per nonzero) and [256+2L, 256+2L+2) (a
+// 128-bit load, lanes with 256+2L < ld). Same staging, lookahead (2) and
+// CSR-order FMA chains as spmm_row_kernel, so the results are bitwise those of
+// the slab kernel; one warp gathers the whole 2.4 KB row per nonzero instead
+// of five 512-byte slabs, and A is read once instead of once per slab.
+template <bool kShift, bool kChunk>
+__global__ void __launch_bounds__(32 * kRowWarps, 2)
+spmm_row_wide_kernel(const int64_t* __restrict__ off, const int32_t* __restrict__ idx, const double* __restrict__ val,
+                     const int32_t* __restrict__ order, int64_t row_start, int64_t rows, const double* __restrict__ x,
+                     double* __restrict__ y, int64_t ld, const double* __restrict__ q,
+                     const double* __restrict__ alpha_p, const int32_t* __restrict__ gate,
+                     const int64_t* __restrict__ chunk_p0, const int64_t* __restrict__ chunk_p1) {
+    constexpr int U = 4;
+    if (gate != nullptr && *gate != 0) return;
+    __shared__ __align__(16) double2 cv[kRowWarps][32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t rpos = row_start + static_cast<int64_t>(blockIdx.x) * kRowWarps + warp;
+    if (rpos >= rows) return;
+    int64_t row, beg, end;
+    if (kChunk) {
+        row = rpos;
+        beg = chunk_p0[rpos];
+        end = chunk_p1[rpos];
+    } else {
+        row = static_cast<int64_t>(order[rpos]);
+        beg = off[row];
+        end = off[row + 1];
+    }
+    const bool act0 = 8 * lane < ld, act1 = 8 * lane + 4 < ld, act2 = 256 + 2 * lane < ld;
+    const double* x0 = x + (act0 ? 8 * lane : 0);
+    const double* x1 = x + (act1 ? 8 * lane + 4 : 0);
+    const double* x2 = x + (act2 ? 256 + 2 * lane : 0);
+    double acc[10] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+    int c = 0;
+    double v = 0.0;
+    if (beg + lane < end) {
+        c = __ldg(idx + beg + lane);
+        v = __ldg(val + beg + lane);
+    }
+    double2* slot = cv[warp];
+    for (int64_t p0 = beg; p0 < end; p0 += 32) {
+        const int cnt = static_cast<int>(end - p0 < 32 ? end - p0 : 32);
+        __syncwarp();
+        slot[lane] = make_double2(v, __longlong_as_double(static_cast<long long>(c)));
+        __syncwarp();
+        if (p0 + 32 + lane < end) {
+            c = __ldg(idx + p0 + 32 + lane);
+            v = __ldg(val + p0 + 32 + lane);
+        }
+        for (int j0 = 0; j0 < cnt; j0 += U) {
+            double xa[U][4], xc[U][4], xb[U][2], vj[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int j = j0 + u;
+                vj[u] = 0.0;
+                if (j < cnt) {
+                    const double2 e = slot[j];
+                    vj[u] = e.x;
+                    const int64_t cj = __double_as_longlong(e.y);
+                    if (act0) ld256(x0 + cj * ld, xa[u]);
+                    if (act1) ld256(x1 + cj * ld, xc[u]);
+                    if (act2) {
+                        const double2 t = __ldg(reinterpret_cast<const double2*>(x2 + cj * ld));
+                        xb[u][0] = t.x;
+                        xb[u][1] = t.y;
+                    }
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                if (j0 + u < cnt) {
+#pragma unroll
+                    for (int t = 0; t < 4; ++t) acc[t] = fma(vj[u], xa[u][t], acc[t]);
+#pragma unroll
+                    for (int t = 0; t < 4; ++t) acc[4 + t] = fma(vj[u], xc[u][t], acc[4 + t]);
+                    acc[8] = fma(vj[u], xb[u][0], acc[8]);
+                    acc[9] = fma(vj[u], xb[u][1], acc[9]);
+                }
+            }
+        }
+    }
+    double* yr = y + (kChunk ? rpos : row) * ld;
+    if (kShift && !kChunk) {
+        const double alpha = *alpha_p;
+        if (alpha != 0.0) {
+            const double* qr = q + row * ld;
+            if (act0) {
+#pragma unroll
+                for (int t = 0; t < 4; ++t) acc[t] = fma(-alpha, qr[8 * lane + t], acc[t]);
+            }
+            if (act1) {
+#pragma unroll
+                for (int t = 0; t < 4; ++t) acc[4 + t] = fma(-alpha, qr[8 * lane + 4 + t], acc[4 + t]);
+            }
+            if (act2) {
+                acc[8] = fma(-alpha, qr[256 + 2 * lane], acc[8]);
+                acc[9] = fma(-alpha, qr[256 + 2 * lane + 1], acc[9]);
+            }
+        }
+    }
+    if (act0) {
+        *reinterpret_cast<double2*>(yr + 8 * lane) = make_double2(acc[0], acc[1]);
+        *reinterpret_cast<double2*>(yr + 8 * lane + 2) = make_double2(acc[2], acc[3]);
+    }
+    if (act1) {
+        *reinterpret_cast<double2*>(yr + 8 * lane + 4) = make_double2(acc[4], acc[5]);
+        *reinterpret_cast<double2*>(yr + 8 * lane + 6) = make_double2(acc[6], acc[7]);
+    }
+    if (act2) *reinterpret_cast<double2*>(yr + 256 + 2 * lane) = make_double2(acc[8], acc[9]);
+}
+
 // y(row_i, :) = sum over the row's chunks, in chunk order, of partial(chunk, :),
 // then the shift epilogue.
 // y(row_i, :) = sum of the row's chunk partials (chunk_slot maps its chunks, in
@@ -950,6 +1062,9 @@ void spmm(const SpmmArgs& s, cudaStream_t stream, int variant, cudaStream_t side
     // ld <= 192; bits 64 / 128 force the 64-column slab kernel for them, bits
     // 256 / 512 raise the whole-row kernel's gather lookahead from 2 to 4 / 8
     const bool row_bulk = (variant & 64) == 0 && s.ld <= 192, row_chunk = (variant & 128) == 0 && s.ld <= 192;
+    // 192 < ld <= 320: the wide whole-row kernel (same bits force the slab kernel)
+    const bool wide_bulk = (variant & 64) == 0 && s.ld > 192 && s.ld <= 320,
+               wide_chunk = (variant & 128) == 0 && s.ld > 192 && s.ld <= 320;
     const int ru = (variant & 256) ? 4 : (variant & 512) ? 8 : 2;
     variant &= 15;
     const bool split = a.nsplit > 0 && partial != nullptr && side != nullptr;
@@ -967,6 +1082,12 @@ void spmm(const SpmmArgs& s, cudaStream_t stream, int variant, cudaStream_t side
             k<<<static_cast<unsigned>(ceil_div(a.nchunks, kRowWarps)), 32 * kRowWarps, 0, side>>>(
                 a.off, a.idx, a.val, a.order, 0, a.nchunks, s.x, partial, s.ld, nullptr, nullptr, s.gate, a.chunk_p0,
                 a.chunk_p1);
+            DSVD_LAUNCH_CHECK();
+        } else if (citems > 0 && wide_chunk) {
+            spmm_row_wide_kernel<false, true><<<static_cast<unsigned>(ceil_div(a.nchunks, kRowWarps)),
+                                                32 * kRowWarps, 0, side>>>(a.off, a.idx, a.val, a.order, 0, a.nchunks,
+                                                                           s.x, partial, s.ld, nullptr, nullptr,
+                                                                           s.gate, a.chunk_p0, a.chunk_p1);
             DSVD_LAUNCH_CHECK();
         } else if (citems > 0) {
             spmm_bulk_kernel<false, true><<<static_cast<unsigned>(ceil_div(citems, 8)), 256, 0, side>>>(
@@ -1044,7 +1165,17 @@ void spmm(const SpmmArgs& s, cudaStream_t stream, int variant, cudaStream_t side
     const int warps_per_block = 8;
     const int64_t first = split ? a.nsplit : hub;  // rows handled above / in chunks
     const int64_t items = skip_bulk ? 0 : (a.rows - first) * nslab;
-    if (items > 0 && row_bulk) {
+    if (items > 0 && wide_bulk) {
+        const unsigned blocks = static_cast<unsigned>(ceil_div(a.rows - first, kRowWarps));
+        if (s.q != nullptr)
+            spmm_row_wide_kernel<true, false><<<blocks, 32 * kRowWarps, 0, stream>>>(
+                a.off, a.idx, a.val, a.order, first, a.rows, s.x, s.y, s.ld, s.q, s.alpha, s.gate, nullptr, nullptr);
+        else
+            spmm_row_wide_kernel<false, false><<<blocks, 32 * kRowWarps, 0, stream>>>(
+                a.off, a.idx, a.val, a.order, first, a.rows, s.x, s.y, s.ld, nullptr, nullptr, s.gate, nullptr,
+                nullptr);
+        DSVD_LAUNCH_CHECK();
+    } else if (items > 0 && row_bulk) {
         const unsigned blocks = static_cast<unsigned>(ceil_div(a.rows - first, kRowWarps));
         if (s.q != nullptr) {
             auto k = ru == 4 ? spmm_row_kernel<true, false, 4>
