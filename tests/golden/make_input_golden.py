@@ -13,6 +13,7 @@ import tempfile
 HERE = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, os.path.dirname(HERE))
 sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
+sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(HERE)), "oracle"))
 from input_cases import MTX_CASES, corrupt_csr  # noqa: E402
 from oracle_lib import Reference  # noqa: E402
 from paper_2404_09276_b200 import errors as E  # noqa: E402
