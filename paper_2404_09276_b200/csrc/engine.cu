@@ -1570,6 +1570,7 @@ int dsvd_solve_csr_device(dsvd_ctx* ctx, int64_t rows, int64_t cols, int64_t nnz
         DSVD_CUDA_CHECK(cudaEventRecord(e0, ctx->stream));
         DevCsr a, at;
         CsrAlloc al{ctx, "csr.", nullptr};
+        pregenerate_omega(ctx, rows, cols, *cfg);  // Omega on the side stream beside the CSC build
         build_pair(ctx, al, rows, cols, nnz, d_off, d_idx, d_val, a, at, false);
         DSVD_CUDA_CHECK(cudaEventRecord(e1, ctx->stream));
         solve_pair(ctx, a, at, *cfg, out, nullptr, nullptr, ctx->shard_row_offset,
