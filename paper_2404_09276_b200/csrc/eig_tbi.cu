@@ -93,6 +93,26 @@ __device__ long long g_trid_probe[192][4];
     } while (0)
 #endif
 
+// sqrt and reciprocal from the hardware approximations plus Newton steps
+// (within an ulp; the step's critical path is the reflector, and the IEEE
+// sequences were ~40% of its latency, tools/micro/tridiag_probe.cu)
+__device__ __forceinline__ double sqrt_nr(double a) {
+    double r;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(a));
+    const double ha = 0.5 * a;
+    r = r * fma(-ha * r, r, 1.5);
+    r = r * fma(-ha * r, r, 1.5);
+    const double s = a * r;
+    return fma(0.5 * r, fma(-s, s, a), s);
+}
+__device__ __forceinline__ double rcp_nr(double a) {
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(a));
+    r = r * fma(-a, r, 2.0);
+    r = r * fma(-a, r, 2.0);
+    return fma(r, fma(-a, r, 1.0), r);
+}
+
 struct Reflector {
     double tau, v0, x0, alpha;
 };
@@ -112,9 +132,9 @@ __device__ __forceinline__ Reflector make_reflector(const double* A, int lda, in
     r.v0 = r.x0;
     const double tail = sig - r.x0 * r.x0;  // sum of squares below the first entry
     if (tail > 0.0) {
-        r.alpha = -copysign(sqrt(sig), r.x0);
+        r.alpha = -copysign(sqrt_nr(sig), r.x0);
         r.v0 = r.x0 - r.alpha;
-        r.tau = 2.0 / (tail + r.v0 * r.v0);
+        r.tau = 2.0 * rcp_nr(tail + r.v0 * r.v0);
     }
     return r;
 }
