@@ -180,7 +180,9 @@ __host__ __device__ inline double log_cr_series(double u) {
     const dd w = mul(z, z);
     constexpr int K = 23;  // |z| <= 0.1716: w^23/47 < 2^-118
     dd p{ddc::kAtanhHi(K - 1), ddc::kAtanhLo(K - 1)};
+#ifdef __CUDA_ARCH__
 #pragma unroll
+#endif
     for (int k = K - 2; k >= 0; --k) p = add(mul(p, w), dd{ddc::kAtanhHi(k), ddc::kAtanhLo(k)});
     dd lg = mul(mul_d(z, 2.0), p);
     const double ed = static_cast<double>(e);
@@ -204,12 +206,16 @@ __host__ __device__ inline double cos_cr_series(double x) {
     dd res;
     if ((k & 1) == 0) {
         dd c{ddc::kCosHi(J - 1), ddc::kCosLo(J - 1)};
+#ifdef __CUDA_ARCH__
 #pragma unroll
+#endif
         for (int j = J - 2; j >= 0; --j) c = add(mul(c, w), dd{ddc::kCosHi(j), ddc::kCosLo(j)});
         res = c;
     } else {
         dd s{ddc::kSinHi(J - 1), ddc::kSinLo(J - 1)};
+#ifdef __CUDA_ARCH__
 #pragma unroll
+#endif
         for (int j = J - 2; j >= 0; --j) s = add(mul(s, w), dd{ddc::kSinHi(j), ddc::kSinLo(j)});
         res = mul(s, r);
     }

@@ -208,7 +208,6 @@ __global__ void rm_to_cm_kernel(const double* __restrict__ src, int64_t rows, in
 // a (8 values, shared by most lanes of a warp -> broadcast) and b (8 values)
 // give 64 DFMA per 16 loads. Chunk partials are reduced in a fixed order.
 constexpr int kG2Rows = 8;        // rows per stage
-constexpr int kG2MaxTiles = 1024; // tile pairs per block (l_pad8 <= 8*44)
 
 __device__ __forceinline__ void cpa16(void* dst, const void* src) {
     const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));

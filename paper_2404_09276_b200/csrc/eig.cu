@@ -213,12 +213,6 @@ __device__ __forceinline__ unsigned cl_map(const void* p, unsigned rank) {
     asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(r) : "r"(s_u32(p)), "r"(rank));
     return r;
 }
-__device__ __forceinline__ void cl_st_v2(unsigned addr, double a, double b) {
-    asm volatile("st.shared::cluster.v2.f64 [%0], {%1, %2};\n" ::"r"(addr), "d"(a), "d"(b) : "memory");
-}
-__device__ __forceinline__ void cl_st_s32(unsigned addr, int v) {
-    asm volatile("st.shared::cluster.s32 [%0], %1;\n" ::"r"(addr), "r"(v) : "memory");
-}
 __device__ __forceinline__ void cl_arrive(unsigned addr) {
     asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];\n" ::"r"(addr) : "memory");
 }
