@@ -439,39 +439,54 @@ gram_dmma_reduce_kernel(const double* __restrict__ partial, int nblk, int nb, in
     g[j * l + i] = s;
 }
 
-// Wide Gram (l > 160, e.g. C4's l = 300): the 32-column strips are grouped in
-// fours (128 columns); CTA (pair of strip groups a <= b, row slab) computes the
-// 4x4 tiles (I, J), I in group a, J in group b, I <= J, one warp per tile (16
-// warps), staging only the columns of its two groups. blockIdx.x (the group
-// pair) varies fastest so the CTAs of one slab share the slab in L2. Same
-// partial layout as gram_dmma_kernel (one triangle of 8x8 blocks per slab).
+// Wide Gram (l > 160, e.g. C4's l = 300): the 32-column strips are split in
+// two halves H0 = [0, h), H1 = [h, NS); a CTA "kind" is the triangle of 4x4
+// tiles inside one half, or a piece of the H0 x H1 rectangle at most 16 tiles
+// big (one warp per tile, 16 warps), so the kinds carry near-equal tile counts
+// (C4: 15, 15, 15, 10). A CTA (kind, row slab) stages only the columns of its
+// one or two strip segments. blockIdx.x (the kind) varies fastest so the CTAs
+// of one slab share it in L2. Same partial layout as gram_dmma_kernel (one
+// triangle of 8x8 blocks per slab).
 constexpr int kGwRows = 32, kGwStages = 3, kGwStride = 264;  // 2 * 264 == 16 (mod 32) banks
+constexpr int kGwMaxKinds = 8;
+
+struct GwKinds {
+    int8_t sa0[kGwMaxKinds], sa1[kGwMaxKinds], sb0[kGwMaxKinds], sb1[kGwMaxKinds];
+};
 
 __global__ void __launch_bounds__(512, 1)
 gram_dmma_wide_kernel(const double* __restrict__ c, int64_t n, int64_t ld, int nb, int64_t rows_per_block,
-                      double* __restrict__ partial, const int32_t* __restrict__ gate) {
+                      const GwKinds kinds, double* __restrict__ partial, const int32_t* __restrict__ gate) {
     if (gate != nullptr && *gate != 0) return;
     extern __shared__ __align__(16) double wsm[];  // [stages][kGwRows][kGwStride]
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int q = lane & 3, g = lane >> 2;
-    int a = 0, t = blockIdx.x;
-    const int ngrp = (nb + 15) / 16;
-    while (t >= ngrp - a) {
-        t -= ngrp - a;
-        ++a;
+    const int kd = blockIdx.x;
+    const int sa0 = kinds.sa0[kd], nA = kinds.sa1[kd] - sa0, sb0 = kinds.sb0[kd], nB = kinds.sb1[kd] - sb0;
+    const bool tri = nB == 0;
+    int I, J;
+    bool active;
+    if (tri) {  // upper triangle of the nA x nA strip tiles, row-major
+        int t = warp, i = 0;
+        while (i < nA && t >= nA - i) {
+            t -= nA - i;
+            ++i;
+        }
+        active = i < nA;
+        I = sa0 + i;
+        J = sa0 + i + t;
+    } else {
+        active = warp < nA * nB;
+        I = sa0 + warp / max(nB, 1);
+        J = sb0 + warp % max(nB, 1);
     }
-    const int b = a + t;
-    const int I = 4 * a + (warp >> 2), J = 4 * b + (warp & 3);
-    const bool active = I <= J && 4 * I < nb && 4 * J < nb;
     const int64_t r_beg = static_cast<int64_t>(blockIdx.y) * rows_per_block;
     const int64_t r_end = min(n, r_beg + rows_per_block);
-    const int64_t c0a = 128 * a, c0b = 128 * b;
-    const bool same = a == b;
-    // staging: 16 rows x (64 + 64) 16-byte chunks per stage, four per thread at
-    // rows (tid >> 7) + 4u of one fixed chunk, so the addresses are set up once
+    // staging: 32 rows x up to 128 16-byte chunks per stage, eight per thread
+    // at rows (tid >> 7) + 4u of one fixed chunk (addresses set up once)
     const int ch = tid & 127, r0t = tid >> 7;
-    const int64_t col = (ch < 64 ? c0a : c0b) + 2 * (ch & 63);
-    const bool col_ok = col < ld && (ch < 64 || !same);
+    const int64_t col = ch < 16 * nA ? 32 * sa0 + 2 * ch : 32 * sb0 + 2 * (ch - 16 * nA);
+    const bool col_ok = ch < 16 * (nA + nB) && col < ld;
     const double* src0 = c + (col_ok ? col : 0);
     double* dst0 = wsm + r0t * kGwStride + 2 * ch;
     auto stage = [&](int slot, int64_t rr0) {
@@ -493,7 +508,7 @@ gram_dmma_wide_kernel(const double* __restrict__ c, int64_t n, int64_t ld, int n
     for (int u = 0; u < 4; ++u)
 #pragma unroll
         for (int v = 0; v < 4; ++v) acc[u][v] = make_double2(0.0, 0.0);
-    const int ia = 32 * (I - 4 * a), jb = (same ? 0 : 128) + 32 * (J - 4 * b);
+    const int ia = 32 * (I - sa0), jb = tri ? 32 * (J - sa0) : 32 * (nA + J - sb0);
     for (int st = 0; st < nst; ++st) {
         cpa_wait<kGwStages - 2>();
         __syncthreads();
@@ -543,19 +558,39 @@ struct GramDmmaPlan {
     int nb = 0, nblk = 0;
     int64_t rpb = 0;
 };
+
+// CTA kinds of gram_dmma_wide_kernel for NS strips of 32 columns (NS <= 10)
+struct GwPlan {
+    GwKinds k{};
+    int n = 0;
+};
+GwPlan gw_kinds(int ns) {
+    GwPlan p;
+    auto add = [&](int a0, int a1, int b0, int b1) {
+        p.k.sa0[p.n] = static_cast<int8_t>(a0);
+        p.k.sa1[p.n] = static_cast<int8_t>(a1);
+        p.k.sb0[p.n] = static_cast<int8_t>(b0);
+        p.k.sb1[p.n] = static_cast<int8_t>(b1);
+        ++p.n;
+    };
+    const int h = (ns + 1) / 2;
+    add(0, h, 0, 0);
+    if (ns > h) add(h, ns, h, h);
+    const int cw = std::max(1, 16 / h);
+    for (int b0 = h; b0 < ns; b0 += cw) add(0, h, b0, std::min(ns, b0 + cw));
+    return p;
+}
 constexpr int kGramNarrowMaxNb = 20;  // gram_dmma_kernel<NB4 <= 5>: l <= 160
-constexpr int kGramWideMaxNb = 64;    // gram_dmma_wide_kernel: l <= 512
+constexpr int kGramWideMaxNb = 40;    // gram_dmma_wide_kernel: l <= 320 (<= 10 strips)
 
 GramDmmaPlan gram_dmma_plan(int64_t n, int64_t l) {
     GramDmmaPlan p;
     p.nb = static_cast<int>((l + 7) / 8);
     if (p.nb > kGramNarrowMaxNb) {
-        // wide: group pairs x slabs. The pairs carry unequal tile counts (a
-        // diagonal pair 10 of 16, an edge pair as few as 1), so ~12 waves of
-        // one CTA per SM let the block scheduler even the load out
-        const int ngrp = (p.nb + 15) / 16, npairs = ngrp * (ngrp + 1) / 2;
+        // wide: kinds x slabs, ~6 waves of one CTA per SM
+        const int nkinds = gw_kinds((p.nb + 3) / 4).n;
         p.nblk = static_cast<int>(std::max<int64_t>(
-            1, std::min<int64_t>(ceil_div(12 * kNumSMs, npairs), ceil_div(n, 16 * kGwRows))));
+            1, std::min<int64_t>(ceil_div(6 * kNumSMs, nkinds), ceil_div(n, 8 * kGwRows))));
         p.rpb = ceil_div(ceil_div(n, p.nblk), kGwRows) * kGwRows;
         p.nblk = static_cast<int>(std::max<int64_t>(1, ceil_div(n, p.rpb)));
         return p;
@@ -584,12 +619,12 @@ void gram_dmma(const double* c, int64_t n, int64_t l, int64_t ld, double* g, voi
     const GramDmmaPlan p = gram_dmma_plan(n, l);
     double* partial = static_cast<double*>(ws);
     if (p.nb > kGramNarrowMaxNb) {
-        const int ngrp = (p.nb + 15) / 16;
+        const GwPlan kp = gw_kinds((p.nb + 3) / 4);
         const size_t smem = sizeof(double) * kGwStages * kGwRows * kGwStride;
         DSVD_CUDA_CHECK(cudaFuncSetAttribute(gram_dmma_wide_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              static_cast<int>(smem)));
-        const dim3 grid(static_cast<unsigned>(ngrp * (ngrp + 1) / 2), static_cast<unsigned>(p.nblk));
-        gram_dmma_wide_kernel<<<grid, 512, smem, stream>>>(c, n, ld, p.nb, p.rpb, partial, gate);
+        const dim3 grid(static_cast<unsigned>(kp.n), static_cast<unsigned>(p.nblk));
+        gram_dmma_wide_kernel<<<grid, 512, smem, stream>>>(c, n, ld, p.nb, p.rpb, kp.k, partial, gate);
         DSVD_LAUNCH_CHECK();
         gram_dmma_reduce_kernel<<<gm_pairs(p.nb), 256, 0, stream>>>(partial, p.nblk, p.nb, l, g, gate);
         DSVD_LAUNCH_CHECK();
