@@ -191,6 +191,7 @@ rescale_dmma_kernel(const double* __restrict__ c, int64_t n, int K, int64_t ldc,
 // fragment addresses follow the swizzle (16-byte chunk c of row r lives at
 // chunk c ^ (r & 7)). Removes the per-thread cp.async address arithmetic,
 // which was ~45% of the issued instructions of rescale_dmma_kernel.
+template <int ST>
 __global__ void __launch_bounds__(kRsThreads, 2)
 rescale_tma_kernel(const __grid_constant__ CUtensorMap cmap, int64_t n, int K, const double* __restrict__ wt,
                    int ldb, int ncol, double* __restrict__ out, int64_t ld_out, int out_colmajor,
@@ -199,9 +200,9 @@ rescale_tma_kernel(const __grid_constant__ CUtensorMap cmap, int64_t n, int K, c
     extern __shared__ __align__(1024) unsigned char rsm_raw[];
     // 1024-byte aligned ring first (128B-swizzle requirement), then W, then barriers
     double* As = reinterpret_cast<double*>(rsm_raw + ((1024 - (su32(rsm_raw) & 1023)) & 1023));
-    double* Bt = As + kRsStages * kRsBM * kRsBK;
+    double* Bt = As + ST * kRsBM * kRsBK;
     uint64_t* full = reinterpret_cast<uint64_t*>(Bt + kRsBN * ldb);
-    uint64_t* wbar = full + kRsStages;
+    uint64_t* wbar = full + ST;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int q = lane & 3, g = lane >> 2;
     const int j0 = blockIdx.x * kRsBN;
@@ -209,7 +210,7 @@ rescale_tma_kernel(const __grid_constant__ CUtensorMap cmap, int64_t n, int K, c
     const int64_t nrb = (n + kRsBM - 1) / kRsBM;
     constexpr unsigned kTileBytes = kRsBM * kRsBK * sizeof(double);
     if (tid == 0) {
-        for (int s = 0; s < kRsStages; ++s) bar_init(&full[s], 1);
+        for (int s = 0; s < ST; ++s) bar_init(&full[s], 1);
         bar_init(wbar, 1);
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
@@ -225,8 +226,8 @@ rescale_tma_kernel(const __grid_constant__ CUtensorMap cmap, int64_t n, int K, c
     for (int64_t rb = blockIdx.y; rb < nrb; rb += gridDim.y) {
         const int y0 = static_cast<int>(rb * kRsBM);
         if (tid == 0) {
-            for (int s = 0; s < kRsStages - 1 && s < nk; ++s) {
-                const unsigned slot = (use + s) % kRsStages;
+            for (int s = 0; s < ST - 1 && s < nk; ++s) {
+                const unsigned slot = (use + s) % ST;
                 bar_expect_tx(&full[slot], kTileBytes);
                 tma_load_2d(As + slot * (kRsBM * kRsBK), &cmap, s * kRsBK, y0, &full[slot]);
             }
@@ -238,13 +239,13 @@ rescale_tma_kernel(const __grid_constant__ CUtensorMap cmap, int64_t n, int K, c
             for (int b = 0; b < 4; ++b) acc[a][b] = make_double2(0.0, 0.0);
         for (int kc = 0; kc < nk; ++kc, ++use) {
             __syncthreads();  // every warp is done with the slot refilled below
-            if (tid == 0 && kc + kRsStages - 1 < nk) {
-                const unsigned slot = (use + kRsStages - 1) % kRsStages;
+            if (tid == 0 && kc + ST - 1 < nk) {
+                const unsigned slot = (use + ST - 1) % ST;
                 bar_expect_tx(&full[slot], kTileBytes);
-                tma_load_2d(As + slot * (kRsBM * kRsBK), &cmap, (kc + kRsStages - 1) * kRsBK, y0, &full[slot]);
+                tma_load_2d(As + slot * (kRsBM * kRsBK), &cmap, (kc + ST - 1) * kRsBK, y0, &full[slot]);
             }
-            const unsigned slot = use % kRsStages;
-            bar_wait(&full[slot], (use / kRsStages) & 1);
+            const unsigned slot = use % ST;
+            bar_wait(&full[slot], (use / ST) & 1);
             const double* A = As + slot * (kRsBM * kRsBK);
 #pragma unroll
             for (int p = 0; p < 2; ++p) {
@@ -670,14 +671,15 @@ void rescale_dmma(const double* c, int64_t n, int64_t K, int64_t ldc, const doub
     const dim3 grid(static_cast<unsigned>(ncb), static_cast<unsigned>(std::min<int64_t>(nrb, 65535)));
     const bool tma = rescale_use_tma && (reinterpret_cast<uintptr_t>(c) % 16) == 0 && (ldc * 8) % 16 == 0;
     if (tma) {
-        const size_t smem = 1024 + sizeof(double) * (kRsStages * kRsBM * kRsBK + static_cast<size_t>(kRsBN) * ldb) +
-                            sizeof(uint64_t) * (kRsStages + 1);
-        DSVD_CUDA_CHECK(cudaFuncSetAttribute(rescale_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             static_cast<int>(smem)));
+        // K > 160: a 2-deep ring keeps two CTAs per SM (the W block grows with K)
+        const int st = K > 160 ? 2 : kRsStages;
+        const size_t smem = 1024 + sizeof(double) * (st * kRsBM * kRsBK + static_cast<size_t>(kRsBN) * ldb) +
+                            sizeof(uint64_t) * (st + 1);
+        auto kern = st == 2 ? rescale_tma_kernel<2> : rescale_tma_kernel<kRsStages>;
+        DSVD_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
         const CUtensorMap cmap = make_cmap(c, n, ldc);
-        rescale_tma_kernel<<<grid, kRsThreads, smem, stream>>>(cmap, n, static_cast<int>(K), wt, ldb,
-                                                               static_cast<int>(ncol), out, ld_out, out_colmajor,
-                                                               gate);
+        kern<<<grid, kRsThreads, smem, stream>>>(cmap, n, static_cast<int>(K), wt, ldb, static_cast<int>(ncol), out,
+                                                 ld_out, out_colmajor, gate);
     } else {
         const size_t smem = sizeof(double) * (static_cast<size_t>(kRsBN) * ldb + kRsStages * kRsBM * kRsBK);
         DSVD_CUDA_CHECK(cudaFuncSetAttribute(rescale_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
