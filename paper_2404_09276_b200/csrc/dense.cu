@@ -18,6 +18,15 @@ constexpr int kK = 16;
 __global__ void gaussian_kernel(double* __restrict__ out, int64_t rows, int64_t l, int64_t ld,
                                 uint64_t seed, int64_t global_rows, int64_t row_offset) {
     const int64_t total = rows * ld;
+    if (total < (int64_t(1) << 32)) {  // 32-bit index arithmetic (no emulated 64-bit division)
+        const uint32_t ld32 = static_cast<uint32_t>(ld);
+        for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < static_cast<uint32_t>(total);
+             e += gridDim.x * blockDim.x) {
+            const uint32_t i = e / ld32, j = e - i * ld32;
+            out[e] = j < l ? normal_at(seed, static_cast<uint64_t>(j) * global_rows + row_offset + i) : 0.0;
+        }
+        return;
+    }
     for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
          e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
         const int64_t i = e / ld;
