@@ -195,6 +195,8 @@ void build_pair(dsvd_ctx* ctx, CsrAlloc& al, int64_t rows, int64_t cols, int64_t
     if (rows < 0 || cols < 0 || nnz < 0) fail(DSVD_SHAPE, "sparse matrix with negative dimension");
     if (rows > 0x7fffffffLL || cols > 0x7fffffffLL)
         fail(DSVD_UNSUPPORTED, "dimensions >= 2^31 are not supported on the device path");
+    if (nnz > 0x7fffffffLL)  // int32 nonzero positions in the CSC build (row-shard larger matrices)
+        fail(DSVD_UNSUPPORTED, "nnz >= 2^31 per device is not supported; shard the rows over GPUs");
     a.rows = rows;
     a.cols = cols;
     a.nnz = nnz;
@@ -1264,6 +1266,7 @@ namespace {
 int64_t assemble_host_triplets(dsvd_ctx* ctx, int64_t rows, int64_t cols, int64_t n, const int64_t* r,
                                const int64_t* c, const double* v) {
     if (rows < 0 || cols < 0 || n < 0) fail(DSVD_SHAPE, "sparse matrix with negative dimension");
+    if (n > 0x7fffffffLL) fail(DSVD_UNSUPPORTED, "more than 2^31 - 1 triplets per assembly");
     cudaStream_t st = ctx->stream;
     int64_t* dr = ctx->tbuf<int64_t>("coo.r", n);
     int64_t* dc = ctx->tbuf<int64_t>("coo.c", n);
