@@ -543,6 +543,36 @@ def test_solve_deterministic(dev, c1):
     assert_bitwise(r1.svd.s, r2.svd.s)
 
 
+def test_concurrent_contexts_on_threads(c1):
+    """One context per thread (the documented pattern for concurrent solves,
+    dashsvd_b200.h): four threads solving at once on one GPU give the same bits
+    as a solve alone."""
+    import threading
+    a = to_dev(c1)
+    cfgs = [d.SolverConfig(k=20, s=10, p=3, alg=d.Algorithm.shifted, seed=s) for s in range(4)]
+    alone = [d.solve(a, c, device=d.Device(0)) for c in cfgs]
+    out = [None] * 4
+    errors = []
+
+    def work(t):
+        try:
+            dv = d.Device(0)
+            out[t] = d.solve(a, cfgs[t], device=dv)
+            dv.close()
+        except Exception as exc:  # surfaced below
+            errors.append(exc)
+
+    th = [threading.Thread(target=work, args=(t,)) for t in range(4)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errors, errors
+    for r, r0 in zip(out, alone):
+        assert_bitwise(r.svd.s, r0.svd.s)
+        assert_bitwise(r.svd.u, r0.svd.u)
+
+
 @pytest.mark.parametrize("alg", ["shifted", "dash"])
 def test_sharded_path_single_rank(oracle, c1, alg):
     """The multi-GPU code path (NCCL communicator, shard bookkeeping, all-reduce
