@@ -49,6 +49,9 @@ def main():
     ap.add_argument("--p", type=int, default=None, help="override p (fixed-p configs)")
     ap.add_argument("--p-max", type=int, default=None, help="override p_max (dash configs)")
     ap.add_argument("--threads", type=int, default=os.cpu_count())
+    ap.add_argument("--alg", choices=["basic", "shifted", "fixed_shift", "dash"], default=None,
+                    help="override the config's algorithm (dash needs --p-max or the config's p_max)")
+    ap.add_argument("--orth", choices=["eigsvd", "qr"], default="eigsvd", help="basic only")
     ap.add_argument("--rmat-scale", type=int, default=None,
                     help="R-MAT configs: generate at this scale instead (draws scaled by 2^(scale - config scale))")
     args = ap.parse_args()
@@ -57,6 +60,14 @@ def main():
         cfg["p"] = args.p
     if args.p_max is not None:
         cfg["p_max"] = args.p_max
+    if args.alg is not None:
+        cfg["alg"] = args.alg
+        if args.alg != "dash" and cfg.get("p", -1) < 0:
+            cfg["p"] = args.p if args.p is not None else 4
+        if args.alg == "dash":
+            cfg["p"] = -1
+            cfg.setdefault("tol", 1e-2)
+            cfg.setdefault("p_max", 100)
     if args.rmat_scale is not None:
         shift = args.rmat_scale - cfg["rmat_scale"]
         cfg["draws"] = int(cfg["draws"] * 2.0 ** shift)
@@ -68,6 +79,8 @@ def main():
     a = bench.make_matrix(cfg, dev)
     t_gen = time.perf_counter() - t0
     scfg = bench.solver_config(cfg)
+    if args.orth == "qr":
+        scfg.orth = d.Orthonormalizer.qr
     k = scfg.k
     d.solve(a, scfg, device=dev)  # warm-up (module load, allocations)
     t0 = time.perf_counter()
@@ -81,7 +94,7 @@ def main():
     ref.set_threads(args.threads)
     t0 = time.perf_counter()
     out = ref.solve(Csr(a.rows, a.cols, a.offsets, a.col_indices, a.values), k, scfg.s, scfg.p, scfg.tol,
-                    scfg.p_max, scfg.alg.name, scfg.seed)
+                    scfg.p_max, scfg.alg.name, scfg.seed, orth=args.orth)
     t_ref = time.perf_counter() - t0
     print(f"[parity] reference solve {t_ref:.1f}s on {args.threads} threads", flush=True)
 
@@ -89,16 +102,19 @@ def main():
     th_u = sin_theta(out["u"], res.svd.u)
     th_v = sin_theta(out["v"], res.svd.v)
     al_g = np.array(res.trace.alphas)
-    sh_g = np.array(res.trace.s_hat_history)
+    sh_g = np.array(res.trace.s_hat_history) if args.orth == "eigsvd" else np.zeros((len(al_g), 0))
     n_it = min(len(al_g), len(out["alphas"]))
     alpha_rel = float(np.max(np.abs(al_g[:n_it] - out["alphas"][:n_it]) / np.maximum(np.abs(out["alphas"][:n_it]),
                                                                                       1e-300))) if n_it else 0.0
-    shat_rel = float(np.max(np.abs(sh_g[:n_it] - out["s_hat"][:n_it]) / np.abs(out["s_hat"][:n_it]))) if n_it else 0.0
-    pve_g, pve_r = pve_ratio(al_g, sh_g, k), pve_ratio(out["alphas"], out["s_hat"], k)
+    has_shat = args.orth == "eigsvd" and n_it > 0
+    shat_rel = float(np.max(np.abs(sh_g[:n_it] - out["s_hat"][:n_it]) / np.abs(out["s_hat"][:n_it]))) \
+        if has_shat else 0.0
+    pve_g, pve_r = (pve_ratio(al_g, sh_g, k), pve_ratio(out["alphas"], out["s_hat"], k)) if has_shat \
+        else (None, None)
     rec = {
         "config": args.config, "workload": cfg["name"], "rows": a.rows, "cols": a.cols, "nnz": a.nnz,
         "k": k, "l": scfg.sketch_width(), "alg": scfg.alg.name, "p": scfg.p, "p_max": scfg.p_max,
-        "tol": scfg.tol, "reduced_p": args.p is not None or args.p_max is not None,
+        "tol": scfg.tol, "orth": args.orth, "reduced_p": args.p is not None or args.p_max is not None,
         "rmat_scale": cfg.get("rmat_scale"),
         "gpu_solve_s": t_gpu, "reference_solve_s": t_ref, "reference_threads": args.threads,
         "sigma_max_rel_err": s_rel, "sin_theta_u": th_u, "sin_theta_v": th_v,
@@ -113,7 +129,8 @@ def main():
                        res.trace.iterations == out["iterations"] and
                        res.trace.stop_reason.name == out["stop_reason"] and
                        (rec["pve_ratio_rel_err"] is None or rec["pve_ratio_rel_err"] <= 1e-6))
-    name = f"parity_{args.config}" + (f"_p{scfg.p}" if args.p is not None else "") + \
+    name = f"parity_{args.config}" + (f"_{args.alg}" if args.alg else "") + \
+        (f"_qr" if args.orth == "qr" else "") + (f"_p{scfg.p}" if args.p is not None else "") + \
         (f"_pmax{scfg.p_max}" if args.p_max is not None else "") + \
         (f"_scale{args.rmat_scale}" if args.rmat_scale is not None else "")
     os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
