@@ -31,20 +31,9 @@
 #include "common.cuh"
 #include "dense.cuh"
 #include "engine.cuh"
-#include "ingest.cuh"
-#include "mtx.hpp"
+#include "engine_internal.cuh"
 #include "qr.cuh"
 
-namespace dsvd {  // metrics.cu
-void col_norms(dsvd_ctx* ctx, const double* x, int64_t ldx, const double* z, int64_t ldz, const double* s,
-               int64_t rows, int k, double* out);
-void lowrank_coef(dsvd_ctx* ctx, const double* w, int64_t ldw, const double* s, const double* v, int64_t ldv,
-                  int64_t rows, int k, double* coef);
-void lowrank_sub(dsvd_ctx* ctx, const double* u, int64_t ldu, const double* coef, int k, double* y, int64_t ldy,
-                 int64_t rows);
-void scale_vec(dsvd_ctx* ctx, const double* z, int64_t ldz, const double* nrm, double* v, int64_t ldv,
-               int64_t rows, int32_t* zero);
-}  // namespace dsvd
 #include "eig.cuh"
 #include "rng.cuh"
 #include "sparse.cuh"
@@ -71,29 +60,14 @@ void set_error(const char* msg, long long index) {
     t_err_index = index;
 }
 
-namespace {
-
 void set_device(dsvd_ctx* ctx) { DSVD_CUDA_CHECK(cudaSetDevice(ctx->device)); }
 
-void count_launch(int n = 1) { g_launches += n; }
+void count_launch(int n) { g_launches += n; }
+
+namespace {
 
 // ---- matrix construction --------------------------------------------------
 
-struct CsrAlloc {
-    // allocate through the context arena (prefix) or as owned buffers
-    dsvd_ctx* ctx;
-    std::string prefix;
-    std::vector<void*>* owned;
-    void* get(const std::string& name, size_t bytes) {
-        if (owned) {
-            void* p = nullptr;
-            DSVD_CUDA_CHECK(cudaMalloc(&p, bytes > 0 ? bytes : 1));
-            owned->push_back(p);
-            return p;
-        }
-        return ctx->buf(prefix + name, bytes);
-    }
-};
 
 // Chunk list of the rows longer than m.split_chunk (the prefix m.hub_rows of
 // m.order): each split row is cut into near-equal CSR ranges of at most
@@ -181,16 +155,13 @@ void build_chunks(dsvd_ctx* ctx, CsrAlloc& al, DevCsr& m, const std::string& tag
 }
 
 // Partial-row workspace for the split chunks of `a` at width ld.
-double* partial_for(dsvd_ctx* ctx, const DevCsr& a, int64_t ld) {
-    if (a.nchunks == 0) return nullptr;
-    return ctx->tbuf<double>("spmm.partial", a.nchunks * ld);
-}
+}  // namespace
 
 // Device CSR (+ transpose + row orders) from int64 offsets / indices and
 // values already on the device.
 void build_pair(dsvd_ctx* ctx, CsrAlloc& al, int64_t rows, int64_t cols, int64_t nnz,
                 const int64_t* d_off, const int64_t* d_idx64, const double* d_val, DevCsr& a,
-                DevCsr& at, bool copy_inputs, cudaEvent_t values_ready = nullptr) {
+                DevCsr& at, bool copy_inputs, cudaEvent_t values_ready) {
     cudaStream_t st = ctx->stream;
     if (rows < 0 || cols < 0 || nnz < 0) fail(DSVD_SHAPE, "sparse matrix with negative dimension");
     if (rows > 0x7fffffffLL || cols > 0x7fffffffLL)
@@ -291,6 +262,8 @@ void upload_pair(dsvd_ctx* ctx, CsrAlloc& al, int64_t rows, int64_t cols, int64_
     }
     build_pair(ctx, al, rows, cols, nnz, d_off, d_idx64, d_val, a, at, false, vals);
 }
+
+namespace {
 
 // ---- config validation (solver.cpp:15-32) ---------------------------------
 
@@ -647,24 +620,6 @@ void end_profile(dsvd_ctx* ctx, int64_t launches_before) {
     }
 }
 
-// Run `f` with the boundary contract: Failure -> status code + message.
-template <class F>
-int guarded(F&& f) {
-    try {
-        f();
-        return DSVD_OK;
-    } catch (const Failure& e) {
-        t_err = e.what();
-        t_err_index = e.index;
-        return e.code;
-    } catch (const std::bad_alloc& e) {
-        t_err = "host allocation failed";
-        return DSVD_OOM;
-    } catch (const std::exception& e) {
-        t_err = e.what();
-        return DSVD_OTHER;
-    }
-}
 
 // basic_core + finalize_col_basis (solver.cpp:118-141, :166-176) on the pair
 // (A, AT) as given: Omega = gaussian_matrix(n, l, seed), q = orth(A Omega),
@@ -1123,362 +1078,6 @@ int dsvd_matrix_bench_spmm(dsvd_matrix* m, int transpose, int64_t l, int variant
     });
 }
 
-// ---- inputs: validation, DSH1 cache, COO assembly ------------------------------------
-
-namespace {
-// Device validation of a CSR already in HBM, raising the reference's error.
-void validate_device_csr(dsvd_ctx* ctx, int64_t rows, int64_t cols, int64_t nnz, const int64_t* d_off,
-                         const int64_t* d_idx, const double* d_val) {
-    if (rows < 0 || cols < 0) fail(DSVD_SHAPE, "sparse matrix with negative dimension");
-    int64_t fb[2] = {0, 0};
-    DSVD_CUDA_CHECK(cudaMemcpyAsync(&fb[0], d_off, sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
-    DSVD_CUDA_CHECK(cudaMemcpyAsync(&fb[1], d_off + rows, sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
-    unsigned long long* first = ctx->tbuf<unsigned long long>("val.first", 1);
-    csr_validate(d_off, d_idx, d_val, rows, cols, nnz, first, ctx->stream);
-    unsigned long long hf = ~0ull;
-    DSVD_CUDA_CHECK(cudaMemcpyAsync(&hf, first, sizeof(hf), cudaMemcpyDeviceToHost, ctx->stream));
-    DSVD_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
-    if (fb[0] != 0 || fb[1] != nnz) fail(DSVD_SHAPE, "offsets must span [0, nnz]");
-    if (hf == ~0ull) return;
-    const int64_t row = static_cast<int64_t>(hf >> 3);
-    const std::string r = std::to_string(row);
-    switch (static_cast<int>(hf & 7)) {
-        case 0: fail(DSVD_SHAPE, "offsets must be non-decreasing");
-        case 1: fail(DSVD_SHAPE, "column index out of range in row " + r);
-        case 2: fail(DSVD_SHAPE, "column indices not strictly increasing in row " + r);
-        case 3: fail(DSVD_NUMERICAL, "non-finite value in row " + r);
-        default: fail(DSVD_NUMERICAL, "explicit zero stored in row " + r);
-    }
-}
-}  // namespace
-
-int dsvd_csr_validate(dsvd_ctx* ctx, int64_t rows, int64_t cols, int64_t nnz, const int64_t* offsets,
-                      const int64_t* col_indices, const double* values) {
-    return guarded([&] {
-        set_device(ctx);
-        if (rows < 0 || cols < 0 || nnz < 0) fail(DSVD_SHAPE, "sparse matrix with negative dimension");
-        int64_t* off = ctx->tbuf<int64_t>("val.off", rows + 1);
-        int64_t* idx = ctx->tbuf<int64_t>("val.idx", nnz);
-        double* val = ctx->tbuf<double>("val.val", nnz);
-        cudaStream_t st = ctx->stream;
-        DSVD_CUDA_CHECK(cudaMemcpyAsync(off, offsets, sizeof(int64_t) * (rows + 1), cudaMemcpyHostToDevice, st));
-        if (nnz) {
-            DSVD_CUDA_CHECK(cudaMemcpyAsync(idx, col_indices, sizeof(int64_t) * nnz, cudaMemcpyHostToDevice, st));
-            DSVD_CUDA_CHECK(cudaMemcpyAsync(val, values, sizeof(double) * nnz, cudaMemcpyHostToDevice, st));
-        }
-        validate_device_csr(ctx, rows, cols, nnz, off, idx, val);
-    });
-}
-
-namespace {
-constexpr char kDsh1[4] = {'D', 'S', 'H', '1'};
-}
-
-int dsvd_save_cache(const char* path, int64_t rows, int64_t cols, int64_t nnz, const int64_t* offsets,
-                    const int64_t* col_indices, const double* values) {
-    return guarded([&] {
-        std::FILE* f = std::fopen(path, "wb");
-        if (!f) fail(DSVD_OTHER, std::string("cannot open ") + path + " for writing");
-        const uint64_t dims[3] = {static_cast<uint64_t>(rows), static_cast<uint64_t>(cols),
-                                  static_cast<uint64_t>(nnz)};
-        bool ok = std::fwrite(kDsh1, 1, 4, f) == 4 && std::fwrite(dims, 8, 3, f) == 3 &&
-                  std::fwrite(offsets, 8, static_cast<size_t>(rows + 1), f) == static_cast<size_t>(rows + 1) &&
-                  std::fwrite(col_indices, 8, static_cast<size_t>(nnz), f) == static_cast<size_t>(nnz) &&
-                  std::fwrite(values, 8, static_cast<size_t>(nnz), f) == static_cast<size_t>(nnz);
-        ok = (std::fclose(f) == 0) && ok;
-        if (!ok) fail(DSVD_OTHER, std::string("failed writing ") + path);
-    });
-}
-
-int dsvd_matrix_load_cache(dsvd_ctx* ctx, const char* path, int validate, dsvd_matrix** out, int64_t* dims_out) {
-    return guarded([&] {
-        set_device(ctx);
-        std::FILE* f = std::fopen(path, "rb");
-        if (!f) fail(DSVD_OTHER, std::string("cannot open ") + path);
-        struct Closer {
-            std::FILE* f;
-            ~Closer() { std::fclose(f); }
-        } closer{f};
-        char magic[4];
-        uint64_t dims[3];
-        if (std::fread(magic, 1, 4, f) != 4) fail(DSVD_FORMAT, "truncated cache file");
-        if (std::memcmp(magic, kDsh1, 4) != 0) fail(DSVD_FORMAT, "not a DSH1 cache file");
-        if (std::fread(dims, 8, 3, f) != 3) fail(DSVD_FORMAT, "truncated cache file");
-        const int64_t rows = static_cast<int64_t>(dims[0]), cols = static_cast<int64_t>(dims[1]),
-                      nnz = static_cast<int64_t>(dims[2]);
-        // one pinned staging buffer: offsets | indices | values, read then uploaded;
-        // a header promising more than the file holds is a truncated file
-        const long here = std::ftell(f);
-        std::fseek(f, 0, SEEK_END);
-        const uint64_t avail = static_cast<uint64_t>(std::ftell(f) - here);
-        std::fseek(f, here, SEEK_SET);
-        if (dims[0] >= avail / 8 || dims[2] > avail / 16 || 8 * (dims[0] + 1 + 2 * dims[2]) > avail)
-            fail(DSVD_FORMAT, "truncated cache file");
-        const size_t bytes = sizeof(int64_t) * (static_cast<size_t>(rows) + 1 + 2 * static_cast<size_t>(nnz));
-        void* host = nullptr;
-        DSVD_CUDA_CHECK(cudaHostAlloc(&host, bytes, cudaHostAllocDefault));
-        struct Freer {
-            void* p;
-            ~Freer() { cudaFreeHost(p); }
-        } freer{host};
-        if (std::fread(host, 1, bytes, f) != bytes) fail(DSVD_FORMAT, "truncated cache file");
-        const int64_t* off = static_cast<const int64_t*>(host);
-        const int64_t* idx = off + rows + 1;
-        const double* val = reinterpret_cast<const double*>(idx + nnz);
-        std::unique_ptr<dsvd_matrix> m(new dsvd_matrix());
-        m->ctx = ctx;
-        m->device = ctx->device;
-        CsrAlloc al{ctx, "", &m->owned};
-        try {
-            if (validate) {
-                // a.validate() (matrix_market.cpp:274) on the device, before the pair is built
-                int64_t* d_off = ctx->tbuf<int64_t>("val.off", rows + 1);
-                int64_t* d_idx = ctx->tbuf<int64_t>("val.idx", nnz);
-                double* d_val = ctx->tbuf<double>("val.val", nnz);
-                cudaStream_t st = ctx->stream;
-                DSVD_CUDA_CHECK(cudaMemcpyAsync(d_off, off, sizeof(int64_t) * (rows + 1), cudaMemcpyHostToDevice, st));
-                if (nnz) {
-                    DSVD_CUDA_CHECK(cudaMemcpyAsync(d_idx, idx, sizeof(int64_t) * nnz, cudaMemcpyHostToDevice, st));
-                    DSVD_CUDA_CHECK(cudaMemcpyAsync(d_val, val, sizeof(double) * nnz, cudaMemcpyHostToDevice, st));
-                }
-                validate_device_csr(ctx, rows, cols, nnz, d_off, d_idx, d_val);
-                build_pair(ctx, al, rows, cols, nnz, d_off, d_idx, d_val, m->a, m->at, true);
-            } else {
-                upload_pair(ctx, al, rows, cols, nnz, off, idx, val, m->a, m->at);
-                DSVD_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));  // the staging buffer dies here
-            }
-        } catch (...) {
-            for (void* p : m->owned) cudaFree(p);
-            throw;
-        }
-        if (dims_out) {
-            dims_out[0] = rows;
-            dims_out[1] = cols;
-            dims_out[2] = nnz;
-        }
-        *out = m.release();
-    });
-}
-
-namespace {
-// assemble() (matrix_market.cpp:90-115) of host triplets into the context's
-// COO result buffers (dsvd_coo_fetch / dsvd_matrix_from_coo read them).
-int64_t assemble_host_triplets(dsvd_ctx* ctx, int64_t rows, int64_t cols, int64_t n, const int64_t* r,
-                               const int64_t* c, const double* v) {
-    if (rows < 0 || cols < 0 || n < 0) fail(DSVD_SHAPE, "sparse matrix with negative dimension");
-    if (n > 0x7fffffffLL) fail(DSVD_UNSUPPORTED, "more than 2^31 - 1 triplets per assembly");
-    cudaStream_t st = ctx->stream;
-    int64_t* dr = ctx->tbuf<int64_t>("coo.r", n);
-    int64_t* dc = ctx->tbuf<int64_t>("coo.c", n);
-    double* dv = ctx->tbuf<double>("coo.v", n);
-    if (n) {
-        DSVD_CUDA_CHECK(cudaMemcpyAsync(dr, r, sizeof(int64_t) * n, cudaMemcpyHostToDevice, st));
-        DSVD_CUDA_CHECK(cudaMemcpyAsync(dc, c, sizeof(int64_t) * n, cudaMemcpyHostToDevice, st));
-        DSVD_CUDA_CHECK(cudaMemcpyAsync(dv, v, sizeof(double) * n, cudaMemcpyHostToDevice, st));
-    }
-    int64_t* off = ctx->tbuf<int64_t>("coo.off", rows + 1);
-    int64_t* idx = ctx->tbuf<int64_t>("coo.idx", n);
-    double* val = ctx->tbuf<double>("coo.val", n);
-    int32_t* bad = ctx->tbuf<int32_t>("coo.bad", 1);
-    ctx->coo_rows = ctx->coo_cols = ctx->coo_nnz = -1;
-    const int64_t nnz =
-        coo_assemble(dr, dc, dv, n, rows, cols, ctx->buf("coo.scratch", coo_scratch_bytes(n)), off, idx, val, bad, st);
-    int32_t hb = 0;
-    DSVD_CUDA_CHECK(cudaMemcpyAsync(&hb, bad, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-    DSVD_CUDA_CHECK(cudaStreamSynchronize(st));
-    if (hb) fail(DSVD_SHAPE, "coordinate out of range");
-    ctx->coo_rows = rows;
-    ctx->coo_cols = cols;
-    ctx->coo_nnz = nnz;
-    return nnz;
-}
-
-void require_coo(dsvd_ctx* ctx) {
-    if (ctx->coo_rows < 0) fail(DSVD_CONFIG, "no assembled matrix in this context");
-}
-}  // namespace
-
-int dsvd_coo_assemble(dsvd_ctx* ctx, int64_t rows, int64_t cols, int64_t n, const int64_t* r, const int64_t* c,
-                      const double* v, int64_t* nnz_out) {
-    return guarded([&] {
-        set_device(ctx);
-        *nnz_out = assemble_host_triplets(ctx, rows, cols, n, r, c, v);
-    });
-}
-
-int dsvd_mtx_assemble(dsvd_ctx* ctx, const char* path, int64_t* dims) {
-    return guarded([&] {
-        set_device(ctx);
-        MtxTriplets t;
-        const MtxStatus stt = mtx_read(path, t);
-        if (stt.code != DSVD_OK) fail(stt.code, stt.what, stt.code == DSVD_PARSE ? stt.line : -1);
-        const int64_t nnz = assemble_host_triplets(ctx, t.rows, t.cols, static_cast<int64_t>(t.v.size()), t.r.data(),
-                                                   t.c.data(), t.v.data());
-        dims[0] = t.rows;
-        dims[1] = t.cols;
-        dims[2] = nnz;
-    });
-}
-
-namespace {
-thread_local MtxTriplets t_mtx;  // dsvd_mtx_read -> dsvd_mtx_fetch
-}
-
-int dsvd_mtx_read(const char* path, int64_t* dims) {
-    return guarded([&] {
-        t_mtx = MtxTriplets{};
-        const MtxStatus stt = mtx_read(path, t_mtx);
-        if (stt.code != DSVD_OK) fail(stt.code, stt.what, stt.code == DSVD_PARSE ? stt.line : -1);
-        dims[0] = t_mtx.rows;
-        dims[1] = t_mtx.cols;
-        dims[2] = static_cast<int64_t>(t_mtx.v.size());
-    });
-}
-
-int dsvd_mtx_fetch(int64_t* r, int64_t* c, double* v) {
-    return guarded([&] {
-        std::copy(t_mtx.r.begin(), t_mtx.r.end(), r);
-        std::copy(t_mtx.c.begin(), t_mtx.c.end(), c);
-        std::copy(t_mtx.v.begin(), t_mtx.v.end(), v);
-        t_mtx = MtxTriplets{};
-    });
-}
-
-namespace {
-thread_local DenseArray t_dense;          // dsvd_dense_read -> dsvd_dense_fetch
-thread_local std::vector<double> t_spec;  // dsvd_spectrum_read -> dsvd_spectrum_fetch
-void raise_mtx(const MtxStatus& stt) {
-    if (stt.code != DSVD_OK) fail(stt.code, stt.what, stt.code == DSVD_PARSE ? stt.line : -1);
-}
-}  // namespace
-
-int dsvd_dense_read(const char* path, int64_t* dims) {
-    return guarded([&] {
-        t_dense = DenseArray{};
-        raise_mtx(dense_read(path, t_dense));
-        dims[0] = t_dense.rows;
-        dims[1] = t_dense.cols;
-    });
-}
-
-int dsvd_dense_fetch(double* colmajor) {
-    return guarded([&] {
-        std::copy(t_dense.data.begin(), t_dense.data.end(), colmajor);
-        t_dense = DenseArray{};
-    });
-}
-
-int dsvd_dense_write(const char* path, int64_t rows, int64_t cols, const double* colmajor) {
-    return guarded([&] { raise_mtx(dense_write(path, rows, cols, colmajor)); });
-}
-
-int dsvd_spectrum_read(const char* path, int64_t* n) {
-    return guarded([&] {
-        t_spec.clear();
-        raise_mtx(spectrum_read(path, t_spec));
-        *n = static_cast<int64_t>(t_spec.size());
-    });
-}
-
-int dsvd_spectrum_fetch(double* sigmas) {
-    return guarded([&] {
-        std::copy(t_spec.begin(), t_spec.end(), sigmas);
-        t_spec.clear();
-    });
-}
-
-int dsvd_spectrum_write(const char* path, const double* sigmas, int64_t n) {
-    return guarded([&] { raise_mtx(spectrum_write(path, sigmas, n)); });
-}
-
-int dsvd_matrix_from_coo(dsvd_ctx* ctx, dsvd_matrix** out) {
-    return guarded([&] {
-        set_device(ctx);
-        require_coo(ctx);
-        std::unique_ptr<dsvd_matrix> m(new dsvd_matrix());
-        m->ctx = ctx;
-        m->device = ctx->device;
-        CsrAlloc al{ctx, "", &m->owned};
-        try {
-            build_pair(ctx, al, ctx->coo_rows, ctx->coo_cols, ctx->coo_nnz, ctx->tbuf<int64_t>("coo.off", 1),
-                       ctx->tbuf<int64_t>("coo.idx", 1), ctx->tbuf<double>("coo.val", 1), m->a, m->at, true);
-            DSVD_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
-        } catch (...) {
-            for (void* p : m->owned) cudaFree(p);
-            throw;
-        }
-        *out = m.release();
-    });
-}
-
-int dsvd_synth_rmat(dsvd_ctx* ctx, int scale, int64_t draws, double a, double b, double c, int value_mode,
-                    uint64_t seed, dsvd_matrix** out, int64_t* nnz_out) {
-    return guarded([&] {
-        set_device(ctx);
-        if (scale < 1 || scale > 30) fail(DSVD_SHAPE, "rmat: scale must be in [1, 30]");
-        if (draws < 0 || draws > 0x7fffffffLL) fail(DSVD_SHAPE, "rmat: draws must be in [0, 2^31)");
-        if (!(a >= 0 && b >= 0 && c >= 0 && a + b + c <= 1.0)) fail(DSVD_CONFIG, "rmat: need a, b, c >= 0, a+b+c <= 1");
-        if (value_mode != 0 && value_mode != 1) fail(DSVD_CONFIG, "rmat: value_mode 0 (ones) or 1 (uniform (0,1])");
-        RmatParams P;
-        P.scale = scale;
-        P.draws = draws;
-        P.t_a = static_cast<uint32_t>(std::llround(a * 65536.0));
-        P.t_ab = static_cast<uint32_t>(std::llround((a + b) * 65536.0));
-        P.t_abc = static_cast<uint32_t>(std::llround((a + b + c) * 65536.0));
-        P.value_mode = value_mode;
-        P.edge_seed = splitmix64_at(seed, 0);
-        P.val_seed = splitmix64_at(seed, 1);
-        const int64_t n = int64_t(1) << scale;
-        int64_t* off = ctx->tbuf<int64_t>("rmat.off", n + 1);
-        int64_t* idx = ctx->tbuf<int64_t>("upload.idx64", draws);
-        double* val = ctx->tbuf<double>("rmat.val", draws);
-        const int64_t nnz = rmat_generate(P, ctx->buf("rmat.scratch", rmat_scratch_bytes(draws)), off, idx, val,
-                                          ctx->stream);
-        ctx->release("rmat.scratch");
-        std::unique_ptr<dsvd_matrix> m(new dsvd_matrix());
-        m->ctx = ctx;
-        m->device = ctx->device;
-        CsrAlloc al{ctx, "", &m->owned};
-        try {
-            build_pair(ctx, al, n, n, nnz, off, idx, val, m->a, m->at, true);
-            DSVD_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
-        } catch (...) {
-            for (void* p : m->owned) cudaFree(p);
-            throw;
-        }
-        ctx->release("rmat.off");
-        ctx->release("rmat.val");
-        *nnz_out = nnz;
-        *out = m.release();
-    });
-}
-
-int dsvd_write_matrix_market(const char* path, int64_t rows, int64_t cols, const int64_t* offsets,
-                             const int64_t* col_indices, const double* values) {
-    return guarded([&] {
-        const MtxStatus stt = mtx_write(path, rows, cols, offsets, col_indices, values);
-        if (stt.code != DSVD_OK) fail(stt.code, stt.what);
-    });
-}
-
-int dsvd_coo_fetch(dsvd_ctx* ctx, int64_t* offsets, int64_t* col_indices, double* values) {
-    return guarded([&] {
-        set_device(ctx);
-        require_coo(ctx);
-        const int64_t rows = ctx->coo_rows, nnz = ctx->coo_nnz;
-        cudaStream_t st = ctx->stream;
-        DSVD_CUDA_CHECK(cudaMemcpyAsync(offsets, ctx->tbuf<int64_t>("coo.off", rows + 1), sizeof(int64_t) * (rows + 1),
-                                        cudaMemcpyDeviceToHost, st));
-        if (nnz) {
-            DSVD_CUDA_CHECK(cudaMemcpyAsync(col_indices, ctx->tbuf<int64_t>("coo.idx", 1), sizeof(int64_t) * nnz,
-                                            cudaMemcpyDeviceToHost, st));
-            DSVD_CUDA_CHECK(cudaMemcpyAsync(values, ctx->tbuf<double>("coo.val", 1), sizeof(double) * nnz,
-                                            cudaMemcpyDeviceToHost, st));
-        }
-        DSVD_CUDA_CHECK(cudaStreamSynchronize(st));
-    });
-}
-
 int dsvd_matrix_hub_rows(const dsvd_matrix* m, int64_t* hub_a, int64_t* hub_at) {
     return guarded([&] {
         *hub_a = m->a.hub_rows;
@@ -1618,159 +1217,6 @@ int dsvd_ctx_timer_stop(dsvd_ctx* ctx, double* elapsed_ms) {
         float ms = 0.f;
         DSVD_CUDA_CHECK(cudaEventElapsedTime(&ms, ctx->timer[0], ctx->timer[1]));
         *elapsed_ms = ms;
-    });
-}
-
-// ---- validation metrics (metrics.cpp:99-206) ----------------------------------------
-
-namespace {
-// Host column-major (rows x k) -> device row-major, stride ld.
-double* upload_block(dsvd_ctx* ctx, const std::string& tag, const double* h, int64_t rows, int64_t k,
-                     int64_t ld) {
-    double* cm = ctx->tbuf<double>(tag + ".cm", rows * k);
-    double* rm = ctx->tbuf<double>(tag, rows * ld);
-    DSVD_CUDA_CHECK(cudaMemcpyAsync(cm, h, sizeof(double) * rows * k, cudaMemcpyHostToDevice, ctx->stream));
-    colmajor_to_rowmajor(cm, rows, k, rm, ld, ctx->stream);
-    return rm;
-}
-void mspmm(dsvd_ctx* ctx, const DevCsr& A, const double* x, double* y, int64_t ld, int64_t l) {
-    spmm(SpmmArgs{&A, x, y, ld, l, nullptr, nullptr, nullptr}, ctx->stream, ctx->spmm_variant, ctx->side,
-         ctx->fork, ctx->join, partial_for(ctx, A, ld));
-}
-std::vector<double> col_norms_host(dsvd_ctx* ctx, const double* x, int64_t ldx, const double* z, int64_t ldz,
-                                   const double* s_dev, int64_t rows, int64_t k) {
-    double* d = ctx->tbuf<double>("met.norms", k);
-    col_norms(ctx, x, ldx, z, ldz, s_dev, rows, static_cast<int>(k), d);
-    std::vector<double> h(static_cast<size_t>(k));
-    DSVD_CUDA_CHECK(cudaMemcpyAsync(h.data(), d, sizeof(double) * k, cudaMemcpyDeviceToHost, ctx->stream));
-    DSVD_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
-    return h;
-}
-void require_sigmas(int64_t n_ref, int64_t count) {
-    if (n_ref < count)
-        fail(DSVD_DEGENERATE, "reference provides " + std::to_string(n_ref) + " singular values, need " +
-                                  std::to_string(count));
-}
-}  // namespace
-
-int dsvd_eps_pve(dsvd_ctx* ctx, const dsvd_matrix* m, const double* u, int64_t k, const double* sigmas,
-                 int64_t n_ref, double* out) {
-    return guarded([&] {
-        set_device(ctx);
-        if (k < 1) fail(DSVD_SHAPE, "eps_pve: U has no columns");
-        require_sigmas(n_ref, k + 1);
-        const double denom = sigmas[k] * sigmas[k];
-        if (denom == 0.0) fail(DSVD_DEGENERATE, "sigma_{k+1} is zero");
-        const DevCsr& A = m->a;
-        const int64_t ld = padded_ld(k);
-        double* U = upload_block(ctx, "met.U", u, A.rows, k, ld);
-        double* W = ctx->tbuf<double>("met.W", A.cols * ld);
-        mspmm(ctx, m->at, U, W, ld, k);  // A^T u_i
-        const std::vector<double> q = col_norms_host(ctx, W, ld, nullptr, 0, nullptr, A.cols, k);
-        double worst = 0.0;
-        for (int64_t i = 0; i < k; ++i) worst = std::max(worst, std::abs(sigmas[i] * sigmas[i] - q[i] * q[i]) / denom);
-        *out = worst;
-    });
-}
-
-int dsvd_eps_res(dsvd_ctx* ctx, const dsvd_matrix* m, const double* u, const double* s, const double* v, int64_t k,
-                 const double* sigmas, int64_t n_ref, double* out) {
-    return guarded([&] {
-        set_device(ctx);
-        if (k < 1) fail(DSVD_SHAPE, "eps_res: no triplets");
-        require_sigmas(n_ref, k);
-        const DevCsr& A = m->a;
-        const int64_t ld = padded_ld(k);
-        double* U = upload_block(ctx, "met.U", u, A.rows, k, ld);
-        double* V = upload_block(ctx, "met.V", v, A.cols, k, ld);
-        double* sd = ctx->tbuf<double>("met.s", k);
-        DSVD_CUDA_CHECK(cudaMemcpyAsync(sd, s, sizeof(double) * k, cudaMemcpyHostToDevice, ctx->stream));
-        double* W = ctx->tbuf<double>("met.W", A.cols * ld);
-        mspmm(ctx, m->at, U, W, ld, k);
-        const std::vector<double> r = col_norms_host(ctx, W, ld, V, ld, sd, A.cols, k);  // ||A^T u_i - s_i v_i||
-        double worst = 0.0;
-        for (int64_t i = 0; i < k; ++i) {
-            if (sigmas[i] == 0.0) fail(DSVD_DEGENERATE, "sigma_i is zero");
-            worst = std::max(worst, r[i] / sigmas[i]);
-        }
-        *out = worst;
-    });
-}
-
-int dsvd_max_triplet_residual(dsvd_ctx* ctx, const dsvd_matrix* m, const double* u, const double* s, const double* v,
-                              int64_t k, double* out) {
-    return guarded([&] {
-        set_device(ctx);
-        const DevCsr& A = m->a;
-        if (k < 1) {
-            *out = 0.0;
-            return;
-        }
-        const int64_t ld = padded_ld(k);
-        double* U = upload_block(ctx, "met.U", u, A.rows, k, ld);
-        double* V = upload_block(ctx, "met.V", v, A.cols, k, ld);
-        double* sd = ctx->tbuf<double>("met.s", k);
-        DSVD_CUDA_CHECK(cudaMemcpyAsync(sd, s, sizeof(double) * k, cudaMemcpyHostToDevice, ctx->stream));
-        double* AV = ctx->tbuf<double>("met.AV", A.rows * ld);
-        mspmm(ctx, A, V, AV, ld, k);
-        const std::vector<double> r = col_norms_host(ctx, AV, ld, U, ld, sd, A.rows, k);  // ||A v_i - s_i u_i||
-        double worst = 0.0;
-        for (int64_t i = 0; i < k; ++i) worst = std::max(worst, r[i]);
-        *out = worst;
-    });
-}
-
-int dsvd_eps_spec(dsvd_ctx* ctx, const dsvd_matrix* m, const double* u, const double* s, const double* v, int64_t k,
-                  const double* sigmas, int64_t n_ref, int64_t power_iters, uint64_t seed, double* out) {
-    return guarded([&] {
-        set_device(ctx);
-        if (k < 1) fail(DSVD_SHAPE, "eps_spec: no triplets");
-        require_sigmas(n_ref, k + 1);
-        const double sk1 = sigmas[k];
-        if (sk1 == 0.0) fail(DSVD_DEGENERATE, "sigma_{k+1} is zero");
-        cudaStream_t st = ctx->stream;
-        const DevCsr& A = m->a;
-        const int64_t rows = A.rows, cols = A.cols;
-        const int64_t ld = padded_ld(k), lv = padded_ld(1);  // vectors as rows x 4 blocks (column 0)
-        double* U = upload_block(ctx, "met.U", u, rows, k, ld);
-        double* V = upload_block(ctx, "met.V", v, cols, k, ld);
-        double* sd = ctx->tbuf<double>("met.s", k);
-        DSVD_CUDA_CHECK(cudaMemcpyAsync(sd, s, sizeof(double) * k, cudaMemcpyHostToDevice, st));
-        double* vv = ctx->tbuf<double>("met.v", cols * lv);
-        double* zz = ctx->tbuf<double>("met.z", cols * lv);
-        double* ww = ctx->tbuf<double>("met.w", rows * lv);
-        double* coef = ctx->tbuf<double>("met.coef", k);
-        double* nrm = ctx->tbuf<double>("met.nrm", 1);
-        int32_t* zero = ctx->tbuf<int32_t>("met.zero", 1);
-        DSVD_CUDA_CHECK(cudaMemsetAsync(zero, 0, sizeof(int32_t), st));
-        DSVD_CUDA_CHECK(cudaMemsetAsync(zz, 0, sizeof(double) * cols * lv, st));
-        gaussian_rowmajor(zz, cols, 1, lv, seed, st);  // gaussian_matrix(op.cols, 1, seed)
-        col_norms(ctx, zz, lv, nullptr, 0, nullptr, cols, 1, nrm);
-        DSVD_CUDA_CHECK(cudaMemsetAsync(vv, 0, sizeof(double) * cols * lv, st));
-        scale_vec(ctx, zz, lv, nrm, vv, lv, cols, zero);
-        // op(x) = A x - U diag(s) V^T x ; op^T(y) = A^T y - V diag(s) U^T y (metrics.cpp:146-153)
-        auto apply = [&]() {
-            mspmm(ctx, A, vv, ww, lv, 1);
-            lowrank_coef(ctx, V, ld, sd, vv, lv, cols, static_cast<int>(k), coef);
-            lowrank_sub(ctx, U, ld, coef, static_cast<int>(k), ww, lv, rows);
-        };
-        for (int64_t it = 0; it < power_iters; ++it) {
-            apply();
-            mspmm(ctx, m->at, ww, zz, lv, 1);
-            lowrank_coef(ctx, U, ld, sd, ww, lv, rows, static_cast<int>(k), coef);
-            lowrank_sub(ctx, V, ld, coef, static_cast<int>(k), zz, lv, cols);
-            col_norms(ctx, zz, lv, nullptr, 0, nullptr, cols, 1, nrm);
-            scale_vec(ctx, zz, lv, nrm, vv, lv, cols, zero);  // v = z / ||z|| (0 -> estimate 0)
-        }
-        apply();
-        double hn = 0.0;
-        int32_t hz = 0;
-        col_norms(ctx, ww, lv, nullptr, 0, nullptr, rows, 1, nrm);
-        DSVD_CUDA_CHECK(cudaMemcpyAsync(&hn, nrm, sizeof(double), cudaMemcpyDeviceToHost, st));
-        DSVD_CUDA_CHECK(cudaMemcpyAsync(&hz, zero, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-        DSVD_CUDA_CHECK(cudaStreamSynchronize(st));
-        const double norm = hz ? 0.0 : hn;
-        *out = (norm - sk1) / sk1;
     });
 }
 
