@@ -132,3 +132,31 @@ def test_dash_stops_at_the_first_passage_of_the_rule(dev):
         assert (ratio <= tol) == (j == n - 1), (j, ratio)
     truth = np.linalg.svd(dense(a), compute_uv=False)
     assert d.eps_pve(a, r.svd.u, truth, device=dev) <= 5e-2
+
+
+def test_acceptance_criterion4_underestimation_sweep(dev):
+    # acceptance.cpp:270-309: 50 matrices x 5 algorithm variants, sigma_hat <= sigma (1 + 1e-10)
+    worst = 0.0
+    for g in range(1, 51):
+        a = d.sparse_random(200, 100, 10, g, True)
+        truth = np.linalg.svd(dense(a), compute_uv=False)
+        for variant in range(5):
+            alg = ["basic", "basic", "shifted", "fixed_shift", "dash"][variant]
+            c = d.SolverConfig(k=10, s=5, p=-1 if alg == "dash" else 3, tol=1e-2, seed=100 + g,
+                               alg=d.Algorithm[alg],
+                               orth=d.Orthonormalizer.qr if variant == 1 else d.Orthonormalizer.eigsvd)
+            s = d.solve(a, c, device=dev).svd.s
+            worst = max(worst, float(np.max(s / truth[:10] - 1.0)))
+    assert worst <= 1e-10, worst
+
+
+def test_acceptance_criterion7_eig_svd_against_an_independent_svd(dev):
+    # acceptance.cpp:423-433: 100 Gaussian 2n x n matrices, sigma relative error <= 1e-8
+    worst = 0.0
+    for i in range(100):
+        n = 10 + (i % 45)
+        x = d.gaussian_matrix(2 * n, n, 1000 + i, device=dev)
+        fast = d.eig_svd(x, device=dev).s
+        slow = np.linalg.svd(x, compute_uv=False)
+        worst = max(worst, float(np.max(np.abs(fast - slow) / slow)))
+    assert worst <= 1e-8, worst
