@@ -160,3 +160,49 @@ def test_acceptance_criterion7_eig_svd_against_an_independent_svd(dev):
         slow = np.linalg.svd(x, compute_uv=False)
         worst = max(worst, float(np.max(np.abs(fast - slow) / slow)))
     assert worst <= 1e-8, worst
+
+
+@pytest.fixture(scope="module")
+def planted(oracle):
+    # dense2_matrix(1000, 0) (synthetic.cpp:51-70): U diag(1/sqrt(i+1)) V^T with U, V the
+    # Householder Q of seeded Gaussian matrices (the oracle's restatements of
+    # gaussian_matrix and qr_orth; the product is formed in numpy)
+    n = 1000
+    sig = 1.0 / np.sqrt(np.arange(1, n + 1, dtype=np.float64))
+    u = oracle.qr_orth(oracle.gaussian_matrix(n, n, oracle.splitmix64_at(0, 0)))
+    v = oracle.qr_orth(oracle.gaussian_matrix(n, n, oracle.splitmix64_at(0, 1)))
+    m = (u * sig) @ v.T
+    off = np.arange(0, n * n + 1, n, dtype=np.int64)
+    idx = np.tile(np.arange(n, dtype=np.int64), n)
+    return d.SparseMatrix(n, n, off, idx, np.ascontiguousarray(m).ravel()), sig
+
+
+def _eps(m, sig, alg, p, seed, dev):
+    r = m.solve(d.SolverConfig(k=100, s=50, p=p, seed=seed, alg=d.Algorithm[alg]))
+    return d.eps_pve(m, r.svd.u, sig, device=dev)
+
+
+def test_acceptance_criteria1_2_shifted_beats_basic_and_frozen(planted, dev):
+    # acceptance.cpp:96-189: on the planted 1000 x 1000 spectrum (k = 100, s = 50),
+    # criterion 1: shifted eps_pve < basic eps_pve in >= 90% of (seed, p) pairs,
+    #   p in {4, 8, 12, 16, 20}, 10 seeds, and the median ratio at p = 20 is <= 0.1;
+    # criterion 2: shifted <= frozen shift at p = 8 and 16 on >= 8 of 10 seeds
+    a, sig = planted
+    m = d.DeviceMatrix(a, dev)
+    wins = pairs = c2 = 0
+    ratios = []
+    for seed in range(1, 11):
+        e_s, e_b, e_f = {}, {}, {}
+        for p in (4, 8, 12, 16, 20):
+            e_s[p] = _eps(m, sig, "shifted", p, seed, dev)
+            e_b[p] = _eps(m, sig, "basic", p, seed, dev)
+            pairs += 1
+            wins += e_s[p] < e_b[p]
+        for p in (8, 16):
+            e_f[p] = _eps(m, sig, "fixed_shift", p, seed, dev)
+        ratios.append(e_s[20] / e_b[20])
+        c2 += all(e_s[p] <= e_f[p] for p in (8, 16))
+    m.close()
+    assert wins >= int(0.9 * pairs + 0.5), (wins, pairs)
+    assert float(np.median(ratios)) <= 0.1, ratios
+    assert c2 >= 8, c2
