@@ -59,4 +59,16 @@ struct Control {
     int32_t status_src;    // 1: the status was raised by the QR orthonormalizer
 };
 
+#ifdef __CUDACC__
+// Gate words (Control::stopped / stop_pending) can be set by a kernel on
+// another stream while the reading kernel runs: read them at L2, not through
+// the non-coherent read-only path, so late blocks see a stop and skip.
+__device__ __forceinline__ bool gate_closed(const int32_t* gate) {
+    if (gate == nullptr) return false;
+    int32_t v;
+    asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(gate));
+    return v != 0;
+}
+#endif
+
 }  // namespace dsvd

@@ -327,7 +327,7 @@ void solve_rescale(dsvd_ctx* ctx, const double* c, int64_t n, int64_t K, int64_t
 // (s, V) of the row-major block c (rows x l, stride ld); U is left to the caller.
 void eig_svd_factors(dsvd_ctx* ctx, const double* c, int64_t rows, int64_t l, int64_t ld,
                      EigSvdOut& o, Control* ctrl, const LoopStep* loop, const int32_t* gate,
-                     bool reduce_gram = false, int64_t floor_rows = -1) {
+                     bool reduce_gram = false, int64_t floor_rows = -1, cudaStream_t eig_stream = nullptr) {
     cudaStream_t st = ctx->stream;
     double* G = ctx->tbuf<double>("eig.G", l * l);
     int sp = ctx->span_begin(K_GRAM);
@@ -346,6 +346,20 @@ void eig_svd_factors(dsvd_ctx* ctx, const double* c, int64_t rows, int64_t l, in
         comm_allreduce_sum(ctx, G, static_cast<size_t>(l * l));
         ctx->span_end(sp);
     }
+    // the l x l eig and the factor assembly (latency-bound, a few SMs) may run
+    // on eig_stream, after the Gram (all SMs) on ctx->stream
+    const cudaStream_t main_stream = ctx->stream;
+    if (eig_stream != nullptr) {
+        DSVD_CUDA_CHECK(cudaEventRecord(ctx->ev_t, st));
+        DSVD_CUDA_CHECK(cudaStreamWaitEvent(eig_stream, ctx->ev_t, 0));
+        st = eig_stream;
+        ctx->stream = eig_stream;  // spans, restored below
+    }
+    struct Restore {
+        dsvd_ctx* c;
+        cudaStream_t s;
+        ~Restore() { c->stream = s; }
+    } restore{ctx, main_stream};
     EigWorkspace ew;
     void* em = ctx->buf("eig.ws", eig_workspace_bytes(static_cast<int>(l), kMaxSweeps));
     eig_workspace_bind(ew, static_cast<int>(l), kMaxSweeps, em);
@@ -451,22 +465,6 @@ void solve_tall(dsvd_ctx* ctx, const DevCsr& A, const DevCsr& AT, const dsvd_con
     ctx->omega_pending = false;
     ctx->span_end(sp);
 
-    // Q = eigSVD(A^T Omega).u
-    sp = ctx->span_begin(K_SPMM2);
-    spmm(SpmmArgs{&AT, Y, T, ld, l, nullptr, nullptr, nullptr}, st, ctx->spmm_variant, ctx->side, ctx->fork,
-         ctx->join, partial_for(ctx, AT, ld));
-    count_launch();
-    ctx->span_end(sp);
-    if (sharded) {
-        sp = ctx->span_begin(K_COMM);
-        comm_allreduce_sum(ctx, T, static_cast<size_t>(n * ld));
-        ctx->span_end(sp);
-    }
-    eig_svd_factors(ctx, T, n, l, ld, eo, ctrl, nullptr, nullptr);
-    sp = ctx->span_begin(K_RESCALE);
-    solve_rescale(ctx, T, n, l, ld, W, l, inv_s, l, Qb[0], ld, 0, nullptr);
-    ctx->span_end(sp);
-
     LoopStep ls;
     ls.k = k;
     ls.tol = cfg.tol;
@@ -475,78 +473,213 @@ void solve_tall(dsvd_ctx* ctx, const DevCsr& A, const DevCsr& AT, const dsvd_con
     ls.s_hat = d_shat;
     ls.cap = cap;
     ls.s_stored = s_stored;
-
     if (dash && ctx->host_flags == nullptr) {
         DSVD_CUDA_CHECK(cudaMallocHost(&ctx->host_flags, sizeof(int32_t) * (kLookahead + 1)));
     }
     std::vector<cudaEvent_t> flag_ev(kLookahead + 1, nullptr);
-    int cur = 0;
-    for (int64_t j = 1; j <= max_iters; ++j) {
-        if (dash && !observer && j > kLookahead) {
-            const int slot = static_cast<int>((j - kLookahead) % (kLookahead + 1));
-            DSVD_CUDA_CHECK(cudaEventSynchronize(flag_ev[slot]));
-            if (ctx->host_flags[slot]) break;
+    Control hc;
+    const double* Qf = nullptr;
+    if (ctx->pipeline != 0) {
+        // Deferred rescale. With Q_{j-1} = T_{j-1} W_{j-1} (W = V diag(1/s) of
+        // eigSVD(T_{j-1}), sign convention folded in), the reference's
+        //   T_j = A^T (A Q_{j-1}) - alpha Q_{j-1}            (solver.cpp:92-95)
+        // equals (A^T (A T_{j-1}) - alpha T_{j-1}) W_{j-1}. Both SpMM passes run on
+        // T_{j-1}, so once the Gram of T_{j-1} is formed (all SMs), its l x l eig
+        // and the shift/stop update (a latency-bound chain on a few SMs) run on
+        // the priority stream beside the A T_{j-1} pass instead of between the
+        // passes; the A^T pass waits for them
+        // (it needs the updated alpha), and one rescale forms T_j. The trace,
+        // stop rule and alpha updates are the same device code on the same
+        // values; Q_N = T_N W_N is formed once for the finalize.
+        double* Tb[2] = {T, Qb[0]};
+        double* P = Qb[1];
+        // Gram on st (all SMs), then the eig chain on the priority stream
+        auto eig_async = [&](const double* tj, const LoopStep* lsp, const int32_t* g) {
+            eig_svd_factors(ctx, tj, n, l, ld, eo, ctrl, lsp, g, false, -1, ctx->eig);
+            DSVD_CUDA_CHECK(cudaEventRecord(ctx->ev_eig, ctx->eig));
+        };
+        double* Qobs[2] = {nullptr, nullptr};
+        if (observer) {
+            Qobs[0] = ctx->tbuf<double>("obs.q0", n * ld);
+            Qobs[1] = ctx->tbuf<double>("obs.q1", n * ld);
         }
-        loop_begin(ctrl, st);
-        count_launch();
-        // Y = A Q
-        sp = ctx->span_begin(K_SPMM1);
-        spmm(SpmmArgs{&A, Qb[cur], Y, ld, l, nullptr, nullptr, gate}, st, ctx->spmm_variant, ctx->side,
-             ctx->fork, ctx->join, partial_for(ctx, A, ld));
-        count_launch();
-        ctx->span_end(sp);
-        // T = A^T Y - alpha Q  (add_scaled skipped when alpha == 0)
+        // T_0 = A^T Omega; eigSVD(T_0) gives Q_0 = T_0 W_0 (solver.cpp:84)
         sp = ctx->span_begin(K_SPMM2);
-        spmm(SpmmArgs{&AT, Y, T, ld, l, sharded ? nullptr : Qb[cur], sharded ? nullptr : &ctrl->alpha,
-                      gate},
-             st, ctx->spmm_variant, ctx->side, ctx->fork, ctx->join, partial_for(ctx, AT, ld));
+        spmm(SpmmArgs{&AT, Y, Tb[0], ld, l, nullptr, nullptr, nullptr}, st, ctx->spmm_variant, ctx->side,
+             ctx->fork, ctx->join, partial_for(ctx, AT, ld));
         count_launch();
         ctx->span_end(sp);
         if (sharded) {
-            // sum the partials first, then apply the shift once (solver.cpp:94)
+            sp = ctx->span_begin(K_COMM);
+            comm_allreduce_sum(ctx, Tb[0], static_cast<size_t>(n * ld));
+            ctx->span_end(sp);
+        }
+        eig_async(Tb[0], nullptr, nullptr);
+        if (observer) {
+            DSVD_CUDA_CHECK(cudaStreamWaitEvent(st, ctx->ev_eig, 0));
+            solve_rescale(ctx, Tb[0], n, l, ld, W, l, inv_s, l, Qobs[0], ld, 0, nullptr);
+        }
+        for (int64_t j = 1; j <= max_iters; ++j) {
+            if (dash && !observer && j > kLookahead) {
+                const int slot = static_cast<int>((j - kLookahead) % (kLookahead + 1));
+                DSVD_CUDA_CHECK(cudaEventSynchronize(flag_ev[slot]));
+                if (ctx->host_flags[slot]) break;
+            }
+            double* tprev = Tb[(j - 1) % 2];
+            // Z = A T_{j-1}, beside eigSVD(T_{j-1}) (its output is only needed if
+            // the loop continues, so a stop decided there just skips the rest)
+            // (dash: gated on stop_pending, which eigSVD(T_{j-1}) may set while
+            // this pass runs — blocks starting after a stop skip their rows)
+            sp = ctx->span_begin(K_SPMM1);
+            spmm(SpmmArgs{&A, tprev, Y, ld, l, nullptr, nullptr, dash ? &ctrl->stop_pending : gate}, st,
+                 ctx->spmm_variant, ctx->side,
+                 ctx->fork, ctx->join, partial_for(ctx, A, ld));
+            count_launch();
+            ctx->span_end(sp);
+            DSVD_CUDA_CHECK(cudaStreamWaitEvent(st, ctx->ev_eig, 0));
+            loop_begin(ctrl, st);
+            count_launch();
+            // P = A^T Z - alpha T_{j-1}  (the shift skipped when alpha == 0)
+            sp = ctx->span_begin(K_SPMM2);
+            spmm(SpmmArgs{&AT, Y, P, ld, l, sharded ? nullptr : tprev, sharded ? nullptr : &ctrl->alpha, gate},
+                 st, ctx->spmm_variant, ctx->side, ctx->fork, ctx->join, partial_for(ctx, AT, ld));
+            count_launch();
+            ctx->span_end(sp);
+            if (sharded) {
+                sp = ctx->span_begin(K_COMM);
+                comm_allreduce_sum(ctx, P, static_cast<size_t>(n * ld));
+                ctx->span_end(sp);
+                shift_update(P, tprev, n * ld, &ctrl->alpha, gate, st);
+                count_launch();
+            }
+            // T_j = P W_{j-1} diag(1/s_{j-1})  (= A^T A Q_{j-1} - alpha Q_{j-1})
+            sp = ctx->span_begin(K_RESCALE);
+            solve_rescale(ctx, P, n, l, ld, W, l, inv_s, l, Tb[j % 2], ld, 0, gate);
+            ctx->span_end(sp);
+            eig_async(Tb[j % 2], &ls, gate);
+            if (dash) {
+                const int slot = static_cast<int>(j % (kLookahead + 1));
+                if (flag_ev[slot] == nullptr) flag_ev[slot] = ctx->event();
+                DSVD_CUDA_CHECK(cudaMemcpyAsync(&ctx->host_flags[slot], &ctrl->stop_pending, sizeof(int32_t),
+                                                cudaMemcpyDeviceToHost, ctx->eig));
+                DSVD_CUDA_CHECK(cudaEventRecord(flag_ev[slot], ctx->eig));
+            }
+            if (observer) {
+                DSVD_CUDA_CHECK(cudaStreamWaitEvent(st, ctx->ev_eig, 0));
+                Control oc = read_control(ctx, ctrl);
+                raise_device_status(oc);
+                solve_rescale(ctx, Tb[j % 2], n, l, ld, W, l, inv_s, l, Qobs[j % 2], ld, 0, nullptr);
+                std::vector<double> qb = to_host_colmajor(ctx, Qobs[(j - 1) % 2], n, l, ld);
+                std::vector<double> qa = to_host_colmajor(ctx, Qobs[j % 2], n, l, ld);
+                std::vector<double> sh(static_cast<size_t>(l));
+                double alpha_used = 0.0;
+                DSVD_CUDA_CHECK(cudaMemcpy(sh.data(), d_shat + (j - 1) * l, sizeof(double) * l,
+                                           cudaMemcpyDeviceToHost));
+                DSVD_CUDA_CHECK(cudaMemcpy(&alpha_used, d_alphas + (j - 1), sizeof(double),
+                                           cudaMemcpyDeviceToHost));
+                observer(j, alpha_used, sh.data(), l, qb.data(), qa.data(), n, user);
+                if (oc.stop_pending) break;
+            }
+        }
+        DSVD_CUDA_CHECK(cudaEventRecord(ctx->ev_eig, ctx->eig));  // incl. the last flag copy
+        DSVD_CUDA_CHECK(cudaStreamWaitEvent(st, ctx->ev_eig, 0));
+        hc = read_control(ctx, ctrl);
+        raise_device_status(hc);
+        io.iterations = hc.iteration;
+        io.stop_reason = dash ? (hc.stop_pending ? DSVD_STOP_TOL_MET : DSVD_STOP_P_MAX_REACHED)
+                              : DSVD_STOP_FIXED_P;
+        ctx->stats.eig_sweeps = hc.total_sweeps;
+        // Q_N = T_N W_N diag(1/s_N): the basis the finalize multiplies by A
+        sp = ctx->span_begin(K_RESCALE);
+        solve_rescale(ctx, Tb[hc.iteration % 2], n, l, ld, W, l, inv_s, l, P, ld, 0, nullptr);
+        ctx->span_end(sp);
+        Qf = P;
+    } else {
+        // Q = eigSVD(A^T Omega).u
+        sp = ctx->span_begin(K_SPMM2);
+        spmm(SpmmArgs{&AT, Y, T, ld, l, nullptr, nullptr, nullptr}, st, ctx->spmm_variant, ctx->side, ctx->fork,
+             ctx->join, partial_for(ctx, AT, ld));
+        count_launch();
+        ctx->span_end(sp);
+        if (sharded) {
             sp = ctx->span_begin(K_COMM);
             comm_allreduce_sum(ctx, T, static_cast<size_t>(n * ld));
             ctx->span_end(sp);
-            shift_update(T, Qb[cur], n * ld, &ctrl->alpha, gate, st);
-            count_launch();
         }
-        eig_svd_factors(ctx, T, n, l, ld, eo, ctrl, &ls, gate);
+        eig_svd_factors(ctx, T, n, l, ld, eo, ctrl, nullptr, nullptr);
         sp = ctx->span_begin(K_RESCALE);
-        solve_rescale(ctx, T, n, l, ld, W, l, inv_s, l, Qb[1 - cur], ld, 0, gate);
+        solve_rescale(ctx, T, n, l, ld, W, l, inv_s, l, Qb[0], ld, 0, nullptr);
         ctx->span_end(sp);
-        if (dash) {
-            const int slot = static_cast<int>(j % (kLookahead + 1));
-            if (flag_ev[slot] == nullptr) flag_ev[slot] = ctx->event();
-            DSVD_CUDA_CHECK(cudaMemcpyAsync(&ctx->host_flags[slot], &ctrl->stop_pending,
-                                            sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-            DSVD_CUDA_CHECK(cudaEventRecord(flag_ev[slot], st));
-        }
-        if (observer) {
-            Control hc = read_control(ctx, ctrl);
-            raise_device_status(hc);
-            std::vector<double> qb = to_host_colmajor(ctx, Qb[cur], n, l, ld);
-            std::vector<double> qa = to_host_colmajor(ctx, Qb[1 - cur], n, l, ld);
-            std::vector<double> sh(static_cast<size_t>(l));
-            double alpha_used = 0.0;
-            DSVD_CUDA_CHECK(cudaMemcpy(sh.data(), d_shat + (j - 1) * l, sizeof(double) * l,
-                                       cudaMemcpyDeviceToHost));
-            DSVD_CUDA_CHECK(cudaMemcpy(&alpha_used, d_alphas + (j - 1), sizeof(double),
-                                       cudaMemcpyDeviceToHost));
-            observer(j, alpha_used, sh.data(), l, qb.data(), qa.data(), n, user);
-            if (hc.stop_pending) {
-                cur = 1 - cur;
-                break;
+
+
+        int cur = 0;
+        for (int64_t j = 1; j <= max_iters; ++j) {
+            if (dash && !observer && j > kLookahead) {
+                const int slot = static_cast<int>((j - kLookahead) % (kLookahead + 1));
+                DSVD_CUDA_CHECK(cudaEventSynchronize(flag_ev[slot]));
+                if (ctx->host_flags[slot]) break;
             }
+            loop_begin(ctrl, st);
+            count_launch();
+            // Y = A Q
+            sp = ctx->span_begin(K_SPMM1);
+            spmm(SpmmArgs{&A, Qb[cur], Y, ld, l, nullptr, nullptr, gate}, st, ctx->spmm_variant, ctx->side,
+                 ctx->fork, ctx->join, partial_for(ctx, A, ld));
+            count_launch();
+            ctx->span_end(sp);
+            // T = A^T Y - alpha Q  (add_scaled skipped when alpha == 0)
+            sp = ctx->span_begin(K_SPMM2);
+            spmm(SpmmArgs{&AT, Y, T, ld, l, sharded ? nullptr : Qb[cur], sharded ? nullptr : &ctrl->alpha,
+                          gate},
+                 st, ctx->spmm_variant, ctx->side, ctx->fork, ctx->join, partial_for(ctx, AT, ld));
+            count_launch();
+            ctx->span_end(sp);
+            if (sharded) {
+                // sum the partials first, then apply the shift once (solver.cpp:94)
+                sp = ctx->span_begin(K_COMM);
+                comm_allreduce_sum(ctx, T, static_cast<size_t>(n * ld));
+                ctx->span_end(sp);
+                shift_update(T, Qb[cur], n * ld, &ctrl->alpha, gate, st);
+                count_launch();
+            }
+            eig_svd_factors(ctx, T, n, l, ld, eo, ctrl, &ls, gate);
+            sp = ctx->span_begin(K_RESCALE);
+            solve_rescale(ctx, T, n, l, ld, W, l, inv_s, l, Qb[1 - cur], ld, 0, gate);
+            ctx->span_end(sp);
+            if (dash) {
+                const int slot = static_cast<int>(j % (kLookahead + 1));
+                if (flag_ev[slot] == nullptr) flag_ev[slot] = ctx->event();
+                DSVD_CUDA_CHECK(cudaMemcpyAsync(&ctx->host_flags[slot], &ctrl->stop_pending,
+                                                sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+                DSVD_CUDA_CHECK(cudaEventRecord(flag_ev[slot], st));
+            }
+            if (observer) {
+                hc = read_control(ctx, ctrl);
+                raise_device_status(hc);
+                std::vector<double> qb = to_host_colmajor(ctx, Qb[cur], n, l, ld);
+                std::vector<double> qa = to_host_colmajor(ctx, Qb[1 - cur], n, l, ld);
+                std::vector<double> sh(static_cast<size_t>(l));
+                double alpha_used = 0.0;
+                DSVD_CUDA_CHECK(cudaMemcpy(sh.data(), d_shat + (j - 1) * l, sizeof(double) * l,
+                                           cudaMemcpyDeviceToHost));
+                DSVD_CUDA_CHECK(cudaMemcpy(&alpha_used, d_alphas + (j - 1), sizeof(double),
+                                           cudaMemcpyDeviceToHost));
+                observer(j, alpha_used, sh.data(), l, qb.data(), qa.data(), n, user);
+                if (hc.stop_pending) {
+                    cur = 1 - cur;
+                    break;
+                }
+            }
+            cur = 1 - cur;
         }
-        cur = 1 - cur;
+        hc = read_control(ctx, ctrl);
+        raise_device_status(hc);
+        io.iterations = hc.iteration;
+        io.stop_reason = dash ? (hc.stop_pending ? DSVD_STOP_TOL_MET : DSVD_STOP_P_MAX_REACHED)
+                              : DSVD_STOP_FIXED_P;
+        ctx->stats.eig_sweeps = hc.total_sweeps;
+        Qf = Qb[hc.iteration % 2];
     }
-    Control hc = read_control(ctx, ctrl);
-    raise_device_status(hc);
-    io.iterations = hc.iteration;
-    io.stop_reason = dash ? (hc.stop_pending ? DSVD_STOP_TOL_MET : DSVD_STOP_P_MAX_REACHED)
-                          : DSVD_STOP_FIXED_P;
-    ctx->stats.eig_sweeps = hc.total_sweeps;
-    const double* Qf = Qb[hc.iteration % 2];
 
     // finalize_row_basis: B = A Q, eigSVD(B), U = B V' diag(1/s) [:, :k], V = Q V'[:, :k]
     control_init(ctrl, s_stored, static_cast<int>(l), st);
@@ -890,6 +1023,11 @@ int dsvd_ctx_create(int device, dsvd_ctx** out) {
         DSVD_CUDA_CHECK(cudaSetDevice(device));
         DSVD_CUDA_CHECK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
         DSVD_CUDA_CHECK(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
+        int prio_lo = 0, prio_hi = 0;
+        DSVD_CUDA_CHECK(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+        DSVD_CUDA_CHECK(cudaStreamCreateWithPriority(&c->eig, cudaStreamNonBlocking, prio_hi));
+        DSVD_CUDA_CHECK(cudaEventCreateWithFlags(&c->ev_t, cudaEventDisableTiming));
+        DSVD_CUDA_CHECK(cudaEventCreateWithFlags(&c->ev_eig, cudaEventDisableTiming));
         DSVD_CUDA_CHECK(cudaEventCreateWithFlags(&c->fork, cudaEventDisableTiming));
         DSVD_CUDA_CHECK(cudaEventCreateWithFlags(&c->join, cudaEventDisableTiming));
         *out = c.release();
@@ -901,6 +1039,7 @@ int dsvd_ctx_destroy(dsvd_ctx* ctx) {
         if (!ctx) return;
         cudaSetDevice(ctx->device);
         cudaStreamSynchronize(ctx->stream);
+        cudaStreamSynchronize(ctx->eig);
         for (auto& kv : ctx->arena)
             if (kv.second.ptr) cudaFree(kv.second.ptr);
         for (auto e : ctx->event_pool) cudaEventDestroy(e);
@@ -911,6 +1050,9 @@ int dsvd_ctx_destroy(dsvd_ctx* ctx) {
         if (ctx->host_flags) cudaFreeHost(ctx->host_flags);
         comm_release(ctx);
         cudaStreamDestroy(ctx->side);
+        cudaStreamDestroy(ctx->eig);
+        cudaEventDestroy(ctx->ev_t);
+        cudaEventDestroy(ctx->ev_eig);
         cudaEventDestroy(ctx->fork);
         cudaEventDestroy(ctx->join);
         if (ctx->omega_ev) cudaEventDestroy(ctx->omega_ev);
@@ -961,6 +1103,9 @@ int dsvd_ctx_set_option(dsvd_ctx* ctx, const char* name, int64_t value) {
         } else if (n == "dense_method") {
             if (value < 0 || value > 1) fail(DSVD_CONFIG, "dense_method: 0 = FP64 tensor cores, 1 = DFMA");
             ctx->dense_method = static_cast<int>(value);
+        } else if (n == "pipeline") {
+            if (value < 0 || value > 1) fail(DSVD_CONFIG, "pipeline: 1 = eigSVD beside the A T pass, 0 = serial");
+            ctx->pipeline = static_cast<int>(value);
         } else if (n == "split_chunk_t") {
             if (value < 0) fail(DSVD_CONFIG, "split_chunk_t must be >= 0");
             ctx->split_chunk_t = value;

@@ -55,6 +55,11 @@ struct dsvd_ctx {
     int dense_method = 0;           // 0: FP64 tensor-core Gram / rescale (dmma.cu), 1: DFMA kernels
     int eig_method = 0;             // 0: tridiagonal + inverse iteration (Jacobi fallback), 1: Jacobi
     cudaStream_t side = nullptr;    // second stream: hub-row SpMM runs beside the bulk kernel
+    // eigSVD stream (highest priority): with pipeline = 1 the Gram + l x l eig of
+    // T_{j-1} run here beside the A T_{j-1} pass on `stream` (solve_tall)
+    cudaStream_t eig = nullptr;
+    cudaEvent_t ev_t = nullptr, ev_eig = nullptr;
+    int pipeline = 1;
     // Omega generated on `side` while the host CSR uploads (host-input solves):
     // the next solve_tall with the same (m, l, seed) waits on omega_ev instead
     // of generating it

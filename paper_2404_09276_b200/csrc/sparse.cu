@@ -44,7 +44,7 @@ spmm_bulk_kernel(const int64_t* __restrict__ off, const int32_t* __restrict__ id
                  double* __restrict__ y, int64_t ld, const double* __restrict__ q,
                  const double* __restrict__ alpha_p, const int32_t* __restrict__ gate,
                  const int64_t* __restrict__ chunk_p0, const int64_t* __restrict__ chunk_p1) {
-    if (gate != nullptr && *gate != 0) return;
+    if (gate_closed(gate)) return;
     const int lane = threadIdx.x & 31;
     // slab-major order: all rows' first 64 columns, then the next 64, ... so
     // the X columns being gathered (rows x 512 B) stay resident in L2
@@ -147,7 +147,7 @@ spmm_row_kernel(const int64_t* __restrict__ off, const int32_t* __restrict__ idx
                 double* __restrict__ y, int64_t ld, const double* __restrict__ q,
                 const double* __restrict__ alpha_p, const int32_t* __restrict__ gate,
                 const int64_t* __restrict__ chunk_p0, const int64_t* __restrict__ chunk_p1) {
-    if (gate != nullptr && *gate != 0) return;
+    if (gate_closed(gate)) return;
     __shared__ __align__(16) double2 cv[kRowWarps][32];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t rpos = row_start + static_cast<int64_t>(blockIdx.x) * kRowWarps + warp;
@@ -247,7 +247,7 @@ spmm_row_wide_kernel(const int64_t* __restrict__ off, const int32_t* __restrict_
                      const double* __restrict__ alpha_p, const int32_t* __restrict__ gate,
                      const int64_t* __restrict__ chunk_p0, const int64_t* __restrict__ chunk_p1) {
     constexpr int U = 4;
-    if (gate != nullptr && *gate != 0) return;
+    if (gate_closed(gate)) return;
     __shared__ __align__(16) double2 cv[kRowWarps][32];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t rpos = row_start + static_cast<int64_t>(blockIdx.x) * kRowWarps + warp;
@@ -359,7 +359,7 @@ split_combine_tree_kernel(const double* __restrict__ partial, const int32_t* __r
                      const int32_t* __restrict__ slot, const int32_t* __restrict__ order, int64_t nsplit,
                      double* __restrict__ y, int64_t ld, const double* __restrict__ q,
                      const double* __restrict__ alpha_p, const int32_t* __restrict__ gate) {
-    if (gate != nullptr && *gate != 0) return;
+    if (gate_closed(gate)) return;
     __shared__ double2 red[8][32];
     const int64_t i = blockIdx.x;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -416,7 +416,7 @@ __global__ void split_combine_kernel(const double* __restrict__ partial, const i
                                      const int32_t* __restrict__ slot, const int32_t* __restrict__ order,
                                      int64_t nsplit, double* __restrict__ y, int64_t ld, const double* __restrict__ q,
                                      const double* __restrict__ alpha_p, const int32_t* __restrict__ gate) {
-    if (gate != nullptr && *gate != 0) return;
+    if (gate_closed(gate)) return;
     const int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
     if (e >= nsplit * ld) return;
     const int64_t i = e / ld, col = e - (e / ld) * ld;
@@ -507,7 +507,7 @@ spmm_hub_kernel(const int64_t* __restrict__ off, const int32_t* __restrict__ idx
                 const int32_t* __restrict__ n_hub_p, int nslab, const double* __restrict__ x,
                 double* __restrict__ y, int64_t ld, const double* __restrict__ q,
                 const double* __restrict__ alpha_p, const int32_t* __restrict__ gate) {
-    if (gate != nullptr && *gate != 0) return;
+    if (gate_closed(gate)) return;
     extern __shared__ double hub_smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t item = static_cast<int64_t>(blockIdx.x) * kHubWarps + warp;
@@ -641,7 +641,7 @@ spmm_hub_tma_kernel(const __grid_constant__ CUtensorMap xmap, const int64_t* __r
                     const int32_t* __restrict__ order, const int32_t* __restrict__ n_hub_p,
                     int nslab, double* __restrict__ y, int64_t ld, const double* __restrict__ q,
                     const double* __restrict__ alpha_p, const int32_t* __restrict__ gate) {
-    if (gate != nullptr && *gate != 0) return;
+    if (gate_closed(gate)) return;
     extern __shared__ __align__(1024) unsigned char tma_raw[];
     unsigned char* base = reinterpret_cast<unsigned char*>(
         (reinterpret_cast<uintptr_t>(tma_raw) + 1023) & ~uintptr_t(1023));
@@ -799,7 +799,7 @@ spmm_hub_deep_kernel(const int64_t* __restrict__ off, const int32_t* __restrict_
                      const int32_t* __restrict__ n_hub_p, int nslab, const double* __restrict__ x,
                      double* __restrict__ y, int64_t ld, const double* __restrict__ q,
                      const double* __restrict__ alpha_p, const int32_t* __restrict__ gate) {
-    if (gate != nullptr && *gate != 0) return;
+    if (gate_closed(gate)) return;
     extern __shared__ __align__(16) double deep_smem[];
     double* ring = deep_smem;                                   // [Dc][32 nnz][32 lanes]
     double* vring = ring + kDeepDc * 32 * 32;                   // [Ic][32]
