@@ -3,9 +3,12 @@ engine runs across GPUs (engine.cu solve_tall with a communicator; comm.cu),
 restated with the oracle's kernels and torch.distributed collectives:
 
   Omega_g    = rows [r_g, r_g+1) of the global sketch, Omega(i, j) = normal_at(seed, j*m + i)
-  T          = allreduce_g( A_g^T Omega_g ),          Q = eigSVD(T).u
-  loop:  T   = allreduce_g( A_g^T (A_g Q) ) - alpha Q  (shift applied once, after the sum)
-         (s, V) = eigSVD(T), Q = T V / s, shift update / PVE stop (replicated)
+  T_0        = allreduce_g( A_g^T Omega_g ),        (s, V) = eigSVD(T_0)
+  loop:  P   = allreduce_g( A_g^T (A_g T) ) - alpha T  (shift applied once, after the sum)
+         T   = P V / s   (= A^T A Q - alpha Q with Q = T V / s: the deferred rescale
+                          of the native loop, which runs both passes on T so the l x l
+                          eig overlaps the A T pass)
+         (s, V) = eigSVD(T), shift update / PVE stop (replicated)
   finalize:  B_g = A_g Q, G = allreduce_g(B_g^T B_g), eig(G), U_g = B_g V' / s, V = Q V'
 
 and checked against the single-process oracle solve: same iteration count,
@@ -55,17 +58,19 @@ def sharded_solve(orc, a_full, k, s, alg, p=-1, tol=1e-2, p_max=100, seed=0):
     for j in range(l):
         for i in range(r1 - r0):
             om[i, j] = orc.normal_at(seed, j * m + r0 + i)
-    q = orc.eig_svd(allreduce(orc.spmm(at, om)))[0]
+    t = allreduce(orc.spmm(at, om))
+    q, sv, vv = orc.eig_svd(t)
     dash = alg == "dash"
     max_iters = p_max if dash else p
     alpha, alpha_stored = 0.0, 0.0
     s_stored = np.zeros(l)
     iters, stop_reason = 0, ("p_max_reached" if dash else "fixed_p")
     for j in range(1, max_iters + 1):
-        t = allreduce(orc.spmm(at, orc.spmm(a, q)))
+        pj = allreduce(orc.spmm(at, orc.spmm(a, t)))
         if alpha != 0.0:
-            t = orc.add_scaled(t, -alpha, q)
-        u, sv, _ = orc.eig_svd(t)
+            pj = orc.add_scaled(pj, -alpha, t)
+        t = np.asfortranarray(orc.matmul(pj, vv) * (1.0 / sv))
+        u, sv, vv = orc.eig_svd(t)
         iters = j
         stop = dash and orc.pve_stop_check(s_stored, alpha_stored, sv, alpha, k, tol)
         q = u

@@ -748,3 +748,30 @@ def test_metrics_degenerate_reference(dev, oracle):
     with pytest.raises(d.DegenerateReference):
         d.eps_spec(to_dev(a), f, np.r_[f.s, 0.0], device=dev)  # sigma_{k+1} == 0
     assert d.max_triplet_residual(to_dev(a), f, device=dev) < 1e-3 * f.s[0]
+
+
+@pytest.mark.parametrize("alg,kw", [("shifted", dict(p=8)), ("dash", dict(tol=1e-2)),
+                                    ("fixed_shift", dict(p=5))])
+def test_loop_schedules_agree(oracle, alg, kw):
+    """The pipelined loop (deferred rescale: both SpMM passes on T_{j-1}, the
+    l x l eig on the priority stream beside the A T pass; engine.cu solve_tall,
+    option pipeline = 1, the default) and the serial loop in the reference's
+    order (pipeline = 0) both meet the solve bars against the oracle, take the
+    same stop decisions, and agree with each other far inside them."""
+    a = d.powerlaw(6000, 2500, 3.5, 1.0, 1.1, 9)
+    ca = Csr(a.rows, a.cols, a.offsets, a.col_indices, a.values)
+    ref = oracle.solve(ca, 24, 12, alg=alg, seed=5, **kw)
+    cfg = d.SolverConfig(k=24, s=12, alg=d.Algorithm[alg], seed=5, **kw)
+    out = []
+    for pipe in (1, 0):
+        dv = d.Device(0)
+        dv.set_option("pipeline", pipe)
+        res = d.solve(a, cfg, device=dv)
+        check_solve(res, ref, 24)
+        out.append(res)
+        dv.close()
+    p1, p0 = out
+    assert p1.trace.iterations == p0.trace.iterations
+    np.testing.assert_allclose(p1.svd.s, p0.svd.s, rtol=1e-11)
+    assert sin_theta(p0.svd.u, p1.svd.u) <= 1e-9
+    assert sin_theta(p0.svd.v, p1.svd.v) <= 1e-9
