@@ -479,7 +479,13 @@ void solve_tall(dsvd_ctx* ctx, const DevCsr& A, const DevCsr& AT, const dsvd_con
     std::vector<cudaEvent_t> flag_ev(kLookahead + 1, nullptr);
     Control hc;
     const double* Qf = nullptr;
-    if (ctx->pipeline != 0) {
+    // auto: pipelined when the eig chain it hides is worth >= 5% of the two
+    // SpMM passes it overlaps (gathers at ~20 TB/s; eig ~0.65 ms at l = 150,
+    // quadratic in l; tools/ab_option.py pipeline on C2 / C3 / C4 in DESIGN 5)
+    const double spmm_s = 2.0 * static_cast<double>(A.nnz) * static_cast<double>(ld) * 8.0 / 20e12;
+    const double eig_s = 0.65e-3 * (static_cast<double>(l) / 150.0) * (static_cast<double>(l) / 150.0);
+    const bool pipelined = ctx->pipeline == 1 || (ctx->pipeline < 0 && eig_s >= 0.05 * spmm_s);
+    if (pipelined) {
         // Deferred rescale. With Q_{j-1} = T_{j-1} W_{j-1} (W = V diag(1/s) of
         // eigSVD(T_{j-1}), sign convention folded in), the reference's
         //   T_j = A^T (A Q_{j-1}) - alpha Q_{j-1}            (solver.cpp:92-95)
@@ -1104,7 +1110,8 @@ int dsvd_ctx_set_option(dsvd_ctx* ctx, const char* name, int64_t value) {
             if (value < 0 || value > 1) fail(DSVD_CONFIG, "dense_method: 0 = FP64 tensor cores, 1 = DFMA");
             ctx->dense_method = static_cast<int>(value);
         } else if (n == "pipeline") {
-            if (value < 0 || value > 1) fail(DSVD_CONFIG, "pipeline: 1 = eigSVD beside the A T pass, 0 = serial");
+            if (value < -1 || value > 1)
+                fail(DSVD_CONFIG, "pipeline: 1 = eig beside the A T pass, 0 = serial, -1 = auto");
             ctx->pipeline = static_cast<int>(value);
         } else if (n == "split_chunk_t") {
             if (value < 0) fail(DSVD_CONFIG, "split_chunk_t must be >= 0");
