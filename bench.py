@@ -68,6 +68,8 @@ def parse():
     ap.add_argument("--config", choices=sorted(CONFIGS), default="c2")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-p", type=int, default=2)
+    ap.add_argument("--option", action="append", default=[], metavar="NAME=VALUE",
+                    help="context option for A/B runs (dsvd_ctx_set_option), e.g. gram_async=1")
     return ap.parse_args()
 
 
@@ -246,6 +248,9 @@ def run_b200(args, rank, world, local_rank):
     if world > 1:
         import torch.distributed as dist
     dev = d.Device(local_rank)
+    for opt in args.option:
+        name, value = opt.split("=", 1)
+        dev.set_option(name, int(value))
     a_full = make_matrix(cfg, dev)
     r0, r1 = shard_rows(a_full, world, rank)
     off = a_full.offsets[r0:r1 + 1] - a_full.offsets[r0]
@@ -385,6 +390,7 @@ def run_b200(args, rank, world, local_rank):
         "config": {"workload": cfg["name"], "rows": a_full.rows, "cols": a_full.cols,
                    "nnz": a_full.nnz, "k": k, "l": l, "p": scfg.p, "alg": cfg["alg"],
                    "parallelism": f"row-shard x{world}" if world > 1 else "1 GPU",
+                   **({"options": args.option} if args.option else {}),
                    "l2": (f"flushed: a 512 MB buffer is written before every timed step (per-step "
                           f"working set {working_set / 2**20:.0f} MB could stay in the 126 MB L2)") if flush_l2 else
                          (f"no flush: per-step working set (CSR+CSC {2 * 12 * a_full.nnz / 1e9:.2f} GB, "

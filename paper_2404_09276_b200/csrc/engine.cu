@@ -329,6 +329,22 @@ void eig_svd_factors(dsvd_ctx* ctx, const double* c, int64_t rows, int64_t l, in
                      EigSvdOut& o, Control* ctrl, const LoopStep* loop, const int32_t* gate,
                      bool reduce_gram = false, int64_t floor_rows = -1, cudaStream_t eig_stream = nullptr) {
     cudaStream_t st = ctx->stream;
+    // the l x l eig and the factor assembly (latency-bound, a few SMs) may run
+    // on eig_stream, after the Gram on ctx->stream (all SMs) — or, with
+    // gram_async, the Gram too
+    const cudaStream_t main_stream = ctx->stream;
+    struct Restore {
+        dsvd_ctx* c;
+        cudaStream_t s;
+        ~Restore() { c->stream = s; }
+    } restore{ctx, main_stream};
+    auto to_eig_stream = [&] {
+        DSVD_CUDA_CHECK(cudaEventRecord(ctx->ev_t, st));
+        DSVD_CUDA_CHECK(cudaStreamWaitEvent(eig_stream, ctx->ev_t, 0));
+        st = eig_stream;
+        ctx->stream = eig_stream;  // spans; restored on return
+    };
+    if (eig_stream != nullptr && ctx->gram_async) to_eig_stream();
     double* G = ctx->tbuf<double>("eig.G", l * l);
     int sp = ctx->span_begin(K_GRAM);
     if (ctx->dense_method == 0 && gram_dmma_supported(l, ld)) {
@@ -346,20 +362,7 @@ void eig_svd_factors(dsvd_ctx* ctx, const double* c, int64_t rows, int64_t l, in
         comm_allreduce_sum(ctx, G, static_cast<size_t>(l * l));
         ctx->span_end(sp);
     }
-    // the l x l eig and the factor assembly (latency-bound, a few SMs) may run
-    // on eig_stream, after the Gram (all SMs) on ctx->stream
-    const cudaStream_t main_stream = ctx->stream;
-    if (eig_stream != nullptr) {
-        DSVD_CUDA_CHECK(cudaEventRecord(ctx->ev_t, st));
-        DSVD_CUDA_CHECK(cudaStreamWaitEvent(eig_stream, ctx->ev_t, 0));
-        st = eig_stream;
-        ctx->stream = eig_stream;  // spans, restored below
-    }
-    struct Restore {
-        dsvd_ctx* c;
-        cudaStream_t s;
-        ~Restore() { c->stream = s; }
-    } restore{ctx, main_stream};
+    if (eig_stream != nullptr && !ctx->gram_async) to_eig_stream();
     EigWorkspace ew;
     void* em = ctx->buf("eig.ws", eig_workspace_bytes(static_cast<int>(l), kMaxSweeps));
     eig_workspace_bind(ew, static_cast<int>(l), kMaxSweeps, em);
@@ -1113,6 +1116,9 @@ int dsvd_ctx_set_option(dsvd_ctx* ctx, const char* name, int64_t value) {
             if (value < -1 || value > 1)
                 fail(DSVD_CONFIG, "pipeline: 1 = eig beside the A T pass, 0 = serial, -1 = auto");
             ctx->pipeline = static_cast<int>(value);
+        } else if (n == "gram_async") {
+            if (value < 0 || value > 1) fail(DSVD_CONFIG, "gram_async: 1 = Gram on the eig stream too, 0 = main");
+            ctx->gram_async = static_cast<int>(value);
         } else if (n == "split_chunk_t") {
             if (value < 0) fail(DSVD_CONFIG, "split_chunk_t must be >= 0");
             ctx->split_chunk_t = value;
