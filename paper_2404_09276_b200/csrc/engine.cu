@@ -1116,6 +1116,14 @@ int dsvd_ctx_set_option(dsvd_ctx* ctx, const char* name, int64_t value) {
             if (value < -1 || value > 1)
                 fail(DSVD_CONFIG, "pipeline: 1 = eig beside the A T pass, 0 = serial, -1 = auto");
             ctx->pipeline = static_cast<int>(value);
+        } else if (n == "eig_priority") {
+            // 1: the eig stream at the highest priority (default), 0: default priority
+            if (value < 0 || value > 1) fail(DSVD_CONFIG, "eig_priority must be 0 or 1");
+            DSVD_CUDA_CHECK(cudaStreamSynchronize(ctx->eig));
+            DSVD_CUDA_CHECK(cudaStreamDestroy(ctx->eig));
+            int lo = 0, hi = 0;
+            DSVD_CUDA_CHECK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+            DSVD_CUDA_CHECK(cudaStreamCreateWithPriority(&ctx->eig, cudaStreamNonBlocking, value ? hi : lo));
         } else if (n == "gram_async") {
             if (value < 0 || value > 1) fail(DSVD_CONFIG, "gram_async: 1 = Gram on the eig stream too, 0 = main");
             ctx->gram_async = static_cast<int>(value);

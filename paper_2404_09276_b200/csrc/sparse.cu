@@ -1058,6 +1058,9 @@ void spmm(const SpmmArgs& s, cudaStream_t stream, int variant, cudaStream_t side
     // variant bits: low nibble selects the hub kernel; 16 skips the bulk rows,
     // 32 skips the hub rows (benchmarking the two halves separately)
     const bool skip_bulk = (variant & 16) != 0, skip_hub = (variant & 32) != 0;
+    // bit 1024: the long-row chunks run on the main stream before the bulk rows
+    // (serial) instead of beside them on the side stream
+    if ((variant & 1024) != 0 && side != nullptr) side = stream;
     // the whole-row kernel takes the bulk rows and the split chunks when
     // ld <= 192; bits 64 / 128 force the 64-column slab kernel for them, bits
     // 256 / 512 raise the whole-row kernel's gather lookahead from 2 to 4 / 8
