@@ -143,7 +143,11 @@ DSVD_API int dsvd_ctx_synchronize(dsvd_ctx* ctx);
  * next call); matrix handles keep their own buffers. For very large inputs
  * that alternate between entry points. */
 DSVD_API int dsvd_ctx_trim(dsvd_ctx* ctx);
-/* Tuning knobs (testing/benchmarking); unknown names -> DSVD_CONFIG. */
+/* Tuning knobs (testing/benchmarking); unknown names -> DSVD_CONFIG.
+ * Loop schedule: "pipeline" -1 auto (default) / 0 serial /
+ * 1 pipelined; "eig_priority" 1 (default) / 0; "gram_async" 0 (default) / 1.
+ * Kernels: "spmm_variant", "split_chunk", "split_chunk_t", "split_panel_rows",
+ * "hub_threshold", "eig_method", "dense_method". */
 DSVD_API int dsvd_ctx_set_option(dsvd_ctx* ctx, const char* name, int64_t value);
 
 /* Multi-GPU: one process per GPU. Rank 0 calls dsvd_comm_unique_id and
