@@ -545,21 +545,41 @@ void solve_tall(dsvd_ctx* ctx, const DevCsr& A, const DevCsr& AT, const dsvd_con
                  ctx->fork, ctx->join, partial_for(ctx, A, ld));
             count_launch();
             ctx->span_end(sp);
-            DSVD_CUDA_CHECK(cudaStreamWaitEvent(st, ctx->ev_eig, 0));
-            loop_begin(ctrl, st);
-            count_launch();
-            // P = A^T Z - alpha T_{j-1}  (the shift skipped when alpha == 0)
-            sp = ctx->span_begin(K_SPMM2);
-            spmm(SpmmArgs{&AT, Y, P, ld, l, sharded ? nullptr : tprev, sharded ? nullptr : &ctrl->alpha, gate},
-                 st, ctx->spmm_variant, ctx->side, ctx->fork, ctx->join, partial_for(ctx, AT, ld));
-            count_launch();
-            ctx->span_end(sp);
-            if (sharded) {
-                sp = ctx->span_begin(K_COMM);
-                comm_allreduce_sum(ctx, P, static_cast<size_t>(n * ld));
+            if (ctx->shift_after) {
+                // P = A^T Z before the wait (both passes overlap the eig), then
+                // P <- fma(-alpha, T_{j-1}, P): the same bits as the fused epilogue
+                sp = ctx->span_begin(K_SPMM2);
+                spmm(SpmmArgs{&AT, Y, P, ld, l, nullptr, nullptr, dash ? &ctrl->stop_pending : gate}, st,
+                     ctx->spmm_variant, ctx->side, ctx->fork, ctx->join, partial_for(ctx, AT, ld));
+                count_launch();
                 ctx->span_end(sp);
+                DSVD_CUDA_CHECK(cudaStreamWaitEvent(st, ctx->ev_eig, 0));
+                loop_begin(ctrl, st);
+                count_launch();
+                if (sharded) {
+                    sp = ctx->span_begin(K_COMM);
+                    comm_allreduce_sum(ctx, P, static_cast<size_t>(n * ld));
+                    ctx->span_end(sp);
+                }
                 shift_update(P, tprev, n * ld, &ctrl->alpha, gate, st);
                 count_launch();
+            } else {
+                DSVD_CUDA_CHECK(cudaStreamWaitEvent(st, ctx->ev_eig, 0));
+                loop_begin(ctrl, st);
+                count_launch();
+                // P = A^T Z - alpha T_{j-1}  (the shift skipped when alpha == 0)
+                sp = ctx->span_begin(K_SPMM2);
+                spmm(SpmmArgs{&AT, Y, P, ld, l, sharded ? nullptr : tprev, sharded ? nullptr : &ctrl->alpha, gate},
+                     st, ctx->spmm_variant, ctx->side, ctx->fork, ctx->join, partial_for(ctx, AT, ld));
+                count_launch();
+                ctx->span_end(sp);
+                if (sharded) {
+                    sp = ctx->span_begin(K_COMM);
+                    comm_allreduce_sum(ctx, P, static_cast<size_t>(n * ld));
+                    ctx->span_end(sp);
+                    shift_update(P, tprev, n * ld, &ctrl->alpha, gate, st);
+                    count_launch();
+                }
             }
             // T_j = P W_{j-1} diag(1/s_{j-1})  (= A^T A Q_{j-1} - alpha Q_{j-1})
             sp = ctx->span_begin(K_RESCALE);
@@ -1124,6 +1144,9 @@ int dsvd_ctx_set_option(dsvd_ctx* ctx, const char* name, int64_t value) {
             int lo = 0, hi = 0;
             DSVD_CUDA_CHECK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
             DSVD_CUDA_CHECK(cudaStreamCreateWithPriority(&ctx->eig, cudaStreamNonBlocking, value ? hi : lo));
+        } else if (n == "shift_after") {
+            if (value < 0 || value > 1) fail(DSVD_CONFIG, "shift_after must be 0 or 1");
+            ctx->shift_after = static_cast<int>(value);
         } else if (n == "gram_async") {
             if (value < 0 || value > 1) fail(DSVD_CONFIG, "gram_async: 1 = Gram on the eig stream too, 0 = main");
             ctx->gram_async = static_cast<int>(value);

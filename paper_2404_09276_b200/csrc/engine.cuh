@@ -59,7 +59,10 @@ struct dsvd_ctx {
     // T_{j-1} run here beside the A T_{j-1} pass on `stream` (solve_tall)
     cudaStream_t eig = nullptr;
     cudaEvent_t ev_t = nullptr, ev_eig = nullptr;
-    int gram_async = 0;  // pipelined loop: Gram on the eig stream too (beside the A T pass)
+    int gram_async = 0;
+    // pipelined loop: A^T pass unshifted before the eig wait, shift as its own
+    // kernel after it (1), or fused into the A^T pass after the wait (0)
+    int shift_after = 0;  // pipelined loop: Gram on the eig stream too (beside the A T pass)
     int pipeline = -1;  // -1: auto (pipeline_pays), 0: serial, 1: pipelined
     // Omega generated on `side` while the host CSR uploads (host-input solves):
     // the next solve_tall with the same (m, l, seed) waits on omega_ev instead
