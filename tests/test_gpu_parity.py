@@ -775,3 +775,36 @@ def test_loop_schedules_agree(oracle, alg, kw):
     np.testing.assert_allclose(p1.svd.s, p0.svd.s, rtol=1e-11)
     assert sin_theta(p0.svd.u, p1.svd.u) <= 1e-9
     assert sin_theta(p0.svd.v, p1.svd.v) <= 1e-9
+
+
+def test_loop_options_validated():
+    dv = d.Device(0)
+    for name, bad in (("pipeline", 2), ("pipeline", -2), ("gram_async", 2), ("shift_after", -1),
+                      ("eig_priority", 3)):
+        with pytest.raises(d.ConfigError):
+            dv.set_option(name, bad)
+    for name, good in (("pipeline", -1), ("pipeline", 0), ("pipeline", 1), ("gram_async", 0),
+                       ("shift_after", 0), ("eig_priority", 1), ("eig_priority", 0)):
+        dv.set_option(name, good)
+    with pytest.raises(d.ConfigError):
+        dv.set_option("no_such_option", 1)
+    dv.close()
+
+
+@pytest.mark.parametrize("opts", [dict(shift_after=1), dict(gram_async=1), dict(eig_priority=0)])
+def test_pipelined_variants_are_bitwise_equal(oracle, opts):
+    """The schedule variants of the pipelined loop move work between streams but
+    compute the same values in the same order: bitwise equal factors."""
+    a = d.powerlaw(5000, 2000, 3.5, 1.0, 1.1, 2)
+    cfg = d.SolverConfig(k=16, s=8, tol=1e-2, seed=2)
+    res = []
+    for extra in ({}, opts):
+        dv = d.Device(0)
+        dv.set_option("pipeline", 1)
+        for k_, v_ in extra.items():
+            dv.set_option(k_, v_)
+        res.append(d.solve(a, cfg, device=dv))
+        dv.close()
+    assert res[0].trace.iterations == res[1].trace.iterations
+    for name in ("u", "s", "v"):
+        assert_bitwise(getattr(res[0].svd, name), getattr(res[1].svd, name))
