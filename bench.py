@@ -1,22 +1,33 @@
 #!/usr/bin/env python
-"""Benchmark of the B200 dashSVD hot path on BASELINE.json's configs[1]
-(200,000 x 100,000 power-law CSR, nnz ~18M, k=100, l=150, p=20 shifted power
-iterations): one "step" is one full solve(a, cfg) — transpose, sketch, 20
-power iterations, finalize.
+"""Benchmark of the B200 dashSVD hot path. Default workload: BASELINE.json
+configs[3] (C4: R-MAT scale 22, 4,194,304^2, ~100M unique edges, k=200, l=300,
+p=30 shifted power iterations; the largest single-GPU configuration, quoted at
+1/2/4/8 GPUs). One "step" is one full solve(a, cfg) — transpose, sketch, p
+power iterations, finalize (the CLI's iterate + finalize boundary,
+tools/dashsvd.cpp:160-171).
 
-  value   device-resident solve seconds (CSR already in HBM, U/S/V left in HBM),
-          CUDA events on the library's stream, max over ranks
-  e2e     the same solve through the public API with host buffers (pinned CSR
-          in, pinned U/S/V out; H2D + D2H inside the timed region)
+  value     device-resident solve seconds (CSR already in HBM, U/S/V left in
+            HBM), CUDA events on the library's stream, max over ranks
+  e2e       the same solve through the public API with host buffers (pinned CSR
+            in, pinned U/S/V out; H2D + D2H inside the timed region)
   roofline  SpMM passes (the dominant kernels): algorithmic bytes per launch
-          (B1 = 12 nnz + 8 (m+1) + 8 n l + 8 m l, B2 = ... + 8 n l)
-          / average launch time, against MEASURED_PEAKS.json hbm_gbs
-  cpu_baseline  the unmodified reference core (oracle/_ref) on the host cores,
-          a bounded sample (p=2 of 20) extrapolated by its per-iteration time
+            (B1 = 12 nnz + 8 (m+1) + 8 n l + 8 m l, B2 = ... + 8 n l)
+            / average launch time, against MEASURED_PEAKS.json hbm_gbs
+  cpu_baseline  the unmodified reference core (oracle/_ref) on the host's
+            physical cores, run in a child process through `--impl reference`
+            (the same bounded sample the reference arm takes)
 
-`--impl reference` times the reference's CPU implementation alone (rank 0).
-Multi-GPU: one process per GPU (torchrun), A row-sharded by nnz, NCCL sum of
-the n x l partials; strong scaling of the same solve.
+`--impl reference` times the reference's CPU implementation alone (rank 0 of a
+torchrun launch; other ranks exit): the input is built by oracle/inputs_gen.c
+(bit-identical to the product's generators; the product library is never
+loaded), then transpose + solve of the reference on all physical cores with
+OMP_PROC_BIND=close / OMP_PLACES=cores. Fixed-p configs whose full reference
+solve takes minutes (C4: ~30 min) run a p = 2 sample and extrapolate with the
+measured per-iteration time; accuracy-controlled configs run to the
+reference's own stop.
+
+Multi-GPU: one process per GPU (torchrun), A row-sharded by nnz (each rank
+holds only its shard on the host), strong scaling of the same solve.
 """
 import argparse
 import json
@@ -33,30 +44,37 @@ sys.path.insert(0, ROOT)
 import numpy as np  # noqa: E402
 
 CONFIGS = {
+    # BASELINE.json configs[0] (the reference's CPU-runnable case)
+    "c1": dict(baseline_index=0, name="C1 sparse_random 10000x5000, 25/row, row decay", rows=10_000, cols=5_000,
+               npr=25, gen_seed=0, k=50, s=25, p=10, alg="shifted", seed=0, ref_sample_p=10),
     # BASELINE.json configs[1]
     "c2": dict(baseline_index=1, name="C2 power-law 200000x100000, lognormal(4,1) rows, Zipf(1.1) cols",
                rows=200_000, cols=100_000, mu=4.0, sigma=1.0, zipf=1.1, ratings=False,
-               gen_seed=2, k=100, s=50, p=20, alg="shifted", seed=0),
-    # BASELINE.json configs[0] (the reference's CPU-runnable case)
-    "c1": dict(baseline_index=0, name="C1 sparse_random 10000x5000, 25/row, row decay", rows=10_000, cols=5_000,
-               npr=25, gen_seed=0, k=50, s=25, p=10, alg="shifted", seed=0),
-    # BASELINE.json configs[2] (dash / PVE control)
-    "c3": dict(baseline_index=2, name="C3 ratings 2000000x500000, lognormal(4.2,1.2), Zipf(1.0), values 1-5",
+               gen_seed=2, k=100, s=50, p=20, alg="shifted", seed=0, ref_sample_p=20),
+    # BASELINE.json configs[2] (dash / PVE control). Rows sample their degree's
+    # columns WITHOUT replacement (274M nnz; SURVEY 8d's with-replacement-and-dedup
+    # rule would give ~208M): a larger workload than BASELINE's "~200M"
+    "c3": dict(baseline_index=2, name="C3 ratings 2000000x500000, lognormal(4.2,1.2), Zipf(1.0), values 1-5, "
+                                      "columns drawn without replacement per row (274M nnz)",
                rows=2_000_000, cols=500_000, mu=4.2, sigma=1.2, zipf=1.0, ratings=True,
                gen_seed=3, k=100, s=50, p=-1, p_max=100, tol=1e-2, alg="dash", seed=0),
     # BASELINE.json configs[3]: R-MAT scale 22, ~100M unique edges (104M draws), values 1.0
     "c4": dict(baseline_index=3, name="C4 R-MAT scale 22, (a,b,c)=(.57,.19,.19), 104M draws -> ~100M unique, values 1.0",
                rows=1 << 22, cols=1 << 22, rmat_scale=22, draws=104_000_000, uniform=False,
-               gen_seed=4, k=200, s=100, p=30, alg="shifted", seed=0),
-    # BASELINE.json configs[4]: R-MAT scale 24, ~1B unique edges (1.05B draws), uniform(0,1] values
+               gen_seed=4, k=200, s=100, p=30, alg="shifted", seed=0, ref_sample_p=2),
+    # BASELINE.json configs[4]: R-MAT scale 24, ~1B unique edges (1.05B draws), uniform(0,1] values.
+    # The full reference solve needs more host memory than the GPU box has: it runs a p = 2
+    # sample extrapolated to N_p = 7 (the device solve's stopping count, profiles/r01_bench_c5.json)
     "c5": dict(baseline_index=4, name="C5 R-MAT scale 24, (a,b,c)=(.57,.19,.19), 1.05B draws -> ~1.0B unique, uniform(0,1]",
                rows=1 << 24, cols=1 << 24, rmat_scale=24, draws=1_050_000_000, uniform=True,
-               gen_seed=5, k=100, s=50, p=-1, p_max=50, tol=1e-2, alg="dash", seed=0),
+               gen_seed=5, k=100, s=50, p=-1, p_max=50, tol=1e-2, alg="dash", seed=0, ref_sample_p=2, ref_np=7),
 }
+DEFAULT_CONFIG = "c4"
 
 CLOCK_FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+METRIC = "dashSVD end-to-end seconds"
 
 
 def parse():
@@ -65,34 +83,47 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
-    ap.add_argument("--config", choices=sorted(CONFIGS), default="c2")
+    ap.add_argument("--config", choices=sorted(CONFIGS), default=DEFAULT_CONFIG)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-sample-p", type=int, default=2)
+    ap.add_argument("--cpu-sample-p", type=int, default=None,
+                    help="power iterations of the reference sample (default: the config's ref_sample_p)")
+    ap.add_argument("--ref-budget-s", type=float, default=200.0,
+                    help="reference arm: keep taking samples while the next one fits this budget (>= 1 sample)")
+    ap.add_argument("--ref-np", type=int, default=None,
+                    help="accuracy-controlled configs sampled below their stop: extrapolate to this N_p")
     ap.add_argument("--option", action="append", default=[], metavar="NAME=VALUE",
                     help="context option for A/B runs (dsvd_ctx_set_option), e.g. gram_async=1")
     return ap.parse_args()
 
 
-def make_matrix(cfg, device=None):
-    import paper_2404_09276_b200 as d
-    if "npr" in cfg:
-        return d.sparse_random(cfg["rows"], cfg["cols"], cfg["npr"], cfg["gen_seed"], True)
-    if "rmat_scale" in cfg:  # generated on the device, brought to the host as the input CSR
-        m = d.rmat(cfg["rmat_scale"], cfg["draws"], uniform_values=cfg["uniform"], seed=cfg["gen_seed"],
-                   device=device)
-        try:
-            return m.download()
-        finally:
-            m.close()
-    return d.powerlaw(cfg["rows"], cfg["cols"], cfg["mu"], cfg["sigma"], cfg["zipf"],
-                      cfg["gen_seed"], ratings=cfg["ratings"])
+def sketch_width(cfg):
+    return cfg["k"] + cfg["s"]
 
 
-def solver_config(cfg):
-    import paper_2404_09276_b200 as d
-    return d.SolverConfig(k=cfg["k"], s=cfg["s"], p=cfg.get("p", -1), tol=cfg.get("tol", 1e-2),
-                          p_max=cfg.get("p_max", 1000), alg=d.Algorithm[cfg["alg"]],
-                          seed=cfg["seed"])
+def config_dict(cfg, nnz, world):
+    """The workload description both arms print (identical dicts)."""
+    l = sketch_width(cfg)
+    ld = (l + 3) // 4 * 4
+    flush = l2_flush(cfg, nnz)
+    d = {"workload": cfg["name"], "rows": cfg["rows"], "cols": cfg["cols"], "nnz": int(nnz), "k": cfg["k"], "l": l,
+         "alg": cfg["alg"]}
+    if cfg["alg"] == "dash":
+        d.update(tol=cfg["tol"], p_max=cfg["p_max"])
+    else:
+        d["p"] = cfg["p"]
+    d["row_shards"] = world
+    d["l2"] = (f"flushed: a 512 MB buffer is written before every timed step (the per-step working set "
+               f"could stay in the 126 MB L2)") if flush else \
+              (f"no flush: per-step working set (CSR+CSC {2 * 12 * nnz / 1e9:.2f} GB, sketch/Y "
+               f"{8 * cfg['rows'] * ld / 1e9:.2f} GB, Q/T {8 * cfg['cols'] * ld / 1e9:.2f} GB each) exceeds the "
+               "126 MB L2")
+    return d
+
+
+def l2_flush(cfg, nnz):
+    ld = (sketch_width(cfg) + 3) // 4 * 4
+    working_set = 24 * nnz + 8 * cfg["rows"] * ld + 3 * 8 * cfg["cols"] * ld
+    return working_set < 2 * 126 * 2**20
 
 
 def measured_peaks():
@@ -112,6 +143,28 @@ def committed_traffic(config_key):
         return entry.get("traffic") if isinstance(entry, dict) else entry
     except Exception:
         return None
+
+
+def host_cpu():
+    """(model name, logical CPUs usable by this process, physical cores among them)."""
+    model, cores = "unknown", set()
+    logical = sorted(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else list(range(os.cpu_count()))
+    try:
+        cur = {}
+        with open("/proc/cpuinfo") as f:
+            for line in f.read().split("\n") + [""]:
+                if not line.strip():
+                    if cur.get("processor") is not None and int(cur["processor"]) in logical:
+                        cores.add((cur.get("physical id", "0"), cur.get("core id", cur["processor"])))
+                    cur = {}
+                    continue
+                k, _, v = line.partition(":")
+                cur[k.strip()] = v.strip()
+                if k.strip() == "model name":
+                    model = v.strip()
+    except OSError:
+        pass
+    return model, len(logical), max(1, len(cores) or len(logical))
 
 
 class ClockSampler:
@@ -164,78 +217,162 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------------
-# CPU reference timing (oracle/_ref = the unmodified reference core)
+# Reference arm: the unmodified reference core (oracle/_ref) on the host cores.
+# Never imports paper_2404_09276_b200.
 # ---------------------------------------------------------------------------------
 
-def reference_sample(a, cfg, threads, p_sample):
-    """Time transpose + solve of the reference on a p_sample-iteration run and
-    extrapolate to the configured iteration count with the measured
-    per-iteration time. Returns (seconds, description, kind)."""
+def reference_matrix(cfg):
     sys.path.insert(0, os.path.join(ROOT, "tests"))
-    from oracle_lib import REF_SO, Csr, Oracle, Reference
-    csr = Csr(a.rows, a.cols, a.offsets, a.col_indices, a.values)
-    p_full = cfg["p"] if cfg["alg"] != "dash" else cfg.get("p_max", 100)
-    ps = max(1, min(p_sample, p_full))
-    if os.path.exists(REF_SO):
-        ref = Reference()
-        ref.set_threads(threads)
-        t0 = time.perf_counter()
-        r = ref.solve(csr, cfg["k"], cfg["s"], p=ps, alg="shifted" if cfg["alg"] != "dash" else "dash",
-                      tol=cfg.get("tol", 1e-2), p_max=ps, seed=cfg["seed"], times=True)
-        wall = time.perf_counter() - t0
-        tm = r["times"]
-        st = tm["stamps"]
-        per_iter = (st[-1] - st[0]) / (len(st) - 1) if len(st) > 1 else st[0]
-        total = tm["transpose"] + tm["solve"] + (p_full - r["iterations"]) * per_iter
-        desc = (f"{cfg['name']}: reference transpose+solve with p={r['iterations']} "
-                f"(of {p_full}) measured {tm['transpose'] + tm['solve']:.2f}s, per-iteration "
-                f"{per_iter:.3f}s, extrapolated to p={p_full}")
-        return total, desc, "reference", wall
-    orc = Oracle()
+    from oracle_lib import InputsGen, Reference
+    if "npr" in cfg:  # the reference's own generator (synthetic.cpp:72-120)
+        return Reference().sparse_random(cfg["rows"], cfg["cols"], cfg["npr"], cfg["gen_seed"], True)
+    gen = InputsGen()
+    if "rmat_scale" in cfg:
+        return gen.rmat(cfg["rmat_scale"], cfg["draws"], uniform=cfg["uniform"], seed=cfg["gen_seed"])
+    return gen.powerlaw(cfg["rows"], cfg["cols"], cfg["mu"], cfg["sigma"], cfg["zipf"], cfg["gen_seed"],
+                        ratings=cfg["ratings"])
+
+
+def reference_sample(ref, a, cfg, p_sample, np_target):
+    """One transpose + solve of the reference. Returns (seconds for the configured
+    solve, description, measured wall seconds, iterations run)."""
+    dash = cfg["alg"] == "dash"
+    if dash:
+        p_run = cfg["p_max"] if p_sample is None else min(p_sample, cfg["p_max"])
+    else:
+        p_run = cfg["p"] if p_sample is None else min(p_sample, cfg["p"])
     t0 = time.perf_counter()
-    orc.solve(csr, cfg["k"], cfg["s"], p=ps, alg="shifted", seed=cfg["seed"])
+    r = ref.solve(a, cfg["k"], cfg["s"], p=p_run if not dash else -1, alg=cfg["alg"], tol=cfg.get("tol", 1e-2),
+                  p_max=p_run if dash else 1000, seed=cfg["seed"], times=True)
     wall = time.perf_counter() - t0
-    return wall * (p_full + 2) / (ps + 2), f"oracle port, p={ps} scaled to p={p_full}", "port", wall
+    tm = r["times"]
+    measured = tm["transpose"] + tm["solve"]
+    st = tm["stamps"]
+    it = r["iterations"]
+    if dash and r["stop_reason"] == "tol_met":
+        return measured, f"transpose + dash solve to the reference's own stop (N_p = {it}), measured", wall, it
+    target = cfg["p"] if not dash else (np_target or cfg.get("ref_np") or cfg["p_max"])
+    if it >= target:
+        return measured, f"transpose + solve, p = {it}, measured", wall, it
+    per_iter = (st[-1] - st[-2]) if len(st) > 1 else st[0]
+    total = measured + (target - it) * per_iter
+    src = "" if not dash else (" (N_p of the device solve)" if np_target or cfg.get("ref_np") else " (p_max)")
+    desc = (f"transpose + solve with p = {it} measured {measured:.2f} s (transpose {tm['transpose']:.2f} s, "
+            f"iteration {it} {per_iter:.2f} s), extrapolated to p = {target}{src} with the measured "
+            f"per-iteration time")
+    return total, desc, wall, it
 
 
 def run_reference_arm(args, rank, world):
-    cfg = CONFIGS[args.config]
     if rank != 0:
         return
-    a = make_matrix(cfg)
-    threads = os.cpu_count() or 1
-    samples = []
-    desc = kind = None
-    for i in range(args.warmup + args.steps):
-        v, desc, kind, _ = reference_sample(a, cfg, threads, args.cpu_sample_p)
-        if i >= args.warmup:
-            samples.append(v)
+    cfg = CONFIGS[args.config]
+    model, logical, physical = host_cpu()
+    os.environ.setdefault("OMP_PROC_BIND", "close")
+    os.environ.setdefault("OMP_PLACES", "cores")
+    os.environ.setdefault("OMP_NUM_THREADS", str(physical))
+    threads = int(os.environ["OMP_NUM_THREADS"])
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from oracle_lib import REF_SO, Csr, Reference
+    if not os.path.exists(REF_SO):
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libdashsvd_ref.so was not built "
+                          "(needs /root/reference at build time)"}), flush=True)
+        return
+    t0 = time.perf_counter()
+    a = reference_matrix(cfg)
+    t_gen = time.perf_counter() - t0
+    ref = Reference()
+    ref.set_threads(threads)
+    p_sample = args.cpu_sample_p if args.cpu_sample_p is not None else cfg.get("ref_sample_p")
+    samples, walls = [], []
+    desc = None
+    while True:
+        v, desc, wall, _ = reference_sample(ref, Csr(a.rows, a.cols, a.offsets, a.col_indices, a.values), cfg,
+                                            p_sample, args.ref_np)
+        samples.append(v)
+        walls.append(wall)
+        if len(samples) >= args.steps or sum(walls) + wall > args.ref_budget_s:
+            break
     value = statistics.mean(samples)
-    line = {"metric": "dashSVD end-to-end seconds", "value": value, "unit": "s",
+    sample = (f"{cfg['name']}: {desc}; {len(samples)} sample(s) of {statistics.mean(walls):.1f} s wall each "
+              f"(input built in {t_gen:.1f} s by oracle/inputs_gen.c, untimed); host {model}, {threads} threads "
+              f"on {physical} physical cores ({logical} logical), OMP_PROC_BIND={os.environ['OMP_PROC_BIND']} "
+              f"OMP_PLACES={os.environ['OMP_PLACES']}")
+    line = {"metric": METRIC, "value": value, "unit": "s",
             "impl": "reference", "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": value * 1e3, "higher_is_better": False,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-            "data": f"synthetic (seeded generator, BASELINE.json configs[{cfg['baseline_index']}] shape)",
-            "config": {"workload": cfg["name"], "rows": a.rows, "cols": a.cols, "nnz": a.nnz,
-                       "k": cfg["k"], "l": cfg["k"] + cfg["s"], "p": cfg.get("p"),
-                       "alg": cfg["alg"]},
-            "cpu_baseline": {"value": value, "unit": "s", "cores": threads, "kind": kind,
-                             "sample": desc},
-            "e2e": {"value": value, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+            "data": f"synthetic (seeded generator, BASELINE.json configs[{cfg['baseline_index']}] shape; no dataset)",
+            "config": config_dict(cfg, a.nnz, world),
+            "cpu_baseline": {"value": value, "unit": "s", "cores": threads, "kind": "reference", "sample": sample},
+            "e2e": {"value": value, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "samples": len(samples), "sample_wall_s": walls}
     print(json.dumps(line), flush=True)
+
+
+def cpu_baseline_child(args, np_target):
+    """The reference arm's sample, run in a child process (its own OpenMP runtime
+    with the binding set before it loads; the product library stays out of it)."""
+    cmd = [sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--config", args.config,
+           "--steps", "1", "--warmup", "0"]
+    if args.cpu_sample_p is not None:
+        cmd += ["--cpu-sample-p", str(args.cpu_sample_p)]
+    if np_target:
+        cmd += ["--ref-np", str(np_target)]
+    env = {k: v for k, v in os.environ.items() if k not in ("RANK", "WORLD_SIZE", "LOCAL_RANK")}
+    try:
+        out = subprocess.run(cmd, capture_output=True, text=True, env=env, timeout=1500).stdout
+        for ln in out.splitlines()[::-1]:
+            if ln.startswith("{"):
+                rec = json.loads(ln)
+                return rec.get("cpu_baseline") or {"unavailable": rec.get("unavailable")}
+    except Exception as exc:  # reported, not fatal
+        return {"unavailable": f"reference sample failed: {exc}"}
+    return {"unavailable": "reference sample printed no result"}
 
 
 # ---------------------------------------------------------------------------------
 # B200 arm
 # ---------------------------------------------------------------------------------
 
-def shard_rows(a, world, rank):
-    """Row shard balanced by nonzeros: rows [r0, r1)."""
-    if world == 1:
-        return 0, a.rows
-    bounds = [int(np.searchsorted(a.offsets, a.nnz * g / world, side="left")) for g in range(world + 1)]
-    bounds[0], bounds[-1] = 0, a.rows
-    return bounds[rank], bounds[rank + 1]
+def shard_bounds(offsets, world):
+    from paper_2404_09276_b200.sharding import shard_bounds as sb
+    return sb(offsets, world)
+
+
+def b200_matrix(cfg, dev, world, rank):
+    """This rank's row shard of the workload on the host, the global nnz and the
+    shard's first row."""
+    import paper_2404_09276_b200 as d
+    from paper_2404_09276_b200.sharding import shard_csr
+    if "rmat_scale" in cfg:  # generated on the device; only this rank's rows come to the host
+        m = d.rmat(cfg["rmat_scale"], cfg["draws"], uniform_values=cfg["uniform"], seed=cfg["gen_seed"],
+                   device=dev)
+        try:
+            off = m.row_offsets()
+            b = shard_bounds(off, world)
+            return m.download_rows(b[rank], b[rank + 1]), m.nnz, b[rank]
+        finally:
+            m.close()
+    if "npr" in cfg:
+        a = d.sparse_random(cfg["rows"], cfg["cols"], cfg["npr"], cfg["gen_seed"], True)
+    else:
+        a = d.powerlaw(cfg["rows"], cfg["cols"], cfg["mu"], cfg["sigma"], cfg["zipf"], cfg["gen_seed"],
+                       ratings=cfg["ratings"])
+    b = shard_bounds(a.offsets, world)
+    return (shard_csr(a, b[rank], b[rank + 1]) if world > 1 else a), a.nnz, b[rank]
+
+
+def make_matrix(cfg, device=None):
+    """The whole workload matrix on the host (tools/parity_large.py, tools/transpose_bytes.py)."""
+    return b200_matrix(cfg, device, 1, 0)[0]
+
+
+def solver_config(cfg):
+    import paper_2404_09276_b200 as d
+    return d.SolverConfig(k=cfg["k"], s=cfg["s"], p=cfg.get("p", -1), tol=cfg.get("tol", 1e-2),
+                          p_max=cfg.get("p_max", 1000), alg=d.Algorithm[cfg["alg"]],
+                          seed=cfg["seed"])
 
 
 def run_b200(args, rank, world, local_rank):
@@ -251,12 +388,7 @@ def run_b200(args, rank, world, local_rank):
     for opt in args.option:
         name, value = opt.split("=", 1)
         dev.set_option(name, int(value))
-    a_full = make_matrix(cfg, dev)
-    r0, r1 = shard_rows(a_full, world, rank)
-    off = a_full.offsets[r0:r1 + 1] - a_full.offsets[r0]
-    sl = slice(int(a_full.offsets[r0]), int(a_full.offsets[r1]))
-    a = d.SparseMatrix(r1 - r0, a_full.cols, off, a_full.col_indices[sl].copy(),
-                       a_full.values[sl].copy())
+    a, nnz_global, r0 = b200_matrix(cfg, dev, world, rank)
     scfg = solver_config(cfg)
     k, l = scfg.k, scfg.sketch_width()
 
@@ -266,7 +398,7 @@ def run_b200(args, rank, world, local_rank):
             uid.copy_(torch.tensor(list(d.comm_unique_id()), dtype=torch.uint8))
         dist.broadcast(uid, 0)
         dev.attach_comm(world, rank, bytes(uid.cpu().tolist()))
-        dev.set_shard(r0, a_full.rows)
+        dev.set_shard(r0, cfg["rows"])
     dev.set_profiling(True)
 
     def barrier():
@@ -304,17 +436,10 @@ def run_b200(args, rank, world, local_rank):
     def e2e_step():
         return d.solve(a, scfg, device=dev, out=(hu, hs, hv))
 
-    # device-resident phase, then (workspaces released) the end-to-end phase
-    for _ in range(args.warmup):
-        dev_step()
-    clocks = ClockSampler(local_rank)
-    stats_list = []
     # L2 policy: inputs larger than L2 run back to back; a working set that
     # could stay L2-resident between steps gets a 512 MB write (a flush)
     # before every timed step, outside that step's events
-    ld_ws = (l + 3) // 4 * 4
-    working_set = 24 * a.nnz + 8 * a.rows * ld_ws + 3 * 8 * a.cols * ld_ws
-    flush_l2 = working_set < 2 * 126 * 2**20
+    flush_l2 = l2_flush(cfg, nnz_global)
     flush_buf = torch.empty(512 * 2**20, dtype=torch.uint8, device="cuda") if flush_l2 else None
 
     def timed(step, collect=None):
@@ -336,6 +461,11 @@ def run_b200(args, rank, world, local_rank):
                 collect.append(r.stats)
         return total, r
 
+    # device-resident phase, then (workspaces released) the end-to-end phase
+    for _ in range(args.warmup):
+        dev_step()
+    clocks = ClockSampler(local_rank)
+    stats_list = []
     with clocks:
         barrier()
         dev_ms, res = timed(dev_step, stats_list)
@@ -369,33 +499,24 @@ def run_b200(args, rank, world, local_rank):
     # the row gathers actually moved through L1/L2: nnz * 8 * ld bytes per pass
     # (ld = l rounded up to 4), against the measured random-gather ceiling
     ld = (l + 3) // 4 * 4
-    gather_bytes_pass = a_full.nnz * 8 * ld
-    sp_passes = sum(s["spmm_launches"] for s in stats_list)
-    gather_tbs = gather_bytes_pass * sp_passes / (sp_ms * 1e-3) / 1e12 if sp_ms > 0 else None
+    gather_bytes_pass = a.nnz * 8 * ld
+    gather_tbs = gather_bytes_pass * sp_launch / (sp_ms * 1e-3) / 1e12 if sp_ms > 0 else None
     breakdown = {key: round(st0[key], 3) for key in ("total_ms", "csc_ms", "spmm_ms", "gram_ms",
-                                                      "eig_ms", "rescale_ms")}
+                                                      "eig_ms", "rescale_ms", "allreduce_ms")}
     breakdown["spmm_pass_ms"] = [round(x, 3) for x in st0["spmm_pass_ms"]]
-    breakdown["eig_sweeps"] = st0["eig_sweeps"]
+    breakdown["loop_schedule"] = "pipelined" if st0["pipelined"] else "serial"
 
     if rank != 0:
         return
     h2d = a.offsets.nbytes + a.col_indices.nbytes + a.values.nbytes
     d2h = hu.nbytes + hs.nbytes + hv.nbytes
     line = {
-        "metric": "dashSVD end-to-end seconds", "value": value, "unit": "s",
+        "metric": METRIC, "value": value, "unit": "s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": value * 1e3, "higher_is_better": False,
-        "scaling": "strong" if world > 1 else "strong", "vs_baseline": None, "dtype": "f64",
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": f"synthetic (seeded generator, BASELINE.json configs[{cfg['baseline_index']}] shape; no dataset)",
-        "config": {"workload": cfg["name"], "rows": a_full.rows, "cols": a_full.cols,
-                   "nnz": a_full.nnz, "k": k, "l": l, "p": scfg.p, "alg": cfg["alg"],
-                   "parallelism": f"row-shard x{world}" if world > 1 else "1 GPU",
-                   **({"options": args.option} if args.option else {}),
-                   "l2": (f"flushed: a 512 MB buffer is written before every timed step (per-step "
-                          f"working set {working_set / 2**20:.0f} MB could stay in the 126 MB L2)") if flush_l2 else
-                         (f"no flush: per-step working set (CSR+CSC {2 * 12 * a_full.nnz / 1e9:.2f} GB, "
-                          f"sketch/Y {8 * a_full.rows * ld / 1e9:.2f} GB, Q/T {8 * a_full.cols * ld / 1e9:.2f} GB "
-                          "each) exceeds the 126 MB L2")},
+        "config": config_dict(cfg, nnz_global, world),
         "e2e": {"value": e2e_value, "unit": "s", "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h)},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
@@ -414,11 +535,14 @@ def run_b200(args, rank, world, local_rank):
         "iterations": e2e_res.trace.iterations,
         "clocks": clocks.summary(),
     }
+    if world > 1:
+        line["mgpu_mode"] = "v1 all-reduce" if any(o == "mgpu_mode=1" for o in args.option) else \
+            "v2 reduce-scatter / all-gather"
+    if args.option:
+        line["options"] = args.option
     if world == 1 and not args.no_cpu_baseline:
-        threads = os.cpu_count() or 1
-        v, desc, kind, _ = reference_sample(a_full, cfg, threads, args.cpu_sample_p)
-        line["cpu_baseline"] = {"value": v, "unit": "s", "cores": threads, "kind": kind,
-                                "sample": desc}
+        np_target = e2e_res.trace.iterations if cfg["alg"] == "dash" else None
+        line["cpu_baseline"] = cpu_baseline_child(args, np_target)
     print(json.dumps(line), flush=True)
 
 

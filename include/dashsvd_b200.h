@@ -59,6 +59,7 @@ enum { DSVD_STOP_FIXED_P = 0, DSVD_STOP_TOL_MET = 1, DSVD_STOP_P_MAX_REACHED = 2
 
 typedef struct dsvd_ctx dsvd_ctx;       /* device, stream, workspaces, optional NCCL comm */
 typedef struct dsvd_matrix dsvd_matrix; /* device-resident CSR(A) + CSR(A^T)              */
+typedef struct dsvd_loopback dsvd_loopback; /* in-process rank group (testing)            */
 
 /* SolverConfig (solver.hpp:22-38). s < 0 means the default max(1, k/2).
  * flags: DSVD_FLAG_DIRECT runs the algorithm on `a` as given, like
@@ -118,7 +119,7 @@ typedef struct {
     double gram_ms;         /* Gram partials + reduction                         */
     double eig_ms;          /* Jacobi eigensolver + rotation replay + finish     */
     double rescale_ms;      /* Q = T V diag(1/s) (and finalize U, V products)    */
-    double allreduce_ms;    /* n x l partial-sum exchange (multi-GPU)            */
+    double allreduce_ms;    /* collectives of a row-sharded solve (multi-GPU)     */
     int64_t spmm_launches;
     int64_t kernel_launches;/* every kernel this library launched in the solve    */
     int64_t eig_sweeps;     /* Jacobi sweeps summed over all eigensolves          */
@@ -126,6 +127,7 @@ typedef struct {
     double spmm_pass_ms[2]; /* pass 1 (A Q) and pass 2 (A^T Y - alpha Q), summed  */
     int64_t spmm_pass_bytes[2];
     int64_t spmm_pass_launches[2];
+    int64_t pipelined;      /* loop schedule of the last solve: 1 pipelined, 0 serial */
 } dsvd_stats;
 
 /* ---- errors --------------------------------------------------------------- */
@@ -146,6 +148,8 @@ DSVD_API int dsvd_ctx_trim(dsvd_ctx* ctx);
 /* Tuning knobs (testing/benchmarking); unknown names -> DSVD_CONFIG.
  * Loop schedule: "pipeline" -1 auto (default) / 0 serial /
  * 1 pipelined; "eig_priority" 1 (default) / 0; "gram_async" 0 (default) / 1.
+ * Row-sharded solves: "mgpu_mode" 2 (default: reduce-scatter + slab dense work
+ * + all-gather) / 1 (all-reduce of the n x l partials, dense work redundant).
  * Kernels: "spmm_variant", "split_chunk", "split_chunk_t", "split_panel_rows",
  * "hub_threshold", "eig_method", "dense_method". */
 DSVD_API int dsvd_ctx_set_option(dsvd_ctx* ctx, const char* name, int64_t value);
@@ -156,6 +160,15 @@ DSVD_API int dsvd_ctx_set_option(dsvd_ctx* ctx, const char* name, int64_t value)
  * context treats the matrix it gets as that rank's row shard. */
 DSVD_API int dsvd_comm_unique_id(uint8_t out[128]);
 DSVD_API int dsvd_ctx_attach_comm(dsvd_ctx* ctx, int nranks, int rank, const uint8_t id[128]);
+/* In-process rank group (testing the row-sharded engine without a multi-GPU
+ * node): nranks (<= 8) contexts of ONE process, each driven by its own host
+ * thread, attach to the group; every collective synchronises the rank's
+ * stream, meets the others at a host barrier and sums their device buffers in
+ * fixed rank order. The contexts may share one GPU (no kernel waits on another
+ * rank). Destroy the group after every attached context. */
+DSVD_API int dsvd_loopback_create(int nranks, dsvd_loopback** out);
+DSVD_API int dsvd_loopback_destroy(dsvd_loopback* group);
+DSVD_API int dsvd_ctx_attach_loopback(dsvd_ctx* ctx, dsvd_loopback* group, int rank);
 /* Row-shard placement used by dsvd_solve_csr / dsvd_solve_csr_device on an
  * attached context: the CSR passed is rows [row_offset, row_offset + rows) of
  * a global_rows x cols matrix. */
@@ -191,6 +204,12 @@ DSVD_API int dsvd_matrix_bench_spmm(dsvd_matrix* m, int transpose, int64_t l, in
 DSVD_API int dsvd_matrix_hub_rows(const dsvd_matrix* m, int64_t* hub_a, int64_t* hub_at);
 /* Download CSR(A) as stored on the device (int64 offsets/indices, host buffers). */
 DSVD_API int dsvd_matrix_download(const dsvd_matrix* m, int64_t* offsets, int64_t* col_indices, double* values);
+/* Rows [r0, r1) of CSR(A) (offsets rebased to 0; r1 - r0 + 1 offsets), e.g. one
+ * rank's row shard of a matrix generated on the device. */
+DSVD_API int dsvd_matrix_download_rows(const dsvd_matrix* m, int64_t r0, int64_t r1, int64_t* offsets,
+                                       int64_t* col_indices, double* values);
+/* The rows + 1 offsets of CSR(A). */
+DSVD_API int dsvd_matrix_row_offsets(const dsvd_matrix* m, int64_t* offsets);
 /* Download the device-built transpose (int64 offsets/indices, host buffers). */
 DSVD_API int dsvd_matrix_download_transpose(const dsvd_matrix* m, int64_t* t_offsets,
                                    int64_t* t_col_indices, double* t_values);
@@ -343,6 +362,10 @@ DSVD_API int dsvd_matmul(dsvd_ctx* ctx, int64_t m, int64_t kk, int64_t n, const 
                 const double* b, double* c);
 /* gaussian_matrix (random.hpp:20 / .cpp:29-36). */
 DSVD_API int dsvd_gaussian_matrix(dsvd_ctx* ctx, int64_t rows, int64_t cols, uint64_t seed, double* out);
+/* Rows [row_offset, row_offset + rows) of gaussian_matrix(global_rows, cols, seed)
+ * (a row shard's sketch Omega_g, random.cpp:29-36 with e = j*global_rows + i). */
+DSVD_API int dsvd_gaussian_rows(dsvd_ctx* ctx, int64_t rows, int64_t cols, uint64_t seed, int64_t global_rows,
+                                int64_t row_offset, double* out);
 DSVD_API uint64_t dsvd_splitmix64_at(uint64_t seed, uint64_t i);
 
 /* ---- synthetic inputs (host, deterministic, thread-count invariant) ------

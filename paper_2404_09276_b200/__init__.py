@@ -10,7 +10,7 @@ from .api import (Algorithm, assemble, eps_sigma, load_dense_array, load_referen
                   write_reference_spectrum, load_cache, load_matrix_market, read_matrix_market_triplets, save_cache, write_matrix_market, Device, DeviceMatrix, EigenPair, IterationState, Orthonormalizer,
                   ShiftTrace, SolveResult, SolverConfig, SparseMatrix, StopReason, TruncatedSvd,
                   basic_rsvd, comm_unique_id, dash_svd, default_device, eig_svd, eps_pve, eps_res,
-                  eps_spec, finalize_row_basis, gaussian_matrix, gram, matmul, max_triplet_residual,
+                  eps_spec, finalize_row_basis, gaussian_matrix, gaussian_rows, gram, LoopbackGroup, matmul, max_triplet_residual,
                   pin, powerlaw, pve_stop_check, rmat,
                   shifted_rsvd, solve, sparse_random, splitmix64_at, spmm, spmm_shift, sym_eig,
                   transpose, unpin, update_shift, validate_config)

@@ -46,7 +46,7 @@ class dsvd_stats(C.Structure):
                 ("eig_ms", D), ("rescale_ms", D), ("allreduce_ms", D), ("spmm_launches", I64),
                 ("kernel_launches", I64), ("eig_sweeps", I64), ("spmm_bytes", I64),
                 ("spmm_pass_ms", D * 2), ("spmm_pass_bytes", I64 * 2),
-                ("spmm_pass_launches", I64 * 2)]
+                ("spmm_pass_launches", I64 * 2), ("pipelined", I64)]
 
     def as_dict(self):
         out = {}
@@ -73,6 +73,9 @@ SIGNATURES = [
     ("dsvd_comm_unique_id", C.c_int, [C.POINTER(C.c_uint8)]),
     ("dsvd_ctx_attach_comm", C.c_int, [P, C.c_int, C.c_int, C.POINTER(C.c_uint8)]),
     ("dsvd_ctx_set_shard", C.c_int, [P, I64, I64]),
+    ("dsvd_loopback_create", C.c_int, [C.c_int, C.POINTER(P)]),
+    ("dsvd_loopback_destroy", C.c_int, [P]),
+    ("dsvd_ctx_attach_loopback", C.c_int, [P, P, C.c_int]),
     ("dsvd_host_register", C.c_int, [P, C.c_size_t]),
     ("dsvd_host_unregister", C.c_int, [P]),
     ("dsvd_matrix_upload", C.c_int, [P, I64, I64, I64, P, P, P, C.POINTER(P)]),
@@ -82,6 +85,8 @@ SIGNATURES = [
     ("dsvd_matrix_shape", C.c_int, [P, C.POINTER(I64), C.POINTER(I64), C.POINTER(I64)]),
     ("dsvd_matrix_download_transpose", C.c_int, [P, P, P, P]),
     ("dsvd_matrix_download", C.c_int, [P, P, P, P]),
+    ("dsvd_matrix_download_rows", C.c_int, [P, I64, I64, P, P, P]),
+    ("dsvd_matrix_row_offsets", C.c_int, [P, P]),
     ("dsvd_matrix_bench_spmm", C.c_int, [P, C.c_int, I64, C.c_int, C.c_int, C.POINTER(D)]),
     ("dsvd_matrix_hub_rows", C.c_int, [P, C.POINTER(I64), C.POINTER(I64)]),
     ("dsvd_solve", C.c_int, [P, P, C.POINTER(dsvd_config), C.POINTER(dsvd_outputs), OBSERVER, P]),
@@ -123,6 +128,7 @@ SIGNATURES = [
     ("dsvd_eig_svd", C.c_int, [P, I64, I64, P, P, P, P]),
     ("dsvd_matmul", C.c_int, [P, I64, I64, I64, P, P, P]),
     ("dsvd_gaussian_matrix", C.c_int, [P, I64, I64, U64, P]),
+    ("dsvd_gaussian_rows", C.c_int, [P, I64, I64, U64, I64, I64, P]),
     ("dsvd_splitmix64_at", U64, [U64, U64]),
     ("dsvd_synth_sparse_random", C.c_int, [I64, I64, I64, U64, C.c_int, C.POINTER(I64)]),
     ("dsvd_synth_powerlaw", C.c_int, [I64, I64, D, D, D, C.c_int, U64, C.POINTER(I64)]),

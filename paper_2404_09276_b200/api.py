@@ -285,6 +285,13 @@ class Device:
         buf = (C.c_uint8 * 128).from_buffer_copy(unique_id)
         check(lib().dsvd_ctx_attach_comm(self._h, int(nranks), int(rank), buf))
 
+    def attach_loopback(self, group: "LoopbackGroup", rank: int) -> None:
+        """Join an in-process rank group (dsvd_ctx_attach_loopback): solves on this
+        context then run the row-sharded engine as `rank` of `group.nranks`, with the
+        collectives summed on the host side in rank order (testing without NCCL)."""
+        check(lib().dsvd_ctx_attach_loopback(self._h, group.handle, int(rank)))
+        group._members.append(self)
+
     def set_shard(self, row_offset: int, global_rows: int) -> None:
         """The CSR given to solve() is rows [row_offset, row_offset + rows) of a
         global_rows x cols matrix (row-sharded multi-GPU solve)."""
@@ -322,6 +329,37 @@ def pin(arr: np.ndarray) -> np.ndarray:
 def unpin(arr: np.ndarray) -> None:
     if arr.nbytes:
         check(lib().dsvd_host_unregister(arr.ctypes.data_as(_P)))
+
+
+class LoopbackGroup:
+    """In-process group of `nranks` contexts (one host thread each) standing in for
+    an NCCL communicator, e.g. several ranks on one GPU (dsvd_loopback_create).
+    Close (or drop) every member Device before the group."""
+
+    def __init__(self, nranks: int):
+        h = _P()
+        check(lib().dsvd_loopback_create(int(nranks), C.byref(h)))
+        self._h = h
+        self.nranks = int(nranks)
+        self._members = []
+
+    @property
+    def handle(self):
+        return self._h
+
+    def close(self) -> None:
+        for dev in self._members:
+            dev.close()
+        self._members = []
+        if self._h:
+            check(lib().dsvd_loopback_destroy(self._h))
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def comm_unique_id() -> bytes:
@@ -398,6 +436,21 @@ class DeviceMatrix:
         check(lib().dsvd_matrix_download(self._h, _ptr(off), _ptr(idx), _ptr(val)))
         return SparseMatrix(self.rows, self.cols, off, idx, val)
 
+    def download_rows(self, r0: int, r1: int) -> SparseMatrix:
+        """Rows [r0, r1) of CSR(A) as a standalone host CSR (e.g. one rank's shard)."""
+        offs = self.row_offsets()
+        n = int(offs[r1] - offs[r0])
+        off = np.empty(r1 - r0 + 1, dtype=np.int64)
+        idx = np.empty(n, dtype=np.int64)
+        val = np.empty(n, dtype=np.float64)
+        check(lib().dsvd_matrix_download_rows(self._h, int(r0), int(r1), _ptr(off), _ptr(idx), _ptr(val)))
+        return SparseMatrix(r1 - r0, self.cols, off, idx, val)
+
+    def row_offsets(self) -> np.ndarray:
+        off = np.empty(self.rows + 1, dtype=np.int64)
+        check(lib().dsvd_matrix_row_offsets(self._h, _ptr(off)))
+        return off
+
     def set_shard(self, row_offset: int, global_rows: int) -> None:
         check(lib().dsvd_matrix_set_shard(self._h, int(row_offset), int(global_rows)))
 
@@ -445,9 +498,13 @@ def _make_outputs(rows, cols, cfg, out=None):
     cap = _trace_cap(cfg)
     if out is not None:  # caller-provided (e.g. pinned) buffers
         u, s, v = out
+        if any(not isinstance(b, np.ndarray) or b.dtype != np.float64 for b in (u, s, v)):
+            raise E.ConfigError("out: u, s and v must be float64 numpy arrays")
+        if any(not b.flags.writeable for b in (u, s, v)):
+            raise E.ConfigError("out: u, s and v must be writeable")
         if u.shape != (rows, k) or v.shape != (cols, k) or s.shape != (k,) or \
-                not u.flags.f_contiguous or not v.flags.f_contiguous:
-            raise E.ShapeError("out: expected Fortran-ordered u (rows x k), v (cols x k), s (k)")
+                not u.flags.f_contiguous or not v.flags.f_contiguous or not s.flags.c_contiguous:
+            raise E.ShapeError("out: expected Fortran-ordered u (rows x k), v (cols x k), contiguous s (k)")
     else:
         u = np.empty((rows, k), dtype=np.float64, order="F")
         s = np.empty(k, dtype=np.float64)
@@ -700,6 +757,17 @@ def gaussian_matrix(rows: int, cols: int, seed: int, device: Optional[Device] = 
     dev = _dev(device)
     check(lib().dsvd_gaussian_matrix(dev.handle, int(rows), int(cols),
                                      int(seed) & 0xFFFFFFFFFFFFFFFF, _ptr(out)))
+    return out
+
+
+def gaussian_rows(rows: int, cols: int, seed: int, global_rows: int, row_offset: int,
+                  device: Optional[Device] = None) -> np.ndarray:
+    """Rows [row_offset, row_offset + rows) of gaussian_matrix(global_rows, cols, seed): the
+    sketch block Omega_g a row shard generates locally (random.cpp:29-36)."""
+    out = np.empty((rows, cols), order="F")
+    dev = _dev(device)
+    check(lib().dsvd_gaussian_rows(dev.handle, int(rows), int(cols), int(seed) & 0xFFFFFFFFFFFFFFFF,
+                                   int(global_rows), int(row_offset), _ptr(out)))
     return out
 
 

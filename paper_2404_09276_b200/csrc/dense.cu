@@ -18,7 +18,10 @@ constexpr int kK = 16;
 __global__ void gaussian_kernel(double* __restrict__ out, int64_t rows, int64_t l, int64_t ld,
                                 uint64_t seed, int64_t global_rows, int64_t row_offset) {
     const int64_t total = rows * ld;
-    if (total < (int64_t(1) << 32)) {  // 32-bit index arithmetic (no emulated 64-bit division)
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    // 32-bit index arithmetic (no emulated 64-bit division) only when no thread's
+    // index can wrap past 2^32 while still below total: total + stride <= 2^32
+    if (total + stride <= (int64_t(1) << 32)) {
         const uint32_t ld32 = static_cast<uint32_t>(ld);
         for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < static_cast<uint32_t>(total);
              e += gridDim.x * blockDim.x) {

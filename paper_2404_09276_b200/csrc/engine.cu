@@ -439,9 +439,21 @@ void solve_tall(dsvd_ctx* ctx, const DevCsr& A, const DevCsr& AT, const dsvd_con
     const int64_t max_iters = dash ? cfg.p_max : cfg.p;
     if (l > 512) fail(DSVD_UNSUPPORTED, "sketch width l > 512 is not supported");
 
+    // Row-sharded v2: the n-row blocks carry n_full = G * n_slab rows
+    // (zero padding rows at the end, so the reduce-scatter splits them evenly);
+    // this rank owns rows [slab0, slab0 + n_slab) of every reduced sum.
+    const bool v2 = sharded && ctx->mgpu_mode == 2;
+    const int64_t n_slab = v2 ? ceil_div(n, ctx->nranks) : n;
+    const int64_t n_full = v2 ? n_slab * ctx->nranks : n;
+    const int64_t slab0 = v2 ? ctx->rank * n_slab : 0;
     double* Y = ctx->tbuf<double>("Y", m * ld);  // Omega, then A Q, then B
-    double* T = ctx->tbuf<double>("T", n * ld);
-    double* Qb[2] = {ctx->tbuf<double>("Q0", n * ld), ctx->tbuf<double>("Q1", n * ld)};
+    double* T = ctx->tbuf<double>("T", n_full * ld);
+    double* Qb[2] = {ctx->tbuf<double>("Q0", n_full * ld), ctx->tbuf<double>("Q1", n_full * ld)};
+    double* S = v2 ? ctx->tbuf<double>("slab", n_slab * ld) : nullptr;
+    if (n_full > n) {  // padding rows stay zero: SpMM writes rows [0, n) only
+        for (double* b : {T, Qb[0], Qb[1]})
+            DSVD_CUDA_CHECK(cudaMemsetAsync(b + n * ld, 0, sizeof(double) * (n_full - n) * ld, st));
+    }
     double* W = ctx->tbuf<double>("W", l * l);
     double* sv = ctx->tbuf<double>("s", l);
     double* inv_s = ctx->tbuf<double>("inv_s", l);
@@ -485,9 +497,44 @@ void solve_tall(dsvd_ctx* ctx, const DevCsr& A, const DevCsr& AT, const dsvd_con
     // auto: pipelined when the eig chain it hides is worth >= 5% of the two
     // SpMM passes it overlaps (gathers at ~20 TB/s; eig ~0.65 ms at l = 150,
     // quadratic in l; tools/ab_option.py pipeline on C2 / C3 / C4 in DESIGN 5)
-    const double spmm_s = 2.0 * static_cast<double>(A.nnz) * static_cast<double>(ld) * 8.0 / 20e12;
+    // (sharded: from the GLOBAL nnz, so every rank takes the same schedule — the
+    // two schedules reduce different partials, A^T A T_{j-1} vs A^T A Q_{j-1})
+    const double nnz_sched = (sharded && ctx->pipeline < 0) ? comm_sum_host(ctx, static_cast<double>(A.nnz))
+                                                            : static_cast<double>(A.nnz);
     const double eig_s = 0.65e-3 * (static_cast<double>(l) / 150.0) * (static_cast<double>(l) / 150.0);
-    const bool pipelined = ctx->pipeline == 1 || (ctx->pipeline < 0 && eig_s >= 0.05 * spmm_s);
+    // eig_s >= 0.05 spmm_s with spmm_s = 2 nnz ld 8 B / 20 TB/s, as an nnz bound
+    const double nnz_auto = ctx->pipeline_auto_nnz > 0 ? static_cast<double>(ctx->pipeline_auto_nnz)
+                                                       : eig_s / (0.05 * 2.0 * static_cast<double>(ld) * 8.0 / 20e12);
+    const bool pipelined = ctx->pipeline == 1 || (ctx->pipeline < 0 && nnz_sched <= nnz_auto);
+    ctx->stats.pipelined = pipelined ? 1 : 0;
+    // Sharded exchange of an n x l partial P (the A^T pass of this rank's rows):
+    // v1 all-reduces it in place and returns P (n rows); v2 reduce-scatters it
+    // and returns this rank's n_slab-row slab of the sum.
+    auto reduce_partial = [&](double* part) -> double* {
+        const int s2 = ctx->span_begin(K_COMM);
+        if (v2) comm_reduce_scatter_sum(ctx, part, S, static_cast<size_t>(n_slab * ld));
+        else comm_allreduce_sum(ctx, part, static_cast<size_t>(n * ld));
+        ctx->span_end(s2);
+        return v2 ? S : part;
+    };
+    // rows of a reduced block handled by this rank, and their offset in a full block
+    const int64_t red_rows = v2 ? n_slab : n;
+    // eigSVD factors of a reduced block (v2: slab Gram + l x l all-reduce)
+    auto factors = [&](const double* c, const LoopStep* lsp, const int32_t* g, cudaStream_t es) {
+        eig_svd_factors(ctx, c, red_rows, l, ld, eo, ctrl, lsp, g, v2, v2 ? n : -1, es);
+    };
+    // dst (full n-row block) = c W diag(1/s) for a reduced block c; v2 rescales
+    // the slab into its rows of dst and all-gathers the other ranks' slabs
+    auto rescale_into = [&](const double* c, double* dst, const int32_t* g) {
+        int s2 = ctx->span_begin(K_RESCALE);
+        solve_rescale(ctx, c, red_rows, l, ld, W, l, inv_s, l, dst + slab0 * ld, ld, 0, g);
+        ctx->span_end(s2);
+        if (v2) {
+            s2 = ctx->span_begin(K_COMM);
+            comm_allgather(ctx, dst + slab0 * ld, dst, static_cast<size_t>(n_slab * ld));
+            ctx->span_end(s2);
+        }
+    };
     if (pipelined) {
         // Deferred rescale. With Q_{j-1} = T_{j-1} W_{j-1} (W = V diag(1/s) of
         // eigSVD(T_{j-1}), sign convention folded in), the reference's
@@ -504,7 +551,7 @@ void solve_tall(dsvd_ctx* ctx, const DevCsr& A, const DevCsr& AT, const dsvd_con
         double* P = Qb[1];
         // Gram on st (all SMs), then the eig chain on the priority stream
         auto eig_async = [&](const double* tj, const LoopStep* lsp, const int32_t* g) {
-            eig_svd_factors(ctx, tj, n, l, ld, eo, ctrl, lsp, g, false, -1, ctx->eig);
+            factors(tj + slab0 * ld, lsp, g, ctx->eig);  // v2: this rank's slab of T_j
             DSVD_CUDA_CHECK(cudaEventRecord(ctx->ev_eig, ctx->eig));
         };
         double* Qobs[2] = {nullptr, nullptr};
@@ -519,9 +566,14 @@ void solve_tall(dsvd_ctx* ctx, const DevCsr& A, const DevCsr& AT, const dsvd_con
         count_launch();
         ctx->span_end(sp);
         if (sharded) {
-            sp = ctx->span_begin(K_COMM);
-            comm_allreduce_sum(ctx, Tb[0], static_cast<size_t>(n * ld));
-            ctx->span_end(sp);
+            double* red = reduce_partial(Tb[0]);
+            if (v2) {  // T_0 = the gathered slabs of the sum
+                DSVD_CUDA_CHECK(cudaMemcpyAsync(Tb[0] + slab0 * ld, red, sizeof(double) * n_slab * ld,
+                                                cudaMemcpyDeviceToDevice, st));
+                sp = ctx->span_begin(K_COMM);
+                comm_allgather(ctx, Tb[0] + slab0 * ld, Tb[0], static_cast<size_t>(n_slab * ld));
+                ctx->span_end(sp);
+            }
         }
         eig_async(Tb[0], nullptr, nullptr);
         if (observer) {
@@ -556,13 +608,10 @@ void solve_tall(dsvd_ctx* ctx, const DevCsr& A, const DevCsr& AT, const dsvd_con
                 DSVD_CUDA_CHECK(cudaStreamWaitEvent(st, ctx->ev_eig, 0));
                 loop_begin(ctrl, st);
                 count_launch();
-                if (sharded) {
-                    sp = ctx->span_begin(K_COMM);
-                    comm_allreduce_sum(ctx, P, static_cast<size_t>(n * ld));
-                    ctx->span_end(sp);
-                }
-                shift_update(P, tprev, n * ld, &ctrl->alpha, gate, st);
+                double* red = sharded ? reduce_partial(P) : P;
+                shift_update(red, tprev + slab0 * ld, red_rows * ld, &ctrl->alpha, gate, st);
                 count_launch();
+                rescale_into(red, Tb[j % 2], gate);
             } else {
                 DSVD_CUDA_CHECK(cudaStreamWaitEvent(st, ctx->ev_eig, 0));
                 loop_begin(ctrl, st);
@@ -573,18 +622,15 @@ void solve_tall(dsvd_ctx* ctx, const DevCsr& A, const DevCsr& AT, const dsvd_con
                      st, ctx->spmm_variant, ctx->side, ctx->fork, ctx->join, partial_for(ctx, AT, ld));
                 count_launch();
                 ctx->span_end(sp);
+                double* red = P;
                 if (sharded) {
-                    sp = ctx->span_begin(K_COMM);
-                    comm_allreduce_sum(ctx, P, static_cast<size_t>(n * ld));
-                    ctx->span_end(sp);
-                    shift_update(P, tprev, n * ld, &ctrl->alpha, gate, st);
+                    red = reduce_partial(P);
+                    shift_update(red, tprev + slab0 * ld, red_rows * ld, &ctrl->alpha, gate, st);
                     count_launch();
                 }
+                // T_j = P W_{j-1} diag(1/s_{j-1})  (= A^T A Q_{j-1} - alpha Q_{j-1})
+                rescale_into(red, Tb[j % 2], gate);
             }
-            // T_j = P W_{j-1} diag(1/s_{j-1})  (= A^T A Q_{j-1} - alpha Q_{j-1})
-            sp = ctx->span_begin(K_RESCALE);
-            solve_rescale(ctx, P, n, l, ld, W, l, inv_s, l, Tb[j % 2], ld, 0, gate);
-            ctx->span_end(sp);
             eig_async(Tb[j % 2], &ls, gate);
             if (dash) {
                 const int slot = static_cast<int>(j % (kLookahead + 1));
@@ -630,15 +676,9 @@ void solve_tall(dsvd_ctx* ctx, const DevCsr& A, const DevCsr& AT, const dsvd_con
              ctx->join, partial_for(ctx, AT, ld));
         count_launch();
         ctx->span_end(sp);
-        if (sharded) {
-            sp = ctx->span_begin(K_COMM);
-            comm_allreduce_sum(ctx, T, static_cast<size_t>(n * ld));
-            ctx->span_end(sp);
-        }
-        eig_svd_factors(ctx, T, n, l, ld, eo, ctrl, nullptr, nullptr);
-        sp = ctx->span_begin(K_RESCALE);
-        solve_rescale(ctx, T, n, l, ld, W, l, inv_s, l, Qb[0], ld, 0, nullptr);
-        ctx->span_end(sp);
+        const double* red0 = sharded ? reduce_partial(T) : T;
+        factors(red0, nullptr, nullptr, nullptr);
+        rescale_into(red0, Qb[0], nullptr);
 
 
         int cur = 0;
@@ -663,18 +703,15 @@ void solve_tall(dsvd_ctx* ctx, const DevCsr& A, const DevCsr& AT, const dsvd_con
                  st, ctx->spmm_variant, ctx->side, ctx->fork, ctx->join, partial_for(ctx, AT, ld));
             count_launch();
             ctx->span_end(sp);
+            double* red = T;
             if (sharded) {
                 // sum the partials first, then apply the shift once (solver.cpp:94)
-                sp = ctx->span_begin(K_COMM);
-                comm_allreduce_sum(ctx, T, static_cast<size_t>(n * ld));
-                ctx->span_end(sp);
-                shift_update(T, Qb[cur], n * ld, &ctrl->alpha, gate, st);
+                red = reduce_partial(T);
+                shift_update(red, Qb[cur] + slab0 * ld, red_rows * ld, &ctrl->alpha, gate, st);
                 count_launch();
             }
-            eig_svd_factors(ctx, T, n, l, ld, eo, ctrl, &ls, gate);
-            sp = ctx->span_begin(K_RESCALE);
-            solve_rescale(ctx, T, n, l, ld, W, l, inv_s, l, Qb[1 - cur], ld, 0, gate);
-            ctx->span_end(sp);
+            factors(red, &ls, gate, nullptr);
+            rescale_into(red, Qb[1 - cur], gate);
             if (dash) {
                 const int slot = static_cast<int>(j % (kLookahead + 1));
                 if (flag_ev[slot] == nullptr) flag_ev[slot] = ctx->event();
@@ -777,6 +814,7 @@ void end_profile(dsvd_ctx* ctx, int64_t launches_before) {
             case K_GRAM: s.gram_ms += ms; break;
             case K_EIG: s.eig_ms += ms; break;
             case K_RESCALE: s.rescale_ms += ms; break;
+            case K_COMM: s.allreduce_ms += ms; break;
             default: break;
         }
     }
@@ -1139,6 +1177,7 @@ int dsvd_ctx_set_option(dsvd_ctx* ctx, const char* name, int64_t value) {
         } else if (n == "eig_priority") {
             // 1: the eig stream at the highest priority (default), 0: default priority
             if (value < 0 || value > 1) fail(DSVD_CONFIG, "eig_priority must be 0 or 1");
+            set_device(ctx);  // the new stream must belong to the context's device
             DSVD_CUDA_CHECK(cudaStreamSynchronize(ctx->eig));
             DSVD_CUDA_CHECK(cudaStreamDestroy(ctx->eig));
             int lo = 0, hi = 0;
@@ -1156,6 +1195,13 @@ int dsvd_ctx_set_option(dsvd_ctx* ctx, const char* name, int64_t value) {
         } else if (n == "split_panel_rows") {
             if (value < 0) fail(DSVD_CONFIG, "split_panel_rows must be >= 0");
             ctx->split_panel_rows = value;
+        } else if (n == "pipeline_auto_nnz") {
+            // the auto schedule's nnz bound (pipelined at or below it); 0 = the cost model
+            if (value < 0) fail(DSVD_CONFIG, "pipeline_auto_nnz must be >= 0");
+            ctx->pipeline_auto_nnz = value;
+        } else if (n == "mgpu_mode") {
+            if (value < 1 || value > 2) fail(DSVD_CONFIG, "mgpu_mode: 1 = all-reduce (v1), 2 = reduce-scatter (v2)");
+            ctx->mgpu_mode = static_cast<int>(value);
         } else if (n == "split_chunk") {
             if (value < 0) fail(DSVD_CONFIG, "split_chunk must be >= 0");
             ctx->split_chunk = value;
@@ -1297,6 +1343,35 @@ int dsvd_matrix_download_transpose(const dsvd_matrix* m, int64_t* t_off, int64_t
 
 int dsvd_matrix_download(const dsvd_matrix* m, int64_t* off, int64_t* idx, double* val) {
     return guarded([&] { download_csr(m, m->a, off, idx, val); });
+}
+
+int dsvd_matrix_download_rows(const dsvd_matrix* m, int64_t r0, int64_t r1, int64_t* off, int64_t* idx,
+                              double* val) {
+    return guarded([&] {
+        const DevCsr& c = m->a;
+        if (r0 < 0 || r1 < r0 || r1 > c.rows) fail(DSVD_SHAPE, "download_rows: row range out of bounds");
+        dsvd_ctx* ctx = m->ctx;
+        set_device(ctx);
+        cudaStream_t st = ctx->stream;
+        DSVD_CUDA_CHECK(cudaMemcpyAsync(off, c.off + r0, sizeof(int64_t) * (r1 - r0 + 1), cudaMemcpyDeviceToHost, st));
+        DSVD_CUDA_CHECK(cudaStreamSynchronize(st));
+        const int64_t p0 = off[0], n = off[r1 - r0] - p0;
+        for (int64_t i = 0; i <= r1 - r0; ++i) off[i] -= p0;
+        if (n > 0) {
+            int64_t* w = ctx->tbuf<int64_t>("dl.idx64", n);
+            widen_indices(c.idx + p0, w, n, st);
+            DSVD_CUDA_CHECK(cudaMemcpyAsync(idx, w, sizeof(int64_t) * n, cudaMemcpyDeviceToHost, st));
+            DSVD_CUDA_CHECK(cudaMemcpyAsync(val, c.val + p0, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
+        }
+        DSVD_CUDA_CHECK(cudaStreamSynchronize(st));
+    });
+}
+
+int dsvd_matrix_row_offsets(const dsvd_matrix* m, int64_t* off) {
+    return guarded([&] {
+        set_device(m->ctx);
+        DSVD_CUDA_CHECK(cudaMemcpy(off, m->a.off, sizeof(int64_t) * (m->a.rows + 1), cudaMemcpyDeviceToHost));
+    });
 }
 
 int dsvd_solve(dsvd_ctx* ctx, const dsvd_matrix* a, const dsvd_config* cfg, dsvd_outputs* out,
@@ -1652,14 +1727,21 @@ int dsvd_matmul(dsvd_ctx* ctx, int64_t m, int64_t kk, int64_t n, const double* a
 }
 
 int dsvd_gaussian_matrix(dsvd_ctx* ctx, int64_t rows, int64_t cols, uint64_t seed, double* out) {
+    return dsvd_gaussian_rows(ctx, rows, cols, seed, rows, 0, out);
+}
+
+int dsvd_gaussian_rows(dsvd_ctx* ctx, int64_t rows, int64_t cols, uint64_t seed, int64_t global_rows,
+                       int64_t row_offset, double* out) {
     return guarded([&] {
         set_device(ctx);
         cudaStream_t st = ctx->stream;
+        if (rows < 0 || cols < 0 || row_offset < 0 || global_rows < row_offset + rows)
+            fail(DSVD_SHAPE, "gaussian rows exceed the global row count");
         if (rows * cols == 0) return;
         const int64_t ld = padded_ld(cols);
         double* R = ctx->tbuf<double>("k.omega", rows * ld);
         double* Cm = ctx->tbuf<double>("k.omegacm", rows * cols);
-        gaussian_rowmajor(R, rows, cols, ld, seed, st);
+        gaussian_rowmajor(R, rows, cols, ld, seed, st, global_rows, row_offset);
         rowmajor_to_colmajor(R, rows, cols, ld, Cm, st);
         DSVD_CUDA_CHECK(cudaMemcpyAsync(out, Cm, sizeof(double) * rows * cols, cudaMemcpyDeviceToHost, st));
         DSVD_CUDA_CHECK(cudaStreamSynchronize(st));

@@ -27,8 +27,17 @@ struct TimedSpan {
     cudaEvent_t a, b;
 };
 
-// Multi-GPU hooks (comm.cu). With one rank they are no-ops.
+// Multi-GPU hooks (comm.cu). With one rank they are no-ops (reduce-scatter /
+// all-gather then copy when send != recv).
+enum CommKind { COMM_NONE = 0, COMM_NCCL = 1, COMM_LOOPBACK = 2 };
+constexpr int kMaxLoopbackRanks = 8;
 void comm_allreduce_sum(dsvd_ctx* ctx, double* buf, size_t count);
+// recv (recvcount) = rows [rank * recvcount, (rank + 1) * recvcount) of the sum of every rank's send
+void comm_reduce_scatter_sum(dsvd_ctx* ctx, const double* send, double* recv, size_t recvcount);
+// recv (nranks * sendcount) = every rank's send in rank order (send may be this rank's slot of recv)
+void comm_allgather(dsvd_ctx* ctx, const double* send, double* recv, size_t sendcount);
+// sum of a host scalar over the ranks (synchronous)
+double comm_sum_host(dsvd_ctx* ctx, double v);
 void comm_release(dsvd_ctx* ctx);
 // thread-local last-error state of the C ABI (engine.cu)
 void set_error(const char* msg, long long index);
@@ -63,7 +72,8 @@ struct dsvd_ctx {
     // pipelined loop: A^T pass unshifted before the eig wait, shift as its own
     // kernel after it (1), or fused into the A^T pass after the wait (0)
     int shift_after = 0;  // pipelined loop: Gram on the eig stream too (beside the A T pass)
-    int pipeline = -1;  // -1: auto (pipeline_pays), 0: serial, 1: pipelined
+    int pipeline = -1;  // -1: auto (pipelined at or below an nnz bound), 0: serial, 1: pipelined
+    int64_t pipeline_auto_nnz = 0;  // override of the auto rule's nnz bound (0: cost model)
     // Omega generated on `side` while the host CSR uploads (host-input solves):
     // the next solve_tall with the same (m, l, seed) waits on omega_ev instead
     // of generating it
@@ -77,9 +87,16 @@ struct dsvd_ctx {
     cudaEvent_t fork = nullptr, join = nullptr;
     int32_t* host_flags = nullptr;  // pinned ring for stop flags
     cudaEvent_t timer[2] = {nullptr, nullptr};
-    // multi-GPU state (comm.cu): NCCL communicator when nranks > 1
+    // multi-GPU state (comm.cu): an NCCL communicator, or an in-process loopback
+    // group (testing); comm != nullptr marks a row-sharded solve
     void* comm = nullptr;
+    int comm_kind = dsvd::COMM_NONE;
+    dsvd_loopback* loopback = nullptr;
     int nranks = 1, rank = 0;
+    // sharded solves: 1 = v1 (all-reduce of the n x l partials, dense work
+    // redundant), 2 = v2 (reduce-scatter, slab Gram + l x l all-reduce, slab
+    // rescale, all-gather); SURVEY 8e
+    int mgpu_mode = 2;
     int64_t shard_row_offset = 0, shard_global_rows = -1;  // for the CSR entry points
 
     void* buf(const std::string& name, size_t bytes) {

@@ -1100,25 +1100,21 @@ void spmm(const SpmmArgs& s, cudaStream_t stream, int variant, cudaStream_t side
         }
     }
     if (hub > 0) {
-        static bool attr = false;
-        if (!attr) {
+        {  // per launch: the attribute is per device (a process may drive several GPUs)
             DSVD_CUDA_CHECK(cudaFuncSetAttribute(spmm_hub_kernel<true>,
                                                  cudaFuncAttributeMaxDynamicSharedMemorySize, kHubSmem));
             DSVD_CUDA_CHECK(cudaFuncSetAttribute(spmm_hub_kernel<false>,
                                                  cudaFuncAttributeMaxDynamicSharedMemorySize, kHubSmem));
-            attr = true;
         }
         DSVD_CUDA_CHECK(cudaEventRecord(fork, stream));
         DSVD_CUDA_CHECK(cudaStreamWaitEvent(side, fork, 0));
     }
     if (hub > 0 && !skip_hub && variant == 2) {
-        static bool dattr = false;
-        if (!dattr) {
+        {  // per launch: the attribute is per device (a process may drive several GPUs)
             DSVD_CUDA_CHECK(cudaFuncSetAttribute(spmm_hub_deep_kernel<true>,
                                                  cudaFuncAttributeMaxDynamicSharedMemorySize, kDeepSmem));
             DSVD_CUDA_CHECK(cudaFuncSetAttribute(spmm_hub_deep_kernel<false>,
                                                  cudaFuncAttributeMaxDynamicSharedMemorySize, kDeepSmem));
-            dattr = true;
         }
         const int nslab32 = static_cast<int>(ceil_div(s.ld, 32));
         const int64_t items = hub * nslab32;
@@ -1132,13 +1128,11 @@ void spmm(const SpmmArgs& s, cudaStream_t stream, int variant, cudaStream_t side
                 s.gate);
         DSVD_LAUNCH_CHECK();
     } else if (hub > 0 && !skip_hub && variant == 0) {
-        static bool tattr = false;
-        if (!tattr) {
+        {  // per launch: the attribute is per device (a process may drive several GPUs)
             DSVD_CUDA_CHECK(cudaFuncSetAttribute(spmm_hub_tma_kernel<true>,
                                                  cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem));
             DSVD_CUDA_CHECK(cudaFuncSetAttribute(spmm_hub_tma_kernel<false>,
                                                  cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem));
-            tattr = true;
         }
         const CUtensorMap xmap = make_xmap(s.x, a.cols, s.ld);
         const int nslab64 = static_cast<int>(ceil_div(s.ld, kTmaW));

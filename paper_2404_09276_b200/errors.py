@@ -54,4 +54,5 @@ class DeviceError(Error):
 
 
 class UnsupportedOnDevice(Error):
-    """A configuration the B200 path does not implement (e.g. the basic algorithm, l > 512)."""
+    """A configuration the B200 path does not implement (e.g. l > 512, QR with l > 160, the basic
+    algorithm on a row-sharded matrix)."""

@@ -3,9 +3,9 @@ built from /root/reference by oracle/Makefile). Run in the dev container:
 
     make -C oracle ref && python tests/golden/make_golden.py
 
-The fixtures pin the oracle restatement (tests/test_oracle_golden.py) and the
-GPU path (tests/test_gpu_golden.py) without needing /root/reference at test
-time. Large factors are stored as wrapping bit-sums plus a few rows.
+The fixtures pin the oracle restatement (tests/test_oracle_golden.py) without
+needing /root/reference at test time; the GPU tests (tests/test_gpu_*.py) then
+compare the device path against that pinned oracle. Large factors are stored as wrapping bit-sums plus a few rows.
 """
 import os
 import sys

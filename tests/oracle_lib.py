@@ -4,6 +4,9 @@
 - ``Reference`` — oracle/_ref/libdashsvd_ref.so, the unmodified reference core
   compiled from /root/reference plus oracle/ref_harness.cpp (present when it was
   built in the dev container; it travels to the GPU box as a built file).
+- ``InputsGen`` — oracle/_build/libinputs.so (oracle/inputs_gen.c): the synthetic
+  matrices of BASELINE.json configs 2-5 built on the host without the product
+  library (bench.py's reference arm).
 
 Both expose the same Python surface: column-major numpy arrays in and out, the
 reference's status codes turned into the exceptions of
@@ -21,6 +24,7 @@ import numpy as np
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 ORACLE_SO = os.path.join(ROOT, "oracle", "_build", "liboracle.so")
 REF_SO = os.path.join(ROOT, "oracle", "_ref", "libdashsvd_ref.so")
+INPUTS_SO = os.path.join(ROOT, "oracle", "_build", "libinputs.so")
 
 _P = C.c_void_p
 _I64 = C.c_int64
@@ -433,3 +437,42 @@ class Reference(_Lib):
             out["times"] = dict(transpose=float(tm[0]), solve=float(tm[1]),
                                 stamps=tm[2:2 + n].copy())
         return out
+
+
+class InputsGen:
+    """oracle/inputs_gen.c: R-MAT (configs 4/5) and power-law (configs 2/3) inputs,
+    bit-identical to the product's generators (tests/test_inputs_gen.py)."""
+
+    def __init__(self, path=INPUTS_SO):
+        if not os.path.exists(path):
+            raise FileNotFoundError(path)
+        self.lib = C.CDLL(path)
+        self.lib.gen_rmat.restype = C.c_int
+        self.lib.gen_rmat.argtypes = [C.c_int, _I64, _D, _D, _D, C.c_int, _U64, C.POINTER(_I64)]
+        self.lib.gen_powerlaw.restype = C.c_int
+        self.lib.gen_powerlaw.argtypes = [_I64, _I64, _D, _D, _D, C.c_int, _U64, C.POINTER(_I64)]
+        self.lib.gen_fetch.restype = None
+        self.lib.gen_fetch.argtypes = [_P, _P, _P]
+
+    def _fetch(self, rows, cols, nnz) -> Csr:
+        off = np.empty(rows + 1, dtype=np.int64)
+        idx = np.empty(nnz, dtype=np.int64)
+        val = np.empty(nnz, dtype=np.float64)
+        self.lib.gen_fetch(_ptr(off), _ptr(idx), _ptr(val))
+        return Csr(rows, cols, off, idx, val)
+
+    def rmat(self, scale, draws, a=0.57, b=0.19, c=0.19, uniform=False, seed=0) -> Csr:
+        nnz = _I64()
+        rc = self.lib.gen_rmat(int(scale), int(draws), a, b, c, 1 if uniform else 0, int(seed), C.byref(nnz))
+        if rc != 0:
+            raise RuntimeError(f"gen_rmat failed ({rc})")
+        n = 1 << int(scale)
+        return self._fetch(n, n, nnz.value)
+
+    def powerlaw(self, rows, cols, mu, sigma, zipf_s, seed, ratings=False) -> Csr:
+        nnz = _I64()
+        rc = self.lib.gen_powerlaw(int(rows), int(cols), mu, sigma, zipf_s, 1 if ratings else 0, int(seed),
+                                   C.byref(nnz))
+        if rc != 0:
+            raise RuntimeError(f"gen_powerlaw failed ({rc})")
+        return self._fetch(rows, cols, nnz.value)
