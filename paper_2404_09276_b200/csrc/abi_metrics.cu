@@ -35,7 +35,7 @@ double* upload_block(dsvd_ctx* ctx, const std::string& tag, const double* h, int
     return rm;
 }
 void mspmm(dsvd_ctx* ctx, const DevCsr& A, const double* x, double* y, int64_t ld, int64_t l) {
-    spmm(SpmmArgs{&A, x, y, ld, l, nullptr, nullptr, nullptr}, ctx->stream, ctx->spmm_variant, ctx->side,
+    spmm(SpmmArgs{&A, x, y, ld, l, nullptr, nullptr, nullptr}, ctx->stream, spmm_var(ctx, ld), ctx->side,
          ctx->fork, ctx->join, partial_for(ctx, A, ld));
 }
 std::vector<double> col_norms_host(dsvd_ctx* ctx, const double* x, int64_t ldx, const double* z, int64_t ldz,

@@ -561,7 +561,7 @@ void solve_tall(dsvd_ctx* ctx, const DevCsr& A, const DevCsr& AT, const dsvd_con
         }
         // T_0 = A^T Omega; eigSVD(T_0) gives Q_0 = T_0 W_0 (solver.cpp:84)
         sp = ctx->span_begin(K_SPMM2);
-        spmm(SpmmArgs{&AT, Y, Tb[0], ld, l, nullptr, nullptr, nullptr}, st, ctx->spmm_variant, ctx->side,
+        spmm(SpmmArgs{&AT, Y, Tb[0], ld, l, nullptr, nullptr, nullptr}, st, spmm_var(ctx, ld), ctx->side,
              ctx->fork, ctx->join, partial_for(ctx, AT, ld));
         count_launch();
         ctx->span_end(sp);
@@ -593,7 +593,7 @@ void solve_tall(dsvd_ctx* ctx, const DevCsr& A, const DevCsr& AT, const dsvd_con
             // this pass runs — blocks starting after a stop skip their rows)
             sp = ctx->span_begin(K_SPMM1);
             spmm(SpmmArgs{&A, tprev, Y, ld, l, nullptr, nullptr, dash ? &ctrl->stop_pending : gate}, st,
-                 ctx->spmm_variant, ctx->side,
+                 spmm_var(ctx, ld), ctx->side,
                  ctx->fork, ctx->join, partial_for(ctx, A, ld));
             count_launch();
             ctx->span_end(sp);
@@ -602,7 +602,7 @@ void solve_tall(dsvd_ctx* ctx, const DevCsr& A, const DevCsr& AT, const dsvd_con
                 // P <- fma(-alpha, T_{j-1}, P): the same bits as the fused epilogue
                 sp = ctx->span_begin(K_SPMM2);
                 spmm(SpmmArgs{&AT, Y, P, ld, l, nullptr, nullptr, dash ? &ctrl->stop_pending : gate}, st,
-                     ctx->spmm_variant, ctx->side, ctx->fork, ctx->join, partial_for(ctx, AT, ld));
+                     spmm_var(ctx, ld), ctx->side, ctx->fork, ctx->join, partial_for(ctx, AT, ld));
                 count_launch();
                 ctx->span_end(sp);
                 DSVD_CUDA_CHECK(cudaStreamWaitEvent(st, ctx->ev_eig, 0));
@@ -619,7 +619,7 @@ void solve_tall(dsvd_ctx* ctx, const DevCsr& A, const DevCsr& AT, const dsvd_con
                 // P = A^T Z - alpha T_{j-1}  (the shift skipped when alpha == 0)
                 sp = ctx->span_begin(K_SPMM2);
                 spmm(SpmmArgs{&AT, Y, P, ld, l, sharded ? nullptr : tprev, sharded ? nullptr : &ctrl->alpha, gate},
-                     st, ctx->spmm_variant, ctx->side, ctx->fork, ctx->join, partial_for(ctx, AT, ld));
+                     st, spmm_var(ctx, ld), ctx->side, ctx->fork, ctx->join, partial_for(ctx, AT, ld));
                 count_launch();
                 ctx->span_end(sp);
                 double* red = P;
@@ -672,7 +672,7 @@ void solve_tall(dsvd_ctx* ctx, const DevCsr& A, const DevCsr& AT, const dsvd_con
     } else {
         // Q = eigSVD(A^T Omega).u
         sp = ctx->span_begin(K_SPMM2);
-        spmm(SpmmArgs{&AT, Y, T, ld, l, nullptr, nullptr, nullptr}, st, ctx->spmm_variant, ctx->side, ctx->fork,
+        spmm(SpmmArgs{&AT, Y, T, ld, l, nullptr, nullptr, nullptr}, st, spmm_var(ctx, ld), ctx->side, ctx->fork,
              ctx->join, partial_for(ctx, AT, ld));
         count_launch();
         ctx->span_end(sp);
@@ -692,7 +692,7 @@ void solve_tall(dsvd_ctx* ctx, const DevCsr& A, const DevCsr& AT, const dsvd_con
             count_launch();
             // Y = A Q
             sp = ctx->span_begin(K_SPMM1);
-            spmm(SpmmArgs{&A, Qb[cur], Y, ld, l, nullptr, nullptr, gate}, st, ctx->spmm_variant, ctx->side,
+            spmm(SpmmArgs{&A, Qb[cur], Y, ld, l, nullptr, nullptr, gate}, st, spmm_var(ctx, ld), ctx->side,
                  ctx->fork, ctx->join, partial_for(ctx, A, ld));
             count_launch();
             ctx->span_end(sp);
@@ -700,7 +700,7 @@ void solve_tall(dsvd_ctx* ctx, const DevCsr& A, const DevCsr& AT, const dsvd_con
             sp = ctx->span_begin(K_SPMM2);
             spmm(SpmmArgs{&AT, Y, T, ld, l, sharded ? nullptr : Qb[cur], sharded ? nullptr : &ctrl->alpha,
                           gate},
-                 st, ctx->spmm_variant, ctx->side, ctx->fork, ctx->join, partial_for(ctx, AT, ld));
+                 st, spmm_var(ctx, ld), ctx->side, ctx->fork, ctx->join, partial_for(ctx, AT, ld));
             count_launch();
             ctx->span_end(sp);
             double* red = T;
@@ -751,7 +751,7 @@ void solve_tall(dsvd_ctx* ctx, const DevCsr& A, const DevCsr& AT, const dsvd_con
     control_init(ctrl, s_stored, static_cast<int>(l), st);
     count_launch();
     sp = ctx->span_begin(K_SPMM1);
-    spmm(SpmmArgs{&A, Qf, Y, ld, l, nullptr, nullptr, nullptr}, st, ctx->spmm_variant, ctx->side, ctx->fork,
+    spmm(SpmmArgs{&A, Qf, Y, ld, l, nullptr, nullptr, nullptr}, st, spmm_var(ctx, ld), ctx->side, ctx->fork,
          ctx->join, partial_for(ctx, A, ld));
     count_launch();
     ctx->span_end(sp);
@@ -859,7 +859,7 @@ void solve_basic(dsvd_ctx* ctx, const DevCsr& A, const DevCsr& AT, const dsvd_co
     count_launch();
     ctx->span_end(sp);
     sp = ctx->span_begin(K_SPMM1);
-    spmm(SpmmArgs{&A, T, Y, ld, l, nullptr, nullptr, nullptr}, st, ctx->spmm_variant, ctx->side, ctx->fork,
+    spmm(SpmmArgs{&A, T, Y, ld, l, nullptr, nullptr, nullptr}, st, spmm_var(ctx, ld), ctx->side, ctx->fork,
          ctx->join, partial_for(ctx, A, ld));
     count_launch();
     ctx->span_end(sp);
@@ -920,12 +920,12 @@ void solve_basic(dsvd_ctx* ctx, const DevCsr& A, const DevCsr& AT, const dsvd_co
     int cur = 0;
     for (int64_t j = 1; j <= p; ++j) {
         sp = ctx->span_begin(K_SPMM2);
-        spmm(SpmmArgs{&AT, Qb[cur], T, ld, l, nullptr, nullptr, nullptr}, st, ctx->spmm_variant, ctx->side,
+        spmm(SpmmArgs{&AT, Qb[cur], T, ld, l, nullptr, nullptr, nullptr}, st, spmm_var(ctx, ld), ctx->side,
              ctx->fork, ctx->join, partial_for(ctx, AT, ld));
         count_launch();
         ctx->span_end(sp);
         sp = ctx->span_begin(K_SPMM1);
-        spmm(SpmmArgs{&A, T, Y, ld, l, nullptr, nullptr, nullptr}, st, ctx->spmm_variant, ctx->side, ctx->fork,
+        spmm(SpmmArgs{&A, T, Y, ld, l, nullptr, nullptr, nullptr}, st, spmm_var(ctx, ld), ctx->side, ctx->fork,
              ctx->join, partial_for(ctx, A, ld));
         count_launch();
         ctx->span_end(sp);
@@ -952,7 +952,7 @@ void solve_basic(dsvd_ctx* ctx, const DevCsr& A, const DevCsr& AT, const dsvd_co
     control_init(ctrl, s_stored, static_cast<int>(l), st);
     count_launch();
     sp = ctx->span_begin(K_SPMM2);
-    spmm(SpmmArgs{&AT, Qf, T, ld, l, nullptr, nullptr, nullptr}, st, ctx->spmm_variant, ctx->side, ctx->fork,
+    spmm(SpmmArgs{&AT, Qf, T, ld, l, nullptr, nullptr, nullptr}, st, spmm_var(ctx, ld), ctx->side, ctx->fork,
          ctx->join, partial_for(ctx, AT, ld));
     count_launch();
     ctx->span_end(sp);
@@ -1162,6 +1162,13 @@ int dsvd_ctx_set_option(dsvd_ctx* ctx, const char* name, int64_t value) {
         const std::string n = name ? name : "";
         if (n == "spmm_variant") {
             ctx->spmm_variant = static_cast<int>(value);
+        } else if (n == "spmm_slab") {
+            if (value != -1 && value != 0 && value != 32 && value != 64)
+                fail(DSVD_CONFIG, "spmm_slab: -1 (auto), 0 (whole rows), 32 or 64 columns");
+            ctx->spmm_slab = static_cast<int>(value);
+        } else if (n == "spmm_slab_hint") {
+            if (value < 0 || value > 1) fail(DSVD_CONFIG, "spmm_slab_hint must be 0 or 1");
+            ctx->spmm_slab_hint = static_cast<int>(value);
         } else if (n == "hub_threshold") {
             ctx->hub_threshold = value;
         } else if (n == "eig_method") {
@@ -1505,7 +1512,7 @@ int dsvd_finalize_row_basis(dsvd_ctx* ctx, const dsvd_matrix* a, const double* q
         DSVD_CUDA_CHECK(cudaMemcpyAsync(qh, q, sizeof(double) * n * l, cudaMemcpyHostToDevice, st));
         colmajor_to_rowmajor(qh, n, l, Q, ld, st);
         control_init(ctrl, s_stored, static_cast<int>(l), st);
-        spmm(SpmmArgs{&A, Q, B, ld, l, nullptr, nullptr, nullptr}, st, ctx->spmm_variant, ctx->side,
+        spmm(SpmmArgs{&A, Q, B, ld, l, nullptr, nullptr, nullptr}, st, spmm_var(ctx, ld), ctx->side,
              ctx->fork, ctx->join, partial_for(ctx, A, ld));
         EigSvdOut eo{W, sv, inv_s};
         eig_svd_factors(ctx, B, m, l, ld, eo, ctrl, nullptr, nullptr);
@@ -1585,7 +1592,7 @@ int dsvd_spmm_shift(dsvd_ctx* ctx, int64_t rows, int64_t cols, int64_t nnz, cons
             colmajor_to_rowmajor(qc, rows, l, Qd, ld, st);
             DSVD_CUDA_CHECK(cudaMemcpyAsync(d_alpha, &alpha, sizeof(double), cudaMemcpyHostToDevice, st));
         }
-        spmm(SpmmArgs{&a, X, Yd, ld, l, Qd, Qd ? d_alpha : nullptr, nullptr}, st, ctx->spmm_variant, ctx->side, ctx->fork, ctx->join,
+        spmm(SpmmArgs{&a, X, Yd, ld, l, Qd, Qd ? d_alpha : nullptr, nullptr}, st, spmm_var(ctx, ld), ctx->side, ctx->fork, ctx->join,
              partial_for(ctx, a, ld));
         rowmajor_to_colmajor(Yd, rows, l, ld, xc, st);
         DSVD_CUDA_CHECK(cudaMemcpyAsync(y, xc, sizeof(double) * rows * l, cudaMemcpyDeviceToHost, st));

@@ -54,6 +54,10 @@ struct dsvd_ctx {
     size_t event_next = 0;
     std::vector<dsvd::TimedSpan> spans;
     int spmm_variant = 0;
+    // column-slab SpMM (sparse.cu spmm_slab_kernel): -1 auto by width, 0 off,
+    // 32 / 64 columns per slab; spmm_slab_hint: L2 evict_first on streaming bytes
+    int spmm_slab = -1;
+    int spmm_slab_hint = 1;
     int64_t hub_threshold = 4096;   // rows with >= this many nonzeros take the hub SpMM path
     // rows longer than split_chunk nonzeros are computed as chunk partials summed
     // in a fixed order (deterministic; 0 = whole chains, bit-exact vs reference)
@@ -141,6 +145,21 @@ struct dsvd_ctx {
         DSVD_CUDA_CHECK(cudaEventRecord(spans[id].b, stream));
     }
 };
+
+namespace dsvd {
+// The spmm() variant bits of a launch at row stride ld: the context's explicit
+// spmm_variant, plus the column-slab kernel where it pays.
+inline int spmm_var(const dsvd_ctx* ctx, int64_t ld) {
+    int v = ctx->spmm_variant;
+    if ((v & (4096 | 8192)) != 0) return v;  // explicit choice
+    int w = ctx->spmm_slab;
+    if (w < 0) w = 0;  // auto: whole-row kernels (pending the B200 A/B)
+    if (w == 32) v |= 4096;
+    else if (w == 64) v |= 8192;
+    if (w > 0 && ctx->spmm_slab_hint) v |= 16384;
+    return v;
+}
+}  // namespace dsvd
 
 struct dsvd_matrix {
     dsvd_ctx* ctx = nullptr;

@@ -345,6 +345,151 @@ spmm_row_wide_kernel(const int64_t* __restrict__ off, const int32_t* __restrict_
     if (act2) *reinterpret_cast<double2*>(yr + 256 + 2 * lane) = make_double2(acc[8], acc[9]);
 }
 
+// Column-slab kernel (slab-major over the whole launch). The work item is a
+// (W-column slab, row) pair; the grid walks every row of slab 0, then every
+// row of slab 1, ... so at any moment the SMs gather from ONE W-column slab of
+// X — 8 W bytes per X row — and the slab's hot rows stay in L2 (C4: a 32-column
+// slab of the 10 GB X is 1.07 GB, and its ~500k hottest rows, ~88% of the R-MAT
+// gathers, fit in the 126 MB L2; a whole 2.4 KB row per gather keeps only ~45%).
+// The price is re-reading the (index, value) stream once per slab (12 B per
+// nonzero per slab), which is why it is a per-ld choice.
+// A warp holds R = 128 / W rows (ordered longest first, so neighbours have
+// similar lengths); each group of G = W / 4 lanes owns one row and gathers the
+// row's slab with one 256-bit load per lane and nonzero, U nonzeros ahead of the
+// FMAs. The chains are the reference's CSR-order FMA chains from 0.0, so the
+// result is bitwise that of the whole-row kernels. The split rows' chunks are
+// items of the same launch (first, in list order), written to `partial`.
+// kHint: the (index, value) stream and the output rows are marked L2
+// evict_first, so the streaming bytes do not evict the slab's hot X rows.
+template <int W>
+struct SlabCfg {
+    static constexpr int G = W / 4;   // lanes per row
+    static constexpr int R = 32 / G;  // rows per warp
+};
+constexpr int kSlabWarps = 8;
+
+__device__ __forceinline__ uint64_t evict_first_policy() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+
+template <bool kHint>
+__device__ __forceinline__ int32_t ld_idx(const int32_t* p, uint64_t pol) {
+    if (!kHint) return __ldg(p);
+    int32_t v;
+    asm("ld.global.nc.L1::no_allocate.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+    return v;
+}
+
+template <bool kHint>
+__device__ __forceinline__ double ld_val(const double* p, uint64_t pol) {
+    if (!kHint) return __ldg(p);
+    double v;
+    asm("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+    return v;
+}
+
+template <bool kHint>
+__device__ __forceinline__ void st4(double* p, const double (&a)[4], uint64_t pol) {
+    if (!kHint) {
+        *reinterpret_cast<double2*>(p) = make_double2(a[0], a[1]);
+        *reinterpret_cast<double2*>(p + 2) = make_double2(a[2], a[3]);
+        return;
+    }
+    asm volatile("st.global.L1::no_allocate.L2::cache_hint.v4.f64 [%0], {%1,%2,%3,%4}, %5;" ::"l"(p), "d"(a[0]),
+                 "d"(a[1]), "d"(a[2]), "d"(a[3]), "l"(pol)
+                 : "memory");
+}
+
+template <bool kShift, int W, int U, bool kHint, int MB>
+__global__ void __launch_bounds__(32 * kSlabWarps, MB)
+spmm_slab_kernel(const int64_t* __restrict__ off, const int32_t* __restrict__ idx, const double* __restrict__ val,
+                 const int32_t* __restrict__ order, int64_t nsplit, int64_t nchunks,
+                 const int64_t* __restrict__ chunk_p0, const int64_t* __restrict__ chunk_p1, int64_t rows,
+                 int64_t blocks_per_slab, const double* __restrict__ x, double* __restrict__ y,
+                 double* __restrict__ partial, int64_t ld, const double* __restrict__ q,
+                 const double* __restrict__ alpha_p, const int32_t* __restrict__ gate) {
+    constexpr int G = SlabCfg<W>::G, R = SlabCfg<W>::R;
+    if (gate_closed(gate)) return;
+    __shared__ __align__(16) double2 cv[kSlabWarps][R][G + 1];  // +1: groups on distinct banks
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int g = lane / G, t = lane % G;
+    const int slab = static_cast<int>(blockIdx.x / blocks_per_slab);
+    const int64_t rb = blockIdx.x - static_cast<int64_t>(slab) * blocks_per_slab;
+    const int64_t items = nchunks + (rows - nsplit);
+    const int64_t it = (rb * kSlabWarps + warp) * R + g;
+    const bool valid = it < items;
+    int64_t beg = 0, end = 0;
+    double* out = nullptr;
+    const double* qrow = nullptr;
+    if (valid) {
+        if (it < nchunks) {
+            beg = chunk_p0[it];
+            end = chunk_p1[it];
+            out = partial + it * ld;
+        } else {
+            const int64_t row = order[nsplit + (it - nchunks)];
+            beg = off[row];
+            end = off[row + 1];
+            out = y + row * ld;
+            if (kShift) qrow = q + row * ld;
+        }
+    }
+    const int64_t col = static_cast<int64_t>(slab) * W + 4 * t;
+    const bool act = valid && col < ld;  // ld is a multiple of 4: all four columns exist
+    const double* xc = x + (act ? col : 0);
+    const int len = static_cast<int>(end - beg);  // <= split_chunk (or a whole short row)
+    int maxlen = len;
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) maxlen = max(maxlen, __shfl_xor_sync(kFull, maxlen, o));
+    const uint64_t pol = kHint ? evict_first_policy() : 0;
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    double2* slot = cv[warp][g];
+    for (int p0 = 0; p0 < maxlen; p0 += G) {
+        int c = 0;
+        double v = 0.0;
+        if (p0 + t < len) {
+            c = ld_idx<kHint>(idx + beg + p0 + t, pol);
+            v = ld_val<kHint>(val + beg + p0 + t, pol);
+        }
+        __syncwarp();
+        slot[t] = make_double2(v, __longlong_as_double(static_cast<long long>(c)));
+        __syncwarp();
+        const int cnt = min(G, maxlen - p0);
+        for (int j0 = 0; j0 < cnt; j0 += U) {
+            double xa[U][4], vj[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int j = j0 + u;
+                vj[u] = 0.0;
+                if (j < cnt && p0 + j < len) {
+                    const double2 e = slot[j];
+                    vj[u] = e.x;
+                    if (act) ld256(xc + __double_as_longlong(e.y) * ld, xa[u]);
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                if (j0 + u < cnt && p0 + j0 + u < len) {
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) acc[k] = fma(vj[u], xa[u][k], acc[k]);
+                }
+            }
+        }
+    }
+    if (!act) return;
+    if (kShift && qrow != nullptr) {
+        const double alpha = *alpha_p;
+        if (alpha != 0.0) {  // solver.cpp:94 skips the update when alpha == 0
+#pragma unroll
+            for (int k = 0; k < 4; ++k) acc[k] = fma(-alpha, qrow[col + k], acc[k]);
+        }
+    }
+    if (it < nchunks) st4<false>(out + col, acc, pol);  // read back by the combine: keep in L2
+    else st4<kHint>(out + col, acc, pol);
+}
+
 // y(row_i, :) = sum over the row's chunks, in chunk order, of partial(chunk, :),
 // then the shift epilogue.
 // y(row_i, :) = sum of the row's chunk partials (chunk_slot maps its chunks, in
@@ -1049,6 +1194,72 @@ int key_bits(int64_t maxval) {
 
 size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 
+// y rows of the split rows = their chunk partials summed in chunk order (+ shift)
+void combine_split(const SpmmArgs& s, cudaStream_t stream, double* partial) {
+    const DevCsr& a = *s.a;
+    // rows with many chunks (hub columns of A^T): the 8-warp tree per row
+    if (a.max_row_chunks > 32) {
+        const dim3 cgrid(static_cast<unsigned>(a.nsplit), static_cast<unsigned>(ceil_div(s.ld, 64)));
+        if (s.q != nullptr)
+            split_combine_tree_kernel<true><<<cgrid, 256, 0, stream>>>(partial, a.split_first, a.chunk_slot, a.order,
+                                                                       a.nsplit, s.y, s.ld, s.q, s.alpha, s.gate);
+        else
+            split_combine_tree_kernel<false><<<cgrid, 256, 0, stream>>>(partial, a.split_first, a.chunk_slot,
+                                                                        a.order, a.nsplit, s.y, s.ld, nullptr,
+                                                                        nullptr, s.gate);
+    } else {
+        const int64_t n = a.nsplit * s.ld;
+        if (s.q != nullptr)
+            split_combine_kernel<true><<<static_cast<unsigned>(ceil_div(n, 256)), 256, 0, stream>>>(
+                partial, a.split_first, a.chunk_slot, a.order, a.nsplit, s.y, s.ld, s.q, s.alpha, s.gate);
+        else
+            split_combine_kernel<false><<<static_cast<unsigned>(ceil_div(n, 256)), 256, 0, stream>>>(
+                partial, a.split_first, a.chunk_slot, a.order, a.nsplit, s.y, s.ld, nullptr, nullptr, s.gate);
+    }
+    DSVD_LAUNCH_CHECK();
+}
+
+template <int W, bool kHint, int U, int MB>
+void launch_slab(const SpmmArgs& s, cudaStream_t stream, double* partial) {
+    const DevCsr& a = *s.a;
+    constexpr int RB = kSlabWarps * SlabCfg<W>::R;
+    const int64_t nsplit = partial != nullptr ? a.nsplit : 0;
+    const int64_t nchunks = partial != nullptr ? a.nchunks : 0;
+    const int64_t items = nchunks + (a.rows - nsplit);
+    const int64_t bps = ceil_div(items, RB);
+    const int64_t nslab = ceil_div(s.ld, W);
+    if (bps * nslab >= (int64_t(1) << 31)) fail(DSVD_UNSUPPORTED, "spmm: slab grid too large");
+    const unsigned blocks = static_cast<unsigned>(bps * nslab);
+    if (s.q != nullptr)
+        spmm_slab_kernel<true, W, U, kHint, MB><<<blocks, 32 * kSlabWarps, 0, stream>>>(
+            a.off, a.idx, a.val, a.order, nsplit, nchunks, a.chunk_p0, a.chunk_p1, a.rows, bps, s.x, s.y, partial,
+            s.ld, s.q, s.alpha, s.gate);
+    else
+        spmm_slab_kernel<false, W, U, kHint, MB><<<blocks, 32 * kSlabWarps, 0, stream>>>(
+            a.off, a.idx, a.val, a.order, nsplit, nchunks, a.chunk_p0, a.chunk_p1, a.rows, bps, s.x, s.y, partial,
+            s.ld, nullptr, nullptr, s.gate);
+    DSVD_LAUNCH_CHECK();
+}
+
+template <int W, bool kHint>
+void launch_slab_u(const SpmmArgs& s, cudaStream_t stream, double* partial, int depth) {
+    // depth 0: 2 gathers ahead at 32 warps/SM; 1: 4 ahead at 24 warps; 2: 2 ahead at 40 warps
+    if (depth == 1) launch_slab<W, kHint, 4, 3>(s, stream, partial);
+    else if (depth == 2) launch_slab<W, kHint, 2, 5>(s, stream, partial);
+    else launch_slab<W, kHint, 2, 4>(s, stream, partial);
+}
+
+void spmm_slab(const SpmmArgs& s, cudaStream_t stream, int w, bool hint, int depth, double* partial) {
+    if (s.a->rows == 0) return;
+    if (w == 32) {
+        if (hint) launch_slab_u<32, true>(s, stream, partial, depth);
+        else launch_slab_u<32, false>(s, stream, partial, depth);
+    } else {
+        if (hint) launch_slab_u<64, true>(s, stream, partial, depth);
+        else launch_slab_u<64, false>(s, stream, partial, depth);
+    }
+}
+
 }  // namespace
 
 void spmm(const SpmmArgs& s, cudaStream_t stream, int variant, cudaStream_t side,
@@ -1069,7 +1280,19 @@ void spmm(const SpmmArgs& s, cudaStream_t stream, int variant, cudaStream_t side
     const bool wide_bulk = (variant & 64) == 0 && s.ld > 192 && s.ld <= 320,
                wide_chunk = (variant & 128) == 0 && s.ld > 192 && s.ld <= 320;
     const int ru = (variant & 256) ? 4 : (variant & 512) ? 8 : 2;
+    // bits 4096 / 8192: the column-slab kernel with 32- / 64-column slabs for the
+    // bulk rows AND the split chunks (one launch, slab-major); 16384: its L2
+    // evict_first hints on the streaming bytes
+    const int slab_w = (variant & 4096) ? 32 : (variant & 8192) ? 64 : 0;
+    const bool slab_hint = (variant & 16384) != 0;
+    // bits 32768 / 65536: slab gather depth 4 at 24 warps/SM / depth 2 at 40 warps/SM
+    const int slab_depth = (variant & 32768) ? 1 : (variant & 65536) ? 2 : 0;
     variant &= 15;
+    if (slab_w > 0 && !skip_bulk && !skip_hub && (a.nsplit == 0 || partial != nullptr)) {
+        spmm_slab(s, stream, slab_w, slab_hint, slab_depth, partial);
+        if (a.nsplit > 0 && partial != nullptr) combine_split(s, stream, partial);
+        return;
+    }
     const bool split = a.nsplit > 0 && partial != nullptr && side != nullptr;
     const int64_t hub = (!split && side != nullptr && a.d_hub_rows != nullptr) ? a.hub_rows : 0;
     if (split) {
@@ -1202,26 +1425,7 @@ void spmm(const SpmmArgs& s, cudaStream_t stream, int variant, cudaStream_t side
     if (split) {
         DSVD_CUDA_CHECK(cudaEventRecord(join, side));
         DSVD_CUDA_CHECK(cudaStreamWaitEvent(stream, join, 0));
-        // rows with many chunks (hub columns of A^T): the 8-warp tree per row
-        if (a.max_row_chunks > 32) {
-            const dim3 cgrid(static_cast<unsigned>(a.nsplit), static_cast<unsigned>(ceil_div(s.ld, 64)));
-            if (s.q != nullptr)
-                split_combine_tree_kernel<true><<<cgrid, 256, 0, stream>>>(partial, a.split_first, a.chunk_slot, a.order,
-                                                                           a.nsplit, s.y, s.ld, s.q, s.alpha, s.gate);
-            else
-                split_combine_tree_kernel<false><<<cgrid, 256, 0, stream>>>(partial, a.split_first, a.chunk_slot,
-                                                                            a.order, a.nsplit, s.y, s.ld, nullptr,
-                                                                            nullptr, s.gate);
-        } else {
-            const int64_t n = a.nsplit * s.ld;
-            if (s.q != nullptr)
-                split_combine_kernel<true><<<static_cast<unsigned>(ceil_div(n, 256)), 256, 0, stream>>>(
-                    partial, a.split_first, a.chunk_slot, a.order, a.nsplit, s.y, s.ld, s.q, s.alpha, s.gate);
-            else
-                split_combine_kernel<false><<<static_cast<unsigned>(ceil_div(n, 256)), 256, 0, stream>>>(
-                    partial, a.split_first, a.chunk_slot, a.order, a.nsplit, s.y, s.ld, nullptr, nullptr, s.gate);
-        }
-        DSVD_LAUNCH_CHECK();
+        combine_split(s, stream, partial);
         return;
     }
     if (hub > 0) {

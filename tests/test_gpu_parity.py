@@ -112,8 +112,13 @@ def test_spmm_bitwise_widths(dev, oracle, c1, l):
 
 
 # spmm_variant bits: 64/128 force the 64-column slab kernel for the bulk rows /
-# split chunks, 256/512 deepen the whole-row kernel's gather lookahead
-@pytest.mark.parametrize("variant", [64, 128, 192, 256, 512])
+# split chunks, 256/512 deepen the whole-row kernel's gather lookahead;
+# 4096/8192 the slab-major column-slab kernel (32/64 columns) with 16384 its L2
+# hints and 32768/65536 its gather depth
+SLAB_VARIANTS = [4096, 8192, 4096 | 16384, 8192 | 16384 | 32768, 4096 | 65536, 4096 | 16384 | 32768]
+
+
+@pytest.mark.parametrize("variant", [64, 128, 192, 256, 512] + SLAB_VARIANTS)
 @pytest.mark.parametrize("l", [2, 75, 150])
 def test_spmm_kernel_variants_bitwise(oracle, variant, l):
     dv = d.Device(0)
@@ -131,6 +136,44 @@ def test_spmm_kernel_variants_bitwise(oracle, variant, l):
         t_ref = oracle.add_scaled(y_ref, -0.25, q)
         assert_bitwise(d.spmm_shift(to_dev(m), x, 0.25, q, device=dv)[short], t_ref[short])
     dv.close()
+
+
+@pytest.mark.parametrize("variant", SLAB_VARIANTS)
+@pytest.mark.parametrize("l", [2, 75, 150, 300])
+def test_spmm_slab_kernel_equals_the_default_split_mode(variant, l):
+    """The slab kernel runs the split rows' chunks in the same launch: every row,
+    split or not, must equal the default kernels' output bitwise (same chains,
+    same chunk partials, same combine), with and without the fused shift."""
+    a = d.powerlaw(7000, 2600, 3.5, 1.0, 1.1, 23)
+    ca = Csr(a.rows, a.cols, a.offsets, a.col_indices, a.values)
+    at = transpose_np(ca)
+    assert np.diff(at.offsets).max() > 512  # split rows present
+    base, dv = d.Device(0), d.Device(0)
+    dv.set_option("spmm_variant", variant)
+    rng = np.random.default_rng(l)
+    for m, x in ((ca, rng.standard_normal((ca.cols, l))), (at, rng.standard_normal((ca.rows, l)))):
+        x = np.asfortranarray(x)
+        q = np.asfortranarray(rng.standard_normal((m.rows, l)))
+        assert_bitwise(d.spmm(to_dev(m), x, device=dv), d.spmm(to_dev(m), x, device=base))
+        assert_bitwise(d.spmm_shift(to_dev(m), x, 0.3, q, device=dv), d.spmm_shift(to_dev(m), x, 0.3, q, device=base))
+    dv.close()
+    base.close()
+
+
+@pytest.mark.parametrize("variant", [4096 | 16384, 8192])
+def test_solve_with_slab_kernel_is_bitwise_the_default_solve(variant):
+    a = d.powerlaw(9000, 4000, 3.5, 1.0, 1.1, 5)
+    cfg = d.SolverConfig(k=20, s=10, tol=1e-2, seed=4)
+    base, dv = d.Device(0), d.Device(0)
+    dv.set_option("spmm_variant", variant)
+    r0 = d.solve(a, cfg, device=base)
+    r1 = d.solve(a, cfg, device=dv)
+    assert r0.trace.iterations == r1.trace.iterations
+    assert_bitwise(r1.svd.s, r0.svd.s)
+    assert_bitwise(r1.svd.u, r0.svd.u)
+    assert_bitwise(r1.svd.v, r0.svd.v)
+    dv.close()
+    base.close()
 
 
 def test_spmm_transpose_pass_bitwise(dev, oracle, c1):

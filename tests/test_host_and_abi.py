@@ -170,3 +170,15 @@ def test_shard_bounds_cover_and_balance(world):
     assert max(per) - min(per) <= int(np.diff(a.offsets).max()) + 1
     for s in shards:
         s.validate()
+
+
+def test_loopback_group_lifecycle_on_the_host():
+    """The in-process rank group is host state only: create / destroy and the
+    argument checks need no GPU."""
+    g = d.LoopbackGroup(3)
+    assert g.nranks == 3
+    g.close()
+    for bad in (0, 9):
+        with pytest.raises(d.ConfigError):
+            d.LoopbackGroup(bad)
+
