@@ -106,11 +106,6 @@ void nccl_poll(dsvd_ctx* ctx, const char* what) {
         fail(DSVD_NCCL, std::string(what) + ": asynchronous NCCL error: " + nccl().GetErrorString(async));
 }
 
-struct NvtxRange {
-    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
-    ~NvtxRange() { nvtxRangePop(); }
-};
-
 // ---- loopback transport ------------------------------------------------------
 
 struct RankPtrs {

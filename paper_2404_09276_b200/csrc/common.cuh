@@ -2,6 +2,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <cstdint>
@@ -37,6 +38,14 @@ inline void cuda_check(cudaError_t e, const char* what, const char* file, int li
 #define DSVD_LAUNCH_CHECK() ::dsvd::cuda_check(cudaGetLastError(), "kernel launch", __FILE__, __LINE__)
 
 constexpr int kNumSMs = 148;
+
+// Host-side NVTX range (nsys / ncu --nvtx timelines) around a phase of the solve.
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 // Row stride of every tall-skinny device block (Omega, Q, Y, T): l rounded up
 // to 4 doubles so each row starts on a 32-byte sector boundary and lanes can

@@ -70,86 +70,55 @@ namespace {
 
 
 // Chunk list of the rows longer than m.split_chunk (the prefix m.hub_rows of
-// m.order): each split row is cut into near-equal CSR ranges of at most
-// split_chunk nonzeros. With panel_rows > 0 (rows with sorted indices only,
-// i.e. the transpose) the ranges are also cut where the gathered X row index
-// crosses a multiple of panel_rows, and the chunk list is ordered by panel:
-// chunks that run together then gather from one panel_rows-row slice of X
-// (~40 MB at ld 152, L2-resident) instead of all of it. Each row's chunks are
-// still summed in CSR order (chunk_slot maps them to list positions).
-void build_chunks(dsvd_ctx* ctx, CsrAlloc& al, DevCsr& m, const std::string& tag, int64_t panel_rows) {
-    cudaStream_t st = ctx->stream;
-    const int64_t ns = m.hub_rows, C = m.split_chunk;
+// m.order), planned on the device (sparse.cu chunk_plan_*): each split row is
+// cut into near-equal CSR ranges of at most split_chunk nonzeros. With
+// npanel > 1 (rows with sorted indices only, i.e. the transpose) the ranges are
+// also cut where the gathered X row index crosses a multiple of panel_rows,
+// and the chunk list is ordered by panel: chunks that run together then gather
+// from one panel_rows-row slice of X (~40 MB at ld 152, L2-resident) instead of
+// all of it. Each row's chunks are still summed in CSR order (chunk_slot maps
+// them to list positions).
+struct ChunkPlan {
+    int npanel = 1;
+    int64_t panel_rows = 0;
+    int32_t* row_nch = nullptr;
+    int32_t* first = nullptr;
+    int32_t* total_max = nullptr;  // device {total, max}
+};
+
+void plan_chunks_count(dsvd_ctx* ctx, CsrAlloc& al, DevCsr& m, const std::string& tag, int64_t panel_rows,
+                       int32_t* total_max, ChunkPlan& cp) {
+    cp.npanel = panel_rows > 0 ? static_cast<int>(std::max<int64_t>(1, ceil_div(m.cols, panel_rows))) : 1;
+    cp.panel_rows = cp.npanel > 1 ? panel_rows : 0;
+    cp.row_nch = ctx->tbuf<int32_t>("chunk.row_nch." + tag, m.rows);
+    cp.first = static_cast<int32_t*>(al.get(tag + ".split_first", sizeof(int32_t) * (m.rows + 1)));
+    cp.total_max = total_max;
+    const size_t tb = chunk_plan_scratch_bytes(m.rows, 1);
+    chunk_plan_count(m, cp.npanel, cp.panel_rows, cp.row_nch, cp.first, total_max, ctx->buf("chunk.temp", tb), tb,
+                     ctx->stream);
+    count_launch(3);
+}
+
+void plan_chunks_emit(dsvd_ctx* ctx, CsrAlloc& al, DevCsr& m, const std::string& tag, const ChunkPlan& cp,
+                      int64_t nc, int64_t max_row) {
+    const int64_t ns = m.hub_rows;
     m.nsplit = 0;
     m.nchunks = 0;
     m.hub_rows = 0;  // split mode does not use the hub kernels
     m.chunk_slot = nullptr;
-    if (ns == 0) return;
-    const int npanel = panel_rows > 0 ? static_cast<int>(std::max<int64_t>(1, ceil_div(m.cols, panel_rows))) : 1;
-    const int64_t nb = ns * (npanel + 1);
-    int64_t* dbe = ctx->tbuf<int64_t>("chunk.bounds", nb);
-    panel_bounds(m, ns, npanel, npanel > 1 ? panel_rows : m.cols + 1, dbe, st);
-    count_launch();
-    std::vector<int64_t> be(static_cast<size_t>(nb));
-    DSVD_CUDA_CHECK(cudaMemcpyAsync(be.data(), dbe, sizeof(int64_t) * nb, cudaMemcpyDeviceToHost, st));
-    DSVD_CUDA_CHECK(cudaStreamSynchronize(st));
-    struct Chunk {
-        int64_t p0, p1;
-        int32_t panel;
-    };
-    std::vector<Chunk> chunks;  // CSR order: row by row, panel by panel
-    std::vector<int32_t> first(static_cast<size_t>(ns + 1), 0);
-    auto cut = [&](int64_t b, int64_t e, int32_t panel) {
-        const int64_t len = e - b;
-        if (len <= 0) return;
-        const int64_t nch = (len + C - 1) / C;
-        const int64_t cs = (len + nch - 1) / nch;
-        for (int64_t j = 0; j < nch; ++j) chunks.push_back({b + j * cs, std::min(e, b + (j + 1) * cs), panel});
-    };
-    for (int64_t i = 0; i < ns; ++i) {
-        first[i] = static_cast<int32_t>(chunks.size());
-        const int64_t* bi = be.data() + i * (npanel + 1);
-        // a row of L nonzeros is cut at every gs-th panel boundary, gs chosen so
-        // the pieces stay about split_chunk long (L / C groups of panels); each
-        // piece is listed under the middle panel of its group
-        const int64_t L = bi[npanel] - bi[0];
-        const int64_t groups = std::max<int64_t>(1, std::min<int64_t>(npanel, L / C));
-        const int gs = static_cast<int>((npanel + groups - 1) / groups);
-        for (int p = 0; p < npanel; p += gs) {
-            const int pe = std::min(npanel, p + gs);
-            cut(bi[p], bi[pe], static_cast<int32_t>((p + pe - 1) / 2));
-        }
-    }
-    first[ns] = static_cast<int32_t>(chunks.size());
-    const int64_t nc = static_cast<int64_t>(chunks.size());
-    m.max_row_chunks = 0;
-    for (int64_t i = 0; i < ns; ++i) m.max_row_chunks = std::max<int64_t>(m.max_row_chunks, first[i + 1] - first[i]);
-    // list position of each chunk: stable by panel
-    std::vector<int32_t> slot(static_cast<size_t>(nc));
-    std::vector<int64_t> p0(static_cast<size_t>(nc)), p1(static_cast<size_t>(nc));
-    {
-        std::vector<int64_t> start(static_cast<size_t>(npanel + 1), 0);
-        for (const Chunk& c : chunks) ++start[c.panel + 1];
-        for (int p = 0; p < npanel; ++p) start[p + 1] += start[p];
-        for (int64_t c = 0; c < nc; ++c) {
-            const int64_t pos = start[chunks[c].panel]++;
-            slot[c] = static_cast<int32_t>(pos);
-            p0[pos] = chunks[c].p0;
-            p1[pos] = chunks[c].p1;
-        }
-    }
+    m.max_row_chunks = max_row;
+    if (ns == 0 || nc == 0) return;
     m.chunk_p0 = static_cast<int64_t*>(al.get(tag + ".chunk_p0", sizeof(int64_t) * nc));
     m.chunk_p1 = static_cast<int64_t*>(al.get(tag + ".chunk_p1", sizeof(int64_t) * nc));
-    m.split_first = static_cast<int32_t*>(al.get(tag + ".split_first", sizeof(int32_t) * (ns + 1)));
-    DSVD_CUDA_CHECK(cudaMemcpyAsync(m.chunk_p0, p0.data(), sizeof(int64_t) * nc, cudaMemcpyHostToDevice, st));
-    DSVD_CUDA_CHECK(cudaMemcpyAsync(m.chunk_p1, p1.data(), sizeof(int64_t) * nc, cudaMemcpyHostToDevice, st));
-    DSVD_CUDA_CHECK(cudaMemcpyAsync(m.split_first, first.data(), sizeof(int32_t) * (ns + 1),
-                                    cudaMemcpyHostToDevice, st));
-    if (npanel > 1) {
-        m.chunk_slot = static_cast<int32_t*>(al.get(tag + ".chunk_slot", sizeof(int32_t) * nc));
-        DSVD_CUDA_CHECK(cudaMemcpyAsync(m.chunk_slot, slot.data(), sizeof(int32_t) * nc, cudaMemcpyHostToDevice, st));
-    }
-    DSVD_CUDA_CHECK(cudaStreamSynchronize(st));  // the host vectors die here
+    m.split_first = cp.first;
+    if (cp.npanel > 1) m.chunk_slot = static_cast<int32_t*>(al.get(tag + ".chunk_slot", sizeof(int32_t) * nc));
+    const size_t tb = chunk_plan_scratch_bytes(m.rows, nc);
+    chunk_plan_emit(m, ns, cp.npanel, cp.panel_rows, cp.first, nc, m.chunk_p0, m.chunk_p1, m.chunk_slot,
+                    ctx->tbuf<int64_t>("chunk.tmp0", nc), ctx->tbuf<int64_t>("chunk.tmp1", nc),
+                    ctx->tbuf<int32_t>("chunk.keys", nc), ctx->tbuf<int32_t>("chunk.keys_s", nc),
+                    ctx->tbuf<int32_t>("chunk.ids", nc), ctx->tbuf<int32_t>("chunk.ids_s", nc),
+                    ctx->buf("chunk.temp", tb), tb, ctx->stream);
+    count_launch(cp.npanel > 1 ? 4 : 1);
     m.nsplit = ns;
     m.nchunks = nc;
 }
@@ -162,6 +131,7 @@ void build_chunks(dsvd_ctx* ctx, CsrAlloc& al, DevCsr& m, const std::string& tag
 void build_pair(dsvd_ctx* ctx, CsrAlloc& al, int64_t rows, int64_t cols, int64_t nnz,
                 const int64_t* d_off, const int64_t* d_idx64, const double* d_val, DevCsr& a,
                 DevCsr& at, bool copy_inputs, cudaEvent_t values_ready) {
+    NvtxRange nvtx("dsvd.csc_build");
     cudaStream_t st = ctx->stream;
     if (rows < 0 || cols < 0 || nnz < 0) fail(DSVD_SHAPE, "sparse matrix with negative dimension");
     if (rows > 0x7fffffffLL || cols > 0x7fffffffLL)
@@ -185,17 +155,21 @@ void build_pair(dsvd_ctx* ctx, CsrAlloc& al, int64_t rows, int64_t cols, int64_t
     }
     a.idx = static_cast<int32_t*>(al.get("a.idx", sizeof(int32_t) * nnz));
     a.order = static_cast<int32_t*>(al.get("a.order", sizeof(int32_t) * (rows > 0 ? rows : 1)));
-    int32_t* bad = ctx->tbuf<int32_t>("bad", 2);
-    DSVD_CUDA_CHECK(cudaMemsetAsync(bad, 0, sizeof(int32_t) * 2, st));
-    check_offsets(a.off, rows, nnz, bad, st);
+    // device scalars read back by the host: {offsets bad, index bad} right away,
+    // {hub rows of A, of A^T, chunk total / max of A, of A^T} in one read at the end
+    int32_t* sc = static_cast<int32_t*>(al.get("plan_scalars", sizeof(int32_t) * 8));
+    DSVD_CUDA_CHECK(cudaMemsetAsync(sc, 0, sizeof(int32_t) * 8, st));
+    check_offsets(a.off, rows, nnz, sc, st);
     count_launch();
-    narrow_indices(d_idx64, a.idx, nnz, cols, bad + 1, st);
+    narrow_indices(d_idx64, a.idx, nnz, cols, sc + 1, st);
     count_launch(nnz > 0);
-    int32_t hbad[2] = {0, 0};
-    DSVD_CUDA_CHECK(cudaMemcpyAsync(hbad, bad, sizeof(hbad), cudaMemcpyDeviceToHost, st));
-    DSVD_CUDA_CHECK(cudaStreamSynchronize(st));
-    if (hbad[0]) fail(DSVD_SHAPE, "offsets must be non-decreasing and span [0, nnz]");
-    if (hbad[1]) fail(DSVD_SHAPE, "column index out of range");
+    {  // malformed offsets would send the transpose out of bounds: check before it runs
+        int32_t hb[2];
+        DSVD_CUDA_CHECK(cudaMemcpyAsync(hb, sc, sizeof(hb), cudaMemcpyDeviceToHost, st));
+        DSVD_CUDA_CHECK(cudaStreamSynchronize(st));
+        if (hb[0]) fail(DSVD_SHAPE, "offsets must be non-decreasing and span [0, nnz]");
+        if (hb[1]) fail(DSVD_SHAPE, "column index out of range");
+    }
 
     at.rows = cols;
     at.cols = rows;
@@ -209,7 +183,6 @@ void build_pair(dsvd_ctx* ctx, CsrAlloc& al, int64_t rows, int64_t cols, int64_t
     void* scratch = ctx->buf("csc.scratch", scratch_bytes);
     build_transpose(a, at, scratch, scratch_bytes, st, values_ready);
     count_launch(nnz > 0 ? 8 : 1);  // 4 own kernels + CUB radix sort passes (estimate)
-    int32_t* hubs = static_cast<int32_t*>(al.get("hub_counts", sizeof(int32_t) * 2));
     // split mode: the "hub" prefix of the row order is the set of rows longer
     // than split_chunk, which are cut into chunks below
     const int64_t C = ctx->split_chunk;
@@ -219,24 +192,27 @@ void build_pair(dsvd_ctx* ctx, CsrAlloc& al, int64_t rows, int64_t cols, int64_t
     at.hub_threshold = Ct > 0 ? Ct + 1 : ctx->hub_threshold;
     a.split_chunk = C;
     at.split_chunk = Ct;
-    a.d_hub_rows = hubs;
-    at.d_hub_rows = hubs + 1;
+    a.d_hub_rows = sc + 2;
+    at.d_hub_rows = sc + 3;
     build_row_order(a, scratch, scratch_bytes, st);
     count_launch(rows > 0 ? 4 : 0);
     build_row_order(at, scratch, scratch_bytes, st);
     count_launch(cols > 0 ? 4 : 0);
-    int32_t hh[2] = {0, 0};
-    if (rows > 0 && cols > 0) {
-        DSVD_CUDA_CHECK(cudaMemcpyAsync(hh, hubs, sizeof(hh), cudaMemcpyDeviceToHost, st));
-        DSVD_CUDA_CHECK(cudaStreamSynchronize(st));
-    }
-    a.hub_rows = rows > 0 ? hh[0] : 0;
-    at.hub_rows = cols > 0 ? hh[1] : 0;
+    ChunkPlan cpa, cpt;
     if (C > 0) {
         // no panels for A: pass 1 gathers (Zipf columns) are L2-friendly already
         // and the caller's rows need not be sorted
-        build_chunks(ctx, al, a, "a", 0);
-        build_chunks(ctx, al, at, "at", ctx->split_panel_rows);
+        plan_chunks_count(ctx, al, a, "a", 0, sc + 4, cpa);
+        plan_chunks_count(ctx, al, at, "at", ctx->split_panel_rows, sc + 6, cpt);
+    }
+    int32_t h[8];
+    DSVD_CUDA_CHECK(cudaMemcpyAsync(h, sc, sizeof(h), cudaMemcpyDeviceToHost, st));
+    DSVD_CUDA_CHECK(cudaStreamSynchronize(st));
+    a.hub_rows = rows > 0 ? h[2] : 0;
+    at.hub_rows = cols > 0 ? h[3] : 0;
+    if (C > 0) {
+        plan_chunks_emit(ctx, al, a, "a", cpa, h[4], h[5]);
+        plan_chunks_emit(ctx, al, at, "at", cpt, h[6], h[7]);
     }
 }
 
@@ -428,6 +404,7 @@ struct SolveIO {
 void solve_tall(dsvd_ctx* ctx, const DevCsr& A, const DevCsr& AT, const dsvd_config& cfg,
                 SolveIO& io, dsvd_observer_fn observer, void* user, int64_t row_offset = 0,
                 int64_t global_m = -1) {
+    NvtxRange nvtx("dsvd.solve_tall");
     cudaStream_t st = ctx->stream;
     const int64_t m = A.rows, n = A.cols;
     const bool sharded = ctx->comm != nullptr;
@@ -581,6 +558,7 @@ void solve_tall(dsvd_ctx* ctx, const DevCsr& A, const DevCsr& AT, const dsvd_con
             solve_rescale(ctx, Tb[0], n, l, ld, W, l, inv_s, l, Qobs[0], ld, 0, nullptr);
         }
         for (int64_t j = 1; j <= max_iters; ++j) {
+            NvtxRange nvtx_it("dsvd.iteration");
             if (dash && !observer && j > kLookahead) {
                 const int slot = static_cast<int>((j - kLookahead) % (kLookahead + 1));
                 DSVD_CUDA_CHECK(cudaEventSynchronize(flag_ev[slot]));
@@ -683,6 +661,7 @@ void solve_tall(dsvd_ctx* ctx, const DevCsr& A, const DevCsr& AT, const dsvd_con
 
         int cur = 0;
         for (int64_t j = 1; j <= max_iters; ++j) {
+            NvtxRange nvtx_it("dsvd.iteration");
             if (dash && !observer && j > kLookahead) {
                 const int slot = static_cast<int>((j - kLookahead) % (kLookahead + 1));
                 DSVD_CUDA_CHECK(cudaEventSynchronize(flag_ev[slot]));
@@ -748,6 +727,7 @@ void solve_tall(dsvd_ctx* ctx, const DevCsr& A, const DevCsr& AT, const dsvd_con
     }
 
     // finalize_row_basis: B = A Q, eigSVD(B), U = B V' diag(1/s) [:, :k], V = Q V'[:, :k]
+    NvtxRange nvtx_fin("dsvd.finalize");
     control_init(ctrl, s_stored, static_cast<int>(l), st);
     count_launch();
     sp = ctx->span_begin(K_SPMM1);
@@ -828,6 +808,7 @@ void end_profile(dsvd_ctx* ctx, int64_t launches_before) {
 // Finalize: f = eigSVD(A^T q), U = q f.v[:, :k], V = f.u[:, :k], s = f.s[:k].
 void solve_basic(dsvd_ctx* ctx, const DevCsr& A, const DevCsr& AT, const dsvd_config& cfg, SolveIO& io,
                  dsvd_observer_fn observer, void* user) {
+    NvtxRange nvtx("dsvd.solve_basic");
     cudaStream_t st = ctx->stream;
     const int64_t m = A.rows, n = A.cols;
     const int64_t k = cfg.k;

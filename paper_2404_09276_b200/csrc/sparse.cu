@@ -15,6 +15,8 @@
 #include <cudaTypedefs.h>
 
 #include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_reduce.cuh>
+#include <cub/device/device_scan.cuh>
 #include <string>
 
 #include "sparse.cuh"
@@ -605,6 +607,93 @@ __global__ void panel_bounds_kernel(const int32_t* __restrict__ order, const int
         else hi = mid;
     }
     bounds[t] = lo;
+}
+
+// ---- split-row chunk planning on the device (build_chunks) ------------------
+// Split row r (order[r], r < *nsplit) of length L is cut into groups of gs
+// consecutive X-row panels (gs = ceil(npanel / max(1, min(npanel, L / C)))), and
+// each group's CSR range into ceil(len / C) near-equal chunks; a chunk is listed
+// under the middle panel of its group. npanel == 1: one group, the whole row.
+
+// first position in [lo, hi) of row data with idx >= key (indices ascending)
+__device__ __forceinline__ int64_t lower_pos(const int32_t* __restrict__ idx, int64_t lo, int64_t hi, int64_t key) {
+    while (lo < hi) {
+        const int64_t mid = lo + (hi - lo) / 2;
+        if (idx[mid] < key) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
+}
+
+template <bool kEmit>
+__device__ __forceinline__ int64_t plan_row(const int64_t* __restrict__ off, const int32_t* __restrict__ idx,
+                                            int64_t row, int npanel, int64_t panel_rows, int64_t C, int64_t out0,
+                                            int64_t* __restrict__ p0, int64_t* __restrict__ p1,
+                                            int32_t* __restrict__ panel) {
+    const int64_t beg = off[row], end = off[row + 1];
+    const int64_t L = end - beg;
+    const int64_t groups = max(int64_t(1), min(static_cast<int64_t>(npanel), L / C));
+    const int gs = static_cast<int>((npanel + groups - 1) / groups);
+    int64_t nch = 0;
+    int64_t b = beg;
+    for (int p = 0; p < npanel; p += gs) {
+        const int pe = min(npanel, p + gs);
+        const int64_t e = pe == npanel ? end : lower_pos(idx, b, end, static_cast<int64_t>(pe) * panel_rows);
+        const int64_t len = e - b;
+        if (len > 0) {
+            const int64_t n = (len + C - 1) / C, cs = (len + n - 1) / n;
+            if (kEmit) {
+                for (int64_t j = 0; j < n; ++j) {
+                    p0[out0 + nch + j] = b + j * cs;
+                    p1[out0 + nch + j] = min(e, b + (j + 1) * cs);
+                    panel[out0 + nch + j] = (p + pe - 1) / 2;
+                }
+            }
+            nch += n;
+        }
+        b = e;
+    }
+    return nch;
+}
+
+// row_nch[r] = chunks of split row r; 0 for the other rows
+__global__ void chunk_count_kernel(const int32_t* __restrict__ order, const int64_t* __restrict__ off,
+                                   const int32_t* __restrict__ idx, int64_t rows, const int32_t* __restrict__ nsplit,
+                                   int npanel, int64_t panel_rows, int64_t C, int32_t* __restrict__ row_nch) {
+    const int64_t ns = *nsplit;
+    for (int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; r < rows;
+         r += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        row_nch[r] = r < ns ? static_cast<int32_t>(plan_row<false>(off, idx, order[r], npanel, panel_rows, C, 0,
+                                                                   nullptr, nullptr, nullptr))
+                            : 0;
+}
+
+__global__ void chunk_emit_kernel(const int32_t* __restrict__ order, const int64_t* __restrict__ off,
+                                  const int32_t* __restrict__ idx, int64_t ns, int npanel, int64_t panel_rows,
+                                  int64_t C, const int32_t* __restrict__ first, int64_t* __restrict__ p0,
+                                  int64_t* __restrict__ p1, int32_t* __restrict__ panel) {
+    for (int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; r < ns;
+         r += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        plan_row<true>(off, idx, order[r], npanel, panel_rows, C, first[r], p0, p1, panel);
+}
+
+// list position `pos` holds chunk ids[pos]: slot[id] = pos, p0/p1 in list order
+__global__ void chunk_place_kernel(const int32_t* __restrict__ ids, int64_t nc, const int64_t* __restrict__ p0,
+                                   const int64_t* __restrict__ p1, int32_t* __restrict__ slot,
+                                   int64_t* __restrict__ q0, int64_t* __restrict__ q1) {
+    for (int64_t pos = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; pos < nc;
+         pos += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int32_t id = ids[pos];
+        slot[id] = static_cast<int32_t>(pos);
+        q0[pos] = p0[id];
+        q1[pos] = p1[id];
+    }
+}
+
+__global__ void iota32_kernel(int32_t* __restrict__ v, int64_t n) {
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        v[i] = static_cast<int32_t>(i);
 }
 
 __global__ void prefix_bounds_kernel(const int32_t* __restrict__ order, const int64_t* __restrict__ off,
@@ -1440,6 +1529,54 @@ void panel_bounds(const DevCsr& m, int64_t nrows, int npanel, int64_t panel_rows
     if (n == 0) return;
     panel_bounds_kernel<<<static_cast<unsigned>(ceil_div(n, 256)), 256, 0, stream>>>(m.order, m.off, m.idx, nrows,
                                                                                    npanel, panel_rows, bounds);
+    DSVD_LAUNCH_CHECK();
+}
+
+size_t chunk_plan_scratch_bytes(int64_t rows, int64_t max_chunks) {
+    size_t a = 0, b = 0, c = 0;
+    const int nr = static_cast<int>(rows > 0 ? rows + 1 : 1), nc = static_cast<int>(max_chunks > 0 ? max_chunks : 1);
+    cub::DeviceScan::InclusiveSum(nullptr, a, static_cast<const int32_t*>(nullptr), static_cast<int32_t*>(nullptr), nr);
+    cub::DeviceReduce::Max(nullptr, b, static_cast<const int32_t*>(nullptr), static_cast<int32_t*>(nullptr), nr);
+    cub::DeviceRadixSort::SortPairs(nullptr, c, static_cast<const int32_t*>(nullptr), static_cast<int32_t*>(nullptr),
+                                    static_cast<const int32_t*>(nullptr), static_cast<int32_t*>(nullptr), nc);
+    return align_up(std::max({a, b, c}));
+}
+
+void chunk_plan_count(const DevCsr& m, int npanel, int64_t panel_rows, int32_t* row_nch, int32_t* first,
+                      int32_t* d_total_max, void* temp, size_t temp_bytes, cudaStream_t stream) {
+    DSVD_CUDA_CHECK(cudaMemsetAsync(first, 0, sizeof(int32_t), stream));
+    DSVD_CUDA_CHECK(cudaMemsetAsync(d_total_max, 0, 2 * sizeof(int32_t), stream));
+    if (m.rows == 0 || m.split_chunk <= 0) return;
+    chunk_count_kernel<<<grid_for(m.rows), 256, 0, stream>>>(m.order, m.off, m.idx, m.rows, m.d_hub_rows, npanel,
+                                                            panel_rows, m.split_chunk, row_nch);
+    DSVD_LAUNCH_CHECK();
+    size_t tb = temp_bytes;
+    DSVD_CUDA_CHECK(cub::DeviceScan::InclusiveSum(temp, tb, row_nch, first + 1, static_cast<int>(m.rows), stream));
+    DSVD_CUDA_CHECK(cudaMemcpyAsync(d_total_max, first + m.rows, sizeof(int32_t), cudaMemcpyDeviceToDevice, stream));
+    tb = temp_bytes;
+    DSVD_CUDA_CHECK(cub::DeviceReduce::Max(temp, tb, row_nch, d_total_max + 1, static_cast<int>(m.rows), stream));
+}
+
+void chunk_plan_emit(const DevCsr& m, int64_t ns, int npanel, int64_t panel_rows, const int32_t* first, int64_t nc,
+                     int64_t* p0, int64_t* p1, int32_t* slot, int64_t* tmp0, int64_t* tmp1, int32_t* keys,
+                     int32_t* keys_sorted, int32_t* ids, int32_t* ids_sorted, void* temp, size_t temp_bytes,
+                     cudaStream_t stream) {
+    if (nc == 0) return;
+    if (npanel <= 1) {  // list order = CSR order, no slot map
+        chunk_emit_kernel<<<grid_for(ns), 256, 0, stream>>>(m.order, m.off, m.idx, ns, npanel, 0, m.split_chunk, first,
+                                                           p0, p1, keys);
+        DSVD_LAUNCH_CHECK();
+        return;
+    }
+    chunk_emit_kernel<<<grid_for(ns), 256, 0, stream>>>(m.order, m.off, m.idx, ns, npanel, panel_rows, m.split_chunk,
+                                                       first, tmp0, tmp1, keys);
+    DSVD_LAUNCH_CHECK();
+    iota32_kernel<<<grid_for(nc), 256, 0, stream>>>(ids, nc);
+    DSVD_LAUNCH_CHECK();
+    size_t tb = temp_bytes;  // stable: chunks of one panel keep their CSR order
+    DSVD_CUDA_CHECK(cub::DeviceRadixSort::SortPairs(temp, tb, keys, keys_sorted, ids, ids_sorted, static_cast<int>(nc),
+                                                    0, key_bits(npanel), stream));
+    chunk_place_kernel<<<grid_for(nc), 256, 0, stream>>>(ids_sorted, nc, tmp0, tmp1, slot, p0, p1);
     DSVD_LAUNCH_CHECK();
 }
 

@@ -63,6 +63,20 @@ void panel_bounds(const DevCsr& m, int64_t nrows, int npanel, int64_t panel_rows
 void spmm(const SpmmArgs& args, cudaStream_t stream, int variant, cudaStream_t side = nullptr,
           cudaEvent_t fork = nullptr, cudaEvent_t join = nullptr, double* partial = nullptr);
 
+// Split-row chunk plan on the device (no host round trip but one scalar read):
+// chunk_plan_count fills row_nch[rows] (chunks per row of m.order, 0 beyond the
+// *m.d_hub_rows split rows), first[rows + 1] (their inclusive prefix, first[0] =
+// 0 — the split_first array) and d_total_max = {total chunks, most chunks of one
+// row}; chunk_plan_emit then writes the nc chunk ranges p0/p1 — in CSR order
+// when npanel <= 1, else stably ordered by panel with slot[id] = list position.
+size_t chunk_plan_scratch_bytes(int64_t rows, int64_t max_chunks);
+void chunk_plan_count(const DevCsr& m, int npanel, int64_t panel_rows, int32_t* row_nch, int32_t* first,
+                      int32_t* d_total_max, void* temp, size_t temp_bytes, cudaStream_t stream);
+void chunk_plan_emit(const DevCsr& m, int64_t ns, int npanel, int64_t panel_rows, const int32_t* first, int64_t nc,
+                     int64_t* p0, int64_t* p1, int32_t* slot, int64_t* tmp0, int64_t* tmp1, int32_t* keys,
+                     int32_t* keys_sorted, int32_t* ids, int32_t* ids_sorted, void* temp, size_t temp_bytes,
+                     cudaStream_t stream);
+
 // Row bounds (offsets) of the first n rows of m.order, for the host-side
 // construction of the split chunk list.
 void prefix_row_bounds(const DevCsr& m, int64_t n, int64_t* d_beg, int64_t* d_end,
