@@ -323,9 +323,10 @@ __device__ __forceinline__ int gm_tri(int a, int j, int nb) { return a * nb - a 
 // 4x4 register-blocked Gram: the 8x8-block grid (padded to NB4*4 blocks) is
 // covered by NB4(NB4+1)/2 tiles of 4x4 blocks on and above the diagonal, one
 // warp each; per 4-row k-step a warp loads 8 fragments (4 on diagonal tiles)
-// for 16 DMMAs. Shared-memory rows are 32*NB4 + 8 doubles (2*S == 16 mod 32
-// banks: the four rows of a fragment load fall in two wavefronts).
-__host__ __device__ constexpr int gm4_stride(int nb4) { return 32 * nb4 + 8; }
+// for 16 DMMAs.
+// Row stride of the staged block: 2 * stride == 8 (mod 32) banks, so the four
+// rows (q = lane & 3) of a half-warp's 64-bit fragment loads hit distinct banks
+__host__ __device__ constexpr int gm4_stride(int nb4) { return 32 * nb4 + 4; }
 
 template <int NB4>
 __global__ void __launch_bounds__(32 * NB4 * (NB4 + 1) / 2, NB4 >= 5 ? 1 : (NB4 == 4 ? 2 : (NB4 == 3 ? 3 : 4)))
@@ -448,7 +449,7 @@ gram_dmma_reduce_kernel(const double* __restrict__ partial, int nblk, int nb, in
 // one or two strip segments. blockIdx.x (the kind) varies fastest so the CTAs
 // of one slab share it in L2. Same partial layout as gram_dmma_kernel (one
 // triangle of 8x8 blocks per slab).
-constexpr int kGwRows = 32, kGwStages = 3, kGwStride = 264;  // 2 * 264 == 16 (mod 32) banks
+constexpr int kGwRows = 32, kGwStages = 3, kGwStride = 260;  // 2 * 260 == 8 (mod 32) banks: conflict-free
 constexpr int kGwMaxKinds = 8;
 
 struct GwKinds {
