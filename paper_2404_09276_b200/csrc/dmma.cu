@@ -372,6 +372,18 @@ gram_dmma_kernel(const double* __restrict__ c, int64_t n, int64_t ld, int nb, in
 #pragma unroll
         for (int v = 0; v < 4; ++v) acc[u][v] = make_double2(0.0, 0.0);
     const bool diag = I == J;
+    // 8x8 blocks this warp must form: inside the nb x nb grid and on or above
+    // the diagonal (diagonal tiles skip their 6 lower blocks, padding tiles the
+    // blocks past nb): DMMA issue slots the other warps of the SM get instead
+    // (NB4 >= 5 only: the smaller instances have no registers to spare for it)
+    unsigned live = NB4 >= 5 ? 0u : 0xffffu;
+    if (NB4 >= 5) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int v = 0; v < 4; ++v)
+                if (4 * I + u < nb && 4 * J + v < nb && (!diag || u <= v)) live |= 1u << (4 * u + v);
+    }
     for (int st = 0; st < nst; ++st) {
         cpa_wait<kGmStages - 2>();
         __syncthreads();
@@ -395,7 +407,8 @@ gram_dmma_kernel(const double* __restrict__ c, int64_t n, int64_t ld, int nb, in
 #pragma unroll
             for (int u = 0; u < 4; ++u)
 #pragma unroll
-                for (int v = 0; v < 4; ++v) dmma884(acc[u][v], fa[u], fb[v]);
+                for (int v = 0; v < 4; ++v)
+                    if (live & (1u << (4 * u + v))) dmma884(acc[u][v], fa[u], fb[v]);
         }
     }
     cpa_wait<0>();
@@ -511,6 +524,12 @@ gram_dmma_wide_kernel(const double* __restrict__ c, int64_t n, int64_t ld, int n
 #pragma unroll
         for (int v = 0; v < 4; ++v) acc[u][v] = make_double2(0.0, 0.0);
     const int ia = 32 * (I - sa0), jb = tri ? 32 * (J - sa0) : 32 * (nA + J - sb0);
+    unsigned live = 0;  // as in gram_dmma_kernel: in-range blocks on or above the diagonal
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v)
+            if (4 * I + u < nb && 4 * J + v < nb && (I != J || u <= v)) live |= 1u << (4 * u + v);
     for (int st = 0; st < nst; ++st) {
         cpa_wait<kGwStages - 2>();
         __syncthreads();
@@ -530,7 +549,8 @@ gram_dmma_wide_kernel(const double* __restrict__ c, int64_t n, int64_t ld, int n
 #pragma unroll
             for (int u = 0; u < 4; ++u)
 #pragma unroll
-                for (int v = 0; v < 4; ++v) dmma884(acc[u][v], fa[u], fb[v]);
+                for (int v = 0; v < 4; ++v)
+                    if (live & (1u << (4 * u + v))) dmma884(acc[u][v], fa[u], fb[v]);
         }
     }
     cpa_wait<0>();

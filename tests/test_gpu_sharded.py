@@ -94,9 +94,14 @@ def plaw():
 
 
 def test_shard_sketch_is_the_global_sketch_bitwise(oracle):
+    """Omega_g = rows [r0, r1) of the global sketch: bitwise the device's full
+    gaussian_matrix rows, and the reference's draws to <= 2 ulp (the device's
+    log/cos are correctly rounded, glibc's are not always; DESIGN 2)."""
     m, l = 997, 37
-    full = oracle.gaussian_matrix(m, l, 2026)
     dv = d.Device(0)
+    full = d.gaussian_matrix(m, l, 2026, device=dv)
+    ref = oracle.gaussian_matrix(m, l, 2026)
+    np.testing.assert_allclose(full, ref, rtol=5e-16, atol=0)
     for r0, r1 in ((0, 400), (400, 997), (123, 124), (996, 997)):
         blk = d.gaussian_rows(r1 - r0, l, 2026, m, r0, device=dv)
         assert np.array_equal(blk.view(np.uint64), np.asfortranarray(full[r0:r1]).view(np.uint64))
