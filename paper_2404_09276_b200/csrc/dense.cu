@@ -16,7 +16,16 @@ constexpr int kTile = 64;
 constexpr int kK = 16;
 
 __global__ void gaussian_kernel(double* __restrict__ out, int64_t rows, int64_t l, int64_t ld,
-                                uint64_t seed, int64_t global_rows, int64_t row_offset) {
+                                uint64_t seed, int64_t global_rows, int64_t row_offset, int w) {
+    if (w > 0) {  // slab-major (sparse.cuh slab_index): writes walk the output contiguously
+        const int64_t total = (ld + w - 1) / w * w * rows;
+        for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
+             e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+            const int64_t jj = e % w, rs = e / w, i = rs % rows, j = (rs / rows) * w + jj;
+            out[e] = j < l ? normal_at(seed, static_cast<uint64_t>(j * global_rows + row_offset + i)) : 0.0;
+        }
+        return;
+    }
     const int64_t total = rows * ld;
     const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
     // 32-bit index arithmetic (no emulated 64-bit division) only when no thread's
@@ -411,11 +420,11 @@ int grid_for(int64_t n) {
 }  // namespace
 
 void gaussian_rowmajor(double* out, int64_t rows, int64_t l, int64_t ld, uint64_t seed,
-                       cudaStream_t stream, int64_t global_rows, int64_t row_offset) {
+                       cudaStream_t stream, int64_t global_rows, int64_t row_offset, int slab_w) {
     if (rows * ld == 0) return;
     if (global_rows < 0) global_rows = rows;
     gaussian_kernel<<<grid_for(rows * ld), 256, 0, stream>>>(out, rows, l, ld, seed, global_rows,
-                                                             row_offset);
+                                                             row_offset, slab_w);
     DSVD_LAUNCH_CHECK();
 }
 

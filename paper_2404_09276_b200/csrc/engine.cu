@@ -423,7 +423,12 @@ void solve_tall(dsvd_ctx* ctx, const DevCsr& A, const DevCsr& AT, const dsvd_con
     const int64_t n_slab = v2 ? ceil_div(n, ctx->nranks) : n;
     const int64_t n_full = v2 ? n_slab * ctx->nranks : n;
     const int64_t slab0 = v2 ? ctx->rank * n_slab : 0;
-    double* Y = ctx->tbuf<double>("Y", m * ld);  // Omega, then A Q, then B
+    // slab-major gathered blocks (column-slab kernel, lw-column slabs): the sketch
+    // and Y = A Q are written slab-major; the pass-1 operand (Q or T, row-major
+    // for the dense kernels) is copied into Xs before each A pass
+    const int lw = slab_layout_width(ctx, ld);
+    double* Y = ctx->tbuf<double>("Y", block_doubles(m, ld, lw));  // Omega, then A Q, then B
+    double* Xs = lw > 0 ? ctx->tbuf<double>("Xs", block_doubles(n, ld, lw)) : nullptr;
     double* T = ctx->tbuf<double>("T", n_full * ld);
     double* Qb[2] = {ctx->tbuf<double>("Q0", n_full * ld), ctx->tbuf<double>("Q1", n_full * ld)};
     double* S = v2 ? ctx->tbuf<double>("slab", n_slab * ld) : nullptr;
@@ -448,10 +453,11 @@ void solve_tall(dsvd_ctx* ctx, const DevCsr& A, const DevCsr& AT, const dsvd_con
     // Omega = gaussian_matrix(m, l, seed) (solver.cpp:83), unless it was already
     // generated beside the host upload (pregenerate_omega)
     int sp = ctx->span_begin(K_OTHER);
-    if (ctx->omega_pending && !sharded && ctx->omega_m == m && ctx->omega_l == l && ctx->omega_seed == cfg.seed) {
+    if (ctx->omega_pending && !sharded && ctx->omega_m == m && ctx->omega_l == l && ctx->omega_seed == cfg.seed &&
+        ctx->omega_slab_w == lw) {
         DSVD_CUDA_CHECK(cudaStreamWaitEvent(st, ctx->omega_ev, 0));
     } else {
-        gaussian_rowmajor(Y, m, l, ld, cfg.seed, st, global_m, row_offset);
+        gaussian_rowmajor(Y, m, l, ld, cfg.seed, st, global_m, row_offset, lw);
         count_launch();
     }
     ctx->omega_pending = false;
@@ -496,6 +502,31 @@ void solve_tall(dsvd_ctx* ctx, const DevCsr& A, const DevCsr& AT, const dsvd_con
     };
     // rows of a reduced block handled by this rank, and their offset in a full block
     const int64_t red_rows = v2 ? n_slab : n;
+    // SpMM launches of the loop: pass 1 (A x -> Y) reads its row-major operand
+    // through the slab-major copy Xs and writes Y slab-major when lw > 0; pass 2
+    // (A^T Y [- alpha q] -> out, row-major) then gathers the slab-major Y
+    auto pass1 = [&](const double* x, double* y_out, bool y_slab_major, const int32_t* g) {
+        SpmmArgs sa{&A, x, y_out, ld, l, nullptr, nullptr, g};
+        if (lw > 0) {
+            to_slab_major(x, n, ld, lw, Xs, st);
+            count_launch();
+            sa.x = Xs;
+            sa.slab = lw;
+            sa.x_slab = true;
+            sa.y_slab = y_slab_major;
+        }
+        spmm(sa, st, spmm_var(ctx, ld), ctx->side, ctx->fork, ctx->join, partial_for(ctx, A, ld));
+        count_launch();
+    };
+    auto pass2 = [&](double* out, const double* q, const double* alpha, const int32_t* g) {
+        SpmmArgs sa{&AT, Y, out, ld, l, q, alpha, g};
+        if (lw > 0) {
+            sa.slab = lw;
+            sa.x_slab = true;
+        }
+        spmm(sa, st, spmm_var(ctx, ld), ctx->side, ctx->fork, ctx->join, partial_for(ctx, AT, ld));
+        count_launch();
+    };
     // eigSVD factors of a reduced block (v2: slab Gram + l x l all-reduce)
     auto factors = [&](const double* c, const LoopStep* lsp, const int32_t* g, cudaStream_t es) {
         eig_svd_factors(ctx, c, red_rows, l, ld, eo, ctrl, lsp, g, v2, v2 ? n : -1, es);
@@ -538,9 +569,7 @@ void solve_tall(dsvd_ctx* ctx, const DevCsr& A, const DevCsr& AT, const dsvd_con
         }
         // T_0 = A^T Omega; eigSVD(T_0) gives Q_0 = T_0 W_0 (solver.cpp:84)
         sp = ctx->span_begin(K_SPMM2);
-        spmm(SpmmArgs{&AT, Y, Tb[0], ld, l, nullptr, nullptr, nullptr}, st, spmm_var(ctx, ld), ctx->side,
-             ctx->fork, ctx->join, partial_for(ctx, AT, ld));
-        count_launch();
+        pass2(Tb[0], nullptr, nullptr, nullptr);
         ctx->span_end(sp);
         if (sharded) {
             double* red = reduce_partial(Tb[0]);
@@ -570,18 +599,13 @@ void solve_tall(dsvd_ctx* ctx, const DevCsr& A, const DevCsr& AT, const dsvd_con
             // (dash: gated on stop_pending, which eigSVD(T_{j-1}) may set while
             // this pass runs — blocks starting after a stop skip their rows)
             sp = ctx->span_begin(K_SPMM1);
-            spmm(SpmmArgs{&A, tprev, Y, ld, l, nullptr, nullptr, dash ? &ctrl->stop_pending : gate}, st,
-                 spmm_var(ctx, ld), ctx->side,
-                 ctx->fork, ctx->join, partial_for(ctx, A, ld));
-            count_launch();
+            pass1(tprev, Y, true, dash ? &ctrl->stop_pending : gate);
             ctx->span_end(sp);
             if (ctx->shift_after) {
                 // P = A^T Z before the wait (both passes overlap the eig), then
                 // P <- fma(-alpha, T_{j-1}, P): the same bits as the fused epilogue
                 sp = ctx->span_begin(K_SPMM2);
-                spmm(SpmmArgs{&AT, Y, P, ld, l, nullptr, nullptr, dash ? &ctrl->stop_pending : gate}, st,
-                     spmm_var(ctx, ld), ctx->side, ctx->fork, ctx->join, partial_for(ctx, AT, ld));
-                count_launch();
+                pass2(P, nullptr, nullptr, dash ? &ctrl->stop_pending : gate);
                 ctx->span_end(sp);
                 DSVD_CUDA_CHECK(cudaStreamWaitEvent(st, ctx->ev_eig, 0));
                 loop_begin(ctrl, st);
@@ -596,9 +620,7 @@ void solve_tall(dsvd_ctx* ctx, const DevCsr& A, const DevCsr& AT, const dsvd_con
                 count_launch();
                 // P = A^T Z - alpha T_{j-1}  (the shift skipped when alpha == 0)
                 sp = ctx->span_begin(K_SPMM2);
-                spmm(SpmmArgs{&AT, Y, P, ld, l, sharded ? nullptr : tprev, sharded ? nullptr : &ctrl->alpha, gate},
-                     st, spmm_var(ctx, ld), ctx->side, ctx->fork, ctx->join, partial_for(ctx, AT, ld));
-                count_launch();
+                pass2(P, sharded ? nullptr : tprev, sharded ? nullptr : &ctrl->alpha, gate);
                 ctx->span_end(sp);
                 double* red = P;
                 if (sharded) {
@@ -650,9 +672,7 @@ void solve_tall(dsvd_ctx* ctx, const DevCsr& A, const DevCsr& AT, const dsvd_con
     } else {
         // Q = eigSVD(A^T Omega).u
         sp = ctx->span_begin(K_SPMM2);
-        spmm(SpmmArgs{&AT, Y, T, ld, l, nullptr, nullptr, nullptr}, st, spmm_var(ctx, ld), ctx->side, ctx->fork,
-             ctx->join, partial_for(ctx, AT, ld));
-        count_launch();
+        pass2(T, nullptr, nullptr, nullptr);
         ctx->span_end(sp);
         const double* red0 = sharded ? reduce_partial(T) : T;
         factors(red0, nullptr, nullptr, nullptr);
@@ -671,16 +691,11 @@ void solve_tall(dsvd_ctx* ctx, const DevCsr& A, const DevCsr& AT, const dsvd_con
             count_launch();
             // Y = A Q
             sp = ctx->span_begin(K_SPMM1);
-            spmm(SpmmArgs{&A, Qb[cur], Y, ld, l, nullptr, nullptr, gate}, st, spmm_var(ctx, ld), ctx->side,
-                 ctx->fork, ctx->join, partial_for(ctx, A, ld));
-            count_launch();
+            pass1(Qb[cur], Y, true, gate);
             ctx->span_end(sp);
             // T = A^T Y - alpha Q  (add_scaled skipped when alpha == 0)
             sp = ctx->span_begin(K_SPMM2);
-            spmm(SpmmArgs{&AT, Y, T, ld, l, sharded ? nullptr : Qb[cur], sharded ? nullptr : &ctrl->alpha,
-                          gate},
-                 st, spmm_var(ctx, ld), ctx->side, ctx->fork, ctx->join, partial_for(ctx, AT, ld));
-            count_launch();
+            pass2(T, sharded ? nullptr : Qb[cur], sharded ? nullptr : &ctrl->alpha, gate);
             ctx->span_end(sp);
             double* red = T;
             if (sharded) {
@@ -731,9 +746,7 @@ void solve_tall(dsvd_ctx* ctx, const DevCsr& A, const DevCsr& AT, const dsvd_con
     control_init(ctrl, s_stored, static_cast<int>(l), st);
     count_launch();
     sp = ctx->span_begin(K_SPMM1);
-    spmm(SpmmArgs{&A, Qf, Y, ld, l, nullptr, nullptr, nullptr}, st, spmm_var(ctx, ld), ctx->side, ctx->fork,
-         ctx->join, partial_for(ctx, A, ld));
-    count_launch();
+    pass1(Qf, Y, false, nullptr);  // B row-major: the Gram and the U product read it
     ctx->span_end(sp);
     eig_svd_factors(ctx, Y, m, l, ld, eo, ctrl, nullptr, nullptr, sharded, global_m);
     hc = read_control(ctx, ctrl);
@@ -972,11 +985,13 @@ void pregenerate_omega(dsvd_ctx* ctx, int64_t rows, int64_t cols, const dsvd_con
     const int64_t l = cfg.k + effective_s(cfg);
     if (l > 512 || m < 1) return;
     const int64_t ld = padded_ld(l);
-    double* Y = ctx->tbuf<double>("Y", m * ld);
+    const int lw = slab_layout_width(ctx, ld);
+    double* Y = ctx->tbuf<double>("Y", block_doubles(m, ld, lw));
     if (!ctx->omega_ev) DSVD_CUDA_CHECK(cudaEventCreateWithFlags(&ctx->omega_ev, cudaEventDisableTiming));
     DSVD_CUDA_CHECK(cudaEventRecord(ctx->fork, ctx->stream));  // earlier work on Y is done
     DSVD_CUDA_CHECK(cudaStreamWaitEvent(ctx->side, ctx->fork, 0));
-    gaussian_rowmajor(Y, m, l, ld, cfg.seed, ctx->side);
+    gaussian_rowmajor(Y, m, l, ld, cfg.seed, ctx->side, -1, 0, lw);
+    ctx->omega_slab_w = lw;
     count_launch();
     DSVD_CUDA_CHECK(cudaEventRecord(ctx->omega_ev, ctx->side));
     ctx->omega_pending = true;
@@ -1147,6 +1162,9 @@ int dsvd_ctx_set_option(dsvd_ctx* ctx, const char* name, int64_t value) {
             if (value != -1 && value != 0 && value != 32 && value != 64)
                 fail(DSVD_CONFIG, "spmm_slab: -1 (auto), 0 (whole rows), 32 or 64 columns");
             ctx->spmm_slab = static_cast<int>(value);
+        } else if (n == "slab_layout") {
+            if (value < 0 || value > 1) fail(DSVD_CONFIG, "slab_layout must be 0 or 1");
+            ctx->slab_layout = static_cast<int>(value);
         } else if (n == "spmm_slab_hint") {
             if (value < 0 || value > 1) fail(DSVD_CONFIG, "spmm_slab_hint must be 0 or 1");
             ctx->spmm_slab_hint = static_cast<int>(value);

@@ -58,6 +58,10 @@ struct dsvd_ctx {
     // 32 / 64 columns per slab; spmm_slab_hint: L2 evict_first on streaming bytes
     int spmm_slab = -1;
     int spmm_slab_hint = 1;
+    // with the column-slab kernel, keep the gathered blocks slab-major (the
+    // sketch and A Q written so, the pass-1 operand converted once per pass)
+    int slab_layout = 1;
+    int omega_slab_w = 0;  // layout of a pregenerated Omega
     int64_t hub_threshold = 4096;   // rows with >= this many nonzeros take the hub SpMM path
     // rows longer than split_chunk nonzeros are computed as chunk partials summed
     // in a fixed order (deterministic; 0 = whole chains, bit-exact vs reference)
@@ -149,6 +153,20 @@ struct dsvd_ctx {
 namespace dsvd {
 // The spmm() variant bits of a launch at row stride ld: the context's explicit
 // spmm_variant, plus the column-slab kernel where it pays.
+inline int spmm_var(const dsvd_ctx* ctx, int64_t ld);
+// Slab width of the slab-major X / Y blocks of a solve at row stride ld (0: all
+// row-major): the column-slab kernel's width when it runs in split mode and
+// the context allows the layout (option "slab_layout").
+inline int slab_layout_width(const dsvd_ctx* ctx, int64_t ld) {
+    if (!ctx->slab_layout || ctx->split_chunk <= 0) return 0;
+    const int v = spmm_var(ctx, ld);
+    if ((v & (16 | 32)) != 0) return 0;
+    return (v & 4096) ? 32 : (v & 8192) ? 64 : 0;
+}
+// Doubles of the Y / sketch buffer (m rows): row-major m x ld or slab-major.
+inline int64_t block_doubles(int64_t rows, int64_t ld, int lw) {
+    return lw > 0 ? std::max(rows * ld, ceil_div(ld, lw) * lw * rows) : rows * ld;
+}
 inline int spmm_var(const dsvd_ctx* ctx, int64_t ld) {
     int v = ctx->spmm_variant;
     if ((v & (4096 | 8192)) != 0) return v;  // explicit choice

@@ -411,7 +411,8 @@ spmm_slab_kernel(const int64_t* __restrict__ off, const int32_t* __restrict__ id
                  const int64_t* __restrict__ chunk_p0, const int64_t* __restrict__ chunk_p1, int64_t rows,
                  int64_t blocks_per_slab, const double* __restrict__ x, double* __restrict__ y,
                  double* __restrict__ partial, int64_t ld, const double* __restrict__ q,
-                 const double* __restrict__ alpha_p, const int32_t* __restrict__ gate) {
+                 const double* __restrict__ alpha_p, const int32_t* __restrict__ gate, int64_t x_rows, bool x_slab,
+                 bool y_slab) {
     constexpr int G = SlabCfg<W>::G, R = SlabCfg<W>::R;
     if (gate_closed(gate)) return;
     __shared__ __align__(16) double2 cv[kSlabWarps][R][G + 1];  // +1: groups on distinct banks
@@ -422,25 +423,27 @@ spmm_slab_kernel(const int64_t* __restrict__ off, const int32_t* __restrict__ id
     const int64_t items = nchunks + (rows - nsplit);
     const int64_t it = (rb * kSlabWarps + warp) * R + g;
     const bool valid = it < items;
+    const int64_t col = static_cast<int64_t>(slab) * W + 4 * t;
     int64_t beg = 0, end = 0;
-    double* out = nullptr;
+    double* out = nullptr;  // this lane's four outputs
     const double* qrow = nullptr;
     if (valid) {
         if (it < nchunks) {
             beg = chunk_p0[it];
             end = chunk_p1[it];
-            out = partial + it * ld;
+            out = partial + it * ld + col;
         } else {
             const int64_t row = order[nsplit + (it - nchunks)];
             beg = off[row];
             end = off[row + 1];
-            out = y + row * ld;
+            out = y_slab ? y + (static_cast<int64_t>(slab) * rows + row) * W + 4 * t : y + row * ld + col;
             if (kShift) qrow = q + row * ld;
         }
     }
-    const int64_t col = static_cast<int64_t>(slab) * W + 4 * t;
     const bool act = valid && col < ld;  // ld is a multiple of 4: all four columns exist
-    const double* xc = x + (act ? col : 0);
+    // X row c's slab: x + c * ld + col (row-major) or x + (slab * x_rows + c) * W + 4t (slab-major)
+    const double* xc = x_slab ? x + static_cast<int64_t>(slab) * x_rows * W + 4 * t : x + (act ? col : 0);
+    const int64_t xstride = x_slab ? W : ld;
     const int len = static_cast<int>(end - beg);  // <= split_chunk (or a whole short row)
     int maxlen = len;
 #pragma unroll
@@ -468,7 +471,7 @@ spmm_slab_kernel(const int64_t* __restrict__ off, const int32_t* __restrict__ id
                 if (j < cnt && p0 + j < len) {
                     const double2 e = slot[j];
                     vj[u] = e.x;
-                    if (act) ld256(xc + __double_as_longlong(e.y) * ld, xa[u]);
+                    if (act) ld256(xc + __double_as_longlong(e.y) * xstride, xa[u]);
                 }
             }
 #pragma unroll
@@ -488,8 +491,8 @@ spmm_slab_kernel(const int64_t* __restrict__ off, const int32_t* __restrict__ id
             for (int k = 0; k < 4; ++k) acc[k] = fma(-alpha, qrow[col + k], acc[k]);
         }
     }
-    if (it < nchunks) st4<false>(out + col, acc, pol);  // read back by the combine: keep in L2
-    else st4<kHint>(out + col, acc, pol);
+    if (it < nchunks) st4<false>(out, acc, pol);  // read back by the combine: keep in L2
+    else st4<kHint>(out, acc, pol);
 }
 
 // y(row_i, :) = sum over the row's chunks, in chunk order, of partial(chunk, :),
@@ -505,7 +508,8 @@ __global__ void __launch_bounds__(256)
 split_combine_tree_kernel(const double* __restrict__ partial, const int32_t* __restrict__ split_first,
                      const int32_t* __restrict__ slot, const int32_t* __restrict__ order, int64_t nsplit,
                      double* __restrict__ y, int64_t ld, const double* __restrict__ q,
-                     const double* __restrict__ alpha_p, const int32_t* __restrict__ gate) {
+                     const double* __restrict__ alpha_p, const int32_t* __restrict__ gate, int y_slab_w = 0,
+                     int64_t y_rows = 0) {
     if (gate_closed(gate)) return;
     __shared__ double2 red[8][32];
     const int64_t i = blockIdx.x;
@@ -553,7 +557,9 @@ split_combine_tree_kernel(const double* __restrict__ partial, const int32_t* __r
             s.y = fma(-alpha, qv.y, s.y);
         }
     }
-    *reinterpret_cast<double2*>(y + row * ld + col) = s;
+    // slab-major output (y_slab_w > 0): col and col + 1 share a slab (both even, w a multiple of 4)
+    double* dst = y_slab_w > 0 ? y + ((col / y_slab_w) * y_rows + row) * y_slab_w + col % y_slab_w : y + row * ld + col;
+    *reinterpret_cast<double2*>(dst) = s;
 }
 
 // Flat variant for rows with few chunks: one thread per output element, the
@@ -562,7 +568,8 @@ template <bool kShift>
 __global__ void split_combine_kernel(const double* __restrict__ partial, const int32_t* __restrict__ split_first,
                                      const int32_t* __restrict__ slot, const int32_t* __restrict__ order,
                                      int64_t nsplit, double* __restrict__ y, int64_t ld, const double* __restrict__ q,
-                                     const double* __restrict__ alpha_p, const int32_t* __restrict__ gate) {
+                                     const double* __restrict__ alpha_p, const int32_t* __restrict__ gate,
+                                     int y_slab_w = 0, int64_t y_rows = 0) {
     if (gate_closed(gate)) return;
     const int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
     if (e >= nsplit * ld) return;
@@ -584,7 +591,7 @@ __global__ void split_combine_kernel(const double* __restrict__ partial, const i
         const double alpha = *alpha_p;
         if (alpha != 0.0) acc = fma(-alpha, q[row * ld + col], acc);
     }
-    y[row * ld + col] = acc;
+    y[y_slab_w > 0 ? ((col / y_slab_w) * y_rows + row) * y_slab_w + col % y_slab_w : row * ld + col] = acc;
 }
 
 __global__ void panel_bounds_kernel(const int32_t* __restrict__ order, const int64_t* __restrict__ off,
@@ -1286,24 +1293,27 @@ size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 // y rows of the split rows = their chunk partials summed in chunk order (+ shift)
 void combine_split(const SpmmArgs& s, cudaStream_t stream, double* partial) {
     const DevCsr& a = *s.a;
+    const int yw = s.y_slab ? s.slab : 0;
     // rows with many chunks (hub columns of A^T): the 8-warp tree per row
     if (a.max_row_chunks > 32) {
         const dim3 cgrid(static_cast<unsigned>(a.nsplit), static_cast<unsigned>(ceil_div(s.ld, 64)));
         if (s.q != nullptr)
             split_combine_tree_kernel<true><<<cgrid, 256, 0, stream>>>(partial, a.split_first, a.chunk_slot, a.order,
-                                                                       a.nsplit, s.y, s.ld, s.q, s.alpha, s.gate);
+                                                                       a.nsplit, s.y, s.ld, s.q, s.alpha, s.gate, yw,
+                                                                       a.rows);
         else
             split_combine_tree_kernel<false><<<cgrid, 256, 0, stream>>>(partial, a.split_first, a.chunk_slot,
                                                                         a.order, a.nsplit, s.y, s.ld, nullptr,
-                                                                        nullptr, s.gate);
+                                                                        nullptr, s.gate, yw, a.rows);
     } else {
         const int64_t n = a.nsplit * s.ld;
         if (s.q != nullptr)
             split_combine_kernel<true><<<static_cast<unsigned>(ceil_div(n, 256)), 256, 0, stream>>>(
-                partial, a.split_first, a.chunk_slot, a.order, a.nsplit, s.y, s.ld, s.q, s.alpha, s.gate);
+                partial, a.split_first, a.chunk_slot, a.order, a.nsplit, s.y, s.ld, s.q, s.alpha, s.gate, yw, a.rows);
         else
             split_combine_kernel<false><<<static_cast<unsigned>(ceil_div(n, 256)), 256, 0, stream>>>(
-                partial, a.split_first, a.chunk_slot, a.order, a.nsplit, s.y, s.ld, nullptr, nullptr, s.gate);
+                partial, a.split_first, a.chunk_slot, a.order, a.nsplit, s.y, s.ld, nullptr, nullptr, s.gate, yw,
+                a.rows);
     }
     DSVD_LAUNCH_CHECK();
 }
@@ -1319,14 +1329,15 @@ void launch_slab(const SpmmArgs& s, cudaStream_t stream, double* partial) {
     const int64_t nslab = ceil_div(s.ld, W);
     if (bps * nslab >= (int64_t(1) << 31)) fail(DSVD_UNSUPPORTED, "spmm: slab grid too large");
     const unsigned blocks = static_cast<unsigned>(bps * nslab);
+    if ((s.x_slab || s.y_slab) && s.slab != W) fail(DSVD_OTHER, "spmm: slab-major block of another slab width");
     if (s.q != nullptr)
         spmm_slab_kernel<true, W, U, kHint, MB><<<blocks, 32 * kSlabWarps, 0, stream>>>(
             a.off, a.idx, a.val, a.order, nsplit, nchunks, a.chunk_p0, a.chunk_p1, a.rows, bps, s.x, s.y, partial,
-            s.ld, s.q, s.alpha, s.gate);
+            s.ld, s.q, s.alpha, s.gate, a.cols, s.x_slab, s.y_slab);
     else
         spmm_slab_kernel<false, W, U, kHint, MB><<<blocks, 32 * kSlabWarps, 0, stream>>>(
             a.off, a.idx, a.val, a.order, nsplit, nchunks, a.chunk_p0, a.chunk_p1, a.rows, bps, s.x, s.y, partial,
-            s.ld, nullptr, nullptr, s.gate);
+            s.ld, nullptr, nullptr, s.gate, a.cols, s.x_slab, s.y_slab);
     DSVD_LAUNCH_CHECK();
 }
 
@@ -1377,7 +1388,10 @@ void spmm(const SpmmArgs& s, cudaStream_t stream, int variant, cudaStream_t side
     // bits 32768 / 65536: slab gather depth 4 at 24 warps/SM / depth 2 at 40 warps/SM
     const int slab_depth = (variant & 32768) ? 1 : (variant & 65536) ? 2 : 0;
     variant &= 15;
-    if (slab_w > 0 && !skip_bulk && !skip_hub && (a.nsplit == 0 || partial != nullptr)) {
+    const bool slab_ok = slab_w > 0 && !skip_bulk && !skip_hub && (a.nsplit == 0 || partial != nullptr);
+    if ((s.x_slab || s.y_slab) && !slab_ok)
+        fail(DSVD_OTHER, "spmm: slab-major blocks need the column-slab kernel (split mode, slab variant bits)");
+    if (slab_ok) {
         spmm_slab(s, stream, slab_w, slab_hint, slab_depth, partial);
         if (a.nsplit > 0 && partial != nullptr) combine_split(s, stream, partial);
         return;
@@ -1532,6 +1546,28 @@ void panel_bounds(const DevCsr& m, int64_t nrows, int npanel, int64_t panel_rows
     DSVD_LAUNCH_CHECK();
 }
 
+// ---- row-major <-> slab-major copies (32-byte units) --------------------------
+template <bool kToSlab>
+__global__ void slab_copy_kernel(const double* __restrict__ src, int64_t rows, int64_t ld, int w,
+                                 double* __restrict__ dst) {
+    // unit e = (slab s, row r, 4-column group t): consecutive threads walk the
+    // slab-major side contiguously, the row-major side in 32-byte pieces
+    const int64_t g = w / 4, nslab = (ld + w - 1) / w, units = nslab * rows * g;
+    for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < units;
+         e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t t = e % g, rs = e / g, r = rs % rows, sl = rs / rows;
+        const int64_t col = sl * w + 4 * t;
+        if (col >= ld) continue;  // past the last column: the slab's padding is never read
+        if (kToSlab) {
+            const double4 v = *reinterpret_cast<const double4*>(src + r * ld + col);
+            *reinterpret_cast<double4*>(dst + 4 * e) = v;
+        } else {
+            const double4 v = *reinterpret_cast<const double4*>(src + 4 * e);
+            *reinterpret_cast<double4*>(dst + r * ld + col) = v;
+        }
+    }
+}
+
 size_t chunk_plan_scratch_bytes(int64_t rows, int64_t max_chunks) {
     size_t a = 0, b = 0, c = 0;
     const int nr = static_cast<int>(rows > 0 ? rows + 1 : 1), nc = static_cast<int>(max_chunks > 0 ? max_chunks : 1);
@@ -1577,6 +1613,18 @@ void chunk_plan_emit(const DevCsr& m, int64_t ns, int npanel, int64_t panel_rows
     DSVD_CUDA_CHECK(cub::DeviceRadixSort::SortPairs(temp, tb, keys, keys_sorted, ids, ids_sorted, static_cast<int>(nc),
                                                     0, key_bits(npanel), stream));
     chunk_place_kernel<<<grid_for(nc), 256, 0, stream>>>(ids_sorted, nc, tmp0, tmp1, slot, p0, p1);
+    DSVD_LAUNCH_CHECK();
+}
+
+void to_slab_major(const double* src, int64_t rows, int64_t ld, int w, double* dst, cudaStream_t stream) {
+    if (rows == 0 || ld == 0) return;
+    slab_copy_kernel<true><<<grid_for(ceil_div(ld, w) * rows * (w / 4)), 256, 0, stream>>>(src, rows, ld, w, dst);
+    DSVD_LAUNCH_CHECK();
+}
+
+void from_slab_major(const double* src, int64_t rows, int64_t ld, int w, double* dst, cudaStream_t stream) {
+    if (rows == 0 || ld == 0) return;
+    slab_copy_kernel<false><<<grid_for(ceil_div(ld, w) * rows * (w / 4)), 256, 0, stream>>>(src, rows, ld, w, dst);
     DSVD_LAUNCH_CHECK();
 }
 

@@ -50,7 +50,23 @@ struct SpmmArgs {
     const double* q;      // shift operand (a.rows x ld) or nullptr
     const double* alpha;  // device scalar: y = fma(-alpha, q, A x) unless alpha == 0
     const int32_t* gate;  // device flag: skip the launch's work when *gate != 0 (or nullptr)
+    // Slab-major layouts (column-slab kernel only, slab width `slab`): element
+    // (i, j) of an r-row block at (j / slab) * r * slab + i * slab + j % slab,
+    // so one slab of X is contiguous (tools/micro/gather_tlb.cu: 256-byte
+    // gathers from a contiguous 1 GB slab run at 16.7 TB/s, from the same
+    // bytes spread over a 10 GB row-major block at 10.7 TB/s).
+    int slab = 0;         // 0: every block row-major with stride ld
+    bool x_slab = false;  // X is slab-major (a.cols rows)
+    bool y_slab = false;  // write Y slab-major (a.rows rows); the shift operand q stays row-major
 };
+
+// Index of element (i, j) of an r-row block in the slab-major layout of width w.
+inline int64_t slab_index(int64_t i, int64_t j, int64_t r, int w) { return (j / w) * r * w + i * w + j % w; }
+// Doubles of an r-row, width-ld block in the slab-major layout of width w.
+inline int64_t slab_block_size(int64_t r, int64_t ld, int w) { return ceil_div(ld, w) * w * r; }
+// Row-major (stride ld) <-> slab-major (width w) copies of an r-row block.
+void to_slab_major(const double* src, int64_t rows, int64_t ld, int w, double* dst, cudaStream_t stream);
+void from_slab_major(const double* src, int64_t rows, int64_t ld, int w, double* dst, cudaStream_t stream);
 
 // Launches the hub-row kernel on `side` (when the matrix has hub rows) and the
 // kernel for all other rows on `stream`; `fork`/`join` order the two streams.

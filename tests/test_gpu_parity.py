@@ -176,6 +176,37 @@ def test_solve_with_slab_kernel_is_bitwise_the_default_solve(variant):
     base.close()
 
 
+@pytest.mark.parametrize("slab", [32, 64])
+@pytest.mark.parametrize("layout", [0, 1])
+@pytest.mark.parametrize("pipeline", [0, 1])
+@pytest.mark.parametrize("alg", ["shifted", "dash"])
+def test_solve_slab_layouts_are_bitwise_the_whole_row_solve(slab, layout, pipeline, alg):
+    """The column-slab kernel with slab-major sketch / A Q blocks (slab_layout 1:
+    Omega and Y written slab-major, the pass-1 operand copied into a slab-major
+    block) or with row-major blocks (slab_layout 0) reproduces the whole-row
+    kernels' solve bitwise, on a width where the slab kernel is the candidate
+    (l = 300) and on l = 150."""
+    a = d.powerlaw(9000, 4000, 3.5, 1.0, 1.1, 6)
+    for k, s_ in ((200, 100), (100, 50)):
+        cfg = (d.SolverConfig(k=k, s=s_, p=3, alg=d.Algorithm.shifted, seed=2) if alg == "shifted"
+               else d.SolverConfig(k=k, s=s_, tol=1e-2, p_max=6, seed=2))
+        base, dv = d.Device(0), d.Device(0)
+        for x in (base, dv):
+            x.set_option("pipeline", pipeline)
+        base.set_option("spmm_slab", 0)
+        dv.set_option("spmm_slab", slab)
+        dv.set_option("slab_layout", layout)
+        r0 = d.solve(a, cfg, device=base)
+        r1 = d.solve(a, cfg, device=dv)
+        assert r0.trace.iterations == r1.trace.iterations
+        assert_bitwise(r1.svd.s, r0.svd.s)
+        assert_bitwise(r1.svd.u, r0.svd.u)
+        assert_bitwise(r1.svd.v, r0.svd.v)
+        assert_bitwise(np.array(r1.trace.alphas), np.array(r0.trace.alphas))
+        dv.close()
+        base.close()
+
+
 def test_spmm_transpose_pass_bitwise(dev, oracle, c1):
     at = oracle.transpose(c1)
     y = np.asfortranarray(np.random.default_rng(3).standard_normal((c1.rows, 75)))

@@ -1,5 +1,5 @@
 """A/B of one context option on a BASELINE config: SpMM passes and a full solve.
-python tools/ab_option.py c2 split_chunk_t 0,256,128"""
+python tools/ab_option.py c2 split_chunk_t 0,256,128 [base_opt=value,...]"""
 import os
 import sys
 
@@ -10,12 +10,15 @@ import paper_2404_09276_b200 as d  # noqa: E402
 cfg = bench.CONFIGS[sys.argv[1]]
 name = sys.argv[2]
 vals = [int(v) for v in sys.argv[3].split(",")]
+base = [kv.split("=") for kv in sys.argv[4].split(",")] if len(sys.argv) > 4 else []
 a = bench.make_matrix(cfg)
 l = cfg["k"] + cfg["s"]
 scfg = bench.solver_config(cfg)
 ref = None
 for v in vals:
     dev = d.Device(0, profiling=True)
+    for bk, bv in base:
+        dev.set_option(bk, int(bv))
     dev.set_option(name, v)
     m = d.DeviceMatrix(a, dev)
     p = [m.bench_spmm(tr, l, 0) for tr in (0, 1)]
