@@ -1165,6 +1165,12 @@ int dsvd_ctx_set_option(dsvd_ctx* ctx, const char* name, int64_t value) {
         } else if (n == "slab_layout") {
             if (value < 0 || value > 1) fail(DSVD_CONFIG, "slab_layout must be 0 or 1");
             ctx->slab_layout = static_cast<int>(value);
+        } else if (n == "spmm_slab_pf") {
+            if (value < 0 || value > 1) fail(DSVD_CONFIG, "spmm_slab_pf must be 0 or 1");
+            ctx->spmm_slab_pf = static_cast<int>(value);
+        } else if (n == "spmm_slab_depth") {
+            if (value < 0 || value > 2) fail(DSVD_CONFIG, "spmm_slab_depth must be 0, 1 or 2");
+            ctx->spmm_slab_depth = static_cast<int>(value);
         } else if (n == "spmm_slab_hint") {
             if (value < 0 || value > 1) fail(DSVD_CONFIG, "spmm_slab_hint must be 0 or 1");
             ctx->spmm_slab_hint = static_cast<int>(value);

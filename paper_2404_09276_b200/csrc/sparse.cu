@@ -404,7 +404,12 @@ __device__ __forceinline__ void st4(double* p, const double (&a)[4], uint64_t po
                  : "memory");
 }
 
-template <bool kShift, int W, int U, bool kHint, int MB>
+// bulk prefetch of [p, p + bytes) into L2 (bytes a multiple of 16)
+__device__ __forceinline__ void prefetch_l2(const void* p, unsigned bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
+template <bool kShift, int W, int U, bool kHint, int MB, bool kPf>
 __global__ void __launch_bounds__(32 * kSlabWarps, MB)
 spmm_slab_kernel(const int64_t* __restrict__ off, const int32_t* __restrict__ idx, const double* __restrict__ val,
                  const int32_t* __restrict__ order, int64_t nsplit, int64_t nchunks,
@@ -415,7 +420,7 @@ spmm_slab_kernel(const int64_t* __restrict__ off, const int32_t* __restrict__ id
                  bool y_slab) {
     constexpr int G = SlabCfg<W>::G, R = SlabCfg<W>::R;
     if (gate_closed(gate)) return;
-    __shared__ __align__(16) double2 cv[kSlabWarps][R][G + 1];  // +1: groups on distinct banks
+    __shared__ __align__(16) double2 cv[kSlabWarps][R][2 * (G + 1)];  // two batches; +1: groups on distinct banks
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int g = lane / G, t = lane % G;
     const int slab = static_cast<int>(blockIdx.x / blocks_per_slab);
@@ -450,36 +455,65 @@ spmm_slab_kernel(const int64_t* __restrict__ off, const int32_t* __restrict__ id
     for (int o = 16; o >= 1; o >>= 1) maxlen = max(maxlen, __shfl_xor_sync(kFull, maxlen, o));
     const uint64_t pol = kHint ? evict_first_policy() : 0;
     double acc[4] = {0.0, 0.0, 0.0, 0.0};
-    double2* slot = cv[warp][g];
-    for (int p0 = 0; p0 < maxlen; p0 += G) {
-        int c = 0;
-        double v = 0.0;
-        if (p0 + t < len) {
-            c = ld_idx<kHint>(idx + beg + p0 + t, pol);
-            v = ld_val<kHint>(val + beg + p0 + t, pol);
+    // Rolling gather pipeline, D = U loads in flight per lane at all times:
+    // nonzero q is consumed (its FMAs, in CSR order) just before the load of
+    // nonzero q + U is issued into the same registers. The (index, value) pairs
+    // sit in a two-batch shared-memory ring per row (batch = G nonzeros, staged
+    // one batch ahead) fed from registers loaded two batches ahead, so neither
+    // the index loads nor the gathers expose their latency at batch boundaries.
+    double2* ring = cv[warp][g];  // [2][G], padded per group
+    const double* xslab = x_slab ? x + static_cast<int64_t>(slab) * x_rows * W : x + static_cast<int64_t>(slab) * W;
+    const unsigned pf_bytes = static_cast<unsigned>(8 * min(static_cast<int64_t>(W), ld - static_cast<int64_t>(slab) * W));
+    int cb = 0;
+    double vb = 0.0;
+    if (t < len) {
+        cb = ld_idx<kHint>(idx + beg + t, pol);
+        vb = ld_val<kHint>(val + beg + t, pol);
+    }
+    ring[t] = make_double2(vb, __longlong_as_double(static_cast<long long>(cb)));  // batch 0
+    cb = 0;
+    vb = 0.0;
+    if (G + t < len) {  // batch 1, staged when batch 0 starts
+        cb = ld_idx<kHint>(idx + beg + G + t, pol);
+        vb = ld_val<kHint>(val + beg + G + t, pol);
+    }
+    __syncwarp();
+    double xa[U][4], va[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {  // the first U gathers
+        va[u] = 0.0;
+        if (u < len && act) {
+            const double2 e = ring[u];
+            va[u] = e.x;
+            ld256(xc + __double_as_longlong(e.y) * xstride, xa[u]);
         }
-        __syncwarp();
-        slot[t] = make_double2(v, __longlong_as_double(static_cast<long long>(c)));
-        __syncwarp();
-        const int cnt = min(G, maxlen - p0);
-        for (int j0 = 0; j0 < cnt; j0 += U) {
-            double xa[U][4], vj[U];
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-                const int j = j0 + u;
-                vj[u] = 0.0;
-                if (j < cnt && p0 + j < len) {
-                    const double2 e = slot[j];
-                    vj[u] = e.x;
-                    if (act) ld256(xc + __double_as_longlong(e.y) * xstride, xa[u]);
-                }
+    }
+    for (int p = 0; p < maxlen; p += U) {
+        if (p % G == 0) {  // entering batch p / G: stage batch p / G + 1, fetch batch p / G + 2
+            const int b = p / G;
+            __syncwarp();
+            ring[((b + 1) & 1) * (G + 1) + t] = make_double2(vb, __longlong_as_double(static_cast<long long>(cb)));
+            __syncwarp();
+            if (kPf && (b + 1) * G + t < len) prefetch_l2(xslab + static_cast<int64_t>(cb) * xstride, pf_bytes);
+            cb = 0;
+            vb = 0.0;
+            if ((b + 2) * G + t < len) {
+                cb = ld_idx<kHint>(idx + beg + (b + 2) * G + t, pol);
+                vb = ld_val<kHint>(val + beg + (b + 2) * G + t, pol);
             }
+        }
 #pragma unroll
-            for (int u = 0; u < U; ++u) {
-                if (j0 + u < cnt && p0 + j0 + u < len) {
+        for (int u = 0; u < U; ++u) {
+            const int q = p + u;
+            if (q < len) {
 #pragma unroll
-                    for (int k = 0; k < 4; ++k) acc[k] = fma(vj[u], xa[u][k], acc[k]);
-                }
+                for (int k = 0; k < 4; ++k) acc[k] = fma(va[u], xa[u][k], acc[k]);
+            }
+            const int qn = q + U;
+            if (qn < len && act) {
+                const double2 e = ring[((qn / G) & 1) * (G + 1) + qn % G];
+                va[u] = e.x;
+                ld256(xc + __double_as_longlong(e.y) * xstride, xa[u]);
             }
         }
     }
@@ -1318,7 +1352,7 @@ void combine_split(const SpmmArgs& s, cudaStream_t stream, double* partial) {
     DSVD_LAUNCH_CHECK();
 }
 
-template <int W, bool kHint, int U, int MB>
+template <int W, bool kHint, int U, int MB, bool kPf>
 void launch_slab(const SpmmArgs& s, cudaStream_t stream, double* partial) {
     const DevCsr& a = *s.a;
     constexpr int RB = kSlabWarps * SlabCfg<W>::R;
@@ -1331,32 +1365,38 @@ void launch_slab(const SpmmArgs& s, cudaStream_t stream, double* partial) {
     const unsigned blocks = static_cast<unsigned>(bps * nslab);
     if ((s.x_slab || s.y_slab) && s.slab != W) fail(DSVD_OTHER, "spmm: slab-major block of another slab width");
     if (s.q != nullptr)
-        spmm_slab_kernel<true, W, U, kHint, MB><<<blocks, 32 * kSlabWarps, 0, stream>>>(
+        spmm_slab_kernel<true, W, U, kHint, MB, kPf><<<blocks, 32 * kSlabWarps, 0, stream>>>(
             a.off, a.idx, a.val, a.order, nsplit, nchunks, a.chunk_p0, a.chunk_p1, a.rows, bps, s.x, s.y, partial,
             s.ld, s.q, s.alpha, s.gate, a.cols, s.x_slab, s.y_slab);
     else
-        spmm_slab_kernel<false, W, U, kHint, MB><<<blocks, 32 * kSlabWarps, 0, stream>>>(
+        spmm_slab_kernel<false, W, U, kHint, MB, kPf><<<blocks, 32 * kSlabWarps, 0, stream>>>(
             a.off, a.idx, a.val, a.order, nsplit, nchunks, a.chunk_p0, a.chunk_p1, a.rows, bps, s.x, s.y, partial,
             s.ld, nullptr, nullptr, s.gate, a.cols, s.x_slab, s.y_slab);
     DSVD_LAUNCH_CHECK();
 }
 
 template <int W, bool kHint>
-void launch_slab_u(const SpmmArgs& s, cudaStream_t stream, double* partial, int depth) {
-    // depth 0: 2 gathers ahead at 32 warps/SM; 1: 4 ahead at 24 warps; 2: 2 ahead at 40 warps
-    if (depth == 1) launch_slab<W, kHint, 4, 3>(s, stream, partial);
-    else if (depth == 2) launch_slab<W, kHint, 2, 5>(s, stream, partial);
-    else launch_slab<W, kHint, 2, 4>(s, stream, partial);
+void launch_slab_u(const SpmmArgs& s, cudaStream_t stream, double* partial, int depth, bool pf) {
+    // gathers in flight per lane / CTAs per SM: depth 0: 4 / 3 (24 warps), 1: 8 / 2, 2: 2 / 4
+    if (pf) {
+        if (depth == 1) launch_slab<W, kHint, 8, 2, true>(s, stream, partial);
+        else if (depth == 2) launch_slab<W, kHint, 2, 4, true>(s, stream, partial);
+        else launch_slab<W, kHint, 4, 3, true>(s, stream, partial);
+        return;
+    }
+    if (depth == 1) launch_slab<W, kHint, 8, 2, false>(s, stream, partial);
+    else if (depth == 2) launch_slab<W, kHint, 2, 4, false>(s, stream, partial);
+    else launch_slab<W, kHint, 4, 3, false>(s, stream, partial);
 }
 
-void spmm_slab(const SpmmArgs& s, cudaStream_t stream, int w, bool hint, int depth, double* partial) {
+void spmm_slab(const SpmmArgs& s, cudaStream_t stream, int w, bool hint, int depth, bool pf, double* partial) {
     if (s.a->rows == 0) return;
     if (w == 32) {
-        if (hint) launch_slab_u<32, true>(s, stream, partial, depth);
-        else launch_slab_u<32, false>(s, stream, partial, depth);
+        if (hint) launch_slab_u<32, true>(s, stream, partial, depth, pf);
+        else launch_slab_u<32, false>(s, stream, partial, depth, pf);
     } else {
-        if (hint) launch_slab_u<64, true>(s, stream, partial, depth);
-        else launch_slab_u<64, false>(s, stream, partial, depth);
+        if (hint) launch_slab_u<64, true>(s, stream, partial, depth, pf);
+        else launch_slab_u<64, false>(s, stream, partial, depth, pf);
     }
 }
 
@@ -1387,12 +1427,14 @@ void spmm(const SpmmArgs& s, cudaStream_t stream, int variant, cudaStream_t side
     const bool slab_hint = (variant & 16384) != 0;
     // bits 32768 / 65536: slab gather depth 4 at 24 warps/SM / depth 2 at 40 warps/SM
     const int slab_depth = (variant & 32768) ? 1 : (variant & 65536) ? 2 : 0;
+    // bit 131072: L2 bulk prefetch of the next batch's X rows (slab kernel)
+    const bool slab_pf = (variant & 131072) != 0;
     variant &= 15;
     const bool slab_ok = slab_w > 0 && !skip_bulk && !skip_hub && (a.nsplit == 0 || partial != nullptr);
     if ((s.x_slab || s.y_slab) && !slab_ok)
         fail(DSVD_OTHER, "spmm: slab-major blocks need the column-slab kernel (split mode, slab variant bits)");
     if (slab_ok) {
-        spmm_slab(s, stream, slab_w, slab_hint, slab_depth, partial);
+        spmm_slab(s, stream, slab_w, slab_hint, slab_depth, slab_pf, partial);
         if (a.nsplit > 0 && partial != nullptr) combine_split(s, stream, partial);
         return;
     }
