@@ -505,8 +505,25 @@ void solve_tall(dsvd_ctx* ctx, const DevCsr& A, const DevCsr& AT, const dsvd_con
     // SpMM launches of the loop: pass 1 (A x -> Y) reads its row-major operand
     // through the slab-major copy Xs and writes Y slab-major when lw > 0; pass 2
     // (A^T Y [- alpha q] -> out, row-major) then gathers the slab-major Y
+    // hot/cold tags for the slab kernel's L2 policies: the hot X rows of pass 1 are
+    // the longest rows of A^T (most referenced columns of A), of pass 2 the
+    // longest rows of A
+    const int32_t* tag_a = nullptr;
+    const int32_t* tag_at = nullptr;
+    if (lw > 0 && ctx->spmm_hot_mb > 0 && A.nnz > 0) {
+        const int64_t k_hot = ctx->spmm_hot_mb * (int64_t(1) << 20) / (8 * lw);
+        uint8_t* hot = ctx->tbuf<uint8_t>("hot.flags", std::max(m, n));
+        int32_t* ta = ctx->tbuf<int32_t>("tag.a", A.nnz);
+        int32_t* tt = ctx->tbuf<int32_t>("tag.at", AT.nnz);
+        tag_hot_indices(A, AT.order, k_hot, hot, ta, st);
+        tag_hot_indices(AT, A.order, k_hot, hot, tt, st);
+        count_launch(4);
+        tag_a = ta;
+        tag_at = tt;
+    }
     auto pass1 = [&](const double* x, double* y_out, bool y_slab_major, const int32_t* g) {
         SpmmArgs sa{&A, x, y_out, ld, l, nullptr, nullptr, g};
+        sa.idx_tag = tag_a;
         if (lw > 0) {
             to_slab_major(x, n, ld, lw, Xs, st);
             count_launch();
@@ -520,6 +537,7 @@ void solve_tall(dsvd_ctx* ctx, const DevCsr& A, const DevCsr& AT, const dsvd_con
     };
     auto pass2 = [&](double* out, const double* q, const double* alpha, const int32_t* g) {
         SpmmArgs sa{&AT, Y, out, ld, l, q, alpha, g};
+        sa.idx_tag = tag_at;
         if (lw > 0) {
             sa.slab = lw;
             sa.x_slab = true;
@@ -1165,9 +1183,9 @@ int dsvd_ctx_set_option(dsvd_ctx* ctx, const char* name, int64_t value) {
         } else if (n == "slab_layout") {
             if (value < 0 || value > 1) fail(DSVD_CONFIG, "slab_layout must be 0 or 1");
             ctx->slab_layout = static_cast<int>(value);
-        } else if (n == "spmm_slab_pf") {
-            if (value < 0 || value > 1) fail(DSVD_CONFIG, "spmm_slab_pf must be 0 or 1");
-            ctx->spmm_slab_pf = static_cast<int>(value);
+        } else if (n == "spmm_hot_mb") {
+            if (value < 0) fail(DSVD_CONFIG, "spmm_hot_mb must be >= 0");
+            ctx->spmm_hot_mb = value;
         } else if (n == "spmm_slab_depth") {
             if (value < 0 || value > 2) fail(DSVD_CONFIG, "spmm_slab_depth must be 0, 1 or 2");
             ctx->spmm_slab_depth = static_cast<int>(value);

@@ -58,7 +58,9 @@ struct dsvd_ctx {
     // 32 / 64 columns per slab; spmm_slab_hint: L2 evict_first on streaming bytes
     int spmm_slab = -1;
     int spmm_slab_hint = 1;
-    int spmm_slab_pf = 1;     // L2 prefetch of the next batch's X rows
+    // column-slab kernel: hot X rows (as many as fit in spmm_hot_mb MB of slab
+    // rows) gathered with L2 evict_last, the rest evict_first; 0 MB = off
+    int64_t spmm_hot_mb = 96;
     int spmm_slab_depth = 0;  // gather depth / occupancy variant (sparse.cu launch_slab_u)
     // with the column-slab kernel, keep the gathered blocks slab-major (the
     // sketch and A Q written so, the pass-1 operand converted once per pass)
@@ -177,7 +179,6 @@ inline int spmm_var(const dsvd_ctx* ctx, int64_t ld) {
     if (w == 32) v |= 4096;
     else if (w == 64) v |= 8192;
     if (w > 0 && ctx->spmm_slab_hint) v |= 16384;
-    if (w > 0 && ctx->spmm_slab_pf) v |= 131072;
     if (w > 0 && ctx->spmm_slab_depth == 1) v |= 32768;
     if (w > 0 && ctx->spmm_slab_depth == 2) v |= 65536;
     return v;

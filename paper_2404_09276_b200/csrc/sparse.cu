@@ -404,12 +404,26 @@ __device__ __forceinline__ void st4(double* p, const double (&a)[4], uint64_t po
                  : "memory");
 }
 
-// bulk prefetch of [p, p + bytes) into L2 (bytes a multiple of 16)
-__device__ __forceinline__ void prefetch_l2(const void* p, unsigned bytes) {
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+__device__ __forceinline__ uint64_t evict_last_policy() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
 }
 
-template <bool kShift, int W, int U, bool kHint, int MB, bool kPf>
+// 256-bit gather with an L2 eviction-priority policy, not allocated in L1
+__device__ __forceinline__ void ld256_pol(const double* p, double (&r)[4], uint64_t pol) {
+    asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f64 {%0,%1,%2,%3}, [%4], %5;"
+        : "=d"(r[0]), "=d"(r[1]), "=d"(r[2]), "=d"(r[3])
+        : "l"(p), "l"(pol));
+}
+
+// kTag: `idx` is the hot/cold-tagged copy of the column indices (sign bit set
+// on the X rows outside the hot set, DevCsr-independent, built per solve by
+// the engine): hot gathers carry L2 evict_last, cold ones evict_first, so the
+// L2 keeps the most-referenced slab rows (an LFU-like policy) instead of LRU's
+// mix (C4: ~84% of the 64-column slab gathers go to the 246k hottest rows, which
+// fit in the L2, but LRU kept only 51-60% hits; profiles/README.md)
+template <bool kShift, int W, int U, bool kHint, int MB, bool kTag>
 __global__ void __launch_bounds__(32 * kSlabWarps, MB)
 spmm_slab_kernel(const int64_t* __restrict__ off, const int32_t* __restrict__ idx, const double* __restrict__ val,
                  const int32_t* __restrict__ order, int64_t nsplit, int64_t nchunks,
@@ -462,8 +476,16 @@ spmm_slab_kernel(const int64_t* __restrict__ off, const int32_t* __restrict__ id
     // one batch ahead) fed from registers loaded two batches ahead, so neither
     // the index loads nor the gathers expose their latency at batch boundaries.
     double2* ring = cv[warp][g];  // [2][G], padded per group
-    const double* xslab = x_slab ? x + static_cast<int64_t>(slab) * x_rows * W : x + static_cast<int64_t>(slab) * W;
-    const unsigned pf_bytes = static_cast<unsigned>(8 * min(static_cast<int64_t>(W), ld - static_cast<int64_t>(slab) * W));
+    const uint64_t pol_hot = kTag ? evict_last_policy() : 0, pol_cold = kTag ? evict_first_policy() : 0;
+    // gather of tagged index e: strip the tag, pick the policy
+    auto gather = [&](long long e, double (&r)[4]) {
+        if (kTag) {
+            const int32_t ci = static_cast<int32_t>(e);
+            ld256_pol(xc + static_cast<int64_t>(ci & 0x7fffffff) * xstride, r, ci < 0 ? pol_cold : pol_hot);
+        } else {
+            ld256(xc + e * xstride, r);
+        }
+    };
     int cb = 0;
     double vb = 0.0;
     if (t < len) {
@@ -485,7 +507,7 @@ spmm_slab_kernel(const int64_t* __restrict__ off, const int32_t* __restrict__ id
         if (u < len && act) {
             const double2 e = ring[u];
             va[u] = e.x;
-            ld256(xc + __double_as_longlong(e.y) * xstride, xa[u]);
+            gather(__double_as_longlong(e.y), xa[u]);
         }
     }
     for (int p = 0; p < maxlen; p += U) {
@@ -494,7 +516,6 @@ spmm_slab_kernel(const int64_t* __restrict__ off, const int32_t* __restrict__ id
             __syncwarp();
             ring[((b + 1) & 1) * (G + 1) + t] = make_double2(vb, __longlong_as_double(static_cast<long long>(cb)));
             __syncwarp();
-            if (kPf && (b + 1) * G + t < len) prefetch_l2(xslab + static_cast<int64_t>(cb) * xstride, pf_bytes);
             cb = 0;
             vb = 0.0;
             if ((b + 2) * G + t < len) {
@@ -513,7 +534,7 @@ spmm_slab_kernel(const int64_t* __restrict__ off, const int32_t* __restrict__ id
             if (qn < len && act) {
                 const double2 e = ring[((qn / G) & 1) * (G + 1) + qn % G];
                 va[u] = e.x;
-                ld256(xc + __double_as_longlong(e.y) * xstride, xa[u]);
+                gather(__double_as_longlong(e.y), xa[u]);
             }
         }
     }
@@ -1352,7 +1373,7 @@ void combine_split(const SpmmArgs& s, cudaStream_t stream, double* partial) {
     DSVD_LAUNCH_CHECK();
 }
 
-template <int W, bool kHint, int U, int MB, bool kPf>
+template <int W, bool kHint, int U, int MB, bool kTag>
 void launch_slab(const SpmmArgs& s, cudaStream_t stream, double* partial) {
     const DevCsr& a = *s.a;
     constexpr int RB = kSlabWarps * SlabCfg<W>::R;
@@ -1364,21 +1385,22 @@ void launch_slab(const SpmmArgs& s, cudaStream_t stream, double* partial) {
     if (bps * nslab >= (int64_t(1) << 31)) fail(DSVD_UNSUPPORTED, "spmm: slab grid too large");
     const unsigned blocks = static_cast<unsigned>(bps * nslab);
     if ((s.x_slab || s.y_slab) && s.slab != W) fail(DSVD_OTHER, "spmm: slab-major block of another slab width");
+    const int32_t* ix = kTag ? s.idx_tag : a.idx;
     if (s.q != nullptr)
-        spmm_slab_kernel<true, W, U, kHint, MB, kPf><<<blocks, 32 * kSlabWarps, 0, stream>>>(
-            a.off, a.idx, a.val, a.order, nsplit, nchunks, a.chunk_p0, a.chunk_p1, a.rows, bps, s.x, s.y, partial,
+        spmm_slab_kernel<true, W, U, kHint, MB, kTag><<<blocks, 32 * kSlabWarps, 0, stream>>>(
+            a.off, ix, a.val, a.order, nsplit, nchunks, a.chunk_p0, a.chunk_p1, a.rows, bps, s.x, s.y, partial,
             s.ld, s.q, s.alpha, s.gate, a.cols, s.x_slab, s.y_slab);
     else
-        spmm_slab_kernel<false, W, U, kHint, MB, kPf><<<blocks, 32 * kSlabWarps, 0, stream>>>(
-            a.off, a.idx, a.val, a.order, nsplit, nchunks, a.chunk_p0, a.chunk_p1, a.rows, bps, s.x, s.y, partial,
+        spmm_slab_kernel<false, W, U, kHint, MB, kTag><<<blocks, 32 * kSlabWarps, 0, stream>>>(
+            a.off, ix, a.val, a.order, nsplit, nchunks, a.chunk_p0, a.chunk_p1, a.rows, bps, s.x, s.y, partial,
             s.ld, nullptr, nullptr, s.gate, a.cols, s.x_slab, s.y_slab);
     DSVD_LAUNCH_CHECK();
 }
 
 template <int W, bool kHint>
-void launch_slab_u(const SpmmArgs& s, cudaStream_t stream, double* partial, int depth, bool pf) {
+void launch_slab_u(const SpmmArgs& s, cudaStream_t stream, double* partial, int depth) {
     // gathers in flight per lane / CTAs per SM: depth 0: 4 / 3 (24 warps), 1: 8 / 2, 2: 2 / 4
-    if (pf) {
+    if (s.idx_tag != nullptr) {
         if (depth == 1) launch_slab<W, kHint, 8, 2, true>(s, stream, partial);
         else if (depth == 2) launch_slab<W, kHint, 2, 4, true>(s, stream, partial);
         else launch_slab<W, kHint, 4, 3, true>(s, stream, partial);
@@ -1389,14 +1411,14 @@ void launch_slab_u(const SpmmArgs& s, cudaStream_t stream, double* partial, int 
     else launch_slab<W, kHint, 4, 3, false>(s, stream, partial);
 }
 
-void spmm_slab(const SpmmArgs& s, cudaStream_t stream, int w, bool hint, int depth, bool pf, double* partial) {
+void spmm_slab(const SpmmArgs& s, cudaStream_t stream, int w, bool hint, int depth, double* partial) {
     if (s.a->rows == 0) return;
     if (w == 32) {
-        if (hint) launch_slab_u<32, true>(s, stream, partial, depth, pf);
-        else launch_slab_u<32, false>(s, stream, partial, depth, pf);
+        if (hint) launch_slab_u<32, true>(s, stream, partial, depth);
+        else launch_slab_u<32, false>(s, stream, partial, depth);
     } else {
-        if (hint) launch_slab_u<64, true>(s, stream, partial, depth, pf);
-        else launch_slab_u<64, false>(s, stream, partial, depth, pf);
+        if (hint) launch_slab_u<64, true>(s, stream, partial, depth);
+        else launch_slab_u<64, false>(s, stream, partial, depth);
     }
 }
 
@@ -1427,14 +1449,13 @@ void spmm(const SpmmArgs& s, cudaStream_t stream, int variant, cudaStream_t side
     const bool slab_hint = (variant & 16384) != 0;
     // bits 32768 / 65536: slab gather depth 4 at 24 warps/SM / depth 2 at 40 warps/SM
     const int slab_depth = (variant & 32768) ? 1 : (variant & 65536) ? 2 : 0;
-    // bit 131072: L2 bulk prefetch of the next batch's X rows (slab kernel)
-    const bool slab_pf = (variant & 131072) != 0;
+
     variant &= 15;
     const bool slab_ok = slab_w > 0 && !skip_bulk && !skip_hub && (a.nsplit == 0 || partial != nullptr);
     if ((s.x_slab || s.y_slab) && !slab_ok)
         fail(DSVD_OTHER, "spmm: slab-major blocks need the column-slab kernel (split mode, slab variant bits)");
     if (slab_ok) {
-        spmm_slab(s, stream, slab_w, slab_hint, slab_depth, slab_pf, partial);
+        spmm_slab(s, stream, slab_w, slab_hint, slab_depth, partial);
         if (a.nsplit > 0 && partial != nullptr) combine_split(s, stream, partial);
         return;
     }
@@ -1656,6 +1677,37 @@ void chunk_plan_emit(const DevCsr& m, int64_t ns, int npanel, int64_t panel_rows
                                                     0, key_bits(npanel), stream));
     chunk_place_kernel<<<grid_for(nc), 256, 0, stream>>>(ids_sorted, nc, tmp0, tmp1, slot, p0, p1);
     DSVD_LAUNCH_CHECK();
+}
+
+// hot[j] = 1 for the k most referenced X rows (the first k entries of the
+// transpose's length order), then idx_tag[p] = idx[p] with the sign bit set
+// when X row idx[p] is not hot.
+__global__ void hot_flags_kernel(const int32_t* __restrict__ order_t, int64_t k, uint8_t* __restrict__ hot) {
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < k;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        hot[order_t[i]] = 1;
+}
+__global__ void tag_indices_kernel(const int32_t* __restrict__ idx, int64_t nnz, const uint8_t* __restrict__ hot,
+                                   int32_t* __restrict__ out) {
+    for (int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; p < nnz;
+         p += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int32_t c = idx[p];
+        out[p] = hot[c] ? c : static_cast<int32_t>(static_cast<uint32_t>(c) | 0x80000000u);
+    }
+}
+
+void tag_hot_indices(const DevCsr& m, const int32_t* order_x, int64_t k, uint8_t* hot, int32_t* idx_tag,
+                     cudaStream_t stream) {
+    DSVD_CUDA_CHECK(cudaMemsetAsync(hot, 0, static_cast<size_t>(m.cols > 0 ? m.cols : 1), stream));
+    k = std::min(k, m.cols);
+    if (k > 0) {
+        hot_flags_kernel<<<grid_for(k), 256, 0, stream>>>(order_x, k, hot);
+        DSVD_LAUNCH_CHECK();
+    }
+    if (m.nnz > 0) {
+        tag_indices_kernel<<<grid_for(m.nnz), 256, 0, stream>>>(m.idx, m.nnz, hot, idx_tag);
+        DSVD_LAUNCH_CHECK();
+    }
 }
 
 void to_slab_major(const double* src, int64_t rows, int64_t ld, int w, double* dst, cudaStream_t stream) {

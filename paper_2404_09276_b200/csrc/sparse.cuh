@@ -58,7 +58,16 @@ struct SpmmArgs {
     int slab = 0;         // 0: every block row-major with stride ld
     bool x_slab = false;  // X is slab-major (a.cols rows)
     bool y_slab = false;  // write Y slab-major (a.rows rows); the shift operand q stays row-major
+    // hot/cold-tagged copy of a.idx (tag_hot_indices) for the column-slab kernel's
+    // L2 eviction priorities, or nullptr
+    const int32_t* idx_tag = nullptr;
 };
+
+// idx_tag = m.idx with the sign bit set on every index outside the hot set, the
+// k X rows listed first in order_x (the most referenced: the row order of the
+// other matrix of the pair). hot is an m.cols-byte scratch.
+void tag_hot_indices(const DevCsr& m, const int32_t* order_x, int64_t k, uint8_t* hot, int32_t* idx_tag,
+                     cudaStream_t stream);
 
 // Index of element (i, j) of an r-row block in the slab-major layout of width w.
 inline int64_t slab_index(int64_t i, int64_t j, int64_t r, int w) { return (j / w) * r * w + i * w + j % w; }
