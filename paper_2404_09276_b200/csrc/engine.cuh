@@ -61,7 +61,7 @@ struct dsvd_ctx {
     // column-slab kernel: hot X rows (as many as fit in spmm_hot_mb MB of slab
     // rows) gathered with L2 evict_last, the rest evict_first; 0 MB = off
     int64_t spmm_hot_mb = 96;
-    int spmm_slab_depth = 0;  // gather depth / occupancy variant (sparse.cu launch_slab_u)
+    int spmm_slab_depth = 2;  // gather depth / occupancy variant (sparse.cu launch_slab_u): 2 in flight, 32 warps
     // with the column-slab kernel, keep the gathered blocks slab-major (the
     // sketch and A Q written so, the pass-1 operand converted once per pass)
     int slab_layout = 1;
@@ -175,7 +175,10 @@ inline int spmm_var(const dsvd_ctx* ctx, int64_t ld) {
     int v = ctx->spmm_variant;
     if ((v & (4096 | 8192)) != 0) return v;  // explicit choice
     int w = ctx->spmm_slab;
-    if (w < 0) w = 0;  // auto: whole-row kernels (pending the B200 A/B)
+    // auto: 64-column slabs above 192 columns (C4, l = 300: both passes 10-15%
+    // faster than the whole-row kernel, tools/ab_option.py); the
+    // whole-row kernel below (C2, l = 150: it gathers from an L2-resident X)
+    if (w < 0) w = ld > 192 ? 64 : 0;
     if (w == 32) v |= 4096;
     else if (w == 64) v |= 8192;
     if (w > 0 && ctx->spmm_slab_hint) v |= 16384;
