@@ -315,6 +315,10 @@ CUtensorMap make_cmap(const double* c, int64_t rows, int64_t ld) {
 }
 
 // ---- gram -------------------------------------------------------------------------
+// 1: skip the DMMAs of padding / below-diagonal 8x8 blocks (predicated per warp).
+// Measured on C4: the predicated issue made the wide Gram slower (596 vs 538 ms
+// per solve), so it is off.
+constexpr int kGramSkip = 0;
 constexpr int kGmRows = 32, kGmStages = 4;
 
 __host__ __device__ constexpr int gm_pairs(int nb) { return nb * (nb + 1) / 2; }
@@ -408,7 +412,7 @@ gram_dmma_kernel(const double* __restrict__ c, int64_t n, int64_t ld, int nb, in
             for (int u = 0; u < 4; ++u)
 #pragma unroll
                 for (int v = 0; v < 4; ++v)
-                    if (live & (1u << (4 * u + v))) dmma884(acc[u][v], fa[u], fb[v]);
+                    if (kGramSkip == 0 || (live & (1u << (4 * u + v)))) dmma884(acc[u][v], fa[u], fb[v]);
         }
     }
     cpa_wait<0>();
@@ -550,7 +554,7 @@ gram_dmma_wide_kernel(const double* __restrict__ c, int64_t n, int64_t ld, int n
             for (int u = 0; u < 4; ++u)
 #pragma unroll
                 for (int v = 0; v < 4; ++v)
-                    if (live & (1u << (4 * u + v))) dmma884(acc[u][v], fa[u], fb[v]);
+                    if (kGramSkip == 0 || (live & (1u << (4 * u + v)))) dmma884(acc[u][v], fa[u], fb[v]);
         }
     }
     cpa_wait<0>();

@@ -431,7 +431,7 @@ spmm_slab_kernel(const int64_t* __restrict__ off, const int32_t* __restrict__ id
                  int64_t blocks_per_slab, const double* __restrict__ x, double* __restrict__ y,
                  double* __restrict__ partial, int64_t ld, const double* __restrict__ q,
                  const double* __restrict__ alpha_p, const int32_t* __restrict__ gate, int64_t x_rows, bool x_slab,
-                 bool y_slab) {
+                 bool y_slab, int64_t active) {
     constexpr int G = SlabCfg<W>::G, R = SlabCfg<W>::R;
     if (gate_closed(gate)) return;
     __shared__ __align__(16) double2 cv[kSlabWarps][R][2 * (G + 1)];  // two batches; +1: groups on distinct banks
@@ -439,7 +439,7 @@ spmm_slab_kernel(const int64_t* __restrict__ off, const int32_t* __restrict__ id
     const int g = lane / G, t = lane % G;
     const int slab = static_cast<int>(blockIdx.x / blocks_per_slab);
     const int64_t rb = blockIdx.x - static_cast<int64_t>(slab) * blocks_per_slab;
-    const int64_t items = nchunks + (rows - nsplit);
+    const int64_t items = nchunks + (active - nsplit);
     const int64_t it = (rb * kSlabWarps + warp) * R + g;
     const bool valid = it < items;
     const int64_t col = static_cast<int64_t>(slab) * W + 4 * t;
@@ -1373,13 +1373,38 @@ void combine_split(const SpmmArgs& s, cudaStream_t stream, double* partial) {
     DSVD_LAUNCH_CHECK();
 }
 
+// Rows without nonzeros (order[i], i in [ne, rows)): y = 0.0, or the shifted
+// update of an empty chain, fma(-alpha, q, 0.0), unless alpha == 0 (add_scaled skipped).
+__global__ void empty_rows_kernel(const int32_t* __restrict__ order, int64_t ne, int64_t rows, int64_t ld,
+                                  double* __restrict__ y, const double* __restrict__ q,
+                                  const double* __restrict__ alpha_p, const int32_t* __restrict__ gate, int y_slab_w) {
+    if (gate_closed(gate)) return;
+    const double alpha = q != nullptr ? *alpha_p : 0.0;
+    const int64_t g = ld / 4, units = (rows - ne) * g;
+    for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < units;
+         e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t row = order[ne + e / g], col = 4 * (e % g);
+        double4 v = make_double4(0.0, 0.0, 0.0, 0.0);
+        if (alpha != 0.0) {
+            const double4 qv = *reinterpret_cast<const double4*>(q + row * ld + col);
+            v = make_double4(fma(-alpha, qv.x, 0.0), fma(-alpha, qv.y, 0.0), fma(-alpha, qv.z, 0.0),
+                             fma(-alpha, qv.w, 0.0));
+        }
+        double* dst = y_slab_w > 0 ? y + ((col / y_slab_w) * rows + row) * y_slab_w + col % y_slab_w : y + row * ld + col;
+        *reinterpret_cast<double4*>(dst) = v;
+    }
+}
+
 template <int W, bool kHint, int U, int MB, bool kTag>
 void launch_slab(const SpmmArgs& s, cudaStream_t stream, double* partial) {
     const DevCsr& a = *s.a;
     constexpr int RB = kSlabWarps * SlabCfg<W>::R;
     const int64_t nsplit = partial != nullptr ? a.nsplit : 0;
     const int64_t nchunks = partial != nullptr ? a.nchunks : 0;
-    const int64_t items = nchunks + (a.rows - nsplit);
+    // rows with nonzeros run through the kernel; the empty tail of a.order is
+    // filled below (or skipped)
+    const int64_t active = a.nonempty_rows >= 0 ? std::max(a.nonempty_rows, nsplit) : a.rows;
+    const int64_t items = nchunks + (active - nsplit);
     const int64_t bps = ceil_div(items, RB);
     const int64_t nslab = ceil_div(s.ld, W);
     if (bps * nslab >= (int64_t(1) << 31)) fail(DSVD_UNSUPPORTED, "spmm: slab grid too large");
@@ -1389,12 +1414,17 @@ void launch_slab(const SpmmArgs& s, cudaStream_t stream, double* partial) {
     if (s.q != nullptr)
         spmm_slab_kernel<true, W, U, kHint, MB, kTag><<<blocks, 32 * kSlabWarps, 0, stream>>>(
             a.off, ix, a.val, a.order, nsplit, nchunks, a.chunk_p0, a.chunk_p1, a.rows, bps, s.x, s.y, partial,
-            s.ld, s.q, s.alpha, s.gate, a.cols, s.x_slab, s.y_slab);
+            s.ld, s.q, s.alpha, s.gate, a.cols, s.x_slab, s.y_slab, active);
     else
         spmm_slab_kernel<false, W, U, kHint, MB, kTag><<<blocks, 32 * kSlabWarps, 0, stream>>>(
             a.off, ix, a.val, a.order, nsplit, nchunks, a.chunk_p0, a.chunk_p1, a.rows, bps, s.x, s.y, partial,
-            s.ld, nullptr, nullptr, s.gate, a.cols, s.x_slab, s.y_slab);
+            s.ld, nullptr, nullptr, s.gate, a.cols, s.x_slab, s.y_slab, active);
     DSVD_LAUNCH_CHECK();
+    if (active < a.rows && !s.skip_empty) {
+        empty_rows_kernel<<<grid_for((a.rows - active) * (s.ld / 4)), 256, 0, stream>>>(
+            a.order, active, a.rows, s.ld, s.y, s.q, s.alpha, s.gate, s.y_slab ? W : 0);
+        DSVD_LAUNCH_CHECK();
+    }
 }
 
 template <int W, bool kHint>
@@ -1824,6 +1854,10 @@ void build_row_order(DevCsr& m, void* scratch, size_t scratch_bytes, cudaStream_
         count_ge_kernel<<<1, 1, 0, stream>>>(len_sorted, m.rows,
                                              m.hub_threshold > 0 ? m.hub_threshold : (int64_t(1) << 40),
                                              m.d_hub_rows);
+        DSVD_LAUNCH_CHECK();
+    }
+    if (m.d_nonempty != nullptr) {
+        count_ge_kernel<<<1, 1, 0, stream>>>(len_sorted, m.rows, 1, m.d_nonempty);
         DSVD_LAUNCH_CHECK();
     }
 }

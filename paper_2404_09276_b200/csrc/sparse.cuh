@@ -21,6 +21,10 @@ struct DevCsr {
     int64_t hub_rows = 0;
     int64_t hub_threshold = 0;
     int32_t* d_hub_rows = nullptr;  // device copy written by build_row_order
+    // rows with at least one nonzero: the prefix order[0 .. nonempty_rows) (-1:
+    // unknown, every row is treated as non-empty); d_nonempty is the device count
+    int64_t nonempty_rows = -1;
+    int32_t* d_nonempty = nullptr;
     // Split mode (split_chunk > 0): rows order[0 .. nsplit) hold more than
     // split_chunk nonzeros and are cut into nchunks CSR ranges of at most
     // split_chunk nonzeros; each chunk's FMA chain goes to a partial row and the
@@ -61,6 +65,10 @@ struct SpmmArgs {
     // hot/cold-tagged copy of a.idx (tag_hot_indices) for the column-slab kernel's
     // L2 eviction priorities, or nullptr
     const int32_t* idx_tag = nullptr;
+    // column-slab kernel: rows without nonzeros (the tail of a.order) are not
+    // written at all (their Y rows are never read, e.g. the loop's A Q), instead
+    // of being set to 0 (or -alpha q)
+    bool skip_empty = false;
 };
 
 // idx_tag = m.idx with the sign bit set on every index outside the hot set, the
