@@ -13,7 +13,11 @@ import threading
 
 from . import errors as E
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "libdashsvd_b200.so")
+# DSVD_CHECKED=1 selects the bounds-checked build (make -C paper_2404_09276_b200/csrc checked:
+# device-side index assertions that trap on a violation; compute-sanitizer is not available
+# on the GPU pool)
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)),
+                        "_lib_checked" if os.environ.get("DSVD_CHECKED") == "1" else "_lib", "libdashsvd_b200.so")
 
 P = C.c_void_p
 I64 = C.c_int64

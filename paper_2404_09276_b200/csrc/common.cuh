@@ -69,6 +69,24 @@ struct Control {
 };
 
 #ifdef __CUDACC__
+// Device-side bounds assertions of the checked build (-DDSVD_CHECKED; `make
+// checked`): a violated invariant prints where and traps, failing the call with
+// a CUDA error. Compiled out of the product build.
+#ifdef DSVD_CHECKED
+#define DSVD_DCHECK(cond)                                                                            \
+    do {                                                                                             \
+        if (!(cond)) {                                                                               \
+            printf("DSVD_DCHECK failed: %s (%s:%d) block %d thread %d\n", #cond, __FILE__, __LINE__, \
+                   static_cast<int>(blockIdx.x), static_cast<int>(threadIdx.x));                     \
+            __trap();                                                                                \
+        }                                                                                            \
+    } while (0)
+#else
+#define DSVD_DCHECK(cond) \
+    do {                  \
+    } while (0)
+#endif
+
 // Gate words (Control::stopped / stop_pending) can be set by a kernel on
 // another stream while the reading kernel runs: read them at L2, not through
 // the non-coherent read-only path, so late blocks see a stop and skip.

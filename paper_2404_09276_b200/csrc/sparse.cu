@@ -450,9 +450,11 @@ spmm_slab_kernel(const int64_t* __restrict__ off, const int32_t* __restrict__ id
         if (it < nchunks) {
             beg = chunk_p0[it];
             end = chunk_p1[it];
+            DSVD_DCHECK(beg <= end);
             out = partial + it * ld + col;
         } else {
             const int64_t row = order[nsplit + (it - nchunks)];
+            DSVD_DCHECK(row >= 0 && row < rows);
             beg = off[row];
             end = off[row + 1];
             out = y_slab ? y + (static_cast<int64_t>(slab) * rows + row) * W + 4 * t : y + row * ld + col;
@@ -481,8 +483,10 @@ spmm_slab_kernel(const int64_t* __restrict__ off, const int32_t* __restrict__ id
     auto gather = [&](long long e, double (&r)[4]) {
         if (kTag) {
             const int32_t ci = static_cast<int32_t>(e);
+            DSVD_DCHECK((ci & 0x7fffffff) < x_rows);
             ld256_pol(xc + static_cast<int64_t>(ci & 0x7fffffff) * xstride, r, ci < 0 ? pol_cold : pol_hot);
         } else {
+            DSVD_DCHECK(e >= 0 && e < x_rows);
             ld256(xc + e * xstride, r);
         }
     };
@@ -578,6 +582,7 @@ split_combine_tree_kernel(const double* __restrict__ partial, const int32_t* __r
     if (act) {
         auto at = [&](int32_t c) {
             const int64_t r = slot != nullptr ? slot[c] : c;
+            DSVD_DCHECK(r >= 0 && c >= c0 && c < c1);
             return *reinterpret_cast<const double2*>(partial + r * ld + col);
         };
         int32_t c = a;
@@ -705,6 +710,7 @@ __device__ __forceinline__ int64_t plan_row(const int64_t* __restrict__ off, con
         if (len > 0) {
             const int64_t n = (len + C - 1) / C, cs = (len + n - 1) / n;
             if (kEmit) {
+                DSVD_DCHECK(b >= beg && e <= end);
                 for (int64_t j = 0; j < n; ++j) {
                     p0[out0 + nch + j] = b + j * cs;
                     p1[out0 + nch + j] = min(e, b + (j + 1) * cs);
@@ -746,6 +752,7 @@ __global__ void chunk_place_kernel(const int32_t* __restrict__ ids, int64_t nc, 
     for (int64_t pos = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; pos < nc;
          pos += static_cast<int64_t>(gridDim.x) * blockDim.x) {
         const int32_t id = ids[pos];
+        DSVD_DCHECK(id >= 0 && id < nc);
         slot[id] = static_cast<int32_t>(pos);
         q0[pos] = p0[id];
         q1[pos] = p1[id];
@@ -1384,6 +1391,7 @@ __global__ void empty_rows_kernel(const int32_t* __restrict__ order, int64_t ne,
     for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < units;
          e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
         const int64_t row = order[ne + e / g], col = 4 * (e % g);
+        DSVD_DCHECK(row >= 0 && row < rows);
         double4 v = make_double4(0.0, 0.0, 0.0, 0.0);
         if (alpha != 0.0) {
             const double4 qv = *reinterpret_cast<const double4*>(q + row * ld + col);
