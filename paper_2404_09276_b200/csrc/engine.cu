@@ -155,6 +155,8 @@ void build_pair(dsvd_ctx* ctx, CsrAlloc& al, int64_t rows, int64_t cols, int64_t
     }
     a.idx = static_cast<int32_t*>(al.get("a.idx", sizeof(int32_t) * nnz));
     a.order = static_cast<int32_t*>(al.get("a.order", sizeof(int32_t) * (rows > 0 ? rows : 1)));
+    a.obeg = static_cast<int64_t*>(al.get("a.obeg", sizeof(int64_t) * (rows > 0 ? rows : 1)));
+    a.olen = static_cast<int32_t*>(al.get("a.olen", sizeof(int32_t) * (rows > 0 ? rows : 1)));
     // device scalars read back by the host: {offsets bad, index bad} right away,
     // {hub rows of A, of A^T, chunk total / max of A, of A^T} in one read at the end
     int32_t* sc = static_cast<int32_t*>(al.get("plan_scalars", sizeof(int32_t) * 10));
@@ -178,6 +180,8 @@ void build_pair(dsvd_ctx* ctx, CsrAlloc& al, int64_t rows, int64_t cols, int64_t
     at.idx = static_cast<int32_t*>(al.get("at.idx", sizeof(int32_t) * nnz));
     at.val = static_cast<double*>(al.get("at.val", sizeof(double) * nnz));
     at.order = static_cast<int32_t*>(al.get("at.order", sizeof(int32_t) * (cols > 0 ? cols : 1)));
+    at.obeg = static_cast<int64_t*>(al.get("at.obeg", sizeof(int64_t) * (cols > 0 ? cols : 1)));
+    at.olen = static_cast<int32_t*>(al.get("at.olen", sizeof(int32_t) * (cols > 0 ? cols : 1)));
     const size_t scratch_bytes =
         std::max({csc_scratch_bytes(rows, cols, nnz), order_scratch_bytes(rows), order_scratch_bytes(cols)});
     void* scratch = ctx->buf("csc.scratch", scratch_bytes);

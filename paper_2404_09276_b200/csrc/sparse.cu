@@ -431,7 +431,7 @@ spmm_slab_kernel(const int64_t* __restrict__ off, const int32_t* __restrict__ id
                  int64_t blocks_per_slab, const double* __restrict__ x, double* __restrict__ y,
                  double* __restrict__ partial, int64_t ld, const double* __restrict__ q,
                  const double* __restrict__ alpha_p, const int32_t* __restrict__ gate, int64_t x_rows, bool x_slab,
-                 bool y_slab, int64_t active) {
+                 bool y_slab, int64_t active, const int64_t* __restrict__ obeg, const int32_t* __restrict__ olen) {
     constexpr int G = SlabCfg<W>::G, R = SlabCfg<W>::R;
     if (gate_closed(gate)) return;
     __shared__ __align__(16) double2 cv[kSlabWarps][R][2 * (G + 1)];  // two batches; +1: groups on distinct banks
@@ -453,10 +453,16 @@ spmm_slab_kernel(const int64_t* __restrict__ off, const int32_t* __restrict__ id
             DSVD_DCHECK(beg <= end);
             out = partial + it * ld + col;
         } else {
-            const int64_t row = order[nsplit + (it - nchunks)];
+            const int64_t pos = nsplit + (it - nchunks);
+            const int64_t row = order[pos];
             DSVD_DCHECK(row >= 0 && row < rows);
-            beg = off[row];
-            end = off[row + 1];
+            if (obeg != nullptr) {  // independent of the order[] load
+                beg = obeg[pos];
+                end = beg + olen[pos];
+            } else {
+                beg = off[row];
+                end = off[row + 1];
+            }
             out = y_slab ? y + (static_cast<int64_t>(slab) * rows + row) * W + 4 * t : y + row * ld + col;
             if (kShift) qrow = q + row * ld;
         }
@@ -1329,6 +1335,17 @@ __global__ void fill_i64_kernel(int64_t* __restrict__ p, int64_t n, int64_t v) {
         p[i] = v;
 }
 
+__global__ void order_ranges_kernel(const int32_t* __restrict__ order, const int64_t* __restrict__ off, int64_t rows,
+                                    int64_t* __restrict__ obeg, int32_t* __restrict__ olen) {
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < rows;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t r = order[i];
+        obeg[i] = off[r];
+        const int64_t n = off[r + 1] - off[r];
+        olen[i] = static_cast<int32_t>(n > 0x7fffffff ? 0x7fffffff : n);
+    }
+}
+
 __global__ void row_lengths_kernel(const int64_t* __restrict__ off, int64_t rows,
                                    int32_t* __restrict__ len, int32_t* __restrict__ ids) {
     for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < rows;
@@ -1422,11 +1439,11 @@ void launch_slab(const SpmmArgs& s, cudaStream_t stream, double* partial) {
     if (s.q != nullptr)
         spmm_slab_kernel<true, W, U, kHint, MB, kTag><<<blocks, 32 * kSlabWarps, 0, stream>>>(
             a.off, ix, a.val, a.order, nsplit, nchunks, a.chunk_p0, a.chunk_p1, a.rows, bps, s.x, s.y, partial,
-            s.ld, s.q, s.alpha, s.gate, a.cols, s.x_slab, s.y_slab, active);
+            s.ld, s.q, s.alpha, s.gate, a.cols, s.x_slab, s.y_slab, active, a.obeg, a.olen);
     else
         spmm_slab_kernel<false, W, U, kHint, MB, kTag><<<blocks, 32 * kSlabWarps, 0, stream>>>(
             a.off, ix, a.val, a.order, nsplit, nchunks, a.chunk_p0, a.chunk_p1, a.rows, bps, s.x, s.y, partial,
-            s.ld, nullptr, nullptr, s.gate, a.cols, s.x_slab, s.y_slab, active);
+            s.ld, nullptr, nullptr, s.gate, a.cols, s.x_slab, s.y_slab, active, a.obeg, a.olen);
     DSVD_LAUNCH_CHECK();
     if (active < a.rows && !s.skip_empty) {
         empty_rows_kernel<<<grid_for((a.rows - active) * (s.ld / 4)), 256, 0, stream>>>(
@@ -1866,6 +1883,10 @@ void build_row_order(DevCsr& m, void* scratch, size_t scratch_bytes, cudaStream_
     }
     if (m.d_nonempty != nullptr) {
         count_ge_kernel<<<1, 1, 0, stream>>>(len_sorted, m.rows, 1, m.d_nonempty);
+        DSVD_LAUNCH_CHECK();
+    }
+    if (m.obeg != nullptr) {
+        order_ranges_kernel<<<grid_for(m.rows), 256, 0, stream>>>(m.order, m.off, m.rows, m.obeg, m.olen);
         DSVD_LAUNCH_CHECK();
     }
 }

@@ -15,6 +15,11 @@ struct DevCsr {
     int32_t* idx = nullptr;
     double* val = nullptr;
     int32_t* order = nullptr;
+    // CSR range of row order[i] in order sequence (obeg[i] = off[order[i]],
+    // olen[i] its length), so the column-slab kernel reads a row's range with one
+    // load beside order[i] instead of a dependent off[] lookup; optional
+    int64_t* obeg = nullptr;
+    int32_t* olen = nullptr;
     int64_t max_row_nnz = 0;
     // rows order[0 .. hub_rows) hold >= hub_threshold nonzeros and take the
     // deep-pipelined hub path of spmm (counted on the device at build time)
