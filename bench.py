@@ -354,6 +354,7 @@ def b200_matrix(cfg, dev, world, rank):
             return m.download_rows(b[rank], b[rank + 1]), m.nnz, b[rank]
         finally:
             m.close()
+            (dev or d.default_device()).trim()  # the generator's workspaces (C5: tens of GB)
     if "npr" in cfg:
         a = d.sparse_random(cfg["rows"], cfg["cols"], cfg["npr"], cfg["gen_seed"], True)
     else:

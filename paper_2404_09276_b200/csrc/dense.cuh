@@ -49,7 +49,7 @@ bool rescale_dmma_supported(int64_t K, int64_t ldc, int64_t ld_out, int out_colm
 size_t rescale_dmma_workspace_bytes(int64_t K, int64_t width);
 void rescale_dmma(const double* c, int64_t n, int64_t K, int64_t ldc, const double* w, int64_t ldw,
                   const double* scale, int64_t ncol, double* out, int64_t ld_out, int out_colmajor, void* ws,
-                  const int32_t* gate, cudaStream_t stream);
+                  const int32_t* gate, cudaStream_t stream, double* out2 = nullptr, int out2_w = 0);
 
 // Column-major (rows x cols) <-> row-major (stride ld, pad columns zeroed).
 void colmajor_to_rowmajor(const double* src, int64_t rows, int64_t cols, double* dst, int64_t ld,

@@ -97,7 +97,7 @@ __global__ void rescale_prep_kernel(const double* __restrict__ w, int64_t ldw, c
 __global__ void __launch_bounds__(kRsThreads, 2)
 rescale_dmma_kernel(const double* __restrict__ c, int64_t n, int K, int64_t ldc, const double* __restrict__ wt,
                     int ldb, int ncol, double* __restrict__ out, int64_t ld_out, int out_colmajor,
-                    const int32_t* __restrict__ gate) {
+                    const int32_t* __restrict__ gate, double* __restrict__ out2, int out2_w) {
     if (gate != nullptr && *gate != 0) return;
     extern __shared__ __align__(16) double rsm[];
     double* Bt = rsm;                // [32][ldb]: W block, transposed
@@ -178,8 +178,11 @@ rescale_dmma_kernel(const double* __restrict__ c, int64_t n, int K, int64_t ldc,
                     if (j + 1 < ncol) out[static_cast<int64_t>(j + 1) * n + r] = v.y;
                 } else if (j + 1 < ld_out) {
                     *reinterpret_cast<double2*>(out + r * ld_out + j) = v;
+                    if (out2 != nullptr)  // the slab-major copy (j even: j, j + 1 share a slab)
+                        *reinterpret_cast<double2*>(out2 + ((j / out2_w) * n + r) * out2_w + j % out2_w) = v;
                 } else if (j < ld_out) {
                     out[r * ld_out + j] = v.x;
+                    if (out2 != nullptr) out2[((j / out2_w) * n + r) * out2_w + j % out2_w] = v.x;
                 }
             }
         }
@@ -195,7 +198,7 @@ template <int ST>
 __global__ void __launch_bounds__(kRsThreads, 2)
 rescale_tma_kernel(const __grid_constant__ CUtensorMap cmap, int64_t n, int K, const double* __restrict__ wt,
                    int ldb, int ncol, double* __restrict__ out, int64_t ld_out, int out_colmajor,
-                   const int32_t* __restrict__ gate) {
+                   const int32_t* __restrict__ gate, double* __restrict__ out2, int out2_w) {
     if (gate != nullptr && *gate != 0) return;
     extern __shared__ __align__(1024) unsigned char rsm_raw[];
     // 1024-byte aligned ring first (128B-swizzle requirement), then W, then barriers
@@ -283,8 +286,11 @@ rescale_tma_kernel(const __grid_constant__ CUtensorMap cmap, int64_t n, int K, c
                     if (j + 1 < ncol) out[static_cast<int64_t>(j + 1) * n + r] = v.y;
                 } else if (j + 1 < ld_out) {
                     *reinterpret_cast<double2*>(out + r * ld_out + j) = v;
+                    if (out2 != nullptr)  // the slab-major copy (j even: j, j + 1 share a slab)
+                        *reinterpret_cast<double2*>(out2 + ((j / out2_w) * n + r) * out2_w + j % out2_w) = v;
                 } else if (j < ld_out) {
                     out[r * ld_out + j] = v.x;
+                    if (out2 != nullptr) out2[((j / out2_w) * n + r) * out2_w + j % out2_w] = v.x;
                 }
             }
         }
@@ -682,7 +688,8 @@ size_t rescale_dmma_workspace_bytes(int64_t K, int64_t width) {
 
 void rescale_dmma(const double* c, int64_t n, int64_t K, int64_t ldc, const double* w, int64_t ldw,
                   const double* scale, int64_t ncol, double* out, int64_t ld_out, int out_colmajor, void* ws,
-                  const int32_t* gate, cudaStream_t stream) {
+                  const int32_t* gate, cudaStream_t stream, double* out2, int out2_w) {
+    if (out2 != nullptr && (out_colmajor || out2_w <= 0 || out2_w % 2 != 0)) fail(DSVD_OTHER, "rescale: bad second output");
     if (n == 0) return;
     const int64_t width = out_colmajor ? ncol : ld_out;
     const int ncb = static_cast<int>(ceil_div(width, kRsBN));
@@ -704,14 +711,14 @@ void rescale_dmma(const double* c, int64_t n, int64_t K, int64_t ldc, const doub
         DSVD_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
         const CUtensorMap cmap = make_cmap(c, n, ldc);
         kern<<<grid, kRsThreads, smem, stream>>>(cmap, n, static_cast<int>(K), wt, ldb, static_cast<int>(ncol), out,
-                                                 ld_out, out_colmajor, gate);
+                                                 ld_out, out_colmajor, gate, out2, out2_w);
     } else {
         const size_t smem = sizeof(double) * (static_cast<size_t>(kRsBN) * ldb + kRsStages * kRsBM * kRsBK);
         DSVD_CUDA_CHECK(cudaFuncSetAttribute(rescale_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              static_cast<int>(smem)));
         rescale_dmma_kernel<<<grid, kRsThreads, smem, stream>>>(c, n, static_cast<int>(K), ldc, wt, ldb,
                                                                 static_cast<int>(ncol), out, ld_out, out_colmajor,
-                                                                gate);
+                                                                gate, out2, out2_w);
     }
     DSVD_LAUNCH_CHECK();
 }

@@ -294,18 +294,22 @@ struct EigSvdOut {
 
 // rescale() of the solve path: FP64 tensor cores when the shape allows
 // (dmma.cu), else the DFMA kernel. Two launches either way on the DMMA path.
-void solve_rescale(dsvd_ctx* ctx, const double* c, int64_t n, int64_t K, int64_t ldc, const double* w,
+// With out2 != nullptr the DMMA path also writes a slab-major copy (width
+// out2_w) of the row-major result and returns true; false: no copy was made.
+bool solve_rescale(dsvd_ctx* ctx, const double* c, int64_t n, int64_t K, int64_t ldc, const double* w,
                    int64_t ldw, const double* scale, int64_t ncol, double* out, int64_t ld_out, int out_colmajor,
-                   const int32_t* gate) {
+                   const int32_t* gate, double* out2 = nullptr, int out2_w = 0) {
     if (ctx->dense_method == 0 && rescale_dmma_supported(K, ldc, ld_out, out_colmajor)) {
         const size_t ws = rescale_dmma_workspace_bytes(K, out_colmajor ? ncol : ld_out);
         rescale_dmma(c, n, K, ldc, w, ldw, scale, ncol, out, ld_out, out_colmajor, ctx->buf("rescale.ws", ws), gate,
-                     ctx->stream);
+                     ctx->stream, out2, out2_w);
         count_launch(2);
+        return out2 != nullptr;
     } else {
         rescale(c, n, K, ldc, w, ldw, scale, ncol, out, ld_out, out_colmajor, gate, ctx->stream);
         count_launch();
     }
+    return false;
 }
 
 // (s, V) of the row-major block c (rows x l, stride ld); U is left to the caller.
@@ -529,12 +533,18 @@ void solve_tall(dsvd_ctx* ctx, const DevCsr& A, const DevCsr& AT, const dsvd_con
         tag_a = ta;
         tag_at = tt;
     }
+    // the block whose slab-major copy Xs currently holds (written by the
+    // rescale that produced it, single-GPU solves), so pass 1 skips the copy
+    const double* xs_holds = nullptr;
     auto pass1 = [&](const double* x, double* y_out, bool y_slab_major, const int32_t* g) {
         SpmmArgs sa{&A, x, y_out, ld, l, nullptr, nullptr, g};
         sa.idx_tag = tag_a;
         if (lw > 0) {
-            to_slab_major(x, n, ld, lw, Xs, st);
-            count_launch();
+            if (xs_holds != x) {
+                to_slab_major(x, n, ld, lw, Xs, st);
+                count_launch();
+                xs_holds = x;
+            }
             sa.x = Xs;
             sa.slab = lw;
             sa.x_slab = true;
@@ -562,7 +572,9 @@ void solve_tall(dsvd_ctx* ctx, const DevCsr& A, const DevCsr& AT, const dsvd_con
     // the slab into its rows of dst and all-gathers the other ranks' slabs
     auto rescale_into = [&](const double* c, double* dst, const int32_t* g) {
         int s2 = ctx->span_begin(K_RESCALE);
-        solve_rescale(ctx, c, red_rows, l, ld, W, l, inv_s, l, dst + slab0 * ld, ld, 0, g);
+        const bool copy = lw > 0 && !sharded;  // the next A pass gathers dst: write its slab-major copy too
+        xs_holds = solve_rescale(ctx, c, red_rows, l, ld, W, l, inv_s, l, dst + slab0 * ld, ld, 0, g,
+                                 copy ? Xs : nullptr, lw) ? dst : nullptr;
         ctx->span_end(s2);
         if (v2) {
             s2 = ctx->span_begin(K_COMM);
@@ -693,7 +705,8 @@ void solve_tall(dsvd_ctx* ctx, const DevCsr& A, const DevCsr& AT, const dsvd_con
         ctx->stats.eig_sweeps = hc.total_sweeps;
         // Q_N = T_N W_N diag(1/s_N): the basis the finalize multiplies by A
         sp = ctx->span_begin(K_RESCALE);
-        solve_rescale(ctx, Tb[hc.iteration % 2], n, l, ld, W, l, inv_s, l, P, ld, 0, nullptr);
+        xs_holds = solve_rescale(ctx, Tb[hc.iteration % 2], n, l, ld, W, l, inv_s, l, P, ld, 0, nullptr,
+                                 lw > 0 && !sharded ? Xs : nullptr, lw) ? P : nullptr;
         ctx->span_end(sp);
         Qf = P;
     } else {
