@@ -159,8 +159,8 @@ void build_pair(dsvd_ctx* ctx, CsrAlloc& al, int64_t rows, int64_t cols, int64_t
     a.olen = static_cast<int32_t*>(al.get("a.olen", sizeof(int32_t) * (rows > 0 ? rows : 1)));
     // device scalars read back by the host: {offsets bad, index bad} right away,
     // {hub rows of A, of A^T, chunk total / max of A, of A^T} in one read at the end
-    int32_t* sc = static_cast<int32_t*>(al.get("plan_scalars", sizeof(int32_t) * 10));
-    DSVD_CUDA_CHECK(cudaMemsetAsync(sc, 0, sizeof(int32_t) * 10, st));
+    int32_t* sc = static_cast<int32_t*>(al.get("plan_scalars", sizeof(int32_t) * 12));
+    DSVD_CUDA_CHECK(cudaMemsetAsync(sc, 0, sizeof(int32_t) * 12, st));
     check_offsets(a.off, rows, nnz, sc, st);
     count_launch();
     narrow_indices(d_idx64, a.idx, nnz, cols, sc + 1, st);
@@ -200,6 +200,8 @@ void build_pair(dsvd_ctx* ctx, CsrAlloc& al, int64_t rows, int64_t cols, int64_t
     at.d_hub_rows = sc + 3;
     a.d_nonempty = sc + 8;
     at.d_nonempty = sc + 9;
+    a.d_long = sc + 10;
+    at.d_long = sc + 11;
     build_row_order(a, scratch, scratch_bytes, st);
     count_launch(rows > 0 ? 4 : 0);
     build_row_order(at, scratch, scratch_bytes, st);
@@ -211,11 +213,13 @@ void build_pair(dsvd_ctx* ctx, CsrAlloc& al, int64_t rows, int64_t cols, int64_t
         plan_chunks_count(ctx, al, a, "a", 0, sc + 4, cpa);
         plan_chunks_count(ctx, al, at, "at", ctx->split_panel_rows, sc + 6, cpt);
     }
-    int32_t h[10];
+    int32_t h[12];
     DSVD_CUDA_CHECK(cudaMemcpyAsync(h, sc, sizeof(h), cudaMemcpyDeviceToHost, st));
     DSVD_CUDA_CHECK(cudaStreamSynchronize(st));
     a.nonempty_rows = rows > 0 ? h[8] : 0;
     at.nonempty_rows = cols > 0 ? h[9] : 0;
+    a.long_rows = rows > 0 ? h[10] : 0;
+    at.long_rows = cols > 0 ? h[11] : 0;
     a.hub_rows = rows > 0 ? h[2] : 0;
     at.hub_rows = cols > 0 ? h[3] : 0;
     if (C > 0) {

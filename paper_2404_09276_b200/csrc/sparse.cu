@@ -1420,31 +1420,45 @@ __global__ void empty_rows_kernel(const int32_t* __restrict__ order, int64_t ne,
     }
 }
 
+// One slab-kernel launch over the chunks [0, nchunks) and the rows at order
+// positions [first, end), slab-major.
 template <int W, bool kHint, int U, int MB, bool kTag>
-void launch_slab(const SpmmArgs& s, cudaStream_t stream, double* partial) {
+void launch_slab_range(const SpmmArgs& s, cudaStream_t stream, double* partial, int64_t nchunks, int64_t first,
+                       int64_t end) {
     const DevCsr& a = *s.a;
     constexpr int RB = kSlabWarps * SlabCfg<W>::R;
-    const int64_t nsplit = partial != nullptr ? a.nsplit : 0;
-    const int64_t nchunks = partial != nullptr ? a.nchunks : 0;
-    // rows with nonzeros run through the kernel; the empty tail of a.order is
-    // filled below (or skipped)
-    const int64_t active = a.nonempty_rows >= 0 ? std::max(a.nonempty_rows, nsplit) : a.rows;
-    const int64_t items = nchunks + (active - nsplit);
+    const int64_t items = nchunks + (end - first);
+    if (items <= 0) return;
     const int64_t bps = ceil_div(items, RB);
     const int64_t nslab = ceil_div(s.ld, W);
     if (bps * nslab >= (int64_t(1) << 31)) fail(DSVD_UNSUPPORTED, "spmm: slab grid too large");
     const unsigned blocks = static_cast<unsigned>(bps * nslab);
-    if ((s.x_slab || s.y_slab) && s.slab != W) fail(DSVD_OTHER, "spmm: slab-major block of another slab width");
     const int32_t* ix = kTag ? s.idx_tag : a.idx;
     if (s.q != nullptr)
         spmm_slab_kernel<true, W, U, kHint, MB, kTag><<<blocks, 32 * kSlabWarps, 0, stream>>>(
-            a.off, ix, a.val, a.order, nsplit, nchunks, a.chunk_p0, a.chunk_p1, a.rows, bps, s.x, s.y, partial,
-            s.ld, s.q, s.alpha, s.gate, a.cols, s.x_slab, s.y_slab, active, a.obeg, a.olen);
+            a.off, ix, a.val, a.order, first, nchunks, a.chunk_p0, a.chunk_p1, a.rows, bps, s.x, s.y, partial,
+            s.ld, s.q, s.alpha, s.gate, a.cols, s.x_slab, s.y_slab, end, a.obeg, a.olen);
     else
         spmm_slab_kernel<false, W, U, kHint, MB, kTag><<<blocks, 32 * kSlabWarps, 0, stream>>>(
-            a.off, ix, a.val, a.order, nsplit, nchunks, a.chunk_p0, a.chunk_p1, a.rows, bps, s.x, s.y, partial,
-            s.ld, nullptr, nullptr, s.gate, a.cols, s.x_slab, s.y_slab, active, a.obeg, a.olen);
+            a.off, ix, a.val, a.order, first, nchunks, a.chunk_p0, a.chunk_p1, a.rows, bps, s.x, s.y, partial,
+            s.ld, nullptr, nullptr, s.gate, a.cols, s.x_slab, s.y_slab, end, a.obeg, a.olen);
     DSVD_LAUNCH_CHECK();
+}
+
+template <int W, bool kHint, int U, int MB, bool kTag>
+void launch_slab(const SpmmArgs& s, cudaStream_t stream, double* partial) {
+    const DevCsr& a = *s.a;
+    const int64_t nsplit = partial != nullptr ? a.nsplit : 0;
+    const int64_t nchunks = partial != nullptr ? a.nchunks : 0;
+    if ((s.x_slab || s.y_slab) && s.slab != W) fail(DSVD_OTHER, "spmm: slab-major block of another slab width");
+    // rows with nonzeros run through the kernel; the empty tail of a.order is
+    // filled below (or skipped). Rows of at most kShortRow nonzeros (their cost
+    // is the per-row load chain, not bandwidth) get their own launch at 48
+    // warps per SM (instead of 32) and one gather in flight per lane.
+    const int64_t active = a.nonempty_rows >= 0 ? std::max(a.nonempty_rows, nsplit) : a.rows;
+    const int64_t nlong = a.long_rows >= 0 ? std::min(std::max(a.long_rows, nsplit), active) : active;
+    launch_slab_range<W, kHint, U, MB, kTag>(s, stream, partial, nchunks, nsplit, nlong);
+    launch_slab_range<W, kHint, 1, 6, kTag>(s, stream, partial, 0, nlong, active);
     if (active < a.rows && !s.skip_empty) {
         empty_rows_kernel<<<grid_for((a.rows - active) * (s.ld / 4)), 256, 0, stream>>>(
             a.order, active, a.rows, s.ld, s.y, s.q, s.alpha, s.gate, s.y_slab ? W : 0);
@@ -1883,6 +1897,10 @@ void build_row_order(DevCsr& m, void* scratch, size_t scratch_bytes, cudaStream_
     }
     if (m.d_nonempty != nullptr) {
         count_ge_kernel<<<1, 1, 0, stream>>>(len_sorted, m.rows, 1, m.d_nonempty);
+        DSVD_LAUNCH_CHECK();
+    }
+    if (m.d_long != nullptr) {
+        count_ge_kernel<<<1, 1, 0, stream>>>(len_sorted, m.rows, kShortRow + 1, m.d_long);
         DSVD_LAUNCH_CHECK();
     }
     if (m.obeg != nullptr) {

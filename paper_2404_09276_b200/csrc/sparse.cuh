@@ -30,6 +30,11 @@ struct DevCsr {
     // unknown, every row is treated as non-empty); d_nonempty is the device count
     int64_t nonempty_rows = -1;
     int32_t* d_nonempty = nullptr;
+    // rows with more than kShortRow nonzeros: the prefix order[0 .. long_rows);
+    // the column-slab kernel runs the short rows after them in a leaner,
+    // higher-occupancy launch (their time is the per-row latency chain)
+    int64_t long_rows = -1;
+    int32_t* d_long = nullptr;
     // Split mode (split_chunk > 0): rows order[0 .. nsplit) hold more than
     // split_chunk nonzeros and are cut into nchunks CSR ranges of at most
     // split_chunk nonzeros; each chunk's FMA chain goes to a partial row and the
@@ -48,6 +53,8 @@ struct DevCsr {
     int32_t* chunk_slot = nullptr;
     int64_t max_row_chunks = 0;  // most chunks of one split row (picks the combine kernel)
 };
+
+constexpr int kShortRow = 8;
 
 // SpMM launch description. X and Y (and Q) are row-major with row stride ld.
 struct SpmmArgs {

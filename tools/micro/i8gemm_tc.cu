@@ -23,7 +23,7 @@
         }                                                                                          \
     } while (0)
 
-constexpr int BM = 128, BK = 128, STAGES = 2;
+constexpr int BM = 128, BK = 128;
 
 __device__ __forceinline__ uint32_t su32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
 
@@ -61,8 +61,8 @@ __host__ __device__ constexpr uint32_t idesc_i8(int M, int N) {
            (static_cast<uint32_t>(M >> 4) << 24);
 }
 
-template <int BN>
-__global__ void __launch_bounds__(128, 1)
+template <int BN, int STAGES, int MINB>
+__global__ void __launch_bounds__(128, MINB)
 i8gemm_kernel(const __grid_constant__ CUtensorMap amap, const __grid_constant__ CUtensorMap bmap, int K,
               int32_t* __restrict__ C, int ldc) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -172,7 +172,7 @@ static CUtensorMap map_i8(const int8_t* ptr, int64_t rows, int64_t K, int box_ro
     return m;
 }
 
-template <int BN>
+template <int BN, int STAGES = 2, int MINB = 1>
 static void run(int M, int N, int K, bool check) {
     std::vector<int8_t> ha(static_cast<size_t>(M) * K), hb(static_cast<size_t>(N) * K);
     uint64_t s = 12345;
@@ -194,9 +194,9 @@ static void run(int M, int N, int K, bool check) {
     CK(cudaMemset(dc, 0, sizeof(int32_t) * M * N));
     const CUtensorMap am = map_i8(da, M, K, BM), bm = map_i8(db, N, K, BN);
     const size_t smem = 1024 + STAGES * (BM + BN) * BK + 64;
-    CK(cudaFuncSetAttribute(i8gemm_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    CK(cudaFuncSetAttribute(i8gemm_kernel<BN, STAGES, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     dim3 grid(M / BM, N / BN);
-    i8gemm_kernel<BN><<<grid, 128, smem>>>(am, bm, K, dc, N);
+    i8gemm_kernel<BN, STAGES, MINB><<<grid, 128, smem>>>(am, bm, K, dc, N);
     CK(cudaGetLastError());
     CK(cudaDeviceSynchronize());
     if (check) {
@@ -220,14 +220,15 @@ static void run(int M, int N, int K, bool check) {
         float best = 1e30f;
         for (int r = 0; r < 5; ++r) {
             cudaEventRecord(e0);
-            i8gemm_kernel<BN><<<grid, 128, smem>>>(am, bm, K, dc, N);
+            i8gemm_kernel<BN, STAGES, MINB><<<grid, 128, smem>>>(am, bm, K, dc, N);
             cudaEventRecord(e1);
             cudaEventSynchronize(e1);
             float ms;
             cudaEventElapsedTime(&ms, e0, e1);
             if (ms < best) best = ms;
         }
-        printf("perf M=%d N=%d K=%d BN=%d: %.3f ms, %.1f TOPS (int8 MAC = 2 ops)\n", M, N, K, BN, best,
+        printf("perf M=%d N=%d K=%d BN=%d stages=%d ctas/SM=%d: %.3f ms, %.1f TOPS (int8 MAC = 2 ops)\n", M, N, K,
+               BN, STAGES, MINB, best,
                2.0 * M * N * K / best / 1e9);
     }
     cudaFree(da);
@@ -240,7 +241,15 @@ int main() {
     run<64>(256, 128, 512, true);
     run<128>(512, 256, 1024, true);
     run<256>(256, 256, 384, true);
+    run<128, 4, 2>(512, 256, 1024, true);
+    run<256, 3, 2>(512, 512, 1024, true);
     run<256>(18944, 256, 8192, false);
     run<128>(18944, 256, 8192, false);
+    run<128, 4, 1>(18944, 512, 8192, false);
+    run<128, 4, 2>(18944, 512, 8192, false);
+    run<256, 3, 1>(18944, 512, 8192, false);
+    run<256, 3, 2>(18944, 512, 8192, false);
+    run<256, 4, 1>(37888, 512, 8192, false);
+    run<128, 6, 1>(37888, 512, 8192, false);
     return 0;
 }
