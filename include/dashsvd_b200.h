@@ -196,8 +196,8 @@ DSVD_API int dsvd_matrix_set_shard(dsvd_matrix* m, int64_t row_offset, int64_t g
 DSVD_API int dsvd_matrix_shape(const dsvd_matrix* m, int64_t* rows, int64_t* cols, int64_t* nnz);
 /* Microbenchmark the SpMM of A (transpose = 0) or A^T (transpose = 1) on a
  * random l-column block: average milliseconds over `iters` launches.
- * variant: 0 = TMA gather4 hub kernel, 1 = cp.async hub kernel; +16 times only
- * the hub rows, +32 only the bulk rows. dsvd_matrix_hub_rows reports how many
+ * variant: the spmm_variant bits (0 = the default kernels; +16 skips the bulk
+ * rows, +32 the long rows; 4096 / 8192 the 32- / 64-column slab kernel). dsvd_matrix_hub_rows reports how many
  * rows of A / A^T take the hub path (option "hub_threshold"). */
 DSVD_API int dsvd_matrix_bench_spmm(dsvd_matrix* m, int transpose, int64_t l, int variant,
                                     int iters, double* ms_out);

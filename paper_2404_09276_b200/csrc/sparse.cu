@@ -11,9 +11,6 @@
 //  - build_transpose: CSR(A^T) as a stable sort of the nonzeros by column
 //    (the counting sort of sparse_matrix.cpp:35-55 is stable in row order),
 //    bitwise equal to the reference.
-#include <cuda.h>
-#include <cudaTypedefs.h>
-
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_reduce.cuh>
 #include <cub/device/device_scan.cuh>
@@ -887,366 +884,6 @@ spmm_hub_kernel(const int64_t* __restrict__ off, const int32_t* __restrict__ idx
 }
 
 
-// ---- hub rows, TMA variant ---------------------------------------------------------
-// CTA = (hub row, 64-column slab), persistent over the hub items. Warp 0 is the
-// producer: it streams the row's (index, value) pairs and issues TMA
-// tile::gather4 copies — four X rows of the slab per instruction — into a
-// kTmaStages-deep shared-memory ring guarded by full/empty mbarriers. Warps 1..2
-// are consumers: one lane per column runs that column's FMA chain over the
-// ring in CSR order (bitwise as above). 64 columns x 8 B per nonzero keeps one
-// CTA's demand near an SM's L2 share at the FMA-latency-bound rate, so a
-// 200k-nonzero row finishes in ~1 ms instead of waiting on the memory system.
-constexpr int kTmaW = 64;
-constexpr int kTmaStageNnz = 32;
-constexpr int kTmaStages = 6;
-constexpr int kTmaConsumers = kTmaW / 32;
-constexpr int kTmaPf = 4;                           // index/value prefetch distance (stages)
-constexpr int kTmaRing = kTmaStages + kTmaPf;       // index/value ring slots
-constexpr int kTmaThreads = 32 * (1 + kTmaConsumers);
-constexpr size_t kTmaStageBytes = sizeof(double) * kTmaStageNnz * kTmaW;
-constexpr size_t kTmaSmem = 1024 + kTmaStages * kTmaStageBytes +
-                            kTmaRing * kTmaStageNnz * (sizeof(double) + sizeof(int32_t)) +
-                            2 * kTmaStages * sizeof(uint64_t);
-
-__device__ __forceinline__ unsigned smem_u32(const void* p) {
-    return static_cast<unsigned>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)),
-                 "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
-    asm volatile(
-        "{\n"
-        ".reg .pred p;\n"
-        "WAIT_%=:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-        "@!p bra WAIT_%=;\n"
-        "}\n" ::"r"(smem_u32(bar)),
-        "r"(parity)
-        : "memory");
-}
-__device__ __forceinline__ void tma_gather4(void* dst, const CUtensorMap* map, int col, int r0,
-                                            int r1, int r2, int r3, uint64_t* bar) {
-    asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cta.global.tile::gather4.mbarrier::complete_tx::bytes"
-        " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];\n" ::"r"(smem_u32(dst)),
-        "l"(reinterpret_cast<uint64_t>(map)), "r"(col), "r"(r0), "r"(r1), "r"(r2), "r"(r3),
-        "r"(smem_u32(bar))
-        : "memory");
-}
-
-template <bool kShift>
-__global__ void __launch_bounds__(kTmaThreads)
-spmm_hub_tma_kernel(const __grid_constant__ CUtensorMap xmap, const int64_t* __restrict__ off,
-                    const int32_t* __restrict__ idx, const double* __restrict__ val,
-                    const int32_t* __restrict__ order, const int32_t* __restrict__ n_hub_p,
-                    int nslab, double* __restrict__ y, int64_t ld, const double* __restrict__ q,
-                    const double* __restrict__ alpha_p, const int32_t* __restrict__ gate) {
-    if (gate_closed(gate)) return;
-    extern __shared__ __align__(1024) unsigned char tma_raw[];
-    unsigned char* base = reinterpret_cast<unsigned char*>(
-        (reinterpret_cast<uintptr_t>(tma_raw) + 1023) & ~uintptr_t(1023));
-    double* data = reinterpret_cast<double*>(base);                        // [S][32][64]
-    double* vring = data + kTmaStages * kTmaStageNnz * kTmaW;               // [R][32]
-    uint64_t* full = reinterpret_cast<uint64_t*>(vring + kTmaRing * kTmaStageNnz);
-    uint64_t* empty = full + kTmaStages;
-    int32_t* iring = reinterpret_cast<int32_t*>(empty + kTmaStages);       // [R][32]
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int64_t items = static_cast<int64_t>(*n_hub_p) * nslab;
-    if (threadIdx.x == 0) {
-        for (int s = 0; s < kTmaStages; ++s) {
-            mbar_init(&full[s], 1);
-            mbar_init(&empty[s], kTmaConsumers);
-        }
-        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-    }
-    __syncthreads();
-    if (warp == 0) {
-        // Producer. Two cursors walk the same flat stage sequence: `pf` fetches
-        // the (index, value) pairs kTmaPf stages ahead with cp.async, `is`
-        // turns landed indices into TMA gathers.
-        struct Cursor {
-            int64_t item, beg, end, p0;
-            int col0;
-            bool valid;
-        };
-        auto seek = [&](Cursor& c) {
-            c.valid = false;
-            while (c.item < items) {
-                const int64_t row = order[c.item / nslab];
-                c.beg = off[row];
-                c.end = off[row + 1];
-                c.col0 = static_cast<int>(c.item % nslab) * kTmaW;
-                if (c.end > c.beg) {
-                    c.p0 = c.beg;
-                    c.valid = true;
-                    return;
-                }
-                c.item += gridDim.x;
-            }
-        };
-        auto advance = [&](Cursor& c) {
-            c.p0 += kTmaStageNnz;
-            if (c.p0 >= c.end) {
-                c.item += gridDim.x;
-                seek(c);
-            }
-        };
-        auto fetch = [&](const Cursor& c, int64_t fs) {
-            const int64_t n = c.end - c.p0;
-            if (lane < n && lane < kTmaStageNnz) {
-                const int r = static_cast<int>(fs % kTmaRing) * kTmaStageNnz + lane;
-                cp_async4(iring + r, idx + c.p0 + lane);
-                cp_async8(vring + r, val + c.p0 + lane);
-            }
-        };
-        if (lane == 0)
-            asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&xmap)) : "memory");
-        Cursor pf{blockIdx.x, 0, 0, 0, 0, false};
-        seek(pf);
-        Cursor is = pf;
-        int64_t fs_pf = 0, fs = 0;
-        for (int k = 0; k < kTmaPf; ++k) {
-            if (pf.valid) {
-                fetch(pf, fs_pf++);
-                advance(pf);
-            }
-            cp_async_commit();
-        }
-        while (is.valid) {
-            if (pf.valid) {
-                fetch(pf, fs_pf++);
-                advance(pf);
-            }
-            cp_async_commit();
-            cp_async_wait<kTmaPf>();  // indices of stage fs have landed
-            __syncwarp();
-            const int cnt = static_cast<int>(is.end - is.p0 < kTmaStageNnz ? is.end - is.p0 : kTmaStageNnz);
-            const int slot = static_cast<int>(fs % kTmaStages);
-            const unsigned ph = static_cast<unsigned>((fs / kTmaStages) & 1);
-            mbar_wait(&empty[slot], ph ^ 1);
-            // lanes 0..ngather-1 each issue one gather4 (four X rows of the slab).
-            // Index slots past cnt may hold stale values; TMA zero-fills any
-            // out-of-range row and the consumers never read those rows.
-            const int ngather = (cnt + 3) / 4;
-            if (lane == 0)
-                mbar_expect_tx(&full[slot], static_cast<unsigned>(ngather * 4 * kTmaW * sizeof(double)));
-            __syncwarp();
-            if (lane < ngather) {
-                const int4 r = reinterpret_cast<const int4*>(
-                    iring + static_cast<int>(fs % kTmaRing) * kTmaStageNnz)[lane];
-                tma_gather4(data + (static_cast<size_t>(slot) * kTmaStageNnz + 4 * lane) * kTmaW, &xmap,
-                            is.col0, r.x, r.y, r.z, r.w, &full[slot]);
-            }
-            __syncwarp();
-            advance(is);
-            ++fs;
-        }
-        cp_async_wait<0>();
-    } else {
-        const int cw = warp - 1;
-        int64_t fs = 0;
-        for (int64_t item = blockIdx.x; item < items; item += gridDim.x) {
-            const int64_t row = order[item / nslab];
-            const int64_t col = static_cast<int64_t>(item % nslab) * kTmaW + cw * 32 + lane;
-            const int64_t beg = off[row], end = off[row + 1];
-            double acc = 0.0;
-            for (int64_t p0 = beg; p0 < end; p0 += kTmaStageNnz) {
-                const int cnt = static_cast<int>(end - p0 < kTmaStageNnz ? end - p0 : kTmaStageNnz);
-                const int slot = static_cast<int>(fs % kTmaStages);
-                mbar_wait(&full[slot], static_cast<unsigned>((fs / kTmaStages) & 1));
-                const double* d = data + static_cast<size_t>(slot) * kTmaStageNnz * kTmaW + cw * 32 + lane;
-                const double* v = vring + static_cast<int>(fs % kTmaRing) * kTmaStageNnz;
-                if (cnt == kTmaStageNnz) {
-#pragma unroll
-                    for (int j = 0; j < kTmaStageNnz; ++j) acc = fma(v[j], d[j * kTmaW], acc);
-                } else {
-                    for (int j = 0; j < cnt; ++j) acc = fma(v[j], d[j * kTmaW], acc);
-                }
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&empty[slot]);
-                ++fs;
-            }
-            if (col < ld) {
-                if (kShift) {
-                    const double alpha = *alpha_p;
-                    if (alpha != 0.0) acc = fma(-alpha, q[row * ld + col], acc);
-                }
-                y[row * ld + col] = acc;
-            }
-        }
-    }
-}
-
-
-// ---- hub rows, deep cp.async variant --------------------------------------------------
-// One warp per CTA, persistent over (hub row, 32-column slab) items, one lane
-// per column. The warp keeps kDeepDc chunks of 32 nonzeros (kDeepDc*8 KB of
-// gathered X) in flight with cp.async into its own shared-memory ring — about
-// one DRAM latency's worth of bytes at the FMA-chain rate — so a hub row runs
-// at ~8 cycles per nonzero (the DFMA latency of its chain) instead of being
-// bound by per-request TMA or LDG limits. Indices/values are fetched 2*kDeepDc
-// chunks ahead. Bitwise identical to the CSR-order chain.
-constexpr int kDeepDc = 10;                       // gather chunks in flight
-constexpr int kDeepIc = 2 * kDeepDc + 2;          // index/value ring (chunks)
-constexpr size_t kDeepSmem = sizeof(double) * kDeepDc * 32 * 32 +
-                             kDeepIc * 32 * (sizeof(double) + sizeof(int32_t)) + 128;
-
-template <bool kShift>
-__global__ void __launch_bounds__(32)
-spmm_hub_deep_kernel(const int64_t* __restrict__ off, const int32_t* __restrict__ idx,
-                     const double* __restrict__ val, const int32_t* __restrict__ order,
-                     const int32_t* __restrict__ n_hub_p, int nslab, const double* __restrict__ x,
-                     double* __restrict__ y, int64_t ld, const double* __restrict__ q,
-                     const double* __restrict__ alpha_p, const int32_t* __restrict__ gate) {
-    if (gate_closed(gate)) return;
-    extern __shared__ __align__(16) double deep_smem[];
-    double* ring = deep_smem;                                   // [Dc][32 nnz][32 lanes]
-    double* vring = ring + kDeepDc * 32 * 32;                   // [Ic][32]
-    int32_t* iring = reinterpret_cast<int32_t*>(vring + kDeepIc * 32);  // [Ic][32]
-    const int lane = threadIdx.x;
-    const int64_t items = static_cast<int64_t>(*n_hub_p) * nslab;
-
-    // a cursor walks the flat sequence of 32-nonzero chunks of this CTA's items
-    struct Cursor {
-        int64_t item, beg, end, p0;
-        int64_t col;
-        bool valid;
-    };
-    auto seek = [&](Cursor& c) {
-        c.valid = false;
-        while (c.item < items) {
-            const int64_t row = order[c.item / nslab];
-            c.beg = off[row];
-            c.end = off[row + 1];
-            c.col = (c.item % nslab) * 32 + lane;
-            if (c.end > c.beg) {
-                c.p0 = c.beg;
-                c.valid = true;
-                return;
-            }
-            c.item += gridDim.x;
-        }
-    };
-    auto advance = [&](Cursor& c) {
-        c.p0 += 32;
-        if (c.p0 >= c.end) {
-            c.item += gridDim.x;
-            seek(c);
-        }
-    };
-    auto fetch_iv = [&](const Cursor& c, int64_t k) {
-        if (!c.valid) return;
-        const int64_t p = c.p0 + lane;
-        if (p < c.end) {
-            const int r = static_cast<int>(k % kDeepIc) * 32 + lane;
-            cp_async4(iring + r, idx + p);
-            cp_async8(vring + r, val + p);
-        }
-    };
-    auto gather = [&](const Cursor& c, int64_t k) {
-        if (!c.valid || c.col >= ld) return;
-        const int32_t* ib = iring + static_cast<int>(k % kDeepIc) * 32;
-        double* slot = ring + static_cast<int>(k % kDeepDc) * 1024 + lane;
-        const double* xc = x + c.col;
-        const int cnt = static_cast<int>(c.end - c.p0 < 32 ? c.end - c.p0 : 32);
-        if (cnt == 32) {
-#pragma unroll
-            for (int j = 0; j < 32; ++j) cp_async8(slot + j * 32, xc + static_cast<int64_t>(ib[j]) * ld);
-        } else {
-            for (int j = 0; j < cnt; ++j) cp_async8(slot + j * 32, xc + static_cast<int64_t>(ib[j]) * ld);
-        }
-    };
-
-    Cursor ci{blockIdx.x, 0, 0, 0, 0, false};  // index fetch cursor (2*Dc ahead)
-    seek(ci);
-    Cursor cg = ci, cc = ci;                    // gather cursor (Dc-1 ahead), consume cursor
-    int64_t ki = 0, kg = 0, kc = 0;
-    for (int k = 0; k < 2 * kDeepDc; ++k) {
-        fetch_iv(ci, ki++);
-        if (ci.valid) advance(ci);
-    }
-    cp_async_commit();
-    cp_async_wait<0>();
-    __syncwarp();
-    for (int k = 0; k < kDeepDc - 1; ++k) {
-        gather(cg, kg++);
-        if (cg.valid) advance(cg);
-        cp_async_commit();
-    }
-    double acc = 0.0;
-    while (cc.valid) {
-        gather(cg, kg++);
-        if (cg.valid) advance(cg);
-        fetch_iv(ci, ki++);
-        if (ci.valid) advance(ci);
-        cp_async_commit();
-        cp_async_wait<kDeepDc - 1>();  // chunk kc has landed
-        __syncwarp();
-        const double* slot = ring + static_cast<int>(kc % kDeepDc) * 1024 + lane;
-        const double* vb = vring + static_cast<int>(kc % kDeepIc) * 32;
-        const int cnt = static_cast<int>(cc.end - cc.p0 < 32 ? cc.end - cc.p0 : 32);
-        if (cnt == 32) {
-#pragma unroll
-            for (int j = 0; j < 32; ++j) acc = fma(vb[j], slot[j * 32], acc);
-        } else {
-            for (int j = 0; j < cnt; ++j) acc = fma(vb[j], slot[j * 32], acc);
-        }
-        __syncwarp();
-        ++kc;
-        const int64_t row_item = cc.item;
-        const int64_t col = cc.col;
-        const bool last = cc.p0 + 32 >= cc.end;
-        advance(cc);
-        if (last) {  // item finished: write its column
-            if (col < ld) {
-                const int64_t row = order[row_item / nslab];
-                if (kShift) {
-                    const double alpha = *alpha_p;
-                    if (alpha != 0.0) acc = fma(-alpha, q[row * ld + col], acc);
-                }
-                y[row * ld + col] = acc;
-            }
-            acc = 0.0;
-        }
-    }
-    cp_async_wait<0>();
-}
-
-// 2-D tensor map over the row-major X block (rows x ld doubles) with a
-// 64-column x 1-row box: the shape tile::gather4 expects.
-CUtensorMap make_xmap(const double* x, int64_t rows, int64_t ld) {
-    static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
-    if (encode == nullptr) {
-        void* fn = nullptr;
-        cudaDriverEntryPointQueryResult q;
-        DSVD_CUDA_CHECK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
-        if (fn == nullptr || q != cudaDriverEntryPointSuccess)
-            fail(DSVD_CUDA, "cuTensorMapEncodeTiled unavailable");
-        encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
-    }
-    CUtensorMap map;
-    const cuuint64_t dims[2] = {static_cast<cuuint64_t>(ld), static_cast<cuuint64_t>(rows)};
-    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld * sizeof(double))};
-    const cuuint32_t box[2] = {kTmaW, 1};
-    const cuuint32_t estr[2] = {1, 1};
-    const CUresult r = encode(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(x), dims,
-                              strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                              CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS) fail(DSVD_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(r));
-    return map;
-}
-
 __global__ void count_ge_kernel(const int32_t* __restrict__ sorted_desc, int64_t n, int64_t t,
                                 int32_t* out) {
     // number of leading entries >= t in a descending array (binary search)
@@ -1497,8 +1134,8 @@ void spmm(const SpmmArgs& s, cudaStream_t stream, int variant, cudaStream_t side
           cudaEvent_t fork, cudaEvent_t join, double* partial) {
     const DevCsr& a = *s.a;
     if (a.rows == 0) return;
-    // variant bits: low nibble selects the hub kernel; 16 skips the bulk rows,
-    // 32 skips the hub rows (benchmarking the two halves separately)
+    // variant bits: 16 skips the bulk rows, 32 skips the hub rows / chunks
+    // (benchmarking the two halves separately)
     const bool skip_bulk = (variant & 16) != 0, skip_hub = (variant & 32) != 0;
     // bit 1024: the long-row chunks run on the main stream before the bulk rows
     // (serial) instead of beside them on the side stream
@@ -1516,10 +1153,8 @@ void spmm(const SpmmArgs& s, cudaStream_t stream, int variant, cudaStream_t side
     // evict_first hints on the streaming bytes
     const int slab_w = (variant & 4096) ? 32 : (variant & 8192) ? 64 : 0;
     const bool slab_hint = (variant & 16384) != 0;
-    // bits 32768 / 65536: slab gather depth 4 at 24 warps/SM / depth 2 at 40 warps/SM
+    // bits 32768 / 65536: slab gather depth (launch_slab_u)
     const int slab_depth = (variant & 32768) ? 1 : (variant & 65536) ? 2 : 0;
-
-    variant &= 15;
     const bool slab_ok = slab_w > 0 && !skip_bulk && !skip_hub && (a.nsplit == 0 || partial != nullptr);
     if ((s.x_slab || s.y_slab) && !slab_ok)
         fail(DSVD_OTHER, "spmm: slab-major blocks need the column-slab kernel (split mode, slab variant bits)");
@@ -1567,44 +1202,7 @@ void spmm(const SpmmArgs& s, cudaStream_t stream, int variant, cudaStream_t side
         DSVD_CUDA_CHECK(cudaEventRecord(fork, stream));
         DSVD_CUDA_CHECK(cudaStreamWaitEvent(side, fork, 0));
     }
-    if (hub > 0 && !skip_hub && variant == 2) {
-        {  // per launch: the attribute is per device (a process may drive several GPUs)
-            DSVD_CUDA_CHECK(cudaFuncSetAttribute(spmm_hub_deep_kernel<true>,
-                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, kDeepSmem));
-            DSVD_CUDA_CHECK(cudaFuncSetAttribute(spmm_hub_deep_kernel<false>,
-                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, kDeepSmem));
-        }
-        const int nslab32 = static_cast<int>(ceil_div(s.ld, 32));
-        const int64_t items = hub * nslab32;
-        const unsigned blocks = static_cast<unsigned>(items < 2 * kNumSMs ? items : 2 * kNumSMs);
-        if (s.q != nullptr)
-            spmm_hub_deep_kernel<true><<<blocks, 32, kDeepSmem, side>>>(
-                a.off, a.idx, a.val, a.order, a.d_hub_rows, nslab32, s.x, s.y, s.ld, s.q, s.alpha, s.gate);
-        else
-            spmm_hub_deep_kernel<false><<<blocks, 32, kDeepSmem, side>>>(
-                a.off, a.idx, a.val, a.order, a.d_hub_rows, nslab32, s.x, s.y, s.ld, nullptr, nullptr,
-                s.gate);
-        DSVD_LAUNCH_CHECK();
-    } else if (hub > 0 && !skip_hub && variant == 0) {
-        {  // per launch: the attribute is per device (a process may drive several GPUs)
-            DSVD_CUDA_CHECK(cudaFuncSetAttribute(spmm_hub_tma_kernel<true>,
-                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem));
-            DSVD_CUDA_CHECK(cudaFuncSetAttribute(spmm_hub_tma_kernel<false>,
-                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem));
-        }
-        const CUtensorMap xmap = make_xmap(s.x, a.cols, s.ld);
-        const int nslab64 = static_cast<int>(ceil_div(s.ld, kTmaW));
-        const int64_t items = hub * nslab64;
-        const unsigned blocks = static_cast<unsigned>(items < 2 * kNumSMs ? items : 2 * kNumSMs);
-        if (s.q != nullptr)
-            spmm_hub_tma_kernel<true><<<blocks, kTmaThreads, kTmaSmem, side>>>(
-                xmap, a.off, a.idx, a.val, a.order, a.d_hub_rows, nslab64, s.y, s.ld, s.q, s.alpha, s.gate);
-        else
-            spmm_hub_tma_kernel<false><<<blocks, kTmaThreads, kTmaSmem, side>>>(
-                xmap, a.off, a.idx, a.val, a.order, a.d_hub_rows, nslab64, s.y, s.ld, nullptr, nullptr,
-                s.gate);
-        DSVD_LAUNCH_CHECK();
-    } else if (hub > 0 && !skip_hub) {
+    if (hub > 0 && !skip_hub) {
         const int nslab32 = static_cast<int>(ceil_div(s.ld, 32));
         const unsigned blocks = static_cast<unsigned>(ceil_div(hub * nslab32, kHubWarps));
         if (s.q != nullptr)

@@ -292,12 +292,10 @@ def hub_dev():
     dv.close()
 
 
-@pytest.mark.parametrize("variant", [0, 1, 2])  # 0: TMA gather4 ring, 1/2: cp.async rings
 @pytest.mark.parametrize("threshold", [1, 9, 33, 200])
-@pytest.mark.parametrize("l", [1, 31, 75, 150])
-def test_spmm_hub_path_bitwise(hub_dev, oracle, c1, threshold, l, variant):
+@pytest.mark.parametrize("l", [1, 31, 75, 150, 300])
+def test_spmm_hub_path_bitwise(hub_dev, oracle, c1, threshold, l):
     hub_dev.set_option("hub_threshold", threshold)
-    hub_dev.set_option("spmm_variant", variant)
     at = oracle.transpose(c1)
     rng = np.random.default_rng(threshold + l)
     y = np.asfortranarray(rng.standard_normal((c1.rows, l)))
@@ -307,10 +305,8 @@ def test_spmm_hub_path_bitwise(hub_dev, oracle, c1, threshold, l, variant):
     assert_bitwise(d.spmm_shift(to_dev(at), y, 0.37, q, device=hub_dev), t_ref)
 
 
-@pytest.mark.parametrize("variant", [0, 1, 2])
-def test_spmm_hub_power_law_bitwise(hub_dev, oracle, variant):
+def test_spmm_hub_power_law_bitwise(hub_dev, oracle):
     hub_dev.set_option("hub_threshold", 64)
-    hub_dev.set_option("spmm_variant", variant)
     a = d.powerlaw(20000, 3000, 3.5, 1.0, 1.1, 12)
     ca = Csr(a.rows, a.cols, a.offsets, a.col_indices, a.values)
     at = transpose_np(ca)
