@@ -145,6 +145,17 @@ def committed_traffic(config_key):
         return None
 
 
+def gather_ceiling(ld):
+    """The measured random-gather rate the SpMM passes are held against."""
+    if ld > 192:  # the column-slab kernel (64-column slabs, slab-major blocks)
+        return {"ceiling_tbs": 17.7,
+                "ceiling_source": "tools/micro/gather_real.cu: the C4 index stream replayed as 512-byte gathers "
+                                  "from one slab-major 64-column block, no FMAs (profiles/README.md)"}
+    return {"ceiling_tbs": 24.1,
+            "ceiling_source": "tools/micro/gather2.cu: 1 KB Zipf(1.1) row gathers over a 122 MB X, no FMAs, "
+                              "8 loads in flight per warp"}
+
+
 def host_cpu():
     """(model name, logical CPUs usable by this process, physical cores among them)."""
     model, cores = "unknown", set()
@@ -528,9 +539,7 @@ def run_b200(args, rank, world, local_rank):
                      "pass_gbs": pass_gbs,
                      "algorithmic_bytes_per_launch": sp_bytes / max(sp_launch, 1),
                      "gather": {"bytes_per_launch": gather_bytes_pass, "achieved_tbs": gather_tbs,
-                                "ceiling_tbs": 24.1,
-                                "ceiling_source": "tools/micro/gather2.cu: 1 KB Zipf(1.1) row gathers over "
-                                                  "a 122 MB X, no FMAs, 8 loads in flight per warp"}},
+                                **gather_ceiling(ld)}},
         "gpu_launches": int(st0["kernel_launches"]) * args.steps,
         "breakdown_last_step": breakdown,
         "iterations": e2e_res.trace.iterations,
