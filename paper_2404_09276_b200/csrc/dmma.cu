@@ -323,8 +323,10 @@ CUtensorMap make_cmap(const double* c, int64_t rows, int64_t ld) {
 // ---- gram -------------------------------------------------------------------------
 // 1: skip the DMMAs of padding / below-diagonal 8x8 blocks (predicated per warp).
 // Measured on C4: the predicated issue made the wide Gram slower (596 vs 538 ms
-// per solve), so it is off.
+// per solve), so it is off; the wide kernel instead runs per-shape DMMA
+// sequences (kGramShapes).
 constexpr int kGramSkip = 0;
+constexpr int kGramShapes = 1;
 constexpr int kGmRows = 32, kGmStages = 4;
 
 __host__ __device__ constexpr int gm_pairs(int nb) { return nb * (nb + 1) / 2; }
@@ -479,6 +481,28 @@ struct GwKinds {
     int8_t sa0[kGwMaxKinds], sa1[kGwMaxKinds], sb0[kGwMaxKinds], sb1[kGwMaxKinds];
 };
 
+// One stage (kGwRows rows) of a warp's 4x4 tile of 8x8 blocks: fragment loads
+// and the DMMAs of the blocks the tile shape forms (kDiag: u <= v only; NV
+// block columns in range).
+template <bool kDiag, int NV>
+__device__ __forceinline__ void gw_ksteps(const double* C, int q, int g, int ia, int jb, double2 (&acc)[4][4]) {
+#pragma unroll
+    for (int ks = 0; ks < kGwRows / 4; ++ks) {
+        const double* row = C + (4 * ks + q) * kGwStride + g;
+        double fa[4], fb[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+            if (!kDiag || u < NV) fa[u] = row[ia + 8 * u];
+#pragma unroll
+        for (int v = 0; v < NV; ++v) fb[v] = row[jb + 8 * v];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int v = 0; v < NV; ++v)
+                if (!kDiag || u <= v) dmma884(acc[u][v], fa[u], fb[v]);
+    }
+}
+
 __global__ void __launch_bounds__(512, 1)
 gram_dmma_wide_kernel(const double* __restrict__ c, int64_t n, int64_t ld, int nb, int64_t rows_per_block,
                       const GwKinds kinds, double* __restrict__ partial, const int32_t* __restrict__ gate) {
@@ -534,12 +558,12 @@ gram_dmma_wide_kernel(const double* __restrict__ c, int64_t n, int64_t ld, int n
 #pragma unroll
         for (int v = 0; v < 4; ++v) acc[u][v] = make_double2(0.0, 0.0);
     const int ia = 32 * (I - sa0), jb = tri ? 32 * (J - sa0) : 32 * (nA + J - sb0);
-    unsigned live = 0;  // as in gram_dmma_kernel: in-range blocks on or above the diagonal
-#pragma unroll
-    for (int u = 0; u < 4; ++u)
-#pragma unroll
-        for (int v = 0; v < 4; ++v)
-            if (4 * I + u < nb && 4 * J + v < nb && (I != J || u <= v)) live |= 1u << (4 * u + v);
+    // Tile shape of this warp: diagonal tiles form only their 10 blocks on or
+    // above the diagonal, tiles of the last strip only its nv in-range block
+    // columns — separate straight-line DMMA sequences per shape (warp-uniform
+    // branch once per stage), not predicated DMMAs
+    const bool diag = I == J;
+    const int nv = min(4, nb - 4 * J);
     for (int st = 0; st < nst; ++st) {
         cpa_wait<kGwStages - 2>();
         __syncthreads();
@@ -548,20 +572,14 @@ gram_dmma_wide_kernel(const double* __restrict__ c, int64_t n, int64_t ld, int n
         cpa_commit();
         if (!active) continue;
         const double* C = wsm + (st % kGwStages) * kGwRows * kGwStride;
-#pragma unroll
-        for (int ks = 0; ks < kGwRows / 4; ++ks) {
-            const double* row = C + (4 * ks + q) * kGwStride + g;
-            double fa[4], fb[4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) fa[u] = row[ia + 8 * u];
-#pragma unroll
-            for (int v = 0; v < 4; ++v) fb[v] = row[jb + 8 * v];
-#pragma unroll
-            for (int u = 0; u < 4; ++u)
-#pragma unroll
-                for (int v = 0; v < 4; ++v)
-                    if (kGramSkip == 0 || (live & (1u << (4 * u + v)))) dmma884(acc[u][v], fa[u], fb[v]);
-        }
+        if (kGramShapes == 0 || (!diag && nv == 4)) gw_ksteps<false, 4>(C, q, g, ia, jb, acc);
+        else if (diag && nv == 4) gw_ksteps<true, 4>(C, q, g, ia, jb, acc);
+        else if (diag && nv == 3) gw_ksteps<true, 3>(C, q, g, ia, jb, acc);
+        else if (diag && nv == 2) gw_ksteps<true, 2>(C, q, g, ia, jb, acc);
+        else if (diag) gw_ksteps<true, 1>(C, q, g, ia, jb, acc);
+        else if (nv == 3) gw_ksteps<false, 3>(C, q, g, ia, jb, acc);
+        else if (nv == 2) gw_ksteps<false, 2>(C, q, g, ia, jb, acc);
+        else gw_ksteps<false, 1>(C, q, g, ia, jb, acc);
     }
     cpa_wait<0>();
     if (!active) return;
