@@ -373,7 +373,7 @@ def dense_dev(request):
 
 @pytest.mark.parametrize("shape", [(10000, 75), (777, 150), (5000, 300), (40, 3), (200003, 150), (9, 160),
                                    (1000, 8), (1000, 1), (4000, 161), (3001, 257), (2500, 512), (70, 300),
-                                   (300001, 300)])
+                                   (300001, 300), (6000, 312), (3000, 320), (2000, 216), (2000, 184)])
 def test_gram_matches_oracle(dense_dev, oracle, shape):
     c = np.asfortranarray(np.random.default_rng(shape[1]).standard_normal(shape))
     g_ref = oracle.gram(c)
