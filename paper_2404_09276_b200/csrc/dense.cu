@@ -461,8 +461,9 @@ Gram2Plan gram2_plan(int64_t n, int64_t l, int64_t ld) {
     p.lp8 = static_cast<int>((l + 7) / 8 * 8);
     p.ntile = p.lp8 / 8;
     p.npair = p.ntile * (p.ntile + 1) / 2;
-    // 8x8 accumulators take ~165 registers: at most 384 threads per block
-    p.ok = p.npair <= 384 && ld % 2 == 0 && p.lp8 >= ld - 3;
+    // one thread per 8x8 block pair, ~190 registers each: at most 256 threads
+    // per block (the kernel's launch bound; l <= 176)
+    p.ok = p.npair <= 256 && ld % 2 == 0 && p.lp8 >= ld - 3;
     const int64_t target = 2 * kNumSMs;
     int64_t rpb = ceil_div(n, target);
     rpb = std::max<int64_t>(kG2Rows, ceil_div(rpb, kG2Rows) * kG2Rows);
