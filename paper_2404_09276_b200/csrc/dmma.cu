@@ -323,10 +323,8 @@ CUtensorMap make_cmap(const double* c, int64_t rows, int64_t ld) {
 // ---- gram -------------------------------------------------------------------------
 // 1: skip the DMMAs of padding / below-diagonal 8x8 blocks (predicated per warp).
 // Measured on C4: the predicated issue made the wide Gram slower (596 vs 538 ms
-// per solve), so it is off; the wide kernel instead runs per-shape DMMA
-// sequences (kGramShapes).
+// per solve), so it is off.
 constexpr int kGramSkip = 0;
-constexpr int kGramShapes = 1;
 constexpr int kGmRows = 32, kGmStages = 4;
 
 __host__ __device__ constexpr int gm_pairs(int nb) { return nb * (nb + 1) / 2; }
@@ -558,12 +556,9 @@ gram_dmma_wide_kernel(const double* __restrict__ c, int64_t n, int64_t ld, int n
 #pragma unroll
         for (int v = 0; v < 4; ++v) acc[u][v] = make_double2(0.0, 0.0);
     const int ia = 32 * (I - sa0), jb = tri ? 32 * (J - sa0) : 32 * (nA + J - sb0);
-    // Tile shape of this warp: diagonal tiles form only their 10 blocks on or
-    // above the diagonal, tiles of the last strip only its nv in-range block
-    // columns — separate straight-line DMMA sequences per shape (warp-uniform
-    // branch once per stage), not predicated DMMAs
-    const bool diag = I == J;
-    const int nv = min(4, nb - 4 * J);
+    // (Forming only the in-range, on-or-above-diagonal 8x8 blocks of each tile —
+    // predicated DMMAs, or per-shape DMMA sequences — was measured on C4 and did
+    // not shorten the kernel: 553 vs 552 ms per solve.)
     for (int st = 0; st < nst; ++st) {
         cpa_wait<kGwStages - 2>();
         __syncthreads();
@@ -572,14 +567,7 @@ gram_dmma_wide_kernel(const double* __restrict__ c, int64_t n, int64_t ld, int n
         cpa_commit();
         if (!active) continue;
         const double* C = wsm + (st % kGwStages) * kGwRows * kGwStride;
-        if (kGramShapes == 0 || (!diag && nv == 4)) gw_ksteps<false, 4>(C, q, g, ia, jb, acc);
-        else if (diag && nv == 4) gw_ksteps<true, 4>(C, q, g, ia, jb, acc);
-        else if (diag && nv == 3) gw_ksteps<true, 3>(C, q, g, ia, jb, acc);
-        else if (diag && nv == 2) gw_ksteps<true, 2>(C, q, g, ia, jb, acc);
-        else if (diag) gw_ksteps<true, 1>(C, q, g, ia, jb, acc);
-        else if (nv == 3) gw_ksteps<false, 3>(C, q, g, ia, jb, acc);
-        else if (nv == 2) gw_ksteps<false, 2>(C, q, g, ia, jb, acc);
-        else gw_ksteps<false, 1>(C, q, g, ia, jb, acc);
+        gw_ksteps<false, 4>(C, q, g, ia, jb, acc);
     }
     cpa_wait<0>();
     if (!active) return;
