@@ -189,6 +189,33 @@ rescale_dmma_kernel(const double* __restrict__ c, int64_t n, int K, int64_t ldc,
     }
 }
 
+// One 16-deep k chunk of a warp's 16 x 32 tile (2 x NB 8x8 DMMA tiles), the C
+// chunk in the TMA ring's 128-byte-swizzled layout.
+template <int NB>
+__device__ __forceinline__ void rs_ksteps(const double* A, const double* Bt, int ldb, int kc, int warp, int g, int q,
+                                          double2 (&acc)[2][4]) {
+#pragma unroll
+    for (int p = 0; p < 2; ++p) {
+        double2 af[2], bf[4];
+#pragma unroll
+        for (int mb = 0; mb < 2; ++mb) {
+            const int r = warp * 16 + mb * 8 + g;
+            af[mb] = *reinterpret_cast<const double2*>(A + r * kRsBK + (((4 * p + q) ^ (r & 7)) << 1));
+        }
+        const int kg = kc * kRsBK + p * 8 + 2 * q;
+#pragma unroll
+        for (int nb = 0; nb < NB; ++nb) bf[nb] = *reinterpret_cast<const double2*>(Bt + (nb * 8 + g) * ldb + kg);
+#pragma unroll
+        for (int mb = 0; mb < 2; ++mb)
+#pragma unroll
+            for (int nb = 0; nb < NB; ++nb) dmma884(acc[mb][nb], af[mb].x, bf[nb].x);
+#pragma unroll
+        for (int mb = 0; mb < 2; ++mb)
+#pragma unroll
+            for (int nb = 0; nb < NB; ++nb) dmma884(acc[mb][nb], af[mb].y, bf[nb].y);
+    }
+}
+
 // TMA-fed variant: one thread streams the C tiles (128 rows x 16 k, 128-byte
 // swizzle) into a kRsStages ring with mbarriers and bulk-copies the W block;
 // fragment addresses follow the swizzle (16-byte chunk c of row r lives at
@@ -212,6 +239,8 @@ rescale_tma_kernel(const __grid_constant__ CUtensorMap cmap, int64_t n, int K, c
     const int nk = (K + kRsBK - 1) / kRsBK;
     const int64_t nrb = (n + kRsBM - 1) / kRsBM;
     constexpr unsigned kTileBytes = kRsBM * kRsBK * sizeof(double);
+    const int width = out_colmajor ? ncol : static_cast<int>(ld_out);
+    const int nbv = min(4, (width - j0 + 7) / 8);  // 8-column tiles with columns in range
     if (tid == 0) {
         for (int s = 0; s < ST; ++s) bar_init(&full[s], 1);
         bar_init(wbar, 1);
@@ -250,27 +279,11 @@ rescale_tma_kernel(const __grid_constant__ CUtensorMap cmap, int64_t n, int K, c
             const unsigned slot = use % ST;
             bar_wait(&full[slot], (use / ST) & 1);
             const double* A = As + slot * (kRsBM * kRsBK);
-#pragma unroll
-            for (int p = 0; p < 2; ++p) {
-                double2 af[2], bf[4];
-#pragma unroll
-                for (int mb = 0; mb < 2; ++mb) {
-                    const int r = warp * 16 + mb * 8 + g;
-                    af[mb] = *reinterpret_cast<const double2*>(A + r * kRsBK + (((4 * p + q) ^ (r & 7)) << 1));
-                }
-                const int kg = kc * kRsBK + p * 8 + 2 * q;
-#pragma unroll
-                for (int nb = 0; nb < 4; ++nb)
-                    bf[nb] = *reinterpret_cast<const double2*>(Bt + (nb * 8 + g) * ldb + kg);
-#pragma unroll
-                for (int mb = 0; mb < 2; ++mb)
-#pragma unroll
-                    for (int nb = 0; nb < 4; ++nb) dmma884(acc[mb][nb], af[mb].x, bf[nb].x);
-#pragma unroll
-                for (int mb = 0; mb < 2; ++mb)
-#pragma unroll
-                    for (int nb = 0; nb < 4; ++nb) dmma884(acc[mb][nb], af[mb].y, bf[nb].y);
-            }
+            // the last column block forms only its in-range 8-column tiles
+            if (nbv == 4) rs_ksteps<4>(A, Bt, ldb, kc, warp, g, q, acc);
+            else if (nbv == 3) rs_ksteps<3>(A, Bt, ldb, kc, warp, g, q, acc);
+            else if (nbv == 2) rs_ksteps<2>(A, Bt, ldb, kc, warp, g, q, acc);
+            else rs_ksteps<1>(A, Bt, ldb, kc, warp, g, q, acc);
         }
         const int64_t r0 = rb * kRsBM;
 #pragma unroll
