@@ -151,7 +151,10 @@ DSVD_API int dsvd_ctx_trim(dsvd_ctx* ctx);
  * Row-sharded solves: "mgpu_mode" 2 (default: reduce-scatter + slab dense work
  * + all-gather) / 1 (all-reduce of the n x l partials, dense work redundant).
  * Kernels: "spmm_variant", "split_chunk", "split_chunk_t", "split_panel_rows",
- * "hub_threshold", "eig_method", "dense_method". */
+ * "hub_threshold", "eig_method", "dense_method"; column-slab SpMM: "spmm_slab"
+ * (-1 auto / 0 / 32 / 64), "slab_layout", "spmm_slab_hint", "spmm_slab_depth",
+ * "spmm_hot_mb", "uniform_values" (1 default: all-equal values are detected at
+ * build time and not streamed; 0: always streamed). */
 DSVD_API int dsvd_ctx_set_option(dsvd_ctx* ctx, const char* name, int64_t value);
 
 /* Multi-GPU: one process per GPU. Rank 0 calls dsvd_comm_unique_id and

@@ -159,8 +159,9 @@ void build_pair(dsvd_ctx* ctx, CsrAlloc& al, int64_t rows, int64_t cols, int64_t
     a.olen = static_cast<int32_t*>(al.get("a.olen", sizeof(int32_t) * (rows > 0 ? rows : 1)));
     // device scalars read back by the host: {offsets bad, index bad} right away,
     // {hub rows of A, of A^T, chunk total / max of A, of A^T} in one read at the end
-    int32_t* sc = static_cast<int32_t*>(al.get("plan_scalars", sizeof(int32_t) * 12));
-    DSVD_CUDA_CHECK(cudaMemsetAsync(sc, 0, sizeof(int32_t) * 12, st));
+    // (+ [12] values not uniform, [14..15] the first value's bits)
+    int32_t* sc = static_cast<int32_t*>(al.get("plan_scalars", sizeof(int32_t) * 16));
+    DSVD_CUDA_CHECK(cudaMemsetAsync(sc, 0, sizeof(int32_t) * 16, st));
     check_offsets(a.off, rows, nnz, sc, st);
     count_launch();
     narrow_indices(d_idx64, a.idx, nnz, cols, sc + 1, st);
@@ -189,6 +190,10 @@ void build_pair(dsvd_ctx* ctx, CsrAlloc& al, int64_t rows, int64_t cols, int64_t
     count_launch(nnz > 0 ? 8 : 1);  // 4 own kernels + CUB radix sort passes (estimate)
     // split mode: the "hub" prefix of the row order is the set of rows longer
     // than split_chunk, which are cut into chunks below
+    if (ctx->uniform_values) {  // a.val is complete on st once the transpose has gathered it
+        check_uniform_values(a.val, nnz, sc + 12, reinterpret_cast<double*>(sc + 14), st);
+        count_launch(nnz > 0);
+    }
     const int64_t C = ctx->split_chunk;
     // the transpose (pass 2) may split shorter rows than A (split_chunk_t)
     const int64_t Ct = C > 0 && ctx->split_chunk_t > 0 ? ctx->split_chunk_t : C;
@@ -213,9 +218,12 @@ void build_pair(dsvd_ctx* ctx, CsrAlloc& al, int64_t rows, int64_t cols, int64_t
         plan_chunks_count(ctx, al, a, "a", 0, sc + 4, cpa);
         plan_chunks_count(ctx, al, at, "at", ctx->split_panel_rows, sc + 6, cpt);
     }
-    int32_t h[12];
+    int32_t h[16];
     DSVD_CUDA_CHECK(cudaMemcpyAsync(h, sc, sizeof(h), cudaMemcpyDeviceToHost, st));
     DSVD_CUDA_CHECK(cudaStreamSynchronize(st));
+    a.uniform = at.uniform = ctx->uniform_values && nnz > 0 && h[12] == 0;
+    std::memcpy(&a.uval, h + 14, sizeof(double));
+    at.uval = a.uval;
     a.nonempty_rows = rows > 0 ? h[8] : 0;
     at.nonempty_rows = cols > 0 ? h[9] : 0;
     a.long_rows = rows > 0 ? h[10] : 0;
@@ -1209,6 +1217,11 @@ int dsvd_ctx_set_option(dsvd_ctx* ctx, const char* name, int64_t value) {
         } else if (n == "slab_layout") {
             if (value < 0 || value > 1) fail(DSVD_CONFIG, "slab_layout must be 0 or 1");
             ctx->slab_layout = static_cast<int>(value);
+        } else if (n == "uniform_values") {
+            // 1: detect all-equal values at build time (the column-slab kernel then
+            // skips the value stream), 0: always stream the values
+            if (value < 0 || value > 1) fail(DSVD_CONFIG, "uniform_values must be 0 or 1");
+            ctx->uniform_values = static_cast<int>(value);
         } else if (n == "spmm_hot_mb") {
             if (value < 0) fail(DSVD_CONFIG, "spmm_hot_mb must be >= 0");
             ctx->spmm_hot_mb = value;

@@ -61,6 +61,7 @@ struct dsvd_ctx {
     // column-slab kernel: hot X rows (as many as fit in spmm_hot_mb MB of slab
     // rows) gathered with L2 evict_last, the rest evict_first; 0 MB = off
     int64_t spmm_hot_mb = 96;
+    int uniform_values = 1;  // detect all-equal values (DevCsr::uniform)
     int spmm_slab_depth = 2;  // gather depth / occupancy variant (sparse.cu launch_slab_u): 2 in flight, 32 warps
     // with the column-slab kernel, keep the gathered blocks slab-major (the
     // sketch and A Q written so, the pass-1 operand converted once per pass)

@@ -428,7 +428,8 @@ spmm_slab_kernel(const int64_t* __restrict__ off, const int32_t* __restrict__ id
                  int64_t blocks_per_slab, const double* __restrict__ x, double* __restrict__ y,
                  double* __restrict__ partial, int64_t ld, const double* __restrict__ q,
                  const double* __restrict__ alpha_p, const int32_t* __restrict__ gate, int64_t x_rows, bool x_slab,
-                 bool y_slab, int64_t active, const int64_t* __restrict__ obeg, const int32_t* __restrict__ olen) {
+                 bool y_slab, int64_t active, const int64_t* __restrict__ obeg, const int32_t* __restrict__ olen,
+                 bool uni, double uval) {
     constexpr int G = SlabCfg<W>::G, R = SlabCfg<W>::R;
     if (gate_closed(gate)) return;
     __shared__ __align__(16) double2 cv[kSlabWarps][R][2 * (G + 1)];  // two batches; +1: groups on distinct banks
@@ -495,16 +496,17 @@ spmm_slab_kernel(const int64_t* __restrict__ off, const int32_t* __restrict__ id
     };
     int cb = 0;
     double vb = 0.0;
+    // (uni: every value is uval, the value stream is not read)
     if (t < len) {
         cb = ld_idx<kHint>(idx + beg + t, pol);
-        vb = ld_val<kHint>(val + beg + t, pol);
+        vb = uni ? uval : ld_val<kHint>(val + beg + t, pol);
     }
     ring[t] = make_double2(vb, __longlong_as_double(static_cast<long long>(cb)));  // batch 0
     cb = 0;
     vb = 0.0;
     if (G + t < len) {  // batch 1, staged when batch 0 starts
         cb = ld_idx<kHint>(idx + beg + G + t, pol);
-        vb = ld_val<kHint>(val + beg + G + t, pol);
+        vb = uni ? uval : ld_val<kHint>(val + beg + G + t, pol);
     }
     __syncwarp();
     double xa[U][4], va[U];
@@ -527,7 +529,7 @@ spmm_slab_kernel(const int64_t* __restrict__ off, const int32_t* __restrict__ id
             vb = 0.0;
             if ((b + 2) * G + t < len) {
                 cb = ld_idx<kHint>(idx + beg + (b + 2) * G + t, pol);
-                vb = ld_val<kHint>(val + beg + (b + 2) * G + t, pol);
+                vb = uni ? uval : ld_val<kHint>(val + beg + (b + 2) * G + t, pol);
             }
         }
 #pragma unroll
@@ -1074,11 +1076,11 @@ void launch_slab_range(const SpmmArgs& s, cudaStream_t stream, double* partial, 
     if (s.q != nullptr)
         spmm_slab_kernel<true, W, U, kHint, MB, kTag><<<blocks, 32 * kSlabWarps, 0, stream>>>(
             a.off, ix, a.val, a.order, first, nchunks, a.chunk_p0, a.chunk_p1, a.rows, bps, s.x, s.y, partial,
-            s.ld, s.q, s.alpha, s.gate, a.cols, s.x_slab, s.y_slab, end, a.obeg, a.olen);
+            s.ld, s.q, s.alpha, s.gate, a.cols, s.x_slab, s.y_slab, end, a.obeg, a.olen, a.uniform, a.uval);
     else
         spmm_slab_kernel<false, W, U, kHint, MB, kTag><<<blocks, 32 * kSlabWarps, 0, stream>>>(
             a.off, ix, a.val, a.order, first, nchunks, a.chunk_p0, a.chunk_p1, a.rows, bps, s.x, s.y, partial,
-            s.ld, nullptr, nullptr, s.gate, a.cols, s.x_slab, s.y_slab, end, a.obeg, a.olen);
+            s.ld, nullptr, nullptr, s.gate, a.cols, s.x_slab, s.y_slab, end, a.obeg, a.olen, a.uniform, a.uval);
     DSVD_LAUNCH_CHECK();
 }
 
@@ -1407,6 +1409,26 @@ void narrow_indices(const int64_t* src, int32_t* dst, int64_t nnz, int64_t cols,
 void widen_indices(const int32_t* src, int64_t* dst, int64_t nnz, cudaStream_t stream) {
     if (nnz == 0) return;
     widen_kernel<<<grid_for(nnz), 256, 0, stream>>>(src, dst, nnz);
+    DSVD_LAUNCH_CHECK();
+}
+
+namespace {
+__global__ void uniform_values_kernel(const double* __restrict__ val, int64_t nnz, int32_t* nonuniform,
+                                      double* first) {
+    const long long v0 = __double_as_longlong(val[0]);
+    if (blockIdx.x == 0 && threadIdx.x == 0) *first = val[0];
+    bool diff = false;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < nnz;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        diff |= __double_as_longlong(__ldg(val + i)) != v0;
+    if (__any_sync(kFull, diff) && (threadIdx.x & 31) == 0) *nonuniform = 1;
+}
+}  // namespace
+
+void check_uniform_values(const double* val, int64_t nnz, int32_t* nonuniform, double* first,
+                          cudaStream_t stream) {
+    if (nnz == 0) return;
+    uniform_values_kernel<<<grid_for(nnz), 256, 0, stream>>>(val, nnz, nonuniform, first);
     DSVD_LAUNCH_CHECK();
 }
 

@@ -21,6 +21,12 @@ struct DevCsr {
     int64_t* obeg = nullptr;
     int32_t* olen = nullptr;
     int64_t max_row_nnz = 0;
+    // every stored value has the bits of uval (e.g. an unweighted graph's 1.0):
+    // the column-slab kernel then multiplies by uval instead of streaming the
+    // values; fma(uval, x, acc) is the same operation on the same operands, so
+    // the chains are bitwise unchanged (set at build time from a device scan)
+    bool uniform = false;
+    double uval = 0.0;
     // rows order[0 .. hub_rows) hold >= hub_threshold nonzeros and take the
     // deep-pipelined hub path of spmm (counted on the device at build time)
     int64_t hub_rows = 0;
@@ -142,6 +148,9 @@ void build_row_order(DevCsr& m, void* scratch, size_t scratch_bytes, cudaStream_
 void narrow_indices(const int64_t* src, int32_t* dst, int64_t nnz, int64_t cols, int32_t* bad,
                     cudaStream_t stream);
 void widen_indices(const int32_t* src, int64_t* dst, int64_t nnz, cudaStream_t stream);
+// *nonuniform = 1 unless all nnz values have the bits of val[0]; *first = val[0]
+void check_uniform_values(const double* val, int64_t nnz, int32_t* nonuniform, double* first,
+                          cudaStream_t stream);
 // Offset checks: off[0] == 0, off[rows] == nnz, non-decreasing -> *bad = 1 otherwise.
 void check_offsets(const int64_t* off, int64_t rows, int64_t nnz, int32_t* bad,
                    cudaStream_t stream);

@@ -207,6 +207,56 @@ def test_solve_slab_layouts_are_bitwise_the_whole_row_solve(slab, layout, pipeli
         base.close()
 
 
+@pytest.mark.parametrize("value", [1.0, -0.37, 0.0, None])
+@pytest.mark.parametrize("slab", [32, 64])
+def test_slab_kernel_uniform_values_bitwise(value, slab):
+    """All-equal values (an unweighted graph's 1.0): the column-slab kernel
+    multiplies by the one value instead of streaming them (uniform_values 1)
+    and must match the value-streaming kernel and the whole-row kernels bitwise,
+    with and without the fused shift; value None: one entry differs, so the
+    detection must fall back to the stream."""
+    a = d.powerlaw(7000, 2600, 3.5, 1.0, 1.1, 29)
+    vals = np.full(a.nnz, 1.0 if value is None else value)
+    if value is None:
+        vals[a.nnz // 2] = 2.0
+    ca = Csr(a.rows, a.cols, a.offsets, a.col_indices, vals)
+    at = transpose_np(ca)
+    devs = [d.Device(0) for _ in range(3)]
+    devs[0].set_option("spmm_slab", 0)
+    for dv, uni in ((devs[1], 0), (devs[2], 1)):
+        dv.set_option("spmm_variant", 4096 if slab == 32 else 8192)
+        dv.set_option("uniform_values", uni)
+    rng = np.random.default_rng(slab)
+    for l in (75, 300):
+        for m, x in ((ca, rng.standard_normal((ca.cols, l))), (at, rng.standard_normal((ca.rows, l)))):
+            x = np.asfortranarray(x)
+            q = np.asfortranarray(rng.standard_normal((m.rows, l)))
+            ref = d.spmm(to_dev(m), x, device=devs[1])
+            refs = d.spmm_shift(to_dev(m), x, 0.3, q, device=devs[1])
+            assert_bitwise(d.spmm(to_dev(m), x, device=devs[0]), ref)
+            assert_bitwise(d.spmm(to_dev(m), x, device=devs[2]), ref)
+            assert_bitwise(d.spmm_shift(to_dev(m), x, 0.3, q, device=devs[2]), refs)
+    for dv in devs:
+        dv.close()
+
+
+def test_solve_uniform_values_is_bitwise_the_streaming_solve():
+    a = d.powerlaw(9000, 4000, 3.5, 1.0, 1.1, 7)
+    a = d.SparseMatrix(a.rows, a.cols, a.offsets, a.col_indices, np.ones(a.nnz))
+    cfg = d.SolverConfig(k=200, s=100, p=3, alg=d.Algorithm.shifted, seed=2)
+    base, dv = d.Device(0), d.Device(0)
+    base.set_option("uniform_values", 0)
+    for x in (base, dv):
+        x.set_option("spmm_slab", 64)
+    r0 = d.solve(a, cfg, device=base)
+    r1 = d.solve(a, cfg, device=dv)
+    assert_bitwise(r1.svd.s, r0.svd.s)
+    assert_bitwise(r1.svd.u, r0.svd.u)
+    assert_bitwise(r1.svd.v, r0.svd.v)
+    dv.close()
+    base.close()
+
+
 def test_spmm_transpose_pass_bitwise(dev, oracle, c1):
     at = oracle.transpose(c1)
     y = np.asfortranarray(np.random.default_rng(3).standard_normal((c1.rows, 75)))
