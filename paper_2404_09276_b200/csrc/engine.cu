@@ -1229,7 +1229,7 @@ int dsvd_ctx_set_option(dsvd_ctx* ctx, const char* name, int64_t value) {
             if (value < 0 || value > 2) fail(DSVD_CONFIG, "spmm_slab_depth must be 0, 1 or 2");
             ctx->spmm_slab_depth = static_cast<int>(value);
         } else if (n == "spmm_slab_hint") {
-            if (value < 0 || value > 1) fail(DSVD_CONFIG, "spmm_slab_hint must be 0 or 1");
+            if (value < 0 || value > 2) fail(DSVD_CONFIG, "spmm_slab_hint: 0 off, 1 every launch, 2 A X pass only");
             ctx->spmm_slab_hint = static_cast<int>(value);
         } else if (n == "hub_threshold") {
             ctx->hub_threshold = value;

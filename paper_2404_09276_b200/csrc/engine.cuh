@@ -56,11 +56,14 @@ struct dsvd_ctx {
     int spmm_variant = 0;
     // column-slab SpMM (sparse.cu spmm_slab_kernel): -1 auto by width, 0 off,
     // 32 / 64 columns per slab; spmm_slab_hint: L2 evict_first on streaming bytes
+    // (1: every launch, 2: only the A X pass that writes a slab-major Y — the A^T
+    // pass is faster without it on C4)
     int spmm_slab = -1;
-    int spmm_slab_hint = 1;
+    int spmm_slab_hint = 2;
     // column-slab kernel: hot X rows (as many as fit in spmm_hot_mb MB of slab
-    // rows) gathered with L2 evict_last, the rest evict_first; 0 MB = off
-    int64_t spmm_hot_mb = 96;
+    // rows) gathered with L2 evict_last, the rest evict_first; 0 MB = off (default:
+    // measured slower on C4 since the kernel's other changes)
+    int64_t spmm_hot_mb = 0;
     int uniform_values = 1;  // detect all-equal values (DevCsr::uniform)
     int spmm_slab_depth = 2;  // gather depth / occupancy variant (sparse.cu launch_slab_u): 2 in flight, 32 warps
     // with the column-slab kernel, keep the gathered blocks slab-major (the
@@ -183,6 +186,7 @@ inline int spmm_var(const dsvd_ctx* ctx, int64_t ld) {
     if (w == 32) v |= 4096;
     else if (w == 64) v |= 8192;
     if (w > 0 && ctx->spmm_slab_hint) v |= 16384;
+    if (w > 0 && ctx->spmm_slab_hint == 2) v |= 131072;
     if (w > 0 && ctx->spmm_slab_depth == 1) v |= 32768;
     if (w > 0 && ctx->spmm_slab_depth == 2) v |= 65536;
     return v;

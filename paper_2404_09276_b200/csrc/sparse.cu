@@ -1154,7 +1154,8 @@ void spmm(const SpmmArgs& s, cudaStream_t stream, int variant, cudaStream_t side
     // bulk rows AND the split chunks (one launch, slab-major); 16384: its L2
     // evict_first hints on the streaming bytes
     const int slab_w = (variant & 4096) ? 32 : (variant & 8192) ? 64 : 0;
-    const bool slab_hint = (variant & 16384) != 0;
+    // bit 131072: the hint only on launches that write a slab-major Y (the A X pass)
+    const bool slab_hint = (variant & 16384) != 0 && (!(variant & 131072) || s.y_slab);
     // bits 32768 / 65536: slab gather depth (launch_slab_u)
     const int slab_depth = (variant & 32768) ? 1 : (variant & 65536) ? 2 : 0;
     const bool slab_ok = slab_w > 0 && !skip_bulk && !skip_hub && (a.nsplit == 0 || partial != nullptr);

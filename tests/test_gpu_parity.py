@@ -240,6 +240,27 @@ def test_slab_kernel_uniform_values_bitwise(value, slab):
         dv.close()
 
 
+@pytest.mark.parametrize("hot_mb", [0, 1])
+@pytest.mark.parametrize("hint", [0, 1, 2])
+def test_solve_slab_l2_policies_are_bitwise_the_whole_row_solve(hot_mb, hint):
+    """The slab kernel's L2 policies (hot/cold-tagged gathers, evict_first on the
+    streaming bytes of every launch or of the A X pass only) change no bits."""
+    a = d.powerlaw(9000, 4000, 3.5, 1.0, 1.1, 8)
+    cfg = d.SolverConfig(k=200, s=100, p=2, alg=d.Algorithm.shifted, seed=3)
+    base, dv = d.Device(0), d.Device(0)
+    base.set_option("spmm_slab", 0)
+    dv.set_option("spmm_slab", 64)
+    dv.set_option("spmm_hot_mb", hot_mb)
+    dv.set_option("spmm_slab_hint", hint)
+    r0 = d.solve(a, cfg, device=base)
+    r1 = d.solve(a, cfg, device=dv)
+    assert_bitwise(r1.svd.s, r0.svd.s)
+    assert_bitwise(r1.svd.u, r0.svd.u)
+    assert_bitwise(r1.svd.v, r0.svd.v)
+    dv.close()
+    base.close()
+
+
 def test_solve_uniform_values_is_bitwise_the_streaming_solve():
     a = d.powerlaw(9000, 4000, 3.5, 1.0, 1.1, 7)
     a = d.SparseMatrix(a.rows, a.cols, a.offsets, a.col_indices, np.ones(a.nnz))
