@@ -309,9 +309,13 @@ def run_reference_arm(args, rank, world):
               f"(input built in {t_gen:.1f} s by oracle/inputs_gen.c, untimed); host {model}, {threads} threads "
               f"on {physical} physical cores ({logical} logical), OMP_PROC_BIND={os.environ['OMP_PROC_BIND']} "
               f"OMP_PLACES={os.environ['OMP_PLACES']}")
+    # steps / warmup: what ran (each step one bounded sample, no warm-up sample:
+    # the reference has no device state to warm); the requested counts beside them
     line = {"metric": METRIC, "value": value, "unit": "s",
-            "impl": "reference", "n_gpus": args.gpus, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": value * 1e3, "higher_is_better": False,
+            "impl": "reference", "n_gpus": args.gpus, "steps": len(samples),
+            "warmup": 0, "requested": {"steps": args.steps, "warmup": args.warmup},
+            "value_kind": "full-workload seconds extrapolated from a bounded sample (cpu_baseline.sample)",
+            "ms_per_step": value * 1e3, "higher_is_better": False,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": f"synthetic (seeded generator, BASELINE.json configs[{cfg['baseline_index']}] shape; no dataset)",
             "config": config_dict(cfg, a.nnz, world),
