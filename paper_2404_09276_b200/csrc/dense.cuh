@@ -42,6 +42,9 @@ void rescale(const double* c, int64_t n, int64_t K, int64_t ldc, const double* w
 // gram / rescale (rescale's scale folded into W), summation order not the
 // reference's FMA chain. Workspace from the *_workspace_bytes functions.
 bool gram_dmma_supported(int64_t l, int64_t ld);
+// tile shape of the wide (l > 160) DMMA Gram: 2 (2x2 blocks of 8x8, default) or 4
+// (4x4); process-wide, for A/B runs (option "gram_tiles")
+void set_gram_wide_tiles(int t);
 size_t gram_dmma_workspace_bytes(int64_t n, int64_t l);
 void gram_dmma(const double* c, int64_t n, int64_t l, int64_t ld, double* g, void* ws, const int32_t* gate,
                cudaStream_t stream);

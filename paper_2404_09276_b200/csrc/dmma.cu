@@ -595,6 +595,131 @@ gram_dmma_wide_kernel(const double* __restrict__ c, int64_t n, int64_t ld, int n
         }
 }
 
+// Wide Gram, 2x2 tiles: the same kinds-of-CTA scheme as gram_dmma_wide_kernel,
+// but over 16-column tiles of 2x2 8x8 blocks, up to four tiles per warp
+// (tiles w, w + 16, w + 32, w + 48 of the kind). At l = 300 (38 blocks, 19 tiles)
+// the 190 tiles on and above the diagonal issue 741 block products per k-step,
+// every one of them useful (the 4x4 tiles issue 880: 320-column padding and the
+// lower halves of the diagonal tiles). Kind encoding as GwKinds, in tile units.
+constexpr int kGw2Tiles = 4;  // tiles per warp
+
+// One stage (kGwRows rows) of a warp's NT 2x2 tiles: per k-step four fragment
+// loads and four DMMAs per tile
+template <int NT>
+__device__ __forceinline__ void gw2_ksteps(const double* C, int q, int g, const int (&ia)[kGw2Tiles],
+                                           const int (&jb)[kGw2Tiles], double2 (&acc)[kGw2Tiles][2][2]) {
+#pragma unroll 2
+    for (int ks = 0; ks < kGwRows / 4; ++ks) {
+        const double* row = C + (4 * ks + q) * kGwStride + g;
+#pragma unroll
+        for (int s = 0; s < NT; ++s) {
+            const double fa0 = row[ia[s]], fa1 = row[ia[s] + 8];
+            const double fb0 = row[jb[s]], fb1 = row[jb[s] + 8];
+            dmma884(acc[s][0][0], fa0, fb0);
+            dmma884(acc[s][1][0], fa1, fb0);
+            dmma884(acc[s][0][1], fa0, fb1);
+            dmma884(acc[s][1][1], fa1, fb1);
+        }
+    }
+}
+
+__global__ void __launch_bounds__(512, 1)
+gram_dmma_wide2_kernel(const double* __restrict__ c, int64_t n, int64_t ld, int nb, int64_t rows_per_block,
+                       const GwKinds kinds, double* __restrict__ partial, const int32_t* __restrict__ gate) {
+    if (gate != nullptr && *gate != 0) return;
+    extern __shared__ __align__(16) double wsm[];  // [stages][kGwRows][kGwStride]
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int q = lane & 3, g = lane >> 2;
+    const int kd = blockIdx.x;
+    const int a0 = kinds.sa0[kd], nA = kinds.sa1[kd] - a0, b0 = kinds.sb0[kd], nB = kinds.sb1[kd] - b0;
+    const bool tri = nB == 0;
+    const int ntile = tri ? nA * (nA + 1) / 2 : nA * nB;
+    // this warp's tiles: global tile coordinates, staged column offsets
+    int ia[kGw2Tiles], jb[kGw2Tiles], ti[kGw2Tiles], tj[kGw2Tiles];
+    bool has[kGw2Tiles];
+#pragma unroll
+    for (int s = 0; s < kGw2Tiles; ++s) {
+        const int t = warp + 16 * s;
+        has[s] = t < ntile;
+        int i = 0, j = 0;
+        if (tri) {
+            int r = t;
+            while (i < nA && r >= nA - i) {
+                r -= nA - i;
+                ++i;
+            }
+            j = i + r;
+        } else {
+            i = t / max(nB, 1);
+            j = t % max(nB, 1);
+        }
+        if (!has[s]) i = j = 0;  // (an absent slot before the last would compute tile (0, 0) unused)
+        ti[s] = a0 + i;
+        tj[s] = tri ? a0 + j : b0 + j;
+        ia[s] = 16 * i;
+        jb[s] = tri ? 16 * j : 16 * (nA + j);
+    }
+    const int ntw = (ntile > warp) ? min(kGw2Tiles, (ntile - warp + 15) / 16) : 0;  // tiles of this warp
+    const int64_t r_beg = static_cast<int64_t>(blockIdx.y) * rows_per_block;
+    const int64_t r_end = min(n, r_beg + rows_per_block);
+    // staging as gram_dmma_wide_kernel: 32 rows x up to 128 16-byte chunks
+    const int ch = tid & 127, r0t = tid >> 7;
+    const int64_t col = ch < 8 * nA ? 16 * a0 + 2 * ch : 16 * b0 + 2 * (ch - 8 * nA);
+    const bool col_ok = ch < 8 * (nA + nB) && col < ld;
+    const double* src0 = c + (col_ok ? col : 0);
+    double* dst0 = wsm + r0t * kGwStride + 2 * ch;
+    auto stage = [&](int slot, int64_t rr0) {
+        double* dst = dst0 + slot * kGwRows * kGwStride;
+#pragma unroll
+        for (int u = 0; u < kGwRows / 4; ++u) {
+            const int64_t gr = rr0 + r0t + 4 * u;
+            const bool ok = col_ok && gr < r_end;
+            cpa16z(dst + 4 * u * kGwStride, ok ? src0 + gr * ld : c, ok);
+        }
+    };
+    const int nst = static_cast<int>(((r_end > r_beg ? r_end - r_beg : int64_t(0)) + kGwRows - 1) / kGwRows);
+    for (int st = 0; st < kGwStages - 1; ++st) {
+        if (st < nst) stage(st, r_beg + st * kGwRows);
+        cpa_commit();
+    }
+    double2 acc[kGw2Tiles][2][2];
+#pragma unroll
+    for (int s = 0; s < kGw2Tiles; ++s)
+#pragma unroll
+        for (int u = 0; u < 2; ++u)
+#pragma unroll
+            for (int v = 0; v < 2; ++v) acc[s][u][v] = make_double2(0.0, 0.0);
+    for (int st = 0; st < nst; ++st) {
+        cpa_wait<kGwStages - 2>();
+        __syncthreads();
+        const int pf = st + kGwStages - 1;
+        if (pf < nst) stage(pf % kGwStages, r_beg + static_cast<int64_t>(pf) * kGwRows);
+        cpa_commit();
+        const double* C = wsm + (st % kGwStages) * kGwRows * kGwStride;
+        // every tile forms its four block products (a diagonal tile's lower
+        // block, 19 of 760 at l = 300, is not stored); one warp-uniform branch
+        // per stage on the warp's tile count
+        if (ntw == 4) gw2_ksteps<4>(C, q, g, ia, jb, acc);
+        else if (ntw == 3) gw2_ksteps<3>(C, q, g, ia, jb, acc);
+        else if (ntw == 2) gw2_ksteps<2>(C, q, g, ia, jb, acc);
+        else if (ntw == 1) gw2_ksteps<1>(C, q, g, ia, jb, acc);
+    }
+    cpa_wait<0>();
+    double* out = partial + static_cast<int64_t>(blockIdx.y) * gm_pairs(nb) * 64;
+#pragma unroll
+    for (int s = 0; s < kGw2Tiles; ++s) {
+        if (!has[s]) continue;
+#pragma unroll
+        for (int u = 0; u < 2; ++u)
+#pragma unroll
+            for (int v = 0; v < 2; ++v) {
+                const int bi = 2 * ti[s] + u, bj = 2 * tj[s] + v;
+                if (bi <= bj && bj < nb)
+                    *reinterpret_cast<double2*>(out + gm_tri(bi, bj, nb) * 64 + g * 8 + 2 * q) = acc[s][u][v];
+            }
+    }
+}
+
 template <int NB4>
 void launch_gram_dmma(const double* c, int64_t n, int64_t ld, int nb, int nblk, int64_t rpb, double* partial,
                       const int32_t* gate, cudaStream_t stream) {
@@ -631,6 +756,26 @@ GwPlan gw_kinds(int ns) {
     for (int b0 = h; b0 < ns; b0 += cw) add(0, h, b0, std::min(ns, b0 + cw));
     return p;
 }
+// CTA kinds of gram_dmma_wide2_kernel for nt 16-column tiles (nt <= 20): the
+// two half triangles and the rectangle between them in pieces of at most 64
+// tiles whose staged columns fit 256
+GwPlan gw2_kinds(int nt) {
+    GwPlan p;
+    auto add = [&](int a0, int a1, int b0, int b1) {
+        p.k.sa0[p.n] = static_cast<int8_t>(a0);
+        p.k.sa1[p.n] = static_cast<int8_t>(a1);
+        p.k.sb0[p.n] = static_cast<int8_t>(b0);
+        p.k.sb1[p.n] = static_cast<int8_t>(b1);
+        ++p.n;
+    };
+    const int h = (nt + 1) / 2;
+    add(0, h, 0, 0);
+    if (nt > h) add(h, nt, h, h);
+    const int cw = std::max(1, std::min(16 * kGw2Tiles / h, 16 - h));
+    for (int b0 = h; b0 < nt; b0 += cw) add(0, h, b0, std::min(nt, b0 + cw));
+    return p;
+}
+int gram_wide_tiles = 2;  // 2: gram_dmma_wide2_kernel (default), 4: gram_dmma_wide_kernel
 constexpr int kGramNarrowMaxNb = 20;  // gram_dmma_kernel<NB4 <= 5>: l <= 160
 constexpr int kGramWideMaxNb = 40;    // gram_dmma_wide_kernel: l <= 320 (<= 10 strips)
 
@@ -639,7 +784,7 @@ GramDmmaPlan gram_dmma_plan(int64_t n, int64_t l) {
     p.nb = static_cast<int>((l + 7) / 8);
     if (p.nb > kGramNarrowMaxNb) {
         // wide: kinds x slabs, ~6 waves of one CTA per SM
-        const int nkinds = gw_kinds((p.nb + 3) / 4).n;
+        const int nkinds = gram_wide_tiles == 2 ? gw2_kinds((p.nb + 1) / 2).n : gw_kinds((p.nb + 3) / 4).n;
         p.nblk = static_cast<int>(std::max<int64_t>(
             1, std::min<int64_t>(ceil_div(6 * kNumSMs, nkinds), ceil_div(n, 8 * kGwRows))));
         p.rpb = ceil_div(ceil_div(n, p.nblk), kGwRows) * kGwRows;
@@ -656,6 +801,8 @@ GramDmmaPlan gram_dmma_plan(int64_t n, int64_t l) {
 
 }  // namespace
 
+void set_gram_wide_tiles(int t) { gram_wide_tiles = t == 4 ? 4 : 2; }
+
 bool gram_dmma_supported(int64_t l, int64_t ld) {
     return l >= 1 && (l + 7) / 8 <= kGramWideMaxNb && ld % 2 == 0 && ld >= l;
 }
@@ -670,12 +817,13 @@ void gram_dmma(const double* c, int64_t n, int64_t l, int64_t ld, double* g, voi
     const GramDmmaPlan p = gram_dmma_plan(n, l);
     double* partial = static_cast<double*>(ws);
     if (p.nb > kGramNarrowMaxNb) {
-        const GwPlan kp = gw_kinds((p.nb + 3) / 4);
+        const bool t2 = gram_wide_tiles == 2;
+        const GwPlan kp = t2 ? gw2_kinds((p.nb + 1) / 2) : gw_kinds((p.nb + 3) / 4);
         const size_t smem = sizeof(double) * kGwStages * kGwRows * kGwStride;
-        DSVD_CUDA_CHECK(cudaFuncSetAttribute(gram_dmma_wide_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             static_cast<int>(smem)));
+        auto kern = t2 ? gram_dmma_wide2_kernel : gram_dmma_wide_kernel;
+        DSVD_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
         const dim3 grid(static_cast<unsigned>(kp.n), static_cast<unsigned>(p.nblk));
-        gram_dmma_wide_kernel<<<grid, 512, smem, stream>>>(c, n, ld, p.nb, p.rpb, kp.k, partial, gate);
+        kern<<<grid, 512, smem, stream>>>(c, n, ld, p.nb, p.rpb, kp.k, partial, gate);
         DSVD_LAUNCH_CHECK();
         gram_dmma_reduce_kernel<<<gm_pairs(p.nb), 256, 0, stream>>>(partial, p.nblk, p.nb, l, g, gate);
         DSVD_LAUNCH_CHECK();

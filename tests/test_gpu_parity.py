@@ -453,6 +453,26 @@ def test_gram_matches_oracle(dense_dev, oracle, shape):
     np.testing.assert_allclose(g, g_ref, rtol=1e-13, atol=1e-13 * np.abs(g_ref).max())
 
 
+@pytest.mark.parametrize("shape", [(5000, 300), (70, 300), (300001, 300), (6000, 312), (3000, 320),
+                                   (2000, 216), (2000, 184), (4000, 161), (3001, 257), (1000, 170)])
+def test_wide_gram_tile_shapes_are_bitwise_equal(oracle, shape):
+    """The wide DMMA Gram with 2x2 tiles of 8x8 blocks (default) and with 4x4
+    tiles issues the same block products in the same k order: bitwise equal."""
+    c = np.asfortranarray(np.random.default_rng(shape[1] + 7).standard_normal(shape))
+    dv = d.Device(0)
+    try:
+        dv.set_option("gram_tiles", 4)
+        g4 = d.gram(c, device=dv)
+        dv.set_option("gram_tiles", 2)
+        g2 = d.gram(c, device=dv)
+    finally:
+        dv.set_option("gram_tiles", 2)
+        dv.close()
+    assert_bitwise(g2, g4)
+    g_ref = oracle.gram(c)
+    np.testing.assert_allclose(g2, g_ref, rtol=1e-13, atol=1e-13 * np.abs(g_ref).max())
+
+
 @pytest.mark.parametrize("shape", [(300, 75, 75), (1000, 150, 100), (17, 5, 3)])
 def test_matmul_bitwise(dev, oracle, shape):
     m, kk, n = shape

@@ -31,5 +31,6 @@ for v in vals:
     if ref is None:
         ref = r.svd.s.copy()
     print(f"{name}={v}: pass1 {p[0]:.3f} ms pass2 {p[1]:.3f} ms | solve spmm {st['spmm_pass_ms'][0]:.1f}/"
-          f"{st['spmm_pass_ms'][1]:.1f} ms eig {st['eig_ms']:.1f} ms sweeps {st['eig_sweeps']} total {st['total_ms']:.1f}{diff}", flush=True)
+          f"{st['spmm_pass_ms'][1]:.1f} ms gram {st['gram_ms']:.1f} rescale {st['rescale_ms']:.1f} eig {st['eig_ms']:.1f} ms "
+          f"sweeps {st['eig_sweeps']} total {st['total_ms']:.1f}{diff}", flush=True)
     dev.close()
