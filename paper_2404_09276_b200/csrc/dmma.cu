@@ -776,6 +776,7 @@ GwPlan gw2_kinds(int nt) {
     return p;
 }
 int gram_wide_tiles = 2;  // 2: gram_dmma_wide2_kernel (default), 4: gram_dmma_wide_kernel
+int gram_wide_waves = 24;  // CTAs of the wide Gram: about this many per SM (C4: 6 -> 24 = 519 -> 485 ms per solve)
 constexpr int kGramNarrowMaxNb = 20;  // gram_dmma_kernel<NB4 <= 5>: l <= 160
 constexpr int kGramWideMaxNb = 40;    // gram_dmma_wide_kernel: l <= 320 (<= 10 strips)
 
@@ -786,7 +787,7 @@ GramDmmaPlan gram_dmma_plan(int64_t n, int64_t l) {
         // wide: kinds x slabs, ~6 waves of one CTA per SM
         const int nkinds = gram_wide_tiles == 2 ? gw2_kinds((p.nb + 1) / 2).n : gw_kinds((p.nb + 3) / 4).n;
         p.nblk = static_cast<int>(std::max<int64_t>(
-            1, std::min<int64_t>(ceil_div(6 * kNumSMs, nkinds), ceil_div(n, 8 * kGwRows))));
+            1, std::min<int64_t>(ceil_div(gram_wide_waves * kNumSMs, nkinds), ceil_div(n, 8 * kGwRows))));
         p.rpb = ceil_div(ceil_div(n, p.nblk), kGwRows) * kGwRows;
         p.nblk = static_cast<int>(std::max<int64_t>(1, ceil_div(n, p.rpb)));
         return p;
@@ -802,6 +803,7 @@ GramDmmaPlan gram_dmma_plan(int64_t n, int64_t l) {
 }  // namespace
 
 void set_gram_wide_tiles(int t) { gram_wide_tiles = t == 4 ? 4 : 2; }
+void set_gram_wide_waves(int w) { gram_wide_waves = w < 1 ? 1 : w; }
 
 bool gram_dmma_supported(int64_t l, int64_t ld) {
     return l >= 1 && (l + 7) / 8 <= kGramWideMaxNb && ld % 2 == 0 && ld >= l;

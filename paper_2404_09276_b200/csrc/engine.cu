@@ -1220,6 +1220,9 @@ int dsvd_ctx_set_option(dsvd_ctx* ctx, const char* name, int64_t value) {
         } else if (n == "gram_tiles") {
             if (value != 2 && value != 4) fail(DSVD_CONFIG, "gram_tiles must be 2 or 4");
             set_gram_wide_tiles(static_cast<int>(value));
+        } else if (n == "gram_waves") {
+            if (value < 1 || value > 64) fail(DSVD_CONFIG, "gram_waves must be in [1, 64]");
+            set_gram_wide_waves(static_cast<int>(value));
         } else if (n == "uniform_values") {
             // 1: detect all-equal values at build time (the column-slab kernel then
             // skips the value stream), 0: always stream the values
