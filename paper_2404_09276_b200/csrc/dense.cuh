@@ -45,7 +45,8 @@ bool gram_dmma_supported(int64_t l, int64_t ld);
 // tile shape of the wide (l > 160) DMMA Gram: 2 (2x2 blocks of 8x8, default) or 4
 // (4x4); process-wide, for A/B runs (option "gram_tiles")
 void set_gram_wide_tiles(int t);
-void set_gram_wide_waves(int w);  // CTAs per SM of the wide Gram grid (option "gram_waves")
+void set_gram_wide_waves(int w);
+void set_rescale_row_ctas(int64_t c);  // grid.y cap of the DMMA rescale (option "rescale_row_ctas")  // CTAs per SM of the wide Gram grid (option "gram_waves")
 size_t gram_dmma_workspace_bytes(int64_t n, int64_t l);
 void gram_dmma(const double* c, int64_t n, int64_t l, int64_t ld, double* g, void* ws, const int32_t* gate,
                cudaStream_t stream);

@@ -844,6 +844,8 @@ void gram_dmma(const double* c, int64_t n, int64_t l, int64_t ld, double* g, voi
 }
 
 bool rescale_use_tma = true;
+int64_t rescale_max_row_ctas = 4096;  // grid.y cap: CTAs loop over row blocks beyond it (C4: 815 -> 798 ms per solve vs 65535: one W load per CTA serves 8 row blocks)
+void set_rescale_row_ctas(int64_t c) { rescale_max_row_ctas = c < 1 ? 1 : std::min<int64_t>(c, 65535); }
 
 bool rescale_dmma_supported(int64_t K, int64_t ldc, int64_t ld_out, int out_colmajor) {
     return K >= 1 && K <= kRsMaxK && ldc % 2 == 0 && ldc >= K && (out_colmajor || ld_out % 2 == 0);
@@ -869,7 +871,7 @@ void rescale_dmma(const double* c, int64_t n, int64_t K, int64_t ldc, const doub
         w, ldw, scale, static_cast<int>(K), static_cast<int>(ncol), npad, ldb, wt, gate);
     DSVD_LAUNCH_CHECK();
     const int64_t nrb = ceil_div(n, kRsBM);
-    const dim3 grid(static_cast<unsigned>(ncb), static_cast<unsigned>(std::min<int64_t>(nrb, 65535)));
+    const dim3 grid(static_cast<unsigned>(ncb), static_cast<unsigned>(std::min<int64_t>(nrb, rescale_max_row_ctas)));
     const bool tma = rescale_use_tma && (reinterpret_cast<uintptr_t>(c) % 16) == 0 && (ldc * 8) % 16 == 0;
     if (tma) {
         // K > 160: a 2-deep ring keeps two CTAs per SM (the W block grows with K)

@@ -1223,6 +1223,9 @@ int dsvd_ctx_set_option(dsvd_ctx* ctx, const char* name, int64_t value) {
         } else if (n == "gram_waves") {
             if (value < 1 || value > 64) fail(DSVD_CONFIG, "gram_waves must be in [1, 64]");
             set_gram_wide_waves(static_cast<int>(value));
+        } else if (n == "rescale_row_ctas") {
+            if (value < 1) fail(DSVD_CONFIG, "rescale_row_ctas must be >= 1");
+            set_rescale_row_ctas(value);
         } else if (n == "uniform_values") {
             // 1: detect all-equal values at build time (the column-slab kernel then
             // skips the value stream), 0: always stream the values
