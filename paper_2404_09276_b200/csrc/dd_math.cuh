@@ -166,6 +166,126 @@ __host__ __device__ inline double cos_cr(double x) {
     return (q == 1 || q == 2) ? -v : v;
 }
 
+// ---- fast paths (Ziv's strategy) ------------------------------------------------
+// Mostly-double evaluations returning a double-double estimate R = Rh + Rl with a
+// proven absolute error bound err; the correctly rounded value is Rh whenever the
+// whole interval [R - err, R + err] rounds to Rh, which the test below decides
+// (Rh = fl(Rh + Rl) after the final renormalisation, so only the side of Rl can
+// cross a rounding boundary; err is doubled to cover the rounding of Rl + err).
+// Otherwise the caller evaluates log_cr / cos_cr above. ~5x fewer FP64
+// operations than the double-double evaluations; tests/ddm_check.cpp checks
+// fast-or-fallback against the series versions bit for bit.
+__host__ __device__ __forceinline__ bool ziv_rounds(dd r, double err) {
+    const double t = r.lo + copysign(2.0 * err, r.lo);
+    return r.hi + t == r.hi;
+}
+
+__host__ __device__ __forceinline__ double tab1(const double* host, const double* dev, int i) {
+#ifdef __CUDA_ARCH__
+    (void)host;
+    return __ldg(dev + i);
+#else
+    (void)dev;
+    return host[i];
+#endif
+}
+
+// log(u), u > 0 finite: u = f 2^e with f in [sqrt(1/2), sqrt(2)); r = 8-bit
+// reciprocal of the 1/256-cell of f, so z = f r - 1 is exact (one FMA) with
+// |z| < 2^-7; log u = e ln2 - log r + log1p(z), log1p(z) = z - z^2/2 + z^3 P(z)
+// with z^2 exact (two_prod) and P to z^8 (truncation < 2^-87). Error: the z^3 P
+// term's roundings (< 2^-53 |z|^3) plus the double-double sums (< 2^-100 of the
+// parts' magnitudes); err below carries a 4x and 16x margin on those.
+__host__ __device__ inline bool log_fast(double u, double* out) {
+    int e;
+    double f = frexp(u, &e);
+    if (f < 0.70710678118654752440) {
+        f *= 2.0;
+        e -= 1;
+    }
+    const int i = static_cast<int>(rint(f * 256.0)) - ddc::kRcpFirst;  // 0 .. 181
+    const double r = tab1(DSVD_TAB(kRcpLogTab), 3 * i);
+    const dd lr{tab1(DSVD_TAB(kRcpLogTab), 3 * i + 1), tab1(DSVD_TAB(kRcpLogTab), 3 * i + 2)};
+    const double z = fma(f, r, -1.0);  // exact
+    const dd z2 = two_prod(z, z);
+    const double p = 0x1.5555555555555p-2 + z * (-0.25 + z * (0.2 + z * (-0x1.5555555555555p-3 +
+                     z * (0x1.2492492492492p-3 + z * (-0.125 + z * (0x1.c71c71c71c71cp-4 +
+                     z * (-0.1 + z * 0x1.745d1745d1746p-4)))))));
+    const double z3p = z2.hi * z * p;
+    dd y = two_sum(z, -0.5 * z2.hi);
+    const double ed = static_cast<double>(e);
+    y.lo += fma(ed, ddc::kLn2Lo, -0.5 * z2.lo) + z3p;
+    y = quick_two_sum(y.hi, y.lo);
+    const dd el{ed * ddc::kLn2Hi, ed * ddc::kLn2Mid};  // both exact (42-bit pieces, |e| <= 1075)
+    const dd res = add(add(el, lr), y);
+    const double err = 0x1p-51 * fabs(z2.hi * z) + 0x1p-96 * (fabs(el.hi) + fabs(lr.hi) + fabs(y.hi));
+    *out = res.hi;
+    return ziv_rounds(res, err);
+}
+
+// cos(x), 0 <= x <= 8: x = k pi/2 + r (three exact Cody-Waite steps, the fourth
+// piece and the third's product added to the low word: |error of r| < 2^-104),
+// r = j/32 + s with |s| <= 1/64, cos/sin(j/32) from the double-double tables,
+// cos s - 1 = -s^2/2 (exact) + s^4 (..), sin s = s + s^3 (..), combined in
+// double-double. Error < 2^-72 absolute (the s^3 terms' roundings) + the
+// reduction's 2^-104; for k odd and j = 0 the result is sin s itself and the
+// polynomial error is relative to s.
+__host__ __device__ inline bool cos_fast(double x, double* out) {
+    const double kq = rint(x * ddc::kTwoOverPi);
+    const int k = static_cast<int>(kq);
+    const double r1 = fma(-kq, ddc::kPio2_1, x);  // exact (Sterbenz; kq * P1 exact)
+    dd r = two_sum(r1, -kq * ddc::kPio2_2);         // kq * P2 exact
+    r.lo = fma(-kq, ddc::kPio2_4, fma(-kq, ddc::kPio2_3, r.lo));
+    r = two_sum(r.hi, r.lo);
+    const int j = static_cast<int>(rint(r.hi * 32.0));  // -25 .. 25
+    const dd s = two_sum(r.hi - j * 0.03125, r.lo);     // r.hi - j/32 exact (Sterbenz)
+    const dd p = two_prod(s.hi, s.hi);
+    const double s2 = p.hi;
+    // cos s - 1 = cm.hi + cm.lo
+    const dd cm{-0.5 * p.hi, fma(-s.hi, s.lo, -0.5 * p.lo) +
+                                 s2 * s2 * (0x1.5555555555555p-5 + s2 * (-0x1.6c16c16c16c17p-10 +
+                                                                         s2 * 0x1.a01a01a01a01ap-16))};
+    // sin s = s.hi + sn_lo
+    const double sn_lo = s.lo + s.hi * s2 * (-0x1.5555555555555p-3 + s2 * (0x1.1111111111111p-7 +
+                                             s2 * (-0x1.a01a01a01a01ap-13 + s2 * 0x1.71de3a556c734p-19)));
+    dd res;
+    double err;
+    if (j == 0) {
+        if ((k & 1) == 0) {
+            res = quick_two_sum(1.0, cm.hi);
+            res = quick_two_sum(res.hi, res.lo + cm.lo);
+            err = 0x1p-78;
+        } else {  // sin s: the s^3 term's roundings, relative to s^3
+            res = quick_two_sum(s.hi, sn_lo);
+            err = 0x1p-50 * fabs(s.hi) * s2;
+        }
+    } else {
+        const int ja = j < 0 ? -j : j;
+        const dd ca = tab_ld(DSVD_TAB(kCosTab), ja);
+        dd sa = tab_ld(DSVD_TAB(kSinTab), ja);
+        if (j < 0) sa = dd{-sa.hi, -sa.lo};
+        // cos s = 1 + cm, sin s = s.hi + sn_lo
+        if ((k & 1) == 0) {  // cos(a + s) = ca + ca cm - sa sin s
+            dd t2 = two_prod(ca.hi, cm.hi);
+            t2.lo += ca.hi * cm.lo + ca.lo * cm.hi;
+            dd t3 = two_prod(-sa.hi, s.hi);
+            t3.lo += -sa.hi * sn_lo - sa.lo * s.hi;
+            res = add(add(ca, t2), t3);
+        } else {  // sin(a + s) = sa + sa cm + ca sin s
+            dd t2 = two_prod(sa.hi, cm.hi);
+            t2.lo += sa.hi * cm.lo + sa.lo * cm.hi;
+            dd t3 = two_prod(ca.hi, s.hi);
+            t3.lo += ca.hi * sn_lo + ca.lo * s.hi;
+            res = add(add(sa, t2), t3);
+        }
+        err = 0x1p-68;  // the s^3 term of sin s: < 2^-70.4
+    }
+    const int q = k & 3;
+    const bool neg = q == 1 || q == 2;
+    *out = neg ? -res.hi : res.hi;
+    return ziv_rounds(res, err + 0x1p-102);
+}
+
 // The series evaluations the table-driven versions above replace (kept as the
 // cross-check of tests/test_ddm.py).
 __host__ __device__ inline double log_cr_series(double u) {

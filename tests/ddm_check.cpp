@@ -8,6 +8,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
+#include <cmath>
 #include <cstring>
 #include <initializer_list>
 
@@ -24,9 +25,27 @@ static bool same(double a, double b) { return std::memcmp(&a, &b, sizeof a) == 0
 
 int main(int argc, char** argv) {
     const long n = argc > 1 ? std::atol(argv[1]) : 1000000;
-    long bad_log = 0, bad_cos = 0, total = 0;
+    long bad_log = 0, bad_cos = 0, total = 0, slow_log = 0, slow_cos = 0;
     auto check = [&](double u, double x) {
         ++total;
+        // the fast paths (Ziv test + fallback), as rng.cuh uses them
+        double fl, fc;
+        if (!dsvd::ddm::log_fast(u, &fl)) {
+            fl = dsvd::ddm::log_cr(u);
+            ++slow_log;
+        }
+        if (!dsvd::ddm::cos_fast(x, &fc)) {
+            fc = dsvd::ddm::cos_cr(x);
+            ++slow_cos;
+        }
+        if (!same(fl, dsvd::ddm::log_cr_series(u))) {
+            if (bad_log < 5) std::printf("fast log %a: %a vs %a\n", u, fl, dsvd::ddm::log_cr_series(u));
+            ++bad_log;
+        }
+        if (!same(fc, dsvd::ddm::cos_cr_series(x))) {
+            if (bad_cos < 5) std::printf("fast cos %a: %a vs %a\n", x, fc, dsvd::ddm::cos_cr_series(x));
+            ++bad_cos;
+        }
         if (!same(dsvd::ddm::log_cr(u), dsvd::ddm::log_cr_series(u))) {
             if (bad_log < 5) std::printf("log %a: %a vs %a\n", u, dsvd::ddm::log_cr(u), dsvd::ddm::log_cr_series(u));
             ++bad_log;
@@ -54,6 +73,13 @@ int main(int argc, char** argv) {
                 const double x = k * 1.5707963267948966 + (j + 0.5) / 32.0 + d;
                 if (x > 0 && x < 6.3) check(0.5, x);
             }
+    // near-midpoint log / cos arguments: the fast path must decline them
+    for (long i = 0; i < n / 100; ++i) {
+        const double u = unit(sm64(11, i));
+        check(u, 6.283185307179586 * unit(sm64(13, i)));
+        check(std::nextafter(u, 1.0), std::nextafter(6.283185307179586 * unit(sm64(13, i)), 7.0));
+    }
+    std::printf("fallbacks log %ld cos %ld of %ld\n", slow_log, slow_cos, total);
     std::printf("mismatches %ld %ld of %ld\n", bad_log, bad_cos, total);
     return 0;
 }
