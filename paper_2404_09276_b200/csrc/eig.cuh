@@ -31,8 +31,10 @@ void jacobi_eig(const double* g, EigWorkspace& w, Control* ctrl, const int32_t* 
 // iteration; callers then run jacobi_eig with need = clustered.
 bool tbi_supported(int l);
 size_t tbi_workspace_bytes(int l);
+// phase 0: the whole path; 1: the tridiagonalisation only (the one long,
+// single-CTA kernel); 2: the rest (multisection .. back-transform)
 void tbi_eig(const double* g, EigWorkspace& w, void* tbi_ws, int32_t* clustered, const int32_t* gate,
-             cudaStream_t stream);
+             cudaStream_t stream, int phase = 0);
 
 // Loop-mode parameters of eig_svd_finish (solver.cpp:97-112).
 struct LoopStep {

@@ -791,7 +791,7 @@ size_t tbi_workspace_bytes(int l) {
 // Runs the tridiagonal path; sets *clustered (device) when the spectrum needs
 // the Jacobi fallback. Writes w.lam / w.vecs (stride w.lp) like jacobi_eig.
 void tbi_eig(const double* g, EigWorkspace& w, void* tbi_ws, int32_t* clustered, const int32_t* gate,
-             cudaStream_t stream) {
+             cudaStream_t stream, int phase) {
     const int n = w.l;
     double* hv = static_cast<double*>(tbi_ws);
     double* tau = hv + static_cast<size_t>(n) * n;
@@ -800,9 +800,10 @@ void tbi_eig(const double* g, EigWorkspace& w, void* tbi_ws, int32_t* clustered,
     double* z = e + n;
     double* S = z + static_cast<size_t>(n) * n;
     double* z2 = S + static_cast<size_t>(n) * n;
+    int32_t* counts = reinterpret_cast<int32_t*>(z2 + static_cast<size_t>(n) * n);
+    if (phase != 2) {
     tbi_clear_kernel<<<1, 1, 0, stream>>>(clustered);
     DSVD_LAUNCH_CHECK();
-    int32_t* counts = reinterpret_cast<int32_t*>(z2 + static_cast<size_t>(n) * n);
     if (n <= kTridSmemMaxN) {
         const size_t s1 = tridiag_smem_bytes(n);
         DSVD_CUDA_CHECK(cudaFuncSetAttribute(tbi_tridiag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -816,6 +817,8 @@ void tbi_eig(const double* g, EigWorkspace& w, void* tbi_ws, int32_t* clustered,
         tbi_tridiag_big_kernel<<<1, kTridBigThreads, s1, stream>>>(g, n, Aw, d, e, hv, tau, gate, nullptr);
     }
     DSVD_LAUNCH_CHECK();
+    }
+    if (phase == 1) return;
     tbi_grid_kernel<<<kGridPts / 512, 256, sizeof(double) * 3 * n, stream>>>(d, e, n, counts, gate, nullptr);
     DSVD_LAUNCH_CHECK();
     const size_t s2 = sizeof(double) * (3 * static_cast<size_t>(n) + kTbiWarps * 3 * static_cast<size_t>(n));

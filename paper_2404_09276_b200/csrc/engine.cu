@@ -327,7 +327,10 @@ bool solve_rescale(dsvd_ctx* ctx, const double* c, int64_t n, int64_t K, int64_t
 // (s, V) of the row-major block c (rows x l, stride ld); U is left to the caller.
 void eig_svd_factors(dsvd_ctx* ctx, const double* c, int64_t rows, int64_t l, int64_t ld,
                      EigSvdOut& o, Control* ctrl, const LoopStep* loop, const int32_t* gate,
-                     bool reduce_gram = false, int64_t floor_rows = -1, cudaStream_t eig_stream = nullptr) {
+                     bool reduce_gram = false, int64_t floor_rows = -1, cudaStream_t eig_stream = nullptr,
+                     int phase = 0) {
+    // phase 0: all; 1: the Gram, then the tridiagonalisation on eig_stream;
+    // 2: the rest of the eig and the assembly on the main stream (after phase 1)
     cudaStream_t st = ctx->stream;
     // the l x l eig and the factor assembly (latency-bound, a few SMs) may run
     // on eig_stream, after the Gram on ctx->stream (all SMs) — or, with
@@ -346,6 +349,24 @@ void eig_svd_factors(dsvd_ctx* ctx, const double* c, int64_t rows, int64_t l, in
     };
     if (eig_stream != nullptr && ctx->gram_async) to_eig_stream();
     double* G = ctx->tbuf<double>("eig.G", l * l);
+    const bool tbi = ctx->eig_method == 0 && tbi_supported(static_cast<int>(l));
+    if (phase == 2) {
+        DSVD_CUDA_CHECK(cudaStreamWaitEvent(st, ctx->ev_eig, 0));
+        EigWorkspace ew;
+        void* em = ctx->buf("eig.ws", eig_workspace_bytes(static_cast<int>(l), kMaxSweeps));
+        eig_workspace_bind(ew, static_cast<int>(l), kMaxSweeps, em);
+        const int sp2 = ctx->span_begin(K_EIG);
+        int32_t* flag = ctx->tbuf<int32_t>("tbi.flag", 1);
+        tbi_eig(G, ew, ctx->buf("tbi.ws", tbi_workspace_bytes(static_cast<int>(l))), flag, gate, st, 2);
+        count_launch(4);
+        jacobi_eig(G, ew, ctrl, gate, st, flag);
+        count_launch(1);
+        eig_svd_finish(ew, floor_rows >= 0 ? floor_rows : rows, o.W, l, o.s, o.inv_s, ctrl, loop, gate, st);
+        count_launch(1);
+        ctx->span_end(sp2);
+        return;
+    }
+    if (phase == 1 && (!tbi || eig_stream == nullptr)) fail(DSVD_OTHER, "eig phase 1 needs the tridiagonal path");
     int sp = ctx->span_begin(K_GRAM);
     if (ctx->dense_method == 0 && gram_dmma_supported(l, ld)) {
         const size_t gws = gram_dmma_workspace_bytes(rows, l);
@@ -367,7 +388,15 @@ void eig_svd_factors(dsvd_ctx* ctx, const double* c, int64_t rows, int64_t l, in
     void* em = ctx->buf("eig.ws", eig_workspace_bytes(static_cast<int>(l), kMaxSweeps));
     eig_workspace_bind(ew, static_cast<int>(l), kMaxSweeps, em);
     sp = ctx->span_begin(K_EIG);
-    if (ctx->eig_method == 0 && tbi_supported(static_cast<int>(l))) {
+    if (phase == 1) {
+        int32_t* flag = ctx->tbuf<int32_t>("tbi.flag", 1);
+        tbi_eig(G, ew, ctx->buf("tbi.ws", tbi_workspace_bytes(static_cast<int>(l))), flag, gate, st, 1);
+        count_launch(2);
+        DSVD_CUDA_CHECK(cudaEventRecord(ctx->ev_eig, st));
+        ctx->span_end(sp);
+        return;
+    }
+    if (tbi) {
         // tridiagonal path; the Jacobi kernels run only if it flags a cluster
         int32_t* flag = ctx->tbuf<int32_t>("tbi.flag", 1);
         tbi_eig(G, ew, ctx->buf("tbi.ws", tbi_workspace_bytes(static_cast<int>(l))), flag, gate, st);
@@ -609,9 +638,54 @@ void solve_tall(dsvd_ctx* ctx, const DevCsr& A, const DevCsr& AT, const dsvd_con
         double* Tb[2] = {T, Qb[0]};
         double* P = Qb[1];
         // Gram on st (all SMs), then the eig chain on the priority stream
-        auto eig_async = [&](const double* tj, const LoopStep* lsp, const int32_t* g) {
-            factors(tj + slab0 * ld, lsp, g, ctx->eig);  // v2: this rank's slab of T_j
-            DSVD_CUDA_CHECK(cudaEventRecord(ctx->ev_eig, ctx->eig));
+        // eig_overlap (DESIGN 5): 1 runs the whole eig chain on the priority stream
+        // beside the A T pass; 2 (default) only the tridiagonalisation there and the
+        // short multi-CTA kernels after the pass on the main stream (at high
+        // priority their CTAs cost the gathering pass more than they take: C4
+        // pass 1 20.1 -> 23.2 ms); 0 the whole chain after the pass
+        // auto (-1): split above l = 160, where the tridiagonalisation is the long
+        // L2-resident kernel (C4: 2.74 -> 2.68 s); whole chain beside the pass below
+        // (C2: 73.6 vs 75.6 ms split); the split needs the tridiagonal eigensolver
+        const bool tbi_ok = ctx->eig_method == 0 && tbi_supported(static_cast<int>(l));
+        int eov = ctx->eig_overlap < 0 ? (l > 160 ? 2 : 1) : ctx->eig_overlap;
+        if (observer || (eov == 2 && !tbi_ok)) eov = 1;
+        const double* inl_t = nullptr;
+        const LoopStep* inl_ls = nullptr;
+        const int32_t* inl_g = nullptr;
+        int64_t inl_j = -1;  // iteration whose stop flag the deferred part decides
+        auto eig_async = [&](const double* tj, const LoopStep* lsp, const int32_t* g, int64_t jj) {
+            if (eov == 1) {
+                factors(tj + slab0 * ld, lsp, g, ctx->eig);  // v2: this rank's slab of T_j
+                DSVD_CUDA_CHECK(cudaEventRecord(ctx->ev_eig, ctx->eig));
+                return;
+            }
+            if (eov == 2)  // Gram on st, the tridiagonalisation on the eig stream
+                eig_svd_factors(ctx, tj + slab0 * ld, red_rows, l, ld, eo, ctrl, lsp, g, v2, v2 ? n : -1, ctx->eig,
+                                1);
+            inl_t = tj;
+            inl_ls = lsp;
+            inl_g = g;
+            inl_j = jj;
+        };
+        // dash: the host's lookahead reads of stop_pending after eigSVD(T_jj)
+        auto flag_copy = [&](int64_t jj, cudaStream_t fs) {
+            if (!dash || jj < 1) return;
+            const int slot = static_cast<int>(jj % (kLookahead + 1));
+            if (flag_ev[slot] == nullptr) flag_ev[slot] = ctx->event();
+            DSVD_CUDA_CHECK(cudaMemcpyAsync(&ctx->host_flags[slot], &ctrl->stop_pending, sizeof(int32_t),
+                                            cudaMemcpyDeviceToHost, fs));
+            DSVD_CUDA_CHECK(cudaEventRecord(flag_ev[slot], fs));
+        };
+        auto eig_deferred = [&] {  // the deferred part, on the main stream
+            if (inl_t == nullptr) return;
+            if (eov == 2)
+                eig_svd_factors(ctx, inl_t + slab0 * ld, red_rows, l, ld, eo, ctrl, inl_ls, inl_g, v2, v2 ? n : -1,
+                                nullptr, 2);
+            else
+                factors(inl_t + slab0 * ld, inl_ls, inl_g, nullptr);
+            DSVD_CUDA_CHECK(cudaEventRecord(ctx->ev_eig, st));
+            flag_copy(inl_j, st);
+            inl_t = nullptr;
         };
         double* Qobs[2] = {nullptr, nullptr};
         if (observer) {
@@ -632,7 +706,7 @@ void solve_tall(dsvd_ctx* ctx, const DevCsr& A, const DevCsr& AT, const dsvd_con
                 ctx->span_end(sp);
             }
         }
-        eig_async(Tb[0], nullptr, nullptr);
+        eig_async(Tb[0], nullptr, nullptr, 0);
         if (observer) {
             DSVD_CUDA_CHECK(cudaStreamWaitEvent(st, ctx->ev_eig, 0));
             solve_rescale(ctx, Tb[0], n, l, ld, W, l, inv_s, l, Qobs[0], ld, 0, nullptr);
@@ -652,6 +726,7 @@ void solve_tall(dsvd_ctx* ctx, const DevCsr& A, const DevCsr& AT, const dsvd_con
             sp = ctx->span_begin(K_SPMM1);
             pass1(tprev, Y, true, dash ? &ctrl->stop_pending : gate);
             ctx->span_end(sp);
+            eig_deferred();
             if (ctx->shift_after) {
                 // P = A^T Z before the wait (both passes overlap the eig), then
                 // P <- fma(-alpha, T_{j-1}, P): the same bits as the fused epilogue
@@ -682,14 +757,8 @@ void solve_tall(dsvd_ctx* ctx, const DevCsr& A, const DevCsr& AT, const dsvd_con
                 // T_j = P W_{j-1} diag(1/s_{j-1})  (= A^T A Q_{j-1} - alpha Q_{j-1})
                 rescale_into(red, Tb[j % 2], gate);
             }
-            eig_async(Tb[j % 2], &ls, gate);
-            if (dash) {
-                const int slot = static_cast<int>(j % (kLookahead + 1));
-                if (flag_ev[slot] == nullptr) flag_ev[slot] = ctx->event();
-                DSVD_CUDA_CHECK(cudaMemcpyAsync(&ctx->host_flags[slot], &ctrl->stop_pending, sizeof(int32_t),
-                                                cudaMemcpyDeviceToHost, ctx->eig));
-                DSVD_CUDA_CHECK(cudaEventRecord(flag_ev[slot], ctx->eig));
-            }
+            eig_async(Tb[j % 2], &ls, gate, j);
+            if (eov == 1) flag_copy(j, ctx->eig);
             if (observer) {
                 DSVD_CUDA_CHECK(cudaStreamWaitEvent(st, ctx->ev_eig, 0));
                 Control oc = read_control(ctx, ctrl);
@@ -707,6 +776,7 @@ void solve_tall(dsvd_ctx* ctx, const DevCsr& A, const DevCsr& AT, const dsvd_con
                 if (oc.stop_pending) break;
             }
         }
+        eig_deferred();
         DSVD_CUDA_CHECK(cudaEventRecord(ctx->ev_eig, ctx->eig));  // incl. the last flag copy
         DSVD_CUDA_CHECK(cudaStreamWaitEvent(st, ctx->ev_eig, 0));
         hc = read_control(ctx, ctrl);
@@ -1261,6 +1331,11 @@ int dsvd_ctx_set_option(dsvd_ctx* ctx, const char* name, int64_t value) {
             int lo = 0, hi = 0;
             DSVD_CUDA_CHECK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
             DSVD_CUDA_CHECK(cudaStreamCreateWithPriority(&ctx->eig, cudaStreamNonBlocking, value ? hi : lo));
+        } else if (n == "eig_overlap") {
+            if (value < -1 || value > 2)
+                fail(DSVD_CONFIG,
+                     "eig_overlap: 2 = tridiagonalisation beside the A T pass, 1 = whole chain, 0 = none, -1 = auto");
+            ctx->eig_overlap = static_cast<int>(value);
         } else if (n == "shift_after") {
             if (value < 0 || value > 1) fail(DSVD_CONFIG, "shift_after must be 0 or 1");
             ctx->shift_after = static_cast<int>(value);

@@ -89,6 +89,11 @@ struct dsvd_ctx {
     // kernel after it (1), or fused into the A^T pass after the wait (0)
     int shift_after = 0;  // pipelined loop: Gram on the eig stream too (beside the A T pass)
     int pipeline = -1;  // -1: auto (pipelined at or below an nnz bound), 0: serial, 1: pipelined
+    // pipelined loop, where eigSVD(T_j) runs: 2 the tridiagonalisation (one long
+    // single-CTA kernel) on the eig stream beside the A T pass, the rest of the chain on the
+    // main stream after it; 1 the whole chain beside the A T pass; 0 all of it after the
+    // pass; -1 (default) 2 above l = 160, else 1
+    int eig_overlap = -1;
     int64_t pipeline_auto_nnz = 0;  // override of the auto rule's nnz bound (0: cost model)
     // Omega generated on `side` while the host CSR uploads (host-input solves):
     // the next solve_tall with the same (m, l, seed) waits on omega_ev instead

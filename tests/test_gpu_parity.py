@@ -941,25 +941,30 @@ def test_loop_schedules_agree(oracle, alg, kw):
 def test_loop_options_validated():
     dv = d.Device(0)
     for name, bad in (("pipeline", 2), ("pipeline", -2), ("gram_async", 2), ("shift_after", -1),
-                      ("eig_priority", 3)):
+                      ("eig_priority", 3), ("eig_overlap", 3), ("eig_overlap", -2)):
         with pytest.raises(d.ConfigError):
             dv.set_option(name, bad)
     for name, good in (("pipeline", -1), ("pipeline", 0), ("pipeline", 1), ("gram_async", 0),
-                       ("shift_after", 0), ("eig_priority", 1), ("eig_priority", 0)):
+                       ("shift_after", 0), ("eig_priority", 1), ("eig_priority", 0), ("eig_overlap", -1),
+                       ("eig_overlap", 0), ("eig_overlap", 1), ("eig_overlap", 2)):
         dv.set_option(name, good)
     with pytest.raises(d.ConfigError):
         dv.set_option("no_such_option", 1)
     dv.close()
 
 
-@pytest.mark.parametrize("opts", [dict(shift_after=1), dict(gram_async=1), dict(eig_priority=0)])
-def test_pipelined_variants_are_bitwise_equal(oracle, opts):
+@pytest.mark.parametrize("base,opts", [({}, dict(shift_after=1)), ({}, dict(gram_async=1)),
+                                       ({}, dict(eig_priority=0)), ({}, dict(eig_overlap=0)),
+                                       ({}, dict(eig_overlap=2)),
+                                       # Jacobi: no tridiagonalisation to split, 2 acts as 1
+                                       (dict(eig_method=1), dict(eig_method=1, eig_overlap=2))])
+def test_pipelined_variants_are_bitwise_equal(oracle, base, opts):
     """The schedule variants of the pipelined loop move work between streams but
     compute the same values in the same order: bitwise equal factors."""
     a = d.powerlaw(5000, 2000, 3.5, 1.0, 1.1, 2)
     cfg = d.SolverConfig(k=16, s=8, tol=1e-2, seed=2)
     res = []
-    for extra in ({}, opts):
+    for extra in (base, opts):
         dv = d.Device(0)
         dv.set_option("pipeline", 1)
         for k_, v_ in extra.items():
@@ -969,3 +974,28 @@ def test_pipelined_variants_are_bitwise_equal(oracle, opts):
     assert res[0].trace.iterations == res[1].trace.iterations
     for name in ("u", "s", "v"):
         assert_bitwise(getattr(res[0].svd, name), getattr(res[1].svd, name))
+
+
+@pytest.mark.parametrize("alg,kw", [("dash", dict(tol=2e-2)), ("shifted", dict(p=5))])
+def test_eig_overlap_wide_sketch(oracle, alg, kw):
+    """l = 180 (> 160: the wide tridiagonalisation, where the default splits the
+    eig chain: tridiagonalisation beside the A T pass, the rest after it on the
+    main stream). Every placement of the chain gives the same bits, and the
+    solve meets the bars against the oracle (dash: the deferred stop flags keep
+    N_p and the stop reason)."""
+    a = d.powerlaw(3000, 1500, 3.0, 1.0, 1.1, 5)
+    ca = Csr(a.rows, a.cols, a.offsets, a.col_indices, a.values)
+    ref = oracle.solve(ca, 120, 60, alg=alg, seed=5, **kw)
+    cfg = d.SolverConfig(k=120, s=60, alg=d.Algorithm[alg], seed=5, **kw)
+    res = []
+    for eov in (-1, 1, 0):
+        dv = d.Device(0)
+        dv.set_option("pipeline", 1)
+        dv.set_option("eig_overlap", eov)
+        res.append(d.solve(a, cfg, device=dv))
+        dv.close()
+    check_solve(res[0], ref, 120)
+    for r in res[1:]:
+        assert r.trace.iterations == res[0].trace.iterations
+        for name in ("u", "s", "v"):
+            assert_bitwise(getattr(res[0].svd, name), getattr(r.svd, name))
