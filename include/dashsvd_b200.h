@@ -147,9 +147,13 @@ DSVD_API int dsvd_ctx_synchronize(dsvd_ctx* ctx);
 DSVD_API int dsvd_ctx_trim(dsvd_ctx* ctx);
 /* Tuning knobs (testing/benchmarking); unknown names -> DSVD_CONFIG.
  * Loop schedule: "pipeline" -1 auto (default) / 0 serial /
- * 1 pipelined; "eig_priority" 1 (default) / 0; "gram_async" 0 (default) / 1.
+ * 1 pipelined; "eig_priority" 1 (default) / 0; "gram_async" 0 (default) / 1;
+ * "eig_overlap" -1 auto (default) / 2 tridiagonalisation beside the A T pass,
+ * rest after it / 1 whole eig chain beside it / 0 none.
  * Row-sharded solves: "mgpu_mode" 2 (default: reduce-scatter + slab dense work
- * + all-gather) / 1 (all-reduce of the n x l partials, dense work redundant).
+ * + all-gather) / 1 (all-reduce of the n x l partials, dense work redundant);
+ * "mgpu_overlap" 1 (default: the A^T pass in G row panels, each panel's partial
+ * reduced on a communication stream while the next panel computes) / 0.
  * Kernels: "spmm_variant", "split_chunk", "split_chunk_t", "split_panel_rows",
  * "hub_threshold", "eig_method", "dense_method"; column-slab SpMM: "spmm_slab"
  * (-1 auto / 0 / 32 / 64), "slab_layout", "spmm_slab_hint", "spmm_slab_depth",

@@ -62,6 +62,8 @@ struct NcclApi {
                               cudaStream_t) = nullptr;
     ncclResult_t (*ReduceScatter)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
                                   cudaStream_t) = nullptr;
+    ncclResult_t (*Reduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, int, ncclComm_t,
+                           cudaStream_t) = nullptr;
     ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
     ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
     ncclResult_t (*CommGetAsyncError)(ncclComm_t, ncclResult_t*) = nullptr;
@@ -85,6 +87,7 @@ NcclApi& nccl() {
     api.CommInitRank = reinterpret_cast<decltype(api.CommInitRank)>(sym("ncclCommInitRank"));
     api.AllReduce = reinterpret_cast<decltype(api.AllReduce)>(sym("ncclAllReduce"));
     api.ReduceScatter = reinterpret_cast<decltype(api.ReduceScatter)>(sym("ncclReduceScatter"));
+    api.Reduce = reinterpret_cast<decltype(api.Reduce)>(sym("ncclReduce"));
     api.AllGather = reinterpret_cast<decltype(api.AllGather)>(sym("ncclAllGather"));
     api.CommDestroy = reinterpret_cast<decltype(api.CommDestroy)>(sym("ncclCommDestroy"));
     api.CommGetAsyncError = reinterpret_cast<decltype(api.CommGetAsyncError)>(sym("ncclCommGetAsyncError"));
@@ -142,9 +145,9 @@ void lb_barrier(dsvd_loopback* g) {
 }
 
 // Post this rank's buffer, wait until every rank posted, return the pointers.
-RankPtrs lb_post(dsvd_ctx* ctx, const double* mine) {
+RankPtrs lb_post(dsvd_ctx* ctx, const double* mine, cudaStream_t stream = nullptr) {
     dsvd_loopback* g = ctx->loopback;
-    DSVD_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));  // the partial is complete
+    DSVD_CUDA_CHECK(cudaStreamSynchronize(stream ? stream : ctx->stream));  // the partial is complete
     {
         std::lock_guard<std::mutex> lock(g->mu);
         g->posted[ctx->rank] = mine;
@@ -161,15 +164,25 @@ int sum_grid(size_t count) {
     return static_cast<int>(b < 1 ? 1 : (b > 148 * 8 ? 148 * 8 : b));
 }
 
-void lb_allreduce(dsvd_ctx* ctx, double* buf, size_t count) {
-    const RankPtrs src = lb_post(ctx, buf);
+void lb_allreduce(dsvd_ctx* ctx, double* buf, size_t count, cudaStream_t s) {
+    const RankPtrs src = lb_post(ctx, buf, s);
     double* tmp = ctx->tbuf<double>("comm.lb.tmp", count);
-    rank_sum_kernel<<<sum_grid(count), 256, 0, ctx->stream>>>(src, ctx->nranks, 0, tmp, count);
+    rank_sum_kernel<<<sum_grid(count), 256, 0, s>>>(src, ctx->nranks, 0, tmp, count);
     DSVD_LAUNCH_CHECK();
-    DSVD_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+    DSVD_CUDA_CHECK(cudaStreamSynchronize(s));
     lb_barrier(ctx->loopback);  // every rank has read every buffer
-    DSVD_CUDA_CHECK(cudaMemcpyAsync(buf, tmp, sizeof(double) * count, cudaMemcpyDeviceToDevice, ctx->stream));
-    DSVD_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+    DSVD_CUDA_CHECK(cudaMemcpyAsync(buf, tmp, sizeof(double) * count, cudaMemcpyDeviceToDevice, s));
+    DSVD_CUDA_CHECK(cudaStreamSynchronize(s));
+}
+
+void lb_reduce(dsvd_ctx* ctx, const double* send, double* recv, size_t count, int root, cudaStream_t s) {
+    const RankPtrs src = lb_post(ctx, send, s);
+    if (ctx->rank == root) {
+        rank_sum_kernel<<<sum_grid(count), 256, 0, s>>>(src, ctx->nranks, 0, recv, count);
+        DSVD_LAUNCH_CHECK();
+        DSVD_CUDA_CHECK(cudaStreamSynchronize(s));
+    }
+    lb_barrier(ctx->loopback);  // the root has read every send
 }
 
 void lb_reduce_scatter(dsvd_ctx* ctx, const double* send, double* recv, size_t recvcount) {
@@ -195,14 +208,29 @@ void lb_allgather(dsvd_ctx* ctx, const double* send, double* recv, size_t sendco
 
 }  // namespace
 
-void comm_allreduce_sum(dsvd_ctx* ctx, double* buf, size_t count) {
+void comm_allreduce_sum(dsvd_ctx* ctx, double* buf, size_t count, cudaStream_t stream) {
     if (ctx->comm_kind == COMM_NONE || count == 0) return;
     NvtxRange r("dsvd.allreduce");
-    if (ctx->comm_kind == COMM_LOOPBACK) return lb_allreduce(ctx, buf, count);
-    nccl_check(nccl().AllReduce(buf, buf, count, ncclDouble, ncclSum, static_cast<ncclComm_t>(ctx->comm),
-                                ctx->stream),
+    const cudaStream_t s = stream ? stream : ctx->stream;
+    if (ctx->comm_kind == COMM_LOOPBACK) return lb_allreduce(ctx, buf, count, s);
+    nccl_check(nccl().AllReduce(buf, buf, count, ncclDouble, ncclSum, static_cast<ncclComm_t>(ctx->comm), s),
                "ncclAllReduce");
     nccl_poll(ctx, "ncclAllReduce");
+}
+
+void comm_reduce_sum(dsvd_ctx* ctx, const double* send, double* recv, size_t count, int root, cudaStream_t stream) {
+    const cudaStream_t s = stream ? stream : ctx->stream;
+    if (ctx->comm_kind == COMM_NONE) {
+        if (send != recv && count)
+            DSVD_CUDA_CHECK(cudaMemcpyAsync(recv, send, sizeof(double) * count, cudaMemcpyDeviceToDevice, s));
+        return;
+    }
+    if (count == 0) return;
+    NvtxRange r("dsvd.reduce");
+    if (ctx->comm_kind == COMM_LOOPBACK) return lb_reduce(ctx, send, recv, count, root, s);
+    nccl_check(nccl().Reduce(send, recv, count, ncclDouble, ncclSum, root, static_cast<ncclComm_t>(ctx->comm), s),
+               "ncclReduce");
+    nccl_poll(ctx, "ncclReduce");
 }
 
 void comm_reduce_scatter_sum(dsvd_ctx* ctx, const double* send, double* recv, size_t recvcount) {

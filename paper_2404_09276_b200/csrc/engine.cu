@@ -236,6 +236,68 @@ void build_pair(dsvd_ctx* ctx, CsrAlloc& al, int64_t rows, int64_t cols, int64_t
     }
 }
 
+// Row panels [bounds[p], bounds[p+1]) of a device CSR as DevCsr views for the
+// exchange overlap of row-sharded solves (solve_tall, mgpu_overlap): the
+// views share the offsets / indices / values (a view's off points at its first
+// row, positions stay absolute) and get their own length order, row ranges and
+// split-row chunk plan. A split row is cut exactly as in the whole matrix
+// (same split_chunk and X-row panels) and its chunks are combined in CSR order,
+// so a panel's rows come out bitwise as in the whole-matrix pass.
+std::vector<DevCsr> build_row_panels(dsvd_ctx* ctx, const DevCsr& m, const std::vector<int64_t>& bounds) {
+    cudaStream_t st = ctx->stream;
+    const int np = static_cast<int>(bounds.size()) - 1;
+    std::vector<int64_t> hoff(bounds.size());
+    for (size_t i = 0; i < bounds.size(); ++i)
+        DSVD_CUDA_CHECK(cudaMemcpyAsync(&hoff[i], m.off + bounds[i], sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    DSVD_CUDA_CHECK(cudaStreamSynchronize(st));
+    CsrAlloc al{ctx, "panel.", nullptr};
+    int32_t* sc = static_cast<int32_t*>(al.get("scalars", sizeof(int32_t) * 8 * (np > 0 ? np : 1)));
+    DSVD_CUDA_CHECK(cudaMemsetAsync(sc, 0, sizeof(int32_t) * 8 * (np > 0 ? np : 1), st));
+    std::vector<DevCsr> v(np);
+    std::vector<ChunkPlan> cp(np);
+    int64_t maxrows = 1;
+    for (int p = 0; p < np; ++p) maxrows = std::max(maxrows, bounds[p + 1] - bounds[p]);
+    const size_t scratch_bytes = order_scratch_bytes(maxrows);
+    void* scratch = ctx->buf("panel.scratch", scratch_bytes);
+    for (int p = 0; p < np; ++p) {
+        DevCsr& d = v[p];
+        const std::string tag = "p" + std::to_string(p);
+        d.rows = bounds[p + 1] - bounds[p];
+        d.cols = m.cols;
+        d.nnz = hoff[p + 1] - hoff[p];
+        d.off = m.off + bounds[p];
+        d.idx = m.idx;
+        d.val = m.val;
+        d.max_row_nnz = m.max_row_nnz;
+        d.uniform = m.uniform;
+        d.uval = m.uval;
+        d.hub_threshold = m.hub_threshold;
+        d.split_chunk = m.split_chunk;
+        const int64_t r = d.rows > 0 ? d.rows : 1;
+        d.order = static_cast<int32_t*>(al.get(tag + ".order", sizeof(int32_t) * r));
+        d.obeg = static_cast<int64_t*>(al.get(tag + ".obeg", sizeof(int64_t) * r));
+        d.olen = static_cast<int32_t*>(al.get(tag + ".olen", sizeof(int32_t) * r));
+        d.d_hub_rows = sc + 8 * p;
+        d.d_nonempty = sc + 8 * p + 1;
+        d.d_long = sc + 8 * p + 2;
+        build_row_order(d, scratch, scratch_bytes, st);
+        count_launch(d.rows > 0 ? 4 : 0);
+        if (d.split_chunk > 0) plan_chunks_count(ctx, al, d, tag, ctx->split_panel_rows, sc + 8 * p + 4, cp[p]);
+    }
+    std::vector<int32_t> h(8 * (np > 0 ? np : 1));
+    DSVD_CUDA_CHECK(cudaMemcpyAsync(h.data(), sc, sizeof(int32_t) * h.size(), cudaMemcpyDeviceToHost, st));
+    DSVD_CUDA_CHECK(cudaStreamSynchronize(st));
+    for (int p = 0; p < np; ++p) {
+        DevCsr& d = v[p];
+        const int32_t* hp = h.data() + 8 * p;
+        d.hub_rows = d.rows > 0 ? hp[0] : 0;
+        d.nonempty_rows = d.rows > 0 ? hp[1] : 0;
+        d.long_rows = d.rows > 0 ? hp[2] : 0;
+        if (d.split_chunk > 0) plan_chunks_emit(ctx, al, d, "p" + std::to_string(p), cp[p], hp[4], hp[5]);
+    }
+    return v;
+}
+
 void upload_pair(dsvd_ctx* ctx, CsrAlloc& al, int64_t rows, int64_t cols, int64_t nnz,
                  const int64_t* off, const int64_t* idx, const double* val, DevCsr& a, DevCsr& at) {
     cudaStream_t st = ctx->stream;
@@ -479,7 +541,8 @@ void solve_tall(dsvd_ctx* ctx, const DevCsr& A, const DevCsr& AT, const dsvd_con
     // slab-major gathered blocks (column-slab kernel, lw-column slabs): the sketch
     // and Y = A Q are written slab-major; the pass-1 operand (Q or T, row-major
     // for the dense kernels) is copied into Xs before each A pass
-    const int lw = slab_layout_width(ctx, ld);
+    const int64_t big_rows = std::max(m, n);
+    const int lw = slab_layout_width(ctx, ld, big_rows);
     double* Y = ctx->tbuf<double>("Y", block_doubles(m, ld, lw));  // Omega, then A Q, then B
     double* Xs = lw > 0 ? ctx->tbuf<double>("Xs", block_doubles(n, ld, lw)) : nullptr;
     double* T = ctx->tbuf<double>("T", n_full * ld);
@@ -555,6 +618,23 @@ void solve_tall(dsvd_ctx* ctx, const DevCsr& A, const DevCsr& AT, const dsvd_con
     };
     // rows of a reduced block handled by this rank, and their offset in a full block
     const int64_t red_rows = v2 ? n_slab : n;
+    // Exchange overlap (mgpu_overlap): the A^T pass in G row panels (the v2 slabs);
+    // each panel's partial is reduced (v2: to its owner rank; v1: all-reduced) on
+    // the communication stream while the next panel computes. Same values as the
+    // whole-pass collective: bitwise in the loopback group's fixed rank order.
+    const bool overlap = sharded && ctx->nranks > 1 && ctx->mgpu_overlap;
+    std::vector<DevCsr> panels;
+    if (overlap) {
+        const int64_t ps = ceil_div(n, ctx->nranks);
+        std::vector<int64_t> bounds;
+        for (int g = 0; g <= ctx->nranks; ++g) bounds.push_back(std::min(n, g * ps));
+        panels = build_row_panels(ctx, AT, bounds);
+        if (!ctx->comm_stream) DSVD_CUDA_CHECK(cudaStreamCreateWithFlags(&ctx->comm_stream, cudaStreamNonBlocking));
+        if (!ctx->comm_ev) DSVD_CUDA_CHECK(cudaEventCreateWithFlags(&ctx->comm_ev, cudaEventDisableTiming));
+        int64_t maxc = 0;
+        for (const DevCsr& pv : panels) maxc = std::max(maxc, pv.nchunks);
+        if (maxc > 0) ctx->tbuf<double>("spmm.partial", maxc * ld);  // sized once, before the loop
+    }
     // SpMM launches of the loop: pass 1 (A x -> Y) reads its row-major operand
     // through the slab-major copy Xs and writes Y slab-major when lw > 0; pass 2
     // (A^T Y [- alpha q] -> out, row-major) then gathers the slab-major Y
@@ -592,7 +672,7 @@ void solve_tall(dsvd_ctx* ctx, const DevCsr& A, const DevCsr& AT, const dsvd_con
             sa.y_slab = y_slab_major;
             sa.skip_empty = y_slab_major;  // the loop's A Q: empty rows of A are never gathered by A^T
         }
-        spmm(sa, st, spmm_var(ctx, ld), ctx->side, ctx->fork, ctx->join, partial_for(ctx, A, ld));
+        spmm(sa, st, spmm_var(ctx, ld, big_rows), ctx->side, ctx->fork, ctx->join, partial_for(ctx, A, ld));
         count_launch();
     };
     auto pass2 = [&](double* out, const double* q, const double* alpha, const int32_t* g) {
@@ -602,8 +682,39 @@ void solve_tall(dsvd_ctx* ctx, const DevCsr& A, const DevCsr& AT, const dsvd_con
             sa.slab = lw;
             sa.x_slab = true;
         }
-        spmm(sa, st, spmm_var(ctx, ld), ctx->side, ctx->fork, ctx->join, partial_for(ctx, AT, ld));
+        spmm(sa, st, spmm_var(ctx, ld, big_rows), ctx->side, ctx->fork, ctx->join, partial_for(ctx, AT, ld));
         count_launch();
+    };
+    // Sharded A^T pass + exchange: returns the reduced block (v1: part, v2: S)
+    auto pass2_reduce = [&](double* part, const int32_t* g) -> double* {
+        if (!overlap) {
+            pass2(part, nullptr, nullptr, g);
+            return reduce_partial(part);
+        }
+        const int64_t ps = ceil_div(n, ctx->nranks);
+        for (int p = 0; p < ctx->nranks; ++p) {
+            const int64_t r0 = std::min(n, p * ps);
+            SpmmArgs sa{&panels[p], Y, part + r0 * ld, ld, l, nullptr, nullptr, g};
+            sa.idx_tag = tag_at;
+            if (lw > 0) {
+                sa.slab = lw;
+                sa.x_slab = true;
+            }
+            spmm(sa, st, spmm_var(ctx, ld, big_rows), ctx->side, ctx->fork, ctx->join,
+                 partial_for(ctx, panels[p], ld));
+            count_launch();
+            DSVD_CUDA_CHECK(cudaEventRecord(ctx->comm_ev, st));
+            DSVD_CUDA_CHECK(cudaStreamWaitEvent(ctx->comm_stream, ctx->comm_ev, 0));
+            if (v2)  // rows [p n_slab, (p+1) n_slab) of the sum (zero padding rows included) to rank p
+                comm_reduce_sum(ctx, part + p * n_slab * ld, S, static_cast<size_t>(n_slab * ld), p,
+                                ctx->comm_stream);
+            else
+                comm_allreduce_sum(ctx, part + r0 * ld, static_cast<size_t>((std::min(n, r0 + ps) - r0) * ld),
+                                   ctx->comm_stream);
+        }
+        DSVD_CUDA_CHECK(cudaEventRecord(ctx->comm_ev, ctx->comm_stream));
+        DSVD_CUDA_CHECK(cudaStreamWaitEvent(st, ctx->comm_ev, 0));
+        return v2 ? S : part;
     };
     // eigSVD factors of a reduced block (v2: slab Gram + l x l all-reduce)
     auto factors = [&](const double* c, const LoopStep* lsp, const int32_t* g, cudaStream_t es) {
@@ -693,11 +804,13 @@ void solve_tall(dsvd_ctx* ctx, const DevCsr& A, const DevCsr& AT, const dsvd_con
             Qobs[1] = ctx->tbuf<double>("obs.q1", n * ld);
         }
         // T_0 = A^T Omega; eigSVD(T_0) gives Q_0 = T_0 W_0 (solver.cpp:84)
+        double* red0 = nullptr;
         sp = ctx->span_begin(K_SPMM2);
-        pass2(Tb[0], nullptr, nullptr, nullptr);
+        if (sharded) red0 = pass2_reduce(Tb[0], nullptr);
+        else pass2(Tb[0], nullptr, nullptr, nullptr);
         ctx->span_end(sp);
         if (sharded) {
-            double* red = reduce_partial(Tb[0]);
+            double* red = red0;
             if (v2) {  // T_0 = the gathered slabs of the sum
                 DSVD_CUDA_CHECK(cudaMemcpyAsync(Tb[0] + slab0 * ld, red, sizeof(double) * n_slab * ld,
                                                 cudaMemcpyDeviceToDevice, st));
@@ -730,13 +843,14 @@ void solve_tall(dsvd_ctx* ctx, const DevCsr& A, const DevCsr& AT, const dsvd_con
             if (ctx->shift_after) {
                 // P = A^T Z before the wait (both passes overlap the eig), then
                 // P <- fma(-alpha, T_{j-1}, P): the same bits as the fused epilogue
+                double* red = P;
                 sp = ctx->span_begin(K_SPMM2);
-                pass2(P, nullptr, nullptr, dash ? &ctrl->stop_pending : gate);
+                if (sharded) red = pass2_reduce(P, dash ? &ctrl->stop_pending : gate);
+                else pass2(P, nullptr, nullptr, dash ? &ctrl->stop_pending : gate);
                 ctx->span_end(sp);
                 DSVD_CUDA_CHECK(cudaStreamWaitEvent(st, ctx->ev_eig, 0));
                 loop_begin(ctrl, st);
                 count_launch();
-                double* red = sharded ? reduce_partial(P) : P;
                 shift_update(red, tprev + slab0 * ld, red_rows * ld, &ctrl->alpha, gate, st);
                 count_launch();
                 rescale_into(red, Tb[j % 2], gate);
@@ -745,12 +859,12 @@ void solve_tall(dsvd_ctx* ctx, const DevCsr& A, const DevCsr& AT, const dsvd_con
                 loop_begin(ctrl, st);
                 count_launch();
                 // P = A^T Z - alpha T_{j-1}  (the shift skipped when alpha == 0)
-                sp = ctx->span_begin(K_SPMM2);
-                pass2(P, sharded ? nullptr : tprev, sharded ? nullptr : &ctrl->alpha, gate);
-                ctx->span_end(sp);
                 double* red = P;
+                sp = ctx->span_begin(K_SPMM2);
+                if (sharded) red = pass2_reduce(P, gate);
+                else pass2(P, tprev, &ctrl->alpha, gate);
+                ctx->span_end(sp);
                 if (sharded) {
-                    red = reduce_partial(P);
                     shift_update(red, tprev + slab0 * ld, red_rows * ld, &ctrl->alpha, gate, st);
                     count_launch();
                 }
@@ -794,9 +908,10 @@ void solve_tall(dsvd_ctx* ctx, const DevCsr& A, const DevCsr& AT, const dsvd_con
     } else {
         // Q = eigSVD(A^T Omega).u
         sp = ctx->span_begin(K_SPMM2);
-        pass2(T, nullptr, nullptr, nullptr);
+        const double* red0 = T;
+        if (sharded) red0 = pass2_reduce(T, nullptr);
+        else pass2(T, nullptr, nullptr, nullptr);
         ctx->span_end(sp);
-        const double* red0 = sharded ? reduce_partial(T) : T;
         factors(red0, nullptr, nullptr, nullptr);
         rescale_into(red0, Qb[0], nullptr);
 
@@ -817,12 +932,12 @@ void solve_tall(dsvd_ctx* ctx, const DevCsr& A, const DevCsr& AT, const dsvd_con
             ctx->span_end(sp);
             // T = A^T Y - alpha Q  (add_scaled skipped when alpha == 0)
             sp = ctx->span_begin(K_SPMM2);
-            pass2(T, sharded ? nullptr : Qb[cur], sharded ? nullptr : &ctrl->alpha, gate);
-            ctx->span_end(sp);
             double* red = T;
+            if (sharded) red = pass2_reduce(T, gate);
+            else pass2(T, Qb[cur], &ctrl->alpha, gate);
+            ctx->span_end(sp);
             if (sharded) {
                 // sum the partials first, then apply the shift once (solver.cpp:94)
-                red = reduce_partial(T);
                 shift_update(red, Qb[cur] + slab0 * ld, red_rows * ld, &ctrl->alpha, gate, st);
                 count_launch();
             }
@@ -1107,7 +1222,7 @@ void pregenerate_omega(dsvd_ctx* ctx, int64_t rows, int64_t cols, const dsvd_con
     const int64_t l = cfg.k + effective_s(cfg);
     if (l > 512 || m < 1) return;
     const int64_t ld = padded_ld(l);
-    const int lw = slab_layout_width(ctx, ld);
+    const int lw = slab_layout_width(ctx, ld, std::max(rows, cols));  // as solve_tall
     double* Y = ctx->tbuf<double>("Y", block_doubles(m, ld, lw));
     if (!ctx->omega_ev) DSVD_CUDA_CHECK(cudaEventCreateWithFlags(&ctx->omega_ev, cudaEventDisableTiming));
     DSVD_CUDA_CHECK(cudaEventRecord(ctx->fork, ctx->stream));  // earlier work on Y is done
@@ -1243,6 +1358,8 @@ int dsvd_ctx_destroy(dsvd_ctx* ctx) {
         if (ctx->omega_ev) cudaEventDestroy(ctx->omega_ev);
         if (ctx->copy_ev) cudaEventDestroy(ctx->copy_ev);
         if (ctx->copy) cudaStreamDestroy(ctx->copy);
+        if (ctx->comm_ev) cudaEventDestroy(ctx->comm_ev);
+        if (ctx->comm_stream) cudaStreamDestroy(ctx->comm_stream);
         cudaStreamDestroy(ctx->stream);
         delete ctx;
     });
@@ -1355,6 +1472,9 @@ int dsvd_ctx_set_option(dsvd_ctx* ctx, const char* name, int64_t value) {
         } else if (n == "mgpu_mode") {
             if (value < 1 || value > 2) fail(DSVD_CONFIG, "mgpu_mode: 1 = all-reduce (v1), 2 = reduce-scatter (v2)");
             ctx->mgpu_mode = static_cast<int>(value);
+        } else if (n == "mgpu_overlap") {
+            if (value < 0 || value > 1) fail(DSVD_CONFIG, "mgpu_overlap must be 0 or 1");
+            ctx->mgpu_overlap = static_cast<int>(value);
         } else if (n == "split_chunk") {
             if (value < 0) fail(DSVD_CONFIG, "split_chunk must be >= 0");
             ctx->split_chunk = value;

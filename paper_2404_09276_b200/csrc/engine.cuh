@@ -31,7 +31,11 @@ struct TimedSpan {
 // all-gather then copy when send != recv).
 enum CommKind { COMM_NONE = 0, COMM_NCCL = 1, COMM_LOOPBACK = 2 };
 constexpr int kMaxLoopbackRanks = 8;
-void comm_allreduce_sum(dsvd_ctx* ctx, double* buf, size_t count);
+// (stream: the stream the collective is ordered on, nullptr = ctx->stream)
+void comm_allreduce_sum(dsvd_ctx* ctx, double* buf, size_t count, cudaStream_t stream = nullptr);
+// recv (count, significant on rank `root` only) = the sum of every rank's send
+void comm_reduce_sum(dsvd_ctx* ctx, const double* send, double* recv, size_t count, int root,
+                     cudaStream_t stream = nullptr);
 // recv (recvcount) = rows [rank * recvcount, (rank + 1) * recvcount) of the sum of every rank's send
 void comm_reduce_scatter_sum(dsvd_ctx* ctx, const double* send, double* recv, size_t recvcount);
 // recv (nranks * sendcount) = every rank's send in rank order (send may be this rank's slot of recv)
@@ -118,6 +122,12 @@ struct dsvd_ctx {
     // redundant), 2 = v2 (reduce-scatter, slab Gram + l x l all-reduce, slab
     // rescale, all-gather); SURVEY 8e
     int mgpu_mode = 2;
+    // sharded solves: the A^T pass runs in G row panels (the v2 slabs) and each
+    // panel's partial is reduced on comm_stream while the next panel computes (1,
+    // default), or the whole pass first and then one collective (0)
+    int mgpu_overlap = 1;
+    cudaStream_t comm_stream = nullptr;
+    cudaEvent_t comm_ev = nullptr;
     int64_t shard_row_offset = 0, shard_global_rows = -1;  // for the CSR entry points
 
     void* buf(const std::string& name, size_t bytes) {
@@ -166,13 +176,14 @@ struct dsvd_ctx {
 namespace dsvd {
 // The spmm() variant bits of a launch at row stride ld: the context's explicit
 // spmm_variant, plus the column-slab kernel where it pays.
-inline int spmm_var(const dsvd_ctx* ctx, int64_t ld);
+// big_rows: the row count of the solve's larger n-row / m-row block (0: unknown).
+inline int spmm_var(const dsvd_ctx* ctx, int64_t ld, int64_t big_rows = 0);
 // Slab width of the slab-major X / Y blocks of a solve at row stride ld (0: all
 // row-major): the column-slab kernel's width when it runs in split mode and
 // the context allows the layout (option "slab_layout").
-inline int slab_layout_width(const dsvd_ctx* ctx, int64_t ld) {
+inline int slab_layout_width(const dsvd_ctx* ctx, int64_t ld, int64_t big_rows = 0) {
     if (!ctx->slab_layout || ctx->split_chunk <= 0) return 0;
-    const int v = spmm_var(ctx, ld);
+    const int v = spmm_var(ctx, ld, big_rows);
     if ((v & (16 | 32)) != 0) return 0;
     return (v & 4096) ? 32 : (v & 8192) ? 64 : 0;
 }
@@ -180,14 +191,16 @@ inline int slab_layout_width(const dsvd_ctx* ctx, int64_t ld) {
 inline int64_t block_doubles(int64_t rows, int64_t ld, int lw) {
     return lw > 0 ? std::max(rows * ld, ceil_div(ld, lw) * lw * rows) : rows * ld;
 }
-inline int spmm_var(const dsvd_ctx* ctx, int64_t ld) {
+inline int spmm_var(const dsvd_ctx* ctx, int64_t ld, int64_t big_rows) {
     int v = ctx->spmm_variant;
     if ((v & (4096 | 8192)) != 0) return v;  // explicit choice
     int w = ctx->spmm_slab;
     // auto: 64-column slabs above 192 columns (C4, l = 300: both passes 10-15%
-    // faster than the whole-row kernel, tools/ab_option.py); the
-    // whole-row kernel below (C2, l = 150: it gathers from an L2-resident X)
-    if (w < 0) w = ld > 192 ? 64 : 0;
+    // faster than the whole-row kernel, tools/ab_option.py); below,
+    // 32-column slabs when the gathered blocks are far beyond the L2 (> 1 GB: C5
+    // 2.96 -> 2.74 s, C3 -1.5%), the whole-row kernel otherwise (C2: X and Y of
+    // 122 / 243 MB stay mostly L2-resident, slabs +20%)
+    if (w < 0) w = ld > 192 ? 64 : (big_rows * ld * 8 > (int64_t(1) << 30) ? 32 : 0);
     if (w == 32) v |= 4096;
     else if (w == 64) v |= 8192;
     if (w > 0 && ctx->spmm_slab_hint) v |= 16384;

@@ -186,3 +186,40 @@ def test_sharded_rerun_is_deterministic(c1):
     for rx, ry in zip(x, y):
         assert np.array_equal(rx.svd.s.view(np.uint64), ry.svd.s.view(np.uint64))
         assert np.array_equal(rx.svd.u.view(np.uint64), ry.svd.u.view(np.uint64))
+
+
+def assert_same_bits(x, y):
+    for rx, ry in zip(x, y):
+        assert rx.trace.iterations == ry.trace.iterations
+        for name in ("u", "s", "v"):
+            a, b = getattr(rx.svd, name), getattr(ry.svd, name)
+            assert np.array_equal(np.ascontiguousarray(a).view(np.uint64), np.ascontiguousarray(b).view(np.uint64))
+
+
+@pytest.mark.parametrize("mode", [1, 2])
+@pytest.mark.parametrize("pipeline", [0, 1])
+def test_exchange_overlap_is_bitwise_the_whole_pass_exchange(plaw, mode, pipeline):
+    """mgpu_overlap = 1 (default): the A^T pass runs in G row panels and each
+    panel's partial is reduced on the communication stream while the next panel
+    computes (v2: ncclReduce to the panel's owner; v1: a per-panel all-reduce).
+    The panels' rows (split hub columns included) are computed exactly as in the
+    whole pass, so the factors are bitwise those of the whole-pass exchange."""
+    cfg = d.SolverConfig(k=24, s=12, tol=1e-2, p_max=20, seed=4)
+    bounds = shard_bounds(plaw.offsets, 3)
+    x = run_sharded(plaw, cfg, bounds, {"mgpu_mode": mode, "pipeline": pipeline, "mgpu_overlap": 0})
+    y = run_sharded(plaw, cfg, bounds, {"mgpu_mode": mode, "pipeline": pipeline, "mgpu_overlap": 1})
+    assert_same_bits(x, y)
+
+
+def test_exchange_overlap_wide_sketch_matches_oracle(oracle, plaw):
+    """l = 200 (> 192: the column-slab SpMM with slab-major Y) with the panelled
+    exchange: against the oracle and bitwise the whole-pass exchange."""
+    k, s = 120, 80
+    cfg = d.SolverConfig(k=k, s=s, p=3, alg=d.Algorithm.shifted, seed=6)
+    ref = oracle.solve(Csr(plaw.rows, plaw.cols, plaw.offsets, plaw.col_indices, plaw.values), k, s, p=3,
+                       alg="shifted", seed=6)
+    bounds = shard_bounds(plaw.offsets, 2)
+    y = run_sharded(plaw, cfg, bounds, {"mgpu_overlap": 1})
+    check_against(y, ref, k)
+    x = run_sharded(plaw, cfg, bounds, {"mgpu_overlap": 0})
+    assert_same_bits(x, y)
