@@ -126,6 +126,9 @@ struct dsvd_ctx {
     // panel's partial is reduced on comm_stream while the next panel computes (1,
     // default), or the whole pass first and then one collective (0)
     int mgpu_overlap = 1;
+    // single-GPU shifted-family solves on the non-empty columns only (engine.cu
+    // build_compact): 1 (default) when >= 2% of the columns are empty, 0 off
+    int compact_cols = 1;
     cudaStream_t comm_stream = nullptr;
     cudaEvent_t comm_ev = nullptr;
     int64_t shard_row_offset = 0, shard_global_rows = -1;  // for the CSR entry points

@@ -1530,4 +1530,82 @@ void build_row_order(DevCsr& m, void* scratch, size_t scratch_bytes, cudaStream_
     }
 }
 
+namespace {
+__global__ void row_flags_kernel(const int64_t* __restrict__ off, int64_t rows, int32_t* __restrict__ flag) {
+    for (int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; r < rows;
+         r += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        flag[r] = off[r + 1] > off[r] ? 1 : 0;
+}
+__global__ void compact_place_kernel(const int64_t* __restrict__ off, int64_t rows, const int32_t* __restrict__ flag,
+                                     const int32_t* __restrict__ pos, int32_t* __restrict__ newid,
+                                     int32_t* __restrict__ oldid, int64_t* __restrict__ off_c) {
+    for (int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; r < rows;
+         r += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        if (flag[r]) {
+            const int32_t p = pos[r];
+            newid[r] = p;
+            oldid[p] = static_cast<int32_t>(r);
+            off_c[p] = off[r];
+        } else {
+            newid[r] = -1;
+        }
+        if (r == rows - 1) off_c[pos[r] + flag[r]] = off[rows];
+    }
+}
+__global__ void remap_ids_kernel(const int32_t* __restrict__ in, int64_t n, const int32_t* __restrict__ map,
+                                 int32_t* __restrict__ out) {
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int32_t v = map[in[i]];
+        DSVD_DCHECK(v >= 0);
+        out[i] = v;
+    }
+}
+__global__ void scatter_rows_kernel(const double* __restrict__ src, int64_t rows_c, int64_t k,
+                                    const int32_t* __restrict__ oldid, double* __restrict__ dst, int64_t rows) {
+    const int64_t total = rows_c * k;
+    for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
+         e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t c = e / rows_c, i = e - c * rows_c;
+        dst[c * rows + oldid[i]] = src[e];
+    }
+}
+}  // namespace
+
+size_t compact_scratch_bytes(int64_t rows) {
+    size_t temp = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, temp, static_cast<const int32_t*>(nullptr), static_cast<int32_t*>(nullptr),
+                                  static_cast<int>(rows > 0 ? rows : 1));
+    return 2 * align_up(sizeof(int32_t) * (rows > 0 ? rows : 1)) + align_up(temp);
+}
+
+void compact_rows_map(const int64_t* off, int64_t rows, int32_t* newid, int32_t* oldid, int64_t* off_c,
+                      void* scratch, size_t scratch_bytes, cudaStream_t stream) {
+    if (rows == 0) return;
+    char* p = static_cast<char*>(scratch);
+    const size_t seg = align_up(sizeof(int32_t) * rows);
+    int32_t* flag = reinterpret_cast<int32_t*>(p);
+    int32_t* pos = reinterpret_cast<int32_t*>(p + seg);
+    size_t tb = scratch_bytes - 2 * seg;
+    row_flags_kernel<<<grid_for(rows), 256, 0, stream>>>(off, rows, flag);
+    DSVD_LAUNCH_CHECK();
+    DSVD_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(p + 2 * seg, tb, flag, pos, static_cast<int>(rows), stream));
+    compact_place_kernel<<<grid_for(rows), 256, 0, stream>>>(off, rows, flag, pos, newid, oldid, off_c);
+    DSVD_LAUNCH_CHECK();
+}
+
+void remap_ids(const int32_t* in, int64_t n, const int32_t* map, int32_t* out, cudaStream_t stream) {
+    if (n == 0) return;
+    remap_ids_kernel<<<grid_for(n), 256, 0, stream>>>(in, n, map, out);
+    DSVD_LAUNCH_CHECK();
+}
+
+void scatter_rows_colmajor(const double* src, int64_t rows_c, int64_t k, const int32_t* oldid, double* dst,
+                           int64_t rows, cudaStream_t stream) {
+    DSVD_CUDA_CHECK(cudaMemsetAsync(dst, 0, sizeof(double) * rows * k, stream));
+    if (rows_c * k == 0) return;
+    scatter_rows_kernel<<<grid_for(rows_c * k), 256, 0, stream>>>(src, rows_c, k, oldid, dst, rows);
+    DSVD_LAUNCH_CHECK();
+}
+
 }  // namespace dsvd

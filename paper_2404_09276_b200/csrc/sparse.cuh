@@ -143,6 +143,19 @@ void build_transpose(const DevCsr& a, DevCsr& at, void* scratch, size_t scratch_
 size_t order_scratch_bytes(int64_t rows);
 void build_row_order(DevCsr& m, void* scratch, size_t scratch_bytes, cudaStream_t stream);
 
+// Compaction of a CSR's empty rows (engine.cu build_compact): newid[r] = the
+// rank of row r among the non-empty rows (-1 if empty), oldid its inverse,
+// off_c the offsets of the non-empty rows (positions unchanged) + nnz.
+size_t compact_scratch_bytes(int64_t rows);
+void compact_rows_map(const int64_t* off, int64_t rows, int32_t* newid, int32_t* oldid, int64_t* off_c,
+                      void* scratch, size_t scratch_bytes, cudaStream_t stream);
+// out[i] = map[in[i]] (column indices, row orders)
+void remap_ids(const int32_t* in, int64_t n, const int32_t* map, int32_t* out, cudaStream_t stream);
+// dst (rows x k, column-major, leading dim rows) = 0 except rows oldid[i] =
+// src row i (src: rows_c x k column-major)
+void scatter_rows_colmajor(const double* src, int64_t rows_c, int64_t k, const int32_t* oldid, double* dst,
+                           int64_t rows, cudaStream_t stream);
+
 // int64 -> int32 column indices with a bounds check; *bad is set to 1 when an
 // index falls outside [0, cols) (the entry is clamped so no kernel faults).
 void narrow_indices(const int64_t* src, int32_t* dst, int64_t nnz, int64_t cols, int32_t* bad,

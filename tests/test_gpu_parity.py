@@ -999,3 +999,58 @@ def test_eig_overlap_wide_sketch(oracle, alg, kw):
         assert r.trace.iterations == res[0].trace.iterations
         for name in ("u", "s", "v"):
             assert_bitwise(getattr(res[0].svd, name), getattr(r.svd, name))
+
+
+def _rmat_host(scale, draws, seed):
+    dv = d.Device(0)
+    m = d.rmat(scale, draws, seed=seed, device=dv)
+    a = m.download()
+    m.close()
+    dv.close()
+    return a
+
+
+@pytest.mark.parametrize("alg,kw", [("shifted", dict(p=4)), ("dash", dict(tol=1e-2))])
+def test_compact_cols_matches_oracle_and_the_full_solve(oracle, alg, kw):
+    """An R-MAT graph with ~half of its columns empty: the solve runs on the
+    non-empty columns only (compact_cols = 1, default) and scatters V back.
+    Against the oracle (which computes every zero row) and the uncompacted
+    device solve: the same N_p, sigma and subspaces to rounding, and V exactly
+    zero on the empty columns."""
+    a = _rmat_host(13, 60000, 3)
+    empty = np.bincount(a.col_indices, minlength=a.cols) == 0
+    assert 0.2 * a.cols < empty.sum() < 0.8 * a.cols
+    ca = Csr(a.rows, a.cols, a.offsets, a.col_indices, a.values)
+    ref = oracle.solve(ca, 40, 20, alg=alg, seed=4, **kw)
+    cfg = d.SolverConfig(k=40, s=20, alg=d.Algorithm[alg], seed=4, **kw)
+    out = []
+    for cc in (1, 0):
+        dv = d.Device(0)
+        dv.set_option("compact_cols", cc)
+        out.append(d.solve(a, cfg, device=dv))
+        dv.close()
+    res, full = out
+    check_solve(res, ref, 40)
+    assert np.all(res.svd.v[empty] == 0.0)
+    assert res.trace.iterations == full.trace.iterations
+    np.testing.assert_allclose(res.svd.s, full.svd.s, rtol=1e-12)
+    assert sin_theta(full.svd.u, res.svd.u) <= 1e-10
+    assert sin_theta(full.svd.v, res.svd.v) <= 1e-10
+
+
+def test_compact_cols_wide_orientation(oracle):
+    """A wide matrix (rows < cols) is solved on its transpose, whose empty
+    columns are A's empty rows: U is the scattered factor there."""
+    a = _rmat_host(13, 60000, 8)
+    r = 3000  # the first rows: a 3000 x 8192 wide matrix with empty rows
+    w = d.SparseMatrix(r, a.cols, a.offsets[:r + 1].copy(), a.col_indices[:a.offsets[r]].copy(),
+                       a.values[:a.offsets[r]].copy())
+    empty_rows = np.diff(w.offsets) == 0
+    assert empty_rows.sum() > 0.05 * r
+    ref = oracle.solve(Csr(w.rows, w.cols, w.offsets, w.col_indices, w.values), 30, 15, p=3, alg="shifted",
+                       seed=1)
+    dv = d.Device(0)
+    res = d.solve(w, d.SolverConfig(k=30, s=15, p=3, alg=d.Algorithm.shifted, seed=1), device=dv)
+    dv.close()
+    check_solve(res, ref, 30)
+    assert np.all(res.svd.u[empty_rows] == 0.0)
