@@ -15,14 +15,25 @@ namespace {
 constexpr int kTile = 64;
 constexpr int kK = 16;
 
+// row_off (optional): the CSR offsets of the matrix whose rows these are; rows
+// without nonzeros are never gathered (A^T Omega reads Omega at A's non-empty
+// rows only), so they are written as 0.0 instead of drawn — the drawn rows are
+// bit for bit the same.
+__device__ __forceinline__ bool row_empty(const int64_t* __restrict__ row_off, int64_t i) {
+    return row_off != nullptr && __ldg(row_off + i) == __ldg(row_off + i + 1);
+}
+
 __global__ void gaussian_kernel(double* __restrict__ out, int64_t rows, int64_t l, int64_t ld,
-                                uint64_t seed, int64_t global_rows, int64_t row_offset, int w) {
+                                uint64_t seed, int64_t global_rows, int64_t row_offset, int w,
+                                const int64_t* __restrict__ row_off) {
     if (w > 0) {  // slab-major (sparse.cuh slab_index): writes walk the output contiguously
         const int64_t total = (ld + w - 1) / w * w * rows;
         for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
              e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
             const int64_t jj = e % w, rs = e / w, i = rs % rows, j = (rs / rows) * w + jj;
-            out[e] = j < l ? normal_at(seed, static_cast<uint64_t>(j * global_rows + row_offset + i)) : 0.0;
+            out[e] = j < l && !row_empty(row_off, i)
+                         ? normal_at(seed, static_cast<uint64_t>(j * global_rows + row_offset + i))
+                         : 0.0;
         }
         return;
     }
@@ -35,7 +46,9 @@ __global__ void gaussian_kernel(double* __restrict__ out, int64_t rows, int64_t 
         for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < static_cast<uint32_t>(total);
              e += gridDim.x * blockDim.x) {
             const uint32_t i = e / ld32, j = e - i * ld32;
-            out[e] = j < l ? normal_at(seed, static_cast<uint64_t>(j) * global_rows + row_offset + i) : 0.0;
+            out[e] = j < l && !row_empty(row_off, i)
+                         ? normal_at(seed, static_cast<uint64_t>(j) * global_rows + row_offset + i)
+                         : 0.0;
         }
         return;
     }
@@ -43,7 +56,9 @@ __global__ void gaussian_kernel(double* __restrict__ out, int64_t rows, int64_t 
          e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
         const int64_t i = e / ld;
         const int64_t j = e - i * ld;
-        out[e] = j < l ? normal_at(seed, static_cast<uint64_t>(j * global_rows + row_offset + i)) : 0.0;
+        out[e] = j < l && !row_empty(row_off, i)
+                     ? normal_at(seed, static_cast<uint64_t>(j * global_rows + row_offset + i))
+                     : 0.0;
     }
 }
 
@@ -420,11 +435,12 @@ int grid_for(int64_t n) {
 }  // namespace
 
 void gaussian_rowmajor(double* out, int64_t rows, int64_t l, int64_t ld, uint64_t seed,
-                       cudaStream_t stream, int64_t global_rows, int64_t row_offset, int slab_w) {
+                       cudaStream_t stream, int64_t global_rows, int64_t row_offset, int slab_w,
+                       const int64_t* row_off) {
     if (rows * ld == 0) return;
     if (global_rows < 0) global_rows = rows;
     gaussian_kernel<<<grid_for(rows * ld), 256, 0, stream>>>(out, rows, l, ld, seed, global_rows,
-                                                             row_offset, slab_w);
+                                                             row_offset, slab_w, row_off);
     DSVD_LAUNCH_CHECK();
 }
 

@@ -11,8 +11,11 @@ namespace dsvd {
 // For a row shard, rows [row_offset, row_offset + rows) of the global
 // global_rows x l sketch are generated (global_rows < 0 means rows).
 // slab_w > 0: written slab-major instead (sparse.cuh slab_index, width slab_w).
+// row_off (optional, device CSR offsets of the matrix these rows belong to):
+// rows without nonzeros are written as 0.0 instead of drawn (never gathered).
 void gaussian_rowmajor(double* out, int64_t rows, int64_t l, int64_t ld, uint64_t seed,
-                       cudaStream_t stream, int64_t global_rows = -1, int64_t row_offset = 0, int slab_w = 0);
+                       cudaStream_t stream, int64_t global_rows = -1, int64_t row_offset = 0, int slab_w = 0,
+                       const int64_t* row_off = nullptr);
 
 // t = fma(-alpha, q, t) elementwise unless *alpha == 0 (add_scaled,
 // dense_kernels.cpp:128-136, as applied at solver.cpp:94). Used after the

@@ -299,12 +299,15 @@ std::vector<DevCsr> build_row_panels(dsvd_ctx* ctx, const DevCsr& m, const std::
 }
 
 void upload_pair(dsvd_ctx* ctx, CsrAlloc& al, int64_t rows, int64_t cols, int64_t nnz,
-                 const int64_t* off, const int64_t* idx, const double* val, DevCsr& a, DevCsr& at) {
+                 const int64_t* off, const int64_t* idx, const double* val, DevCsr& a, DevCsr& at,
+                 const dsvd_config* omega_cfg) {
     cudaStream_t st = ctx->stream;
     int64_t* d_off = static_cast<int64_t*>(al.get("a.off", sizeof(int64_t) * (rows + 1)));
     int64_t* d_idx64 = ctx->tbuf<int64_t>("upload.idx64", nnz);
     double* d_val = static_cast<double*>(al.get("a.val", sizeof(double) * nnz));
     DSVD_CUDA_CHECK(cudaMemcpyAsync(d_off, off, sizeof(int64_t) * (rows + 1), cudaMemcpyHostToDevice, st));
+    // the sketch on the side stream once the offsets are there (its empty rows are not drawn)
+    if (omega_cfg != nullptr) pregenerate_omega(ctx, rows, cols, *omega_cfg, d_off);
     cudaEvent_t vals = nullptr;
     if (nnz) {
         DSVD_CUDA_CHECK(cudaMemcpyAsync(d_idx64, idx, sizeof(int64_t) * nnz, cudaMemcpyHostToDevice, st));
@@ -623,7 +626,7 @@ void solve_tall(dsvd_ctx* ctx, const DevCsr& A, const DevCsr& AT, const dsvd_con
         ctx->omega_slab_w == lw) {
         DSVD_CUDA_CHECK(cudaStreamWaitEvent(st, ctx->omega_ev, 0));
     } else {
-        gaussian_rowmajor(Y, m, l, ld, cfg.seed, st, global_m, row_offset, lw);
+        gaussian_rowmajor(Y, m, l, ld, cfg.seed, st, global_m, row_offset, lw, A.off);
         count_launch();
     }
     ctx->omega_pending = false;
@@ -1273,9 +1276,13 @@ void solve_basic(dsvd_ctx* ctx, const DevCsr& A, const DevCsr& AT, const dsvd_co
     DSVD_CUDA_CHECK(cudaStreamSynchronize(st));
 }
 
+}  // namespace
+
 // Starts Omega for the solve of an m x n host matrix on the side stream, so it
 // overlaps the CSR upload that follows on the main stream (single-GPU solves).
-void pregenerate_omega(dsvd_ctx* ctx, int64_t rows, int64_t cols, const dsvd_config& cfg) {
+// d_off (optional): the device offsets of A's rows, ordered on ctx->stream; with the tall
+// orientation the sketch rows of empty rows of A are then written as zeros, not drawn.
+void pregenerate_omega(dsvd_ctx* ctx, int64_t rows, int64_t cols, const dsvd_config& cfg, const int64_t* d_off) {
     ctx->omega_pending = false;
     if (ctx->comm != nullptr || cfg.k < 1 || cfg.alg == DSVD_ALG_BASIC) return;
     const bool direct = (cfg.flags & DSVD_FLAG_DIRECT) != 0;
@@ -1288,7 +1295,7 @@ void pregenerate_omega(dsvd_ctx* ctx, int64_t rows, int64_t cols, const dsvd_con
     if (!ctx->omega_ev) DSVD_CUDA_CHECK(cudaEventCreateWithFlags(&ctx->omega_ev, cudaEventDisableTiming));
     DSVD_CUDA_CHECK(cudaEventRecord(ctx->fork, ctx->stream));  // earlier work on Y is done
     DSVD_CUDA_CHECK(cudaStreamWaitEvent(ctx->side, ctx->fork, 0));
-    gaussian_rowmajor(Y, m, l, ld, cfg.seed, ctx->side, -1, 0, lw);
+    gaussian_rowmajor(Y, m, l, ld, cfg.seed, ctx->side, -1, 0, lw, m == rows ? d_off : nullptr);
     ctx->omega_slab_w = lw;
     count_launch();
     DSVD_CUDA_CHECK(cudaEventRecord(ctx->omega_ev, ctx->side));
@@ -1297,6 +1304,8 @@ void pregenerate_omega(dsvd_ctx* ctx, int64_t rows, int64_t cols, const dsvd_con
     ctx->omega_l = l;
     ctx->omega_seed = cfg.seed;
 }
+
+namespace {
 
 void solve_pair(dsvd_ctx* ctx, const DevCsr& a, const DevCsr& at, const dsvd_config& cfg,
                 dsvd_outputs* out, dsvd_observer_fn observer, void* user, int64_t row_offset = 0,
@@ -1756,8 +1765,7 @@ int dsvd_solve_csr(dsvd_ctx* ctx, int64_t rows, int64_t cols, int64_t nnz, const
         DSVD_CUDA_CHECK(cudaEventRecord(e0, ctx->stream));
         DevCsr a, at;
         CsrAlloc al{ctx, "csr.", nullptr};
-        pregenerate_omega(ctx, rows, cols, *cfg);
-        upload_pair(ctx, al, rows, cols, nnz, offsets, col_indices, values, a, at);
+        upload_pair(ctx, al, rows, cols, nnz, offsets, col_indices, values, a, at, cfg);
         DSVD_CUDA_CHECK(cudaEventRecord(e1, ctx->stream));
         solve_pair(ctx, a, at, *cfg, out, nullptr, nullptr, ctx->shard_row_offset,
                    ctx->shard_global_rows);
@@ -1786,7 +1794,7 @@ int dsvd_solve_csr_device(dsvd_ctx* ctx, int64_t rows, int64_t cols, int64_t nnz
         DSVD_CUDA_CHECK(cudaEventRecord(e0, ctx->stream));
         DevCsr a, at;
         CsrAlloc al{ctx, "csr.", nullptr};
-        pregenerate_omega(ctx, rows, cols, *cfg);  // Omega on the side stream beside the CSC build
+        pregenerate_omega(ctx, rows, cols, *cfg, d_off);  // Omega on the side stream beside the CSC build
         build_pair(ctx, al, rows, cols, nnz, d_off, d_idx, d_val, a, at, false);
         DSVD_CUDA_CHECK(cudaEventRecord(e1, ctx->stream));
         solve_pair(ctx, a, at, *cfg, out, nullptr, nullptr, ctx->shard_row_offset,

@@ -38,8 +38,15 @@ void build_pair(dsvd_ctx* ctx, CsrAlloc& al, int64_t rows, int64_t cols, int64_t
                 const int64_t* d_idx64, const double* d_val, DevCsr& a, DevCsr& at, bool copy_inputs,
                 cudaEvent_t values_ready = nullptr);
 // The same from host arrays (values copied on ctx->copy beside the CSC build).
+// omega_cfg: also start the solve's sketch on the side stream once the offsets
+// are on the device (pregenerate_omega).
 void upload_pair(dsvd_ctx* ctx, CsrAlloc& al, int64_t rows, int64_t cols, int64_t nnz, const int64_t* off,
-                 const int64_t* idx, const double* val, DevCsr& a, DevCsr& at);
+                 const int64_t* idx, const double* val, DevCsr& a, DevCsr& at,
+                 const dsvd_config* omega_cfg = nullptr);
+// Starts the sketch Omega of a solve of an rows x cols matrix on the side stream
+// (the next solve_tall with the same shape / seed waits on it instead).
+void pregenerate_omega(dsvd_ctx* ctx, int64_t rows, int64_t cols, const dsvd_config& cfg,
+                       const int64_t* d_off = nullptr);
 
 // Partial rows of the split chunks (spmm's `partial` argument) in the context arena.
 inline double* partial_for(dsvd_ctx* ctx, const DevCsr& a, int64_t ld) {
