@@ -1054,3 +1054,46 @@ def test_compact_cols_wide_orientation(oracle):
     dv.close()
     check_solve(res, ref, 30)
     assert np.all(res.svd.u[empty_rows] == 0.0)
+
+
+def test_compact_cols_device_outputs_are_the_host_outputs():
+    """The device-resident entry point (dsvd_solve_csr_device, bench.py's `value`
+    path) with column compaction: V is scattered into the caller's device buffer
+    with zero rows, bitwise the host-output solve. (Device buffers through
+    cuda-python: importing torch after NCCL was dlopen'd by an earlier test
+    would clash with its bundled NCCL.)"""
+    rt = pytest.importorskip("cuda.bindings.runtime")
+    a = _rmat_host(12, 30000, 11)
+    k = 20
+    cfg = d.SolverConfig(k=k, s=10, p=3, alg=d.Algorithm.shifted, seed=2)
+    dv = d.Device(0)
+    host = d.solve(a, cfg, device=dv)
+    H2D, D2H = rt.cudaMemcpyKind.cudaMemcpyHostToDevice, rt.cudaMemcpyKind.cudaMemcpyDeviceToHost
+    bufs = []
+
+    def up(x):
+        err, p = rt.cudaMalloc(max(x.nbytes, 8))
+        assert err == rt.cudaError_t.cudaSuccess
+        bufs.append(p)
+        if x.nbytes:
+            assert rt.cudaMemcpy(p, x.ctypes.data, x.nbytes, H2D)[0] == rt.cudaError_t.cudaSuccess
+        return p
+
+    off = up(np.ascontiguousarray(a.offsets, dtype=np.int64))
+    idx = up(np.ascontiguousarray(a.col_indices, dtype=np.int64))
+    val = up(np.ascontiguousarray(a.values))
+    u_h = np.full((a.rows, k), np.nan, order="F")
+    v_h = np.full((a.cols, k), np.nan, order="F")
+    s_h = np.empty(k)
+    du, dvv, ds = up(u_h), up(v_h), up(s_h)
+    res = d.api.solve_device_csr(a.rows, a.cols, a.nnz, off, idx, val, cfg, du, ds, dvv, device=dv)
+    for hb, db in ((u_h, du), (v_h, dvv), (s_h, ds)):
+        assert rt.cudaMemcpy(hb.ctypes.data, db, hb.nbytes, D2H)[0] == rt.cudaError_t.cudaSuccess
+    for p in bufs:
+        rt.cudaFree(p)
+    dv.close()
+    assert res.trace.iterations == host.trace.iterations
+    assert_bitwise(s_h, host.svd.s)
+    assert_bitwise(u_h, host.svd.u)
+    assert_bitwise(v_h, host.svd.v)
+    assert (np.bincount(a.col_indices, minlength=a.cols) == 0).sum() > 0.05 * a.cols
