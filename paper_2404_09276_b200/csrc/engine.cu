@@ -160,8 +160,8 @@ void build_pair(dsvd_ctx* ctx, CsrAlloc& al, int64_t rows, int64_t cols, int64_t
     // device scalars read back by the host: {offsets bad, index bad} right away,
     // {hub rows of A, of A^T, chunk total / max of A, of A^T} in one read at the end
     // (+ [12] values not uniform, [14..15] the first value's bits)
-    int32_t* sc = static_cast<int32_t*>(al.get("plan_scalars", sizeof(int32_t) * 16));
-    DSVD_CUDA_CHECK(cudaMemsetAsync(sc, 0, sizeof(int32_t) * 16, st));
+    int32_t* sc = static_cast<int32_t*>(al.get("plan_scalars", sizeof(int32_t) * 18));
+    DSVD_CUDA_CHECK(cudaMemsetAsync(sc, 0, sizeof(int32_t) * 18, st));
     check_offsets(a.off, rows, nnz, sc, st);
     count_launch();
     narrow_indices(d_idx64, a.idx, nnz, cols, sc + 1, st);
@@ -207,6 +207,8 @@ void build_pair(dsvd_ctx* ctx, CsrAlloc& al, int64_t rows, int64_t cols, int64_t
     at.d_nonempty = sc + 9;
     a.d_long = sc + 10;
     at.d_long = sc + 11;
+    a.d_mid = sc + 16;
+    at.d_mid = sc + 17;
     build_row_order(a, scratch, scratch_bytes, st);
     count_launch(rows > 0 ? 4 : 0);
     build_row_order(at, scratch, scratch_bytes, st);
@@ -218,7 +220,7 @@ void build_pair(dsvd_ctx* ctx, CsrAlloc& al, int64_t rows, int64_t cols, int64_t
         plan_chunks_count(ctx, al, a, "a", 0, sc + 4, cpa);
         plan_chunks_count(ctx, al, at, "at", ctx->split_panel_rows, sc + 6, cpt);
     }
-    int32_t h[16];
+    int32_t h[18];
     DSVD_CUDA_CHECK(cudaMemcpyAsync(h, sc, sizeof(h), cudaMemcpyDeviceToHost, st));
     DSVD_CUDA_CHECK(cudaStreamSynchronize(st));
     a.uniform = at.uniform = ctx->uniform_values && nnz > 0 && h[12] == 0;
@@ -228,6 +230,8 @@ void build_pair(dsvd_ctx* ctx, CsrAlloc& al, int64_t rows, int64_t cols, int64_t
     at.nonempty_rows = cols > 0 ? h[9] : 0;
     a.long_rows = rows > 0 ? h[10] : 0;
     at.long_rows = cols > 0 ? h[11] : 0;
+    a.mid_rows = rows > 0 ? h[16] : 0;
+    at.mid_rows = cols > 0 ? h[17] : 0;
     a.hub_rows = rows > 0 ? h[2] : 0;
     at.hub_rows = cols > 0 ? h[3] : 0;
     if (C > 0) {
@@ -280,6 +284,7 @@ std::vector<DevCsr> build_row_panels(dsvd_ctx* ctx, const DevCsr& m, const std::
         d.d_hub_rows = sc + 8 * p;
         d.d_nonempty = sc + 8 * p + 1;
         d.d_long = sc + 8 * p + 2;
+        d.d_mid = sc + 8 * p + 3;
         build_row_order(d, scratch, scratch_bytes, st);
         count_launch(d.rows > 0 ? 4 : 0);
         if (d.split_chunk > 0) plan_chunks_count(ctx, al, d, tag, ctx->split_panel_rows, sc + 8 * p + 4, cp[p]);
@@ -293,6 +298,7 @@ std::vector<DevCsr> build_row_panels(dsvd_ctx* ctx, const DevCsr& m, const std::
         d.hub_rows = d.rows > 0 ? hp[0] : 0;
         d.nonempty_rows = d.rows > 0 ? hp[1] : 0;
         d.long_rows = d.rows > 0 ? hp[2] : 0;
+        d.mid_rows = d.rows > 0 ? hp[3] : 0;
         if (d.split_chunk > 0) plan_chunks_emit(ctx, al, d, "p" + std::to_string(p), cp[p], hp[4], hp[5]);
     }
     return v;
@@ -558,6 +564,7 @@ Compact build_compact(dsvd_ctx* ctx, const DevCsr& A, const DevCsr& AT) {
     c.at.order = order_c;
     c.at.nonempty_rows = nne;
     if (c.at.long_rows > nne) c.at.long_rows = nne;
+    if (c.at.mid_rows > nne) c.at.mid_rows = nne;
     c.oldid = oldid;
     return c;
 }
@@ -1490,6 +1497,9 @@ int dsvd_ctx_set_option(dsvd_ctx* ctx, const char* name, int64_t value) {
         } else if (n == "gram_tiles") {
             if (value != 2 && value != 4) fail(DSVD_CONFIG, "gram_tiles must be 2 or 4");
             set_gram_wide_tiles(static_cast<int>(value));
+        } else if (n == "spmm_short_rows") {
+            if (value < 0 || value > 2) fail(DSVD_CONFIG, "spmm_short_rows: 0 off, 1 rows <= 8 nonzeros, 2 rows <= 32");
+            set_spmm_short_rows(static_cast<int>(value));
         } else if (n == "gram_waves") {
             if (value < 1 || value > 64) fail(DSVD_CONFIG, "gram_waves must be in [1, 64]");
             set_gram_wide_waves(static_cast<int>(value));

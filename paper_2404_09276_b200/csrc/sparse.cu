@@ -1059,6 +1059,83 @@ __global__ void empty_rows_kernel(const int32_t* __restrict__ order, int64_t ne,
     }
 }
 
+// Short rows (at most kShortRow nonzeros) as whole rows: one 16-lane group per
+// row gathers all of each nonzero's slab-major X row at once (round r covers
+// columns 64r .. 64r + 63: one 64-column slab, or two 32-column slabs), so the
+// row's metadata and index loads and its latency chain are paid once per row
+// instead of once per (row, slab). Every column's FMA chain is the slab
+// kernel's (CSR order, the same shift epilogue): the rows are bitwise those of
+// the per-slab launch.
+constexpr int kShortRounds = 5;  // ld <= 320
+template <bool kShift, int W>
+__global__ void __launch_bounds__(256, 2)
+spmm_short_rows_kernel(const int32_t* __restrict__ idx, const double* __restrict__ val,
+                       const int32_t* __restrict__ order, const int64_t* __restrict__ obeg,
+                       const int32_t* __restrict__ olen, int64_t first, int64_t end, int64_t rows,
+                       const double* __restrict__ x, int64_t x_rows, double* __restrict__ y, int64_t ld, bool y_slab,
+                       const double* __restrict__ q, const double* __restrict__ alpha_p,
+                       const int32_t* __restrict__ gate, bool uni, double uval) {
+    if (gate_closed(gate)) return;
+    const int lane = threadIdx.x & 31, t = lane & 15;
+    const unsigned gmask = 0xffffu << (lane & 16);
+    const int64_t pos = first + (static_cast<int64_t>(blockIdx.x) * 16 + (threadIdx.x >> 4));
+    if (pos >= end) return;  // whole 16-lane groups leave together
+    const int64_t row = order[pos];
+    const int64_t beg = obeg[pos];
+    const int len = olen[pos];
+    DSVD_DCHECK(row >= 0 && row < rows && len <= kMidRow);
+    // this lane's columns: 4t .. 4t + 3 of each 64-column round, at slab c / W, offset c % W
+    int64_t xoff[kShortRounds];
+#pragma unroll
+    for (int r = 0; r < kShortRounds; ++r) {
+        const int c = 64 * r + 4 * t;
+        xoff[r] = static_cast<int64_t>(c / W) * x_rows * W + c % W;
+    }
+    double acc[kShortRounds][4];
+#pragma unroll
+    for (int r = 0; r < kShortRounds; ++r)
+#pragma unroll
+        for (int k = 0; k < 4; ++k) acc[r][k] = 0.0;
+    int ci = 0;
+    double vi = 0.0;
+    for (int p = 0; p < len; ++p) {
+        if ((p & 15) == 0) {  // the next 16 (index, value) pairs, one per lane
+            ci = 0;
+            vi = 0.0;
+            if (p + t < len) {
+                ci = idx[beg + p + t];
+                vi = uni ? uval : val[beg + p + t];
+            }
+        }
+        const int64_t c = __shfl_sync(gmask, ci, p & 15, 16);
+        const double v = __shfl_sync(gmask, vi, p & 15, 16);
+        DSVD_DCHECK(c >= 0 && c < x_rows);
+        double xa[kShortRounds][4];
+#pragma unroll
+        for (int r = 0; r < kShortRounds; ++r)
+            if (64 * r + 4 * t < ld) ld256(x + xoff[r] + c * W, xa[r]);
+#pragma unroll
+        for (int r = 0; r < kShortRounds; ++r)
+            if (64 * r + 4 * t < ld)
+#pragma unroll
+                for (int k = 0; k < 4; ++k) acc[r][k] = fma(v, xa[r][k], acc[r][k]);
+    }
+    const double alpha = kShift ? *alpha_p : 0.0;
+#pragma unroll
+    for (int r = 0; r < kShortRounds; ++r) {
+        const int64_t col = 64 * r + 4 * t;
+        if (col >= ld) continue;
+        if (kShift && alpha != 0.0) {  // solver.cpp:94 skips the update when alpha == 0
+#pragma unroll
+            for (int k = 0; k < 4; ++k) acc[r][k] = fma(-alpha, q[row * ld + col + k], acc[r][k]);
+        }
+        double* out = y_slab ? y + ((col / W) * rows + row) * W + col % W : y + row * ld + col;
+        *reinterpret_cast<double4*>(out) = make_double4(acc[r][0], acc[r][1], acc[r][2], acc[r][3]);
+    }
+}
+
+int g_short_whole_rows = 1;  // option "spmm_short_rows" (sparse.cuh set_spmm_short_rows)
+
 // One slab-kernel launch over the chunks [0, nchunks) and the rows at order
 // positions [first, end), slab-major.
 template <int W, bool kHint, int U, int MB, bool kTag>
@@ -1096,8 +1173,25 @@ void launch_slab(const SpmmArgs& s, cudaStream_t stream, double* partial) {
     // warps per SM (instead of 32) and one gather in flight per lane.
     const int64_t active = a.nonempty_rows >= 0 ? std::max(a.nonempty_rows, nsplit) : a.rows;
     const int64_t nlong = a.long_rows >= 0 ? std::min(std::max(a.long_rows, nsplit), active) : active;
-    launch_slab_range<W, kHint, U, MB, kTag>(s, stream, partial, nchunks, nsplit, nlong);
-    launch_slab_range<W, kHint, 1, 6, kTag>(s, stream, partial, 0, nlong, active);
+    const bool whole = g_short_whole_rows && s.x_slab && !kTag && s.ld <= 64 * kShortRounds &&
+                       a.obeg != nullptr && (g_short_whole_rows == 1 || a.mid_rows >= 0);
+    // whole-row short rows: from position ws on (rows of at most kShortRow, or kMidRow, nonzeros)
+    const int64_t ws = !whole ? nlong : (g_short_whole_rows == 1 ? nlong : std::min(std::max(a.mid_rows, nsplit), active));
+    launch_slab_range<W, kHint, U, MB, kTag>(s, stream, partial, nchunks, nsplit, whole ? ws : nlong);
+    if (whole && active > ws) {
+        const unsigned blocks = static_cast<unsigned>(ceil_div(active - ws, 16));
+        if (s.q != nullptr)
+            spmm_short_rows_kernel<true, W><<<blocks, 256, 0, stream>>>(
+                a.idx, a.val, a.order, a.obeg, a.olen, ws, active, a.rows, s.x, a.cols, s.y, s.ld, s.y_slab, s.q,
+                s.alpha, s.gate, a.uniform, a.uval);
+        else
+            spmm_short_rows_kernel<false, W><<<blocks, 256, 0, stream>>>(
+                a.idx, a.val, a.order, a.obeg, a.olen, ws, active, a.rows, s.x, a.cols, s.y, s.ld, s.y_slab,
+                nullptr, nullptr, s.gate, a.uniform, a.uval);
+        DSVD_LAUNCH_CHECK();
+    } else if (!whole) {
+        launch_slab_range<W, kHint, 1, 6, kTag>(s, stream, partial, 0, nlong, active);
+    }
     if (active < a.rows && !s.skip_empty) {
         empty_rows_kernel<<<grid_for((a.rows - active) * (s.ld / 4)), 256, 0, stream>>>(
             a.order, active, a.rows, s.ld, s.y, s.q, s.alpha, s.gate, s.y_slab ? W : 0);
@@ -1131,6 +1225,8 @@ void spmm_slab(const SpmmArgs& s, cudaStream_t stream, int w, bool hint, int dep
 }
 
 }  // namespace
+
+void set_spmm_short_rows(int v) { g_short_whole_rows = v < 0 ? 0 : (v > 2 ? 2 : v); }
 
 void spmm(const SpmmArgs& s, cudaStream_t stream, int variant, cudaStream_t side,
           cudaEvent_t fork, cudaEvent_t join, double* partial) {
@@ -1518,6 +1614,10 @@ void build_row_order(DevCsr& m, void* scratch, size_t scratch_bytes, cudaStream_
     }
     if (m.d_nonempty != nullptr) {
         count_ge_kernel<<<1, 1, 0, stream>>>(len_sorted, m.rows, 1, m.d_nonempty);
+        DSVD_LAUNCH_CHECK();
+    }
+    if (m.d_mid != nullptr) {
+        count_ge_kernel<<<1, 1, 0, stream>>>(len_sorted, m.rows, kMidRow + 1, m.d_mid);
         DSVD_LAUNCH_CHECK();
     }
     if (m.d_long != nullptr) {

@@ -41,6 +41,10 @@ struct DevCsr {
     // higher-occupancy launch (their time is the per-row latency chain)
     int64_t long_rows = -1;
     int32_t* d_long = nullptr;
+    // rows with more than kMidRow nonzeros: the prefix order[0 .. mid_rows) (the
+    // whole-row short-row kernel may take the rows after it; -1: unknown)
+    int64_t mid_rows = -1;
+    int32_t* d_mid = nullptr;
     // Split mode (split_chunk > 0): rows order[0 .. nsplit) hold more than
     // split_chunk nonzeros and are cut into nchunks CSR ranges of at most
     // split_chunk nonzeros; each chunk's FMA chain goes to a partial row and the
@@ -61,6 +65,7 @@ struct DevCsr {
 };
 
 constexpr int kShortRow = 8;
+constexpr int kMidRow = 32;
 
 // SpMM launch description. X and Y (and Q) are row-major with row stride ld.
 struct SpmmArgs {
@@ -142,6 +147,9 @@ void build_transpose(const DevCsr& a, DevCsr& at, void* scratch, size_t scratch_
 // and the number of rows with >= m.hub_threshold nonzeros into *m.d_hub_rows.
 size_t order_scratch_bytes(int64_t rows);
 void build_row_order(DevCsr& m, void* scratch, size_t scratch_bytes, cudaStream_t stream);
+// The short rows of the column-slab SpMM as whole rows: 0 off (per-slab items), 1 rows of
+// at most kShortRow nonzeros, 2 rows of at most kMidRow nonzeros
+void set_spmm_short_rows(int v);
 
 // Compaction of a CSR's empty rows (engine.cu build_compact): newid[r] = the
 // rank of row r among the non-empty rows (-1 if empty), oldid its inverse,

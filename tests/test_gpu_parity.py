@@ -1097,3 +1097,26 @@ def test_compact_cols_device_outputs_are_the_host_outputs():
     assert_bitwise(u_h, host.svd.u)
     assert_bitwise(v_h, host.svd.v)
     assert (np.bincount(a.col_indices, minlength=a.cols) == 0).sum() > 0.05 * a.cols
+
+
+@pytest.mark.parametrize("slab,k,s_", [(64, 200, 100), (32, 100, 50)])
+@pytest.mark.parametrize("mode", [1, 2])
+def test_short_rows_whole_row_kernel_is_bitwise_the_per_slab_launch(slab, k, s_, mode):
+    """spmm_short_rows (default 1): the column-slab SpMM's rows of at most 8 (mode 2: 32)
+    nonzeros run as whole rows, one 16-lane group gathering every slab of a nonzero at
+    once, instead of one (row, slab) item each. Same FMA chains: bitwise the per-slab
+    launch (mode 0), for 64- and 32-column slabs, on both passes of a shifted solve."""
+    a = d.powerlaw(9000, 4000, 2.0, 1.2, 1.1, 13)  # many rows of 1..8 and 9..32 nonzeros
+    deg = np.diff(a.offsets)
+    assert ((deg > 0) & (deg <= 8)).sum() > 1000 and ((deg > 8) & (deg <= 32)).sum() > 500
+    cfg = d.SolverConfig(k=k, s=s_, p=3, alg=d.Algorithm.shifted, seed=2)
+    out = []
+    for m in (0, mode):
+        dv = d.Device(0)
+        dv.set_option("spmm_slab", slab)
+        dv.set_option("spmm_short_rows", m)
+        out.append(d.solve(a, cfg, device=dv))
+        dv.close()
+    for name in ("u", "s", "v"):
+        assert_bitwise(getattr(out[0].svd, name), getattr(out[1].svd, name))
+    d.Device(0).set_option("spmm_short_rows", 1)  # process-wide knob: back to the default
