@@ -153,7 +153,9 @@ DSVD_API int dsvd_ctx_trim(dsvd_ctx* ctx);
  * Row-sharded solves: "mgpu_mode" 2 (default: reduce-scatter + slab dense work
  * + all-gather) / 1 (all-reduce of the n x l partials, dense work redundant);
  * "mgpu_overlap" 1 (default: the A^T pass in G row panels, each panel's partial
- * reduced on a communication stream while the next panel computes) / 0.
+ * reduced on a communication stream while the next panel computes) / 0 / 2 (v2:
+ * each panel's rows stored by the SpMM straight into the owner's landing buffer
+ * over peer memory — CUDA IPC under NCCL — then a barrier and the owner's sum).
  * Kernels: "spmm_variant", "split_chunk", "split_chunk_t", "split_panel_rows",
  * "hub_threshold", "eig_method", "dense_method"; column-slab SpMM: "spmm_slab"
  * (-1 auto / 0 / 32 / 64), "slab_layout", "spmm_slab_hint", "spmm_slab_depth",

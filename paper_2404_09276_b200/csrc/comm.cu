@@ -262,6 +262,66 @@ void comm_allgather(dsvd_ctx* ctx, const double* send, double* recv, size_t send
     nccl_poll(ctx, "ncclAllGather");
 }
 
+void comm_sum_slots(const double* slots, int nslots, size_t count, double* out, cudaStream_t stream) {
+    RankPtrs src{};
+    for (int g = 0; g < nslots; ++g) src.p[g] = slots + g * count;
+    rank_sum_kernel<<<sum_grid(count), 256, 0, stream>>>(src, nslots, 0, out, count);
+    DSVD_LAUNCH_CHECK();
+}
+
+void comm_barrier(dsvd_ctx* ctx, cudaStream_t stream) {
+    if (ctx->comm_kind == COMM_NONE) return;
+    const cudaStream_t s = stream ? stream : ctx->stream;
+    NvtxRange r("dsvd.barrier");
+    if (ctx->comm_kind == COMM_LOOPBACK) {
+        DSVD_CUDA_CHECK(cudaStreamSynchronize(s));
+        lb_barrier(ctx->loopback);
+        return;
+    }
+    // a one-element all-reduce on the stream: no rank gets past it before every
+    // rank's earlier work on its stream (incl. its peer stores) has completed
+    double* d = ctx->tbuf<double>("comm.barrier", 1);
+    nccl_check(nccl().AllReduce(d, d, 1, ncclDouble, ncclSum, static_cast<ncclComm_t>(ctx->comm), s),
+               "ncclAllReduce (barrier)");
+    nccl_poll(ctx, "barrier");
+}
+
+void comm_exchange_peers(dsvd_ctx* ctx, void* mine, std::vector<void*>& peers) {
+    peers.assign(ctx->nranks, nullptr);
+    peers[ctx->rank] = mine;
+    if (ctx->comm_kind == COMM_NONE) return;
+    if (ctx->comm_kind == COMM_LOOPBACK) {  // one process, one address space
+        const RankPtrs src = lb_post(ctx, static_cast<const double*>(mine));
+        for (int g = 0; g < ctx->nranks; ++g) peers[g] = const_cast<double*>(src.p[g]);
+        lb_barrier(ctx->loopback);  // every rank has read the posted pointers
+        return;
+    }
+    // NCCL: CUDA IPC handles of every rank's buffer, all-gathered, opened here
+    cudaIpcMemHandle_t h;
+    DSVD_CUDA_CHECK(cudaIpcGetMemHandle(&h, mine));
+    static_assert(sizeof(cudaIpcMemHandle_t) == 64, "cudaIpcMemHandle_t is 64 bytes");
+    char* d = ctx->tbuf<char>("comm.ipc", 64 * static_cast<size_t>(ctx->nranks + 1));
+    DSVD_CUDA_CHECK(cudaMemcpyAsync(d + 64 * ctx->nranks, &h, 64, cudaMemcpyHostToDevice, ctx->stream));
+    nccl_check(nccl().AllGather(d + 64 * ctx->nranks, d, 64, ncclChar, static_cast<ncclComm_t>(ctx->comm), ctx->stream),
+               "ncclAllGather (IPC handles)");
+    std::vector<cudaIpcMemHandle_t> all(ctx->nranks);
+    DSVD_CUDA_CHECK(cudaMemcpyAsync(all.data(), d, 64 * static_cast<size_t>(ctx->nranks), cudaMemcpyDeviceToHost,
+                                    ctx->stream));
+    DSVD_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+    nccl_poll(ctx, "IPC handle exchange");
+    for (int g = 0; g < ctx->nranks; ++g) {
+        if (g == ctx->rank) continue;
+        DSVD_CUDA_CHECK(cudaIpcOpenMemHandle(&peers[g], all[g], cudaIpcMemLazyEnablePeerAccess));
+    }
+}
+
+void comm_close_peers(dsvd_ctx* ctx, std::vector<void*>& peers) {
+    if (ctx->comm_kind == COMM_NCCL)
+        for (int g = 0; g < static_cast<int>(peers.size()); ++g)
+            if (g != ctx->rank && peers[g] != nullptr) cudaIpcCloseMemHandle(peers[g]);
+    peers.clear();
+}
+
 double comm_sum_host(dsvd_ctx* ctx, double v) {
     if (ctx->comm_kind == COMM_NONE) return v;
     double* d = ctx->tbuf<double>("comm.scalar", 1);

@@ -686,6 +686,30 @@ void solve_tall(dsvd_ctx* ctx, const DevCsr& A, const DevCsr& AT, const dsvd_con
     // the communication stream while the next panel computes. Same values as the
     // whole-pass collective: bitwise in the loopback group's fixed rank order.
     const bool overlap = sharded && ctx->nranks > 1 && ctx->mgpu_overlap;
+    // fused exchange (mgpu_overlap 2, v2): each panel's SpMM stores its rows
+    // straight into the owner's landing buffer (slot `rank`), a barrier, then the
+    // owner sums its G slots in rank order — no separate reduction collective
+    const bool fused = overlap && v2 && ctx->mgpu_overlap == 2;
+    std::vector<void*> peers;
+    struct PeerGuard {
+        dsvd_ctx* c;
+        std::vector<void*>* p;
+        ~PeerGuard() { comm_close_peers(c, *p); }
+    } peer_guard{ctx, &peers};
+    if (fused) {
+        const size_t lb = sizeof(double) * static_cast<size_t>(ctx->nranks) * n_slab * ld;
+        if (ctx->landing_bytes != lb) {
+            if (ctx->landing) DSVD_CUDA_CHECK(cudaFree(ctx->landing));
+            ctx->landing = nullptr;
+            ctx->landing_bytes = 0;
+            DSVD_CUDA_CHECK(cudaMalloc(&ctx->landing, lb));
+            ctx->landing_bytes = lb;
+            // padding rows of the last panel are never stored: they stay zero
+            DSVD_CUDA_CHECK(cudaMemsetAsync(ctx->landing, 0, lb, st));
+            DSVD_CUDA_CHECK(cudaStreamSynchronize(st));
+        }
+        comm_exchange_peers(ctx, ctx->landing, peers);
+    }
     std::vector<DevCsr> panels;
     if (overlap) {
         const int64_t ps = ceil_div(n, ctx->nranks);
@@ -755,6 +779,26 @@ void solve_tall(dsvd_ctx* ctx, const DevCsr& A, const DevCsr& AT, const dsvd_con
             return reduce_partial(part);
         }
         const int64_t ps = ceil_div(n, ctx->nranks);
+        if (fused) {
+            for (int p = 0; p < ctx->nranks; ++p) {
+                double* dst = static_cast<double*>(peers[p]) + ctx->rank * n_slab * ld;  // owner p, slot rank
+                SpmmArgs sa{&panels[p], Y, dst, ld, l, nullptr, nullptr, g};
+                sa.idx_tag = tag_at;
+                if (lw > 0) {
+                    sa.slab = lw;
+                    sa.x_slab = true;
+                }
+                spmm(sa, st, spmm_var(ctx, ld, big_rows), ctx->side, ctx->fork, ctx->join,
+                     partial_for(ctx, panels[p], ld));
+                count_launch();
+            }
+            const int sp3 = ctx->span_begin(K_COMM);
+            comm_barrier(ctx, st);  // every rank's stores into every landing buffer are done
+            comm_sum_slots(ctx->landing, ctx->nranks, static_cast<size_t>(n_slab * ld), S, st);
+            count_launch();
+            ctx->span_end(sp3);
+            return S;
+        }
         for (int p = 0; p < ctx->nranks; ++p) {
             const int64_t r0 = std::min(n, p * ps);
             SpmmArgs sa{&panels[p], Y, part + r0 * ld, ld, l, nullptr, nullptr, g};
@@ -1462,6 +1506,7 @@ int dsvd_ctx_destroy(dsvd_ctx* ctx) {
         if (ctx->copy) cudaStreamDestroy(ctx->copy);
         if (ctx->comm_ev) cudaEventDestroy(ctx->comm_ev);
         if (ctx->comm_stream) cudaStreamDestroy(ctx->comm_stream);
+        if (ctx->landing) cudaFree(ctx->landing);
         cudaStreamDestroy(ctx->stream);
         delete ctx;
     });
@@ -1581,7 +1626,8 @@ int dsvd_ctx_set_option(dsvd_ctx* ctx, const char* name, int64_t value) {
             if (value < 0 || value > 1) fail(DSVD_CONFIG, "compact_cols must be 0 or 1");
             ctx->compact_cols = static_cast<int>(value);
         } else if (n == "mgpu_overlap") {
-            if (value < 0 || value > 1) fail(DSVD_CONFIG, "mgpu_overlap must be 0 or 1");
+            if (value < 0 || value > 2)
+                fail(DSVD_CONFIG, "mgpu_overlap: 0 whole-pass collective, 1 panelled reductions, 2 fused peer stores");
             ctx->mgpu_overlap = static_cast<int>(value);
         } else if (n == "split_chunk") {
             if (value < 0) fail(DSVD_CONFIG, "split_chunk must be >= 0");

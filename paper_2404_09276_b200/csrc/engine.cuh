@@ -33,6 +33,18 @@ enum CommKind { COMM_NONE = 0, COMM_NCCL = 1, COMM_LOOPBACK = 2 };
 constexpr int kMaxLoopbackRanks = 8;
 // (stream: the stream the collective is ordered on, nullptr = ctx->stream)
 void comm_allreduce_sum(dsvd_ctx* ctx, double* buf, size_t count, cudaStream_t stream = nullptr);
+// Peer buffers for the fused exchange (mgpu_overlap 2): every rank's `mine`
+// (device memory from cudaMalloc, the same size on every rank) as addresses
+// this rank can store to — the loopback group's own pointers, or CUDA IPC
+// mappings exchanged over NCCL. peers[rank] == mine. comm_close_peers unmaps.
+void comm_exchange_peers(dsvd_ctx* ctx, void* mine, std::vector<void*>& peers);
+void comm_close_peers(dsvd_ctx* ctx, std::vector<void*>& peers);
+// Every rank's work on `stream` so far is complete (and its stores visible)
+// before any rank's later work on its stream.
+void comm_barrier(dsvd_ctx* ctx, cudaStream_t stream = nullptr);
+// out[i] = slots[i] + slots[count + i] + ... (nslots slots, in slot order: the
+// loopback reduction's rank order)
+void comm_sum_slots(const double* slots, int nslots, size_t count, double* out, cudaStream_t stream);
 // recv (count, significant on rank `root` only) = the sum of every rank's send
 void comm_reduce_sum(dsvd_ctx* ctx, const double* send, double* recv, size_t count, int root,
                      cudaStream_t stream = nullptr);
@@ -126,6 +138,10 @@ struct dsvd_ctx {
     // panel's partial is reduced on comm_stream while the next panel computes (1,
     // default), or the whole pass first and then one collective (0)
     int mgpu_overlap = 1;
+    // mgpu_overlap 2 (v2): the A^T pass stores each row panel straight into its
+    // owner's landing buffer (G source slots of n_slab rows), the owner sums them
+    double* landing = nullptr;
+    size_t landing_bytes = 0;
     // single-GPU shifted-family solves on the non-empty columns only (engine.cu
     // build_compact): 1 (default) when >= 2% of the columns are empty, 0 off
     int compact_cols = 1;

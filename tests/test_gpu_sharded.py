@@ -223,3 +223,32 @@ def test_exchange_overlap_wide_sketch_matches_oracle(oracle, plaw):
     check_against(y, ref, k)
     x = run_sharded(plaw, cfg, bounds, {"mgpu_overlap": 0})
     assert_same_bits(x, y)
+
+
+@pytest.mark.parametrize("pipeline", [0, 1])
+@pytest.mark.parametrize("alg", ["dash", "shifted"])
+def test_fused_exchange_is_bitwise_the_reduce_scatter(plaw, pipeline, alg):
+    """mgpu_overlap = 2 (v2): each row panel of the A^T pass is stored straight
+    into its owner's landing buffer (slot = the source rank; peer memory — here the
+    loopback group's own pointers), then a barrier and the owner's rank-order sum
+    of its slots. Bitwise the loopback reduce-scatter (same rank-order sums)."""
+    kw = dict(tol=1e-2, p_max=20) if alg == "dash" else dict(p=4)
+    cfg = d.SolverConfig(k=24, s=12, alg=d.Algorithm[alg], seed=4, **kw)
+    bounds = shard_bounds(plaw.offsets, 3)
+    x = run_sharded(plaw, cfg, bounds, {"pipeline": pipeline, "mgpu_overlap": 0})
+    y = run_sharded(plaw, cfg, bounds, {"pipeline": pipeline, "mgpu_overlap": 2})
+    assert_same_bits(x, y)
+
+
+def test_fused_exchange_wide_sketch_matches_oracle(oracle, plaw):
+    """The fused exchange on the column-slab SpMM (l = 200), 2 ranks, twice in a row
+    on the same contexts (the landing buffers are reused), against the oracle."""
+    k, s = 120, 80
+    cfg = d.SolverConfig(k=k, s=s, p=3, alg=d.Algorithm.shifted, seed=6)
+    ref = oracle.solve(Csr(plaw.rows, plaw.cols, plaw.offsets, plaw.col_indices, plaw.values), k, s, p=3,
+                       alg="shifted", seed=6)
+    bounds = shard_bounds(plaw.offsets, 2)
+    y = run_sharded(plaw, cfg, bounds, {"mgpu_overlap": 2})
+    check_against(y, ref, k)
+    x = run_sharded(plaw, cfg, bounds, {"mgpu_overlap": 0})
+    assert_same_bits(x, y)
