@@ -55,9 +55,18 @@ void gram_dmma(const double* c, int64_t n, int64_t l, int64_t ld, double* g, voi
                cudaStream_t stream);
 bool rescale_dmma_supported(int64_t K, int64_t ldc, int64_t ld_out, int out_colmajor);
 size_t rescale_dmma_workspace_bytes(int64_t K, int64_t width);
+// Extra row-major destinations of the rescale (the fused all-gather of a
+// row-sharded solve: the same rows stored into the other ranks' blocks over
+// peer memory); n == 0: none.
+constexpr int kMaxPeerOut = 8;
+struct PeerOut {
+    double* p[kMaxPeerOut];
+    int n;
+};
 void rescale_dmma(const double* c, int64_t n, int64_t K, int64_t ldc, const double* w, int64_t ldw,
                   const double* scale, int64_t ncol, double* out, int64_t ld_out, int out_colmajor, void* ws,
-                  const int32_t* gate, cudaStream_t stream, double* out2 = nullptr, int out2_w = 0);
+                  const int32_t* gate, cudaStream_t stream, double* out2 = nullptr, int out2_w = 0,
+                  const PeerOut* peers = nullptr);
 
 // Column-major (rows x cols) <-> row-major (stride ld, pad columns zeroed).
 void colmajor_to_rowmajor(const double* src, int64_t rows, int64_t cols, double* dst, int64_t ld,

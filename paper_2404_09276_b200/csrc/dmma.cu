@@ -97,7 +97,8 @@ __global__ void rescale_prep_kernel(const double* __restrict__ w, int64_t ldw, c
 __global__ void __launch_bounds__(kRsThreads, 2)
 rescale_dmma_kernel(const double* __restrict__ c, int64_t n, int K, int64_t ldc, const double* __restrict__ wt,
                     int ldb, int ncol, double* __restrict__ out, int64_t ld_out, int out_colmajor,
-                    const int32_t* __restrict__ gate, double* __restrict__ out2, int out2_w) {
+                    const int32_t* __restrict__ gate, double* __restrict__ out2, int out2_w,
+                   const PeerOut peers) {
     if (gate != nullptr && *gate != 0) return;
     extern __shared__ __align__(16) double rsm[];
     double* Bt = rsm;                // [32][ldb]: W block, transposed
@@ -180,9 +181,12 @@ rescale_dmma_kernel(const double* __restrict__ c, int64_t n, int K, int64_t ldc,
                     *reinterpret_cast<double2*>(out + r * ld_out + j) = v;
                     if (out2 != nullptr)  // the slab-major copy (j even: j, j + 1 share a slab)
                         *reinterpret_cast<double2*>(out2 + ((j / out2_w) * n + r) * out2_w + j % out2_w) = v;
+                    for (int pp = 0; pp < peers.n; ++pp)  // the other ranks' copies of these rows
+                        *reinterpret_cast<double2*>(peers.p[pp] + r * ld_out + j) = v;
                 } else if (j < ld_out) {
                     out[r * ld_out + j] = v.x;
                     if (out2 != nullptr) out2[((j / out2_w) * n + r) * out2_w + j % out2_w] = v.x;
+                    for (int pp = 0; pp < peers.n; ++pp) peers.p[pp][r * ld_out + j] = v.x;
                 }
             }
         }
@@ -225,7 +229,8 @@ template <int ST>
 __global__ void __launch_bounds__(kRsThreads, 2)
 rescale_tma_kernel(const __grid_constant__ CUtensorMap cmap, int64_t n, int K, const double* __restrict__ wt,
                    int ldb, int ncol, double* __restrict__ out, int64_t ld_out, int out_colmajor,
-                   const int32_t* __restrict__ gate, double* __restrict__ out2, int out2_w) {
+                   const int32_t* __restrict__ gate, double* __restrict__ out2, int out2_w,
+                   const PeerOut peers) {
     if (gate != nullptr && *gate != 0) return;
     extern __shared__ __align__(1024) unsigned char rsm_raw[];
     // 1024-byte aligned ring first (128B-swizzle requirement), then W, then barriers
@@ -301,9 +306,12 @@ rescale_tma_kernel(const __grid_constant__ CUtensorMap cmap, int64_t n, int K, c
                     *reinterpret_cast<double2*>(out + r * ld_out + j) = v;
                     if (out2 != nullptr)  // the slab-major copy (j even: j, j + 1 share a slab)
                         *reinterpret_cast<double2*>(out2 + ((j / out2_w) * n + r) * out2_w + j % out2_w) = v;
+                    for (int pp = 0; pp < peers.n; ++pp)  // the other ranks' copies of these rows
+                        *reinterpret_cast<double2*>(peers.p[pp] + r * ld_out + j) = v;
                 } else if (j < ld_out) {
                     out[r * ld_out + j] = v.x;
                     if (out2 != nullptr) out2[((j / out2_w) * n + r) * out2_w + j % out2_w] = v.x;
+                    for (int pp = 0; pp < peers.n; ++pp) peers.p[pp][r * ld_out + j] = v.x;
                 }
             }
         }
@@ -859,8 +867,13 @@ size_t rescale_dmma_workspace_bytes(int64_t K, int64_t width) {
 
 void rescale_dmma(const double* c, int64_t n, int64_t K, int64_t ldc, const double* w, int64_t ldw,
                   const double* scale, int64_t ncol, double* out, int64_t ld_out, int out_colmajor, void* ws,
-                  const int32_t* gate, cudaStream_t stream, double* out2, int out2_w) {
+                  const int32_t* gate, cudaStream_t stream, double* out2, int out2_w, const PeerOut* peers) {
     if (out2 != nullptr && (out_colmajor || out2_w <= 0 || out2_w % 2 != 0)) fail(DSVD_OTHER, "rescale: bad second output");
+    PeerOut po{};
+    if (peers != nullptr) {
+        if (out_colmajor || peers->n > kMaxPeerOut) fail(DSVD_OTHER, "rescale: bad peer outputs");
+        po = *peers;
+    }
     if (n == 0) return;
     const int64_t width = out_colmajor ? ncol : ld_out;
     const int ncb = static_cast<int>(ceil_div(width, kRsBN));
@@ -882,14 +895,14 @@ void rescale_dmma(const double* c, int64_t n, int64_t K, int64_t ldc, const doub
         DSVD_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
         const CUtensorMap cmap = make_cmap(c, n, ldc);
         kern<<<grid, kRsThreads, smem, stream>>>(cmap, n, static_cast<int>(K), wt, ldb, static_cast<int>(ncol), out,
-                                                 ld_out, out_colmajor, gate, out2, out2_w);
+                                                 ld_out, out_colmajor, gate, out2, out2_w, po);
     } else {
         const size_t smem = sizeof(double) * (static_cast<size_t>(kRsBN) * ldb + kRsStages * kRsBM * kRsBK);
         DSVD_CUDA_CHECK(cudaFuncSetAttribute(rescale_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              static_cast<int>(smem)));
         rescale_dmma_kernel<<<grid, kRsThreads, smem, stream>>>(c, n, static_cast<int>(K), ldc, wt, ldb,
                                                                 static_cast<int>(ncol), out, ld_out, out_colmajor,
-                                                                gate, out2, out2_w);
+                                                                gate, out2, out2_w, po);
     }
     DSVD_LAUNCH_CHECK();
 }

@@ -381,14 +381,15 @@ struct EigSvdOut {
 // out2_w) of the row-major result and returns true; false: no copy was made.
 bool solve_rescale(dsvd_ctx* ctx, const double* c, int64_t n, int64_t K, int64_t ldc, const double* w,
                    int64_t ldw, const double* scale, int64_t ncol, double* out, int64_t ld_out, int out_colmajor,
-                   const int32_t* gate, double* out2 = nullptr, int out2_w = 0) {
+                   const int32_t* gate, double* out2 = nullptr, int out2_w = 0, const PeerOut* peers = nullptr) {
     if (ctx->dense_method == 0 && rescale_dmma_supported(K, ldc, ld_out, out_colmajor)) {
         const size_t ws = rescale_dmma_workspace_bytes(K, out_colmajor ? ncol : ld_out);
         rescale_dmma(c, n, K, ldc, w, ldw, scale, ncol, out, ld_out, out_colmajor, ctx->buf("rescale.ws", ws), gate,
-                     ctx->stream, out2, out2_w);
+                     ctx->stream, out2, out2_w, peers);
         count_launch(2);
         return out2 != nullptr;
     } else {
+        if (peers != nullptr && peers->n > 0) fail(DSVD_OTHER, "rescale: peer outputs need the tensor-core rescale");
         rescale(c, n, K, ldc, w, ldw, scale, ncol, out, ld_out, out_colmajor, gate, ctx->stream);
         count_launch();
     }
@@ -710,6 +711,20 @@ void solve_tall(dsvd_ctx* ctx, const DevCsr& A, const DevCsr& AT, const dsvd_con
         }
         comm_exchange_peers(ctx, ctx->landing, peers);
     }
+    // fused all-gather: the rescale stores each slab row into every rank's copy of
+    // the destination block (the tensor-core rescale; peers of T, Q0 and Q1)
+    const bool fused_ag = fused && ctx->dense_method == 0 && rescale_dmma_supported(l, ld, ld, 0) &&
+                          ctx->nranks - 1 <= kMaxPeerOut;
+    std::map<const double*, std::vector<void*>> blk_peers;
+    struct BlkGuard {
+        dsvd_ctx* c;
+        std::map<const double*, std::vector<void*>>* m;
+        ~BlkGuard() {
+            for (auto& kv : *m) comm_close_peers(c, kv.second);
+        }
+    } blk_guard{ctx, &blk_peers};
+    if (fused_ag)
+        for (double* b : {T, Qb[0], Qb[1]}) comm_exchange_peers(ctx, b, blk_peers[b]);
     std::vector<DevCsr> panels;
     if (overlap) {
         const int64_t ps = ceil_div(n, ctx->nranks);
@@ -832,6 +847,20 @@ void solve_tall(dsvd_ctx* ctx, const DevCsr& A, const DevCsr& AT, const dsvd_con
     auto rescale_into = [&](const double* c, double* dst, const int32_t* g) {
         int s2 = ctx->span_begin(K_RESCALE);
         const bool copy = lw > 0 && !sharded;  // the next A pass gathers dst: write its slab-major copy too
+        auto bp = blk_peers.find(dst);
+        if (fused_ag && bp != blk_peers.end()) {
+            // this rank's slab rows, stored into every rank's dst; then a barrier for the all-gather
+            PeerOut po{};
+            for (int r = 0; r < ctx->nranks; ++r)
+                if (r != ctx->rank) po.p[po.n++] = static_cast<double*>(bp->second[r]) + slab0 * ld;
+            solve_rescale(ctx, c, red_rows, l, ld, W, l, inv_s, l, dst + slab0 * ld, ld, 0, g, nullptr, 0, &po);
+            xs_holds = nullptr;
+            ctx->span_end(s2);
+            s2 = ctx->span_begin(K_COMM);
+            comm_barrier(ctx, st);
+            ctx->span_end(s2);
+            return;
+        }
         xs_holds = solve_rescale(ctx, c, red_rows, l, ld, W, l, inv_s, l, dst + slab0 * ld, ld, 0, g,
                                  copy ? Xs : nullptr, lw) ? dst : nullptr;
         ctx->span_end(s2);
