@@ -94,6 +94,7 @@ __global__ void rescale_prep_kernel(const double* __restrict__ w, int64_t ldw, c
     }
 }
 
+template <bool kPeers>
 __global__ void __launch_bounds__(kRsThreads, 2)
 rescale_dmma_kernel(const double* __restrict__ c, int64_t n, int K, int64_t ldc, const double* __restrict__ wt,
                     int ldb, int ncol, double* __restrict__ out, int64_t ld_out, int out_colmajor,
@@ -181,12 +182,15 @@ rescale_dmma_kernel(const double* __restrict__ c, int64_t n, int K, int64_t ldc,
                     *reinterpret_cast<double2*>(out + r * ld_out + j) = v;
                     if (out2 != nullptr)  // the slab-major copy (j even: j, j + 1 share a slab)
                         *reinterpret_cast<double2*>(out2 + ((j / out2_w) * n + r) * out2_w + j % out2_w) = v;
-                    for (int pp = 0; pp < peers.n; ++pp)  // the other ranks' copies of these rows
-                        *reinterpret_cast<double2*>(peers.p[pp] + r * ld_out + j) = v;
+#pragma unroll
+                    for (int pp = 0; pp < kMaxPeerOut; ++pp)  // the other ranks' copies of these rows
+                        if (kPeers && pp < peers.n) *reinterpret_cast<double2*>(peers.p[pp] + r * ld_out + j) = v;
                 } else if (j < ld_out) {
                     out[r * ld_out + j] = v.x;
                     if (out2 != nullptr) out2[((j / out2_w) * n + r) * out2_w + j % out2_w] = v.x;
-                    for (int pp = 0; pp < peers.n; ++pp) peers.p[pp][r * ld_out + j] = v.x;
+#pragma unroll
+                    for (int pp = 0; pp < kMaxPeerOut; ++pp)
+                        if (kPeers && pp < peers.n) peers.p[pp][r * ld_out + j] = v.x;
                 }
             }
         }
@@ -225,7 +229,7 @@ __device__ __forceinline__ void rs_ksteps(const double* A, const double* Bt, int
 // fragment addresses follow the swizzle (16-byte chunk c of row r lives at
 // chunk c ^ (r & 7)). Removes the per-thread cp.async address arithmetic,
 // which was ~45% of the issued instructions of rescale_dmma_kernel.
-template <int ST>
+template <int ST, bool kPeers>
 __global__ void __launch_bounds__(kRsThreads, 2)
 rescale_tma_kernel(const __grid_constant__ CUtensorMap cmap, int64_t n, int K, const double* __restrict__ wt,
                    int ldb, int ncol, double* __restrict__ out, int64_t ld_out, int out_colmajor,
@@ -306,12 +310,15 @@ rescale_tma_kernel(const __grid_constant__ CUtensorMap cmap, int64_t n, int K, c
                     *reinterpret_cast<double2*>(out + r * ld_out + j) = v;
                     if (out2 != nullptr)  // the slab-major copy (j even: j, j + 1 share a slab)
                         *reinterpret_cast<double2*>(out2 + ((j / out2_w) * n + r) * out2_w + j % out2_w) = v;
-                    for (int pp = 0; pp < peers.n; ++pp)  // the other ranks' copies of these rows
-                        *reinterpret_cast<double2*>(peers.p[pp] + r * ld_out + j) = v;
+#pragma unroll
+                    for (int pp = 0; pp < kMaxPeerOut; ++pp)  // the other ranks' copies of these rows
+                        if (kPeers && pp < peers.n) *reinterpret_cast<double2*>(peers.p[pp] + r * ld_out + j) = v;
                 } else if (j < ld_out) {
                     out[r * ld_out + j] = v.x;
                     if (out2 != nullptr) out2[((j / out2_w) * n + r) * out2_w + j % out2_w] = v.x;
-                    for (int pp = 0; pp < peers.n; ++pp) peers.p[pp][r * ld_out + j] = v.x;
+#pragma unroll
+                    for (int pp = 0; pp < kMaxPeerOut; ++pp)
+                        if (kPeers && pp < peers.n) peers.p[pp][r * ld_out + j] = v.x;
                 }
             }
         }
@@ -891,16 +898,18 @@ void rescale_dmma(const double* c, int64_t n, int64_t K, int64_t ldc, const doub
         const int st = K > 160 ? 2 : kRsStages;
         const size_t smem = 1024 + sizeof(double) * (st * kRsBM * kRsBK + static_cast<size_t>(kRsBN) * ldb) +
                             sizeof(uint64_t) * (st + 1);
-        auto kern = st == 2 ? rescale_tma_kernel<2> : rescale_tma_kernel<kRsStages>;
+        auto kern = po.n > 0 ? (st == 2 ? rescale_tma_kernel<2, true> : rescale_tma_kernel<kRsStages, true>)
+                             : (st == 2 ? rescale_tma_kernel<2, false> : rescale_tma_kernel<kRsStages, false>);
         DSVD_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
         const CUtensorMap cmap = make_cmap(c, n, ldc);
         kern<<<grid, kRsThreads, smem, stream>>>(cmap, n, static_cast<int>(K), wt, ldb, static_cast<int>(ncol), out,
                                                  ld_out, out_colmajor, gate, out2, out2_w, po);
     } else {
         const size_t smem = sizeof(double) * (static_cast<size_t>(kRsBN) * ldb + kRsStages * kRsBM * kRsBK);
-        DSVD_CUDA_CHECK(cudaFuncSetAttribute(rescale_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        auto kd = po.n > 0 ? rescale_dmma_kernel<true> : rescale_dmma_kernel<false>;
+        DSVD_CUDA_CHECK(cudaFuncSetAttribute(kd, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              static_cast<int>(smem)));
-        rescale_dmma_kernel<<<grid, kRsThreads, smem, stream>>>(c, n, static_cast<int>(K), ldc, wt, ldb,
+        kd<<<grid, kRsThreads, smem, stream>>>(c, n, static_cast<int>(K), ldc, wt, ldb,
                                                                 static_cast<int>(ncol), out, ld_out, out_colmajor,
                                                                 gate, out2, out2_w, po);
     }
