@@ -1118,15 +1118,56 @@ void solve_tall(dsvd_ctx* ctx, const DevCsr& A, const DevCsr& AT, const dsvd_con
     NvtxRange nvtx_fin("dsvd.finalize");
     control_init(ctrl, s_stored, static_cast<int>(l), st);
     count_launch();
+    // Row compaction of the finalize (single GPU, column-slab path): B's rows of
+    // empty rows of A are exactly zero, so B is formed on the non-empty rows only
+    // — a view of A whose length order is renumbered to compact row ids (the slab
+    // kernels read each row's range from obeg / olen, not from the offsets) — and
+    // the Gram and U = B V' diag(1/s) run on them; U is scattered back with zero
+    // rows. The rank floor keeps the full row count.
+    const int64_t m_ne = A.nonempty_rows;
+    const bool compact_m = ctx->compact_cols && !sharded && lw > 0 && A.obeg != nullptr && m_ne >= l &&
+                           m_ne < m && (m - m_ne) * 50 >= m;
+    const int32_t* oldid_m = nullptr;
+    const int64_t m_b = compact_m ? m_ne : m;
     sp = ctx->span_begin(K_SPMM1);
-    pass1(Qf, Y, false, nullptr);  // B row-major: the Gram and the U product read it
+    if (compact_m) {
+        int32_t* newid = ctx->tbuf<int32_t>("ccm.newid", m);
+        int32_t* oldid = ctx->tbuf<int32_t>("ccm.oldid", m_ne);
+        int64_t* off_c = ctx->tbuf<int64_t>("ccm.off", m_ne + 1);
+        const size_t sb = compact_scratch_bytes(m);
+        compact_rows_map(A.off, m, newid, oldid, off_c, ctx->buf("cc.scratch", sb), sb, st);
+        int32_t* order_c = ctx->tbuf<int32_t>("ccm.order", m_ne);
+        remap_ids(A.order, m_ne, newid, order_c, st);  // the non-empty rows are the order's prefix
+        count_launch(4);
+        DevCsr Av = A;
+        Av.rows = m_ne;
+        Av.off = off_c;
+        Av.order = order_c;
+        Av.nonempty_rows = m_ne;
+        Av.long_rows = std::min(Av.long_rows, m_ne);
+        Av.mid_rows = std::min(Av.mid_rows, m_ne);
+        if (xs_holds != Qf) {
+            to_slab_major(Qf, n, ld, lw, Xs, st);
+            count_launch();
+            xs_holds = Qf;
+        }
+        SpmmArgs sa{&Av, Xs, Y, ld, l, nullptr, nullptr, nullptr};
+        sa.idx_tag = tag_a;
+        sa.slab = lw;
+        sa.x_slab = true;
+        spmm(sa, st, spmm_var(ctx, ld, big_rows), ctx->side, ctx->fork, ctx->join, partial_for(ctx, Av, ld));
+        count_launch();
+        oldid_m = oldid;
+    } else {
+        pass1(Qf, Y, false, nullptr);  // B row-major: the Gram and the U product read it
+    }
     ctx->span_end(sp);
-    eig_svd_factors(ctx, Y, m, l, ld, eo, ctrl, nullptr, nullptr, sharded, global_m);
+    eig_svd_factors(ctx, Y, m_b, l, ld, eo, ctrl, nullptr, nullptr, sharded, global_m);
     hc = read_control(ctx, ctrl);
     raise_device_status(hc);
     ctx->stats.eig_sweeps += hc.total_sweeps;
 
-    double* du = io.on_device ? io.u : ctx->tbuf<double>("out.u", m * k);
+    double* du = io.on_device && !compact_m ? io.u : ctx->tbuf<double>(compact_m ? "out.uc" : "out.u", m_b * k);
     const bool scatter_v = io.v_rows != nullptr;
     const int64_t n_out = scatter_v ? io.v_full : n;
     double* dv = io.on_device && !scatter_v ? io.v : ctx->tbuf<double>(scatter_v ? "out.vc" : "out.v", n * k);
@@ -1149,7 +1190,13 @@ void solve_tall(dsvd_ctx* ctx, const DevCsr& A, const DevCsr& AT, const dsvd_con
         vs = ctx->copy;
         DSVD_CUDA_CHECK(cudaMemcpyAsync(io.v, dv, sizeof(double) * n_out * k, cudaMemcpyDeviceToHost, vs));
     }
-    solve_rescale(ctx, Y, m, l, ld, W, l, inv_s, k, du, 0, 1, nullptr);
+    solve_rescale(ctx, Y, m_b, l, ld, W, l, inv_s, k, du, 0, 1, nullptr);
+    if (compact_m) {  // U of the non-empty rows -> all rows (zero rows elsewhere)
+        double* duf = io.on_device ? io.u : ctx->tbuf<double>("out.u", m * k);
+        scatter_rows_colmajor(du, m_ne, k, oldid_m, duf, m, st);
+        count_launch();
+        du = duf;
+    }
     ctx->span_end(sp);
     if (io.on_device) {
         DSVD_CUDA_CHECK(cudaMemcpyAsync(io.s, sv, sizeof(double) * k, cudaMemcpyDeviceToDevice, st));

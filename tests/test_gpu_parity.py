@@ -1120,3 +1120,30 @@ def test_short_rows_whole_row_kernel_is_bitwise_the_per_slab_launch(slab, k, s_,
     for name in ("u", "s", "v"):
         assert_bitwise(getattr(out[0].svd, name), getattr(out[1].svd, name))
     d.Device(0).set_option("spmm_short_rows", 1)  # process-wide knob: back to the default
+
+
+@pytest.mark.parametrize("slab", [64, 32])
+def test_compact_rows_in_the_finalize(oracle, slab):
+    """Column-slab path (forced here at l = 60): the finalize forms B = A Q on the
+    non-empty rows of A only (a view of A with its length order renumbered), runs
+    the Gram and U = B V' diag(1/s) on them and scatters U back. Against the oracle
+    and the uncompacted solve; U exactly zero on A's empty rows."""
+    a = _rmat_host(13, 60000, 21)
+    empty_rows = np.diff(a.offsets) == 0
+    assert 0.2 * a.rows < empty_rows.sum() < 0.8 * a.rows
+    ca = Csr(a.rows, a.cols, a.offsets, a.col_indices, a.values)
+    ref = oracle.solve(ca, 40, 20, p=3, alg="shifted", seed=3)
+    cfg = d.SolverConfig(k=40, s=20, p=3, alg=d.Algorithm.shifted, seed=3)
+    out = []
+    for cc in (1, 0):
+        dv = d.Device(0)
+        dv.set_option("spmm_slab", slab)
+        dv.set_option("compact_cols", cc)
+        out.append(d.solve(a, cfg, device=dv))
+        dv.close()
+    res, full = out
+    check_solve(res, ref, 40)
+    assert np.all(res.svd.u[empty_rows] == 0.0)
+    np.testing.assert_allclose(res.svd.s, full.svd.s, rtol=1e-12)
+    assert sin_theta(full.svd.u, res.svd.u) <= 1e-10
+    assert sin_theta(full.svd.v, res.svd.v) <= 1e-10
