@@ -160,7 +160,14 @@ DSVD_API int dsvd_ctx_trim(dsvd_ctx* ctx);
  * "hub_threshold", "eig_method", "dense_method"; column-slab SpMM: "spmm_slab"
  * (-1 auto / 0 / 32 / 64), "slab_layout", "spmm_slab_hint", "spmm_slab_depth",
  * "spmm_hot_mb", "uniform_values" (1 default: all-equal values are detected at
- * build time and not streamed; 0: always streamed). */
+ * build time and not streamed; 0: always streamed).
+ * Host buffers: "host_staging" 1 (default: PAGEABLE host inputs / outputs of a
+ * solve — std::vector, numpy — move through a ring of 4 pinned slots, the copy
+ * engine streaming one slot while host threads fill or drain another) / 0 (plain
+ * cudaMemcpyAsync through the driver's bounce buffer); "host_stage_chunk" bytes
+ * per slot (default 32 MB); "host_copy_threads" (0 default: min(16, cores)).
+ * Pinned (dsvd_host_register / cudaHostAlloc) and device pointers are copied
+ * directly either way. */
 DSVD_API int dsvd_ctx_set_option(dsvd_ctx* ctx, const char* name, int64_t value);
 
 /* Multi-GPU: one process per GPU. Rank 0 calls dsvd_comm_unique_id and

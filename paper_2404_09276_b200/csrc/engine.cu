@@ -26,6 +26,7 @@
 #include <map>
 #include <memory>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "common.cuh"
@@ -63,6 +64,117 @@ void set_error(const char* msg, long long index) {
 void set_device(dsvd_ctx* ctx) { DSVD_CUDA_CHECK(cudaSetDevice(ctx->device)); }
 
 void count_launch(int n) { g_launches += n; }
+
+// ---- host <-> device copies that may touch pageable memory ----------------
+// The reference-shaped API hands back std::vector / numpy factors, i.e.
+// pageable memory, and its inputs usually live there too. A cudaMemcpyAsync
+// to or from pageable memory runs through the driver's bounce buffer at a
+// fraction of the PCIe rate (C4's 13.4 GB of U and V: ~2.9 s against ~0.25 s
+// pinned). Pageable copies therefore go through a ring of pinned slots: the
+// copy stream moves slot c over PCIe while host threads move slot c - 1 to or
+// from the caller's buffer (host_parallel_memcpy, which also takes the
+// buffer's first-touch page faults in parallel). Pinned, registered and
+// device pointers keep the plain cudaMemcpyAsync.
+void host_parallel_memcpy(void* dst, const void* src, size_t bytes, int threads);
+
+bool host_is_pageable(const void* p) {
+    cudaPointerAttributes at{};
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+        cudaGetLastError();
+        return true;
+    }
+    return at.type == cudaMemoryTypeUnregistered;
+}
+
+namespace {
+
+bool use_staging(dsvd_ctx* ctx, const void* host, size_t bytes) {
+    return ctx->host_staging && bytes >= (size_t(1) << 20) && host_is_pageable(host);
+}
+
+int copy_threads(dsvd_ctx* ctx) {
+    if (ctx->host_copy_threads > 0) return ctx->host_copy_threads;
+    const int cores = static_cast<int>(std::thread::hardware_concurrency());
+    return std::max(1, std::min(16, cores));
+}
+
+// the staging ring, every slot idle (no copy in flight reads or writes it)
+char* stage_ring(dsvd_ctx* ctx) {
+    const size_t chunk = static_cast<size_t>(ctx->stage_chunk);
+    for (cudaEvent_t& e : ctx->stage_ev) {
+        if (!e) DSVD_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        DSVD_CUDA_CHECK(cudaEventSynchronize(e));
+    }
+    if (ctx->stage && ctx->stage_alloc_chunk != chunk) {
+        DSVD_CUDA_CHECK(cudaFreeHost(ctx->stage));
+        ctx->stage = nullptr;
+    }
+    if (!ctx->stage) {
+        DSVD_CUDA_CHECK(cudaHostAlloc(&ctx->stage, chunk * dsvd_ctx::kStageSlots, cudaHostAllocPortable));
+        ctx->stage_alloc_chunk = chunk;
+    }
+    return ctx->stage;
+}
+
+}  // namespace
+
+// device -> host. The source is complete once `producer`'s work enqueued so
+// far has run (or, when given, once `ready` has fired). Returns with the bytes in `dst` (host-blocking, like a
+// cudaMemcpyAsync into pageable memory).
+void copy_d2h(dsvd_ctx* ctx, void* dst, const void* src, size_t bytes, cudaStream_t producer,
+              cudaEvent_t ready) {
+    if (!use_staging(ctx, dst, bytes)) {
+        if (ready) DSVD_CUDA_CHECK(cudaStreamWaitEvent(producer, ready, 0));
+        DSVD_CUDA_CHECK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, producer));
+        return;
+    }
+    char* ring = stage_ring(ctx);
+    if (!ctx->copy) DSVD_CUDA_CHECK(cudaStreamCreateWithFlags(&ctx->copy, cudaStreamNonBlocking));
+    if (!ready) {
+        if (!ctx->copy_ev) DSVD_CUDA_CHECK(cudaEventCreateWithFlags(&ctx->copy_ev, cudaEventDisableTiming));
+        DSVD_CUDA_CHECK(cudaEventRecord(ctx->copy_ev, producer));
+        ready = ctx->copy_ev;
+    }
+    DSVD_CUDA_CHECK(cudaStreamWaitEvent(ctx->copy, ready, 0));
+    const size_t chunk = static_cast<size_t>(ctx->stage_chunk);
+    const size_t nch = (bytes + chunk - 1) / chunk;
+    const int ns = dsvd_ctx::kStageSlots, threads = copy_threads(ctx);
+    auto issue = [&](size_t c) {
+        const size_t n = std::min(chunk, bytes - c * chunk);
+        char* slot = ring + (c % ns) * chunk;
+        DSVD_CUDA_CHECK(cudaMemcpyAsync(slot, static_cast<const char*>(src) + c * chunk, n,
+                                        cudaMemcpyDeviceToHost, ctx->copy));
+        DSVD_CUDA_CHECK(cudaEventRecord(ctx->stage_ev[c % ns], ctx->copy));
+    };
+    for (size_t c = 0; c < std::min<size_t>(ns, nch); ++c) issue(c);
+    for (size_t c = 0; c < nch; ++c) {
+        DSVD_CUDA_CHECK(cudaEventSynchronize(ctx->stage_ev[c % ns]));
+        const size_t n = std::min(chunk, bytes - c * chunk);
+        host_parallel_memcpy(static_cast<char*>(dst) + c * chunk, ring + (c % ns) * chunk, n, threads);
+        if (c + ns < nch) issue(c + ns);
+    }
+}
+
+// host -> device, ordered on `st` (later work on `st` sees the bytes). Returns
+// once the source has been read (host-blocking for pageable sources).
+void copy_h2d(dsvd_ctx* ctx, void* dst, const void* src, size_t bytes, cudaStream_t st) {
+    if (!use_staging(ctx, src, bytes)) {
+        DSVD_CUDA_CHECK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st));
+        return;
+    }
+    char* ring = stage_ring(ctx);
+    const size_t chunk = static_cast<size_t>(ctx->stage_chunk);
+    const size_t nch = (bytes + chunk - 1) / chunk;
+    const int ns = dsvd_ctx::kStageSlots, threads = copy_threads(ctx);
+    for (size_t c = 0; c < nch; ++c) {
+        const size_t n = std::min(chunk, bytes - c * chunk);
+        char* slot = ring + (c % ns) * chunk;
+        DSVD_CUDA_CHECK(cudaEventSynchronize(ctx->stage_ev[c % ns]));  // the slot's last upload is done
+        host_parallel_memcpy(slot, static_cast<const char*>(src) + c * chunk, n, threads);
+        DSVD_CUDA_CHECK(cudaMemcpyAsync(static_cast<char*>(dst) + c * chunk, slot, n, cudaMemcpyHostToDevice, st));
+        DSVD_CUDA_CHECK(cudaEventRecord(ctx->stage_ev[c % ns], st));
+    }
+}
 
 namespace {
 
@@ -311,11 +423,15 @@ void upload_pair(dsvd_ctx* ctx, CsrAlloc& al, int64_t rows, int64_t cols, int64_
     int64_t* d_off = static_cast<int64_t*>(al.get("a.off", sizeof(int64_t) * (rows + 1)));
     int64_t* d_idx64 = ctx->tbuf<int64_t>("upload.idx64", nnz);
     double* d_val = static_cast<double*>(al.get("a.val", sizeof(double) * nnz));
-    DSVD_CUDA_CHECK(cudaMemcpyAsync(d_off, off, sizeof(int64_t) * (rows + 1), cudaMemcpyHostToDevice, st));
+    copy_h2d(ctx, d_off, off, sizeof(int64_t) * (rows + 1), st);
     // the sketch on the side stream once the offsets are there (its empty rows are not drawn)
     if (omega_cfg != nullptr) pregenerate_omega(ctx, rows, cols, *omega_cfg, d_off);
     cudaEvent_t vals = nullptr;
-    if (nnz) {
+    if (nnz && (use_staging(ctx, idx, sizeof(int64_t) * nnz) || use_staging(ctx, val, sizeof(double) * nnz))) {
+        // pageable CSR: both arrays through the staging ring, in order on st
+        copy_h2d(ctx, d_idx64, idx, sizeof(int64_t) * nnz, st);
+        copy_h2d(ctx, d_val, val, sizeof(double) * nnz, st);
+    } else if (nnz) {
         DSVD_CUDA_CHECK(cudaMemcpyAsync(d_idx64, idx, sizeof(int64_t) * nnz, cudaMemcpyHostToDevice, st));
         // the values travel on the copy stream while the structure is checked,
         // narrowed and sorted on the main stream (needed first by the CSC gather)
@@ -1182,7 +1298,12 @@ void solve_tall(dsvd_ctx* ctx, const DevCsr& A, const DevCsr& AT, const dsvd_con
         dv = dvf;
     }
     cudaStream_t vs = st;
-    if (!io.on_device) {
+    // pageable V: staged after U's rescale is enqueued (the staged copy blocks the host)
+    const bool v_staged = !io.on_device && use_staging(ctx, io.v, sizeof(double) * n_out * k);
+    if (v_staged) {
+        if (!ctx->stage_ready) DSVD_CUDA_CHECK(cudaEventCreateWithFlags(&ctx->stage_ready, cudaEventDisableTiming));
+        DSVD_CUDA_CHECK(cudaEventRecord(ctx->stage_ready, st));
+    } else if (!io.on_device) {
         if (!ctx->copy) DSVD_CUDA_CHECK(cudaStreamCreateWithFlags(&ctx->copy, cudaStreamNonBlocking));
         if (!ctx->copy_ev) DSVD_CUDA_CHECK(cudaEventCreateWithFlags(&ctx->copy_ev, cudaEventDisableTiming));
         DSVD_CUDA_CHECK(cudaEventRecord(ctx->copy_ev, st));
@@ -1202,10 +1323,13 @@ void solve_tall(dsvd_ctx* ctx, const DevCsr& A, const DevCsr& AT, const dsvd_con
         DSVD_CUDA_CHECK(cudaMemcpyAsync(io.s, sv, sizeof(double) * k, cudaMemcpyDeviceToDevice, st));
     } else {
         sp = ctx->span_begin(K_OTHER);
-        DSVD_CUDA_CHECK(cudaMemcpyAsync(io.u, du, sizeof(double) * m * k, cudaMemcpyDeviceToHost, st));
+        if (v_staged) copy_d2h(ctx, io.v, dv, sizeof(double) * n_out * k, st, ctx->stage_ready);
+        copy_d2h(ctx, io.u, du, sizeof(double) * m * k, st);
         DSVD_CUDA_CHECK(cudaMemcpyAsync(io.s, sv, sizeof(double) * k, cudaMemcpyDeviceToHost, st));
-        DSVD_CUDA_CHECK(cudaEventRecord(ctx->copy_ev, vs));  // V's copy is part of the solve
-        DSVD_CUDA_CHECK(cudaStreamWaitEvent(st, ctx->copy_ev, 0));
+        if (!v_staged) {
+            DSVD_CUDA_CHECK(cudaEventRecord(ctx->copy_ev, vs));  // V's copy is part of the solve
+            DSVD_CUDA_CHECK(cudaStreamWaitEvent(st, ctx->copy_ev, 0));
+        }
         ctx->span_end(sp);
     }
     const int64_t nrec = std::min(io.iterations, io.cap);
@@ -1403,8 +1527,8 @@ void solve_basic(dsvd_ctx* ctx, const DevCsr& A, const DevCsr& AT, const dsvd_co
     if (io.on_device) {
         DSVD_CUDA_CHECK(cudaMemcpyAsync(io.s, sv, sizeof(double) * k, cudaMemcpyDeviceToDevice, st));
     } else {
-        DSVD_CUDA_CHECK(cudaMemcpyAsync(io.u, du, sizeof(double) * m * k, cudaMemcpyDeviceToHost, st));
-        DSVD_CUDA_CHECK(cudaMemcpyAsync(io.v, dv, sizeof(double) * n * k, cudaMemcpyDeviceToHost, st));
+        copy_d2h(ctx, io.u, du, sizeof(double) * m * k, st);
+        copy_d2h(ctx, io.v, dv, sizeof(double) * n * k, st);
         DSVD_CUDA_CHECK(cudaMemcpyAsync(io.s, sv, sizeof(double) * k, cudaMemcpyDeviceToHost, st));
     }
     const int64_t nrec = std::min(io.iterations, io.cap);
@@ -1570,6 +1694,13 @@ int dsvd_ctx_destroy(dsvd_ctx* ctx) {
             cudaEventDestroy(ctx->timer[1]);
         }
         if (ctx->host_flags) cudaFreeHost(ctx->host_flags);
+        for (cudaEvent_t e : ctx->stage_ev)
+            if (e) {
+                cudaEventSynchronize(e);
+                cudaEventDestroy(e);
+            }
+        if (ctx->stage) cudaFreeHost(ctx->stage);
+        if (ctx->stage_ready) cudaEventDestroy(ctx->stage_ready);
         comm_release(ctx);
         cudaStreamDestroy(ctx->side);
         cudaStreamDestroy(ctx->eig);
@@ -1665,6 +1796,18 @@ int dsvd_ctx_set_option(dsvd_ctx* ctx, const char* name, int64_t value) {
             if (value < -1 || value > 1)
                 fail(DSVD_CONFIG, "pipeline: 1 = eig beside the A T pass, 0 = serial, -1 = auto");
             ctx->pipeline = static_cast<int>(value);
+        } else if (n == "host_staging") {
+            // 1 (default): pageable host buffers go through the pinned staging ring; 0: plain copies
+            if (value < 0 || value > 1) fail(DSVD_CONFIG, "host_staging must be 0 or 1");
+            ctx->host_staging = static_cast<int>(value);
+        } else if (n == "host_copy_threads") {
+            if (value < 0 || value > 256) fail(DSVD_CONFIG, "host_copy_threads must be in [0, 256] (0: auto)");
+            ctx->host_copy_threads = static_cast<int>(value);
+        } else if (n == "host_stage_chunk") {
+            // bytes per staging slot (4 slots)
+            if (value < 4096 || value > (int64_t(1) << 30) || value % 4096)
+                fail(DSVD_CONFIG, "host_stage_chunk must be a multiple of 4096 in [4 KB, 1 GB]");
+            ctx->stage_chunk = value;
         } else if (n == "eig_priority") {
             // 1: the eig stream at the highest priority (default), 0: default priority
             if (value < 0 || value > 1) fail(DSVD_CONFIG, "eig_priority must be 0 or 1");

@@ -119,6 +119,18 @@ struct dsvd_ctx {
     uint64_t omega_seed = 0;
     cudaEvent_t omega_ev = nullptr;
     cudaStream_t copy = nullptr;      // host->device copy of the CSR values (upload_pair)
+    // staged copies to / from PAGEABLE host buffers (engine.cu copy_h2d / copy_d2h):
+    // a ring of pinned slots, the device streaming one slot while host threads move
+    // another (option host_staging = 0: plain cudaMemcpyAsync through the driver's
+    // bounce buffer)
+    static constexpr int kStageSlots = 4;
+    char* stage = nullptr;  // kStageSlots x stage_chunk bytes, pinned
+    size_t stage_alloc_chunk = 0;
+    cudaEvent_t stage_ev[kStageSlots] = {};
+    cudaEvent_t stage_ready = nullptr;  // a staged device->host source is complete
+    int64_t stage_chunk = int64_t(32) << 20;
+    int host_staging = 1;
+    int host_copy_threads = 0;  // 0: min(16, host cores)
     int64_t coo_rows = -1, coo_cols = -1, coo_nnz = -1;  // last assembled CSR (dsvd_coo_fetch, _from_coo)
     cudaEvent_t copy_ev = nullptr;
     cudaEvent_t fork = nullptr, join = nullptr;

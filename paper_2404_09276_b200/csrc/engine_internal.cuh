@@ -15,6 +15,12 @@ namespace dsvd {
 
 void set_device(dsvd_ctx* ctx);
 void count_launch(int n = 1);
+// host <-> device copies that stage pageable host buffers through pinned slots
+// (engine.cu); pinned / registered / device pointers take one cudaMemcpyAsync
+bool host_is_pageable(const void* p);
+void copy_d2h(dsvd_ctx* ctx, void* dst, const void* src, size_t bytes, cudaStream_t producer,
+              cudaEvent_t ready = nullptr);
+void copy_h2d(dsvd_ctx* ctx, void* dst, const void* src, size_t bytes, cudaStream_t st);
 
 struct CsrAlloc {
     // allocate through the context arena (prefix) or as owned buffers
