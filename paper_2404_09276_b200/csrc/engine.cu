@@ -76,6 +76,7 @@ void count_launch(int n) { g_launches += n; }
 // buffer's first-touch page faults in parallel). Pinned, registered and
 // device pointers keep the plain cudaMemcpyAsync.
 void host_parallel_memcpy(void* dst, const void* src, size_t bytes, int threads);
+void host_prefault(void* p, size_t bytes, int threads);
 
 bool host_is_pageable(const void* p) {
     cudaPointerAttributes at{};
@@ -118,6 +119,28 @@ char* stage_ring(dsvd_ctx* ctx) {
 
 }  // namespace
 
+void prefault_join(dsvd_ctx* ctx) noexcept {
+    if (ctx->prefault) {
+        if (ctx->prefault->joinable()) ctx->prefault->join();
+        ctx->prefault.reset();
+    }
+}
+
+// A solve's pageable host outputs (u: rows x k, v: cols x k) are faulted in on
+// a host thread while the device computes; the staged copies join it first.
+void prefault_outputs(dsvd_ctx* ctx, const dsvd_outputs* out, int64_t rows, int64_t cols, int64_t k) {
+    prefault_join(ctx);
+    if (!ctx->host_staging || out->outputs_on_device) return;
+    std::vector<std::pair<void*, size_t>> r;
+    const size_t ub = sizeof(double) * rows * k, vb = sizeof(double) * cols * k;
+    if (out->u && use_staging(ctx, out->u, ub)) r.emplace_back(out->u, ub);
+    if (out->v && use_staging(ctx, out->v, vb)) r.emplace_back(out->v, vb);
+    if (r.empty()) return;
+    ctx->prefault = std::make_unique<std::thread>([r] {
+        for (const auto& x : r) host_prefault(x.first, x.second, 4);
+    });
+}
+
 // device -> host. The source is complete once `producer`'s work enqueued so
 // far has run (or, when given, once `ready` has fired). Returns with the bytes in `dst` (host-blocking, like a
 // cudaMemcpyAsync into pageable memory).
@@ -128,6 +151,7 @@ void copy_d2h(dsvd_ctx* ctx, void* dst, const void* src, size_t bytes, cudaStrea
         DSVD_CUDA_CHECK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, producer));
         return;
     }
+    prefault_join(ctx);  // the destination's pages are in
     char* ring = stage_ring(ctx);
     if (!ctx->copy) DSVD_CUDA_CHECK(cudaStreamCreateWithFlags(&ctx->copy, cudaStreamNonBlocking));
     if (!ready) {
@@ -2029,6 +2053,8 @@ int dsvd_solve(dsvd_ctx* ctx, const dsvd_matrix* a, const dsvd_config* cfg, dsvd
         begin_profile(ctx);
         cudaEvent_t e0 = ctx->event(), e1 = ctx->event();
         DSVD_CUDA_CHECK(cudaEventRecord(e0, ctx->stream));
+        PrefaultScope pf{ctx};
+        prefault_outputs(ctx, out, a->a.rows, a->a.cols, cfg->k);
         solve_pair(ctx, a->a, a->at, *cfg, out, observer, user, a->row_offset, a->global_rows);
         DSVD_CUDA_CHECK(cudaEventRecord(e1, ctx->stream));
         DSVD_CUDA_CHECK(cudaEventSynchronize(e1));
@@ -2050,6 +2076,8 @@ int dsvd_solve_csr(dsvd_ctx* ctx, int64_t rows, int64_t cols, int64_t nnz, const
         begin_profile(ctx);
         cudaEvent_t e0 = ctx->event(), e1 = ctx->event(), e2 = ctx->event();
         DSVD_CUDA_CHECK(cudaEventRecord(e0, ctx->stream));
+        PrefaultScope pf{ctx};
+        prefault_outputs(ctx, out, rows, cols, cfg->k);
         DevCsr a, at;
         CsrAlloc al{ctx, "csr.", nullptr};
         upload_pair(ctx, al, rows, cols, nnz, offsets, col_indices, values, a, at, cfg);

@@ -3,7 +3,9 @@
 
 #include <atomic>
 #include <map>
+#include <memory>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "common.cuh"
@@ -131,6 +133,8 @@ struct dsvd_ctx {
     int64_t stage_chunk = int64_t(32) << 20;
     int host_staging = 1;
     int host_copy_threads = 0;  // 0: min(16, host cores)
+    // touches the pages of pageable host outputs while the solve runs (engine.cu prefault_outputs)
+    std::unique_ptr<std::thread> prefault;
     int64_t coo_rows = -1, coo_cols = -1, coo_nnz = -1;  // last assembled CSR (dsvd_coo_fetch, _from_coo)
     cudaEvent_t copy_ev = nullptr;
     cudaEvent_t fork = nullptr, join = nullptr;

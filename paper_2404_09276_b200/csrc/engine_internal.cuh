@@ -21,6 +21,14 @@ bool host_is_pageable(const void* p);
 void copy_d2h(dsvd_ctx* ctx, void* dst, const void* src, size_t bytes, cudaStream_t producer,
               cudaEvent_t ready = nullptr);
 void copy_h2d(dsvd_ctx* ctx, void* dst, const void* src, size_t bytes, cudaStream_t st);
+// page-in of pageable host outputs on a host thread during the solve (joined by
+// copy_d2h and, on every exit path, by PrefaultScope)
+void prefault_outputs(dsvd_ctx* ctx, const dsvd_outputs* out, int64_t rows, int64_t cols, int64_t k);
+void prefault_join(dsvd_ctx* ctx) noexcept;
+struct PrefaultScope {
+    dsvd_ctx* ctx;
+    ~PrefaultScope() { prefault_join(ctx); }
+};
 
 struct CsrAlloc {
     // allocate through the context arena (prefix) or as owned buffers
