@@ -123,6 +123,7 @@ def main():
         "alpha_trace_max_rel_err": alpha_rel, "s_hat_trace_max_rel_err": shat_rel,
         "pve_ratio": [pve_g, pve_r],
         "pve_ratio_rel_err": (abs(pve_g - pve_r) / abs(pve_r)) if (pve_g is not None and pve_r) else None,
+        "build": os.environ.get("DSVD_BUILD"),
         "bars": {"sigma_rel": 1e-8, "angle": 1e-6, "iterations": "equal", "pve": "equal (rel 1e-6)"},
     }
     rec["pass"] = bool(s_rel <= 1e-8 and th_u <= 1e-6 and th_v <= 1e-6 and
