@@ -617,13 +617,17 @@ gram_dmma_wide_kernel(const double* __restrict__ c, int64_t n, int64_t ld, int n
 // every one of them useful (the 4x4 tiles issue 880: 320-column padding and the
 // lower halves of the diagonal tiles). Kind encoding as GwKinds, in tile units.
 constexpr int kGw2Tiles = 4;  // tiles per warp
+#ifndef DSVD_GW2_UNROLL
+#define DSVD_GW2_UNROLL 8
+#endif
+constexpr int kGw2Unroll = DSVD_GW2_UNROLL;  // k-steps unrolled in gw2_ksteps (C4 Gram per solve: 2 -> 274.5 ms, 4 -> 272.5, 8 -> 269.4; profiles/r02_ab_gw2_unroll.txt)
 
 // One stage (kGwRows rows) of a warp's NT 2x2 tiles: per k-step four fragment
 // loads and four DMMAs per tile
 template <int NT>
 __device__ __forceinline__ void gw2_ksteps(const double* C, int q, int g, const int (&ia)[kGw2Tiles],
                                            const int (&jb)[kGw2Tiles], double2 (&acc)[kGw2Tiles][2][2]) {
-#pragma unroll 2
+#pragma unroll kGw2Unroll
     for (int ks = 0; ks < kGwRows / 4; ++ks) {
         const double* row = C + (4 * ks + q) * kGwStride + g;
 #pragma unroll
